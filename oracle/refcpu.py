@@ -1,0 +1,238 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY -- ctypes view of the CPU restatement.
+
+Loads oracle/_build/librefcpu.so (built by oracle/Makefile from
+oracle/refcpu/*.{hpp,cpp}). Only tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs may import this module, and
+only as the checker / CPU baseline; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "librefcpu.so")
+_lib = None
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        _lib = C.CDLL(_LIB_PATH)
+        _lib.refcpu_last_error.restype = C.c_char_p
+    return _lib
+
+
+class _Problem(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int), ("ny", C.c_int), ("lx", C.c_double), ("ly", C.c_double),
+        ("lam", C.c_double), ("mu", C.c_double), ("k_perm", C.c_double), ("eta", C.c_double),
+        ("biot_m", C.c_double), ("biot_b", C.c_double), ("k_perm_cells", C.POINTER(C.c_double)),
+        ("penalty", C.c_double), ("disp_kind", C.c_int * 4), ("disp_data", (C.c_double * 2) * 4),
+        ("flow_kind", C.c_int * 4), ("flow_data", C.c_double * 4),
+    ]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("restart", C.c_int), ("max_iter", C.c_int), ("sweeps", C.c_int),
+                ("stab", C.c_double), ("backend", C.c_int), ("flexible", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("history_len", C.c_int),
+                ("final_rel_res", C.c_double), ("setup_seconds", C.c_double), ("solve_seconds", C.c_double)]
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(lib().refcpu_last_error().decode())
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+DISP = {"fixed": 0, "traction": 1, "roller_x": 2, "roller_y": 3}
+FLOW = {"pressure": 0, "no_flow": 1}
+TAGS = ("left", "right", "bottom", "top")
+
+
+class RefProblem:
+    """Assembled operators of one problem description (see
+    paper_1801_04984_b200.problem.ProblemSpec.to_dict for the fields)."""
+
+    def __init__(self, spec: dict):
+        p = _Problem()
+        p.nx, p.ny, p.lx, p.ly = spec["nx"], spec["ny"], spec["lx"], spec["ly"]
+        p.lam, p.mu, p.k_perm, p.eta = spec["lam"], spec["mu"], spec["k_perm"], spec["eta"]
+        p.biot_m, p.biot_b, p.penalty = spec["biot_m"], spec["biot_b"], spec["penalty"]
+        self._k = None
+        if spec.get("k_perm_cells") is not None:
+            self._k = np.ascontiguousarray(spec["k_perm_cells"], dtype=np.float64)
+            p.k_perm_cells = _dp(self._k)
+        for s, tag in enumerate(TAGS):
+            kind, data = spec["disp"][tag]
+            p.disp_kind[s] = DISP[kind]
+            p.disp_data[s][0], p.disp_data[s][1] = data
+            fk, fd = spec["flow"][tag]
+            p.flow_kind[s] = FLOW[fk]
+            p.flow_data[s] = fd
+        self.spec = spec
+        h = C.c_void_p()
+        _check(lib().refcpu_create(C.byref(p), C.byref(h)))
+        self._h = h
+        sz = (C.c_longlong * 8)()
+        _check(lib().refcpu_sizes(self._h, sz))
+        self.n_u, self.n_q, self.n_p = sz[0], sz[1], sz[2]
+        self.nnz = dict(zip(("A", "M_q", "B", "E", "M_p"), sz[3:8]))
+        self.n_total = self.n_u + self.n_q + self.n_p
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().refcpu_destroy(self._h)
+            self._h = None
+
+    def csr(self, name):
+        rows = {"A": self.n_u, "M_q": self.n_q, "B": self.n_q, "E": self.n_u, "M_p": self.n_p}[name]
+        which = ("A", "M_q", "B", "E", "M_p").index(name)
+        nnz = self.nnz[name]
+        off = np.empty(rows + 1, np.int32)
+        idx = np.empty(nnz, np.int32)
+        val = np.empty(nnz, np.float64)
+        _check(lib().refcpu_export_csr(self._h, which, _ip(off), _ip(idx), _dp(val)))
+        return off, idx, val
+
+    def misc(self):
+        mp = np.empty(self.n_p, np.float64)
+        qc = np.empty(self.n_q, np.int8)
+        b, im, kdr = C.c_double(), C.c_double(), C.c_double()
+        _check(lib().refcpu_export_misc(self._h, _dp(mp), qc.ctypes.data_as(C.c_void_p), C.byref(b), C.byref(im),
+                                        C.byref(kdr)))
+        return dict(m_p_diag=mp, q_constrained=qc, biot_b=b.value, inv_m=im.value, k_dr=kdr.value)
+
+    def assemble_rhs(self, t):
+        u, q, p = np.empty(self.n_u), np.empty(self.n_q), np.empty(self.n_p)
+        _check(lib().refcpu_assemble_rhs(self._h, C.c_double(t), _dp(u), _dp(q), _dp(p)))
+        return u, q, p
+
+    def spacetime_csr(self, theta, tau):
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        m = theta.shape[0]
+        sp = C.c_void_p()
+        rn = (C.c_longlong * 2)()
+        _check(lib().refcpu_spacetime_build(self._h, m, _dp(theta), C.c_double(tau), C.byref(sp), rn))
+        off = np.empty(rn[0] + 1, np.int32)
+        idx = np.empty(rn[1], np.int32)
+        val = np.empty(rn[1], np.float64)
+        _check(lib().refcpu_spacetime_export(sp, _ip(off), _ip(idx), _dp(val)))
+        lib().refcpu_spacetime_destroy(sp)
+        return off, idx, val
+
+    def apply_block(self, theta, tau, x):
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        _check(lib().refcpu_apply_block(self._h, theta.shape[0], _dp(theta), C.c_double(tau), _dp(x), _dp(y)))
+        return y
+
+    def precondition(self, lam, tau, r, sweeps=1, stab=-1.0, backend=0):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.empty_like(r)
+        _check(lib().refcpu_precondition(self._h, C.c_double(lam), C.c_double(tau), C.c_double(stab), sweeps, backend,
+                                         _dp(r), _dp(z)))
+        return z
+
+    @staticmethod
+    def _opts(tol, restart, max_iter, sweeps, stab, backend, flexible):
+        o = _Opts()
+        o.tol, o.restart, o.max_iter, o.sweeps, o.stab = tol, restart, max_iter, sweeps, stab
+        o.backend, o.flexible = int(backend), int(flexible)
+        return o
+
+    def block_solve(self, r, tau, rhs, tol=1e-10, restart=50, max_iter=400, sweeps=1, stab=-1.0, backend=0,
+                    flexible=False):
+        o = self._opts(tol, restart, max_iter, sweeps, stab, backend, flexible)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty_like(rhs)
+        rep = _Report()
+        hist = np.empty(max_iter + 2, np.float64)
+        _check(lib().refcpu_block_solve(self._h, r, C.c_double(tau), C.byref(o), _dp(rhs), _dp(x), C.byref(rep),
+                                        _dp(hist), len(hist)))
+        return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
+                       final_rel_res=rep.final_rel_res, history=hist[:rep.history_len].copy(),
+                       setup_seconds=rep.setup_seconds, solve_seconds=rep.solve_seconds)
+
+    def march(self, r, T, n_slabs, tol=1e-10, restart=50, max_iter=400, sweeps=1, stab=-1.0, backend=0,
+              flexible=False, keep_states=False, max_slabs=0):
+        o = self._opts(tol, restart, max_iter, sweeps, stab, backend, flexible)
+        its = np.zeros(n_slabs, np.int32)
+        res = np.zeros(n_slabs)
+        secs = np.zeros(n_slabs)
+        setup = C.c_double()
+        end = np.empty(self.n_total)
+        run = n_slabs if max_slabs <= 0 else min(max_slabs, n_slabs)
+        states = np.empty((run, r + 1, self.n_total)) if keep_states else None
+        _check(lib().refcpu_march(self._h, r, C.c_double(T), n_slabs, C.byref(o), _ip(its), _dp(res), _dp(secs),
+                                  C.byref(setup), _dp(end), _dp(states) if keep_states else None, max_slabs))
+        return dict(iterations=its[:run], final_res=res[:run], solve_seconds=secs[:run],
+                    setup_seconds=setup.value, end_state=end, states=states)
+
+    def slab_rhs(self, r, t0, tau, u_prev, p_prev):
+        out = np.empty((r + 1) * self.n_total)
+        _check(lib().refcpu_slab_rhs(self._h, r, C.c_double(t0), C.c_double(tau),
+                                     _dp(np.ascontiguousarray(u_prev, np.float64)),
+                                     _dp(np.ascontiguousarray(p_prev, np.float64)), _dp(out)))
+        return out
+
+    def schur_forward(self, r, R):
+        R = np.ascontiguousarray(R, np.float64)
+        out = np.empty_like(R)
+        _check(lib().refcpu_schur_forward(self._h, r, _dp(R), _dp(out)))
+        return out
+
+
+def time_constants(r):
+    n = r + 1
+    nodes, w, phi = np.empty(n), np.empty(n), np.empty(n)
+    G, T, Q = np.empty((n, n)), np.empty((n, n)), np.empty((n, n))
+    _check(lib().refcpu_time_constants(r, _dp(nodes), _dp(w), _dp(phi), _dp(G), _dp(T), _dp(Q)))
+    return dict(nodes=nodes, weights=w, phi_at0=phi, G_hat=G, T=T, Q=Q)
+
+
+def csr_apply(off, idx, val, x, threads=1):
+    """SparseMatrix::apply (sparse.hpp:30-40) with 64-bit offsets."""
+    off64 = np.ascontiguousarray(off, dtype=np.int64)
+    y = np.empty(len(off64) - 1)
+    _check(lib().refcpu_csr_apply(len(off64) - 1, off64.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                  _ip(np.ascontiguousarray(idx, np.int32)), _dp(np.ascontiguousarray(val, np.float64)),
+                                  _dp(np.ascontiguousarray(x, np.float64)), _dp(y), threads))
+    return y
+
+
+def uniform(seed, n):
+    out = np.empty(n)
+    lib().refcpu_uniform(C.c_ulonglong(seed), C.c_longlong(n), _dp(out))
+    return out
+
+
+def lognormal(seed, n, sigma=1.0):
+    out = np.empty(n)
+    lib().refcpu_lognormal(C.c_ulonglong(seed), C.c_longlong(n), C.c_double(sigma), _dp(out))
+    return out

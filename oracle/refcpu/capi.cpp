@@ -1,0 +1,414 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY. Not part of the product.
+//
+// C ABI over the CPU restatement, loaded by tests/ (ctypes) and by bench.py's
+// cpu_baseline / --impl reference legs. The product library never links it.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "solver.hpp"
+
+using namespace refcpu;
+
+extern "C" {
+
+// Problem description for the structured-rectangle configurations with
+// constant boundary data (BASELINE configs, Terzaghi column).
+typedef struct {
+    int nx, ny;
+    double lx, ly;
+    double lambda, mu, k_perm, eta, biot_m, biot_b;
+    const double* k_perm_cells;  // nullptr or nx*ny values (cell c = j*nx + i)
+    double penalty;
+    int disp_kind[4];        // per tag left,right,bottom,top: 0 fixed, 1 traction, 2 roller_x, 3 roller_y
+    double disp_data[4][2];  // constant Dirichlet value (fixed) or traction vector (others)
+    int flow_kind[4];        // 0 pressure, 1 no_flow
+    double flow_data[4];     // constant prescribed pressure
+} refcpu_problem;
+
+struct Handle {
+    Mesh mesh;
+    DofMaps dofs;
+    SpatialOperators ops;
+    VolumeData data;
+    std::string err;
+};
+
+static thread_local std::string g_err;
+
+const char* refcpu_last_error() { return g_err.c_str(); }
+
+#define GUARD_BEGIN try {
+#define GUARD_END                        \
+    }                                    \
+    catch (const SolverError& e) {       \
+        g_err = e.what();                \
+        return 2;                        \
+    }                                    \
+    catch (const std::exception& e) {    \
+        g_err = e.what();                \
+        return 1;                        \
+    }                                    \
+    return 0;
+
+static BoundarySpec make_bc(const refcpu_problem* p) {
+    BoundarySpec bc;
+    const FaceTag tags[4] = {FaceTag::left, FaceTag::right, FaceTag::bottom, FaceTag::top};
+    for (int s = 0; s < 4; ++s) {
+        const double d0 = p->disp_data[s][0], d1 = p->disp_data[s][1];
+        VectorFieldT vf;
+        if (d0 != 0.0 || d1 != 0.0)
+            vf = [d0, d1](double, double, double) { return std::array<double, 2>{d0, d1}; };
+        DisplacementBC db;
+        switch (p->disp_kind[s]) {
+            case 0: db = DisplacementBC::fixed(vf); break;
+            case 1: db = DisplacementBC::traction(vf); break;
+            case 2: db = DisplacementBC::roller_x(vf); break;
+            case 3: db = DisplacementBC::roller_y(vf); break;
+            default: throw std::invalid_argument("bad displacement kind");
+        }
+        bc.set_displacement(tags[s], db);
+        if (p->flow_kind[s] == 0) {
+            const double pv = p->flow_data[s];
+            ScalarFieldT sf;
+            if (pv != 0.0) sf = [pv](double, double, double) { return pv; };
+            bc.set_flow(tags[s], FlowBC::pressure(sf));
+        } else {
+            bc.set_flow(tags[s], FlowBC::no_flow());
+        }
+    }
+    return bc;
+}
+
+int refcpu_create(const refcpu_problem* p, void** out) {
+    GUARD_BEGIN
+    auto h = std::make_unique<Handle>();
+    h->mesh = build_mesh(p->nx, p->ny, p->lx, p->ly);
+    h->dofs = build_dof_maps(h->mesh);
+    MaterialParameters mat = material_from_lame(p->lambda, p->mu, p->k_perm, p->eta, p->biot_m, p->biot_b);
+    if (p->k_perm_cells) mat.k_perm_cells.assign(p->k_perm_cells, p->k_perm_cells + p->nx * p->ny);
+    mat.validate();
+    h->ops = assemble_operators(h->mesh, h->dofs, mat, p->penalty, make_bc(p));
+    *out = h.release();
+    GUARD_END
+}
+
+void refcpu_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+// sizes[0..] = n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E), nnz(M_p)
+int refcpu_sizes(void* hp, long long* sizes) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    sizes[0] = h->ops.n_u;
+    sizes[1] = h->ops.n_q;
+    sizes[2] = h->ops.n_p;
+    sizes[3] = h->ops.A.nnz();
+    sizes[4] = h->ops.M_q.nnz();
+    sizes[5] = h->ops.B.nnz();
+    sizes[6] = h->ops.E.nnz();
+    sizes[7] = h->ops.M_p.nnz();
+    GUARD_END
+}
+
+static const SparseMatrix& pick(Handle* h, int which) {
+    switch (which) {
+        case 0: return h->ops.A;
+        case 1: return h->ops.M_q;
+        case 2: return h->ops.B;
+        case 3: return h->ops.E;
+        case 4: return h->ops.M_p;
+    }
+    throw std::invalid_argument("bad block id");
+}
+
+// Export block `which` (0 A, 1 M_q, 2 B, 3 E, 4 M_p) as CSR.
+int refcpu_export_csr(void* hp, int which, int* off, int* idx, double* val) {
+    GUARD_BEGIN
+    const SparseMatrix& s = pick(static_cast<Handle*>(hp), which);
+    std::memcpy(off, s.row_offsets.data(), sizeof(int) * (s.rows + 1));
+    std::memcpy(idx, s.col_indices.data(), sizeof(int) * s.nnz());
+    std::memcpy(val, s.values.data(), sizeof(double) * s.nnz());
+    GUARD_END
+}
+
+int refcpu_export_misc(void* hp, double* m_p_diag, signed char* q_constrained, double* b_biot, double* inv_m,
+                       double* k_dr) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    std::memcpy(m_p_diag, h->ops.m_p_diag.data(), sizeof(double) * h->ops.n_p);
+    for (int i = 0; i < h->ops.n_q; ++i) q_constrained[i] = h->ops.q_constrained[i];
+    *b_biot = h->ops.mat.biot_b;
+    *inv_m = 1.0 / h->ops.mat.biot_m;
+    *k_dr = h->ops.mat.k_dr;
+    GUARD_END
+}
+
+// assemble_rhs at time t (constant boundary data; no volume data).
+int refcpu_assemble_rhs(void* hp, double t, double* u, double* q, double* p) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const FieldVecs r = assemble_rhs(h->mesh, h->dofs, h->ops.mat, h->ops, h->data, t);
+    std::memcpy(u, r.u.data(), sizeof(double) * r.u.size());
+    std::memcpy(q, r.q.data(), sizeof(double) * r.q.size());
+    std::memcpy(p, r.p.data(), sizeof(double) * r.p.size());
+    GUARD_END
+}
+
+// Time basis and Schur constants for degree r (r <= 1): out arrays sized
+// (r+1), (r+1)^2.
+int refcpu_time_constants(int r, double* nodes, double* weights, double* phi0, double* G_hat, double* T, double* Q) {
+    GUARD_BEGIN
+    const TimeBasis b = time_matrices(r);
+    const SchurForm s = real_schur(b);
+    const int n = r + 1;
+    for (int i = 0; i < n; ++i) {
+        nodes[i] = b.nodes[i];
+        weights[i] = b.weights[i];
+        phi0[i] = b.phi_at0[i];
+    }
+    for (int i = 0; i < n * n; ++i) {
+        G_hat[i] = b.G_hat[i];
+        T[i] = s.T[i];
+        Q[i] = s.Q[i];
+    }
+    GUARD_END
+}
+
+struct StCsr {
+    SparseMatrix s;
+};
+
+// Canonical space-time operator for block theta (m x m row-major), tau.
+int refcpu_spacetime_build(void* hp, int m, const double* theta, double tau, void** out, long long* rows_nnz) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    auto st = std::make_unique<StCsr>();
+    st->s = build_spacetime_csr(h->ops, std::vector<double>(theta, theta + m * m), m, tau);
+    rows_nnz[0] = st->s.rows;
+    rows_nnz[1] = st->s.nnz();
+    *out = st.release();
+    GUARD_END
+}
+int refcpu_spacetime_export(void* sp, int* off, int* idx, double* val) {
+    GUARD_BEGIN
+    const SparseMatrix& s = static_cast<StCsr*>(sp)->s;
+    std::memcpy(off, s.row_offsets.data(), sizeof(int) * (s.rows + 1));
+    std::memcpy(idx, s.col_indices.data(), sizeof(int) * s.nnz());
+    std::memcpy(val, s.values.data(), sizeof(double) * s.nnz());
+    GUARD_END
+}
+void refcpu_spacetime_destroy(void* sp) { delete static_cast<StCsr*>(sp); }
+
+// SparseMatrix::apply (sparse.hpp:30-40) on caller-provided CSR; optional
+// OpenMP over rows (each row is still summed sequentially, so the result is
+// bit-identical for any thread count).
+int refcpu_csr_apply(int rows, const long long* off, const int* idx, const double* val, const double* x, double* y,
+                     int threads) {
+    GUARD_BEGIN
+#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : 1)
+    for (int i = 0; i < rows; ++i) {
+        double s = 0.0;
+        for (long long k = off[i]; k < off[i + 1]; ++k) s += val[k] * x[idx[k]];
+        y[i] = s;
+    }
+    GUARD_END
+}
+
+// Block operator apply (fixed_stress.hpp:38-60).
+int refcpu_apply_block(void* hp, int m, const double* theta, double tau, const double* x, double* y) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    apply_block_operator(h->ops, std::vector<double>(theta, theta + m * m), m, tau, x, y);
+    GUARD_END
+}
+
+// Truncated fixed-stress preconditioner for one time component, lambda.
+int refcpu_precondition(void* hp, double lambda, double tau, double stab, int sweeps, int backend, const double* r,
+                        double* z) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const InnerBackend be = backend ? InnerBackend::banded : InnerBackend::dense;
+    if (stab < 0.0) stab = h->ops.mat.biot_b * h->ops.mat.biot_b / h->ops.mat.k_dr;
+    FixedStressSolver fs(h->ops, {lambda}, 1, tau, stab, make_a_solver(h->ops, be), be, h->mesh.nx, h->mesh.ny);
+    fs.precondition(r, z, sweeps);
+    GUARD_END
+}
+
+typedef struct {
+    double tol;
+    int restart, max_iter;
+    int sweeps;
+    double stab;  // < 0: b^2 / K_dr
+    int backend;  // 0 dense LU (reference-exact), 1 banded sparse-direct
+    int flexible; // 0 gmres (slab.hpp:227), 1 gmres_flexible
+} refcpu_solve_opts;
+
+typedef struct {
+    int converged, iterations, history_len;
+    double final_rel_res;
+    double setup_seconds, solve_seconds;
+} refcpu_report;
+
+static SolveOptions to_opts(const refcpu_solve_opts* o) {
+    SolveOptions s;
+    s.gmres.tol = o->tol;
+    s.gmres.restart = o->restart;
+    s.gmres.max_iter = o->max_iter;
+    s.fs.truncation_sweeps = o->sweeps;
+    s.fs.stab = o->stab;
+    s.backend = o->backend ? InnerBackend::banded : InnerBackend::dense;
+    s.flexible = o->flexible != 0;
+    return s;
+}
+
+// One GMRES solve of the transformed diagonal block (the hot path,
+// slab.hpp:456-473) for degree r's single Schur block and a given rhs.
+int refcpu_block_solve(void* hp, int r, double tau, const refcpu_solve_opts* o, const double* rhs, double* x,
+                       refcpu_report* rep, double* history, int history_cap) {
+    using clk = std::chrono::steady_clock;
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const TimeBasis basis = time_matrices(r);
+    const SchurForm schur = real_schur(basis);
+    const auto t0 = clk::now();
+    SlabSolver solver(h->ops, basis, schur, tau, to_opts(o), h->mesh.nx, h->mesh.ny);
+    const auto t1 = clk::now();
+    const int m = schur.block_sizes[0];
+    Vec b(rhs, rhs + static_cast<size_t>(m) * h->ops.n_total());
+    BlockReport br;
+    Vec sol;
+    try {
+        sol = solver.solve_block(0, b, br);
+    } catch (const SolverError&) {
+        throw;
+    }
+    const auto t2 = clk::now();
+    std::copy(sol.begin(), sol.end(), x);
+    rep->converged = br.report.converged;
+    rep->iterations = br.report.iterations;
+    rep->history_len = static_cast<int>(br.report.residual_history.size());
+    rep->final_rel_res = br.report.final_relative_residual;
+    rep->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+    rep->solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+    for (int i = 0; i < std::min(history_cap, rep->history_len); ++i) history[i] = br.report.residual_history[i];
+    GUARD_END
+}
+
+// Monolithic-spectral march (march.hpp:45-79,109-117) over uniform slabs.
+// Per slab s: iterations[s], final_res[s], solve_seconds[s]; the end trace
+// of the final slab (u, q, p stacked, n_total) in end_state; optionally the
+// full per-slab state (all r+1 components, n_slabs*(r+1)*n_total) in states.
+int refcpu_march(void* hp, int r, double T, int n_slabs, const refcpu_solve_opts* o, int* iterations,
+                 double* final_res, double* solve_seconds, double* setup_seconds, double* end_state, double* states,
+                 int max_slabs) {
+    using clk = std::chrono::steady_clock;
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const SpatialOperators& ops = h->ops;
+    const TimePartition part = uniform_partition(T, n_slabs);
+    const TimeBasis basis = time_matrices(r);
+    const SchurForm schur = real_schur(basis);
+    Vec u_prev(ops.n_u, 0.0), p_prev(ops.n_p, 0.0);
+    std::unique_ptr<SlabSolver> spectral;
+    double cached_tau = -1.0;
+    const int nt = ops.n_total();
+    const int run = max_slabs > 0 ? std::min(max_slabs, part.n_slabs()) : part.n_slabs();
+    *setup_seconds = 0.0;
+    for (int n = 0; n < run; ++n) {
+        const double tau = part.slab_length(n), t0 = part.t_begin(n);
+        std::vector<FieldVecs> nodal(basis.n_nodes());
+        for (int i = 0; i < basis.n_nodes(); ++i)
+            nodal[i] = assemble_rhs(h->mesh, h->dofs, ops.mat, ops, h->data, t0 + basis.nodes[i] * tau);
+        const SlabSystem sys = build_slab_system(ops, basis, tau, nodal, u_prev, p_prev);
+        const bool rebuild = cached_tau < 0.0 || std::abs(tau - cached_tau) > 1e-12 * tau;
+        try {
+            if (rebuild) {
+                const auto a = clk::now();
+                spectral = std::make_unique<SlabSolver>(ops, basis, schur, tau, to_opts(o), h->mesh.nx, h->mesh.ny);
+                *setup_seconds += std::chrono::duration<double>(clk::now() - a).count();
+            }
+            std::vector<BlockReport> reps;
+            const auto a = clk::now();
+            const std::vector<FieldVecs> st = spectral->solve(sys, reps);
+            solve_seconds[n] = std::chrono::duration<double>(clk::now() - a).count();
+            int it = 0;
+            double res = 0.0;
+            for (const BlockReport& br : reps) {
+                it = std::max(it, br.gmres_iterations);
+                res = std::max(res, br.report.final_relative_residual);
+            }
+            iterations[n] = it;
+            final_res[n] = res;
+            cached_tau = tau;
+            u_prev = st.back().u;
+            p_prev = st.back().p;
+            if (states)
+                for (int i = 0; i < basis.n_nodes(); ++i) {
+                    double* dst = states + (static_cast<size_t>(n) * basis.n_nodes() + i) * nt;
+                    std::copy(st[i].u.begin(), st[i].u.end(), dst);
+                    std::copy(st[i].q.begin(), st[i].q.end(), dst + ops.n_u);
+                    std::copy(st[i].p.begin(), st[i].p.end(), dst + ops.n_u + ops.n_q);
+                }
+            if (n == run - 1 && end_state) {
+                std::copy(st.back().u.begin(), st.back().u.end(), end_state);
+                std::copy(st.back().q.begin(), st.back().q.end(), end_state + ops.n_u);
+                std::copy(st.back().p.begin(), st.back().p.end(), end_state + ops.n_u + ops.n_q);
+            }
+        } catch (const SolverError& e) {
+            char buf[64];
+            std::snprintf(buf, sizeof(buf), "%f", part.t_end(n));
+            throw SolverError("slab " + std::to_string(n) + " (t_n = " + buf + "): " + e.what());
+        }
+    }
+    GUARD_END
+}
+
+// Slab right-hand side for a given jump (u_prev, p_prev) and slab start t0:
+// out is (r+1)*n_total, stacked per Radau node (slab.hpp:58-87).
+int refcpu_slab_rhs(void* hp, int r, double t0, double tau, const double* u_prev, const double* p_prev, double* out) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const TimeBasis basis = time_matrices(r);
+    std::vector<FieldVecs> nodal(basis.n_nodes());
+    for (int i = 0; i < basis.n_nodes(); ++i)
+        nodal[i] = assemble_rhs(h->mesh, h->dofs, h->ops.mat, h->ops, h->data, t0 + basis.nodes[i] * tau);
+    const SlabSystem sys = build_slab_system(h->ops, basis, tau, nodal, Vec(u_prev, u_prev + h->ops.n_u),
+                                             Vec(p_prev, p_prev + h->ops.n_p));
+    for (int i = 0; i < basis.n_nodes(); ++i) std::copy(sys.rhs[i].begin(), sys.rhs[i].end(), out + i * h->ops.n_total());
+    GUARD_END
+}
+
+// Forward transform of the slab rhs into the Schur basis for degree r (single
+// block): shat_i = sum_j Q(j,i) R_j / w_j (slab.hpp:186-188).
+int refcpu_schur_forward(void* hp, int r, const double* R, double* shat) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const TimeBasis basis = time_matrices(r);
+    const SchurForm s = real_schur(basis);
+    const int n = r + 1, nt = h->ops.n_total();
+    for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < nt; ++k) shat[i * nt + k] = 0.0;
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < nt; ++k) shat[i * nt + k] += s.q(j, i) * (R[j * nt + k] / basis.weights[j]);
+    }
+    GUARD_END
+}
+
+// Seeded generators:
+//   uniform x_i = -1 + 2 * ((mt19937_64() >> 11) * 2^-53)
+//   normal z = sqrt(-2 ln u1) cos(2 pi u2), u1 = ((g>>11)+1) 2^-53, u2 = (g>>11) 2^-53
+void refcpu_uniform(unsigned long long seed, long long n, double* out) {
+    std::mt19937_64 g(seed);
+    for (long long i = 0; i < n; ++i) out[i] = -1.0 + 2.0 * (static_cast<double>(g() >> 11) * 0x1.0p-53);
+}
+void refcpu_lognormal(unsigned long long seed, long long n, double sigma, double* out) {
+    std::mt19937_64 g(seed);
+    for (long long i = 0; i < n; ++i) {
+        const double u1 = (static_cast<double>(g() >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = static_cast<double>(g() >> 11) * 0x1.0p-53;
+        out[i] = std::exp(sigma * (std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2)));
+    }
+}
+
+}  // extern "C"
