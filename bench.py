@@ -1,0 +1,285 @@
+"""Benchmark of the hot path: the preconditioned GMRES solve of the dG(1)
+space-time slab system of BASELINE config 1 (128^2, 20 slabs, lognormal K),
+plus the space-time SpMV bandwidth sweep of config 3 (256^2 .. 1024^2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step is one slab of the device-resident march (slab rhs, Schur transform,
+GMRES with the fixed-stress preconditioner, back-transform, jump update).
+`value` is the GMRES solve time per time slab (ms, max over ranks, lower is
+better); `e2e` is the same through the C ABI with host buffers (rhs H2D and
+solution D2H inside the timed region). Multi-GPU (N > 1): replicas only
+(DESIGN.md). The oracle (oracle/) is used only by the cpu_baseline leg and by
+--impl reference.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMRES solve time/time-slab (config 1: 128^2 dG(1)); GDoF/s space-time SpMV (frac of HBM roofline)"
+WORKLOAD = "config1: 2D Biot 128x128, dG(1), tau=0.05, GMRES(50) tol 1e-10, 1 fixed-stress sweep"
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc = index, None
+        self.path = f"/tmp/pdg_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_config1(slabs):
+    """CPU leg: the oracle (Eigen-free restatement of the reference, exact
+    banded sparse-direct inner solves) on config 1 for `slabs` slabs."""
+    from oracle import refcpu
+    from paper_1801_04984_b200 import problem as P
+    refcpu.build()
+    run = P.RUNS["config1"]
+    k = np.load(os.path.join(ROOT, "tests", "golden", "config1_k_perm.npy"))
+    spec = P.ProblemSpec(nx=128, ny=128, disp=P.baseline_bcs()[0], flow=P.baseline_bcs()[1], k_perm_cells=k,
+                         **P.baseline_material())
+    rp = refcpu.RefProblem(spec.to_dict())
+    return rp.march(run["r"], run["T"], run["n_slabs"], tol=run["tol"], restart=run["restart"], backend=1,
+                    max_slabs=slabs)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    slabs = max(1, min(args.warmup + args.steps, 20))
+    t0 = time.time()
+    res = oracle_config1(slabs)
+    secs = res["solve_seconds"][1:] if slabs > 1 else res["solve_seconds"]
+    ms = 1e3 * float(np.mean(secs))
+    sample = (f"{slabs} slabs of config 1 (first slab as warm-up when more than one; setup "
+              f"{res['setup_seconds']:.1f} s excluded); oracle = Eigen-free restatement of the reference with exact "
+              "banded sparse-direct inner solves; factorisation OpenMP-parallel, triangular solves serial")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/slab", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded lognormal K, BASELINE config 1)",
+        "config": {"workload": WORKLOAD, "slabs_run": slabs},
+        "cpu_baseline": {"value": ms, "unit": "ms/slab", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": ms, "unit": "ms/slab", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations": [int(i) for i in res["iterations"]], "wall_s": time.time() - t0}), flush=True)
+
+
+def spmv_sweep(sizes, reps, peak):
+    """Config 3: canonical dG(1) operator at n x n, `reps` back-to-back
+    applications, each CUDA-event timed on the library stream; median."""
+    import torch
+    from paper_1801_04984_b200 import problem as P, solver as S
+    T = S.time_constants(1)["T"]
+    out = []
+    for n in sizes:
+        ops = S.SpatialOperators.assemble(P.config3(n))
+        op = S.SpaceTimeOperator(ops, T, 0.05)
+        x = torch.from_numpy(P.uniform_vector(P.X_SEED, op.rows)).cuda()
+        y = torch.empty_like(x)
+        op.apply_device(x.data_ptr(), y.data_ptr(), 3)
+        t = sorted(op.apply_device(x.data_ptr(), y.data_ptr(), reps, times=True))
+        med = t[len(t) // 2] * 1e-3
+        b_alg = 8.0 * (op.nnz + 2 * op.rows)
+        gbs = b_alg / med / 1e9
+        out.append({"n": n, "rows": op.rows, "nnz": op.nnz, "median_ms": med * 1e3, "min_ms": t[0],
+                    "gdof_s": op.rows / med / 1e9, "alg_GB": b_alg / 1e9, "achieved_GBs": gbs, "frac": gbs / peak})
+        del op, ops, x, y
+        torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--spmv-sizes", default="256,512,1024")
+    ap.add_argument("--spmv-reps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-slabs", type=int, default=2)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1801_04984_b200 import _lib, problem as P, solver as S
+
+    peak, peak_kind = hbm_peak()
+    L = _lib.lib()
+    run = P.RUNS["config1"]
+    tau = run["T"] / run["n_slabs"]
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]))
+    t_setup = time.time()
+    ops = S.SpatialOperators.assemble(P.config1(128), device=local)
+    slab = S.SlabSolver(ops, run["r"], tau, opt)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+    nt, nn = ops.n_total, run["r"] + 1
+    dev = torch.device("cuda", local)
+    u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
+    p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
+    rhs = torch.empty(nn * nt, dtype=torch.float64, device=dev)
+    out = torch.empty_like(rhs)
+    rhs_host = []
+
+    def step(n, keep=False):
+        slab.rhs_device(tau * n, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+        if keep:
+            rhs_host.append(rhs.cpu().pin_memory().numpy())
+        rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+        end = out[run["r"] * nt:(run["r"] + 1) * nt]
+        u_prev.copy_(end[:ops.n_u])
+        p_prev.copy_(end[ops.n_u + ops.n_q:])
+        return rep
+
+    for n in range(args.warmup):
+        step(n)
+    # the rhs of the timed slabs, for the e2e leg (collected outside the timed region)
+    snap = (u_prev.clone(), p_prev.clone())
+    for n in range(args.warmup, args.warmup + args.steps):
+        step(n, keep=True)
+    u_prev.copy_(snap[0])
+    p_prev.copy_(snap[1])
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    iters = []
+    launches0 = L.pdg_util_launch_count()
+    S.profile(enable=True, reset=True)
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for n in range(args.warmup, args.warmup + args.steps):
+            iters.append(step(n).iterations)
+        e1.record()
+        torch.cuda.synchronize()
+    phases_raw = S.profile(enable=False)
+    launches = L.pdg_util_launch_count() - launches0
+    ms_dev = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.summary()
+    phases = {k: {"ms_per_step": v[0] / args.steps, "calls_per_step": v[1] / args.steps,
+                  "alg_GB_per_call": (v[2] / v[1] / 1e9) if v[1] else 0.0,
+                  "achieved_GBs": (v[2] / (v[0] * 1e-3) / 1e9) if v[0] else 0.0} for k, v in phases_raw.items()}
+    dom = max(phases, key=lambda k: phases[k]["ms_per_step"])
+    ach = phases[dom]["achieved_GBs"]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_kind": peak_kind, "traffic": None,
+                "share_of_step": phases[dom]["ms_per_step"] / ms_dev if ms_dev else None}
+
+    # e2e: the reference-facing call (pdg_slab_solve) with HOST buffers
+    e2e = []
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        _, _rep = slab.solve(rhs_host[k])
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = float(np.mean(e2e))
+
+    t = torch.tensor([ms_dev, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_dev, e2e_ms = float(t[0]), float(t[1])
+
+    spmv = spmv_sweep([int(s) for s in args.spmv_sizes.split(",") if s], args.spmv_reps, peak) \
+        if rank == 0 and args.spmv_sizes else []
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+        res = oracle_config1(args.cpu_slabs)
+        secs = res["solve_seconds"][1:] if args.cpu_slabs > 1 else res["solve_seconds"]
+        cpu = {"value": 1e3 * float(np.mean(secs)), "unit": "ms/slab", "cores": os.cpu_count(), "kind": "port",
+               "iterations": [int(i) for i in res["iterations"]],
+               "sample": f"{args.cpu_slabs} slab(s) of config 1 on the host (setup {res['setup_seconds']:.1f} s "
+                         "excluded); oracle with exact banded sparse-direct inner solves; factorisation "
+                         "OpenMP-parallel, triangular solves serial"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ms_dev, "unit": "ms/slab", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded lognormal K, BASELINE config 1)",
+            "config": {"workload": WORKLOAD, "rows_per_block": nn * nt,
+                       "l2": "no flush: per-step working set (A factor ~3 GB) > 126 MB L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "setup_s": setup_s},
+            "iterations": iters,
+            "e2e": {"value": e2e_ms, "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
+                    "d2h_bytes_per_step": 8 * nn * nt},
+            "gpu_launches": int(launches), "roofline": roofline, "phases": phases, "spmv": spmv, "clocks": clocks,
+            "cpu_baseline": cpu}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,183 @@
+/*
+ * porodg_b200 -- C ABI of the B200-native (sm_100a) solver for the porodg
+ * reference's hot path: the preconditioned GMRES solve of one transformed
+ * dG(r)-in-time Biot slab block.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj/include/porodg/):
+ *
+ *   pdg_ops_upload / pdg_ops_assemble
+ *       SpatialOperators produced by assemble_operators  (assembly.hpp:38-52, :177-395)
+ *   pdg_block_create
+ *       SlabSolver ctor, BlockSolverKind::gmres_fs branch (slab.hpp:154-171):
+ *       the shared A factorisation (slab.hpp:155), the block operator
+ *       FixedStressSolver(T_gg) and the per-component preconditioner
+ *       FixedStressSolver(lambda = T_gg(0,0)) (slab.hpp:161-169)
+ *   pdg_block_solve
+ *       gmres(op, pre, rhs, opt.gmres) for one diagonal Schur block
+ *       (slab.hpp:220-234 -> gmres.hpp:145-150 -> gmres_impl gmres.hpp:40-139)
+ *   pdg_block_apply
+ *       FixedStressSolver::apply_block -> apply_block_operator (fixed_stress.hpp:38-60,104-106),
+ *       evaluated on the canonical assembled space-time operator
+ *   pdg_block_precondition
+ *       FixedStressSolver::precondition (fixed_stress.hpp:177-181) per time component
+ *   pdg_slab_create / pdg_slab_solve
+ *       SlabSolver::solve (slab.hpp:179-255): Schur transform, block solve, back-transform
+ *   pdg_spmv_csr
+ *       SparseMatrix::apply (sparse.hpp:30-40), order-fixed (bit-identical)
+ *
+ * Conventions: plain pointers and sizes, caller-owned HOST buffers (copied
+ * inside the call) unless a function name ends in _device. Every function
+ * returns a pdg_status; the message of the last failure on the calling
+ * thread is pdg_last_error(). Handles are not thread-safe; destroy order is
+ * block/slab -> ops -> ctx.
+ */
+#ifndef PORODG_B200_H
+#define PORODG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PDG_OK = 0,
+    PDG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    PDG_NOT_CONVERGED = 2,    /* SolverError (GMRES budget, singular factor) */
+    PDG_CUDA_ERROR = 3,
+    PDG_NCCL_ERROR = 4,
+    PDG_OUT_OF_MEMORY = 5
+} pdg_status;
+
+typedef struct pdg_ctx pdg_ctx;
+typedef struct pdg_ops pdg_ops;
+typedef struct pdg_block pdg_block;
+typedef struct pdg_slab pdg_slab;
+
+/* CSR view (SparseMatrix, sparse.hpp:20-27): int32 offsets and indices. */
+typedef struct {
+    int rows, cols, nnz;
+    const int* row_offsets;  /* rows + 1 */
+    const int* col_indices;  /* nnz, strictly increasing per row */
+    const double* values;    /* nnz */
+} pdg_csr;
+
+/* Structured mesh + material + constant boundary data (mesh.hpp:73,
+ * material.hpp:25, boundary.hpp:27-69) for on-device assembly. */
+typedef struct {
+    int nx, ny;
+    double lx, ly;
+    double lambda, mu, k_perm, eta, biot_m, biot_b;
+    const double* k_perm_cells; /* NULL or nx*ny values, cell c = j*nx + i */
+    double penalty;             /* SIPG gamma (problems.hpp:273 default 10) */
+    int disp_kind[4];           /* tags left,right,bottom,top: 0 fixed 1 traction 2 roller_x 3 roller_y */
+    double disp_data[4][2];     /* constant Dirichlet value / traction vector */
+    int flow_kind[4];           /* 0 pressure, 1 no_flow */
+    double flow_data[4];        /* constant boundary pressure */
+} pdg_problem;
+
+/* GmresOptions (gmres.hpp:24-28) + FixedStressConfig (fixed_stress.hpp:17-22). */
+typedef struct {
+    double tol;     /* relative true residual, default 1e-10 */
+    int restart;    /* default 100 in the reference, 50 in the BASELINE configs */
+    int max_iter;   /* default 400 */
+    int sweeps;     /* truncated fixed-stress sweeps per preconditioner call, default 1 */
+    double stab;    /* < 0: b^2 / K_dr (fixed_stress.hpp:23-27) */
+    int candidate;  /* 0: x + P(V y) as gmres.hpp:116 (reference); 1: x + Z y (gmres_flexible, gmres.hpp:113-114) */
+} pdg_gmres_opts;
+
+/* SolverReport (gmres.hpp:15-20) plus timings. */
+typedef struct {
+    int converged;
+    int iterations;
+    double final_rel_res;
+    double* history;   /* caller buffer for the true-residual history, may be NULL */
+    int history_cap;
+    int history_len;
+    double device_ms;  /* device time of the solve (CUDA events on the block's stream) */
+    int kernel_launches;
+} pdg_report;
+
+const char* pdg_last_error(void);
+const char* pdg_version(void);
+
+int pdg_ctx_create(int device, pdg_ctx** out);
+void pdg_ctx_destroy(pdg_ctx* ctx);
+
+/* Upload reference-assembled operators (SpatialOperators) from host CSR. */
+int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B,
+                   const pdg_csr* E, const double* m_p_diag, const signed char* q_constrained, double biot_b,
+                   double inv_m, double k_dr, pdg_ops** out);
+/* Assemble the operators on the device (one thread block per cell / face). */
+int pdg_ops_assemble(pdg_ctx* ctx, const pdg_problem* problem, pdg_ops** out);
+/* Sizes: n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E). */
+int pdg_ops_sizes(const pdg_ops* ops, long long sizes[7]);
+/* Download block `which` (0 A, 1 M_q, 2 B, 3 E) as CSR into caller buffers. */
+int pdg_ops_download(const pdg_ops* ops, int which, int* row_offsets, int* col_indices, double* values);
+/* assemble_rhs (assembly.hpp:467-563) for constant boundary data at time t. */
+int pdg_ops_rhs(const pdg_ops* ops, double t, double* u, double* q, double* p);
+void pdg_ops_destroy(pdg_ops* ops);
+
+/* One transformed diagonal block: theta is m x m row-major (T_gg), lambda_pre
+ * the preconditioner's time weight (T_gg(0,0)). */
+int pdg_block_create(pdg_ops* ops, int m, const double* theta, double tau, double lambda_pre,
+                     const pdg_gmres_opts* opts, pdg_block** out);
+int pdg_block_rows(const pdg_block* blk, long long* rows, long long* nnz);
+/* x = GMRES solution of (Theta (x) D + tau K) x = rhs. Host buffers of m * n_total doubles. */
+int pdg_block_solve(pdg_block* blk, const double* rhs, double* x, pdg_report* rep);
+/* Same with device pointers (no host copies). */
+int pdg_block_solve_device(pdg_block* blk, const double* rhs_dev, double* x_dev, pdg_report* rep);
+/* y = op(x); mode 0: order-fixed canonical operator (bit-defined). */
+int pdg_block_apply(pdg_block* blk, int mode, const double* x, double* y);
+int pdg_block_apply_device(pdg_block* blk, int mode, const double* x_dev, double* y_dev, int repeats, float* ms);
+/* z = precondition(r) for all m components (slab.hpp:221-226). */
+int pdg_block_precondition(pdg_block* blk, const double* r, double* z);
+/* Download the canonical space-time CSR (rows+1 offsets as int64). */
+int pdg_block_download_csr(const pdg_block* blk, long long* row_offsets, int* col_indices, double* values);
+void pdg_block_destroy(pdg_block* blk);
+
+/* The canonical space-time operator alone (no preconditioner / factorisation):
+ * the object of the SpMV bandwidth sweep (BASELINE config 3). */
+typedef struct pdg_op pdg_op;
+int pdg_op_create(pdg_ops* ops, int m, const double* theta, double tau, pdg_op** out);
+int pdg_op_rows(const pdg_op* op, long long* rows, long long* nnz);
+/* y = op(x) `repeats` times on device buffers; per-launch times (ms) into times_ms[repeats] if not NULL. */
+int pdg_op_apply_device(pdg_op* op, const double* x_dev, double* y_dev, int repeats, float* times_ms);
+int pdg_op_download_csr(const pdg_op* op, long long* row_offsets, int* col_indices, double* values);
+void pdg_op_destroy(pdg_op* op);
+
+/* Per-phase device timing (CUDA events on the library stream). Phases:
+ * 0 space-time SpMV, 1 displacement solve, 2 flow solve, 3 other preconditioner
+ * kernels, 4 Krylov vector kernels, 5 slab transforms / rhs. alg_bytes is the
+ * algorithmic traffic summed over the calls. */
+void pdg_profile_enable(int on);
+void pdg_profile_reset(void);
+int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes);
+
+/* Slab solver for dG(r), r <= 1 (SlabSolver, slab.hpp:133-274). */
+int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts, pdg_slab** out);
+/* rhs: (r+1) * n_total stacked per Radau node (SlabSystem::rhs); out: (r+1) * n_total solution comps. */
+int pdg_slab_solve(pdg_slab* slab, const double* rhs, double* out, pdg_report* rep);
+int pdg_slab_solve_device(pdg_slab* slab, const double* rhs_dev, double* out_dev, pdg_report* rep);
+/* Slab right-hand side (build_slab_system, slab.hpp:58-87) on the device: jump data u_prev/p_prev
+ * (device), slab start t0 -> rhs_dev ((r+1) * n_total). */
+int pdg_slab_rhs_device(pdg_slab* slab, double t0, const double* u_prev_dev, const double* p_prev_dev, double* rhs_dev);
+void pdg_slab_destroy(pdg_slab* slab);
+
+/* Order-fixed CSR SpMV (SparseMatrix::apply) on device buffers. */
+int pdg_spmv_csr_device(int rows, const long long* row_offsets_dev, const int* col_indices_dev,
+                        const double* values_dev, const double* x_dev, double* y_dev);
+
+/* dG(r) time constants, r <= 1 (time_matrices + real_schur, time_basis.hpp:135-182,
+ * schur.hpp:101-173): nodes, weights, phi(0) [r+1], T and Q [(r+1)^2 row-major]. */
+int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q);
+
+/* Seeded workload generators (Inputs). */
+void pdg_util_uniform(unsigned long long seed, long long n, double* out);
+void pdg_util_lognormal(unsigned long long seed, long long n, double sigma, double* out);
+/* Number of library kernel launches issued on the calling thread so far. */
+long long pdg_util_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,558 @@
+// Fixed-stress preconditioner, deterministic Krylov kernels and the GMRES
+// driver of one slab block.
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "block.cuh"
+
+namespace pdg {
+
+namespace {
+
+constexpr int kRedBlocks = 256;  // fixed => reductions are bit-reproducible on any GPU
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+    return s;  // valid on thread 0
+}
+
+// partial[b * ncols + j] = sum over this block's rows of V_j . w
+__global__ void __launch_bounds__(kRedThreads) k_multidot1(long long n, int ncols, const double* __restrict__ V,
+                                                           const double* __restrict__ w, double* __restrict__ partial) {
+    __shared__ double sh[32];
+    for (int j0 = 0; j0 < ncols; j0 += 4) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+            const double wr = w[r];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (j0 + q < ncols) a[q] += V[(long long)(j0 + q) * n + r] * wr;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double s = block_sum(a[q], sh);
+            if (threadIdx.x == 0 && j0 + q < ncols) partial[(long long)blockIdx.x * ncols + j0 + q] = s;
+        }
+    }
+}
+
+// out[j] = sum_b partial[b * ncols + j]  (one block per column, fixed tree)
+__global__ void __launch_bounds__(kRedThreads) k_multidot2(int nparts, int ncols, const double* __restrict__ partial,
+                                                           double* __restrict__ out) {
+    __shared__ double sh[32];
+    const int j = blockIdx.x;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v += partial[(long long)b * ncols + j];
+    const double s = block_sum(v, sh);
+    if (threadIdx.x == 0) out[j] = s;
+}
+
+// w -= sum_j h_j V_j, subtracting column by column in j order
+__global__ void k_multiaxpy(long long n, int ncols, const double* __restrict__ V, const double* __restrict__ h,
+                            double* __restrict__ w) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        double v = w[r];
+        for (int j = 0; j < ncols; ++j) v -= h[j] * V[(long long)j * n + r];
+        w[r] = v;
+    }
+}
+
+// out = base + sum_j y_j V_j (base may be null => 0), summed in j order from 0.0
+__global__ void k_combine(long long n, int ncols, const double* __restrict__ V, const double* __restrict__ y,
+                          const double* __restrict__ base, double* __restrict__ out) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < ncols; ++j) s += V[(long long)j * n + r] * y[j];
+        out[r] = base ? base[r] + s : s;
+    }
+}
+
+__global__ void k_scale_div(long long n, const double* __restrict__ src, const double* __restrict__ d, double* __restrict__ dst) {
+    const double dv = *d;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        dst[r] = src[r] / dv;
+}
+
+__global__ void k_sub(long long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        out[r] = a[r] - b[r];
+}
+
+__global__ void k_add(long long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        out[r] = a[r] + b[r];
+}
+
+__global__ void k_sqrt(double* v) { *v = sqrt(*v); }
+
+// ---- fixed-stress sweep kernels (fixed_stress.hpp:109-139) ------------------
+// fp_i = r_p_i [+ lambda (b E^T u_i - stab m_p p_i) for sweeps after the first]
+__global__ void k_flow_fp(int m, int np, int nt, int nu, int nq, int lag, double lambda, double b, double stab,
+                          const double* __restrict__ r, const double* __restrict__ xold, const int* et_off,
+                          const int* et_idx, const double* et_val, const double* m_p, double* __restrict__ fp) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
+        double pr = r[(long long)i * nt + nu + nq + c];
+        if (lag) {
+            double et = 0.0;
+            for (int k = et_off[c]; k < et_off[c + 1]; ++k) et += et_val[k] * xold[(long long)i * nt + et_idx[k]];
+            pr += lambda * (b * et - stab * (m_p[c] * xold[(long long)i * nt + nu + nq + c]));
+        }
+        fp[t] = pr;
+    }
+}
+// rq_i[f] = r_q_i[f] - sum_{B row f} (w bv) (dinv_c fp_c)
+__global__ void k_flow_rq(int m, int nq, int np, int nt, int nu, double w, const double* __restrict__ r,
+                          const double* __restrict__ fp, const int* b_off, const int* b_idx, const double* b_val,
+                          const double* __restrict__ dinv, double* __restrict__ rq) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nq; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nq), f = static_cast<int>(t % nq);
+        double v = r[(long long)i * nt + nu + f];
+        for (int k = b_off[f]; k < b_off[f + 1]; ++k) {
+            const int c = b_idx[k];
+            v -= w * b_val[k] * (dinv[c] * fp[(long long)i * np + c]);
+        }
+        rq[t] = v;
+    }
+}
+// p_i[c] = dinv_c (fp_c - w sum_{B^T row c} bv q_f)   (q already in z)
+__global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const double* __restrict__ fp,
+                         const int* bt_off, const int* bt_idx, const double* bt_val, const double* __restrict__ dinv,
+                         double* __restrict__ z) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
+        double btq = 0.0;
+        for (int k = bt_off[c]; k < bt_off[c + 1]; ++k) btq += bt_val[k] * z[(long long)i * nt + nu + bt_idx[k]];
+        z[(long long)i * nt + nu + nq + c] = dinv[c] * (fp[t] - w * btq);
+    }
+}
+// mech_i = r_u_i / w + b (E p_i)
+__global__ void k_mech_rhs(int m, int nu, int nt, int nq, double w, double b, const double* __restrict__ r,
+                           const double* __restrict__ z, const int* e_off, const int* e_idx, const double* e_val,
+                           double* __restrict__ mech) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nu; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nu), k0 = static_cast<int>(t % nu);
+        double ep = 0.0;
+        for (int k = e_off[k0]; k < e_off[k0 + 1]; ++k) ep += e_val[k] * z[(long long)i * nt + nu + nq + e_idx[k]];
+        mech[t] = r[(long long)i * nt + k0] / w + b * ep;
+    }
+}
+
+// S_q dense blocks (face-row order), one thread per face row: no write conflicts.
+__global__ void k_flow_schur_blocks(int nq, double w, const int* mq_off, const int* mq_idx, const double* mq_val,
+                                    const int* b_off, const int* b_idx, const double* b_val, const int* bt_off,
+                                    const int* bt_idx, const double* bt_val, const double* dinv, const int* inv_perm,
+                                    const int* blk_of, const int* loc_of, const int* bsz, const long long* dD,
+                                    const long long* dC, double* dense, int* err) {
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nq; f += gridDim.x * blockDim.x) {
+        const int nr = inv_perm[f], jr = blk_of[nr], lr = loc_of[nr];
+        auto add = [&](int f2, double v) {
+            const int nc = inv_perm[f2], jc = blk_of[nc], lc = loc_of[nc];
+            if (jc == jr)
+                dense[dD[jr] + lr + (long long)lc * bsz[jr]] += v;
+            else if (jr == jc + 1)
+                dense[dC[jc] + lr + (long long)lc * bsz[jr]] += v;
+            else if (jc != jr + 1)
+                atomicOr(err, 1);
+        };
+        for (int k = mq_off[f]; k < mq_off[f + 1]; ++k) add(mq_idx[k], w * mq_val[k]);
+        for (int k = b_off[f]; k < b_off[f + 1]; ++k) {
+            const int c = b_idx[k];
+            const double wa = w * b_val[k];
+            for (int q = bt_off[c]; q < bt_off[c + 1]; ++q) add(bt_idx[q], -(wa * (w * bt_val[q])) * dinv[c]);
+        }
+    }
+}
+
+__global__ void k_dinv(int np, double coef, const double* m_p, double* dinv) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) dinv[c] = 1.0 / (-coef * m_p[c]);
+}
+
+// ---- host least squares: Householder QR with column pivoting ---------------
+// min || beta e1 - H y ||, H (rows x cols) column-major; numerical rank as in
+// a column-pivoted QR with threshold eps * max column norm.
+std::vector<double> ls_colpiv(std::vector<double> a, int rows, int cols, std::vector<double> rhs) {
+    auto A = [&](int i, int j) -> double& { return a[(size_t)j * rows + i]; };
+    const int size = std::min(rows, cols);
+    std::vector<double> tau(size, 0.0), nrm(cols);
+    std::vector<int> piv(cols);
+    for (int j = 0; j < cols; ++j) piv[j] = j;
+    double maxn = 0.0;
+    for (int j = 0; j < cols; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < rows; ++i) s += A(i, j) * A(i, j);
+        nrm[j] = std::sqrt(s);
+        maxn = std::max(maxn, nrm[j]);
+    }
+    const double eps = std::numeric_limits<double>::epsilon();
+    const double thr = (maxn * eps) * (maxn * eps) / rows;
+    int rank = size;
+    for (int k = 0; k < size; ++k) {
+        // exact remaining column norms (rows k..)
+        int best = k;
+        double bestv = -1.0;
+        for (int j = k; j < cols; ++j) {
+            double s = 0.0;
+            for (int i = k; i < rows; ++i) s += A(i, j) * A(i, j);
+            nrm[j] = s;
+            if (s > bestv) {
+                bestv = s;
+                best = j;
+            }
+        }
+        if (rank == size && bestv < thr * (rows - k)) rank = k;
+        if (best != k) {
+            for (int i = 0; i < rows; ++i) std::swap(A(i, k), A(i, best));
+            std::swap(piv[k], piv[best]);
+        }
+        double tail = 0.0;
+        for (int i = k + 1; i < rows; ++i) tail += A(i, k) * A(i, k);
+        const double c0 = A(k, k);
+        double beta;
+        if (tail <= std::numeric_limits<double>::min()) {
+            tau[k] = 0.0;
+            beta = c0;
+            for (int i = k + 1; i < rows; ++i) A(i, k) = 0.0;
+        } else {
+            beta = std::sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            for (int i = k + 1; i < rows; ++i) A(i, k) /= (c0 - beta);
+            tau[k] = (beta - c0) / beta;
+        }
+        A(k, k) = beta;
+        if (tau[k] != 0.0)
+            for (int j = k + 1; j < cols; ++j) {
+                double t = A(k, j);
+                for (int i = k + 1; i < rows; ++i) t += A(i, k) * A(i, j);
+                A(k, j) -= tau[k] * t;
+                for (int i = k + 1; i < rows; ++i) A(i, j) -= tau[k] * A(i, k) * t;
+            }
+    }
+    std::vector<double> y(cols, 0.0);
+    if (rank == 0) return y;
+    for (int k = 0; k < rank; ++k) {
+        if (tau[k] == 0.0) continue;
+        double t = rhs[k];
+        for (int i = k + 1; i < rows; ++i) t += A(i, k) * rhs[i];
+        rhs[k] -= tau[k] * t;
+        for (int i = k + 1; i < rows; ++i) rhs[i] -= tau[k] * A(i, k) * t;
+    }
+    for (int i = rank - 1; i >= 0; --i) {
+        double s = rhs[i];
+        for (int j = i + 1; j < rank; ++j) s -= A(i, j) * rhs[j];
+        rhs[i] = s / A(i, i);
+    }
+    for (int i = 0; i < rank; ++i) y[piv[i]] = rhs[i];
+    return y;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st) {
+    auto a = std::make_shared<ASolver>();
+    // cell-row order: block j = displacement dofs of cell row j (8 nx each)
+    require(ops.nx > 0 && ops.ny > 0 && ops.n_u == 8 * ops.nx * ops.ny, "A solver: mesh dimensions do not match n_u");
+    std::vector<int> bs(ops.ny, 8 * ops.nx);
+    a->chol.factor(ops.n_u, ops.A.off.p, ops.A.idx.p, ops.A.val.p, {}, bs, max_rhs, st);
+    return a;
+}
+
+void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lambda_, double stab_, int sweeps_,
+                           std::shared_ptr<ASolver> a_, cudaStream_t st) {
+    ops = &o;
+    m = m_;
+    tau = tau_;
+    lambda = lambda_;
+    stab = stab_;
+    sweeps = sweeps_;
+    w = tau * 1.0;
+    a = std::move(a_);
+    require(sweeps >= 1, "fixed-stress: sweep counts must be >= 1");
+    require(lambda * (o.inv_m + stab) > 0.0, "fixed-stress: flow storage block must be negative definite");
+    dinv.alloc(o.n_p);
+    k_dinv<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, lambda * (o.inv_m + stab), o.m_p.p, dinv.p);
+    PDG_CHECK_LAUNCH();
+    // face-row permutation: level j horizontal faces, then row j vertical faces
+    const int nx = o.nx, ny = o.ny;
+    require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
+    std::vector<int> perm;
+    std::vector<int> bs;
+    perm.reserve(o.n_q);
+    for (int j = 0; j <= ny; ++j) {
+        const size_t before = perm.size();
+        for (int i = 0; i < nx; ++i) perm.push_back(j * nx + i);
+        if (j < ny)
+            for (int i = 0; i <= nx; ++i) perm.push_back(nx * (ny + 1) + i * ny + j);
+        bs.push_back(static_cast<int>(perm.size() - before));
+    }
+    flow.prof_phase = PROF_FLOW_SOLVE;
+    flow.layout(o.n_q, perm, bs);
+    flow.max_rhs = m;
+    DBuf<double> dense(flow.dense_total());
+    dense.zero(st);
+    std::vector<long long> dD(flow.nb), dC(flow.nb);
+    for (int j = 0; j < flow.nb; ++j) {
+        dD[j] = flow.dense_d_offset(j);
+        dC[j] = flow.dense_c_offset(j);
+    }
+    DBuf<long long> ddD, ddC;
+    ddD.upload(dD, st);
+    ddC.upload(dC, st);
+    DBuf<int> err(1);
+    err.zero(st);
+    k_flow_schur_blocks<<<grid_for(o.n_q, 256), 256, 0, st>>>(o.n_q, w, o.M_q.off.p, o.M_q.idx.p, o.M_q.val.p, o.B.off.p,
+                                                               o.B.idx.p, o.B.val.p, o.Bt.off.p, o.Bt.idx.p, o.Bt.val.p,
+                                                               dinv.p, flow.inv_perm.p, flow.blk_of.p, flow.loc_of.p,
+                                                               flow.d_bsz.p, ddD.p, ddC.p, dense.p, err.p);
+    PDG_CHECK_LAUNCH();
+    int herr = 0;
+    PDG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    require(herr == 0, "fixed-stress: flow Schur complement is not block tridiagonal in face-row order");
+    flow.factor_dense(dense.p, dense.p, st);
+    rq.alloc((size_t)m * o.n_q);
+    fp.alloc((size_t)m * o.n_p);
+    mech.alloc((size_t)m * o.n_u);
+    if (sweeps > 1) xold.alloc((size_t)m * o.n_total());
+}
+
+void FixedStressPre::apply(const double* r, double* z, cudaStream_t st) {
+    const SpatialOps& o = *ops;
+    const int nt = o.n_total(), nu = o.n_u, nq = o.n_q, np = o.n_p;
+    for (int s = 0; s < sweeps; ++s) {
+        const int lag = s > 0;
+        if (lag) PDG_CUDA(cudaMemcpyAsync(xold.p, z, sizeof(double) * (size_t)m * nt, cudaMemcpyDeviceToDevice, st));
+        {
+        ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (2.0 * np + 2.0 * nq + 3.0 * o.B.nnz));
+        k_flow_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, lag, lambda, o.biot_b, stab, r,
+                                                                    lag ? xold.p : nullptr, o.Et.off.p, o.Et.idx.p,
+                                                                    o.Et.val.p, o.m_p.p, fp.p);
+        k_flow_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, w, r, fp.p, o.B.off.p, o.B.idx.p,
+                                                                    o.B.val.p, dinv.p, rq.p);
+        count_launch(2);
+        PDG_CHECK_LAUNCH();
+        }
+        flow.solve(rq.p, nq, z + nu, nt, m, st);
+        {
+        ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (3.0 * np + 2.0 * o.Bt.nnz + 2.0 * nu + 2.0 * o.E.nnz));
+        k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fp.p, o.Bt.off.p, o.Bt.idx.p,
+                                                                   o.Bt.val.p, dinv.p, z);
+        k_mech_rhs<<<grid_for((long long)m * nu, 256), 256, 0, st>>>(m, nu, nt, nq, w, o.biot_b, r, z, o.E.off.p,
+                                                                     o.E.idx.p, o.E.val.p, mech.p);
+        count_launch(2);
+        PDG_CHECK_LAUNCH();
+        }
+        a->chol.solve(mech.p, nu, z, nt, m, st);
+    }
+}
+
+void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
+    n = n_;
+    restart = restart_;
+    V.alloc((size_t)n * (restart + 1));
+    if (keep_z) Z.alloc((size_t)n * restart);
+    w.alloc(n);
+    x.alloc(n);
+    r.alloc(n);
+    cand.alloc(n);
+    t.alloc(n);
+    y_dev.alloc(restart + 2);
+    h_dev.alloc(restart + 2);
+    partial.alloc((size_t)kRedBlocks * (restart + 2));
+    norm_dev.alloc(4);
+    if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (restart + 8)));
+    (void)st;
+}
+Gmres::~Gmres() {
+    if (h_host) cudaFreeHost(h_host);
+}
+
+void Block::create(const SpatialOps& o, int m_, const double* th, double tau_, double lambda_, const pdg_gmres_opts& op_,
+                   std::shared_ptr<ASolver> a) {
+    ops = &o;
+    ctx = o.ctx;
+    m = m_;
+    tau = tau_;
+    lambda = lambda_;
+    theta.assign(th, th + m * m);
+    opts = op_;
+    require(opts.tol > 0.0 && opts.tol < 1.0, "gmres: tol must be in (0,1)");
+    require(opts.restart >= 1 && opts.max_iter >= 1, "gmres: bad iteration limits");
+    require(tau > 0.0, "FixedStressSolver: tau must be positive");
+    cudaStream_t st = ctx->stream;
+    op.build(o, m, th, tau, st);
+    const double stab = opts.stab < 0.0 ? o.biot_b * o.biot_b / o.k_dr : opts.stab;
+    require(stab >= 0.0, "fixed-stress: stabilization must be nonnegative");
+    if (!a) a = make_a_solver(o, 2, st);
+    pre.setup(o, m, tau, lambda, stab, opts.sweeps, a, st);
+    kr.setup(rows(), opts.restart, opts.candidate == 1, st);
+    PDG_CUDA(cudaEventCreate(&ev0));
+    PDG_CUDA(cudaEventCreate(&ev1));
+    PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+Block::~Block() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+}
+
+namespace {
+struct KrylovOps {
+    cudaStream_t st;
+    Gmres& g;
+    // out[j] (device) = V_j . w for j < ncols ; returns on host in g.h_host
+    void multidot(const double* V, int ncols, const double* w, double* out_dev) {
+        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 1));
+        k_multidot1<<<kRedBlocks, kRedThreads, 0, st>>>(g.n, ncols, V, w, g.partial.p);
+        k_multidot2<<<ncols, kRedThreads, 0, st>>>(kRedBlocks, ncols, g.partial.p, out_dev);
+        count_launch(2);
+        PDG_CHECK_LAUNCH();
+    }
+    double norm(const double* v) {
+        multidot(v, 1, v, g.norm_dev.p);
+        ProfScope prof(PROF_KRYLOV, st, 0.0);
+        k_sqrt<<<1, 1, 0, st>>>(g.norm_dev.p);
+        count_launch();
+        PDG_CUDA(cudaMemcpyAsync(g.h_host, g.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        PDG_CUDA(cudaStreamSynchronize(st));
+        return g.h_host[0];
+    }
+};
+}  // namespace
+
+void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_index) {
+    cudaStream_t st = ctx->stream;
+    const long long n = rows();
+    const unsigned gr = grid_for(n, 256);
+    const long long launches0 = g_launches;
+    KrylovOps K{st, kr};
+    PDG_CUDA(cudaEventRecord(ev0, st));
+    std::vector<double> hist;
+    const double bnorm = K.norm(b);
+    bool converged = false;
+    int total = 0;
+    double true_res = bnorm;
+    auto finish = [&](double final_rel) {
+        PDG_CUDA(cudaEventRecord(ev1, st));
+        PDG_CUDA(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        PDG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+        if (rep) {
+            rep->converged = converged;
+            rep->iterations = total;
+            rep->final_rel_res = final_rel;
+            rep->history_len = static_cast<int>(hist.size());
+            if (rep->history)
+                for (int i = 0; i < std::min<int>(rep->history_cap, (int)hist.size()); ++i) rep->history[i] = hist[i];
+            rep->device_ms = ms;
+            rep->kernel_launches = static_cast<int>(g_launches - launches0);
+        }
+    };
+    if (bnorm <= 1e-14) {  // gmres.hpp:56-62
+        PDG_CUDA(cudaMemsetAsync(x_out, 0, sizeof(double) * n, st));
+        converged = true;
+        hist.push_back(bnorm);
+        finish(0.0);
+        return;
+    }
+    PDG_CUDA(cudaMemsetAsync(kr.x.p, 0, sizeof(double) * n, st));
+    hist.push_back(true_res);
+    const int restart = opts.restart, max_iter = opts.max_iter;
+    const bool flexible = opts.candidate == 1;
+    std::vector<double> H;
+    bool x_is_zero = true;
+    while (total < max_iter) {
+        if (x_is_zero) {  // r = b - op(0) = b exactly
+            PDG_CUDA(cudaMemcpyAsync(kr.r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        } else {
+            op.apply(kr.x.p, kr.t.p, st);
+            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_sub<<<gr, 256, 0, st>>>(n, b, kr.t.p, kr.r.p); }
+            count_launch();
+        }
+        const double beta = K.norm(kr.r.p);
+        if (beta / bnorm <= opts.tol) break;
+        const int mm = std::min(restart, max_iter - total);
+        H.assign((size_t)(mm + 1) * mm, 0.0);
+        auto h = [&](int i, int j) -> double& { return H[(size_t)j * (mm + 1) + i]; };
+        // v_0 = r / beta
+        { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_scale_div<<<gr, 256, 0, st>>>(n, kr.r.p, kr.norm_dev.p, kr.V.p); }
+        count_launch();
+        bool done = false;
+        for (int k = 0; k < mm && !done; ++k) {
+            double* vk = kr.V.p + (size_t)k * n;
+            double* zk = flexible ? kr.Z.p + (size_t)k * n : kr.cand.p;
+            pre.apply(vk, zk, st);
+            op.apply(zk, kr.w.p, st);
+            for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, two passes
+                K.multidot(kr.V.p, k + 1, kr.w.p, kr.h_dev.p);
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_multiaxpy<<<gr, 256, 0, st>>>(n, k + 1, kr.V.p, kr.h_dev.p, kr.w.p); }
+                count_launch();
+                PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaStreamSynchronize(st));
+                for (int i = 0; i <= k; ++i) h(i, k) += kr.h_host[i];
+            }
+            h(k + 1, k) = K.norm(kr.w.p);
+            double cn = 0.0;
+            for (int i = 0; i <= mm; ++i) cn += h(i, k) * h(i, k);
+            const bool breakdown = h(k + 1, k) <= 1e-14 * std::sqrt(cn);
+            if (!breakdown) {
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_scale_div<<<gr, 256, 0, st>>>(n, kr.w.p, kr.norm_dev.p, kr.V.p + (size_t)(k + 1) * n); }
+                count_launch();
+            }
+            ++total;
+            std::vector<double> hk((size_t)(k + 2) * (k + 1));
+            for (int j = 0; j <= k; ++j)
+                for (int i = 0; i < k + 2; ++i) hk[(size_t)j * (k + 2) + i] = h(i, j);
+            std::vector<double> e1(k + 2, 0.0);
+            e1[0] = beta;
+            const std::vector<double> y = ls_colpiv(hk, k + 2, k + 1, e1);
+            PDG_CUDA(cudaMemcpyAsync(kr.y_dev.p, y.data(), sizeof(double) * (k + 1), cudaMemcpyHostToDevice, st));
+            if (flexible) {  // cand = x + Z y
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                count_launch();
+            } else {  // cand = x + P(V y)   (gmres.hpp:116)
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.V.p, kr.y_dev.p, nullptr, kr.t.p); }
+                count_launch();
+                pre.apply(kr.t.p, kr.r.p, st);
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_add<<<gr, 256, 0, st>>>(n, kr.x.p, kr.r.p, kr.cand.p); }
+                count_launch();
+            }
+            // true residual (gmres.hpp:68-72)
+            op.apply(kr.cand.p, kr.t.p, st);
+            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_sub<<<gr, 256, 0, st>>>(n, b, kr.t.p, kr.r.p); }
+            count_launch();
+            true_res = K.norm(kr.r.p);
+            hist.push_back(true_res);
+            const bool ok = true_res / bnorm <= opts.tol;
+            if (ok || breakdown || k == mm - 1 || total >= max_iter) {
+                PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                x_is_zero = false;
+                done = true;
+                converged = ok;
+            }
+        }
+        if (converged) break;
+    }
+    const double final_rel = true_res / bnorm;
+    if (!converged) converged = final_rel <= opts.tol;
+    PDG_CUDA(cudaMemcpyAsync(x_out, kr.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    finish(final_rel);
+    if (!converged) {
+        char buf[64];
+        std::snprintf(buf, sizeof(buf), "%f", final_rel);
+        throw Error(PDG_NOT_CONVERGED,
+                    "slab block " + std::to_string(block_index) + ": GMRES did not converge (rel res " + buf + ")");
+    }
+}
+
+}  // namespace pdg

@@ -1,0 +1,64 @@
+// One transformed diagonal slab block on the device: canonical space-time
+// operator, truncated fixed-stress preconditioner and right-preconditioned
+// GMRES (slab.hpp:154-171, :220-234; fixed_stress.hpp:109-181; gmres.hpp:40-139).
+#pragma once
+
+#include <memory>
+
+#include "blocktri.cuh"
+#include "ops.cuh"
+#include "spacetime_op.cuh"
+
+namespace pdg {
+
+// Shared exact displacement solve (the reference shares one DenseLu of A
+// across all blocks, slab.hpp:155 / fixed_stress.hpp:89-94).
+struct ASolver {
+    BlockTriChol chol;
+};
+std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st);
+
+// FixedStressSolver(lambda) :: precondition for each of the m components.
+struct FixedStressPre {
+    const SpatialOps* ops = nullptr;
+    int m = 1, sweeps = 1;
+    double tau = 0, lambda = 0, stab = 0, w = 0;
+    std::shared_ptr<ASolver> a;
+    BlockTriChol flow;  // S_q = w M_q - w^2 B D^{-1} B^T in face-row order
+    DBuf<double> dinv;  // 1 / (-(lambda (1/M + stab)) m_p)
+    DBuf<double> rq, fp, mech, xold;
+    void setup(const SpatialOps& ops, int m, double tau, double lambda, double stab, int sweeps,
+               std::shared_ptr<ASolver> a, cudaStream_t st);
+    void apply(const double* r, double* z, cudaStream_t st);
+};
+
+struct Gmres {
+    long long n = 0;
+    int restart = 50;
+    DBuf<double> V, Z, w, x, r, cand, t, y_dev, h_dev, partial, norm_dev;
+    double* h_host = nullptr;  // pinned
+    void setup(long long n, int restart, bool keep_z, cudaStream_t st);
+    ~Gmres();
+};
+
+struct Block {
+    Ctx* ctx = nullptr;
+    const SpatialOps* ops = nullptr;
+    int m = 1;
+    double tau = 0, lambda = 0;
+    std::vector<double> theta;
+    pdg_gmres_opts opts{};
+    SpaceTimeOp op;
+    FixedStressPre pre;
+    Gmres kr;
+    DBuf<double> io_in, io_out;  // host-boundary staging
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long rows() const { return (long long)m * ops->n_total(); }
+    void create(const SpatialOps& ops, int m, const double* theta, double tau, double lambda,
+                const pdg_gmres_opts& o, std::shared_ptr<ASolver> a);
+    // GMRES solve, device pointers, on ctx->stream. Throws Error(PDG_NOT_CONVERGED) like slab.hpp:228-230.
+    void solve(const double* b, double* x, pdg_report* rep, int block_index = 0);
+    ~Block();
+};
+
+}  // namespace pdg

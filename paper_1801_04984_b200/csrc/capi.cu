@@ -1,0 +1,517 @@
+// C ABI of porodg_b200 (include/porodg_b200.h).
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "block.cuh"
+#include "timebasis.hpp"
+
+namespace pdg {
+thread_local long long g_launches = 0;
+static thread_local std::string g_err;
+}  // namespace pdg
+
+using namespace pdg;
+
+struct pdg_ctx {
+    Ctx c;
+};
+struct pdg_ops {
+    SpatialOps s;
+    std::shared_ptr<ASolver> a;  // shared displacement factorisation (slab.hpp:155)
+};
+struct pdg_block {
+    Block b;
+    DBuf<double> io_a, io_b;
+};
+struct pdg_op {
+    Ctx* ctx = nullptr;
+    SpaceTimeOp op;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+struct pdg_slab {
+    pdg_ops* ops = nullptr;
+    TimeConsts tc;
+    double tau = 0;
+    std::unique_ptr<pdg_block> blk;
+    DBuf<double> d_Q, d_w, d_phi0, shat, ysol, io_a, io_b, rhs_u, rhs_q, rhs_p, djump, et_u;
+};
+
+#define API_BEGIN try {
+#define API_END                                 \
+    }                                           \
+    catch (const pdg::Error& e) {               \
+        g_err = e.what();                       \
+        return e.status;                        \
+    }                                           \
+    catch (const std::bad_alloc& e) {           \
+        g_err = e.what();                       \
+        return PDG_OUT_OF_MEMORY;               \
+    }                                           \
+    catch (const std::exception& e) {           \
+        g_err = e.what();                       \
+        return PDG_INVALID_ARGUMENT;            \
+    }                                           \
+    return PDG_OK;
+
+namespace {
+
+__global__ void k_schur_fwd(int nn, long long nt, const double* Q, const double* w, const double* R, double* shat) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn * nt; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nt);
+        const long long k = t % nt;
+        double s = 0.0;
+        for (int j = 0; j < nn; ++j) s += Q[j * nn + i] * (R[j * nt + k] / w[j]);
+        shat[t] = s;
+    }
+}
+__global__ void k_schur_bwd(int nn, long long nt, const double* Q, const double* y, double* X) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn * nt; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nt);
+        const long long k = t % nt;
+        double s = 0.0;
+        for (int j = 0; j < nn; ++j) s += Q[i * nn + j] * y[j * nt + k];
+        X[t] = s;
+    }
+}
+// djump = (-b) E^T u - (1/M) (m_p p)   (assembly.hpp:409-413)
+__global__ void k_time_derivative(int np, double mb, double im, const int* et_off, const int* et_idx, const double* et_val,
+                                  const double* m_p, const double* u, const double* p, double* out) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = et_off[c]; k < et_off[c + 1]; ++k) s += et_val[k] * u[et_idx[k]];
+        out[c] = mb * s - im * (m_p[c] * p[c]);
+    }
+}
+// R_i = (tau w_i) [u;q;p]_i + phi0_i djump (p rows)   (slab.hpp:76-84)
+__global__ void k_slab_rhs(int nn, int nu, int nq, int np, double tau, const double* w, const double* phi0,
+                           const double* ru, const double* rq, const double* rp, const double* djump, double* R) {
+    const long long nt = (long long)nu + nq + np;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn * nt; t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nt);
+        const long long k = t % nt;
+        const double s = tau * w[i];
+        double v;
+        if (k < nu)
+            v = s * ru[(long long)i * nu + k];
+        else if (k < nu + nq)
+            v = s * rq[(long long)i * nq + (k - nu)];
+        else
+            v = s * rp[(long long)i * np + (k - nu - nq)] + phi0[i] * djump[k - nu - nq];
+        R[t] = v;
+    }
+}
+
+void finish_ops(SpatialOps& s, cudaStream_t st) {
+    csr_transpose(s.E, s.Et, st);
+    csr_transpose(s.B, s.Bt, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pdg_last_error(void) { return g_err.c_str(); }
+const char* pdg_version(void) { return "porodg_b200 0.1 (sm_100a)"; }
+
+int pdg_ctx_create(int device, pdg_ctx** out) {
+    API_BEGIN
+    require(out != nullptr, "pdg_ctx_create: null out");
+    int n = 0;
+    PDG_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "pdg_ctx_create: bad device index");
+    PDG_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<pdg_ctx>();
+    c->c.device = device;
+    PDG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+    *out = c.release();
+    API_END
+}
+
+void pdg_ctx_destroy(pdg_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+}
+
+int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B, const pdg_csr* E,
+                   const double* m_p_diag, const signed char* q_constrained, double biot_b, double inv_m, double k_dr,
+                   pdg_ops** out) {
+    API_BEGIN
+    require(ctx && A && M_q && B && E && m_p_diag && out, "pdg_ops_upload: null argument");
+    require(nx > 0 && ny > 0, "pdg_ops_upload: mesh dimensions must be positive");
+    PDG_CUDA(cudaSetDevice(ctx->c.device));
+    cudaStream_t st = ctx->c.stream;
+    auto o = std::make_unique<pdg_ops>();
+    SpatialOps& s = o->s;
+    s.ctx = &ctx->c;
+    s.nx = nx;
+    s.ny = ny;
+    s.n_u = A->rows;
+    s.n_q = M_q->rows;
+    s.n_p = B->cols;
+    require(A->cols == s.n_u && E->rows == s.n_u && E->cols == s.n_p && B->rows == s.n_q && M_q->cols == s.n_q,
+            "pdg_ops_upload: block dimensions are inconsistent");
+    require(s.n_u == 8 * nx * ny && s.n_p == nx * ny, "pdg_ops_upload: sizes do not match an nx x ny mesh");
+    s.biot_b = biot_b;
+    s.inv_m = inv_m;
+    s.k_dr = k_dr;
+    csr_upload(s.A, *A, st);
+    csr_upload(s.M_q, *M_q, st);
+    csr_upload(s.B, *B, st);
+    csr_upload(s.E, *E, st);
+    s.m_p.upload(m_p_diag, s.n_p, st);
+    s.q_constrained.alloc(s.n_q);
+    if (q_constrained) s.q_constrained.upload(q_constrained, s.n_q, st);
+    finish_ops(s, st);
+    *out = o.release();
+    API_END
+}
+
+int pdg_ops_assemble(pdg_ctx* ctx, const pdg_problem* problem, pdg_ops** out) {
+    API_BEGIN
+    require(ctx && problem && out, "pdg_ops_assemble: null argument");
+    PDG_CUDA(cudaSetDevice(ctx->c.device));
+    cudaStream_t st = ctx->c.stream;
+    auto o = std::make_unique<pdg_ops>();
+    o->s.ctx = &ctx->c;
+    assemble_ops_device(o->s, *problem, st);
+    finish_ops(o->s, st);
+    *out = o.release();
+    API_END
+}
+
+int pdg_ops_sizes(const pdg_ops* ops, long long sizes[7]) {
+    API_BEGIN
+    require(ops && sizes, "pdg_ops_sizes: null argument");
+    const SpatialOps& s = ops->s;
+    sizes[0] = s.n_u;
+    sizes[1] = s.n_q;
+    sizes[2] = s.n_p;
+    sizes[3] = s.A.nnz;
+    sizes[4] = s.M_q.nnz;
+    sizes[5] = s.B.nnz;
+    sizes[6] = s.E.nnz;
+    API_END
+}
+
+int pdg_ops_download(const pdg_ops* ops, int which, int* row_offsets, int* col_indices, double* values) {
+    API_BEGIN
+    require(ops != nullptr, "pdg_ops_download: null ops");
+    const SpatialOps& s = ops->s;
+    const DCsr* m = which == 0 ? &s.A : which == 1 ? &s.M_q : which == 2 ? &s.B : which == 3 ? &s.E : nullptr;
+    require(m != nullptr, "pdg_ops_download: bad block id");
+    cudaStream_t st = s.ctx->stream;
+    PDG_CUDA(cudaMemcpyAsync(row_offsets, m->off.p, sizeof(int) * (m->rows + 1), cudaMemcpyDeviceToHost, st));
+    if (m->nnz) {
+        PDG_CUDA(cudaMemcpyAsync(col_indices, m->idx.p, sizeof(int) * m->nnz, cudaMemcpyDeviceToHost, st));
+        PDG_CUDA(cudaMemcpyAsync(values, m->val.p, sizeof(double) * m->nnz, cudaMemcpyDeviceToHost, st));
+    }
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_ops_rhs(const pdg_ops* ops, double t, double* u, double* q, double* p) {
+    API_BEGIN
+    require(ops && u && q && p, "pdg_ops_rhs: null argument");
+    const SpatialOps& s = ops->s;
+    require(s.has_problem, "pdg_ops_rhs: operators were uploaded without a problem description");
+    cudaStream_t st = s.ctx->stream;
+    DBuf<double> du(s.n_u), dq(s.n_q), dp(s.n_p);
+    assemble_rhs_device(s, t, du.p, dq.p, dp.p, st);
+    PDG_CUDA(cudaMemcpyAsync(u, du.p, sizeof(double) * s.n_u, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(q, dq.p, sizeof(double) * s.n_q, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(p, dp.p, sizeof(double) * s.n_p, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+void pdg_ops_destroy(pdg_ops* ops) { delete ops; }
+
+int pdg_block_create(pdg_ops* ops, int m, const double* theta, double tau, double lambda_pre,
+                     const pdg_gmres_opts* opts, pdg_block** out) {
+    API_BEGIN
+    require(ops && theta && opts && out, "pdg_block_create: null argument");
+    PDG_CUDA(cudaSetDevice(ops->s.ctx->device));
+    if (!ops->a) ops->a = make_a_solver(ops->s, 2, ops->s.ctx->stream);
+    auto b = std::make_unique<pdg_block>();
+    b->b.create(ops->s, m, theta, tau, lambda_pre, *opts, ops->a);
+    const long long n = b->b.rows();
+    b->io_a.alloc(n);
+    b->io_b.alloc(n);
+    *out = b.release();
+    API_END
+}
+
+int pdg_block_rows(const pdg_block* blk, long long* rows, long long* nnz) {
+    API_BEGIN
+    require(blk && rows && nnz, "pdg_block_rows: null argument");
+    *rows = blk->b.op.rows;
+    *nnz = blk->b.op.nnz;
+    API_END
+}
+
+int pdg_block_solve(pdg_block* blk, const double* rhs, double* x, pdg_report* rep) {
+    API_BEGIN
+    require(blk && rhs && x, "pdg_block_solve: null argument");
+    cudaStream_t st = blk->b.ctx->stream;
+    const long long n = blk->b.rows();
+    PDG_CUDA(cudaMemcpyAsync(blk->io_a.p, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    blk->b.solve(blk->io_a.p, blk->io_b.p, rep);
+    PDG_CUDA(cudaMemcpyAsync(x, blk->io_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_block_solve_device(pdg_block* blk, const double* rhs_dev, double* x_dev, pdg_report* rep) {
+    API_BEGIN
+    require(blk && rhs_dev && x_dev, "pdg_block_solve_device: null argument");
+    blk->b.solve(rhs_dev, x_dev, rep);
+    PDG_CUDA(cudaStreamSynchronize(blk->b.ctx->stream));
+    API_END
+}
+
+int pdg_block_apply(pdg_block* blk, int mode, const double* x, double* y) {
+    API_BEGIN
+    require(blk && x && y, "pdg_block_apply: null argument");
+    require(mode == 0, "pdg_block_apply: unknown mode");
+    cudaStream_t st = blk->b.ctx->stream;
+    const long long n = blk->b.rows();
+    PDG_CUDA(cudaMemcpyAsync(blk->io_a.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    blk->b.op.apply(blk->io_a.p, blk->io_b.p, st);
+    PDG_CUDA(cudaMemcpyAsync(y, blk->io_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_block_apply_device(pdg_block* blk, int mode, const double* x_dev, double* y_dev, int repeats, float* ms) {
+    API_BEGIN
+    require(blk && x_dev && y_dev, "pdg_block_apply_device: null argument");
+    require(mode == 0, "pdg_block_apply_device: unknown mode");
+    cudaStream_t st = blk->b.ctx->stream;
+    if (repeats < 1) repeats = 1;
+    PDG_CUDA(cudaEventRecord(blk->b.ev0, st));
+    for (int i = 0; i < repeats; ++i) blk->b.op.apply(x_dev, y_dev, st);
+    PDG_CUDA(cudaEventRecord(blk->b.ev1, st));
+    PDG_CUDA(cudaEventSynchronize(blk->b.ev1));
+    float t = 0.f;
+    PDG_CUDA(cudaEventElapsedTime(&t, blk->b.ev0, blk->b.ev1));
+    if (ms) *ms = t;
+    API_END
+}
+
+int pdg_block_precondition(pdg_block* blk, const double* r, double* z) {
+    API_BEGIN
+    require(blk && r && z, "pdg_block_precondition: null argument");
+    cudaStream_t st = blk->b.ctx->stream;
+    const long long n = blk->b.rows();
+    PDG_CUDA(cudaMemcpyAsync(blk->io_a.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    blk->b.pre.apply(blk->io_a.p, blk->io_b.p, st);
+    PDG_CUDA(cudaMemcpyAsync(z, blk->io_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_block_download_csr(const pdg_block* blk, long long* row_offsets, int* col_indices, double* values) {
+    API_BEGIN
+    require(blk && row_offsets && col_indices && values, "pdg_block_download_csr: null argument");
+    std::vector<long long> off;
+    std::vector<int> idx;
+    std::vector<double> val;
+    blk->b.op.to_csr(off, idx, val, blk->b.ctx->stream);
+    std::memcpy(row_offsets, off.data(), sizeof(long long) * off.size());
+    std::memcpy(col_indices, idx.data(), sizeof(int) * idx.size());
+    std::memcpy(values, val.data(), sizeof(double) * val.size());
+    API_END
+}
+
+void pdg_block_destroy(pdg_block* blk) { delete blk; }
+
+int pdg_op_create(pdg_ops* ops, int m, const double* theta, double tau, pdg_op** out) {
+    API_BEGIN
+    require(ops && theta && out, "pdg_op_create: null argument");
+    require(tau > 0.0, "pdg_op_create: tau must be positive");
+    PDG_CUDA(cudaSetDevice(ops->s.ctx->device));
+    auto o = std::make_unique<pdg_op>();
+    o->ctx = ops->s.ctx;
+    o->op.build(ops->s, m, theta, tau, o->ctx->stream);
+    PDG_CUDA(cudaEventCreate(&o->e0));
+    PDG_CUDA(cudaEventCreate(&o->e1));
+    PDG_CUDA(cudaStreamSynchronize(o->ctx->stream));
+    *out = o.release();
+    API_END
+}
+
+int pdg_op_rows(const pdg_op* op, long long* rows, long long* nnz) {
+    API_BEGIN
+    require(op && rows && nnz, "pdg_op_rows: null argument");
+    *rows = op->op.rows;
+    *nnz = op->op.nnz;
+    API_END
+}
+
+int pdg_op_apply_device(pdg_op* op, const double* x_dev, double* y_dev, int repeats, float* times_ms) {
+    API_BEGIN
+    require(op && x_dev && y_dev, "pdg_op_apply_device: null argument");
+    cudaStream_t st = op->ctx->stream;
+    for (int i = 0; i < std::max(repeats, 1); ++i) {
+        PDG_CUDA(cudaEventRecord(op->e0, st));
+        op->op.apply(x_dev, y_dev, st);
+        PDG_CUDA(cudaEventRecord(op->e1, st));
+        if (times_ms) {
+            PDG_CUDA(cudaEventSynchronize(op->e1));
+            PDG_CUDA(cudaEventElapsedTime(&times_ms[i], op->e0, op->e1));
+        }
+    }
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_op_download_csr(const pdg_op* op, long long* row_offsets, int* col_indices, double* values) {
+    API_BEGIN
+    require(op && row_offsets && col_indices && values, "pdg_op_download_csr: null argument");
+    std::vector<long long> off;
+    std::vector<int> idx;
+    std::vector<double> val;
+    op->op.to_csr(off, idx, val, op->ctx->stream);
+    std::memcpy(row_offsets, off.data(), sizeof(long long) * off.size());
+    std::memcpy(col_indices, idx.data(), sizeof(int) * idx.size());
+    std::memcpy(values, val.data(), sizeof(double) * val.size());
+    API_END
+}
+
+void pdg_op_destroy(pdg_op* op) {
+    if (!op) return;
+    if (op->e0) cudaEventDestroy(op->e0);
+    if (op->e1) cudaEventDestroy(op->e1);
+    delete op;
+}
+
+int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts, pdg_slab** out) {
+    API_BEGIN
+    require(ops && opts && out, "pdg_slab_create: null argument");
+    require(r == 0 || r == 1, "pdg_slab_create: r must be 0 or 1");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
+    auto s = std::make_unique<pdg_slab>();
+    s->ops = ops;
+    s->tc = time_consts(r);
+    s->tau = tau;
+    const int nn = r + 1;
+    pdg_block* b = nullptr;
+    const int rc = pdg_block_create(ops, nn, s->tc.T.data(), tau, s->tc.T[0], opts, &b);
+    if (rc != PDG_OK) return rc;
+    s->blk.reset(b);
+    cudaStream_t st = ops->s.ctx->stream;
+    s->d_Q.upload(s->tc.Q, st);
+    s->d_w.upload(s->tc.weights, st);
+    s->d_phi0.upload(s->tc.phi0, st);
+    const long long nt = ops->s.n_total();
+    s->shat.alloc(nn * nt);
+    s->ysol.alloc(nn * nt);
+    s->io_a.alloc(nn * nt);
+    s->io_b.alloc(nn * nt);
+    *out = s.release();
+    API_END
+}
+
+int pdg_slab_solve_device(pdg_slab* s, const double* rhs_dev, double* out_dev, pdg_report* rep) {
+    API_BEGIN
+    require(s && rhs_dev && out_dev, "pdg_slab_solve: null argument");
+    cudaStream_t st = s->ops->s.ctx->stream;
+    const int nn = s->tc.n;
+    const long long nt = s->ops->s.n_total();
+    { ProfScope prof(PROF_SLAB, st, 8.0 * 3 * nn * nt);
+    k_schur_fwd<<<grid_for(nn * nt, 256), 256, 0, st>>>(nn, nt, s->d_Q.p, s->d_w.p, rhs_dev, s->shat.p); }
+    count_launch();
+    PDG_CHECK_LAUNCH();
+    s->blk->b.solve(s->shat.p, s->ysol.p, rep, 0);
+    { ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * nt);
+    k_schur_bwd<<<grid_for(nn * nt, 256), 256, 0, st>>>(nn, nt, s->d_Q.p, s->ysol.p, out_dev); }
+    count_launch();
+    PDG_CHECK_LAUNCH();
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_slab_solve(pdg_slab* s, const double* rhs, double* out, pdg_report* rep) {
+    API_BEGIN
+    require(s && rhs && out, "pdg_slab_solve: null argument");
+    cudaStream_t st = s->ops->s.ctx->stream;
+    const long long n = s->tc.n * (long long)s->ops->s.n_total();
+    PDG_CUDA(cudaMemcpyAsync(s->io_a.p, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    const int rc = pdg_slab_solve_device(s, s->io_a.p, s->io_b.p, rep);
+    if (rc != PDG_OK) return rc;
+    PDG_CUDA(cudaMemcpyAsync(out, s->io_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_slab_rhs_device(pdg_slab* s, double t0, const double* u_prev_dev, const double* p_prev_dev, double* rhs_dev) {
+    API_BEGIN
+    require(s && u_prev_dev && p_prev_dev && rhs_dev, "pdg_slab_rhs_device: null argument");
+    const SpatialOps& o = s->ops->s;
+    require(o.has_problem, "pdg_slab_rhs_device: operators were uploaded without a problem description");
+    cudaStream_t st = o.ctx->stream;
+    const int nn = s->tc.n;
+    if (!s->rhs_u.n) {
+        s->rhs_u.alloc((size_t)nn * o.n_u);
+        s->rhs_q.alloc((size_t)nn * o.n_q);
+        s->rhs_p.alloc((size_t)nn * o.n_p);
+        s->djump.alloc(o.n_p);
+    }
+    ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * o.n_total());
+    for (int i = 0; i < nn; ++i)
+        assemble_rhs_device(o, t0 + s->tc.nodes[i] * s->tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
+                            s->rhs_p.p + (size_t)i * o.n_p, st);
+    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
+                                                             o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
+    k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, s->tau, s->d_w.p,
+                                                                           s->d_phi0.p, s->rhs_u.p, s->rhs_q.p,
+                                                                           s->rhs_p.p, s->djump.p, rhs_dev);
+    count_launch(2);
+    PDG_CHECK_LAUNCH();
+    API_END
+}
+
+void pdg_slab_destroy(pdg_slab* s) { delete s; }
+
+int pdg_spmv_csr_device(int rows, const long long* off, const int* idx, const double* val, const double* x, double* y) {
+    API_BEGIN
+    spmv_csr_device(rows, off, idx, val, x, y, 0);
+    PDG_CUDA(cudaStreamSynchronize(0));
+    API_END
+}
+
+int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q) {
+    API_BEGIN
+    require(nodes && weights && phi0 && T && Q, "pdg_time_constants: null argument");
+    const TimeConsts tc = time_consts(r);
+    for (int i = 0; i < tc.n; ++i) {
+        nodes[i] = tc.nodes[i];
+        weights[i] = tc.weights[i];
+        phi0[i] = tc.phi0[i];
+    }
+    for (int i = 0; i < tc.n * tc.n; ++i) {
+        T[i] = tc.T[i];
+        Q[i] = tc.Q[i];
+    }
+    API_END
+}
+
+void pdg_util_uniform(unsigned long long seed, long long n, double* out) {
+    std::mt19937_64 g(seed);
+    for (long long i = 0; i < n; ++i) out[i] = -1.0 + 2.0 * (static_cast<double>(g() >> 11) * 0x1.0p-53);
+}
+
+void pdg_util_lognormal(unsigned long long seed, long long n, double sigma, double* out) {
+    std::mt19937_64 g(seed);
+    for (long long i = 0; i < n; ++i) {
+        const double u1 = (static_cast<double>(g() >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = static_cast<double>(g() >> 11) * 0x1.0p-53;
+        out[i] = std::exp(sigma * (std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2)));
+    }
+}
+
+long long pdg_util_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// Canonical assembled space-time operator of one transformed slab block and
+// its order-fixed SpMV (DESIGN.md section "Space-time operator").
+#pragma once
+
+#include "common.cuh"
+
+namespace pdg {
+
+struct SpatialOps;  // defined in ops.cuh
+
+// Cell-blocked sliced layout:
+//  U class : one group per (component i, cell c) = the 8 displacement rows of
+//            the cell, which share one column list (A columns of the cell and
+//            its face neighbours, then their E columns). Values are stored
+//            [group][entry k][row l] (8 doubles per k), so the 8 lanes that
+//            own a group read 64 contiguous bytes per step and share one
+//            column index.
+//  S class : q- and p-rows, SELL-32: slice of 32 consecutive rows,
+//            [slice][entry k][lane], per-entry column index.
+// Every row is summed sequentially in ascending global column order with
+// __dmul_rn/__dadd_rn: bit-identical to SparseMatrix::apply
+// (sparse.hpp:30-40) on the canonical CSR.
+struct SpaceTimeOp {
+    int m = 1;           // time components in the block
+    int nt = 0;          // n_u + n_q + n_p
+    int n_u = 0, n_q = 0, n_p = 0, n_cells = 0;
+    long long rows = 0, nnz = 0;
+    // U class
+    long long u_groups = 0, u_entries = 0;  // entries counted per group (x8 values)
+    DBuf<long long> u_off;                  // u_groups + 1 (entry offset per group)
+    DBuf<int> u_col;                        // u_entries
+    DBuf<double> u_val;                     // 8 * u_entries
+    // S class
+    long long s_rows = 0, s_slices = 0, s_slots = 0;
+    DBuf<long long> s_off;  // s_slices + 1 (slot offset per slice, slots of 32)
+    DBuf<int> s_len;        // s_rows
+    DBuf<int> s_col;        // 32 * s_slots
+    DBuf<double> s_val;     // 32 * s_slots
+
+    void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st);
+    void apply(const double* x, double* y, cudaStream_t st) const;
+    // canonical CSR download (tests / CPU bitwise check)
+    void to_csr(std::vector<long long>& off, std::vector<int>& idx, std::vector<double>& val, cudaStream_t st) const;
+};
+
+void spmv_csr_device(int rows, const long long* off, const int* idx, const double* val, const double* x, double* y,
+                     cudaStream_t st);
+
+}  // namespace pdg

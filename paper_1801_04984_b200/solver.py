@@ -1,0 +1,350 @@
+"""Host-side mirror of the reference's slab-solve interface over the C ABI.
+
+Names and argument meaning follow porodg (paths relative to
+/root/reference/proj/include/porodg/):
+  SpatialOperators       assembly.hpp:38-52   (device-resident here)
+  GmresOptions           gmres.hpp:24-28
+  FixedStressConfig      fixed_stress.hpp:17-22
+  SolveOptions           slab.hpp:123-127     (block_solver is always the GPU gmres_fs path)
+  SolverReport           gmres.hpp:15-20
+  BlockSolver            one SlabSolver diagonal block (slab.hpp:154-171, :220-234)
+  SlabSolver             slab.hpp:133-274 (r <= 1)
+  march                  march.hpp:45-79,109-117 (monolithic-spectral branch)
+Errors: SolverError for non-convergence (slab.hpp:228-230, same message text),
+InvalidArgument for the reference's std::invalid_argument cases.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import InvalidArgument, SolverError, check, lib  # noqa: F401
+
+_ctx_cache = {}
+
+
+def context(device: int = 0):
+    """One library context (device + stream) per device."""
+    if device not in _ctx_cache:
+        h = C.c_void_p()
+        check(lib().pdg_ctx_create(device, C.byref(h)))
+        _ctx_cache[device] = h
+    return _ctx_cache[device]
+
+
+def _dp(a):
+    return a.ctypes.data_as(_lib.DP)
+
+
+def _ip(a):
+    return a.ctypes.data_as(_lib.IP)
+
+
+@dataclass
+class GmresOptions:
+    tol: float = 1e-10
+    restart: int = 100
+    max_iter: int = 400
+
+
+@dataclass
+class FixedStressConfig:
+    stab: float = -1.0  # < 0: b^2 / K_dr
+    truncation_sweeps: int = 1
+
+
+@dataclass
+class SolveOptions:
+    gmres: GmresOptions = field(default_factory=GmresOptions)
+    fs: FixedStressConfig = field(default_factory=FixedStressConfig)
+    # "reference": candidate x + P(V y) (gmres.hpp:116); "flexible": x + Z y (gmres_flexible)
+    candidate: str = "reference"
+
+    def to_struct(self):
+        o = _lib.GmresOpts()
+        o.tol, o.restart, o.max_iter = self.gmres.tol, self.gmres.restart, self.gmres.max_iter
+        o.sweeps, o.stab = self.fs.truncation_sweeps, self.fs.stab
+        o.candidate = {"reference": 0, "flexible": 1}[self.candidate]
+        return o
+
+
+@dataclass
+class SolverReport:
+    converged: bool
+    iterations: int
+    final_relative_residual: float
+    residual_history: np.ndarray
+    device_ms: float
+    kernel_launches: int
+
+
+def _report(cap):
+    rep = _lib.Report()
+    hist = np.zeros(cap, dtype=np.float64)
+    rep.history = _dp(hist)
+    rep.history_cap = cap
+    return rep, hist
+
+
+def _to_report(rep, hist):
+    return SolverReport(bool(rep.converged), rep.iterations, rep.final_rel_res, hist[:rep.history_len].copy(),
+                        rep.device_ms, rep.kernel_launches)
+
+
+def _csr_struct(off, idx, val, rows, cols):
+    off = np.ascontiguousarray(off, np.int32)
+    idx = np.ascontiguousarray(idx, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    s = _lib.CSR(rows, cols, len(val), _ip(off), _ip(idx), _dp(val))
+    return s, (off, idx, val)
+
+
+def time_constants(r: int):
+    """dG(r) constants (nodes, weights, phi(0), Schur T and Q) as the library computes them."""
+    n = r + 1
+    nodes, w, phi = np.empty(n), np.empty(n), np.empty(n)
+    T, Q = np.empty((n, n)), np.empty((n, n))
+    check(lib().pdg_time_constants(r, _dp(nodes), _dp(w), _dp(phi), _dp(T), _dp(Q)))
+    return dict(nodes=nodes, weights=w, phi_at0=phi, T=T, Q=Q)
+
+
+class SpaceTimeOperator:
+    """The canonical assembled space-time operator alone (pdg_op_*): the object
+    of the SpMV bandwidth sweep (BASELINE config 3)."""
+
+    def __init__(self, ops, theta, tau):
+        self.theta = np.ascontiguousarray(np.atleast_2d(theta), np.float64)
+        h = C.c_void_p()
+        check(lib().pdg_op_create(ops._h, self.theta.shape[0], _dp(self.theta), tau, C.byref(h)))
+        self._h = h
+        rows, nnz = C.c_longlong(), C.c_longlong()
+        check(lib().pdg_op_rows(self._h, C.byref(rows), C.byref(nnz)))
+        self.rows, self.nnz = rows.value, nnz.value
+
+    def apply_device(self, x_ptr: int, y_ptr: int, repeats: int = 1, times: bool = False):
+        buf = (C.c_float * max(repeats, 1))() if times else None
+        check(lib().pdg_op_apply_device(self._h, x_ptr, y_ptr, repeats, buf))
+        return [buf[i] for i in range(repeats)] if times else None
+
+    def csr(self):
+        off = np.empty(self.rows + 1, np.int64)
+        idx = np.empty(self.nnz, np.int32)
+        val = np.empty(self.nnz, np.float64)
+        check(lib().pdg_op_download_csr(self._h, off.ctypes.data_as(_lib.LLP), _ip(idx), _dp(val)))
+        return off, idx, val
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pdg_op_destroy(self._h)
+            self._h = None
+
+
+def profile(enable: bool | None = None, reset: bool = False):
+    """Per-phase device timing (pdg_profile_*). Returns {phase: (ms, calls, alg_bytes)}."""
+    L = lib()
+    if reset:
+        L.pdg_profile_reset()
+    if enable is not None:
+        L.pdg_profile_enable(1 if enable else 0)
+    out = {}
+    for i, nm in enumerate(PROFILE_PHASES):
+        ms, calls, by = C.c_double(), C.c_longlong(), C.c_double()
+        L.pdg_profile_read(i, C.byref(ms), C.byref(calls), C.byref(by))
+        out[nm] = (ms.value, calls.value, by.value)
+    return out
+
+
+PROFILE_PHASES = ("spmv", "a_solve", "flow_solve", "precond_other", "krylov", "slab_transforms")
+
+
+class SpatialOperators:
+    """Device-resident A, M_q, B, E, m_p (SpatialOperators, assembly.hpp:38-52)."""
+
+    def __init__(self, handle, nx, ny):
+        self._h = handle
+        self.nx, self.ny = nx, ny
+        sz = (C.c_longlong * 7)()
+        check(lib().pdg_ops_sizes(self._h, sz))
+        self.n_u, self.n_q, self.n_p = sz[0], sz[1], sz[2]
+        self.nnz = dict(A=sz[3], M_q=sz[4], B=sz[5], E=sz[6])
+        self.n_total = self.n_u + self.n_q + self.n_p
+
+    @classmethod
+    def assemble(cls, spec, device: int = 0):
+        """assemble_operators (assembly.hpp:177-395) on the device."""
+        p, keep = spec.to_struct()
+        h = C.c_void_p()
+        check(lib().pdg_ops_assemble(context(device), C.byref(p), C.byref(h)))
+        del keep
+        return cls(h, spec.nx, spec.ny)
+
+    @classmethod
+    def upload(cls, nx, ny, blocks, m_p_diag, q_constrained, biot_b, inv_m, k_dr, device: int = 0):
+        """Upload host CSR blocks {'A','M_q','B','E': (off, idx, val)}."""
+        n_u, n_p = 8 * nx * ny, nx * ny
+        n_q = nx * (ny + 1) + (nx + 1) * ny
+        dims = dict(A=(n_u, n_u), M_q=(n_q, n_q), B=(n_q, n_p), E=(n_u, n_p))
+        structs, keep = {}, []
+        for k, (r, c) in dims.items():
+            structs[k], arrs = _csr_struct(*blocks[k], r, c)
+            keep.append(arrs)
+        mp = np.ascontiguousarray(m_p_diag, np.float64)
+        qc = np.ascontiguousarray(q_constrained, np.int8)
+        h = C.c_void_p()
+        check(lib().pdg_ops_upload(context(device), nx, ny, C.byref(structs["A"]), C.byref(structs["M_q"]),
+                                   C.byref(structs["B"]), C.byref(structs["E"]), _dp(mp),
+                                   qc.ctypes.data_as(C.POINTER(C.c_byte)), biot_b, inv_m, k_dr, C.byref(h)))
+        return cls(h, nx, ny)
+
+    def download(self, name):
+        rows = dict(A=self.n_u, M_q=self.n_q, B=self.n_q, E=self.n_u)[name]
+        nnz = self.nnz[name]
+        off, idx, val = np.empty(rows + 1, np.int32), np.empty(nnz, np.int32), np.empty(nnz, np.float64)
+        check(lib().pdg_ops_download(self._h, ("A", "M_q", "B", "E").index(name), _ip(off), _ip(idx), _dp(val)))
+        return off, idx, val
+
+    def rhs(self, t):
+        """assemble_rhs at time t (constant boundary data)."""
+        u, q, p = np.empty(self.n_u), np.empty(self.n_q), np.empty(self.n_p)
+        check(lib().pdg_ops_rhs(self._h, t, _dp(u), _dp(q), _dp(p)))
+        return u, q, p
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pdg_ops_destroy(self._h)
+            self._h = None
+
+
+class BlockSolver:
+    """One transformed diagonal block (Theta = T_gg, kappa = 1, preconditioner
+    lambda = T_gg(0,0)) solved by right-preconditioned GMRES on the GPU."""
+
+    def __init__(self, ops: SpatialOperators, theta, tau, lambda_pre=None, opt: SolveOptions | None = None):
+        self.ops = ops
+        self.theta = np.ascontiguousarray(np.atleast_2d(theta), np.float64)
+        self.m = self.theta.shape[0]
+        self.tau = tau
+        self.opt = opt or SolveOptions()
+        lam = self.theta[0, 0] if lambda_pre is None else lambda_pre
+        h = C.c_void_p()
+        o = self.opt.to_struct()
+        check(lib().pdg_block_create(ops._h, self.m, _dp(self.theta), tau, lam, C.byref(o), C.byref(h)))
+        self._h = h
+        rows, nnz = C.c_longlong(), C.c_longlong()
+        check(lib().pdg_block_rows(self._h, C.byref(rows), C.byref(nnz)))
+        self.rows, self.nnz = rows.value, nnz.value
+
+    def solve(self, rhs):
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        assert rhs.size == self.rows
+        x = np.empty_like(rhs)
+        rep, hist = _report(self.opt.gmres.max_iter + 2)
+        check(lib().pdg_block_solve(self._h, _dp(rhs), _dp(x), C.byref(rep)))
+        return x, _to_report(rep, hist)
+
+    def solve_device(self, rhs_ptr: int, x_ptr: int):
+        rep, hist = _report(self.opt.gmres.max_iter + 2)
+        check(lib().pdg_block_solve_device(self._h, rhs_ptr, x_ptr, C.byref(rep)))
+        return _to_report(rep, hist)
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        check(lib().pdg_block_apply(self._h, 0, _dp(x), _dp(y)))
+        return y
+
+    def apply_device(self, x_ptr: int, y_ptr: int, repeats: int = 1) -> float:
+        ms = C.c_float()
+        check(lib().pdg_block_apply_device(self._h, 0, x_ptr, y_ptr, repeats, C.byref(ms)))
+        return ms.value
+
+    def precondition(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        check(lib().pdg_block_precondition(self._h, _dp(r), _dp(z)))
+        return z
+
+    def csr(self):
+        off = np.empty(self.rows + 1, np.int64)
+        idx = np.empty(self.nnz, np.int32)
+        val = np.empty(self.nnz, np.float64)
+        check(lib().pdg_block_download_csr(self._h, off.ctypes.data_as(_lib.LLP), _ip(idx), _dp(val)))
+        return off, idx, val
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pdg_block_destroy(self._h)
+            self._h = None
+
+
+class SlabSolver:
+    """SlabSolver (slab.hpp:133-274) for dG(r), r in {0, 1}: Schur transform,
+    GMRES block solve and back-transform on the device."""
+
+    def __init__(self, ops: SpatialOperators, r: int, tau: float, opt: SolveOptions | None = None):
+        self.ops, self.r, self.tau = ops, r, tau
+        self.opt = opt or SolveOptions()
+        h = C.c_void_p()
+        o = self.opt.to_struct()
+        check(lib().pdg_slab_create(ops._h, r, tau, C.byref(o), C.byref(h)))
+        self._h = h
+        self.n = (r + 1) * ops.n_total
+
+    def solve(self, rhs):
+        """rhs: (r+1) * n_total stacked SlabSystem::rhs -> (r+1) * n_total state."""
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        assert rhs.size == self.n
+        out = np.empty_like(rhs)
+        rep, hist = _report(self.opt.gmres.max_iter + 2)
+        check(lib().pdg_slab_solve(self._h, _dp(rhs), _dp(out), C.byref(rep)))
+        return out, _to_report(rep, hist)
+
+    def solve_device(self, rhs_ptr: int, out_ptr: int):
+        rep, hist = _report(self.opt.gmres.max_iter + 2)
+        check(lib().pdg_slab_solve_device(self._h, rhs_ptr, out_ptr, C.byref(rep)))
+        return _to_report(rep, hist)
+
+    def rhs_device(self, t0: float, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int):
+        check(lib().pdg_slab_rhs_device(self._h, t0, u_prev_ptr, p_prev_ptr, rhs_ptr))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pdg_slab_destroy(self._h)
+            self._h = None
+
+
+def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptions | None = None,
+          keep_states: bool = False):
+    """Monolithic-spectral march (march.hpp:45-79,109-117) with a device-resident
+    slab loop: the slab right-hand side, the Schur transforms and the jump data
+    never leave the GPU. Returns per-slab reports (and states if asked)."""
+    import torch
+
+    opt = opt or SolveOptions()
+    tau = T / n_slabs
+    slab = SlabSolver(ops, r, tau, opt)
+    nt = ops.n_total
+    dev = torch.device("cuda")
+    u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
+    p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
+    rhs = torch.empty((r + 1) * nt, dtype=torch.float64, device=dev)
+    out = torch.empty_like(rhs)
+    reports, states = [], []
+    for n in range(n_slabs):
+        t0 = T * n / n_slabs
+        torch.cuda.synchronize()
+        slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+        try:
+            rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+        except SolverError as e:
+            raise SolverError(e.status, f"slab {n} (t_n = {T * (n + 1) / n_slabs:f}): {e}") from None
+        reports.append(rep)
+        end = out[r * nt:(r + 1) * nt]
+        u_prev.copy_(end[:ops.n_u])
+        p_prev.copy_(end[ops.n_u + ops.n_q:])
+        if keep_states:
+            states.append(out.cpu().numpy().copy())
+    return reports, states

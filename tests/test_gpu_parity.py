@@ -1,0 +1,221 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+on the same seeded inputs. Bars: bit-exact for the assembled operators and the
+order-fixed SpMV; GMRES iterations within +-1 and per-slab relative L2
+difference <= 1e-9 for the solves (BASELINE.json north_star)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1801_04984_b200 import problem as P
+from paper_1801_04984_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SOLVE_RTOL = 1e-9  # per-slab relative L2 (north_star)
+
+
+def _bc_variants():
+    """Boundary combinations covering every Nitsche / flux branch of the assembly."""
+    out = []
+    a = P.config0()
+    a.nx, a.ny = 5, 3
+    out.append(a)
+    b = P.terzaghi_recorded()
+    out.append(b)
+    c = P.config1(6)
+    c.disp = {"left": ("fixed", (0.0, 0.0)), "right": ("roller_x", (0.0, 0.3)),
+              "bottom": ("roller_y", (0.2, 0.0)), "top": ("traction", (0.1, -1.0))}
+    c.flow = {"left": ("pressure", 0.5), "right": ("no_flow", 0.0), "bottom": ("no_flow", 0.0),
+              "top": ("pressure", -0.25)}
+    c.lx, c.ly = 1.3, 0.9
+    out.append(c)
+    d = P.config0()
+    d.nx, d.ny = 7, 4
+    d.disp = {t: ("fixed", (0.0, 0.0)) for t in P.TAGS}
+    d.flow = {t: ("pressure", 0.0) for t in P.TAGS}
+    out.append(d)
+    out.append(P.config1(32))
+    return out
+
+
+@pytest.mark.parametrize("spec", _bc_variants(), ids=lambda s: f"{s.nx}x{s.ny}")
+def test_device_assembly_bit_identical(oracle, spec):
+    """pdg_ops_assemble (one thread block per cell) == assemble_operators +
+    csr_from_triplets (assembly.hpp:177-395, sparse.hpp:83-110), bit for bit."""
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    for name in ("A", "M_q", "B", "E"):
+        ro, ri, rv = rp.csr(name)
+        go, gi, gv = ops.download(name)
+        assert np.array_equal(ro, go), name
+        assert np.array_equal(ri, gi), name
+        assert np.array_equal(rv, gv), name  # exact (== treats +0/-0 alike)
+    u, q, p = rp.assemble_rhs(0.3)
+    gu, gq, gp = ops.rhs(0.3)
+    assert np.array_equal(u, gu) and np.array_equal(q, gq) and np.array_equal(p, gp)
+
+
+def _upload_from_oracle(rp, spec):
+    m = rp.misc()
+    blocks = {k: rp.csr(k) for k in ("A", "M_q", "B", "E")}
+    return S.SpatialOperators.upload(spec.nx, spec.ny, blocks, m["m_p_diag"], m["q_constrained"], m["biot_b"],
+                                     m["inv_m"], m["k_dr"])
+
+
+@pytest.mark.parametrize("n,r", [(16, 0), (16, 1), (64, 1)])
+def test_spacetime_operator_and_spmv_bit_identical(oracle, n, r):
+    """Canonical space-time CSR and order-fixed SpMV == SparseMatrix::apply on
+    the oracle's canonical CSR (sparse.hpp:30-40), bit for bit."""
+    spec = P.config1(n)
+    rp = oracle.RefProblem(spec.to_dict())
+    T = oracle.time_constants(r)["T"]
+    tau = 0.1 if r == 0 else 0.05
+    ops = S.SpatialOperators.assemble(spec)
+    blk = S.BlockSolver(ops, T, tau, opt=S.SolveOptions(gmres=S.GmresOptions(restart=10)))
+    ro, ri, rv = rp.spacetime_csr(T, tau)
+    go, gi, gv = blk.csr()
+    assert np.array_equal(ro.astype(np.int64), go)
+    assert np.array_equal(ri, gi)
+    assert np.array_equal(rv, gv)
+    x = P.uniform_vector(P.X_SEED, blk.rows)
+    assert np.array_equal(blk.apply(x), oracle.csr_apply(ro, ri, rv, x))
+
+
+def test_spmv_edge_inputs(oracle):
+    """Zero, signed-zero and single-cell inputs: 1x1 mesh, x = 0 -> y = 0 exactly."""
+    spec = P.config0()
+    spec.nx = spec.ny = 1
+    rp = oracle.RefProblem(spec.to_dict())
+    T = oracle.time_constants(1)["T"]
+    ops = S.SpatialOperators.assemble(spec)
+    blk = S.BlockSolver(ops, T, 0.05)
+    ro, ri, rv = rp.spacetime_csr(T, 0.05)
+    for x in (np.zeros(blk.rows), -np.zeros(blk.rows), P.uniform_vector(7, blk.rows)):
+        assert np.array_equal(blk.apply(x), oracle.csr_apply(ro, ri, rv, x))
+
+
+@pytest.mark.parametrize("n,lam", [(16, 1.0), (16, 2.0), (32, 1.7)])
+def test_preconditioner_matches_oracle(oracle, n, lam):
+    """One truncated fixed-stress sweep with exact inner solves
+    (fixed_stress.hpp:109-139,177-181): GPU block-tridiagonal Cholesky vs the
+    oracle's dense LU / banded Cholesky, and bit-identical repeats."""
+    spec = P.config1(n)
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    tau = 0.05
+    blk = S.BlockSolver(ops, np.array([[lam]]), tau)
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(blk.rows)
+    z = blk.precondition(r)
+    z_ref = rp.precondition(lam, tau, r, backend=0)
+    z_band = rp.precondition(lam, tau, r, backend=1)
+    # two exact CPU solvers already differ by kappa * eps; the GPU solve must sit in that band
+    band = np.linalg.norm(z_band - z_ref) / np.linalg.norm(z_ref)
+    assert np.linalg.norm(z - z_ref) <= max(1e-10, 10 * band) * np.linalg.norm(z_ref)
+    assert np.array_equal(z, blk.precondition(r))
+    # linearity (test_coupling.cpp:308-335)
+    r2 = rng.standard_normal(blk.rows)
+    z2 = blk.precondition(r2)
+    zc = blk.precondition(0.3 * r - 1.7 * r2)
+    assert np.max(np.abs(zc - (0.3 * z - 1.7 * z2))) <= 1e-12 * np.max(np.abs(zc))
+
+
+@pytest.mark.parametrize("candidate", ["reference", "flexible"])
+def test_march_config0_parity(oracle, candidate):
+    """BASELINE config 0 (16^2, dG(0), 10 slabs): iterations +-1, per-slab rel L2 <= 1e-9."""
+    g = np.load(os.path.join(GOLDEN, "config0_oracle.npz"))
+    spec = P.config0()
+    run = P.RUNS["config0"]
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]), candidate=candidate)
+    reps, states = S.march(ops, run["r"], run["T"], run["n_slabs"], opt, keep_states=True)
+    for s, rep in enumerate(reps):
+        assert rep.converged
+        assert abs(rep.iterations - int(g["iterations"][s])) <= 1
+        ref = g["states"][s].ravel()
+        assert np.linalg.norm(states[s] - ref) <= SOLVE_RTOL * np.linalg.norm(ref)
+
+
+def test_march_terzaghi_reproduces_reference_log():
+    """The reference's recorded iteration log (proj/out/iterations.csv) on the GPU:
+    identical iteration counts; final residuals to the log's precision band."""
+    ref = json.load(open(os.path.join(GOLDEN, "reference_iterations.json")))
+    g = np.load(os.path.join(GOLDEN, "terzaghi_oracle.npz"))
+    spec = P.terzaghi_recorded()
+    run = P.RUNS["terzaghi_recorded"]
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]))
+    reps, states = S.march(ops, run["r"], run["T"], run["n_slabs"], opt, keep_states=True)
+    assert [r.iterations for r in reps] == ref["gmres_iterations"]
+    np.testing.assert_allclose([r.final_relative_residual for r in reps], ref["final_residual"], rtol=1e-3)
+    for s in range(len(reps)):
+        refs = g["states"][s].ravel()
+        assert np.linalg.norm(states[s] - refs) <= SOLVE_RTOL * np.linalg.norm(refs)
+
+
+def test_block_solve_upload_path_matches_oracle(oracle):
+    """pdg_ops_upload (reference-assembled CSR) + pdg_block_solve == oracle block solve."""
+    spec = P.config1(24)
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = _upload_from_oracle(rp, spec)
+    t = oracle.time_constants(1)
+    tau = 0.05
+    u_prev = np.zeros(rp.n_u)
+    p_prev = np.zeros(rp.n_p)
+    R = rp.slab_rhs(1, 0.0, tau, u_prev, p_prev)
+    shat = rp.schur_forward(1, R)
+    x_ref, rep_ref = rp.block_solve(1, tau, shat, tol=1e-10, restart=50, backend=0)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50))
+    blk = S.BlockSolver(ops, t["T"], tau, opt=opt)
+    x, rep = blk.solve(shat)
+    assert rep.converged and abs(rep.iterations - rep_ref["iterations"]) <= 1
+    assert np.linalg.norm(x - x_ref) <= SOLVE_RTOL * np.linalg.norm(x_ref)
+    assert len(rep.residual_history) == rep.iterations + 1
+
+
+def test_nonconvergence_raises_solver_error():
+    """max_iter too small -> SolverError with the reference's message (slab.hpp:228-230)."""
+    spec = P.config1(16)
+    ops = S.SpatialOperators.assemble(spec)
+    T = np.array([[1.0]])
+    blk = S.BlockSolver(ops, T, 0.1, opt=S.SolveOptions(gmres=S.GmresOptions(tol=1e-14, restart=1, max_iter=1)))
+    rhs = P.uniform_vector(5, blk.rows)
+    with pytest.raises(S.SolverError, match=r"slab block 0: GMRES did not converge \(rel res"):
+        blk.solve(rhs)
+
+
+def test_zero_rhs_and_invalid_args():
+    spec = P.config0()
+    ops = S.SpatialOperators.assemble(spec)
+    blk = S.BlockSolver(ops, np.array([[1.0]]), 0.1)
+    x, rep = blk.solve(np.zeros(blk.rows))
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    with pytest.raises(S.InvalidArgument):
+        S.BlockSolver(ops, np.array([[1.0]]), -0.1)
+    with pytest.raises(S.InvalidArgument):
+        S.BlockSolver(ops, np.array([[1.0]]), 0.1, opt=S.SolveOptions(gmres=S.GmresOptions(tol=2.0)))
+    bad = P.config0()
+    bad.penalty = -1.0
+    with pytest.raises(S.InvalidArgument):
+        S.SpatialOperators.assemble(bad)
+
+
+@pytest.mark.parametrize("slabs", [3])
+def test_march_config1_parity(oracle, slabs):
+    """BASELINE config 1 (128^2, dG(1), lognormal K): first slabs vs the oracle
+    with exact sparse-direct inner solves."""
+    spec = P.config1(128)
+    run = P.RUNS["config1"]
+    rp = oracle.RefProblem(spec.to_dict())
+    ref = rp.march(run["r"], run["T"], run["n_slabs"], tol=run["tol"], restart=run["restart"], backend=1,
+                   keep_states=True, max_slabs=slabs)
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]))
+    # march only `slabs` slabs of the 20-slab partition
+    reps, states = S.march(ops, run["r"], run["T"] * slabs / run["n_slabs"], slabs, opt, keep_states=True)
+    for s in range(slabs):
+        assert abs(reps[s].iterations - int(ref["iterations"][s])) <= 1
+        rs = ref["states"][s].ravel()
+        assert np.linalg.norm(states[s] - rs) <= SOLVE_RTOL * np.linalg.norm(rs)

@@ -1,0 +1,116 @@
+"""CPU tests of the oracle (test infrastructure) against the reference's own
+known-answer tests and recorded output. No GPU."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1801_04984_b200 import problem as P
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_oracle_kats_pass(oracle):
+    """Every reference KAT restated in oracle/refcpu/kat_main.cpp passes
+    (test_linsolve.cpp, test_time_dg.cpp, test_coupling.cpp, acceptance.cpp
+    criteria 1 and 8, proj/out/iterations.csv)."""
+    exe = os.path.join(os.path.dirname(oracle.__file__), "_build", "refcpu_kat")
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "[FAIL]" not in out.stdout
+    assert out.stdout.count("[PASS]") >= 30
+
+
+def test_oracle_reproduces_reference_iteration_log(oracle):
+    """proj/out/iterations.csv: 7 GMRES iterations per slab and the logged
+    final relative residuals (printed with 7 significant digits)."""
+    ref = json.load(open(os.path.join(GOLDEN, "reference_iterations.json")))
+    spec = P.terzaghi_recorded()
+    run = P.RUNS["terzaghi_recorded"]
+    rp = oracle.RefProblem(spec.to_dict())
+    res = rp.march(run["r"], run["T"], run["n_slabs"], tol=run["tol"], restart=run["restart"], backend=0)
+    assert list(res["iterations"]) == ref["gmres_iterations"]
+    np.testing.assert_allclose(res["final_res"], ref["final_residual"], rtol=5e-5)
+
+
+def test_operator_sizes_match_closed_forms(oracle):
+    """SURVEY.md Appendix B closed forms (nnz includes stored zeros)."""
+    for n in (4, 16):
+        spec = P.config0()
+        spec.nx = spec.ny = n
+        rp = oracle.RefProblem(spec.to_dict())
+        N, F_int = n * n, 2 * n * (n - 1)
+        assert (rp.n_u, rp.n_q, rp.n_p) == (8 * N, 2 * n * (n + 1), N)
+        assert rp.nnz["A"] == 64 * N + 128 * F_int
+        assert rp.nnz["E"] == 8 * N + 16 * F_int
+        assert rp.nnz["B"] == 2 * F_int + n
+        assert rp.nnz["M_q"] == 2 * n * (n + 1) + 2 * ((n - 2) * n + n * (n - 1))
+        t = oracle.time_constants(0)
+        off, idx, val = rp.spacetime_csr(t["T"], 0.1)
+        dg0 = rp.nnz["A"] + 2 * rp.nnz["E"] + rp.nnz["M_q"] + 2 * rp.nnz["B"] + N
+        assert len(val) == dg0
+        t1 = oracle.time_constants(1)
+        off, idx, val = rp.spacetime_csr(t1["T"], 0.05)
+        assert len(val) == 2 * dg0 + 2 * (rp.nnz["E"] + N)
+    # config 0 canonical operator: 100,960 nnz
+    rp = oracle.RefProblem(P.config0().to_dict())
+    assert len(rp.spacetime_csr(oracle.time_constants(0)["T"], 0.1)[2]) == 100960
+
+
+def test_spacetime_csr_is_the_reference_block_operator(oracle):
+    """The canonical assembled operator applied to x equals the reference's
+    matrix-free apply_block_operator (fixed_stress.hpp:38-60) to roundoff."""
+    spec = P.config0()
+    spec.nx = spec.ny = 6
+    rp = oracle.RefProblem(spec.to_dict())
+    rng = np.random.default_rng(3)
+    for r, tau in ((0, 0.1), (1, 0.05)):
+        T = oracle.time_constants(r)["T"]
+        off, idx, val = rp.spacetime_csr(T, tau)
+        x = rng.standard_normal((r + 1) * rp.n_total)
+        y_csr = oracle.csr_apply(off, idx, val, x)
+        y_mf = rp.apply_block(T, tau, x)
+        assert np.max(np.abs(y_csr - y_mf)) <= 1e-12 * np.max(np.abs(y_mf))
+
+
+def test_banded_backend_matches_dense(oracle):
+    """Exact sparse-direct inner solves (the config-1 oracle backend) give the
+    dense-LU reference's iteration counts and solutions to 1e-10 (the two exact
+    solvers differ in roundoff, amplified by the conditioning at GMRES tol 1e-10)."""
+    for n, r in ((8, 0), (8, 1)):
+        spec = P.config1(n)
+        rp = oracle.RefProblem(spec.to_dict())
+        a = rp.march(r, 1.0, 4, restart=50, tol=1e-10, backend=0, keep_states=True)
+        b = rp.march(r, 1.0, 4, restart=50, tol=1e-10, backend=1, keep_states=True)
+        assert np.array_equal(a["iterations"], b["iterations"])
+        for s in range(4):
+            d = np.linalg.norm(a["states"][s] - b["states"][s]) / np.linalg.norm(a["states"][s])
+            assert d <= 1e-10
+
+
+def test_config0_golden(oracle):
+    g = np.load(os.path.join(GOLDEN, "config0_oracle.npz"))
+    rp = oracle.RefProblem(P.config0().to_dict())
+    run = P.RUNS["config0"]
+    res = rp.march(run["r"], run["T"], run["n_slabs"], tol=run["tol"], restart=run["restart"], backend=0,
+                   keep_states=True)
+    assert np.array_equal(res["iterations"], g["iterations"])
+    assert np.array_equal(res["states"], g["states"])
+
+
+def test_seeded_generators_match_fixture(oracle):
+    k = oracle.lognormal(P.K_SEED, 128 * 128, 1.0)
+    assert np.array_equal(k, np.load(os.path.join(GOLDEN, "config1_k_perm.npy")))
+    x = oracle.uniform(P.X_SEED, 1000)
+    assert x.min() >= -1.0 and x.max() < 1.0
+
+
+def test_time_constants_closed_forms(oracle):
+    t = oracle.time_constants(1)
+    np.testing.assert_allclose(t["nodes"], [1 / 3, 1.0], atol=1e-14)
+    np.testing.assert_allclose(t["weights"], [0.75, 0.25], atol=1e-14)
+    np.testing.assert_allclose(t["G_hat"], [[9 / 8, 3 / 8], [-9 / 8, 5 / 8]], atol=1e-13)
+    T = t["T"]
+    assert abs(T[0, 0] - T[1, 1]) < 1e-12 and abs(T[0, 1] * T[1, 0] + 2.0) < 1e-12
