@@ -153,6 +153,13 @@ void pdg_profile_enable(int on);
 void pdg_profile_reset(void);
 int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes);
 
+/* Diagnostics: run one preconditioner application of `blk` with per-step
+ * %globaltimer stamps in the last recurrence of solver `which` (0 displacement,
+ * 1 flow); out[(cta * nsteps + step) * 3 + phase] (ns), phases: step start,
+ * sources gathered, rows stored. *ctas / *nsteps receive the shape. */
+int pdg_debug_recurrence_timing(pdg_block* blk, int which, unsigned long long* out, long long cap, int* ctas,
+                                int* nsteps);
+
 /* Slab solver for dG(r), r <= 1 (SlabSolver, slab.hpp:133-274). */
 int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts, pdg_slab** out);
 /* rhs: (r+1) * n_total stacked per Radau node (SlabSystem::rhs); out: (r+1) * n_total solution comps. */

@@ -97,6 +97,7 @@ _SIGS = {
     "pdg_profile_reset": (None, []),
     "pdg_profile_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), LLP, C.POINTER(C.c_double)]),
     "pdg_time_constants": (C.c_int, [C.c_int, DP, DP, DP, DP, DP]),
+    "pdg_debug_recurrence_timing": (C.c_int, [VP, C.c_int, C.POINTER(C.c_ulonglong), C.c_longlong, IP, IP]),
     "pdg_util_uniform": (None, [C.c_ulonglong, C.c_longlong, DP]),
     "pdg_util_lognormal": (None, [C.c_ulonglong, C.c_longlong, C.c_double, DP]),
     "pdg_util_launch_count": (C.c_longlong, []),

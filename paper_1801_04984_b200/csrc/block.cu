@@ -319,7 +319,7 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     PDG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     PDG_CUDA(cudaStreamSynchronize(st));
     require(herr == 0, "fixed-stress: flow Schur complement is not block tridiagonal in face-row order");
-    flow.factor_dense(dense.p, dense.p, st);
+    flow.factor_dense(dense.p, st);
     rq.alloc((size_t)m * o.n_q);
     fp.alloc((size_t)m * o.n_p);
     mech.alloc((size_t)m * o.n_u);

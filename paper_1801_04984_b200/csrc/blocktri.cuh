@@ -12,63 +12,74 @@
 
 namespace pdg {
 
-// A = L L^T with L block lower bidiagonal: diag L_j, subdiag K_j = L_{j+1,j}.
-// Stored for the solve:
-//   Linv_j = L_j^{-1}                      (col-major, lower)      -- c_j = Linv_j b_j,  e_j = Linv_j^T y_j
-//   M_j    = Linv_j K_{j-1}  (row-major)   -- forward  y_j = c_j - M_j y_{j-1}
-//   N_j    = Linv_j^T K_j^T  (row-major)   -- backward x_j = e_j - N_j x_{j+1}
-// The two recurrences run in one persistent cooperative kernel each.
+// One task of a recurrence step for one chain: rows of block `tgt` are
+// out_tgt = in_tgt - F1 out_src1 - F2 out_src2 (missing sources skipped; a
+// task without sources copies in_tgt). F are row-major (ld padded).
+struct RecTask {
+    int tgt, src1, src2, ld1, ld2;
+    long long off1, off2;
+};
+
+// Twisted ("burn at both ends") block Cholesky A = P P^T with twist block t:
+// blocks 0..t-1 are eliminated from the top (L_j, K_j = L_{j+1,j}), blocks
+// nb-1..t+1 from the bottom (L'_j, K'_j = L_{j-1,j}), and
+// L_t L_t^T = A_tt - K_{t-1} K_{t-1}^T - K'_{t+1} K'_{t+1}^T.
+// Stored for the solve (all row-major, 256-byte aligned, rows padded to 16 B):
+//   Linv_j (col-major and row-major copies)   c = Linv b, e = Linv^T y (block-diagonal passes)
+//   F_j = Linv_j K_{j-1}   (1 <= j <= t)      forward, top chain
+//   G_j = Linv_j K'_{j+1}  (t <= j <= nb-2)   forward, bottom chain
+//   N_j = Linv_j^T K_j^T   (0 <= j <= t-1)    backward, top chain (from t down)
+//   N'_j = Linv_j^T K'_j^T (t+1 <= j <= nb-1) backward, bottom chain (from t up)
+// The two chains of each substitution run concurrently in one persistent
+// cooperative kernel, so a solve has about nb dependent steps instead of 2 nb.
 struct BlockTriChol {
-    int n = 0, nb = 0, max_b = 0;
-    std::vector<int> bsz, boff;            // block sizes / offsets (permuted order)
-    std::vector<long long> o_linv, o_m, o_n;  // offsets into store
-    DBuf<double> store;
+    int n = 0, nb = 0, max_b = 0, twist = 0;
+    std::vector<int> bsz, boff;
     DBuf<int> d_bsz, d_boff;
-    DBuf<long long> d_olinv, d_om, d_on;
-    DBuf<int> perm;  // new -> old (empty = identity)
-    DBuf<unsigned int> bar;  // grid barrier state
-    int coop_blocks = 0;
-    void* rec_fn = nullptr;  // register-prefetch recurrence (fallback) for max_b
-    bool use_tma = false;    // TMA-pipelined recurrence available
-    int tma_blocks = 0, tma_stages = 0, maxld = 0;
-    size_t tma_smem = 0;
-    std::vector<long long> o_linvr;
-    std::vector<int> ld_m, ld_n, ld_l;
-    DBuf<long long> d_olinvr;
-    DBuf<int> d_ldm, d_ldn, d_ldl;
-    DBuf<unsigned int> counter;
-    DBuf<uint4> ll;  // LL lines (value + flag) of the dataflow recurrence, n * max_rhs
-    unsigned long long tag_call = 0;
+    DBuf<int> perm;                 // new -> old (empty = identity)
+    DBuf<int> inv_perm, blk_of, loc_of;
+    DBuf<double> store;
+    std::vector<long long> o_linv, o_linvr;
+    std::vector<int> ld_l;
+    DBuf<long long> d_olinv, d_olinvr;
+    DBuf<int> d_ldl;
+    // recurrence schedules (forward, backward): steps x 2 chains
+    std::vector<RecTask> fwd, bwd;
+    DBuf<RecTask> d_fwd, d_bwd;
+    double factor_bytes = 0.0;       // bytes of the stored solve matrices read per solve
+    // recurrence kernel configuration
+    int rpc = 8, g0 = 0, g1 = 0, stages = 1, maxld = 0;
+    size_t smem = 0;
+    DBuf<uint4> ll;                  // LL lines (value + flag), n * max_rhs
+    unsigned long long call = 0;
     int prof_phase = PROF_A_SOLVE;
-    // algorithmic bytes of one solve: L read by the forward and the backward
-    // substitution (stored as Linv lower + M + N = 3 m^2/block) + b in, x out
-    double alg_bytes(int nrhs) const;
-    // work vectors (n * max_rhs)
     int max_rhs = 0;
+    bool debug_timing = false;       // per-step %globaltimer stamps of the last recurrence into dbg
+    DBuf<unsigned long long> dbg;
     DBuf<double> wb, wc, wy, we, wx;
 
     // Factor the SPD matrix given as device CSR rows (natural numbering) with
     // permutation perm_host (new -> old, empty = identity) and block sizes.
     void factor(int n_, const int* off, const int* idx, const double* val, const std::vector<int>& perm_host,
                 const std::vector<int>& block_sizes, int max_rhs_, cudaStream_t st);
-    // Factor from dense blocks already scattered (used by the flow Schur complement builder).
-    void factor_dense(double* D, double* C, cudaStream_t st);
-    // x = A^{-1} b for nrhs right-hand sides; b/x columns at stride ldb/ldx (natural numbering).
+    // Factor from dense blocks already scattered by a builder (layout()/dense offsets).
+    void factor_dense(double* dense, cudaStream_t st);
+    // x = A^{-1} b for nrhs <= 2 right-hand sides; columns at stride ldb/ldx (natural numbering).
     void solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
-    void recurrence(int dir, const double* in, double* out, int nrhs, cudaStream_t st);
+    // algorithmic bytes of one solve: the factor read by both substitutions + b in, x out
+    double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 
-    // helpers exposed to builders
+    // builder helpers: dense diagonal blocks D_j (m_j x m_j col-major) and
+    // sub-diagonal blocks C_j = A_{j+1,j} (m_{j+1} x m_j col-major)
     void layout(int n_, const std::vector<int>& perm_host, const std::vector<int>& block_sizes);
     long long dense_d_offset(int j) const { return dD_[j]; }
     long long dense_c_offset(int j) const { return dC_[j]; }
     long long dense_total() const { return dtot_; }
-    DBuf<int> inv_perm;  // old -> new
-    DBuf<int> blk_of;    // new index -> block
-    DBuf<int> loc_of;    // new index -> local index
 
 private:
     std::vector<long long> dD_, dC_;
     long long dtot_ = 0;
+    void recurrence(const DBuf<RecTask>& sched, int nsteps, const double* in, double* out, int nrhs, cudaStream_t st);
 };
 
 // cuBLAS / cuSOLVER handles bound to a stream (setup only).

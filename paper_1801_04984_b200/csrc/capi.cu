@@ -327,6 +327,24 @@ int pdg_block_download_csr(const pdg_block* blk, long long* row_offsets, int* co
 
 void pdg_block_destroy(pdg_block* blk) { delete blk; }
 
+int pdg_debug_recurrence_timing(pdg_block* blk, int which, unsigned long long* out, long long cap, int* ctas,
+                                int* nsteps) {
+    API_BEGIN
+    require(blk && out && ctas && nsteps, "pdg_debug_recurrence_timing: null argument");
+    BlockTriChol& c = which == 0 ? blk->b.pre.a->chol : blk->b.pre.flow;
+    cudaStream_t st = blk->b.ctx->stream;
+    c.debug_timing = true;
+    PDG_CUDA(cudaMemsetAsync(blk->io_a.p, 0, sizeof(double) * blk->b.rows(), st));
+    blk->b.pre.apply(blk->io_a.p, blk->io_b.p, st);
+    PDG_CUDA(cudaStreamSynchronize(st));
+    c.debug_timing = false;
+    std::vector<unsigned long long> h = c.dbg.download(st);
+    *ctas = c.g0 + c.g1;
+    *nsteps = static_cast<int>(c.bwd.size() / 2);
+    std::memcpy(out, h.data(), sizeof(unsigned long long) * std::min<long long>(cap, (long long)h.size()));
+    API_END
+}
+
 int pdg_op_create(pdg_ops* ops, int m, const double* theta, double tau, pdg_op** out) {
     API_BEGIN
     require(ops && theta && out, "pdg_op_create: null argument");
