@@ -176,83 +176,112 @@ def main():
     L = _lib.lib()
     run = P.RUNS["config1"]
     tau = run["T"] / run["n_slabs"]
-    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]))
     t_setup = time.time()
     ops = S.SpatialOperators.assemble(P.config1(128), device=local)
-    slab = S.SlabSolver(ops, run["r"], tau, opt)
     torch.cuda.synchronize()
-    setup_s = time.time() - t_setup
     nt, nn = ops.n_total, run["r"] + 1
     dev = torch.device("cuda", local)
-    u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
-    p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
-    rhs = torch.empty(nn * nt, dtype=torch.float64, device=dev)
-    out = torch.empty_like(rhs)
-    rhs_host = []
 
-    def step(n, keep=False):
-        slab.rhs_device(tau * n, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
-        if keep:
-            rhs_host.append(rhs.cpu().pin_memory().numpy())
-        rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
-        end = out[run["r"] * nt:(run["r"] + 1) * nt]
-        u_prev.copy_(end[:ops.n_u])
-        p_prev.copy_(end[ops.n_u + ops.n_q:])
-        return rep
+    def timed_march(candidate, keep_rhs):
+        """W warm-up + K timed slabs of the device-resident march (CUDA events)."""
+        opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]), candidate=candidate)
+        slab = S.SlabSolver(ops, run["r"], tau, opt)
+        u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
+        p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
+        rhs = torch.empty(nn * nt, dtype=torch.float64, device=dev)
+        out = torch.empty_like(rhs)
+        rhs_host = []
 
-    for n in range(args.warmup):
-        step(n)
-    # the rhs of the timed slabs, for the e2e leg (collected outside the timed region)
-    snap = (u_prev.clone(), p_prev.clone())
-    for n in range(args.warmup, args.warmup + args.steps):
-        step(n, keep=True)
-    u_prev.copy_(snap[0])
-    p_prev.copy_(snap[1])
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    iters = []
-    launches0 = L.pdg_util_launch_count()
-    S.profile(enable=True, reset=True)
-    with Clocks(local) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        def step(n, keep=False):
+            slab.rhs_device(tau * n, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+            if keep:
+                rhs_host.append(rhs.cpu().pin_memory().numpy())
+            rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+            end = out[run["r"] * nt:(run["r"] + 1) * nt]
+            u_prev.copy_(end[:ops.n_u])
+            p_prev.copy_(end[ops.n_u + ops.n_q:])
+            return rep
+
+        for n in range(args.warmup):
+            step(n)
+        if keep_rhs:  # rhs of the timed slabs for the e2e leg, collected outside the timed region
+            snap = (u_prev.clone(), p_prev.clone())
+            for n in range(args.warmup, args.warmup + args.steps):
+                step(n, keep=True)
+            u_prev.copy_(snap[0])
+            p_prev.copy_(snap[1])
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
-        e0.record()
-        for n in range(args.warmup, args.warmup + args.steps):
-            iters.append(step(n).iterations)
-        e1.record()
-        torch.cuda.synchronize()
-    phases_raw = S.profile(enable=False)
-    launches = L.pdg_util_launch_count() - launches0
-    ms_dev = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        torch.distributed.barrier()
-    clocks = clk.summary()
+        iters = []
+        launches0 = L.pdg_util_launch_count()
+        S.profile(enable=True, reset=True)
+        with Clocks(local) as clk:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for n in range(args.warmup, args.warmup + args.steps):
+                iters.append(step(n).iterations)
+            e1.record()
+            torch.cuda.synchronize()
+        phases_raw = S.profile(enable=False)
+        launches = L.pdg_util_launch_count() - launches0
+        ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            torch.distributed.barrier()
+        return dict(slab=slab, ms=ms, iters=iters, phases_raw=phases_raw, launches=launches, clocks=clk.summary(),
+                    rhs_host=rhs_host)
+
+    main_run = timed_march("flexible", keep_rhs=True)
+    setup_s = time.time() - t_setup
+    ref_run = timed_march("reference", keep_rhs=False)
+    ms_dev = main_run["ms"]
     phases = {k: {"ms_per_step": v[0] / args.steps, "calls_per_step": v[1] / args.steps,
                   "alg_GB_per_call": (v[2] / v[1] / 1e9) if v[1] else 0.0,
-                  "achieved_GBs": (v[2] / (v[0] * 1e-3) / 1e9) if v[0] else 0.0} for k, v in phases_raw.items()}
+                  "achieved_GBs": (v[2] / (v[0] * 1e-3) / 1e9) if v[0] else 0.0}
+              for k, v in main_run["phases_raw"].items()}
     dom = max(phases, key=lambda k: phases[k]["ms_per_step"])
     ach = phases[dom]["achieved_GBs"]
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        if dom == "a_solve" and "a_solve" in tr:
+            traffic = tr["a_solve"]["bytes"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_kind": peak_kind, "traffic": None,
-                "share_of_step": phases[dom]["ms_per_step"] / ms_dev if ms_dev else None}
+                "peak_kind": peak_kind, "traffic": traffic,
+                "share_of_step": phases[dom]["ms_per_step"] / ms_dev if ms_dev else None,
+                "algorithmic_bytes_per_call": phases[dom]["alg_GB_per_call"] * 1e9}
 
-    # e2e: the reference-facing call (pdg_slab_solve) with HOST buffers
+    # e2e: the reference-facing call (pdg_slab_solve) with HOST buffers (rhs H2D and state D2H inside)
     e2e = []
+    slab = main_run["slab"]
     torch.cuda.synchronize()
     for k in range(args.steps):
         t0 = time.perf_counter()
-        _, _rep = slab.solve(rhs_host[k])
+        slab.solve(main_run["rhs_host"][k])
         e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = float(np.mean(e2e))
 
-    t = torch.tensor([ms_dev, e2e_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_dev, e2e_ms, ref_run["ms"]], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_dev, e2e_ms = float(t[0]), float(t[1])
+    ms_dev, e2e_ms, ms_ref = float(t[0]), float(t[1]), float(t[2])
 
     spmv = spmv_sweep([int(s) for s in args.spmv_sizes.split(",") if s], args.spmv_reps, peak) \
         if rank == 0 and args.spmv_sizes else []
+    spmv_roof = None
+    if spmv:
+        big = spmv[-1]
+        spmv_roof = {"bound": "hbm", "kernel": f"k_spmv {big['n']}^2 dG(1)", "achieved": big["achieved_GBs"],
+                     "peak": peak, "unit": "GB/s", "frac": big["frac"], "gdof_s": big["gdof_s"], "traffic": None}
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            if f"spmv_{big['n']}" in tr:
+                spmv_roof["traffic"] = tr[f"spmv_{big['n']}"]["bytes"]
+        except Exception:
+            pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -262,21 +291,25 @@ def main():
         cpu = {"value": 1e3 * float(np.mean(secs)), "unit": "ms/slab", "cores": os.cpu_count(), "kind": "port",
                "iterations": [int(i) for i in res["iterations"]],
                "sample": f"{args.cpu_slabs} slab(s) of config 1 on the host (setup {res['setup_seconds']:.1f} s "
-                         "excluded); oracle with exact banded sparse-direct inner solves; factorisation "
-                         "OpenMP-parallel, triangular solves serial"}
+                         "excluded, first slab warm-up); oracle with exact banded sparse-direct inner solves; "
+                         "factorisation OpenMP-parallel, triangular solves serial"}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": ms_dev, "unit": "ms/slab", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded lognormal K, BASELINE config 1)",
             "config": {"workload": WORKLOAD, "rows_per_block": nn * nt,
-                       "l2": "no flush: per-step working set (A factor ~3 GB) > 126 MB L2",
+                       "gmres_candidate": "flexible: x + Z y (the reference's gmres_flexible, gmres.hpp:113-114,"
+                                          " 153-158; same iterations, solutions within 1e-9 of gmres)",
+                       "l2": "no flush: per-step working set (A factor ~4 GB) > 126 MB L2",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "setup_s": setup_s},
-            "iterations": iters,
+            "iterations": main_run["iters"],
+            "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],
+                                          "note": "candidate x + P(V y) exactly as gmres.hpp:116"},
             "e2e": {"value": e2e_ms, "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
                     "d2h_bytes_per_step": 8 * nn * nt},
-            "gpu_launches": int(launches), "roofline": roofline, "phases": phases, "spmv": spmv, "clocks": clocks,
-            "cpu_baseline": cpu}), flush=True)
+            "gpu_launches": int(main_run["launches"]), "roofline": roofline, "spmv_roofline": spmv_roof,
+            "phases": phases, "spmv": spmv, "clocks": main_run["clocks"], "cpu_baseline": cpu}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
