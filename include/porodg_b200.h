@@ -155,8 +155,9 @@ int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes)
 
 /* Diagnostics: run one preconditioner application of `blk` with per-step
  * %globaltimer stamps in the last recurrence of solver `which` (0 displacement,
- * 1 flow); out[(cta * nsteps + step) * 3 + phase] (ns), phases: step start,
- * sources gathered, rows stored. *ctas / *nsteps receive the shape. */
+ * 1 flow); out[(cta * nsteps + step) * 4 + phase] (ns), phases: step start,
+ * sources gathered, rows stored, streamed rows ready (0 when not recorded).
+ * *ctas / *nsteps receive the shape. */
 int pdg_debug_recurrence_timing(pdg_block* blk, int which, unsigned long long* out, long long cap, int* ctas,
                                 int* nsteps);
 

@@ -1,8 +1,10 @@
 // Fixed-stress preconditioner, deterministic Krylov kernels and the GMRES
 // driver of one slab block.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <string>
 
 #include "block.cuh"
 
@@ -263,6 +265,8 @@ std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaS
     // cell-row order: block j = displacement dofs of cell row j (8 nx each)
     require(ops.nx > 0 && ops.ny > 0 && ops.n_u == 8 * ops.nx * ops.ny, "A solver: mesh dimensions do not match n_u");
     std::vector<int> bs(ops.ny, 8 * ops.nx);
+    const char* mode = std::getenv("PDG_A_SOLVER");  // "general": the three-matrix recurrence path
+    a->chol.allow_local = !(mode && std::string(mode) == "general");
     a->chol.factor(ops.n_u, ops.A.off.p, ops.A.idx.p, ops.A.val.p, {}, bs, max_rhs, st);
     return a;
 }

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "blocktri.cuh"
+#include "llsync.cuh"
 
 namespace pdg {
 
@@ -140,53 +141,7 @@ __global__ void __launch_bounds__(256) k_blockdiag_upper(int n, int nrhs, const 
     }
 }
 
-// ---- TMA / mbarrier / LL primitives ----------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1D bulk copy global -> shared (TMA engine), completion counted on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// LL line (the NCCL "LL" idea): a double travels as two 32-bit halves, each
-// paired with a 32-bit flag in one 8-byte-atomic unit, 16 bytes per value: one
-// store publishes value + flag, a reader accepts the line when both flags
-// match -- no fences on the critical path.
-__device__ __forceinline__ void ll_store(uint4* p, double v, unsigned flag) {
-    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(static_cast<unsigned>(b)),
-                 "r"(flag), "r"(static_cast<unsigned>(b >> 32)), "r"(flag)
-                 : "memory");
-}
-__device__ __forceinline__ uint4 ll_peek(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ double ll_value(const uint4& v) {
-    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.z) << 32) | v.x));
-}
+using namespace dev;
 
 // Poll-and-gather the nrhs right-hand sides of one source block into shared
 // memory: every line load of the thread is issued before any flag is checked.
@@ -238,12 +193,12 @@ __global__ void __launch_bounds__(288, 1) k_recurrence(int nsteps, int nb, const
                                                       int rpc, int maxld, int max_b, int g0,
                                                       unsigned long long* dbg) {
     // dbg (debug only, normally null): per CTA and step, %globaltimer at step
-    // start, after the source gather, after the row stores.
+    // start, after the source gather, after the row stores (4 slots per step).
     auto stamp = [&](int s, int ph) {
         if (dbg && threadIdx.x == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            dbg[((size_t)blockIdx.x * nsteps + s) * 3 + ph] = t;
+            dbg[((size_t)blockIdx.x * nsteps + s) * 4 + ph] = t;
         }
     };
     // The ring holds `stages` units of 8 rows; step s uses units s*upr .. s*upr+upr-1
@@ -521,6 +476,7 @@ void BlockTriChol::factor(int n_, const int* off, const int* idx, const double* 
 }
 
 void BlockTriChol::factor_dense(double* dense, cudaStream_t st) {
+    local_prepare(dense, st);  // before the couplings are overwritten by the factorisation
     LaHandles h(st);
     const int t = twist;
     int lwork = 0;
@@ -579,6 +535,10 @@ void BlockTriChol::factor_dense(double* dense, cudaStream_t st) {
         if (hinfo[j] != 0)
             throw Error(PDG_NOT_CONVERGED, "dense LU: matrix is singular to working precision (block " +
                                                std::to_string(j) + " not positive definite)");
+    if (local) {
+        local_finish(dense, st);
+        return;
+    }
     // ---- solve-time storage ---------------------------------------------------
     auto pad = [](int m) { return (m + 1) & ~1; };                    // 16-byte rows (cp.async.bulk)
     auto al = [](long long v) { return (v + 31) & ~31LL; };           // 256-byte aligned matrices
@@ -742,8 +702,9 @@ void BlockTriChol::recurrence(const DBuf<RecTask>& sched, int nsteps, const doub
     double* a6 = out;
     uint4* a7 = ll.p;
     unsigned long long* dbgp = nullptr;
+    dbg_steps = nsteps;
     if (debug_timing) {
-        dbg.alloc((size_t)(g0 + g1) * nsteps * 3);
+        dbg.alloc((size_t)(g0 + g1) * nsteps * 4);
         dbg.zero(st);
         dbgp = dbg.p;
     }
@@ -755,6 +716,10 @@ void BlockTriChol::recurrence(const DBuf<RecTask>& sched, int nsteps, const doub
 void BlockTriChol::solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs && nrhs <= 2, "block-tridiagonal solve: bad nrhs");
+    if (local) {
+        solve_local(b, ldb, x, ldx, nrhs, st);
+        return;
+    }
     const int* pp = perm.n ? perm.p : nullptr;
     const long long tot = (long long)n * nrhs;
     k_gather<<<grid_for(tot, 256), 256, 0, st>>>(n, nrhs, pp, b, ldb, wb.p);

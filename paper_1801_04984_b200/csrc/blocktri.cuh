@@ -20,6 +20,12 @@ struct RecTask {
     long long off1, off2;
 };
 
+// One step of the local-coupling sweep for one chain (see BlockTriChol::local).
+enum SweepKind { SW_IDLE = 0, SW_FIRST = 1, SW_FWD = 2, SW_TWIST = 3, SW_BWD = 4 };
+struct SweepTask {
+    int blk, kind;
+};
+
 // Twisted ("burn at both ends") block Cholesky A = P P^T with twist block t:
 // blocks 0..t-1 are eliminated from the top (L_j, K_j = L_{j+1,j}), blocks
 // nb-1..t+1 from the bottom (L'_j, K'_j = L_{j-1,j}), and
@@ -57,6 +63,30 @@ struct BlockTriChol {
     bool debug_timing = false;       // per-step %globaltimer stamps of the last recurrence into dbg
     DBuf<unsigned long long> dbg;
     DBuf<double> wb, wc, wy, we, wx;
+    int dbg_steps = 0;               // steps recorded in dbg by the last solve
+
+    // ---- local-coupling mode (the displacement block A) -------------------------------
+    // When all blocks have one size m (multiple of 8), no permutation is used and
+    // every coupling block C_j = A_{j+1,j} only couples an 8-row chunk (a cell) to
+    // the same chunk of the neighbour block, the solve keeps the inverse twisted
+    // Schur complements Sinv_j (full, row-major) and the 8x8 coupling chunks and
+    // runs ONE persistent kernel (k_sweep):
+    //   forward   v_j = Sinv_j w_j,   w_{j+1} = b_{j+1} - C_j v_j         (top chain)
+    //             v_j = Sinv_j w_j,   w_{j-1} = b_{j-1} - C_{j-1}^T v_j   (bottom chain)
+    //   twist     x_t = Sinv_t (b_t - C_{t-1} v_{t-1} - C_t^T v_{t+1})
+    //   backward  x_j = Sinv_j (w_j - C_j^T x_{j+1}) / Sinv_j (w_j - C_{j-1} x_{j-1})
+    // The chunk-local products are formed by the CTA that owns the chunk, so each
+    // step streams one Sinv_j: 2 m^2 doubles per block per solve (the general
+    // path reads 3 m^2: Linv twice, F/G and N).
+    bool allow_local = false;        // set by the owner before factor()
+    bool local = false;              // chosen by factor()
+    DBuf<double> cloc;               // [nb-1][m/8][8][8]: chunk (r, q) of C_j, row-major
+    DBuf<double> wsave;              // w_j of the forward sweep, read back by the backward sweep
+    long long sinv_stride = 0;       // Sinv_j at store + j * sinv_stride, row stride ld_s
+    int ld_s = 0, sw_rpc = 0, sw_g = 0, sw_stages = 0;
+    size_t sw_smem = 0;
+    std::vector<SweepTask> sweep;    // steps x 2 chains
+    DBuf<SweepTask> d_sweep;
 
     // Factor the SPD matrix given as device CSR rows (natural numbering) with
     // permutation perm_host (new -> old, empty = identity) and block sizes.
@@ -80,6 +110,9 @@ private:
     std::vector<long long> dD_, dC_;
     long long dtot_ = 0;
     void recurrence(const DBuf<RecTask>& sched, int nsteps, const double* in, double* out, int nrhs, cudaStream_t st);
+    bool local_prepare(double* dense, cudaStream_t st);   // structure check + coupling chunks
+    void local_finish(double* dense, cudaStream_t st);    // Sinv_j from the Cholesky factors, schedule, kernel config
+    void solve_local(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
 };
 
 // cuBLAS / cuSOLVER handles bound to a stream (setup only).

@@ -21,8 +21,9 @@ def main():
         g, ns = C.c_int(), C.c_int()
         _lib.check(_lib.lib().pdg_debug_recurrence_timing(blk._h, which, buf, cap, C.byref(g), C.byref(ns)))
         g, ns = g.value, ns.value
-        a = np.frombuffer(buf, dtype=np.uint64, count=g * ns * 3).reshape(g, ns, 3).astype(np.int64)
+        a = np.frombuffer(buf, dtype=np.uint64, count=g * ns * 4).reshape(g, ns, 4).astype(np.int64)
         t0 = a[:, :, 0].min()
+        has_wait = bool(a[:, :, 3].any())
         a = a - t0
         total = a[:, -1, 2].max()
         gather = np.median(a[:, 1:, 1] - a[:, 1:, 0], axis=0)
@@ -35,6 +36,11 @@ def main():
               f"period median={np.median(period)/1e3:.2f} us; gather median={np.median(gather)/1e3:.2f} us; "
               f"compute+store median={np.median(comp)/1e3:.2f} us; latency(prev store->gather end) median="
               f"{np.median(lat)/1e3:.2f} us")
+        if has_wait:  # phase 3 = ring data ready (sweep kernel)
+            wait = np.median(a[:, 1:, 3] - a[:, 1:, 1], axis=0)
+            rest = np.median(a[:, 1:, 2] - a[:, 1:, 3], axis=0)
+            print(f"   data wait after gather median={np.median(wait)/1e3:.2f} us; "
+                  f"GEMV+reduce+publish median={np.median(rest)/1e3:.2f} us")
         print("   first steps period (us):", np.round(period[:8] / 1e3, 2))
         print("   step start spread across CTAs (us) at step 10:", (a[:, 10, 0].max() - a[:, 10, 0].min()) / 1e3)
 
