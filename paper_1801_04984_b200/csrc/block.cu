@@ -1,5 +1,6 @@
 // Fixed-stress preconditioner, deterministic Krylov kernels and the GMRES
 // driver of one slab block.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>

@@ -12,12 +12,16 @@
 
 namespace pdg {
 
-// One task of a recurrence step for one chain: rows of block `tgt` are
-// out_tgt = in_tgt - F1 out_src1 - F2 out_src2 (missing sources skipped; a
-// task without sources copies in_tgt). F are row-major (ld padded).
-struct RecTask {
-    int tgt, src1, src2, ld1, ld2;
-    long long off1, off2;
+struct LaHandles;
+
+// One step of the dense sweep for one chain (see blocktri_dense.cu): output
+// rows [0, mout) of the step = M * [seg0; seg1], M row-major at store + moff
+// (row stride ld). seg0: n0 values at LL offset in0 (or from b at b0 when
+// in0 < 0); seg1: n1 values at LL offset in1. Outputs go to LL offset out_ll
+// and/or x offset out_x (-1 = none); moff < 0 = idle.
+struct DenseTask {
+    long long moff, in0, in1, b0, out_ll, out_x;
+    int n0, n1, mout, ld;
 };
 
 // One step of the local-coupling sweep for one chain (see BlockTriChol::local).
@@ -30,39 +34,28 @@ struct SweepTask {
 // blocks 0..t-1 are eliminated from the top (L_j, K_j = L_{j+1,j}), blocks
 // nb-1..t+1 from the bottom (L'_j, K'_j = L_{j-1,j}), and
 // L_t L_t^T = A_tt - K_{t-1} K_{t-1}^T - K'_{t+1} K'_{t+1}^T.
-// Stored for the solve (all row-major, 256-byte aligned, rows padded to 16 B):
-//   Linv_j (col-major and row-major copies)   c = Linv b, e = Linv^T y (block-diagonal passes)
-//   F_j = Linv_j K_{j-1}   (1 <= j <= t)      forward, top chain
-//   G_j = Linv_j K'_{j+1}  (t <= j <= nb-2)   forward, bottom chain
-//   N_j = Linv_j^T K_j^T   (0 <= j <= t-1)    backward, top chain (from t down)
-//   N'_j = Linv_j^T K'_j^T (t+1 <= j <= nb-1) backward, bottom chain (from t up)
-// The two chains of each substitution run concurrently in one persistent
-// cooperative kernel, so a solve has about nb dependent steps instead of 2 nb.
+// A solve is ONE persistent cooperative kernel in which a top and a bottom
+// chain run concurrently as a barrier-free dataflow (LL lines between CTAs,
+// TMA-streamed matrix rows), about nb dependent steps in all:
+//   local mode  (chunk-local couplings, the displacement block): k_sweep,
+//               blocktri_local.cu, stores Sinv_j of the twisted Schur complements;
+//   dense mode  (any coupling, the flow block): k_sweep_dense,
+//               blocktri_dense.cu, stores [Linv | -Linv K]-type step matrices.
 struct BlockTriChol {
     int n = 0, nb = 0, max_b = 0, twist = 0;
     std::vector<int> bsz, boff;
     DBuf<int> d_bsz, d_boff;
     DBuf<int> perm;                 // new -> old (empty = identity)
     DBuf<int> inv_perm, blk_of, loc_of;
-    DBuf<double> store;
-    std::vector<long long> o_linv, o_linvr;
-    std::vector<int> ld_l;
-    DBuf<long long> d_olinv, d_olinvr;
-    DBuf<int> d_ldl;
-    // recurrence schedules (forward, backward): steps x 2 chains
-    std::vector<RecTask> fwd, bwd;
-    DBuf<RecTask> d_fwd, d_bwd;
+    DBuf<double> store;              // the solve matrices
     double factor_bytes = 0.0;       // bytes of the stored solve matrices read per solve
-    // recurrence kernel configuration
-    int rpc = 8, g0 = 0, g1 = 0, stages = 1, maxld = 0;
-    size_t smem = 0;
-    DBuf<uint4> ll;                  // LL lines (value + flag), n * max_rhs
+    DBuf<uint4> ll;                  // LL lines (value + flag)
     unsigned long long call = 0;
     int prof_phase = PROF_A_SOLVE;
     int max_rhs = 0;
     bool debug_timing = false;       // per-step %globaltimer stamps of the last recurrence into dbg
     DBuf<unsigned long long> dbg;
-    DBuf<double> wb, wc, wy, we, wx;
+    DBuf<double> wb, wx;             // permuted right-hand sides / solutions (dense mode)
     int dbg_steps = 0;               // steps recorded in dbg by the last solve
 
     // ---- local-coupling mode (the displacement block A) -------------------------------
@@ -88,6 +81,13 @@ struct BlockTriChol {
     std::vector<SweepTask> sweep;    // steps x 2 chains
     DBuf<SweepTask> d_sweep;
 
+    // ---- dense-sweep mode (any coupling pattern: the flow solve) -------------------------
+    std::vector<DenseTask> dsched;   // steps x 2 chains
+    DBuf<DenseTask> d_dsched;
+    long long d_lln = 0;
+    int d_ldmax = 0, d_g = 0, d_stages = 0;
+    size_t d_smem = 0;
+
     // Factor the SPD matrix given as device CSR rows (natural numbering) with
     // permutation perm_host (new -> old, empty = identity) and block sizes.
     void factor(int n_, const int* off, const int* idx, const double* val, const std::vector<int>& perm_host,
@@ -109,10 +109,12 @@ struct BlockTriChol {
 private:
     std::vector<long long> dD_, dC_;
     long long dtot_ = 0;
-    void recurrence(const DBuf<RecTask>& sched, int nsteps, const double* in, double* out, int nrhs, cudaStream_t st);
     bool local_prepare(double* dense, cudaStream_t st);   // structure check + coupling chunks
     void local_finish(double* dense, cudaStream_t st);    // Sinv_j from the Cholesky factors, schedule, kernel config
     void solve_local(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+    void dense_finish(LaHandles& h, const double* dense, const double* kp, const std::vector<long long>& oKp,
+                      cudaStream_t st);
+    void solve_dense(const double* b, double* x, int nrhs, cudaStream_t st);
 };
 
 // cuBLAS / cuSOLVER handles bound to a stream (setup only).

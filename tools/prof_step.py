@@ -16,8 +16,16 @@ def main():
     cand = sys.argv[3] if len(sys.argv) > 3 else "reference"
     ops = S.SpatialOperators.assemble(P.config1(n))
     opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=cand)
+    phases = os.environ.get("PROF_PHASES") == "1"
+    if phases:
+        S.march(ops, 1, 0.05, 1, opt)  # warm-up
+        S.profile(enable=True, reset=True)
     reps, _ = S.march(ops, 1, 0.05 * slabs, slabs, opt)
     torch.cuda.synchronize()
+    if phases:
+        for nm, (ms, calls, by) in S.profile(enable=False).items():
+            print(f"  {nm:16s} {ms / slabs:8.3f} ms/slab {calls / slabs:6.1f} calls/slab "
+                  f"{(by / (ms * 1e-3) / 1e9 if ms else 0):8.1f} GB/s")
     print("iterations", [r.iterations for r in reps], "device_ms", [round(r.device_ms, 3) for r in reps])
 
 
