@@ -28,44 +28,104 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return s;  // valid on thread 0
 }
 
-// partial[b * ncols + j] = sum over this block's rows of V_j . w
+// Deterministic Krylov reductions: kRedBlocks fixed-size blocks write one
+// partial per (block, column) (grid-stride rows, fixed order), and every
+// consumer re-sums the kRedBlocks partials of a column with the same fixed
+// tree, so results are bit-reproducible on any GPU and no separate
+// "finish the reduction" launch is needed.
+
+// partial[b * ncols + j] = sum over this block's rows of V_j . w (8 columns per pass)
 __global__ void __launch_bounds__(kRedThreads) k_multidot1(long long n, int ncols, const double* __restrict__ V,
                                                            const double* __restrict__ w, double* __restrict__ partial) {
-    __shared__ double sh[32];
-    for (int j0 = 0; j0 < ncols; j0 += 4) {
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
+    __shared__ double sh[8][kRedThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j0 = 0; j0 < ncols; j0 += 8) {
+        double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
             const double wr = w[r];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 8; ++q)
                 if (j0 + q < ncols) a[q] += V[(long long)(j0 + q) * n + r] * wr;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double s = block_sum(a[q], sh);
-            if (threadIdx.x == 0 && j0 + q < ncols) partial[(long long)blockIdx.x * ncols + j0 + q] = s;
+        for (int q = 0; q < 8; ++q)
+            for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sh[q][warp] = a[q];
+        __syncthreads();
+        if (threadIdx.x < 8 && j0 + threadIdx.x < ncols) {
+            double s = 0.0;
+            for (int i = 0; i < kRedThreads / 32; ++i) s += sh[threadIdx.x][i];
+            partial[(long long)blockIdx.x * ncols + j0 + threadIdx.x] = s;
         }
+        __syncthreads();
     }
 }
 
-// out[j] = sum_b partial[b * ncols + j]  (one block per column, fixed tree)
-__global__ void __launch_bounds__(kRedThreads) k_multidot2(int nparts, int ncols, const double* __restrict__ partial,
-                                                           double* __restrict__ out) {
-    __shared__ double sh[32];
-    const int j = blockIdx.x;
+// Sum of the kRedBlocks partials of column j (fixed tree); valid on thread 0.
+__device__ __forceinline__ double sum_partials(const double* __restrict__ partial, int ncols, int j, double* sh) {
     double v = 0.0;
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v += partial[(long long)b * ncols + j];
-    const double s = block_sum(v, sh);
-    if (threadIdx.x == 0) out[j] = s;
+    for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += partial[(long long)b * ncols + j];
+    return block_sum(v, sh);
 }
 
+// h = column sums of the partials (block 0 writes them to h_out), then
 // w -= sum_j h_j V_j, subtracting column by column in j order
-__global__ void k_multiaxpy(long long n, int ncols, const double* __restrict__ V, const double* __restrict__ h,
-                            double* __restrict__ w) {
+__global__ void __launch_bounds__(kRedThreads) k_red_multiaxpy(long long n, int ncols, const double* __restrict__ partial,
+                                                               const double* __restrict__ V, double* __restrict__ w,
+                                                               double* __restrict__ h_out) {
+    __shared__ double sh[32];
+    extern __shared__ double hs[];  // [ncols]
+    for (int j = 0; j < ncols; ++j) {
+        const double s = sum_partials(partial, ncols, j, sh);
+        if (threadIdx.x == 0) hs[j] = s;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int j = threadIdx.x; j < ncols; j += blockDim.x) h_out[j] = hs[j];
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
         double v = w[r];
-        for (int j = 0; j < ncols; ++j) v -= h[j] * V[(long long)j * n + r];
+        for (int j = 0; j < ncols; ++j) v -= hs[j] * V[(long long)j * n + r];
         w[r] = v;
+    }
+}
+
+// nrm = sqrt(sum of the partials); dst = src / nrm (dst may be null); block 0 writes nrm
+__global__ void __launch_bounds__(kRedThreads) k_red_norm_scale(long long n, const double* __restrict__ partial,
+                                                                const double* __restrict__ src, double* __restrict__ dst,
+                                                                double* __restrict__ nrm_out) {
+    __shared__ double sh[32];
+    __shared__ double nv;
+    const double s = sum_partials(partial, 1, 0, sh);
+    if (threadIdx.x == 0) nv = sqrt(s);
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nrm_out = nv;
+    if (!dst) return;
+    const double d = nv;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        dst[r] = src[r] / d;
+}
+
+// out = a - b, and the partial sums of out . out (same layout as k_multidot1 with one column)
+__global__ void __launch_bounds__(kRedThreads) k_sub_dot(long long n, const double* __restrict__ a,
+                                                         const double* __restrict__ b, double* __restrict__ out,
+                                                         double* __restrict__ partial) {
+    __shared__ double sh[kRedThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc = 0.0;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        const double v = a[r] - b[r];
+        out[r] = v;
+        acc += v * v;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sh[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < kRedThreads / 32; ++i) s += sh[i];
+        partial[blockIdx.x] = s;
     }
 }
 
@@ -79,23 +139,10 @@ __global__ void k_combine(long long n, int ncols, const double* __restrict__ V, 
     }
 }
 
-__global__ void k_scale_div(long long n, const double* __restrict__ src, const double* __restrict__ d, double* __restrict__ dst) {
-    const double dv = *d;
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
-        dst[r] = src[r] / dv;
-}
-
-__global__ void k_sub(long long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
-        out[r] = a[r] - b[r];
-}
-
 __global__ void k_add(long long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
         out[r] = a[r] + b[r];
 }
-
-__global__ void k_sqrt(double* v) { *v = sqrt(*v); }
 
 // ---- fixed-stress sweep kernels (fixed_stress.hpp:109-139) ------------------
 // fp_i = r_p_i [+ lambda (b E^T u_i - stab m_p p_i) for sweeps after the first]
@@ -372,10 +419,10 @@ void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
     cand.alloc(n);
     t.alloc(n);
     y_dev.alloc(restart + 2);
-    h_dev.alloc(restart + 2);
+    h_dev.alloc(2 * (restart + 2));
     partial.alloc((size_t)kRedBlocks * (restart + 2));
     norm_dev.alloc(4);
-    if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (restart + 8)));
+    if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (2 * restart + 8)));
     (void)st;
 }
 Gmres::~Gmres() {
@@ -415,19 +462,46 @@ namespace {
 struct KrylovOps {
     cudaStream_t st;
     Gmres& g;
-    // out[j] (device) = V_j . w for j < ncols ; returns on host in g.h_host
-    void multidot(const double* V, int ncols, const double* w, double* out_dev) {
+    unsigned gr;  // elementwise grid (a few blocks per SM)
+    // partials of V_j . w for j < ncols
+    void dots(const double* V, int ncols, const double* w) {
         ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 1));
         k_multidot1<<<kRedBlocks, kRedThreads, 0, st>>>(g.n, ncols, V, w, g.partial.p);
-        k_multidot2<<<ncols, kRedThreads, 0, st>>>(kRedBlocks, ncols, g.partial.p, out_dev);
-        count_launch(2);
+        count_launch();
         PDG_CHECK_LAUNCH();
     }
-    double norm(const double* v) {
-        multidot(v, 1, v, g.norm_dev.p);
-        ProfScope prof(PROF_KRYLOV, st, 0.0);
-        k_sqrt<<<1, 1, 0, st>>>(g.norm_dev.p);
+    // one Gram-Schmidt pass: h_out = V^T w (device), w -= V h
+    void gs_pass(const double* V, int ncols, double* w, double* h_out) {
+        dots(V, ncols, w);
+        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 2));
+        k_red_multiaxpy<<<gr, kRedThreads, sizeof(double) * ncols, st>>>(g.n, ncols, g.partial.p, V, w, h_out);
         count_launch();
+        PDG_CHECK_LAUNCH();
+    }
+    // norm of v into g.norm_dev (device); dst = v / norm when dst != null
+    void norm_dev(const double* v, double* dst) {
+        dots(v, 1, v);
+        ProfScope prof(PROF_KRYLOV, st, dst ? 16.0 * (double)g.n : 0.0);
+        k_red_norm_scale<<<dst ? gr : 1, kRedThreads, 0, st>>>(g.n, g.partial.p, v, dst, g.norm_dev.p);
+        count_launch();
+        PDG_CHECK_LAUNCH();
+    }
+    // r = b - t and ||r|| on the host
+    double sub_norm(const double* b, const double* t, double* r) {
+        {
+            ProfScope prof(PROF_KRYLOV, st, 24.0 * (double)g.n);
+            k_sub_dot<<<kRedBlocks, kRedThreads, 0, st>>>(g.n, b, t, r, g.partial.p);
+            k_red_norm_scale<<<1, kRedThreads, 0, st>>>(g.n, g.partial.p, r, nullptr, g.norm_dev.p);
+            count_launch(2);
+            PDG_CHECK_LAUNCH();
+        }
+        return fetch_norm();
+    }
+    double norm(const double* v) {
+        norm_dev(v, nullptr);
+        return fetch_norm();
+    }
+    double fetch_norm() {
         PDG_CUDA(cudaMemcpyAsync(g.h_host, g.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         PDG_CUDA(cudaStreamSynchronize(st));
         return g.h_host[0];
@@ -440,7 +514,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     const long long n = rows();
     const unsigned gr = grid_for(n, 256);
     const long long launches0 = g_launches;
-    KrylovOps K{st, kr};
+    KrylovOps K{st, kr, static_cast<unsigned>(2 * num_sms())};
     PDG_CUDA(cudaEventRecord(ev0, st));
     std::vector<double> hist;
     const double bnorm = K.norm(b);
@@ -477,43 +551,40 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     std::vector<double> H;
     bool x_is_zero = true;
     while (total < max_iter) {
+        double beta;
         if (x_is_zero) {  // r = b - op(0) = b exactly
             PDG_CUDA(cudaMemcpyAsync(kr.r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            beta = K.norm(kr.r.p);
         } else {
             op.apply(kr.x.p, kr.t.p, st);
-            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_sub<<<gr, 256, 0, st>>>(n, b, kr.t.p, kr.r.p); }
-            count_launch();
+            beta = K.sub_norm(b, kr.t.p, kr.r.p);
         }
-        const double beta = K.norm(kr.r.p);
         if (beta / bnorm <= opts.tol) break;
         const int mm = std::min(restart, max_iter - total);
         H.assign((size_t)(mm + 1) * mm, 0.0);
         auto h = [&](int i, int j) -> double& { return H[(size_t)j * (mm + 1) + i]; };
-        // v_0 = r / beta
-        { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_scale_div<<<gr, 256, 0, st>>>(n, kr.r.p, kr.norm_dev.p, kr.V.p); }
-        count_launch();
+        // v_0 = r / beta (beta recomputed on the device by the same fixed tree)
+        K.norm_dev(kr.r.p, kr.V.p);
         bool done = false;
         for (int k = 0; k < mm && !done; ++k) {
             double* vk = kr.V.p + (size_t)k * n;
             double* zk = flexible ? kr.Z.p + (size_t)k * n : kr.cand.p;
             pre.apply(vk, zk, st);
             op.apply(zk, kr.w.p, st);
-            for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, two passes
-                K.multidot(kr.V.p, k + 1, kr.w.p, kr.h_dev.p);
-                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_multiaxpy<<<gr, 256, 0, st>>>(n, k + 1, kr.V.p, kr.h_dev.p, kr.w.p); }
-                count_launch();
-                PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
-                PDG_CUDA(cudaStreamSynchronize(st));
-                for (int i = 0; i <= k; ++i) h(i, k) += kr.h_host[i];
-            }
-            h(k + 1, k) = K.norm(kr.w.p);
+            // classical Gram-Schmidt, two passes, and the new norm, all on the device;
+            // the Hessenberg column comes back in ONE transfer
+            for (int pass = 0; pass < 2; ++pass) K.gs_pass(kr.V.p, k + 1, kr.w.p, kr.h_dev.p + (size_t)pass * (k + 1));
+            // h(k+1,k) = ||w|| and v_{k+1} = w / h(k+1,k) (unused when the column breaks down)
+            K.norm_dev(kr.w.p, kr.V.p + (size_t)(k + 1) * n);
+            PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * 2 * (k + 1), cudaMemcpyDeviceToHost, st));
+            PDG_CUDA(cudaMemcpyAsync(kr.h_host + 2 * (k + 1), kr.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            PDG_CUDA(cudaStreamSynchronize(st));
+            for (int pass = 0; pass < 2; ++pass)
+                for (int i = 0; i <= k; ++i) h(i, k) += kr.h_host[(size_t)pass * (k + 1) + i];
+            h(k + 1, k) = kr.h_host[2 * (k + 1)];
             double cn = 0.0;
             for (int i = 0; i <= mm; ++i) cn += h(i, k) * h(i, k);
             const bool breakdown = h(k + 1, k) <= 1e-14 * std::sqrt(cn);
-            if (!breakdown) {
-                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_scale_div<<<gr, 256, 0, st>>>(n, kr.w.p, kr.norm_dev.p, kr.V.p + (size_t)(k + 1) * n); }
-                count_launch();
-            }
             ++total;
             std::vector<double> hk((size_t)(k + 2) * (k + 1));
             for (int j = 0; j <= k; ++j)
@@ -534,9 +605,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             }
             // true residual (gmres.hpp:68-72)
             op.apply(kr.cand.p, kr.t.p, st);
-            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_sub<<<gr, 256, 0, st>>>(n, b, kr.t.p, kr.r.p); }
-            count_launch();
-            true_res = K.norm(kr.r.p);
+            true_res = K.sub_norm(b, kr.t.p, kr.r.p);
             hist.push_back(true_res);
             const bool ok = true_res / bnorm <= opts.tol;
             if (ok || breakdown || k == mm - 1 || total >= max_iter) {
