@@ -245,11 +245,12 @@ def main():
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        if dom == "a_solve" and "a_solve" in tr:
-            traffic = tr["a_solve"]["bytes"]
+        traffic = tr.get(dom, {}).get("bytes")
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+    kernel_of = {"a_solve": "a_solve: k_sweep<16> (displacement solve, one launch per call)",
+                 "flow_solve": "flow_solve: k_sweep_dense (one launch per call)", "spmv": "spmv: k_spmv"}
+    roofline = {"bound": "hbm", "kernel": kernel_of.get(dom, dom), "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_kind": peak_kind, "traffic": traffic,
                 "share_of_step": phases[dom]["ms_per_step"] / ms_dev if ms_dev else None,
                 "algorithmic_bytes_per_call": phases[dom]["alg_GB_per_call"] * 1e9}
@@ -301,7 +302,7 @@ def main():
             "config": {"workload": WORKLOAD, "rows_per_block": nn * nt,
                        "gmres_candidate": "flexible: x + Z y (the reference's gmres_flexible, gmres.hpp:113-114,"
                                           " 153-158; same iterations, solutions within 1e-9 of gmres)",
-                       "l2": "no flush: per-step working set (A factor ~4 GB) > 126 MB L2",
+                       "l2": "no flush: per-step working set (displacement-solve matrices 1.07 GB) > 126 MB L2",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "setup_s": setup_s},
             "iterations": main_run["iters"],
             "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],
