@@ -177,6 +177,18 @@ int pdg_spmv_csr_device(int rows, const long long* row_offsets_dev, const int* c
 
 /* dG(r) time constants, r <= 1 (time_matrices + real_schur, time_basis.hpp:135-182,
  * schur.hpp:101-173): nodes, weights, phi(0) [r+1], T and Q [(r+1)^2 row-major]. */
+/* local_mass_residual (slab.hpp:292-318): the discrete per-cell mass balance of
+ * one slab. rhs and state are (r+1)*n_total doubles stacked per Radau node
+ * (the slab system right-hand side and its solution, [u q p] per node);
+ * residual receives |residual| per cell (n_p), *scale the maximum over cells of
+ * the summed constituent magnitudes. Bit-identical to the reference's arithmetic.
+ * pdg_mass_residual takes host buffers, the _device variant device pointers
+ * (*scale is always a host pointer). */
+int pdg_mass_residual(pdg_ops* ops, int r, double tau, const double* rhs, const double* state, double* residual,
+                      double* scale);
+int pdg_mass_residual_device(pdg_ops* ops, int r, double tau, const double* rhs_dev, const double* state_dev,
+                             double* residual_dev, double* scale);
+
 int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q);
 
 /* Seeded workload generators (Inputs). */

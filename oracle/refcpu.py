@@ -207,6 +207,14 @@ class RefProblem:
         _check(lib().refcpu_schur_forward(self._h, r, _dp(R), _dp(out)))
         return out
 
+    def mass_residual(self, r, tau, rhs, state):
+        """local_mass_residual (slab.hpp:292-318): (|residual| per cell, scale)."""
+        out = np.empty(self.n_p)
+        sc = C.c_double()
+        _check(lib().refcpu_mass_residual(self._h, r, C.c_double(tau), _dp(np.ascontiguousarray(rhs, np.float64)),
+                                          _dp(np.ascontiguousarray(state, np.float64)), _dp(out), C.byref(sc)))
+        return out, sc.value
+
 
 def time_constants(r):
     n = r + 1

@@ -395,6 +395,26 @@ int refcpu_schur_forward(void* hp, int r, const double* R, double* shat) {
     GUARD_END
 }
 
+// local_mass_residual (slab.hpp:292-318) of a slab state: rhs and state are
+// (r+1)*n_total, stacked per Radau node; residual is n_p.
+int refcpu_mass_residual(void* hp, int r, double tau, const double* rhs, const double* state, double* residual,
+                         double* scale) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const TimeBasis basis = time_matrices(r);
+    const int n = basis.n_nodes(), nt = h->ops.n_total();
+    std::vector<Vec> R(n);
+    std::vector<const double*> comps(n);
+    for (int i = 0; i < n; ++i) {
+        R[i].assign(rhs + (long long)i * nt, rhs + (long long)(i + 1) * nt);
+        comps[i] = state + (long long)i * nt;
+    }
+    const MassResidual mr = local_mass_residual(h->ops, basis, tau, R, comps);
+    std::copy(mr.residual.begin(), mr.residual.end(), residual);
+    *scale = mr.scale;
+    GUARD_END
+}
+
 // Seeded generators:
 //   uniform x_i = -1 + 2 * ((mt19937_64() >> 11) * 2^-53)
 //   normal z = sqrt(-2 ln u1) cos(2 pi u2), u1 = ((g>>11)+1) 2^-53, u2 = (g>>11) 2^-53

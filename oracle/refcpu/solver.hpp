@@ -486,6 +486,48 @@ inline SlabSystem build_slab_system(const SpatialOperators& ops, const TimeBasis
     return sys;
 }
 
+// slab.hpp:283-318 : discrete local mass balance of a converged slab. For
+// each cell: sum over the time test functions i of
+//   storage_i = sum_j G_hat(i,j) D(u_j, p_j)   (j ascending, zero entries skipped)
+//   flux_i    = (tau w_i) B^T q_i
+//   src_i     = p-rows of rhs_i
+// residual += (storage + flux) - src, scale += (|storage| + |flux|) + |src|;
+// returns |residual| per cell and scale = max over cells.
+struct MassResidual {
+    Vec residual;
+    double scale = 0.0;
+};
+inline MassResidual local_mass_residual(const SpatialOperators& ops, const TimeBasis& basis, double tau,
+                                        const std::vector<Vec>& rhs, const std::vector<const double*>& comps) {
+    const int n = basis.n_nodes(), np = ops.n_p, nu = ops.n_u, nq = ops.n_q;
+    std::vector<Vec> dp(n), kp(n);
+    for (int j = 0; j < n; ++j) {
+        dp[j] = apply_time_derivative_p(ops, comps[j], comps[j] + nu + nq);
+        kp[j] = ops.B.apply_transpose(Vec(comps[j] + nu, comps[j] + nu + nq));
+    }
+    MassResidual out;
+    out.residual.assign(np, 0.0);
+    Vec scale(np, 0.0);
+    for (int i = 0; i < n; ++i) {
+        Vec storage(np, 0.0);
+        for (int j = 0; j < n; ++j) {
+            const double g = basis.G_hat[i * n + j];
+            if (g != 0.0)
+                for (int c = 0; c < np; ++c) storage[c] += g * dp[j][c];
+        }
+        const double s = tau * basis.weights[i];
+        for (int c = 0; c < np; ++c) {
+            const double flux = s * kp[i][c];
+            const double src = rhs[i][nu + nq + c];
+            out.residual[c] += (storage[c] + flux) - src;
+            scale[c] += (std::fabs(storage[c]) + std::fabs(flux)) + std::fabs(src);
+        }
+    }
+    for (double& v : out.residual) v = std::fabs(v);
+    for (double v : scale) out.scale = std::max(out.scale, v);
+    return out;
+}
+
 struct BlockReport {
     int block_index = 0, block_size = 1, gmres_iterations = 0, fs_sweeps = 0;
     SolverReport report;

@@ -96,6 +96,8 @@ _SIGS = {
     "pdg_profile_enable": (None, [C.c_int]),
     "pdg_profile_reset": (None, []),
     "pdg_profile_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), LLP, C.POINTER(C.c_double)]),
+    "pdg_mass_residual": (C.c_int, [VP, C.c_int, C.c_double, DP, DP, DP, DP]),
+    "pdg_mass_residual_device": (C.c_int, [VP, C.c_int, C.c_double, VP, VP, VP, DP]),
     "pdg_time_constants": (C.c_int, [C.c_int, DP, DP, DP, DP, DP]),
     "pdg_debug_recurrence_timing": (C.c_int, [VP, C.c_int, C.POINTER(C.c_ulonglong), C.c_longlong, IP, IP]),
     "pdg_util_uniform": (None, [C.c_ulonglong, C.c_longlong, DP]),

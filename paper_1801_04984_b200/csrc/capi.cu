@@ -56,6 +56,13 @@ struct pdg_slab {
 
 namespace {
 
+inline double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+
 __global__ void k_schur_fwd(int nn, long long nt, const double* Q, const double* w, const double* R, double* shat) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn * nt; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / nt);
@@ -75,12 +82,20 @@ __global__ void k_schur_bwd(int nn, long long nt, const double* Q, const double*
     }
 }
 // djump = (-b) E^T u - (1/M) (m_p p)   (assembly.hpp:409-413)
+// D(u,p)_c = (-b) (E^T u)_c - (1/M) (m_p,c p_c)   (assembly.hpp:409-413); E^T u summed
+// in ascending row order of E from 0.0 like SparseMatrix::apply_transpose
+// (sparse.hpp:43-50), no FMA: bit-identical to the reference's arithmetic.
+__device__ __forceinline__ double time_derivative_p(int c, double mb, double im, const int* et_off, const int* et_idx,
+                                                    const double* et_val, const double* m_p, const double* u,
+                                                    const double* p) {
+    double s = 0.0;
+    for (int k = et_off[c]; k < et_off[c + 1]; ++k) s = __dadd_rn(s, __dmul_rn(et_val[k], u[et_idx[k]]));
+    return __dsub_rn(__dmul_rn(mb, s), __dmul_rn(im, __dmul_rn(m_p[c], p[c])));
+}
 __global__ void k_time_derivative(int np, double mb, double im, const int* et_off, const int* et_idx, const double* et_val,
                                   const double* m_p, const double* u, const double* p, double* out) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int k = et_off[c]; k < et_off[c + 1]; ++k) s += et_val[k] * u[et_idx[k]];
-        out[c] = mb * s - im * (m_p[c] * p[c]);
+        out[c] = time_derivative_p(c, mb, im, et_off, et_idx, et_val, m_p, u, p);
     }
 }
 // R_i = (tau w_i) [u;q;p]_i + phi0_i djump (p rows)   (slab.hpp:76-84)
@@ -90,15 +105,54 @@ __global__ void k_slab_rhs(int nn, int nu, int nq, int np, double tau, const dou
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn * nt; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / nt);
         const long long k = t % nt;
-        const double s = tau * w[i];
+        const double s = __dmul_rn(tau, w[i]);
         double v;
         if (k < nu)
-            v = s * ru[(long long)i * nu + k];
+            v = __dmul_rn(s, ru[(long long)i * nu + k]);
         else if (k < nu + nq)
-            v = s * rq[(long long)i * nq + (k - nu)];
+            v = __dmul_rn(s, rq[(long long)i * nq + (k - nu)]);
         else
-            v = s * rp[(long long)i * np + (k - nu - nq)] + phi0[i] * djump[k - nu - nq];
+            v = __dadd_rn(__dmul_rn(s, rp[(long long)i * np + (k - nu - nq)]), __dmul_rn(phi0[i], djump[k - nu - nq]));
         R[t] = v;
+    }
+}
+
+// local_mass_residual (slab.hpp:292-318), one thread per cell: for each time
+// test function i, storage = sum_j G(i,j) D(u_j,p_j) (j ascending, zero entries
+// skipped), flux = (tau w_i) (B^T q_i), src = p-rows of rhs_i;
+// res += (storage + flux) - src, scale += (|storage| + |flux|) + |src|.
+// Writes |res| per cell; the scale maximum is an order-free atomic max on the
+// (non-negative) double bits. Same operation order as the reference, no FMA.
+constexpr int kMaxNodes = 4;
+__global__ void k_mass_residual(int np, int nu, int nq, int n, const double* __restrict__ G, const double* __restrict__ w,
+                                double tau, double mb, double im, const double* __restrict__ m_p, const int* et_off,
+                                const int* et_idx, const double* et_val, const int* bt_off, const int* bt_idx,
+                                const double* bt_val, const double* __restrict__ rhs, const double* __restrict__ state,
+                                double* __restrict__ residual, unsigned long long* scale_bits) {
+    const long long nt = (long long)nu + nq + np;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
+        double dp[kMaxNodes], kp[kMaxNodes];
+        for (int j = 0; j < n; ++j) {
+            const double* x = state + j * nt;
+            dp[j] = time_derivative_p(c, mb, im, et_off, et_idx, et_val, m_p, x, x + nu + nq);
+            double s = 0.0;
+            for (int k = bt_off[c]; k < bt_off[c + 1]; ++k) s = __dadd_rn(s, __dmul_rn(bt_val[k], x[nu + bt_idx[k]]));
+            kp[j] = s;
+        }
+        double res = 0.0, sc = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double storage = 0.0;
+            for (int j = 0; j < n; ++j) {
+                const double g = G[i * n + j];
+                if (g != 0.0) storage = __dadd_rn(storage, __dmul_rn(g, dp[j]));
+            }
+            const double flux = __dmul_rn(__dmul_rn(tau, w[i]), kp[i]);
+            const double src = rhs[i * nt + nu + nq + c];
+            res = __dadd_rn(res, __dsub_rn(__dadd_rn(storage, flux), src));
+            sc = __dadd_rn(sc, __dadd_rn(__dadd_rn(fabs(storage), fabs(flux)), fabs(src)));
+        }
+        residual[c] = fabs(res);
+        atomicMax(scale_bits, static_cast<unsigned long long>(__double_as_longlong(sc)));
     }
 }
 
@@ -497,6 +551,51 @@ int pdg_spmv_csr_device(int rows, const long long* off, const int* idx, const do
     API_BEGIN
     spmv_csr_device(rows, off, idx, val, x, y, 0);
     PDG_CUDA(cudaStreamSynchronize(0));
+    API_END
+}
+
+int pdg_mass_residual_device(pdg_ops* ops, int r, double tau, const double* rhs_dev, const double* state_dev,
+                             double* residual_dev, double* scale) {
+    API_BEGIN
+    require(ops && rhs_dev && state_dev && residual_dev && scale, "pdg_mass_residual: null argument");
+    require(r >= 0 && r + 1 <= kMaxNodes, "pdg_mass_residual: unsupported dG degree");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
+    const SpatialOps& o = ops->s;
+    cudaStream_t st = o.ctx->stream;
+    const TimeConsts tc = time_consts(r);
+    DBuf<double> g, w;
+    g.upload(tc.G, st);
+    w.upload(tc.weights, st);
+    DBuf<unsigned long long> sb(1);
+    sb.zero(st);
+    ProfScope prof(PROF_SLAB, st, 8.0 * 2 * tc.n * o.n_total());
+    k_mass_residual<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, o.n_u, o.n_q, tc.n, g.p, w.p, tau, -o.biot_b, o.inv_m,
+                                                           o.m_p.p, o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.Bt.off.p,
+                                                           o.Bt.idx.p, o.Bt.val.p, rhs_dev, state_dev, residual_dev, sb.p);
+    count_launch();
+    PDG_CHECK_LAUNCH();
+    unsigned long long bits = 0;
+    PDG_CUDA(cudaMemcpyAsync(&bits, sb.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    *scale = bits_to_double(bits);
+    API_END
+}
+
+int pdg_mass_residual(pdg_ops* ops, int r, double tau, const double* rhs, const double* state, double* residual,
+                      double* scale) {
+    API_BEGIN
+    require(ops && rhs && state && residual && scale, "pdg_mass_residual: null argument");
+    require(r >= 0 && r + 1 <= kMaxNodes, "pdg_mass_residual: unsupported dG degree");
+    const SpatialOps& o = ops->s;
+    cudaStream_t st = o.ctx->stream;
+    const size_t len = (size_t)(r + 1) * o.n_total();
+    DBuf<double> drhs, dstate, dres(o.n_p);
+    drhs.upload(rhs, len, st);
+    dstate.upload(state, len, st);
+    const int rc = pdg_mass_residual_device(ops, r, tau, drhs.p, dstate.p, dres.p, scale);
+    if (rc != PDG_OK) return rc;
+    PDG_CUDA(cudaMemcpyAsync(residual, dres.p, sizeof(double) * o.n_p, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
     API_END
 }
 

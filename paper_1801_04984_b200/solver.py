@@ -79,6 +79,7 @@ class SolverReport:
     residual_history: np.ndarray
     device_ms: float
     kernel_launches: int
+    mass_rel: float | None = None  # max per-cell local mass residual / scale (march(..., mass_check=True))
 
 
 def _report(cap):
@@ -212,6 +213,19 @@ class SpatialOperators:
         check(lib().pdg_ops_rhs(self._h, t, _dp(u), _dp(q), _dp(p)))
         return u, q, p
 
+    def mass_residual(self, r, tau, rhs, state):
+        """local_mass_residual (slab.hpp:292-318) of one slab on the GPU: rhs and
+        state are (r+1, n_total) (slab right-hand side and solution per Radau
+        node). Returns (|residual| per cell, scale)."""
+        rhs = np.ascontiguousarray(rhs, np.float64).reshape(-1)
+        state = np.ascontiguousarray(state, np.float64).reshape(-1)
+        if rhs.size != (r + 1) * self.n_total or state.size != (r + 1) * self.n_total:
+            raise InvalidArgument("mass_residual: rhs/state must hold (r+1)*n_total values")
+        res = np.empty(self.n_p)
+        sc = C.c_double()
+        check(lib().pdg_mass_residual(self._h, r, tau, _dp(rhs), _dp(state), _dp(res), C.byref(sc)))
+        return res, sc.value
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib._lib is not None:
             _lib._lib.pdg_ops_destroy(self._h)
@@ -310,6 +324,14 @@ class SlabSolver:
     def rhs_device(self, t0: float, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int):
         check(lib().pdg_slab_rhs_device(self._h, t0, u_prev_ptr, p_prev_ptr, rhs_ptr))
 
+    def mass_residual_device(self, rhs_ptr: int, state_ptr: int, residual_ptr: int) -> float:
+        """local_mass_residual (slab.hpp:292-318) of a device slab system/state
+        into residual_ptr (n_p doubles); returns the scale."""
+        sc = C.c_double()
+        check(lib().pdg_mass_residual_device(self.ops._h, self.r, self.tau, rhs_ptr, state_ptr, residual_ptr,
+                                             C.byref(sc)))
+        return sc.value
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib._lib is not None:
             _lib._lib.pdg_slab_destroy(self._h)
@@ -317,10 +339,12 @@ class SlabSolver:
 
 
 def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptions | None = None,
-          keep_states: bool = False):
+          keep_states: bool = False, mass_check: bool = False):
     """Monolithic-spectral march (march.hpp:45-79,109-117) with a device-resident
     slab loop: the slab right-hand side, the Schur transforms and the jump data
-    never leave the GPU. Returns per-slab reports (and states if asked)."""
+    never leave the GPU. Returns per-slab reports (and states if asked). With
+    mass_check, each report carries the slab's local mass balance
+    max_c |residual_c| / scale (slab.hpp:292-318, computed on the device)."""
     import torch
 
     opt = opt or SolveOptions()
@@ -341,6 +365,10 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
             rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
         except SolverError as e:
             raise SolverError(e.status, f"slab {n} (t_n = {T * (n + 1) / n_slabs:f}): {e}") from None
+        if mass_check:
+            res = torch.empty(ops.n_p, dtype=torch.float64, device=dev)
+            scale = slab.mass_residual_device(rhs.data_ptr(), out.data_ptr(), res.data_ptr())
+            rep.mass_rel = float(res.max().item()) / scale if scale > 0.0 else 0.0
         reports.append(rep)
         end = out[r * nt:(r + 1) * nt]
         u_prev.copy_(end[:ops.n_u])

@@ -114,3 +114,47 @@ def test_time_constants_closed_forms(oracle):
     np.testing.assert_allclose(t["G_hat"], [[9 / 8, 3 / 8], [-9 / 8, 5 / 8]], atol=1e-13)
     T = t["T"]
     assert abs(T[0, 0] - T[1, 1]) < 1e-12 and abs(T[0, 1] * T[1, 0] + 2.0) < 1e-12
+
+
+def _slab_rhs_sequence(rp, r, tau, states, u0=None, p0=None):
+    """The slab right-hand sides of a march (slab.hpp:58-87): slab n uses the end
+    trace of slab n-1 as jump data (march.hpp:110-112)."""
+    nu, nq = rp.n_u, rp.n_q
+    u_prev = np.zeros(nu) if u0 is None else u0
+    p_prev = np.zeros(rp.n_p) if p0 is None else p0
+    out = []
+    for n in range(len(states)):
+        out.append(rp.slab_rhs(r, n * tau, tau, u_prev, p_prev))
+        end = np.asarray(states[n]).reshape(r + 1, -1)[r]
+        u_prev, p_prev = end[:nu], end[nu + nq:]
+    return out
+
+
+def test_oracle_mass_residual_zero_state(oracle):
+    """MassConservation.ZeroSolutionZeroResidual (test_coupling.cpp:417-432)."""
+    rp = oracle.RefProblem(P.config0().to_dict())
+    res, scale = rp.mass_residual(0, 0.1, np.zeros(rp.n_total), np.zeros(rp.n_total))
+    assert res.max() == 0.0 and scale == 0.0
+
+
+def terzaghi_column(ny=32):
+    """acceptance.cpp terzaghi_column(ny): the "terzaghi" preset (problems.hpp:220-240),
+    nx = 1, square cells."""
+    spec = P.terzaghi_recorded()
+    spec.ny, spec.lx = ny, 1.0 / ny
+    return spec
+
+
+@pytest.mark.parametrize("r", [0, 1])
+def test_oracle_mass_conservation_converged(oracle, r):
+    """MassConservation.ConvergedSlabBalancesLocally (test_coupling.cpp:434-469)
+    and acceptance criterion 7 (acceptance.cpp:347-355, the Terzaghi column): a
+    slab solved to tight tolerance balances mass per cell to <= 1e-10 x scale."""
+    rp = oracle.RefProblem(terzaghi_column().to_dict())
+    tau = 0.02
+    run = rp.march(r, 3 * tau, 3, tol=1e-12, restart=100, keep_states=True)
+    rhs = _slab_rhs_sequence(rp, r, tau, run["states"])
+    for n in range(3):
+        res, scale = rp.mass_residual(r, tau, rhs[n], run["states"][n])
+        assert scale > 0.0
+        assert res.max() <= 1e-10 * scale, (n, res.max() / scale)
