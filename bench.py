@@ -193,7 +193,11 @@ def main():
         rhs_host = []
 
         def step(n, keep=False):
-            slab.rhs_device(tau * n, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+            # slab n of the uniform partition (time_basis.hpp:33-40, extended past T when
+            # W + K > n_slabs): its own start and length, as the reference's march uses them
+            t0 = run["T"] * n / run["n_slabs"]
+            t1 = run["T"] * (n + 1) / run["n_slabs"]
+            slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=t1 - t0)
             if keep:
                 rhs_host.append(rhs.cpu().pin_memory().numpy())
             rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())

@@ -167,8 +167,11 @@ int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts,
 int pdg_slab_solve(pdg_slab* slab, const double* rhs, double* out, pdg_report* rep);
 int pdg_slab_solve_device(pdg_slab* slab, const double* rhs_dev, double* out_dev, pdg_report* rep);
 /* Slab right-hand side (build_slab_system, slab.hpp:58-87) on the device: jump data u_prev/p_prev
- * (device), slab start t0 -> rhs_dev ((r+1) * n_total). */
-int pdg_slab_rhs_device(pdg_slab* slab, double t0, const double* u_prev_dev, const double* p_prev_dev, double* rhs_dev);
+ * (device), slab start t0 and length tau (the slab's own length, march.hpp:63-64; it may differ in
+ * the last bits from the tau the solver was built with, as in the reference) -> rhs_dev
+ * ((r+1) * n_total). */
+int pdg_slab_rhs_device(pdg_slab* slab, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
+                        double* rhs_dev);
 void pdg_slab_destroy(pdg_slab* slab);
 
 /* Order-fixed CSR SpMV (SparseMatrix::apply) on device buffers. */

@@ -85,7 +85,7 @@ _SIGS = {
     "pdg_slab_create": (C.c_int, [VP, C.c_int, C.c_double, C.POINTER(GmresOpts), C.POINTER(VP)]),
     "pdg_slab_solve": (C.c_int, [VP, DP, DP, C.POINTER(Report)]),
     "pdg_slab_solve_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
-    "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_destroy": (None, [VP]),
     "pdg_spmv_csr_device": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_op_create": (C.c_int, [VP, C.c_int, DP, C.c_double, C.POINTER(VP)]),

@@ -518,9 +518,11 @@ int pdg_slab_solve(pdg_slab* s, const double* rhs, double* out, pdg_report* rep)
     API_END
 }
 
-int pdg_slab_rhs_device(pdg_slab* s, double t0, const double* u_prev_dev, const double* p_prev_dev, double* rhs_dev) {
+int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
+                        double* rhs_dev) {
     API_BEGIN
     require(s && u_prev_dev && p_prev_dev && rhs_dev, "pdg_slab_rhs_device: null argument");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
     const SpatialOps& o = s->ops->s;
     require(o.has_problem, "pdg_slab_rhs_device: operators were uploaded without a problem description");
     cudaStream_t st = o.ctx->stream;
@@ -533,11 +535,11 @@ int pdg_slab_rhs_device(pdg_slab* s, double t0, const double* u_prev_dev, const 
     }
     ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * o.n_total());
     for (int i = 0; i < nn; ++i)
-        assemble_rhs_device(o, t0 + s->tc.nodes[i] * s->tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
+        assemble_rhs_device(o, t0 + s->tc.nodes[i] * tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
                             s->rhs_p.p + (size_t)i * o.n_p, st);
     k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
                                                              o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
-    k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, s->tau, s->d_w.p,
+    k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, tau, s->d_w.p,
                                                                            s->d_phi0.p, s->rhs_u.p, s->rhs_q.p,
                                                                            s->rhs_p.p, s->djump.p, rhs_dev);
     count_launch(2);

@@ -321,21 +321,34 @@ class SlabSolver:
         check(lib().pdg_slab_solve_device(self._h, rhs_ptr, out_ptr, C.byref(rep)))
         return _to_report(rep, hist)
 
-    def rhs_device(self, t0: float, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int):
-        check(lib().pdg_slab_rhs_device(self._h, t0, u_prev_ptr, p_prev_ptr, rhs_ptr))
+    def rhs_device(self, t0: float, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int, tau: float | None = None):
+        """build_slab_system on the device for the slab [t0, t0 + tau] (tau defaults
+        to the solver's)."""
+        check(lib().pdg_slab_rhs_device(self._h, t0, self.tau if tau is None else tau, u_prev_ptr, p_prev_ptr,
+                                        rhs_ptr))
 
-    def mass_residual_device(self, rhs_ptr: int, state_ptr: int, residual_ptr: int) -> float:
+    def mass_residual_device(self, rhs_ptr: int, state_ptr: int, residual_ptr: int, tau: float | None = None) -> float:
         """local_mass_residual (slab.hpp:292-318) of a device slab system/state
-        into residual_ptr (n_p doubles); returns the scale."""
+        (slab length tau, default the solver's) into residual_ptr (n_p doubles);
+        returns the scale."""
         sc = C.c_double()
-        check(lib().pdg_mass_residual_device(self.ops._h, self.r, self.tau, rhs_ptr, state_ptr, residual_ptr,
-                                             C.byref(sc)))
+        check(lib().pdg_mass_residual_device(self.ops._h, self.r, self.tau if tau is None else tau, rhs_ptr,
+                                             state_ptr, residual_ptr, C.byref(sc)))
         return sc.value
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib._lib is not None:
             _lib._lib.pdg_slab_destroy(self._h)
             self._h = None
+
+
+def uniform_partition(T: float, n_slabs: int):
+    """TimePartition t_points of uniform_partition (time_basis.hpp:33-40): T*n/N, last = T."""
+    if not T > 0.0 or n_slabs < 1:
+        raise InvalidArgument("uniform_partition: bad arguments")
+    pts = [T * n / n_slabs for n in range(n_slabs + 1)]
+    pts[-1] = T
+    return pts
 
 
 def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptions | None = None,
@@ -348,8 +361,8 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
     import torch
 
     opt = opt or SolveOptions()
-    tau = T / n_slabs
-    slab = SlabSolver(ops, r, tau, opt)
+    t_points = uniform_partition(T, n_slabs)
+    slab, cached_tau = None, -1.0
     nt = ops.n_total
     dev = torch.device("cuda")
     u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
@@ -358,16 +371,21 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
     out = torch.empty_like(rhs)
     reports, states = [], []
     for n in range(n_slabs):
-        t0 = T * n / n_slabs
+        # the slab's own length and start (march.hpp:63-64); the solver is rebuilt
+        # only when tau changes by more than 1e-12 tau (march.hpp:72)
+        tau, t0 = t_points[n + 1] - t_points[n], t_points[n]
+        if slab is None or abs(tau - cached_tau) > 1e-12 * tau:
+            slab = SlabSolver(ops, r, tau, opt)
+        cached_tau = tau
         torch.cuda.synchronize()
-        slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+        slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=tau)
         try:
             rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
         except SolverError as e:
-            raise SolverError(e.status, f"slab {n} (t_n = {T * (n + 1) / n_slabs:f}): {e}") from None
+            raise SolverError(e.status, f"slab {n} (t_n = {t_points[n + 1]:f}): {e}") from None
         if mass_check:
             res = torch.empty(ops.n_p, dtype=torch.float64, device=dev)
-            scale = slab.mass_residual_device(rhs.data_ptr(), out.data_ptr(), res.data_ptr())
+            scale = slab.mass_residual_device(rhs.data_ptr(), out.data_ptr(), res.data_ptr(), tau=tau)
             rep.mass_rel = float(res.max().item()) / scale if scale > 0.0 else 0.0
         reports.append(rep)
         end = out[r * nt:(r + 1) * nt]

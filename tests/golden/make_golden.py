@@ -2,7 +2,9 @@
 
 reference_iterations.json  -- the reference's own recorded run
                               (/root/reference/proj/out/iterations.csv),
-                              parsed into numbers; the oracle must reproduce it.
+                              parsed into numbers plus its raw lines (the
+                              iteration-log schema, csv.hpp:56-71); the oracle
+                              must reproduce it.
 config1_k_perm.npy         -- per-cell permeability of config 1 (seed 1801),
                               from the oracle's generator.
 config0_oracle.npz         -- oracle march of config 0 (dense inner solves):
@@ -32,7 +34,8 @@ def main():
                    slab_index=[int(r["slab_index"]) for r in rows], t_n=[float(r["t_n"]) for r in rows],
                    gmres_iterations=[int(r["gmres_iterations"]) for r in rows],
                    fs_sweeps=[int(r["fs_sweeps"]) for r in rows],
-                   final_residual=[float(r["final_residual"]) for r in rows])
+                   final_residual=[float(r["final_residual"]) for r in rows],
+                   lines=open(ref_csv).read().splitlines())
         json.dump(out, open(os.path.join(HERE, "reference_iterations.json"), "w"), indent=1)
     k = refcpu.lognormal(P.K_SEED, 128 * 128, 1.0)
     np.save(os.path.join(HERE, "config1_k_perm.npy"), k)

@@ -327,3 +327,30 @@ def test_slab_rhs_device_bit_identical(oracle, r):
     slab.rhs_device(t0, u.data_ptr(), p.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), rp.slab_rhs(r, t0, tau, u_prev, p_prev))
+    # a slab whose own length differs from the solver's in the last bits (march.hpp:63-72)
+    tau2 = 0.30000000000000004 - 0.25
+    slab.rhs_device(0.25, u.data_ptr(), p.data_ptr(), out.data_ptr(), tau=tau2)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), rp.slab_rhs(r, 0.25, tau2, u_prev, p_prev))
+
+
+def test_iteration_log_from_gpu_march():
+    """The GPU march's iteration log (csv.hpp:56-71 schema) against the
+    reference's recorded proj/out/iterations.csv: identical fields, logged
+    residuals to the log's precision band; the driver line format."""
+    from paper_1801_04984_b200 import runlog
+
+    ref = json.load(open(os.path.join(GOLDEN, "reference_iterations.json")))
+    spec = P.terzaghi_recorded()
+    run = P.RUNS["terzaghi_recorded"]
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]))
+    reps, _ = S.march(ops, run["r"], run["T"], run["n_slabs"], opt)
+    t_points = S.uniform_partition(run["T"], run["n_slabs"])
+    lines = runlog.iteration_log_lines(reps, t_points, run["r"])
+    assert lines[0] == ref["lines"][0] and len(lines) == len(ref["lines"])
+    for a, b in zip(lines[1:], ref["lines"][1:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[:6] == fb[:6], (a, b)
+        assert abs(float(fa[6]) - float(fb[6])) <= 1e-3 * float(fb[6]), (a, b)
+    assert runlog.slab_line(9, t_points[10], reps[9], run["r"]).startswith("slab    9  t_n=0.2          method=")

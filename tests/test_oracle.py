@@ -158,3 +158,33 @@ def test_oracle_mass_conservation_converged(oracle, r):
         res, scale = rp.mass_residual(r, tau, rhs[n], run["states"][n])
         assert scale > 0.0
         assert res.max() <= 1e-10 * scale, (n, res.max() / scale)
+
+
+def _compare_logs(lines, ref_lines, res_rtol):
+    assert lines[0] == ref_lines[0]  # schema (csv.hpp:60)
+    assert len(lines) == len(ref_lines)
+    for a, b in zip(lines[1:], ref_lines[1:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[:6] == fb[:6], (a, b)  # slab, t_n text, block, type, iterations, sweeps
+        assert abs(float(fa[6]) - float(fb[6])) <= res_rtol * float(fb[6]), (a, b)
+
+
+def test_iteration_log_schema_reproduces_reference(oracle):
+    """write_iteration_log (csv.hpp:56-71) restated in the host mirror: fed with
+    the oracle's march of the recorded run, it reproduces proj/out/iterations.csv
+    field for field (residuals to the 5e-6 the oracle matches them to)."""
+    from types import SimpleNamespace
+
+    from paper_1801_04984_b200 import runlog, solver as S
+
+    ref = json.load(open(os.path.join(GOLDEN, "reference_iterations.json")))
+    spec = P.terzaghi_recorded()
+    run = P.RUNS["terzaghi_recorded"]
+    rp = oracle.RefProblem(spec.to_dict())
+    res = rp.march(run["r"], run["T"], run["n_slabs"], tol=run["tol"], restart=run["restart"])
+    reps = [SimpleNamespace(iterations=int(i), final_relative_residual=float(f))
+            for i, f in zip(res["iterations"], res["final_res"])]
+    t_points = S.uniform_partition(run["T"], run["n_slabs"])
+    _compare_logs(runlog.iteration_log_lines(reps, t_points, run["r"]), ref["lines"], 1e-5)
+    line = runlog.slab_line(0, t_points[1], reps[0], run["r"])
+    assert line.startswith("slab    0  t_n=0.02         method=monolithic-spectral iters=7 res=7.69")
