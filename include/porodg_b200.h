@@ -180,6 +180,24 @@ int pdg_spmv_csr_device(int rows, const long long* row_offsets_dev, const int* c
 
 /* dG(r) time constants, r <= 1 (time_matrices + real_schur, time_basis.hpp:135-182,
  * schur.hpp:101-173): nodes, weights, phi(0) [r+1], T and Q [(r+1)^2 row-major]. */
+/* Fixed-stress solver of the fixed-stress march (FixedStressSolver::solve,
+ * fixed_stress.hpp:144-172, as built at march.hpp:83-84: Theta = G_hat, kappa =
+ * the Radau weights): sweeps on the untransformed slab block from x0 (null =
+ * zero) until ||rhs - A x|| <= tol ||rhs||; rep->iterations = sweeps
+ * (BlockReport::fs_sweeps). Fails with PDG_NOT_CONVERGED and the reference's
+ * text "fixed-stress did not converge (rel res ...)". Device path: dG(0). */
+typedef struct pdg_fs pdg_fs;
+typedef struct {
+    double tol;     /* FixedStressConfig::tol (default 1e-10) */
+    int max_sweeps; /* FixedStressConfig::max_sweeps (default 200) */
+    double stab;    /* < 0: b^2 / K_dr */
+} pdg_fs_opts;
+int pdg_fs_create(pdg_ops* ops, int r, double tau, const pdg_fs_opts* opts, pdg_fs** out);
+/* rhs, x0, x: (r+1) * n_total stacked per Radau node (host buffers / device pointers) */
+int pdg_fs_solve(pdg_fs* fs, const double* rhs, const double* x0, double* x, pdg_report* rep);
+int pdg_fs_solve_device(pdg_fs* fs, const double* rhs_dev, const double* x0_dev, double* x_dev, pdg_report* rep);
+void pdg_fs_destroy(pdg_fs* fs);
+
 /* local_mass_residual (slab.hpp:292-318): the discrete per-cell mass balance of
  * one slab. rhs and state are (r+1)*n_total doubles stacked per Radau node
  * (the slab system right-hand side and its solution, [u q p] per node);

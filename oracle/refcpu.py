@@ -194,6 +194,20 @@ class RefProblem:
         return dict(iterations=its[:run], final_res=res[:run], solve_seconds=secs[:run],
                     setup_seconds=setup.value, end_state=end, states=states)
 
+    def march_fs(self, r, T, n_slabs, tol=1e-10, max_sweeps=200, stab=-1.0, backend=0, keep_states=False,
+                 max_slabs=0):
+        """Fixed-stress march (march.hpp:80-108): per-slab sweep counts and final
+        relative residuals (and all slab states)."""
+        run = n_slabs if max_slabs <= 0 else min(max_slabs, n_slabs)
+        sw = np.zeros(n_slabs, np.int32)
+        res = np.zeros(n_slabs)
+        secs = np.zeros(n_slabs)
+        states = np.empty((run, r + 1, self.n_total)) if keep_states else None
+        _check(lib().refcpu_march_fs(self._h, r, C.c_double(T), n_slabs, C.c_double(tol), max_sweeps,
+                                     C.c_double(stab), backend, _ip(sw), _dp(res), _dp(secs),
+                                     _dp(states) if keep_states else None, max_slabs))
+        return dict(sweeps=sw[:run], final_res=res[:run], solve_seconds=secs[:run], states=states)
+
     def slab_rhs(self, r, t0, tau, u_prev, p_prev):
         out = np.empty((r + 1) * self.n_total)
         _check(lib().refcpu_slab_rhs(self._h, r, C.c_double(t0), C.c_double(tau),

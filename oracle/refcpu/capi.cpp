@@ -364,6 +364,74 @@ int refcpu_march(void* hp, int r, double T, int n_slabs, const refcpu_solve_opts
     GUARD_END
 }
 
+// Fixed-stress march (march.hpp:80-108): per slab, FixedStressSolver(ops,
+// G_hat, weights, tau, stab) iterated to tol on the untransformed slab block
+// (fixed_stress.hpp:144-172), warm-started from the previous end trace in every
+// component (march.hpp:87-93); rebuilt only when tau changes (march.hpp:72).
+// sweeps[n] = BlockReport::fs_sweeps of slab n; states as refcpu_march.
+int refcpu_march_fs(void* hp, int r, double T, int n_slabs, double tol, int max_sweeps, double stab, int backend,
+                    int* sweeps, double* final_res, double* solve_seconds, double* states, int max_slabs) {
+    using clk = std::chrono::steady_clock;
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const SpatialOperators& ops = h->ops;
+    const TimePartition part = uniform_partition(T, n_slabs);
+    const TimeBasis basis = time_matrices(r);
+    const int nn = basis.n_nodes(), nt = ops.n_total();
+    FixedStressConfig cfg;
+    cfg.tol = tol;
+    cfg.max_sweeps = max_sweeps;
+    cfg.stab = stab;
+    if (!(cfg.tol > 0.0 && cfg.tol < 1.0)) throw std::invalid_argument("fixed-stress: tol must be in (0,1)");
+    if (cfg.max_sweeps < 1) throw std::invalid_argument("fixed-stress: sweep counts must be >= 1");
+    const double st = cfg.resolve_stab(ops.mat);
+    const InnerBackend be = backend ? InnerBackend::banded : InnerBackend::dense;
+    std::shared_ptr<InnerSolver> a = make_a_solver(ops, be);
+    Vec u_prev(ops.n_u, 0.0), p_prev(ops.n_p, 0.0), trace_prev;
+    std::unique_ptr<FixedStressSolver> fs;
+    double cached_tau = -1.0;
+    const int run = max_slabs > 0 ? std::min(max_slabs, part.n_slabs()) : part.n_slabs();
+    for (int n = 0; n < run; ++n) {
+        const double tau = part.slab_length(n), t0 = part.t_begin(n);
+        std::vector<FieldVecs> nodal(nn);
+        for (int i = 0; i < nn; ++i)
+            nodal[i] = assemble_rhs(h->mesh, h->dofs, ops.mat, ops, h->data, t0 + basis.nodes[i] * tau);
+        const SlabSystem sys = build_slab_system(ops, basis, tau, nodal, u_prev, p_prev);
+        const bool rebuild = cached_tau < 0.0 || std::abs(tau - cached_tau) > 1e-12 * tau;
+        try {
+            if (rebuild)
+                fs = std::make_unique<FixedStressSolver>(ops, basis.G_hat, nn, tau, st, a, be, h->mesh.nx, h->mesh.ny,
+                                                         basis.weights);
+            Vec rhs(static_cast<size_t>(nn) * nt);
+            for (int i = 0; i < nn; ++i) std::copy(sys.rhs[i].begin(), sys.rhs[i].end(), rhs.begin() + i * nt);
+            Vec x0;
+            if (!trace_prev.empty()) {
+                x0.resize(rhs.size());
+                for (int i = 0; i < nn; ++i) std::copy(trace_prev.begin(), trace_prev.end(), x0.begin() + i * nt);
+            }
+            SolverReport rep;
+            const auto a0 = clk::now();
+            const Vec x = fs->solve(rhs, cfg, x0, rep);
+            if (solve_seconds) solve_seconds[n] = std::chrono::duration<double>(clk::now() - a0).count();
+            if (!rep.converged)
+                throw SolverError("fixed-stress did not converge (rel res " + std::to_string(rep.final_relative_residual) +
+                                  ")");
+            sweeps[n] = rep.iterations;
+            final_res[n] = rep.final_relative_residual;
+            cached_tau = tau;
+            const double* end = &x[static_cast<size_t>(nn - 1) * nt];
+            u_prev.assign(end, end + ops.n_u);
+            p_prev.assign(end + ops.n_u + ops.n_q, end + nt);
+            trace_prev.assign(end, end + nt);
+            if (states) std::copy(x.begin(), x.end(), states + static_cast<size_t>(n) * nn * nt);
+        } catch (const SolverError& e) {
+            throw SolverError("slab " + std::to_string(n) + " (t_n = " + std::to_string(part.t_end(n)) + "): " +
+                              e.what());
+        }
+    }
+    GUARD_END
+}
+
 // Slab right-hand side for a given jump (u_prev, p_prev) and slab start t0:
 // out is (r+1)*n_total, stacked per Radau node (slab.hpp:58-87).
 int refcpu_slab_rhs(void* hp, int r, double t0, double tau, const double* u_prev, const double* p_prev, double* out) {

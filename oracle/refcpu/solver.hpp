@@ -227,9 +227,9 @@ struct FixedStressConfig {
     }
 };
 
-// fixed_stress.hpp:38-60 (kappa = 1)
+// fixed_stress.hpp:38-60 (kappa empty = all ones, as in the slab solver, slab.hpp:162)
 inline void apply_block_operator(const SpatialOperators& ops, const std::vector<double>& theta, int m, double tau,
-                                 const double* x, double* y) {
+                                 const double* x, double* y, const std::vector<double>& kappa = {}) {
     const int nt = ops.n_total(), nu = ops.n_u, nq = ops.n_q, np = ops.n_p;
     const double b = ops.mat.biot_b;
     std::vector<Vec> dp(m);
@@ -239,7 +239,7 @@ inline void apply_block_operator(const SpatialOperators& ops, const std::vector<
         const double* u = x + i * nt;
         const double* q = x + i * nt + nu;
         const double* p = x + i * nt + nu + nq;
-        const double w = tau * 1.0;
+        const double w = tau * (kappa.empty() ? 1.0 : kappa[i]);
         ops.A.apply(u, au.data());
         ops.E.apply(p, ep.data());
         for (int k = 0; k < nu; ++k) y[i * nt + k] = w * (au[k] - b * ep[k]);
@@ -328,13 +328,16 @@ inline std::shared_ptr<InnerSolver> make_a_solver(const SpatialOperators& ops, I
 class FixedStressSolver {
 public:
     FixedStressSolver(const SpatialOperators& ops, std::vector<double> theta, int m, double tau, double stab,
-                      std::shared_ptr<InnerSolver> a_solver, InnerBackend be, int nx, int ny)
+                      std::shared_ptr<InnerSolver> a_solver, InnerBackend be, int nx, int ny,
+                      std::vector<double> kappa = {})
         : ops_(&ops), theta_(std::move(theta)), m_(m), tau_(tau), stab_(stab), a_(std::move(a_solver)), be_(be),
-          nx_(nx), ny_(ny) {
+          nx_(nx), ny_(ny), kappa_(kappa.empty() ? std::vector<double>(m, 1.0) : std::move(kappa)) {
+        if (static_cast<int>(kappa_.size()) != m_ || static_cast<int>(theta_.size()) != m_ * m_)
+            throw std::invalid_argument("FixedStressSolver: weight dimensions mismatch");
         if (!(tau_ > 0.0)) throw std::invalid_argument("FixedStressSolver: tau must be positive");
     }
     int block_size() const { return m_ * ops_->n_total(); }
-    void apply_block(const double* x, double* y) const { apply_block_operator(*ops_, theta_, m_, tau_, x, y); }
+    void apply_block(const double* x, double* y) const { apply_block_operator(*ops_, theta_, m_, tau_, x, y, kappa_); }
 
     // fixed_stress.hpp:109-139
     Vec sweep(const Vec& x, const double* rhs) const {
@@ -362,7 +365,7 @@ public:
         for (int i = 0; i < m_; ++i) {
             const double* p_new = &fsol[m_ * nq + i * np];
             const double* q_new = &fsol[i * nq];
-            const double w = tau_ * 1.0;
+            const double w = tau_ * kappa_[i];
             ops_->E.apply(p_new, ep.data());
             for (int k = 0; k < nu; ++k) mech[k] = rhs[i * nt + k] / w + b * ep[k];
             a_->solve(mech.data(), &xn[i * nt]);
@@ -417,14 +420,14 @@ private:
         const int nq = ops_->n_q, np = ops_->n_p;
         const double inv_m = 1.0 / ops_->mat.biot_m;
         if (be_ == InnerBackend::banded && m_ == 1) {
-            flow_ = std::make_shared<FlowSchurSolver>(*ops_, nx_, ny_, tau_ * 1.0, theta_[0], inv_m, stab_);
+            flow_ = std::make_shared<FlowSchurSolver>(*ops_, nx_, ny_, tau_ * kappa_[0], theta_[0], inv_m, stab_);
             return;
         }
         const int nf = m_ * (nq + np);
         std::vector<double> f(static_cast<size_t>(nf) * nf, 0.0);
         auto F = [&](int i, int j) -> double& { return f[static_cast<size_t>(i) * nf + j]; };
         for (int i = 0; i < m_; ++i) {
-            const double w = tau_ * 1.0;
+            const double w = tau_ * kappa_[i];
             for (int r = 0; r < nq; ++r)
                 for (int k = ops_->M_q.row_offsets[r]; k < ops_->M_q.row_offsets[r + 1]; ++k)
                     F(i * nq + r, i * nq + ops_->M_q.col_indices[k]) = w * ops_->M_q.values[k];
@@ -449,6 +452,7 @@ private:
     std::shared_ptr<InnerSolver> a_;
     InnerBackend be_;
     int nx_, ny_;
+    std::vector<double> kappa_;
     mutable std::shared_ptr<InnerSolver> flow_;
 };
 

@@ -49,6 +49,10 @@ class GmresOpts(C.Structure):
                 ("stab", C.c_double), ("candidate", C.c_int)]
 
 
+class FsOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_sweeps", C.c_int), ("stab", C.c_double)]
+
+
 class Report(C.Structure):
     _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("final_rel_res", C.c_double),
                 ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int), ("history_len", C.c_int),
@@ -87,6 +91,10 @@ _SIGS = {
     "pdg_slab_solve_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
     "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_destroy": (None, [VP]),
+    "pdg_fs_create": (C.c_int, [VP, C.c_int, C.c_double, C.POINTER(FsOpts), C.POINTER(VP)]),
+    "pdg_fs_solve": (C.c_int, [VP, DP, DP, DP, C.POINTER(Report)]),
+    "pdg_fs_solve_device": (C.c_int, [VP, VP, VP, VP, C.POINTER(Report)]),
+    "pdg_fs_destroy": (None, [VP]),
     "pdg_spmv_csr_device": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_op_create": (C.c_int, [VP, C.c_int, DP, C.c_double, C.POINTER(VP)]),
     "pdg_op_rows": (C.c_int, [VP, LLP, LLP]),

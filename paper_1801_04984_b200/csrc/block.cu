@@ -8,6 +8,7 @@
 #include <string>
 
 #include "block.cuh"
+#include "timebasis.hpp"
 
 namespace pdg {
 
@@ -379,23 +380,31 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
 }
 
 void FixedStressPre::apply(const double* r, double* z, cudaStream_t st) {
+    const size_t len = (size_t)m * ops->n_total();
+    for (int s = 0; s < sweeps; ++s) {
+        if (s > 0) PDG_CUDA(cudaMemcpyAsync(xold.p, z, sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
+        sweep_once(s > 0 ? xold.p : nullptr, r, z, st);
+    }
+}
+
+// One flow-then-mechanics sweep (fixed_stress.hpp:109-139) from iterate xprev
+// (null = the zero iterate) into z (z must not alias xprev or r).
+void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z, cudaStream_t st) {
     const SpatialOps& o = *ops;
     const int nt = o.n_total(), nu = o.n_u, nq = o.n_q, np = o.n_p;
-    for (int s = 0; s < sweeps; ++s) {
-        const int lag = s > 0;
-        if (lag) PDG_CUDA(cudaMemcpyAsync(xold.p, z, sizeof(double) * (size_t)m * nt, cudaMemcpyDeviceToDevice, st));
-        {
+    const int lag = xprev != nullptr;
+    {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (2.0 * np + 2.0 * nq + 3.0 * o.B.nnz));
         k_flow_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, lag, lambda, o.biot_b, stab, r,
-                                                                    lag ? xold.p : nullptr, o.Et.off.p, o.Et.idx.p,
-                                                                    o.Et.val.p, o.m_p.p, fp.p);
+                                                                    xprev, o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.m_p.p,
+                                                                    fp.p);
         k_flow_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, w, r, fp.p, o.B.off.p, o.B.idx.p,
                                                                     o.B.val.p, dinv.p, rq.p);
         count_launch(2);
         PDG_CHECK_LAUNCH();
-        }
-        flow.solve(rq.p, nq, z + nu, nt, m, st);
-        {
+    }
+    flow.solve(rq.p, nq, z + nu, nt, m, st);
+    {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (3.0 * np + 2.0 * o.Bt.nnz + 2.0 * nu + 2.0 * o.E.nnz));
         k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fp.p, o.Bt.off.p, o.Bt.idx.p,
                                                                    o.Bt.val.p, dinv.p, z);
@@ -403,9 +412,8 @@ void FixedStressPre::apply(const double* r, double* z, cudaStream_t st) {
                                                                      o.E.idx.p, o.E.val.p, mech.p);
         count_launch(2);
         PDG_CHECK_LAUNCH();
-        }
-        a->chol.solve(mech.p, nu, z, nt, m, st);
     }
+    a->chol.solve(mech.p, nu, z, nt, m, st);
 }
 
 void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
@@ -626,6 +634,102 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
         std::snprintf(buf, sizeof(buf), "%f", final_rel);
         throw Error(PDG_NOT_CONVERGED,
                     "slab block " + std::to_string(block_index) + ": GMRES did not converge (rel res " + buf + ")");
+    }
+}
+
+void FsSolver::create(const SpatialOps& o, int r, double tau_, double stab, std::shared_ptr<ASolver> a) {
+    require(r == 0, "fixed-stress solver: the device path covers dG(0); dG(r >= 1) couples the time components in "
+                    "the flow block (non-symmetric), not on the device yet");
+    require(tau_ > 0.0, "FixedStressSolver: tau must be positive");
+    stab = stab < 0.0 ? o.biot_b * o.biot_b / o.k_dr : stab;  // FixedStressConfig::resolve_stab
+    require(stab >= 0.0, "fixed-stress: stabilization must be nonnegative");
+    ctx = o.ctx;
+    ops = &o;
+    m = r + 1;
+    tau = tau_;
+    cudaStream_t st = ctx->stream;
+    const TimeConsts tc = time_consts(r);  // Theta = G_hat, kappa = weights (both [1] for r = 0)
+    op.build(o, m, tc.G.data(), tau, st);
+    if (!a) a = make_a_solver(o, 2, st);
+    pre.setup(o, m, tau, tc.G[0], stab, 1, a, st);
+    const long long n = (long long)m * o.n_total();
+    red.setup(n, 1, false, st);
+    xa.alloc(n);
+    xb.alloc(n);
+    t.alloc(n);
+    this->r.alloc(n);
+    PDG_CUDA(cudaEventCreate(&ev0));
+    PDG_CUDA(cudaEventCreate(&ev1));
+    PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+FsSolver::~FsSolver() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+}
+
+void FsSolver::solve(const double* rhs, const double* x0, double* x_out, double tol, int max_sweeps, pdg_report* rep) {
+    require(tol > 0.0 && tol < 1.0, "fixed-stress: tol must be in (0,1)");
+    require(max_sweeps >= 1, "fixed-stress: sweep counts must be >= 1");
+    cudaStream_t st = ctx->stream;
+    const long long n = (long long)m * ops->n_total();
+    const long long launches0 = g_launches;
+    KrylovOps K{st, red, static_cast<unsigned>(2 * num_sms())};
+    PDG_CUDA(cudaEventRecord(ev0, st));
+    std::vector<double> hist;
+    double* x = xa.p;
+    double* xn = xb.p;
+    if (x0)
+        PDG_CUDA(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    else
+        PDG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    auto residual = [&](const double* v) {
+        op.apply(v, t.p, st);
+        return K.sub_norm(rhs, t.p, r.p);
+    };
+    const double rnorm = K.norm(rhs);
+    bool converged = false;
+    int iters = 0;
+    double final_rel = 0.0;
+    if (rnorm <= 1e-14) {  // fixed_stress.hpp:154-159
+        hist.push_back(residual(x));
+        converged = true;
+        PDG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    } else {
+        double res = residual(x);
+        hist.push_back(res);
+        for (int k = 0; k < max_sweeps; ++k) {
+            pre.sweep_once(x, rhs, xn, st);
+            std::swap(x, xn);
+            ++iters;
+            res = residual(x);
+            hist.push_back(res);
+            if (res / rnorm <= tol) {
+                converged = true;
+                break;
+            }
+        }
+        final_rel = res / rnorm;
+    }
+    PDG_CUDA(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    PDG_CUDA(cudaEventRecord(ev1, st));
+    PDG_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    PDG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    if (rep) {
+        rep->converged = converged;
+        rep->iterations = iters;
+        rep->final_rel_res = final_rel;
+        rep->history_len = static_cast<int>(hist.size());
+        if (rep->history)
+            for (int i = 0; i < std::min<int>(rep->history_cap, (int)hist.size()); ++i) rep->history[i] = hist[i];
+        rep->device_ms = ms;
+        rep->kernel_launches = static_cast<int>(g_launches - launches0);
+    }
+    if (!converged) {
+        char buf[64];
+        std::snprintf(buf, sizeof(buf), "%f", final_rel);
+        throw Error(PDG_NOT_CONVERGED, std::string("fixed-stress did not converge (rel res ") + buf + ")");
     }
 }
 

@@ -30,6 +30,7 @@ struct FixedStressPre {
     void setup(const SpatialOps& ops, int m, double tau, double lambda, double stab, int sweeps,
                std::shared_ptr<ASolver> a, cudaStream_t st);
     void apply(const double* r, double* z, cudaStream_t st);
+    void sweep_once(const double* xprev, const double* r, double* z, cudaStream_t st);
 };
 
 struct Gmres {
@@ -59,6 +60,26 @@ struct Block {
     // GMRES solve, device pointers, on ctx->stream. Throws Error(PDG_NOT_CONVERGED) like slab.hpp:228-230.
     void solve(const double* b, double* x, pdg_report* rep, int block_index = 0);
     ~Block();
+};
+
+// FixedStressSolver::solve (fixed_stress.hpp:144-172) on the untransformed
+// slab block of the fixed-stress march (march.hpp:80-108): Theta = G_hat,
+// kappa = the Radau weights. Sweeps from x0 until the true residual of the
+// coupled block drops below tol ||rhs||. Device path for dG(0) (one component).
+struct FsSolver {
+    Ctx* ctx = nullptr;
+    const SpatialOps* ops = nullptr;
+    int m = 1;
+    double tau = 0;
+    SpaceTimeOp op;
+    FixedStressPre pre;
+    Gmres red;  // reduction buffers
+    DBuf<double> xa, xb, t, r;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    void create(const SpatialOps& ops, int r, double tau, double stab, std::shared_ptr<ASolver> a);
+    // x0 may be null (zero initial guess). Throws Error(PDG_NOT_CONVERGED) like march.hpp:95-97.
+    void solve(const double* rhs, const double* x0, double* x_out, double tol, int max_sweeps, pdg_report* rep);
+    ~FsSolver();
 };
 
 }  // namespace pdg

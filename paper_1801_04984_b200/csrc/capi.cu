@@ -29,6 +29,12 @@ struct pdg_op {
     SpaceTimeOp op;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
+struct pdg_fs {
+    pdg_ops* ops = nullptr;
+    FsSolver fs;
+    pdg_fs_opts opts{};
+    DBuf<double> io_a, io_b, io_c;
+};
 struct pdg_slab {
     pdg_ops* ops = nullptr;
     TimeConsts tc;
@@ -600,6 +606,48 @@ int pdg_mass_residual(pdg_ops* ops, int r, double tau, const double* rhs, const 
     PDG_CUDA(cudaStreamSynchronize(st));
     API_END
 }
+
+int pdg_fs_create(pdg_ops* ops, int r, double tau, const pdg_fs_opts* opts, pdg_fs** out) {
+    API_BEGIN
+    require(ops && opts && out, "pdg_fs_create: null argument");
+    require(opts->tol > 0.0 && opts->tol < 1.0, "fixed-stress: tol must be in (0,1)");
+    require(opts->max_sweeps >= 1, "fixed-stress: sweep counts must be >= 1");
+    PDG_CUDA(cudaSetDevice(ops->s.ctx->device));
+    auto f = std::make_unique<pdg_fs>();
+    f->ops = ops;
+    f->opts = *opts;
+    if (!ops->a) ops->a = make_a_solver(ops->s, 2, ops->s.ctx->stream);
+    f->fs.create(ops->s, r, tau, opts->stab, ops->a);
+    *out = f.release();
+    API_END
+}
+
+int pdg_fs_solve_device(pdg_fs* f, const double* rhs_dev, const double* x0_dev, double* x_dev, pdg_report* rep) {
+    API_BEGIN
+    require(f && rhs_dev && x_dev, "pdg_fs_solve: null argument");
+    f->fs.solve(rhs_dev, x0_dev, x_dev, f->opts.tol, f->opts.max_sweeps, rep);
+    API_END
+}
+
+int pdg_fs_solve(pdg_fs* f, const double* rhs, const double* x0, double* x, pdg_report* rep) {
+    API_BEGIN
+    require(f && rhs && x, "pdg_fs_solve: null argument");
+    cudaStream_t st = f->ops->s.ctx->stream;
+    const size_t n = (size_t)f->fs.m * f->ops->s.n_total();
+    if (!f->io_a.n) {
+        f->io_a.alloc(n);
+        f->io_b.alloc(n);
+        f->io_c.alloc(n);
+    }
+    PDG_CUDA(cudaMemcpyAsync(f->io_a.p, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    if (x0) PDG_CUDA(cudaMemcpyAsync(f->io_c.p, x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    f->fs.solve(f->io_a.p, x0 ? f->io_c.p : nullptr, f->io_b.p, f->opts.tol, f->opts.max_sweeps, rep);
+    PDG_CUDA(cudaMemcpyAsync(x, f->io_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+void pdg_fs_destroy(pdg_fs* f) { delete f; }
 
 int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q) {
     API_BEGIN

@@ -52,8 +52,11 @@ class GmresOptions:
 
 @dataclass
 class FixedStressConfig:
+    """FixedStressConfig (fixed_stress.hpp:17-35)."""
     stab: float = -1.0  # < 0: b^2 / K_dr
-    truncation_sweeps: int = 1
+    truncation_sweeps: int = 1  # sweeps per preconditioner application
+    tol: float = 1e-10  # fixed-stress march: true-residual tolerance
+    max_sweeps: int = 200  # fixed-stress march: sweep limit
 
 
 @dataclass
@@ -342,6 +345,41 @@ class SlabSolver:
             self._h = None
 
 
+class FixedStressSolver:
+    """FixedStressSolver::solve (fixed_stress.hpp:144-172) of the fixed-stress
+    march (march.hpp:80-108): Theta = G_hat, kappa = Radau weights, sweeps on the
+    untransformed slab block from a warm start. Device path: dG(0)."""
+
+    def __init__(self, ops: SpatialOperators, r: int, tau: float, cfg: FixedStressConfig | None = None):
+        self.ops, self.r, self.tau = ops, r, tau
+        self.cfg = cfg or FixedStressConfig()
+        o = _lib.FsOpts()
+        o.tol, o.max_sweeps, o.stab = self.cfg.tol, self.cfg.max_sweeps, self.cfg.stab
+        h = C.c_void_p()
+        check(lib().pdg_fs_create(ops._h, r, tau, C.byref(o), C.byref(h)))
+        self._h = h
+        self.n = (r + 1) * ops.n_total
+
+    def solve(self, rhs, x0=None):
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        assert rhs.size == self.n
+        x0p = None if x0 is None else _dp(np.ascontiguousarray(x0, np.float64))
+        out = np.empty_like(rhs)
+        rep, hist = _report(self.cfg.max_sweeps + 2)
+        check(lib().pdg_fs_solve(self._h, _dp(rhs), x0p, _dp(out), C.byref(rep)))
+        return out, _to_report(rep, hist)
+
+    def solve_device(self, rhs_ptr: int, x0_ptr: int | None, out_ptr: int):
+        rep, hist = _report(self.cfg.max_sweeps + 2)
+        check(lib().pdg_fs_solve_device(self._h, rhs_ptr, x0_ptr, out_ptr, C.byref(rep)))
+        return _to_report(rep, hist)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pdg_fs_destroy(self._h)
+            self._h = None
+
+
 def uniform_partition(T: float, n_slabs: int):
     """TimePartition t_points of uniform_partition (time_basis.hpp:33-40): T*n/N, last = T."""
     if not T > 0.0 or n_slabs < 1:
@@ -352,12 +390,17 @@ def uniform_partition(T: float, n_slabs: int):
 
 
 def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptions | None = None,
-          keep_states: bool = False, mass_check: bool = False):
+          keep_states: bool = False, mass_check: bool = False, method: str = "monolithic-spectral"):
     """Monolithic-spectral march (march.hpp:45-79,109-117) with a device-resident
     slab loop: the slab right-hand side, the Schur transforms and the jump data
     never leave the GPU. Returns per-slab reports (and states if asked). With
     mass_check, each report carries the slab's local mass balance
-    max_c |residual_c| / scale (slab.hpp:292-318, computed on the device)."""
+    max_c |residual_c| / scale (slab.hpp:292-318, computed on the device).
+    method "fixed-stress" runs the fixed-stress branch (march.hpp:80-108): one
+    FixedStressSolver per tau, warm-started from the previous end trace in every
+    component; report.iterations is then the sweep count (fs_sweeps)."""
+    if method not in ("monolithic-spectral", "fixed-stress"):
+        raise InvalidArgument(f"march: unknown method {method!r}")
     import torch
 
     opt = opt or SolveOptions()
@@ -370,17 +413,22 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
     rhs = torch.empty((r + 1) * nt, dtype=torch.float64, device=dev)
     out = torch.empty_like(rhs)
     reports, states = [], []
+    x0 = None
     for n in range(n_slabs):
         # the slab's own length and start (march.hpp:63-64); the solver is rebuilt
         # only when tau changes by more than 1e-12 tau (march.hpp:72)
         tau, t0 = t_points[n + 1] - t_points[n], t_points[n]
         if slab is None or abs(tau - cached_tau) > 1e-12 * tau:
             slab = SlabSolver(ops, r, tau, opt)
+            fs = FixedStressSolver(ops, r, tau, opt.fs) if method == "fixed-stress" else None
         cached_tau = tau
         torch.cuda.synchronize()
         slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=tau)
         try:
-            rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+            if fs is None:
+                rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+            else:  # warm start: the previous end trace in every component (march.hpp:87-93)
+                rep = fs.solve_device(rhs.data_ptr(), None if x0 is None else x0.data_ptr(), out.data_ptr())
         except SolverError as e:
             raise SolverError(e.status, f"slab {n} (t_n = {t_points[n + 1]:f}): {e}") from None
         if mass_check:
@@ -391,6 +439,8 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
         end = out[r * nt:(r + 1) * nt]
         u_prev.copy_(end[:ops.n_u])
         p_prev.copy_(end[ops.n_u + ops.n_q:])
+        if method == "fixed-stress":
+            x0 = end.repeat(r + 1)  # made before the next slab's synchronize
         if keep_states:
             states.append(out.cpu().numpy().copy())
     return reports, states
