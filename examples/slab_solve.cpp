@@ -48,7 +48,19 @@ int main() {
         for (double v : x) nrm += v * v;
         std::printf("config0 slab 0: converged=%d iterations=%d rel_res=%.3e |x|=%.6e n_total=%lld\n", rep.converged,
                     rep.iterations, rep.final_relative_residual, std::sqrt(nrm), nt);
-        return rep.converged ? 0 : 1;
+        // local mass balance of the solved slab (slab.hpp:292-318)
+        auto [res, scale] = mass_residual(ops, 0, tau, rhs, x);
+        double worst = 0.0;
+        for (double v : res) worst = std::fmax(worst, v);
+        std::printf("mass balance: max|res|/scale=%.3e\n", scale > 0.0 ? worst / scale : 0.0);
+        // the same slab by the fixed-stress method (march.hpp:80-108)
+        FixedStressSolver fs(ops, 0, tau);
+        auto [xf, rf] = fs.solve(rhs);
+        double d = 0.0;
+        for (size_t i = 0; i < x.size(); ++i) d += (x[i] - xf[i]) * (x[i] - xf[i]);
+        std::printf("fixed-stress: converged=%d sweeps=%d |x_fs - x|/|x|=%.3e\n", rf.converged, rf.iterations,
+                    std::sqrt(d / nrm));
+        return rep.converged && rf.converged ? 0 : 1;
     } catch (const std::exception& e) {
         std::printf("error: %s\n", e.what());
         return 2;

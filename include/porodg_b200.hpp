@@ -146,4 +146,61 @@ private:
     long long n_ = 0;
 };
 
+// FixedStressSolver of the fixed-stress march (fixed_stress.hpp:144-172 as built
+// at march.hpp:83-84): solve(rhs, x0) sweeps from x0 (empty = zero) until the
+// true residual drops below tol; report.iterations = fs_sweeps. Device path: dG(0).
+class FixedStressSolver {
+public:
+    FixedStressSolver(SpatialOperators& ops, int r, double tau, double tol = 1e-10, int max_sweeps = 200,
+                      double stab = -1.0)
+        : r_(r), n_(ops.n_total()), cap_(max_sweeps + 2) {
+        const pdg_fs_opts o{tol, max_sweeps, stab};
+        check(pdg_fs_create(ops.get(), r, tau, &o, &h_));
+    }
+    ~FixedStressSolver() { pdg_fs_destroy(h_); }
+    FixedStressSolver(const FixedStressSolver&) = delete;
+    FixedStressSolver& operator=(const FixedStressSolver&) = delete;
+
+    template <class Vec>
+    std::pair<std::vector<double>, SolverReport> solve(const Vec& rhs, const Vec* x0 = nullptr) const {
+        if (static_cast<long long>(rhs.size()) != (r_ + 1) * n_ ||
+            (x0 && static_cast<long long>(x0->size()) != (r_ + 1) * n_))
+            throw std::invalid_argument("fixed-stress: bad initial guess size");
+        std::vector<double> out(rhs.size()), hist(cap_);
+        pdg_report rep{};
+        rep.history = hist.data();
+        rep.history_cap = cap_;
+        check(pdg_fs_solve(h_, rhs.data(), x0 ? x0->data() : nullptr, out.data(), &rep));
+        SolverReport sr;
+        sr.converged = rep.converged != 0;
+        sr.iterations = rep.iterations;
+        sr.final_relative_residual = rep.final_rel_res;
+        sr.residual_history.assign(hist.begin(), hist.begin() + std::min(rep.history_len, cap_));
+        sr.device_ms = rep.device_ms;
+        return {std::move(out), std::move(sr)};
+    }
+
+private:
+    pdg_fs* h_ = nullptr;
+    int r_ = 0;
+    long long n_ = 0;
+    int cap_ = 0;
+};
+
+// local_mass_residual (slab.hpp:292-318): |residual| per cell and the scale, from
+// the stacked slab rhs and state ((r+1) * n_total each).
+template <class Vec>
+std::pair<std::vector<double>, double> mass_residual(SpatialOperators& ops, int r, double tau, const Vec& rhs,
+                                                     const Vec& state) {
+    long long s[7];
+    check(pdg_ops_sizes(ops.get(), s));
+    if (static_cast<long long>(rhs.size()) != (r + 1) * ops.n_total() ||
+        static_cast<long long>(state.size()) != (r + 1) * ops.n_total())
+        throw std::invalid_argument("mass_residual: rhs/state dimension mismatch");
+    std::vector<double> res(s[2]);
+    double scale = 0.0;
+    check(pdg_mass_residual(ops.get(), r, tau, rhs.data(), state.data(), res.data(), &scale));
+    return {std::move(res), scale};
+}
+
 }  // namespace porodg_b200

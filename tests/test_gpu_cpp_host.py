@@ -27,3 +27,6 @@ def test_cpp_host_layer_solves_config0_slab(tmp_path):
     out = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "converged=1 iterations=3" in out.stdout
+    assert "fixed-stress: converged=1" in out.stdout
+    worst = float(out.stdout.split("max|res|/scale=")[1].split()[0])
+    assert worst < 1e-8
