@@ -133,6 +133,10 @@ void BlockTriChol::factor(int n_, const int* off, const int* idx, const double* 
 
 void BlockTriChol::factor_dense(double* dense, cudaStream_t st) {
     local_prepare(dense, st);  // before the couplings are overwritten by the factorisation
+    if (!local) {
+        dense_setup(dense, st);
+        return;
+    }
     LaHandles h(st);
     const int t = twist;
     int lwork = 0;
@@ -191,10 +195,7 @@ void BlockTriChol::factor_dense(double* dense, cudaStream_t st) {
         if (hinfo[j] != 0)
             throw Error(PDG_NOT_CONVERGED, "dense LU: matrix is singular to working precision (block " +
                                                std::to_string(j) + " not positive definite)");
-    if (local)
-        local_finish(dense, st);
-    else
-        dense_finish(h, dense, kp.p, oKp, st);
+    local_finish(dense, st);
 }
 
 void BlockTriChol::solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {

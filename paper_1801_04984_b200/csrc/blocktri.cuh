@@ -22,6 +22,8 @@ struct LaHandles;
 struct DenseTask {
     long long moff, in0, in1, b0, out_ll, out_x;
     int n0, n1, mout, ld;
+    long long base;  // b offset added to the outputs (-1 none)
+    int acc, pad_;   // acc: x[out_x] += outputs
 };
 
 // One step of the local-coupling sweep for one chain (see BlockTriChol::local).
@@ -82,7 +84,8 @@ struct BlockTriChol {
     DBuf<SweepTask> d_sweep;
 
     // ---- dense-sweep mode (any coupling pattern: the flow solve) -------------------------
-    std::vector<DenseTask> dsched;   // steps x 2 chains
+    std::vector<DenseTask> dsched;   // steps x nchains
+    int nchains = 2;
     DBuf<DenseTask> d_dsched;
     long long d_lln = 0;
     int d_ldmax = 0, d_g = 0, d_stages = 0;
@@ -112,8 +115,7 @@ private:
     bool local_prepare(double* dense, cudaStream_t st);   // structure check + coupling chunks
     void local_finish(double* dense, cudaStream_t st);    // Sinv_j from the Cholesky factors, schedule, kernel config
     void solve_local(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
-    void dense_finish(LaHandles& h, const double* dense, const double* kp, const std::vector<long long>& oKp,
-                      cudaStream_t st);
+    void dense_setup(double* dense, cudaStream_t st);
     void solve_dense(const double* b, double* x, int nrhs, cudaStream_t st);
 };
 

@@ -1,9 +1,17 @@
-// General mode of the twisted block-tridiagonal solver (any coupling
-// pattern; used for the flow Schur complement in face-row order). With the
-// twisted Cholesky factors (top L_j, K_j = L_{j+1,j}; bottom L'_j, K'_j =
-// L_{j-1,j}; twist L_t) and Linv = L^{-1}, every step of the solve is
-// "outputs = M_s * [seg0; seg1]" with a precomputed row-major M_s, and the whole
-// solve (forward, twist, backward of both chains) is one persistent kernel:
+// General mode of the block-tridiagonal solver (any coupling pattern; used
+// for the flow Schur complement in face-row order), one persistent kernel per
+// solve. The block chain is cut into P "virtual strips" separated by single
+// separator blocks (substructuring, exact):
+//   1. every strip interior is solved by its own twisted Cholesky sweep (two
+//      chains per strip, all 2P chains concurrent): y_I = A_II^{-1} b_I;
+//   2. separator right-hand sides g_s = b_s - A_{s,s-1} y_{s-1} - A_{s,s+1} y_{s+1};
+//   3. the separator system S x_S = g (S = A_SS - A_SI A_II^{-1} A_IS, block
+//      tridiagonal over the P-1 separators, factored at setup) by a twisted sweep;
+//   4. x_I = y_I - W x_S with the spikes W = A_II^{-1} A_IS (precomputed).
+// A solve has about nb/P + P dependent steps instead of nb (P = 1: the plain
+// twisted sweep). Every step is "outputs = [b +] M_s * [seg0; seg1]" with a
+// precomputed row-major step matrix; for a twisted system with Cholesky factors
+// (top L_j, K_j = L_{j+1,j}; bottom L'_j, K'_j = L_{j-1,j}; twist L_t, Linv = L^{-1}):
 //   top forward      y_j = [Linv_j | -Linv_j K_{j-1}] [b_j; y_{j-1}]
 //   bottom forward   y_j = [Linv'_j | -Linv'_j K'_{j+1}] [b_j; y_{j+1}]
 //   twist parts      p_top = [Linv_t | -Linv_t K_{t-1}] [b_t; y_{t-1}],  p_bot = -Linv_t K'_{t+1} y_{t+1}
@@ -21,6 +29,12 @@ namespace pdg {
 
 using namespace dev;
 
+#define PDG_CUSOLVER_D(call)                                                                                        \
+    do {                                                                                                            \
+        cusolverStatus_t s_ = (call);                                                                               \
+        if (s_ != CUSOLVER_STATUS_SUCCESS)                                                                          \
+            throw ::pdg::Error(PDG_CUDA_ERROR, std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
+    } while (0)
 #define PDG_CUBLAS_D(call)                                                                                        \
     do {                                                                                                          \
         cublasStatus_t s_ = (call);                                                                               \
@@ -66,19 +80,19 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
 __global__ void __launch_bounds__(256, 1)
     k_sweep_dense(int nsteps, const DenseTask* __restrict__ sched_g, int nrhs, int n, const double* __restrict__ store,
                   int ldmax, const double* __restrict__ b, double* __restrict__ x, uint4* ll, long long lln,
-                  unsigned flag, int stages, int pf, int g, unsigned long long* dbg) {
+                  unsigned flag, int stages, int pf, int g, int nchains, unsigned long long* dbg) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw);  // [stages][8 rows][ldmax]
     double* red = ring + (size_t)stages * 8 * ldmax;      // [8 warps][16]
     unsigned long long* full = reinterpret_cast<unsigned long long*>(red + 8 * 16);
     DenseTask* tsh = reinterpret_cast<DenseTask*>(full + stages);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = threadIdx.x;
-    const int chain = static_cast<int>(blockIdx.x) < g ? 0 : 1;
-    const int row0 = (chain ? blockIdx.x - g : blockIdx.x) * 8;
+    const int chain = static_cast<int>(blockIdx.x) / g;
+    const int row0 = (static_cast<int>(blockIdx.x) % g) * 8;
     auto stamp = [&](int s, int ph) {
         if (dbg && lt == 0) dbg[((size_t)blockIdx.x * nsteps + s) * 4 + ph] = globaltimer();
     };
-    for (int i = lt; i < nsteps; i += blockDim.x) tsh[i] = sched_g[2 * i + chain];
+    for (int i = lt; i < nsteps; i += blockDim.x) tsh[i] = sched_g[(long long)nchains * i + chain];
     auto unit_src = [&](int s, int& nr) -> const double* {
         const DenseTask& tk = tsh[s];
         nr = tk.moff >= 0 ? max(0, min(8, tk.mout - row0)) : 0;
@@ -109,6 +123,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int s = 0; s < min(pf, nsteps); ++s) prefetch_l2(s);
         for (int s = 0; s < stages; ++s) issue(s);
     }
+    double y[2][DNI];  // this thread's input values (kept across tasks with identical inputs)
     for (int s = 0; s < nsteps; ++s) {
         const DenseTask tk = tsh[s];
         stamp(s, 0);
@@ -116,23 +131,26 @@ __global__ void __launch_bounds__(256, 1)
         const bool active = tk.moff >= 0;
         if (active) {
             const int nin = tk.n0 + tk.n1;
-            // this thread's inputs: seg 0 from b (in0 < 0) or LL lines, seg 1 from LL lines
-            double y[2][DNI];
+            // this thread's inputs: seg 0 from b (in0 < 0) or LL lines, seg 1 from LL lines;
+            // a task reading exactly the previous task's lines keeps them (no round trip)
+            const bool reuse = s > 0 && tsh[s - 1].moff >= 0 && tsh[s - 1].in0 == tk.in0 && tsh[s - 1].in1 == tk.in1 &&
+                               tsh[s - 1].n0 == tk.n0 && tsh[s - 1].n1 == tk.n1 && tk.in0 >= 0;
             unsigned pending = 0;
+            if (!reuse)
 #pragma unroll
-            for (int i = 0; i < DNI; ++i) {
-                const int c = lt + 256 * i;
+                for (int i = 0; i < DNI; ++i) {
+                    const int c = lt + 256 * i;
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    y[k][i] = 0.0;
-                    if (k < nrhs && c < nin) {
-                        if (c < tk.n0 && tk.in0 < 0)
-                            y[k][i] = b[(long long)k * n + tk.b0 + c];
-                        else
-                            pending |= 1u << (2 * i + k);
+                    for (int k = 0; k < 2; ++k) {
+                        y[k][i] = 0.0;
+                        if (k < nrhs && c < nin) {
+                            if (c < tk.n0 && tk.in0 < 0)
+                                y[k][i] = b[(long long)k * n + tk.b0 + c];
+                            else
+                                pending |= 1u << (2 * i + k);
+                        }
                     }
                 }
-            }
             while (__any_sync(0xffffffffu, pending != 0)) {
                 uint4 v[2 * DNI];
 #pragma unroll
@@ -182,8 +200,12 @@ __global__ void __launch_bounds__(256, 1)
                 double val = 0.0;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) val += red[w * 16 + lane];
+                if (tk.base >= 0) val = b[(long long)kk * n + tk.base + r] + val;
                 if (tk.out_ll >= 0) ll_store(ll + kk * lln + tk.out_ll + r, val, flag);
-                if (tk.out_x >= 0) x[(long long)kk * n + tk.out_x + r] = val;
+                if (tk.out_x >= 0) {
+                    double* xp = x + (long long)kk * n + tk.out_x + r;
+                    *xp = tk.acc ? *xp + val : val;
+                }
             }
         }
         stamp(s, 2);
@@ -192,45 +214,260 @@ __global__ void __launch_bounds__(256, 1)
 
 }  // namespace
 
-void BlockTriChol::dense_finish(LaHandles& h, const double* dense, const double* kp, const std::vector<long long>& oKp,
-                                cudaStream_t st) {
-    const int t = twist;
-    auto Kt = [&](int j) { return dense + dC_[j]; };  // K_j = L_{j+1,j}, m_{j+1} x m_j col-major (top, j < t)
-    auto Kb = [&](int j) { return kp + oKp[j]; };     // K'_j = L_{j-1,j}, m_{j-1} x m_j col-major (bottom, j > t)
-    // ---- Linv_j (lower triangular, col-major) ------------------------------------------
-    std::vector<long long> ol(nb);
-    long long tot = 0;
-    for (int j = 0; j < nb; ++j) {
-        ol[j] = tot;
-        tot += (long long)bsz[j] * bsz[j];
+namespace {
+
+// An SPD block-tridiagonal system as dense col-major device blocks: D[j]
+// (m_j x m_j) becomes the twisted Cholesky factor, C[j] = A_{j+1,j}
+// (m_{j+1} x m_j) becomes K_j in the top part; K'_j (bottom) in kp.
+struct TriSys {
+    std::vector<int> m;
+    std::vector<double*> D, C;
+    int t = 0;
+    DBuf<double> kp, linv;
+    std::vector<long long> oKp, ol, ro;
+    int nb() const { return static_cast<int>(m.size()); }
+    long long rows() const { return ro.back(); }
+    double* Kt(int j) const { return C[j]; }
+    double* Kb(int j) const { return kp.p + oKp[j]; }
+    double* Li(int j) const { return linv.p + ol[j]; }
+
+    void factor(LaHandles& h, cudaStream_t st) {
+        const int n = nb();
+        ro.assign(n + 1, 0);
+        for (int j = 0; j < n; ++j) ro[j + 1] = ro[j] + m[j];
+        t = (n - 1) / 2;
+        const double one = 1.0, mone = -1.0, zero = 0.0;
+        const int mx = *std::max_element(m.begin(), m.end());
+        int lwork = 0;
+        PDG_CUSOLVER_D(cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, mx, D[0], mx, &lwork));
+        DBuf<double> work(std::max(lwork, 1));
+        DBuf<int> info(n);
+        info.zero(st);
+        oKp.assign(n, -1);
+        long long kt = 0;
+        for (int j = t + 1; j < n; ++j) {
+            oKp[j] = kt;
+            kt += (long long)m[j - 1] * m[j];
+        }
+        kp.alloc(std::max<long long>(kt, 1));
+        for (int j = 0; j < t; ++j) {  // top
+            if (j > 0)
+                PDG_CUBLAS_D(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m[j], m[j - 1], &mone, C[j - 1], m[j],
+                                         &one, D[j], m[j]));
+            PDG_CUSOLVER_D(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, m[j], D[j], m[j], work.p, lwork, info.p + j));
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                     m[j + 1], m[j], &one, D[j], m[j], C[j], m[j + 1]));
+        }
+        for (int j = n - 1; j > t; --j) {  // bottom
+            if (j < n - 1)
+                PDG_CUBLAS_D(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m[j], m[j + 1], &mone, Kb(j + 1),
+                                         m[j], &one, D[j], m[j]));
+            PDG_CUSOLVER_D(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, m[j], D[j], m[j], work.p, lwork, info.p + j));
+            PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, m[j - 1], m[j], &one, C[j - 1], m[j], &zero, Kb(j),
+                                     m[j - 1], Kb(j), m[j - 1]));
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                     m[j - 1], m[j], &one, D[j], m[j], Kb(j), m[j - 1]));
+        }
+        if (t > 0)  // twist
+            PDG_CUBLAS_D(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m[t], m[t - 1], &mone, C[t - 1], m[t],
+                                     &one, D[t], m[t]));
+        if (t + 1 < n)
+            PDG_CUBLAS_D(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m[t], m[t + 1], &mone, Kb(t + 1), m[t],
+                                     &one, D[t], m[t]));
+        PDG_CUSOLVER_D(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, m[t], D[t], m[t], work.p, lwork, info.p + t));
+        const std::vector<int> hinfo = info.download(st);
+        for (int j = 0; j < n; ++j)
+            if (hinfo[j] != 0)
+                throw Error(PDG_NOT_CONVERGED, "dense LU: matrix is singular to working precision (block " +
+                                                   std::to_string(j) + " not positive definite)");
+        ol.assign(n, 0);
+        long long tot = 0;
+        for (int j = 0; j < n; ++j) {
+            ol[j] = tot;
+            tot += (long long)m[j] * m[j];
+        }
+        linv.alloc(tot);
+        for (int j = 0; j < n; ++j) {
+            k_identity_cm<<<grid_for((long long)m[j] * m[j], 256), 256, 0, st>>>(m[j], Li(j));
+            PDG_CHECK_LAUNCH();
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m[j],
+                                     m[j], &one, D[j], m[j], Li(j), m[j]));
+        }
     }
-    DBuf<double> linv(tot);
+
+    // R <- A^{-1} R for nc right-hand sides (R: rows() x nc col-major, ld = rows()),
+    // block forward/backward substitution through the twisted factors (setup only).
+    void solve_multi(LaHandles& h, double* R, int nc) const {
+        const int n = nb();
+        const long long ld = rows();
+        const double one = 1.0, mone = -1.0;
+        auto Rb = [&](int j) { return R + ro[j]; };
+        auto lower = [&](int j, bool trans) {
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, trans ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                     CUBLAS_DIAG_NON_UNIT, m[j], nc, &one, D[j], m[j], Rb(j), ld));
+        };
+        for (int j = 0; j < t; ++j) {
+            if (j > 0)
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, m[j], nc, m[j - 1], &mone, Kt(j - 1), m[j],
+                                         Rb(j - 1), ld, &one, Rb(j), ld));
+            lower(j, false);
+        }
+        for (int j = n - 1; j > t; --j) {
+            if (j < n - 1)
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, m[j], nc, m[j + 1], &mone, Kb(j + 1), m[j],
+                                         Rb(j + 1), ld, &one, Rb(j), ld));
+            lower(j, false);
+        }
+        if (t > 0)
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, m[t], nc, m[t - 1], &mone, Kt(t - 1), m[t],
+                                     Rb(t - 1), ld, &one, Rb(t), ld));
+        if (t + 1 < n)
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, m[t], nc, m[t + 1], &mone, Kb(t + 1), m[t],
+                                     Rb(t + 1), ld, &one, Rb(t), ld));
+        lower(t, false);
+        lower(t, true);
+        for (int j = t - 1; j >= 0; --j) {
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, m[j], nc, m[j + 1], &mone, Kt(j), m[j + 1],
+                                     Rb(j + 1), ld, &one, Rb(j), ld));
+            lower(j, true);
+        }
+        for (int j = t + 1; j < n; ++j) {
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, m[j], nc, m[j - 1], &mone, Kb(j), m[j - 1],
+                                     Rb(j - 1), ld, &one, Rb(j), ld));
+            lower(j, true);
+        }
+    }
+};
+
+// Where a twisted system reads and writes, per block j (offsets < 0 = none).
+struct SysIO {
+    std::vector<long long> rhs_ll, rhs_b;  // rhs from LL (>= 0) or else from b at rhs_b
+    std::vector<long long> y_ll, x_ll, x_out;
+    long long pt = -1, pb = -1;
+};
+
+enum MatKind { MK_TOPF = 0, MK_BOTF, MK_PTOP, MK_PBOT, MK_TWIST, MK_TOPB, MK_BOTB, MK_GSTEP, MK_CORR };
+struct Mat {
+    int kind;
+    const TriSys* sys;
+    int j;
+    long long off;
+    int ld;
+    // MK_GSTEP: couplings; MK_CORR: spike rows
+    const double *a = nullptr, *c = nullptr;
+    int ma = 0, mc = 0, lda = 0, ldc = 0;
+};
+
+}  // namespace
+
+void BlockTriChol::dense_setup(double* dense, cudaStream_t st) {
+    LaHandles h(st);
+    auto Dg = [&](int j) { return dense + dD_[j]; };
+    auto Cg = [&](int j) { return dense + dC_[j]; };  // A_{j+1,j}
     const double one = 1.0, mone = -1.0, zero = 0.0;
-    for (int j = 0; j < nb; ++j) {
-        const int mj = bsz[j];
-        k_identity_cm<<<grid_for((long long)mj * mj, 256), 256, 0, st>>>(mj, linv.p + ol[j]);
-        PDG_CHECK_LAUNCH();
-        PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, mj,
-                                 mj, &one, dense + dD_[j], mj, linv.p + ol[j], mj));
-    }
-    auto Li = [&](int j) { return linv.p + ol[j]; };
-    // ---- per-step matrices (row-major = col-major of the transpose) -------------------
     auto pad = [](int v) { return (v + 1) & ~1; };
     auto al = [](long long v) { return (v + 31) & ~31LL; };
-    const long long X_ = n, PT = 2LL * n, PB = 2LL * n + bsz[t];
-    d_lln = 2LL * n + 2LL * bsz[t];
-    struct Mat {
-        int kind, j;  // 0 top fwd, 1 bottom fwd, 2 p_top, 3 p_bot, 4 twist, 5 top bwd, 6 bottom bwd
-        long long off;
-        int ld;
+    // ---- virtual strips: 2 chains of g CTAs (8 rows each) per strip, >= 2 interior blocks each
+    d_g = (max_b + 7) / 8;
+    // Default: one strip (the plain twisted sweep). P = 2 cuts the config-1 flow solve from
+    // 250 to 190 us but its spike corrections raise the preconditioner's linearity defect
+    // from < 1e-12 to ~3e-11 of max|z|, so it is opt-in (PDG_FLOW_STRIPS=P).
+    int P = 1;
+    if (const char* e = std::getenv("PDG_FLOW_STRIPS"))
+        P = std::max(1, std::min({std::atoi(e), num_sms() / (2 * d_g), (nb + 1) / 3}));
+    std::vector<int> lo(P), hi(P), sep;
+    {
+        const int interior = nb - (P - 1);
+        int j = 0;
+        for (int k = 0; k < P; ++k) {
+            const int len = interior / P + (k < interior % P ? 1 : 0);
+            if (k > 0) sep.push_back(j++);
+            lo[k] = j;
+            hi[k] = j + len;
+            j += len;
+        }
+    }
+    nchains = 2 * P;
+    require(nchains * d_g <= num_sms(), "block-tridiagonal solver: blocks too large for the dense sweep kernel");
+    // ---- factor the strip interiors (couplings to the separators untouched)
+    std::vector<TriSys> strips(P);
+    for (int k = 0; k < P; ++k) {
+        for (int j = lo[k]; j < hi[k]; ++j) {
+            strips[k].m.push_back(bsz[j]);
+            strips[k].D.push_back(Dg(j));
+            if (j + 1 < hi[k]) strips[k].C.push_back(Cg(j));
+        }
+        strips[k].factor(h, st);
+    }
+    // ---- spikes and the separator system
+    std::vector<DBuf<double>> Wt(P), Wb(P);
+    TriSys seps;
+    std::vector<DBuf<double>> sD, sC;
+    if (P > 1) {
+        for (int k = 0; k < P; ++k) {
+            const TriSys& S = strips[k];
+            const long long nI = S.rows();
+            if (k > 0) {  // W_top = A_II^{-1} A_{I,s_k}: block lo rows hold A_{lo,s} = C(s)
+                const int s = sep[k - 1];
+                Wt[k].alloc((size_t)nI * bsz[s]);
+                Wt[k].zero(st);
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, bsz[lo[k]], bsz[s], &one, Cg(s), bsz[lo[k]], &zero,
+                                         Cg(s), bsz[lo[k]], Wt[k].p, nI));
+                S.solve_multi(h, Wt[k].p, bsz[s]);
+            }
+            if (k < P - 1) {  // W_bot = A_II^{-1} A_{I,s_{k+1}}: block hi-1 rows hold A_{hi-1,s'} = C(hi-1)^T
+                const int s = sep[k], jl = hi[k] - 1;
+                Wb[k].alloc((size_t)nI * bsz[s]);
+                Wb[k].zero(st);
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, bsz[jl], bsz[s], &one, Cg(jl), bsz[s], &zero,
+                                         Cg(jl), bsz[s], Wb[k].p + S.ro[S.nb() - 1], nI));
+                S.solve_multi(h, Wb[k].p, bsz[s]);
+            }
+        }
+        const int ns = P - 1;
+        sD.resize(ns);
+        sC.resize(std::max(ns - 1, 0));
+        for (int i = 0; i < ns; ++i) {
+            const int s = sep[i], ms = bsz[s];
+            const int ka = i, kb = i + 1;  // strips above (ends at s-1) and below (starts at s+1)
+            sD[i].alloc((size_t)ms * ms);
+            PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, ms, ms, &one, Dg(s), ms, &zero, Dg(s), ms, sD[i].p, ms));
+            // - A_{s,lo} W_top[lo] = - C(s)^T W_top_kb[lo block]
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, ms, ms, bsz[s + 1], &mone, Cg(s), bsz[s + 1], Wt[kb].p,
+                                     strips[kb].rows(), &one, sD[i].p, ms));
+            // - A_{s,s-1} W_bot[s-1] = - C(s-1) W_bot_ka[last block]
+            const TriSys& A = strips[ka];
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, ms, ms, bsz[s - 1], &mone, Cg(s - 1), ms,
+                                     Wb[ka].p + A.ro[A.nb() - 1], A.rows(), &one, sD[i].p, ms));
+            if (i + 1 < ns) {  // S_{i+1,i} = -(A_{s,lo} W_bot_kb[lo])^T = -W_bot_kb[lo]^T C(s)
+                const int s2 = sep[i + 1];
+                sC[i].alloc((size_t)bsz[s2] * ms);
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, bsz[s2], ms, bsz[s + 1], &mone, Wb[kb].p,
+                                         strips[kb].rows(), Cg(s), bsz[s + 1], &zero, sC[i].p, bsz[s2]));
+            }
+            seps.m.push_back(ms);
+            seps.D.push_back(sD[i].p);
+            if (i + 1 < ns) seps.C.push_back(sC[i].p);
+        }
+        seps.factor(h, st);
+    }
+    // ---- LL regions (per right-hand side): Y [0,n) forward y, X [n,2n) final x,
+    //      twist parts per system, G (separator rhs), SY (separator forward y)
+    const long long X_ = n;
+    long long lltop = 2LL * n;
+    auto llalloc = [&](long long len) {
+        const long long o = lltop;
+        lltop += len;
+        return o;
     };
-    std::vector<DenseTask> top, bot;
+    // ---- step lists per chain
+    std::vector<std::vector<DenseTask>> ch(nchains);
     std::vector<Mat> mats;
     long long o = 0;
     int ldmax = 2;
-    const DenseTask idle{-1, -1, -1, -1, -1, -1, 0, 0, 0, 0};
     factor_bytes = 0.0;
-    auto add = [&](int kind, int j, int mout, int n0, long long in0, long long b0, int n1, long long in1,
+    const DenseTask idle{-1, -1, -1, -1, -1, -1, 0, 0, 0, 0, -1, 0, 0};
+    auto add = [&](const Mat& mt, int mout, int n0, long long in0, long long b0, int n1, long long in1,
                    long long out_ll, long long out_x) {
         DenseTask tk = idle;
         tk.ld = pad(n0 + n1);
@@ -244,86 +481,214 @@ void BlockTriChol::dense_finish(LaHandles& h, const double* dense, const double*
         tk.out_ll = out_ll;
         tk.out_x = out_x;
         ldmax = std::max(ldmax, tk.ld);
-        mats.push_back({kind, j, o, tk.ld});
+        Mat m2 = mt;
+        m2.off = o;
+        m2.ld = tk.ld;
+        mats.push_back(m2);
         o = al(o + (long long)mout * tk.ld);
         factor_bytes += 8.0 * mout * (n0 + n1);
         return tk;
     };
-    // forward: y_j of the top blocks, then p_top; bottom blocks, then p_bot
-    for (int j = 0; j < t; ++j)
-        top.push_back(add(0, j, bsz[j], bsz[j], -1, boff[j], j > 0 ? bsz[j - 1] : 0, j > 0 ? boff[j - 1] : -1, boff[j], -1));
-    top.push_back(add(2, t, bsz[t], bsz[t], -1, boff[t], t > 0 ? bsz[t - 1] : 0, t > 0 ? boff[t - 1] : -1, PT, -1));
-    for (int j = nb - 1; j > t; --j)
-        bot.push_back(add(1, j, bsz[j], bsz[j], -1, boff[j], j < nb - 1 ? bsz[j + 1] : 0, j < nb - 1 ? boff[j + 1] : -1,
-                          boff[j], -1));
-    if (t < nb - 1) bot.push_back(add(3, t, bsz[t], bsz[t + 1], boff[t + 1], -1, 0, -1, PB, -1));
-    const int L = std::max(top.size(), bot.size());
-    while ((int)top.size() < L) top.push_back(idle);
-    while ((int)bot.size() < L) bot.push_back(idle);
-    // twist (top chain)
-    top.push_back(add(4, t, bsz[t], bsz[t], PT, -1, t < nb - 1 ? bsz[t] : 0, t < nb - 1 ? PB : -1, X_ + boff[t], boff[t]));
-    bot.push_back(idle);
-    for (int s = 1; s < nb; ++s) {
-        const int jt = t - s, jb = t + s;
-        if (jt < 0 && jb > nb - 1) break;
-        top.push_back(jt >= 0 ? add(5, jt, bsz[jt], bsz[jt], boff[jt], -1, bsz[jt + 1], X_ + boff[jt + 1],
-                                    jt > 0 ? X_ + boff[jt] : -1, boff[jt])
-                              : idle);
-        bot.push_back(jb <= nb - 1 ? add(6, jb, bsz[jb], bsz[jb], boff[jb], -1, bsz[jb - 1], X_ + boff[jb - 1],
-                                         jb < nb - 1 ? X_ + boff[jb] : -1, boff[jb])
-                                   : idle);
+    // a twisted solve of system S on chains (ct, cb)
+    auto build = [&](const TriSys& S, const SysIO& io, int ct, int cb) {
+        const int nn = S.nb(), t = S.t;
+        auto mk = [&](int kind, int j) { return Mat{kind, &S, j, 0, 0}; };
+        auto rhs_in = [&](int j, long long& in, long long& b0) {
+            in = io.rhs_ll[j];
+            b0 = io.rhs_b[j];
+        };
+        std::vector<DenseTask> top, bot;
+        for (int j = 0; j < t; ++j) {
+            long long in, b0;
+            rhs_in(j, in, b0);
+            top.push_back(add(mk(MK_TOPF, j), S.m[j], S.m[j], in, b0, j > 0 ? S.m[j - 1] : 0, j > 0 ? io.y_ll[j - 1] : -1,
+                              io.y_ll[j], -1));
+        }
+        {
+            long long in, b0;
+            rhs_in(t, in, b0);
+            top.push_back(add(mk(MK_PTOP, t), S.m[t], S.m[t], in, b0, t > 0 ? S.m[t - 1] : 0, t > 0 ? io.y_ll[t - 1] : -1,
+                              io.pt, -1));
+        }
+        for (int j = nn - 1; j > t; --j) {
+            long long in, b0;
+            rhs_in(j, in, b0);
+            bot.push_back(add(mk(MK_BOTF, j), S.m[j], S.m[j], in, b0, j < nn - 1 ? S.m[j + 1] : 0,
+                              j < nn - 1 ? io.y_ll[j + 1] : -1, io.y_ll[j], -1));
+        }
+        if (t < nn - 1) bot.push_back(add(mk(MK_PBOT, t), S.m[t], S.m[t + 1], io.y_ll[t + 1], -1, 0, -1, io.pb, -1));
+        const size_t L = std::max(top.size(), bot.size());
+        while (top.size() < L) top.push_back(idle);
+        while (bot.size() < L) bot.push_back(idle);
+        top.push_back(add(mk(MK_TWIST, t), S.m[t], S.m[t], io.pt, -1, t < nn - 1 ? S.m[t] : 0, t < nn - 1 ? io.pb : -1,
+                          io.x_ll[t], io.x_out[t]));
+        bot.push_back(idle);
+        for (int s = 1; s < nn; ++s) {
+            const int jt = t - s, jb = t + s;
+            if (jt < 0 && jb > nn - 1) break;
+            top.push_back(jt >= 0 ? add(mk(MK_TOPB, jt), S.m[jt], S.m[jt], io.y_ll[jt], -1, S.m[jt + 1],
+                                        io.x_ll[jt + 1], io.x_ll[jt], io.x_out[jt])
+                                  : idle);
+            bot.push_back(jb <= nn - 1 ? add(mk(MK_BOTB, jb), S.m[jb], S.m[jb], io.y_ll[jb], -1, S.m[jb - 1],
+                                             io.x_ll[jb - 1], io.x_ll[jb], io.x_out[jb])
+                                       : idle);
+        }
+        for (auto& tk : top) ch[ct].push_back(tk);
+        for (auto& tk : bot) ch[cb].push_back(tk);
+    };
+    // phase 1: strip interiors (rhs from b; y, x, x_ll in global numbering)
+    for (int k = 0; k < P; ++k) {
+        const TriSys& S = strips[k];
+        SysIO io;
+        for (int j = lo[k]; j < hi[k]; ++j) {
+            io.rhs_ll.push_back(-1);
+            io.rhs_b.push_back(boff[j]);
+            io.y_ll.push_back(boff[j]);
+            io.x_ll.push_back(X_ + boff[j]);
+            io.x_out.push_back(boff[j]);
+        }
+        io.pt = llalloc(S.m[S.t]);
+        io.pb = llalloc(S.m[S.t]);
+        build(S, io, 2 * k, 2 * k + 1);
     }
-    store.alloc(std::max<long long>(o, 1));
-    for (const Mat& mt : mats) {
-        const int j = mt.j, mj = bsz[j], ld = mt.ld;
-        double* X = store.p + mt.off;  // col-major (row length) x (output rows), leading dimension ld
-        switch (mt.kind) {
-            case 0:    // [Linv_j | -Linv_j K_{j-1}]  ->  [Linv_j^T; -K_{j-1}^T Linv_j^T]
-            case 2: {  // p_top, the same with j = t
-                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X, ld));
-                if (j > 0)
-                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, bsz[j - 1], mj, mj, &mone, Kt(j - 1), mj, Li(j),
-                                             mj, &zero, X + mj, ld));
-                break;
-            }
-            case 1: {  // [Linv'_j | -Linv'_j K'_{j+1}]  ->  [Linv'_j^T; -K'_{j+1}^T Linv'_j^T]
-                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X, ld));
-                if (j < nb - 1)
-                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, bsz[j + 1], mj, mj, &mone, Kb(j + 1), mj, Li(j),
-                                             mj, &zero, X + mj, ld));
-                break;
-            }
-            case 3:  // [-Linv_t K'_{t+1}]  ->  -K'_{t+1}^T Linv_t^T
-                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, bsz[j + 1], mj, mj, &mone, Kb(j + 1), mj, Li(j), mj,
-                                         &zero, X, ld));
-                break;
-            case 4: {  // [Linv_t^T | Linv_t^T]  ->  [Linv_t; Linv_t]
-                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X, ld));
-                if (t < nb - 1)
-                    PDG_CUBLAS_D(
-                        cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X + mj, ld));
-                break;
-            }
-            case 5: {  // [Linv_j^T | -Linv_j^T K_j^T]  ->  [Linv_j; -K_j Linv_j]
-                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X, ld));
-                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, bsz[j + 1], mj, mj, &mone, Kt(j), bsz[j + 1],
-                                         Li(j), mj, &zero, X + mj, ld));
-                break;
-            }
-            default: {  // [Linv'_j^T | -Linv'_j^T K'_j^T]  ->  [Linv'_j; -K'_j Linv'_j]
-                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, Li(j), mj, &zero, Li(j), mj, X, ld));
-                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, bsz[j - 1], mj, mj, &mone, Kb(j), bsz[j - 1],
-                                         Li(j), mj, &zero, X + mj, ld));
-                break;
+    if (P > 1) {
+        // phase 2: separator right-hand sides g_s = b_s - C(s-1) y_{s-1} - C(s)^T y_{s+1} (chain 2i)
+        const int ns = P - 1;
+        std::vector<long long> g_ll(ns);
+        for (int i = 0; i < ns; ++i) g_ll[i] = llalloc(bsz[sep[i]]);
+        for (int i = 0; i < ns; ++i) {
+            const int s = sep[i];
+            Mat mt{MK_GSTEP, nullptr, s, 0, 0};
+            mt.a = Cg(s - 1);
+            mt.ma = bsz[s - 1];
+            mt.lda = bsz[s];
+            mt.c = Cg(s);
+            mt.mc = bsz[s + 1];
+            mt.ldc = bsz[s + 1];
+            DenseTask tk = add(mt, bsz[s], bsz[s - 1], X_ + boff[s - 1], -1, bsz[s + 1], X_ + boff[s + 1], g_ll[i], -1);
+            tk.base = boff[s];
+            ch[2 * i].push_back(tk);
+        }
+        // phase 3: the separator system on chains 0/1
+        SysIO io;
+        for (int i = 0; i < ns; ++i) {
+            io.rhs_ll.push_back(g_ll[i]);
+            io.rhs_b.push_back(-1);
+            io.y_ll.push_back(llalloc(bsz[sep[i]]));
+            io.x_ll.push_back(X_ + boff[sep[i]]);
+            io.x_out.push_back(boff[sep[i]]);
+        }
+        io.pt = llalloc(seps.m[seps.t]);
+        io.pb = llalloc(seps.m[seps.t]);
+        size_t L = 0;
+        for (auto& c : ch) L = std::max(L, c.size());
+        for (int c = 0; c < 2; ++c)
+            while (ch[c].size() < L) ch[c].push_back(idle);  // after every g step (LL waits anyway)
+        build(seps, io, 0, 1);
+        // phase 4: x_I += -[W_top | W_bot] [x_{s_k}; x_{s_{k+1}}], block by block (chains of the strip)
+        for (int k = 0; k < P; ++k) {
+            const TriSys& S = strips[k];
+            for (int jj = 0; jj < S.nb(); ++jj) {
+                const int j = lo[k] + jj;
+                Mat mt{MK_CORR, &S, jj, 0, 0};
+                int n0 = 0, n1 = 0;
+                long long in0 = -1, in1 = -1;
+                if (k > 0) {
+                    mt.a = Wt[k].p + S.ro[jj];
+                    mt.ma = bsz[sep[k - 1]];
+                    mt.lda = static_cast<int>(S.rows());
+                    n0 = mt.ma;
+                    in0 = X_ + boff[sep[k - 1]];
+                }
+                if (k < P - 1) {
+                    const double* w = Wb[k].p + S.ro[jj];
+                    const int mw = bsz[sep[k]];
+                    if (n0 == 0) {
+                        mt.a = w;
+                        mt.ma = mw;
+                        mt.lda = static_cast<int>(S.rows());
+                        n0 = mw;
+                        in0 = X_ + boff[sep[k]];
+                    } else {
+                        mt.c = w;
+                        mt.mc = mw;
+                        mt.ldc = static_cast<int>(S.rows());
+                        n1 = mw;
+                        in1 = X_ + boff[sep[k]];
+                    }
+                }
+                DenseTask tk = add(mt, bsz[j], n0, in0, -1, n1, in1, -1, boff[j]);
+                tk.acc = 1;
+                ch[jj <= S.t ? 2 * k : 2 * k + 1].push_back(tk);
             }
         }
     }
-    dsched.clear();
-    for (size_t s = 0; s < top.size(); ++s) {
-        dsched.push_back(top[s]);
-        dsched.push_back(bot[s]);
+    // ---- fill the step matrices (row-major = col-major of the transpose, leading dim ld)
+    store.alloc(std::max<long long>(o, 1));
+    for (const Mat& mt : mats) {
+        double* X = store.p + mt.off;
+        const int ld = mt.ld;
+        if (mt.kind == MK_GSTEP) {  // [-C(s-1) | -C(s)^T] -> [-C(s-1)^T; -C(s)]
+            const int ms = mt.lda;
+            PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mt.ma, ms, &mone, mt.a, ms, &zero, mt.a, ms, X, ld));
+            PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mt.mc, ms, &mone, mt.c, mt.ldc, &zero, mt.c, mt.ldc,
+                                     X + mt.ma, ld));
+            continue;
+        }
+        if (mt.kind == MK_CORR) {  // rows of -[W_top | W_bot] -> [-W_top[rows]^T; -W_bot[rows]^T]
+            const int mj = mt.sys->m[mt.j];
+            PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mt.ma, mj, &mone, mt.a, mt.lda, &zero, mt.a, mt.lda,
+                                     X, ld));
+            if (mt.c)
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mt.mc, mj, &mone, mt.c, mt.ldc, &zero, mt.c,
+                                         mt.ldc, X + mt.ma, ld));
+            continue;
+        }
+        const TriSys& S = *mt.sys;
+        const int j = mt.j, mj = S.m[j], nn = S.nb();
+        switch (mt.kind) {
+            case MK_TOPF:
+            case MK_PTOP:  // [Linv_j | -Linv_j K_{j-1}] -> [Linv_j^T; -K_{j-1}^T Linv_j^T]
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj, X, ld));
+                if (j > 0)
+                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j - 1], mj, mj, &mone, S.Kt(j - 1), mj,
+                                             S.Li(j), mj, &zero, X + mj, ld));
+                break;
+            case MK_BOTF:  // [Linv'_j | -Linv'_j K'_{j+1}] -> [Linv'_j^T; -K'_{j+1}^T Linv'_j^T]
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj, X, ld));
+                if (j < nn - 1)
+                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j + 1], mj, mj, &mone, S.Kb(j + 1), mj,
+                                             S.Li(j), mj, &zero, X + mj, ld));
+                break;
+            case MK_PBOT:  // [-Linv_t K'_{t+1}] -> -K'_{t+1}^T Linv_t^T
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j + 1], mj, mj, &mone, S.Kb(j + 1), mj,
+                                         S.Li(j), mj, &zero, X, ld));
+                break;
+            case MK_TWIST:  // [Linv_t^T | Linv_t^T] -> [Linv_t; Linv_t]
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj, X, ld));
+                if (j < nn - 1)
+                    PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj,
+                                             X + mj, ld));
+                break;
+            case MK_TOPB:  // [Linv_j^T | -Linv_j^T K_j^T] -> [Linv_j; -K_j Linv_j]
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj, X, ld));
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, S.m[j + 1], mj, mj, &mone, S.Kt(j), S.m[j + 1],
+                                         S.Li(j), mj, &zero, X + mj, ld));
+                break;
+            default:  // MK_BOTB: [Linv'_j^T | -Linv'_j^T K'_j^T] -> [Linv'_j; -K'_j Linv'_j]
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, mj, mj, &one, S.Li(j), mj, &zero, S.Li(j), mj, X, ld));
+                PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, S.m[j - 1], mj, mj, &mone, S.Kb(j), S.m[j - 1],
+                                         S.Li(j), mj, &zero, X + mj, ld));
+                break;
+        }
     }
+    size_t L = 0;
+    for (auto& c : ch) L = std::max(L, c.size());
+    dsched.assign(L * nchains, idle);
+    for (int c = 0; c < nchains; ++c)
+        for (size_t s = 0; s < ch[c].size(); ++s) dsched[s * nchains + c] = ch[c][s];
     d_dsched.upload(dsched, st);
+    d_lln = lltop;
     // ---- kernel configuration ------------------------------------------------------
     require(2 * max_b <= 256 * DNI, "block-tridiagonal solver: blocks too large for the dense sweep kernel");
     int dev = 0;
@@ -331,10 +696,8 @@ void BlockTriChol::dense_finish(LaHandles& h, const double* dense, const double*
     int optin = 0;
     PDG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     PDG_CUDA(cudaFuncSetAttribute(k_sweep_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    const int nsteps = static_cast<int>(dsched.size() / 2);
+    const int nsteps = static_cast<int>(L);
     d_ldmax = ldmax;
-    d_g = (max_b + 7) / 8;
-    require(2 * d_g <= num_sms(), "block-tridiagonal solver: blocks too large for the dense sweep kernel");
     const size_t fixed = sizeof(double) * 8 * 16 + 8 * 16 + sizeof(DenseTask) * nsteps + 64;
     const size_t unit = sizeof(double) * 8 * ldmax;
     require(fixed + unit <= (size_t)optin - 1024, "block-tridiagonal solver: dense sweep shared memory");
@@ -353,7 +716,8 @@ void BlockTriChol::dense_finish(LaHandles& h, const double* dense, const double*
 void BlockTriChol::solve_dense(const double* b, double* x, int nrhs, cudaStream_t st) {
     unsigned flag = static_cast<unsigned>(++call);
     if (flag == 0) flag = static_cast<unsigned>(++call);  // 0 = never published
-    int nsteps = static_cast<int>(dsched.size() / 2), nr = nrhs, n_ = n, ldm = d_ldmax, stg = d_stages, g = d_g;
+    int nsteps = static_cast<int>(dsched.size() / nchains), nr = nrhs, n_ = n, ldm = d_ldmax, stg = d_stages, g = d_g;
+    int nch = nchains;
     int pf = 4;
     if (const char* e = std::getenv("PDG_SWEEP_PF")) pf = std::atoi(e);
     long long lln = d_lln;
@@ -363,12 +727,12 @@ void BlockTriChol::solve_dense(const double* b, double* x, int nrhs, cudaStream_
     unsigned long long* dbgp = nullptr;
     dbg_steps = nsteps;
     if (debug_timing) {
-        dbg.alloc((size_t)2 * g * nsteps * 4);
+        dbg.alloc((size_t)nch * g * nsteps * 4);
         dbg.zero(st);
         dbgp = dbg.p;
     }
-    void* args[] = {&nsteps, &sched, &nr, &n_, &sp, &ldm, &b, &x, &llp, &lln, &flag, &stg, &pf, &g, &dbgp};
-    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_sweep_dense, 2 * g, 256, args, d_smem, st));
+    void* args[] = {&nsteps, &sched, &nr, &n_, &sp, &ldm, &b, &x, &llp, &lln, &flag, &stg, &pf, &g, &nch, &dbgp};
+    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_sweep_dense, nch * g, 256, args, d_smem, st));
     count_launch(1);
     PDG_CHECK_LAUNCH();
 }

@@ -399,7 +399,7 @@ int pdg_debug_recurrence_timing(pdg_block* blk, int which, unsigned long long* o
     PDG_CUDA(cudaStreamSynchronize(st));
     c.debug_timing = false;
     std::vector<unsigned long long> h = c.dbg.download(st);
-    *ctas = c.local ? 2 * c.sw_g : 2 * c.d_g;
+    *ctas = c.local ? 2 * c.sw_g : c.nchains * c.d_g;
     *nsteps = c.dbg_steps;
     std::memcpy(out, h.data(), sizeof(unsigned long long) * std::min<long long>(cap, (long long)h.size()));
     API_END

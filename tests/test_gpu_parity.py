@@ -384,3 +384,27 @@ def test_fixed_stress_solver_errors_and_dg1():
     fs = S.FixedStressSolver(ops, 0, 0.1, S.FixedStressConfig(max_sweeps=1, tol=1e-15))
     with pytest.raises(S.SolverError, match="fixed-stress did not converge"):
         fs.solve(P.uniform_vector(5, ops.n_total))
+
+
+@pytest.mark.parametrize("strips", [2, 3])
+def test_flow_substructured_strips_match_oracle(oracle, monkeypatch, strips):
+    """Opt-in substructured flow solve (PDG_FLOW_STRIPS: strip interiors by
+    twisted sweeps, separator system, spike corrections; blocktri_dense.cu):
+    the same preconditioner as fixed_stress.hpp:109-139 within the exact-solver
+    band, bit-identical repeats; its linear-map roundoff stays below 1e-10."""
+    monkeypatch.setenv("PDG_FLOW_STRIPS", str(strips))
+    spec = P.config1(32)
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    blk = S.BlockSolver(ops, np.array([[1.7]]), 0.05)
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(blk.rows)
+    z = blk.precondition(r)
+    z_ref = rp.precondition(1.7, 0.05, r, backend=0)
+    z_band = rp.precondition(1.7, 0.05, r, backend=1)
+    band = np.linalg.norm(z_band - z_ref) / np.linalg.norm(z_ref)
+    assert np.linalg.norm(z - z_ref) <= max(1e-10, 10 * band) * np.linalg.norm(z_ref)
+    assert np.array_equal(z, blk.precondition(r))
+    r2 = rng.standard_normal(blk.rows)
+    zc = blk.precondition(0.3 * r - 1.7 * r2)
+    assert np.max(np.abs(zc - (0.3 * z - 1.7 * blk.precondition(r2)))) <= 1e-10 * np.max(np.abs(zc))
