@@ -148,6 +148,46 @@ def spmv_sweep(sizes, reps, peak):
     return out
 
 
+def spmv_distributed(n, reps, peak, rank, world, dist):
+    """Config 3 at N GPUs, strong scaling: every rank owns a strip of cell rows of
+    the n x n operator (parallel.DeviceStripSpMV), one application = NCCL halo
+    exchange + strip SpMV. Per rank: exchange timed with CUDA events on torch's
+    stream, SpMV with CUDA events on the library stream; max over ranks."""
+    import torch
+    from paper_1801_04984_b200 import parallel as par, problem as P, solver as S
+    T = S.time_constants(1)["T"]
+    ops = S.SpatialOperators.assemble(P.config3(n), device=torch.cuda.current_device())
+    op = S.SpaceTimeOperator(ops, T, 0.05)
+    sp = par.DeviceStripSpMV(op, n, n, 2, rank, world, dist)
+    x = torch.from_numpy(P.uniform_vector(P.X_SEED, op.rows)).cuda()
+    y = torch.zeros_like(x)
+    for _ in range(3):
+        sp.apply(x, y)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ex_ms, sp_ms = 0.0, 0.0
+    for _ in range(reps):
+        e0.record()
+        sp.exchange(x)
+        e1.record()
+        e1.synchronize()
+        ex_ms += e0.elapsed_time(e1)
+        sp_ms += sp.op.apply_strip_device(x.data_ptr(), y.data_ptr(), 1, True)[0]
+    t = torch.tensor([(ex_ms + sp_ms) / reps, ex_ms / reps, sp_ms / reps], dtype=torch.float64, device=x.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    b_alg = 8.0 * (op.nnz + 2 * op.rows)
+    out = {"n": n, "n_gpus": world, "scaling": "strong", "rows": op.rows, "ms_per_apply": ms,
+           "exchange_ms": float(t[1]), "spmv_ms": float(t[2]), "gdof_s": op.rows / (ms * 1e-3) / 1e9,
+           "achieved_GBs_total": b_alg / (ms * 1e-3) / 1e9, "frac_of_n_gpus_peak": b_alg / (ms * 1e-3) / 1e9 / (peak * world),
+           "halo_doubles_per_rank": sp.halo_doubles,
+           "note": "strip-partitioned rows (parallel.DeviceStripSpMV), NCCL send/recv halo, max over ranks"}
+    del sp, op, ops, x, y
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -274,6 +314,9 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_dev, e2e_ms, ms_ref = float(t[0]), float(t[1]), float(t[2])
 
+    spmv_dist = None
+    if world > 1 and args.spmv_sizes:
+        spmv_dist = spmv_distributed(int(args.spmv_sizes.split(",")[-1]), 20, peak, rank, world, torch.distributed)
     spmv = spmv_sweep([int(s) for s in args.spmv_sizes.split(",") if s], args.spmv_reps, peak) \
         if rank == 0 and args.spmv_sizes else []
     spmv_roof = None
@@ -314,7 +357,8 @@ def main():
             "e2e": {"value": e2e_ms, "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
                     "d2h_bytes_per_step": 8 * nn * nt},
             "gpu_launches": int(main_run["launches"]), "roofline": roofline, "spmv_roofline": spmv_roof,
-            "phases": phases, "spmv": spmv, "clocks": main_run["clocks"], "cpu_baseline": cpu}), flush=True)
+            "phases": phases, "spmv": spmv, "spmv_distributed": spmv_dist, "clocks": main_run["clocks"],
+            "cpu_baseline": cpu}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -143,6 +143,13 @@ int pdg_op_rows(const pdg_op* op, long long* rows, long long* nnz);
 /* y = op(x) `repeats` times on device buffers; per-launch times (ms) into times_ms[repeats] if not NULL. */
 int pdg_op_apply_device(pdg_op* op, const double* x_dev, double* y_dev, int repeats, float* times_ms);
 int pdg_op_download_csr(const pdg_op* op, long long* row_offsets, int* col_indices, double* values);
+/* Multi-GPU row partitioning: this rank owns the strip of cell rows
+ * [r0, r1) of the nx x ny mesh (u and p rows of its cells, q rows of its face rows:
+ * horizontal faces of level j belong to row min(j, ny-1), vertical faces to their
+ * row). apply_strip writes only the owned rows of y; x must hold the owned entries
+ * and the one-cell-row halo (global numbering). Bit-identical per row to apply. */
+int pdg_op_set_strip(pdg_op* op, int nx, int ny, int r0, int r1);
+int pdg_op_apply_strip_device(pdg_op* op, const double* x_dev, double* y_dev, int repeats, float* times_ms);
 void pdg_op_destroy(pdg_op* op);
 
 /* Per-phase device timing (CUDA events on the library stream). Phases:

@@ -99,6 +99,8 @@ _SIGS = {
     "pdg_op_create": (C.c_int, [VP, C.c_int, DP, C.c_double, C.POINTER(VP)]),
     "pdg_op_rows": (C.c_int, [VP, LLP, LLP]),
     "pdg_op_apply_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_float)]),
+    "pdg_op_set_strip": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "pdg_op_apply_strip_device": (C.c_int, [VP, VP, VP, C.c_int, C.POINTER(C.c_float)]),
     "pdg_op_download_csr": (C.c_int, [VP, LLP, IP, DP]),
     "pdg_op_destroy": (None, [VP]),
     "pdg_profile_enable": (None, [C.c_int]),

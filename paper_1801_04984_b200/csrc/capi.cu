@@ -445,6 +445,30 @@ int pdg_op_apply_device(pdg_op* op, const double* x_dev, double* y_dev, int repe
     API_END
 }
 
+int pdg_op_set_strip(pdg_op* op, int nx, int ny, int r0, int r1) {
+    API_BEGIN
+    require(op, "pdg_op_set_strip: null argument");
+    op->op.set_strip(nx, ny, r0, r1, op->ctx->stream);
+    API_END
+}
+
+int pdg_op_apply_strip_device(pdg_op* op, const double* x_dev, double* y_dev, int repeats, float* times_ms) {
+    API_BEGIN
+    require(op && x_dev && y_dev, "pdg_op_apply_strip_device: null argument");
+    cudaStream_t st = op->ctx->stream;
+    for (int i = 0; i < std::max(repeats, 1); ++i) {
+        PDG_CUDA(cudaEventRecord(op->e0, st));
+        op->op.apply_strip(x_dev, y_dev, st);
+        PDG_CUDA(cudaEventRecord(op->e1, st));
+        if (times_ms) {
+            PDG_CUDA(cudaEventSynchronize(op->e1));
+            PDG_CUDA(cudaEventElapsedTime(&times_ms[i], op->e0, op->e1));
+        }
+    }
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
 int pdg_op_download_csr(const pdg_op* op, long long* row_offsets, int* col_indices, double* values) {
     API_BEGIN
     require(op && row_offsets && col_indices && values, "pdg_op_download_csr: null argument");

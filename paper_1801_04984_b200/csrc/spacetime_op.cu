@@ -183,6 +183,77 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, long l
     }
 }
 
+// Owned-row test of an S-class row for the strip of cell rows [r0, r1):
+// flux rows by face row (horizontal faces level j -> row min(j, ny-1), vertical
+// faces column-major -> their row, mesh.hpp:59-60), pressure rows by cell row.
+__device__ __forceinline__ bool s_row_owned(long long srow, int nq, int np, int nx, int ny, int r0, int r1) {
+    const int loc = static_cast<int>(srow % (nq + np));
+    int row;
+    if (loc < nq) {
+        const int nh = nx * (ny + 1);
+        row = loc < nh ? min(loc / nx, ny - 1) : (loc - nh) % ny;
+    } else {
+        row = (loc - nq) / nx;
+    }
+    return row >= r0 && row < r1;
+}
+
+// k_spmv restricted to a strip: U groups of the strip's cells (every component),
+// the listed S slices, writes masked to owned rows.
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_strip(long long u_threads, int cell0, int ncells_strip, int gu,
+                                                           long long n_slices, const long long* __restrict__ slices,
+                                                           long long s_rows,
+                                                           int n_cells, int nt, int nu, int nq, int np, int nx, int ny,
+                                                           int r0, int r1, const long long* __restrict__ u_off,
+                                                           const int* __restrict__ u_col, const double* __restrict__ u_val,
+                                                           const long long* __restrict__ s_off, const int* __restrict__ s_len,
+                                                           const int* __restrict__ s_col, const double* __restrict__ s_val,
+                                                           const double* __restrict__ x, double* __restrict__ y) {
+    if (static_cast<int>(blockIdx.x) < gu) {
+        const long long stride = (long long)gu * blockDim.x;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
+            const long long gl = t >> 3;  // local group: component-major over the strip's cells
+            const int l = static_cast<int>(t & 7);
+            const int i = static_cast<int>(gl / ncells_strip);
+            const int c = cell0 + static_cast<int>(gl % ncells_strip);
+            const long long g = (long long)i * n_cells + c;
+            const long long b = __ldg(&u_off[g]), e = __ldg(&u_off[g + 1]);
+            double s = 0.0;
+#pragma unroll 8
+            for (long long k = b; k < e; ++k) {
+                const double v = __ldcs(&u_val[k * 8 + l]);
+                const double xv = __ldg(&x[__ldg(&u_col[k])]);
+                s = __dadd_rn(s, __dmul_rn(v, xv));
+            }
+            y[(long long)i * nt + 8 * c + l] = s;
+        }
+    } else {
+        const int bid = blockIdx.x - gu;
+        const long long stride = (long long)(gridDim.x - gu) * blockDim.x;
+        for (long long t = bid * (long long)blockDim.x + threadIdx.x; t < n_slices * 32; t += stride) {
+            const long long sl = __ldg(&slices[t >> 5]);
+            const int lane = static_cast<int>(t & 31);
+            const long long srow = sl * 32 + lane;
+            if (srow >= s_rows) continue;
+            const long long b = __ldg(&s_off[sl]);
+            const int len = __ldg(&s_len[srow]);
+            double s = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < len; ++k) {
+                const long long pos = (b + k) * 32 + lane;
+                const double v = __ldcs(&s_val[pos]);
+                const double xv = __ldg(&x[__ldcs(&s_col[pos])]);
+                s = __dadd_rn(s, __dmul_rn(v, xv));
+            }
+            if (s_row_owned(srow, nq, np, nx, ny, r0, r1)) {
+                const int i = static_cast<int>(srow / (nq + np));
+                const int loc = static_cast<int>(srow - (long long)i * (nq + np));
+                y[(long long)i * nt + nu + loc] = s;
+            }
+        }
+    }
+}
+
 long long exclusive_scan_ll(const long long* in, long long* out, long long n, cudaStream_t st) {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, st);
@@ -265,6 +336,54 @@ void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     k_spmv<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p, u_val.p,
                                            s_off.p, s_len.p, s_col.p, s_val.p, x, y);
+    count_launch();
+    PDG_CHECK_LAUNCH();
+}
+
+void SpaceTimeOp::set_strip(int nx, int ny, int r0, int r1, cudaStream_t st) {
+    require(nx > 0 && ny > 0 && (long long)nx * ny == n_cells, "space-time block: strip mesh does not match the operator");
+    require(0 <= r0 && r0 < r1 && r1 <= ny, "space-time block: bad strip rows");
+    strip_nx = nx;
+    strip_ny = ny;
+    strip_r0 = r0;
+    strip_r1 = r1;
+    // S slices holding an owned row (host scan of the row -> owner rule)
+    const int nh = nx * (ny + 1);
+    auto owned = [&](long long srow) {
+        const int loc = static_cast<int>(srow % (n_q + n_p));
+        int row;
+        if (loc < n_q)
+            row = loc < nh ? std::min(loc / nx, ny - 1) : (loc - nh) % ny;
+        else
+            row = (loc - n_q) / nx;
+        return row >= r0 && row < r1;
+    };
+    std::vector<long long> sl;
+    for (long long s = 0; s < s_slices; ++s) {
+        bool any = false;
+        for (int l = 0; l < 32 && !any; ++l) {
+            const long long srow = s * 32 + l;
+            any = srow < s_rows && owned(srow);
+        }
+        if (any) sl.push_back(s);
+    }
+    strip_slices.upload(sl, st);
+    strip_slices.n = sl.size();
+    PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void SpaceTimeOp::apply_strip(const double* x, double* y, cudaStream_t st) const {
+    require(strip_nx > 0, "space-time block: no strip set");
+    const int cell0 = strip_r0 * strip_nx, ncs = (strip_r1 - strip_r0) * strip_nx;
+    const long long u_threads = (long long)m * ncs * 8;
+    const long long ns = static_cast<long long>(strip_slices.n);
+    const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
+    const int gs = static_cast<int>(
+        std::max<long long>(1, std::min<long long>((ns * 32 + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16)));
+    ProfScope prof(PROF_SPMV, st, 0.0);
+    k_spmv_strip<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, cell0, ncs, gu, ns, strip_slices.p, s_rows, n_cells, nt, n_u, n_q,
+                                                 n_p, strip_nx, strip_ny, strip_r0, strip_r1, u_off.p, u_col.p, u_val.p,
+                                                 s_off.p, s_len.p, s_col.p, s_val.p, x, y);
     count_launch();
     PDG_CHECK_LAUNCH();
 }

@@ -39,6 +39,15 @@ struct SpaceTimeOp {
 
     void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st);
     void apply(const double* x, double* y, cudaStream_t st) const;
+    // Rows owned by the strip of cell rows [r0, r1) of an nx x ny mesh (multi-GPU
+    // row partitioning): displacement and pressure rows of its
+    // cells, flux rows of its face rows. Only owned y entries are written; x must
+    // hold the owned entries and the one-cell-row halo. Same per-row arithmetic as
+    // apply(): the union over strips is bit-identical to it.
+    int strip_nx = 0, strip_ny = 0, strip_r0 = 0, strip_r1 = 0;
+    DBuf<long long> strip_slices;  // S-class slices holding at least one owned row
+    void set_strip(int nx, int ny, int r0, int r1, cudaStream_t st);
+    void apply_strip(const double* x, double* y, cudaStream_t st) const;
     // canonical CSR download (tests / CPU bitwise check)
     void to_csr(std::vector<long long>& off, std::vector<int>& idx, std::vector<double>& val, cudaStream_t st) const;
 };

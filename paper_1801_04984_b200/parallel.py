@@ -543,3 +543,111 @@ def dist_gmres(op_plan, pre, b, dist, nranks, tol=1e-10, restart=50, max_iter=40
                 converged = true_res / bnorm <= tol
                 break
     return x, dict(converged=converged, iterations=total, final_rel_res=true_res / bnorm)
+
+
+# ---------------------------------------------------------------------------
+# Device path of the distributed operator (pdg_op_set_strip /
+# pdg_op_apply_strip_device): every rank keeps x in global numbering, computes
+# its strip's rows with the same per-row arithmetic as the single-GPU SpMV, and
+# exchanges a one-cell-row halo with its neighbours (NCCL send/recv through
+# torch.distributed on the device).
+# ---------------------------------------------------------------------------
+
+
+def strip_boundary_dofs(nx: int, ny: int, m: int, row: int):
+    """Global indices (m-component layout [u_0 q_0 p_0 | ...]) of the dofs a
+    neighbour needs from cell row `row`: u and p of its cells and the faces of
+    face row `row` (horizontal level `row`, plus the top level when row = ny-1,
+    and the vertical faces of the row)."""
+    n_u, nh = 8 * nx * ny, nx * (ny + 1)
+    n_q = nh + (nx + 1) * ny
+    n_p = nx * ny
+    nt = n_u + n_q + n_p
+    cells = row * nx + np.arange(nx)
+    u = (8 * cells[:, None] + np.arange(8)[None, :]).ravel()
+    levels = [row] + ([ny] if row == ny - 1 else [])
+    qh = np.concatenate([lv * nx + np.arange(nx) for lv in levels])
+    qv = nh + np.arange(nx + 1) * ny + row
+    q = n_u + np.concatenate([qh, qv])
+    p = n_u + n_q + cells
+    one = np.sort(np.concatenate([u, q, p]))
+    return np.concatenate([one + i * nt for i in range(m)])
+
+
+def strip_exchange_sets(nx: int, ny: int, m: int, strips, rank: int):
+    """send[k] / recv[k] global index sets between this rank and its neighbours."""
+    r0, r1 = strips[rank]
+    send, recv = {}, {}
+    if rank > 0:
+        send[rank - 1] = strip_boundary_dofs(nx, ny, m, r0)
+        recv[rank - 1] = strip_boundary_dofs(nx, ny, m, strips[rank - 1][1] - 1)
+    if rank < len(strips) - 1:
+        send[rank + 1] = strip_boundary_dofs(nx, ny, m, r1 - 1)
+        recv[rank + 1] = strip_boundary_dofs(nx, ny, m, strips[rank + 1][0])
+    return send, recv
+
+
+class StripHalo:
+    """The neighbour exchange of the strip partition on `device` tensors in
+    global numbering (point-to-point through torch.distributed: NCCL on GPUs,
+    gloo on the CPU in the tests)."""
+
+    def __init__(self, nx: int, ny: int, m: int, rank: int, nranks: int, dist=None, device="cuda"):
+        import torch
+
+        self.rank, self.nranks, self.dist = rank, nranks, dist
+        self.strips = strip_partition(ny, nranks)
+        send, recv = strip_exchange_sets(nx, ny, m, self.strips, rank)
+        dev = torch.device(device)
+        self.send = {k: torch.as_tensor(v, dtype=torch.int64, device=dev) for k, v in send.items()}
+        self.recv = {k: torch.as_tensor(v, dtype=torch.int64, device=dev) for k, v in recv.items()}
+        self.sbuf = {k: torch.empty(len(v), dtype=torch.float64, device=dev) for k, v in send.items()}
+        self.rbuf = {k: torch.empty(len(v), dtype=torch.float64, device=dev) for k, v in recv.items()}
+        self.halo_doubles = sum(len(v) for v in recv.values())
+
+    def exchange(self, x):
+        """Fill x's halo entries from the neighbours."""
+        if self.dist is None or self.nranks == 1:
+            return
+        reqs = []
+        for k, idx in sorted(self.send.items()):
+            torch_index_select(x, idx, self.sbuf[k])
+            reqs.append(self.dist.isend(self.sbuf[k], k))
+        for k in sorted(self.recv):
+            reqs.append(self.dist.irecv(self.rbuf[k], k))
+        for r in reqs:
+            r.wait()
+        for k, idx in self.recv.items():
+            x.index_copy_(0, idx, self.rbuf[k])
+
+
+class DeviceStripSpMV:
+    """y_owned = (A x)_owned on this rank's GPU for the strip partition of the
+    space-time operator `op` (solver.SpaceTimeOperator): halo exchange of the
+    neighbour boundary rows (StripHalo), then the strip SpMV
+    (pdg_op_apply_strip_device)."""
+
+    def __init__(self, op, nx: int, ny: int, m: int, rank: int, nranks: int, dist=None, device="cuda"):
+        self.op = op
+        self.halo = StripHalo(nx, ny, m, rank, nranks, dist, device)
+        r0, r1 = self.halo.strips[rank]
+        op.set_strip(nx, ny, r0, r1)
+        self.halo_doubles = self.halo.halo_doubles
+
+    def exchange(self, x):
+        self.halo.exchange(x)
+
+    def apply(self, x, y, repeats=1, times=False):
+        """Exchange, then the strip SpMV (y: owned rows written). The library runs
+        on its own stream, so the exchange is completed on torch's stream first."""
+        import torch
+
+        self.exchange(x)
+        torch.cuda.current_stream().synchronize()
+        return self.op.apply_strip_device(x.data_ptr(), y.data_ptr(), repeats, times)
+
+
+def torch_index_select(x, idx, out):
+    import torch
+
+    torch.index_select(x, 0, idx, out=out)

@@ -140,6 +140,15 @@ class SpaceTimeOperator:
         check(lib().pdg_op_download_csr(self._h, off.ctypes.data_as(_lib.LLP), _ip(idx), _dp(val)))
         return off, idx, val
 
+    def set_strip(self, nx: int, ny: int, r0: int, r1: int):
+        """Own the rows of the strip of cell rows [r0, r1) (multi-GPU partitioning)."""
+        check(lib().pdg_op_set_strip(self._h, nx, ny, r0, r1))
+
+    def apply_strip_device(self, x_ptr: int, y_ptr: int, repeats: int = 1, times: bool = False):
+        buf = (C.c_float * max(repeats, 1))() if times else None
+        check(lib().pdg_op_apply_strip_device(self._h, x_ptr, y_ptr, repeats, buf))
+        return [buf[i] for i in range(repeats)] if times else None
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib._lib is not None:
             _lib._lib.pdg_op_destroy(self._h)

@@ -207,3 +207,71 @@ def test_distributed_gmres_matches_oracle_gloo(world):
     for rank, its, its_ref, err in res:
         assert not isinstance(its, str), its
         assert abs(its - its_ref) <= 1 and err <= 1e-9, (rank, its, its_ref, err)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strip_exchange_sets_cover_the_halo(oracle, world):
+    """The device path's neighbour exchange (parallel.strip_exchange_sets) holds
+    every column the owned rows of the space-time operator read that the rank
+    does not own, and each rank sends only entries it owns."""
+    n, m = 8, 2
+    spec = P.config1(n)
+    rp = oracle.RefProblem(spec.to_dict())
+    off, idx, _ = rp.spacetime_csr(oracle.time_constants(1)["T"], 0.05)
+    strips = par.strip_partition(n, world)
+    owner = par.row_owner(n, n, m, strips)
+    for k in range(world):
+        rows = np.flatnonzero(owner == k)
+        cols = np.unique(np.concatenate([idx[off[r]:off[r + 1]] for r in rows]))
+        need = cols[owner[cols] != k]
+        send, recv = par.strip_exchange_sets(n, n, m, strips, k)
+        have = np.concatenate(list(recv.values())) if recv else np.zeros(0, np.int64)
+        assert np.all(np.isin(need, have)), k
+        for dst, s in send.items():
+            assert np.all(owner[s] == k)
+            assert np.array_equal(s, par.strip_exchange_sets(n, n, m, strips, dst)[1][k])
+
+
+def _halo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, m = 8, 2
+        strips = par.strip_partition(n, world)
+        owner = par.row_owner(n, n, m, strips)
+        truth = P.uniform_vector(P.X_SEED, len(owner))
+        x = torch.from_numpy(np.where(owner == rank, truth, np.nan))
+        halo = par.StripHalo(n, n, m, rank, world, dist, device="cpu")
+        halo.exchange(x)
+        _, recv = par.strip_exchange_sets(n, n, m, strips, rank)
+        got = np.concatenate([x.numpy()[v] for v in recv.values()])
+        ref = np.concatenate([truth[v] for v in recv.values()])
+        q.put((rank, bool(np.array_equal(got, ref)), bool(np.array_equal(x.numpy()[owner == rank], truth[owner == rank]))))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strip_halo_exchange_gloo(world):
+    """StripHalo (the exchange of the device distributed SpMV) delivers exactly
+    the neighbours' boundary values and leaves the owned entries alone."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok_halo, ok_own in res:
+        assert ok_halo is True and ok_own is True, (rank, ok_halo)
