@@ -443,3 +443,53 @@ def test_strip_spmv_is_the_single_gpu_spmv(oracle, world):
         assert torch.equal(yk[own], y_ref[own]), k
         covered |= owner == k
     assert covered.all()
+
+
+@pytest.mark.parametrize("restart,candidate", [(2, "reference"), (3, "flexible"), (1, "reference")])
+def test_gmres_restart_accounting_matches_oracle(oracle, restart, candidate):
+    """Restarted GMRES (gmres.hpp:75-131: m = min(restart, left), true residual
+    recomputed at each cycle start, history of true residuals): with a restart
+    far below the iteration count, the GPU walks the same cycles as the oracle:
+    same iteration count, same residual history to roundoff, same solution."""
+    spec = P.config1(16)
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    t = oracle.time_constants(1)
+    tau = 0.05
+    R = rp.slab_rhs(1, 0.0, tau, np.zeros(rp.n_u), np.zeros(rp.n_p))
+    shat = rp.schur_forward(1, R)
+    x_ref, rep_ref = rp.block_solve(1, tau, shat, tol=1e-10, restart=restart, max_iter=400, backend=0,
+                                    flexible=candidate == "flexible")
+    blk = S.BlockSolver(ops, t["T"], tau, opt=S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=restart),
+                                                             candidate=candidate))
+    x, rep = blk.solve(shat)
+    assert rep.converged and rep_ref["converged"]
+    assert abs(rep.iterations - rep_ref["iterations"]) <= 1, (rep.iterations, rep_ref["iterations"])
+    h, hr = np.asarray(rep.residual_history), np.asarray(rep_ref["history"])
+    k = min(len(h), len(hr))
+    assert np.allclose(h[:k], hr[:k], rtol=1e-6, atol=1e-9 * hr[0])
+    assert np.linalg.norm(x - x_ref) <= SOLVE_RTOL * np.linalg.norm(x_ref)
+
+
+def test_march_nonsquare_mixed_bcs_matches_oracle(oracle):
+    """A non-square mesh (nx != ny), non-unit domain and every boundary kind
+    (fixed / roller_x / roller_y / traction; pressure / no_flow) through the
+    whole device march (dG(1), 3 slabs) vs the oracle: iterations +-1, states
+    within 1e-9."""
+    spec = P.config1(6)
+    spec.nx, spec.ny = 12, 7
+    spec.k_perm_cells = P.lognormal_field(P.K_SEED, spec.nx * spec.ny)
+    spec.disp = {"left": ("fixed", (0.0, 0.0)), "right": ("roller_x", (0.0, 0.3)),
+                 "bottom": ("roller_y", (0.2, 0.0)), "top": ("traction", (0.1, -1.0))}
+    spec.flow = {"left": ("pressure", 0.5), "right": ("no_flow", 0.0), "bottom": ("no_flow", 0.0),
+                 "top": ("pressure", -0.25)}
+    spec.lx, spec.ly = 1.3, 0.9
+    rp = oracle.RefProblem(spec.to_dict())
+    ref = rp.march(1, 0.15, 3, tol=1e-10, restart=50, keep_states=True, backend=0)
+    ops = S.SpatialOperators.assemble(spec)
+    reps, states = S.march(ops, 1, 0.15, 3, S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50)),
+                           keep_states=True)
+    for n, rep in enumerate(reps):
+        assert rep.converged and abs(rep.iterations - int(ref["iterations"][n])) <= 1
+        refs = ref["states"][n].ravel()
+        assert np.linalg.norm(states[n] - refs) <= SOLVE_RTOL * np.linalg.norm(refs)
