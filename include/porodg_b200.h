@@ -205,6 +205,19 @@ int pdg_fs_solve(pdg_fs* fs, const double* rhs, const double* x0, double* x, pdg
 int pdg_fs_solve_device(pdg_fs* fs, const double* rhs_dev, const double* x0_dev, double* x_dev, pdg_report* rep);
 void pdg_fs_destroy(pdg_fs* fs);
 
+/* Exact SPD block-tridiagonal solver (the inner solves of the fixed-stress
+ * preconditioner, fixed_stress.hpp:109-139) for a host CSR that is block
+ * tridiagonal under the symmetric permutation perm (new -> old; NULL =
+ * identity) with the given block sizes. allow_local: use the chunk-local sweep
+ * when the couplings are 8x8 cell-local. solve: nrhs <= 2 columns of n doubles
+ * (device pointers, contiguous). Used for the strip interiors of the multi-GPU
+ * substructured solve. */
+typedef struct pdg_tri pdg_tri;
+int pdg_tri_create(pdg_ctx* ctx, const pdg_csr* A, const int* perm, const int* block_sizes, int nblocks,
+                   int allow_local, pdg_tri** out);
+int pdg_tri_solve_device(pdg_tri* t, const double* b_dev, double* x_dev, int nrhs);
+void pdg_tri_destroy(pdg_tri* t);
+
 /* local_mass_residual (slab.hpp:292-318): the discrete per-cell mass balance of
  * one slab. rhs and state are (r+1)*n_total doubles stacked per Radau node
  * (the slab system right-hand side and its solution, [u q p] per node);

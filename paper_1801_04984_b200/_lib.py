@@ -106,6 +106,9 @@ _SIGS = {
     "pdg_profile_enable": (None, [C.c_int]),
     "pdg_profile_reset": (None, []),
     "pdg_profile_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), LLP, C.POINTER(C.c_double)]),
+    "pdg_tri_create": (C.c_int, [VP, C.POINTER(CSR), IP, IP, C.c_int, C.c_int, C.POINTER(VP)]),
+    "pdg_tri_solve_device": (C.c_int, [VP, VP, VP, C.c_int]),
+    "pdg_tri_destroy": (None, [VP]),
     "pdg_mass_residual": (C.c_int, [VP, C.c_int, C.c_double, DP, DP, DP, DP]),
     "pdg_mass_residual_device": (C.c_int, [VP, C.c_int, C.c_double, VP, VP, VP, DP]),
     "pdg_time_constants": (C.c_int, [C.c_int, DP, DP, DP, DP, DP]),

@@ -29,6 +29,11 @@ struct pdg_op {
     SpaceTimeOp op;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
+struct pdg_tri {
+    Ctx* ctx = nullptr;
+    DCsr A;
+    BlockTriChol chol;
+};
 struct pdg_fs {
     pdg_ops* ops = nullptr;
     FsSolver fs;
@@ -672,6 +677,35 @@ int pdg_fs_solve(pdg_fs* f, const double* rhs, const double* x0, double* x, pdg_
 }
 
 void pdg_fs_destroy(pdg_fs* f) { delete f; }
+
+int pdg_tri_create(pdg_ctx* ctx, const pdg_csr* A, const int* perm, const int* block_sizes, int nblocks,
+                   int allow_local, pdg_tri** out) {
+    API_BEGIN
+    require(ctx && A && block_sizes && out && nblocks >= 1, "pdg_tri_create: null argument");
+    require(A->rows == A->cols, "pdg_tri_create: matrix must be square");
+    PDG_CUDA(cudaSetDevice(ctx->c.device));
+    auto t = std::make_unique<pdg_tri>();
+    t->ctx = &ctx->c;
+    cudaStream_t st = ctx->c.stream;
+    csr_upload(t->A, *A, st);
+    std::vector<int> p;
+    if (perm) p.assign(perm, perm + A->rows);
+    t->chol.allow_local = allow_local != 0;
+    t->chol.factor(A->rows, t->A.off.p, t->A.idx.p, t->A.val.p, p, std::vector<int>(block_sizes, block_sizes + nblocks), 2,
+                   st);
+    *out = t.release();
+    API_END
+}
+
+int pdg_tri_solve_device(pdg_tri* t, const double* b_dev, double* x_dev, int nrhs) {
+    API_BEGIN
+    require(t && b_dev && x_dev, "pdg_tri_solve: null argument");
+    t->chol.solve(b_dev, t->chol.n, x_dev, t->chol.n, nrhs, t->ctx->stream);
+    PDG_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    API_END
+}
+
+void pdg_tri_destroy(pdg_tri* t) { delete t; }
 
 int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q) {
     API_BEGIN
