@@ -188,6 +188,39 @@ def spmv_distributed(n, reps, peak, rank, world, dist):
     return out
 
 
+def solve_distributed(slabs, rank, world, dist, local):
+    """Config 1 slab block solve (dG(1) transformed block, GMRES tol 1e-10) strong-
+    scaled over the ranks (distributed.DeviceDistributedBlock: strip SpMV, exact
+    substructured inner solves, rank-ordered Krylov sums over NCCL). Timed per
+    solve with barriers + synchronize; max over ranks. A correct-by-construction
+    prototype (torch glue, host least squares), reported beside the headline."""
+    import torch
+    from paper_1801_04984_b200 import distributed as D, problem as P, solver as S
+    comm = D.Comm(dist, rank, world)
+    T = S.time_constants(1)["T"]
+    t0 = time.time()
+    blk = D.DeviceDistributedBlock(P.config1(128), T, 0.05, rank, comm, device=local, candidate="flexible")
+    setup = time.time() - t0
+    rhs = P.uniform_vector(P.X_SEED, 2 * blk.nt)
+    b = torch.as_tensor(rhs[blk.owned.cpu().numpy()], device=blk.dev)
+    blk.solve(b)  # warm-up
+    ms, its = [], []
+    for _ in range(slabs):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        _, rep = blk.solve(b)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms.append((time.perf_counter() - a) * 1e3)
+        its.append(rep["iterations"])
+    t = torch.tensor([float(np.mean(ms))], dtype=torch.float64, device=blk.dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"n_gpus": world, "scaling": "strong", "ms_per_block_solve": float(t[0]), "iterations": its,
+            "setup_s": setup, "note": "distributed.DeviceDistributedBlock (prototype: torch glue, host least squares); "
+                                      "wall clock between barriers, max over ranks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,9 +347,17 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_dev, e2e_ms, ms_ref = float(t[0]), float(t[1]), float(t[2])
 
-    spmv_dist = None
+    spmv_dist = solve_dist = None
     if world > 1 and args.spmv_sizes:
-        spmv_dist = spmv_distributed(int(args.spmv_sizes.split(",")[-1]), 20, peak, rank, world, torch.distributed)
+        try:
+            spmv_dist = spmv_distributed(int(args.spmv_sizes.split(",")[-1]), 20, peak, rank, world, torch.distributed)
+        except Exception as e:  # report, do not lose the headline line
+            spmv_dist = {"error": repr(e)[:300]}
+    if world > 1:
+        try:
+            solve_dist = solve_distributed(3, rank, world, torch.distributed, local)
+        except Exception as e:
+            solve_dist = {"error": repr(e)[:300]}
     spmv = spmv_sweep([int(s) for s in args.spmv_sizes.split(",") if s], args.spmv_reps, peak) \
         if rank == 0 and args.spmv_sizes else []
     spmv_roof = None
@@ -357,7 +398,8 @@ def main():
             "e2e": {"value": e2e_ms, "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
                     "d2h_bytes_per_step": 8 * nn * nt},
             "gpu_launches": int(main_run["launches"]), "roofline": roofline, "spmv_roofline": spmv_roof,
-            "phases": phases, "spmv": spmv, "spmv_distributed": spmv_dist, "clocks": main_run["clocks"],
+            "phases": phases, "spmv": spmv, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist,
+            "clocks": main_run["clocks"],
             "cpu_baseline": cpu}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
