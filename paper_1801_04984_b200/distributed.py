@@ -60,7 +60,8 @@ class Comm:
         for k in sorted(send):
             reqs.append(self.dist.isend(self._out(x[send[k]].contiguous()), k))
         for k in sorted(recv):
-            bufs[k] = torch.empty(len(recv[k]), dtype=x.dtype, device="cpu" if self.host else x.device)
+            bufs[k] = torch.empty((len(recv[k]),) + tuple(x.shape[1:]), dtype=x.dtype,
+                                  device="cpu" if self.host else x.device)
             reqs.append(self.dist.irecv(bufs[k], k))
         for r in reqs:
             r.wait()
@@ -168,20 +169,22 @@ class DeviceStripTri:
         self.ASI_bot = None if self.W_bot is None else torch.tensor(self.A_IS_bot.T.toarray(), device=dev)
 
     def solve(self, b_glob):
-        """b_glob: global-numbering device vector holding this rank's interior and
-        separator entries; returns x in global numbering (own entries only)."""
+        """b_glob: global-numbering device vector (n,) or right-hand sides (n, k)
+        holding this rank's interior and separator entries; returns x in global
+        numbering (own entries only)."""
         import torch
 
-        y = self.tri.solve(b_glob[self.glob_I])
+        B = b_glob.reshape(b_glob.shape[0], -1)
+        y = self.tri.solve(B[self.glob_I])
         k = self.rank
-        g = torch.zeros(int(self.so[-1]), dtype=torch.float64, device=self.dev)
+        g = torch.zeros((int(self.so[-1]), B.shape[1]), dtype=torch.float64, device=self.dev)
         if self.sep is not None:
-            g[int(self.so[k - 1]):int(self.so[k])] += b_glob[self.glob_S] - self.ASI_top @ y
+            g[int(self.so[k - 1]):int(self.so[k])] += B[self.glob_S] - self.ASI_top @ y
         if self.W_bot is not None:
             g[int(self.so[k]):int(self.so[k + 1])] -= self.ASI_bot @ y
         g = self.comm.ordered_sum(g)
-        x = torch.zeros_like(b_glob)
-        xs = torch.cholesky_solve(g.reshape(-1, 1), self.L).reshape(-1) if g.numel() else g
+        x = torch.zeros_like(B)
+        xs = torch.cholesky_solve(g, self.L) if g.numel() else g
         xi = y
         if self.sep is not None:
             xk = xs[int(self.so[k - 1]):int(self.so[k])]
@@ -190,7 +193,7 @@ class DeviceStripTri:
         if self.W_bot is not None:
             xi = xi - self.W_bot @ xs[int(self.so[k]):int(self.so[k + 1])]
         x[self.glob_I] = xi
-        return x
+        return x.reshape(b_glob.shape)
 
 
 class DeviceFixedStressPre:
@@ -252,22 +255,25 @@ class DeviceFixedStressPre:
         self.mech = DeviceStripTri(A, None, np.full(ny, 8 * nx), strips, rank, comm, device)
 
     def apply(self, r):
+        """r: (nt, k) global-numbering components (owned entries valid), all k
+        time components of the block at once (the inner solves batch them)."""
         import torch
 
         nu, nq, w = self.nu, self.nq, self.w
-        fp = torch.where(self.own_c, r[nu + nq:], torch.zeros_like(r[nu + nq:]))
+        oc, of, ou = self.own_c[:, None], self.own_f[:, None], self.own_u[:, None]
+        fp = torch.where(oc, r[nu + nq:], torch.zeros_like(r[nu + nq:]))
         self.comm.exchange(fp, *self.plan_fp)
-        rq = torch.where(self.own_f, r[nu:nu + nq] - w * (self.B @ (self.dinv * fp)), torch.zeros_like(r[nu:nu + nq]))
+        rq = torch.where(of, r[nu:nu + nq] - w * (self.B @ (self.dinv[:, None] * fp)), torch.zeros_like(r[nu:nu + nq]))
         q = self.flow.solve(rq)
         self.comm.exchange(q, *self.plan_q)
-        p = torch.where(self.own_c, self.dinv * (fp - w * (self.Bt @ q)), torch.zeros_like(fp))
+        p = torch.where(oc, self.dinv[:, None] * (fp - w * (self.Bt @ q)), torch.zeros_like(fp))
         self.comm.exchange(p, *self.plan_p)
-        mech = torch.where(self.own_u, r[:nu] / w + self.b * (self.E @ p), torch.zeros_like(r[:nu]))
+        mech = torch.where(ou, r[:nu] / w + self.b * (self.E @ p), torch.zeros_like(r[:nu]))
         u = self.mech.solve(mech)
         z = torch.zeros_like(r)
-        z[:nu] = torch.where(self.own_u, u, z[:nu])
-        z[nu:nu + nq] = torch.where(self.own_f, q, z[nu:nu + nq])
-        z[nu + nq:] = torch.where(self.own_c, p, z[nu + nq:])
+        z[:nu] = torch.where(ou, u, z[:nu])
+        z[nu:nu + nq] = torch.where(of, q, z[nu:nu + nq])
+        z[nu + nq:] = torch.where(oc, p, z[nu + nq:])
         return z
 
 
@@ -324,13 +330,9 @@ class DeviceDistributedBlock:
     def prec(self, v):
         import torch
 
-        out = torch.empty_like(v)
-        for i in range(self.m):
-            seg = slice(i * self.n_own1, (i + 1) * self.n_own1)
-            r = torch.zeros(self.nt, dtype=torch.float64, device=self.dev)
-            r[self.owned_comp] = v[seg]
-            out[seg] = self.pre.apply(r)[self.owned_comp]
-        return out
+        R = torch.zeros((self.nt, self.m), dtype=torch.float64, device=self.dev)
+        R[self.owned_comp] = v.reshape(self.m, self.n_own1).T
+        return self.pre.apply(R)[self.owned_comp].T.reshape(-1)
 
     def nrm(self, v):
         return float(self.comm.ordered_sum((v @ v).reshape(1))[0].sqrt())
