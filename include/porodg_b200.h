@@ -208,8 +208,10 @@ void pdg_fs_destroy(pdg_fs* fs);
 /* Exact SPD block-tridiagonal solver (the inner solves of the fixed-stress
  * preconditioner, fixed_stress.hpp:109-139) for a host CSR that is block
  * tridiagonal under the symmetric permutation perm (new -> old; NULL =
- * identity) with the given block sizes. allow_local: use the chunk-local sweep
- * when the couplings are 8x8 cell-local. solve: nrhs <= 2 columns of n doubles
+ * identity) with the given block sizes. allow_local (flags): bit 0 = use the
+ * chunk-local sweep when the couplings are 8x8 cell-local; bit 1 = the matrix is
+ * NOT symmetric (twisted block LU with in-block partial pivoting instead of
+ * Cholesky; no pivoting across blocks). solve: nrhs <= 2 columns of n doubles
  * (device pointers, contiguous). Used for the strip interiors of the multi-GPU
  * substructured solve. */
 typedef struct pdg_tri pdg_tri;

@@ -34,9 +34,11 @@ LaHandles::~LaHandles() {
 
 namespace {
 
+// dense diagonal blocks D_j, sub-diagonal C_j = A_{j+1,j} and (non-symmetric
+// matrices, dU != null) super-diagonal U_j = A_{j,j+1}, all col-major
 __global__ void k_scatter_blocks(int n, const int* off, const int* idx, const double* val, const int* inv_perm,
                                  const int* blk_of, const int* loc_of, const int* bsz, const long long* dD,
-                                 const long long* dC, double* dense, int* err) {
+                                 const long long* dC, const long long* dU, double* dense, int* err) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         const int nr = inv_perm ? inv_perm[r] : r;
         const int jr = blk_of[nr], lr = loc_of[nr];
@@ -47,7 +49,9 @@ __global__ void k_scatter_blocks(int n, const int* off, const int* idx, const do
                 dense[dD[jr] + lr + (long long)lc * bsz[jr]] = val[k];
             else if (jr == jc + 1)
                 dense[dC[jc] + lr + (long long)lc * bsz[jr]] = val[k];
-            else if (jc != jr + 1)
+            else if (jc == jr + 1) {
+                if (dU) dense[dU[jr] + lr + (long long)lc * bsz[jr]] = val[k];
+            } else
                 atomicOr(err, 1);
         }
     }
@@ -104,6 +108,12 @@ void BlockTriChol::layout(int n_, const std::vector<int>& perm_host, const std::
         dC_[j] = o;
         o += (long long)bsz[j + 1] * bsz[j];
     }
+    dU_.assign(nb, -1);
+    if (!symmetric)
+        for (int j = 0; j + 1 < nb; ++j) {
+            dU_[j] = o;
+            o += (long long)bsz[j] * bsz[j + 1];
+        }
     dtot_ = o;
     d_bsz.upload(bsz);
     d_boff.upload(std::vector<int>(boff.begin(), boff.end() - 1));
@@ -116,13 +126,15 @@ void BlockTriChol::factor(int n_, const int* off, const int* idx, const double* 
     max_rhs = max_rhs_;
     DBuf<double> dense(dtot_);
     dense.zero(st);
-    DBuf<long long> ddD, ddC;
+    DBuf<long long> ddD, ddC, ddU;
     ddD.upload(dD_, st);
     ddC.upload(dC_, st);
+    if (!symmetric) ddU.upload(dU_, st);
     DBuf<int> err(1);
     err.zero(st);
     k_scatter_blocks<<<grid_for(n, 256), 256, 0, st>>>(n, off, idx, val, perm.n ? inv_perm.p : nullptr, blk_of.p,
-                                                        loc_of.p, d_bsz.p, ddD.p, ddC.p, dense.p, err.p);
+                                                        loc_of.p, d_bsz.p, ddD.p, ddC.p, symmetric ? nullptr : ddU.p,
+                                                        dense.p, err.p);
     PDG_CHECK_LAUNCH();
     int herr = 0;
     PDG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -132,6 +144,10 @@ void BlockTriChol::factor(int n_, const int* off, const int* idx, const double* 
 }
 
 void BlockTriChol::factor_dense(double* dense, cudaStream_t st) {
+    if (!symmetric) {  // twisted block LU, dense-sweep solve
+        dense_setup(dense, st);
+        return;
+    }
     local_prepare(dense, st);  // before the couplings are overwritten by the factorisation
     if (!local) {
         dense_setup(dense, st);

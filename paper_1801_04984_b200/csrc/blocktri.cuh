@@ -74,6 +74,7 @@ struct BlockTriChol {
     // step streams one Sinv_j: 2 m^2 doubles per block per solve (the general
     // path reads 3 m^2: Linv twice, F/G and N).
     bool allow_local = false;        // set by the owner before factor()
+    bool symmetric = true;           // false: non-symmetric matrix, twisted block LU (set before layout/factor)
     bool local = false;              // chosen by factor()
     DBuf<double> cloc;               // [nb-1][m/8][8][8]: chunk (r, q) of C_j, row-major
     DBuf<double> wsave;              // w_j of the forward sweep, read back by the backward sweep
@@ -107,10 +108,11 @@ struct BlockTriChol {
     void layout(int n_, const std::vector<int>& perm_host, const std::vector<int>& block_sizes);
     long long dense_d_offset(int j) const { return dD_[j]; }
     long long dense_c_offset(int j) const { return dC_[j]; }
+    long long dense_u_offset(int j) const { return dU_[j]; }  // non-symmetric: A_{j,j+1}
     long long dense_total() const { return dtot_; }
 
 private:
-    std::vector<long long> dD_, dC_;
+    std::vector<long long> dD_, dC_, dU_;
     long long dtot_ = 0;
     bool local_prepare(double* dense, cudaStream_t st);   // structure check + coupling chunks
     void local_finish(double* dense, cudaStream_t st);    // Sinv_j from the Cholesky factors, schedule, kernel config

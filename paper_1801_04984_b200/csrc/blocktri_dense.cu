@@ -52,6 +52,15 @@ __global__ void k_identity_cm(int m, double* a) {
         a[t] = (t % m == t / m) ? 1.0 : 0.0;
 }
 
+// (P I)[r, c] = (c == perm[r]), col-major m x m
+__global__ void k_perm_identity(int m, const int* perm, double* a) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * m;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int r = static_cast<int>(t % m), c = static_cast<int>(t / m);
+        a[t] = perm[r] == c ? 1.0 : 0.0;
+    }
+}
+
 // Sum of 16 per-lane values across the warp, reduce-scatter style: on return
 // lanes 2i and 2i+1 hold the warp total of index i (fixed order).
 __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lane) {
@@ -221,15 +230,103 @@ namespace {
 // (m_{j+1} x m_j) becomes K_j in the top part; K'_j (bottom) in kp.
 struct TriSys {
     std::vector<int> m;
-    std::vector<double*> D, C;
+    std::vector<double*> D, C, U;  // U[j] = A_{j,j+1} (m_j x m_{j+1}): non-symmetric systems only
     int t = 0;
+    bool lu = false;               // twisted block LU (non-symmetric) instead of Cholesky
     DBuf<double> kp, linv;
     std::vector<long long> oKp, ol, ro;
+    // LU: LP_j = L_j^{-1} P_j in linv, Ui_j = U_j^{-1}, top Kt_j = A_{j+1,j} Ui_j and
+    // Ku_j = LP_j A_{j,j+1}, bottom Kb_j = A_{j-1,j} Ui'_j and Kbu_j = LP'_j A_{j,j-1}
+    DBuf<double> ui, ktb, kub, kbb, kbub;
+    std::vector<long long> oKt, oKu, oKb, oKbu;
     int nb() const { return static_cast<int>(m.size()); }
     long long rows() const { return ro.back(); }
-    double* Kt(int j) const { return C[j]; }
-    double* Kb(int j) const { return kp.p + oKp[j]; }
+    double* Kt(int j) const { return lu ? ktb.p + oKt[j] : C[j]; }
+    double* Kb(int j) const { return lu ? kbb.p + oKb[j] : kp.p + oKp[j]; }
     double* Li(int j) const { return linv.p + ol[j]; }
+    double* Ui(int j) const { return ui.p + ol[j]; }
+    double* Ku(int j) const { return kub.p + oKu[j]; }
+    double* Kbu(int j) const { return kbub.p + oKbu[j]; }
+
+    void factor_lu(LaHandles& h, cudaStream_t st) {
+        const int n = nb();
+        ro.assign(n + 1, 0);
+        for (int j = 0; j < n; ++j) ro[j + 1] = ro[j] + m[j];
+        t = (n - 1) / 2;
+        const double one = 1.0, mone = -1.0, zero = 0.0;
+        const int mx = *std::max_element(m.begin(), m.end());
+        int lwork = 0;
+        PDG_CUSOLVER_D(cusolverDnDgetrf_bufferSize(h.solver, mx, mx, D[0], mx, &lwork));
+        DBuf<double> work(std::max(lwork, 1));
+        DBuf<int> ipiv(mx), info(1), dperm(mx);
+        ol.assign(n, 0);
+        oKt.assign(n, -1);
+        oKu.assign(n, -1);
+        oKb.assign(n, -1);
+        oKbu.assign(n, -1);
+        long long tot = 0, kt = 0, kb = 0;
+        for (int j = 0; j < n; ++j) {
+            ol[j] = tot;
+            tot += (long long)m[j] * m[j];
+            if (j < t) {
+                oKt[j] = oKu[j] = kt;
+                kt += (long long)m[j + 1] * m[j];
+            }
+            if (j > t) {
+                oKb[j] = oKbu[j] = kb;
+                kb += (long long)m[j - 1] * m[j];
+            }
+        }
+        linv.alloc(tot);
+        ui.alloc(tot);
+        ktb.alloc(std::max<long long>(kt, 1));
+        kub.alloc(std::max<long long>(kt, 1));
+        kbb.alloc(std::max<long long>(kb, 1));
+        kbub.alloc(std::max<long long>(kb, 1));
+        auto lu_block = [&](int j) {  // P S = L U; LP_j = L^{-1} P, Ui_j = U^{-1}
+            const int mj = m[j];
+            PDG_CUSOLVER_D(cusolverDnDgetrf(h.solver, mj, mj, D[j], mj, work.p, ipiv.p, info.p));
+            std::vector<int> piv(mj), pm(mj);
+            PDG_CUDA(cudaMemcpyAsync(piv.data(), ipiv.p, sizeof(int) * mj, cudaMemcpyDeviceToHost, st));
+            int hinfo = 0;
+            PDG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            PDG_CUDA(cudaStreamSynchronize(st));
+            if (hinfo != 0)
+                throw Error(PDG_NOT_CONVERGED, "dense LU: matrix is singular to working precision (block " +
+                                                   std::to_string(j) + ")");
+            for (int i = 0; i < mj; ++i) pm[i] = i;
+            for (int i = 0; i < mj; ++i) std::swap(pm[i], pm[piv[i] - 1]);
+            PDG_CUDA(cudaMemcpyAsync(dperm.p, pm.data(), sizeof(int) * mj, cudaMemcpyHostToDevice, st));
+            k_perm_identity<<<grid_for((long long)mj * mj, 256), 256, 0, st>>>(mj, dperm.p, Li(j));
+            k_identity_cm<<<grid_for((long long)mj * mj, 256), 256, 0, st>>>(mj, Ui(j));
+            PDG_CHECK_LAUNCH();
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_UNIT, mj, mj,
+                                     &one, D[j], mj, Li(j), mj));
+            PDG_CUBLAS_D(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, mj,
+                                     mj, &one, D[j], mj, Ui(j), mj));
+        };
+        auto mm = [&](int rows, int cols, int inner, double a, const double* A_, int lda, const double* B_, int ldb,
+                      double b, double* C_, int ldc) {
+            PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, cols, inner, &a, A_, lda, B_, ldb, &b, C_, ldc));
+        };
+        for (int j = 0; j < t; ++j) {  // top: S_j = A_jj - Kt_{j-1} Ku_{j-1}
+            if (j > 0) mm(m[j], m[j], m[j - 1], -1.0, Kt(j - 1), m[j], Ku(j - 1), m[j - 1], 1.0, D[j], m[j]);
+            lu_block(j);
+            mm(m[j + 1], m[j], m[j], 1.0, C[j], m[j + 1], Ui(j), m[j], 0.0, Kt(j), m[j + 1]);
+            mm(m[j], m[j + 1], m[j], 1.0, Li(j), m[j], U[j], m[j], 0.0, Ku(j), m[j]);
+        }
+        for (int j = n - 1; j > t; --j) {  // bottom: S'_j = A_jj - Kb_{j+1} Kbu_{j+1}
+            if (j < n - 1) mm(m[j], m[j], m[j + 1], -1.0, Kb(j + 1), m[j], Kbu(j + 1), m[j + 1], 1.0, D[j], m[j]);
+            lu_block(j);
+            mm(m[j - 1], m[j], m[j], 1.0, U[j - 1], m[j - 1], Ui(j), m[j], 0.0, Kb(j), m[j - 1]);
+            mm(m[j], m[j - 1], m[j], 1.0, Li(j), m[j], C[j - 1], m[j], 0.0, Kbu(j), m[j]);
+        }
+        if (t > 0) mm(m[t], m[t], m[t - 1], -1.0, Kt(t - 1), m[t], Ku(t - 1), m[t - 1], 1.0, D[t], m[t]);
+        if (t + 1 < n) mm(m[t], m[t], m[t + 1], -1.0, Kb(t + 1), m[t], Kbu(t + 1), m[t + 1], 1.0, D[t], m[t]);
+        lu_block(t);
+        (void)zero;
+        (void)mone;
+    }
 
     void factor(LaHandles& h, cudaStream_t st) {
         const int n = nb();
@@ -375,6 +472,7 @@ void BlockTriChol::dense_setup(double* dense, cudaStream_t st) {
     int P = 1;
     if (const char* e = std::getenv("PDG_FLOW_STRIPS"))
         P = std::max(1, std::min({std::atoi(e), num_sms() / (2 * d_g), (nb + 1) / 3}));
+    if (!symmetric) P = 1;  // the substructured path is SPD-only
     std::vector<int> lo(P), hi(P), sep;
     {
         const int interior = nb - (P - 1);
@@ -395,9 +493,16 @@ void BlockTriChol::dense_setup(double* dense, cudaStream_t st) {
         for (int j = lo[k]; j < hi[k]; ++j) {
             strips[k].m.push_back(bsz[j]);
             strips[k].D.push_back(Dg(j));
-            if (j + 1 < hi[k]) strips[k].C.push_back(Cg(j));
+            if (j + 1 < hi[k]) {
+                strips[k].C.push_back(Cg(j));
+                if (!symmetric) strips[k].U.push_back(dense + dU_[j]);
+            }
         }
-        strips[k].factor(h, st);
+        strips[k].lu = !symmetric;
+        if (strips[k].lu)
+            strips[k].factor_lu(h, st);
+        else
+            strips[k].factor(h, st);
     }
     // ---- spikes and the separator system
     std::vector<DBuf<double>> Wt(P), Wb(P);
@@ -646,6 +751,45 @@ void BlockTriChol::dense_setup(double* dense, cudaStream_t st) {
         }
         const TriSys& S = *mt.sys;
         const int j = mt.j, mj = S.m[j], nn = S.nb();
+        if (S.lu) {  // twisted block LU: LP = L^{-1} P, Ui = U^{-1} (module comment, non-symmetric form)
+            auto trT = [&](const double* A_, double* dst) {
+                PDG_CUBLAS_D(cublasDgeam(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, mj, mj, &one, A_, mj, &zero, A_, mj, dst, ld));
+            };
+            switch (mt.kind) {
+                case MK_TOPF:
+                case MK_PTOP:  // [LP_j | -LP_j Kt_{j-1}] -> [LP_j^T; -Kt_{j-1}^T LP_j^T]
+                    trT(S.Li(j), X);
+                    if (j > 0)
+                        PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j - 1], mj, mj, &mone, S.Kt(j - 1), mj,
+                                                 S.Li(j), mj, &zero, X + mj, ld));
+                    break;
+                case MK_BOTF:  // [LP'_j | -LP'_j Kb_{j+1}] -> [LP'_j^T; -Kb_{j+1}^T LP'_j^T]
+                    trT(S.Li(j), X);
+                    if (j < nn - 1)
+                        PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j + 1], mj, mj, &mone, S.Kb(j + 1), mj,
+                                                 S.Li(j), mj, &zero, X + mj, ld));
+                    break;
+                case MK_PBOT:  // -LP_t Kb_{t+1} -> -Kb_{t+1}^T LP_t^T
+                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j + 1], mj, mj, &mone, S.Kb(j + 1), mj,
+                                             S.Li(j), mj, &zero, X, ld));
+                    break;
+                case MK_TWIST:  // [Ui_t | Ui_t] -> [Ui_t^T; Ui_t^T]
+                    trT(S.Ui(j), X);
+                    if (j < nn - 1) trT(S.Ui(j), X + mj);
+                    break;
+                case MK_TOPB:  // [Ui_j | -Ui_j Ku_j] -> [Ui_j^T; -Ku_j^T Ui_j^T]
+                    trT(S.Ui(j), X);
+                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j + 1], mj, mj, &mone, S.Ku(j), mj,
+                                             S.Ui(j), mj, &zero, X + mj, ld));
+                    break;
+                default:  // MK_BOTB: [Ui'_j | -Ui'_j Kbu_j] -> [Ui'_j^T; -Kbu_j^T Ui'_j^T]
+                    trT(S.Ui(j), X);
+                    PDG_CUBLAS_D(cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_T, S.m[j - 1], mj, mj, &mone, S.Kbu(j), mj,
+                                             S.Ui(j), mj, &zero, X + mj, ld));
+                    break;
+            }
+            continue;
+        }
         switch (mt.kind) {
             case MK_TOPF:
             case MK_PTOP:  // [Linv_j | -Linv_j K_{j-1}] -> [Linv_j^T; -K_{j-1}^T Linv_j^T]

@@ -690,7 +690,8 @@ int pdg_tri_create(pdg_ctx* ctx, const pdg_csr* A, const int* perm, const int* b
     csr_upload(t->A, *A, st);
     std::vector<int> p;
     if (perm) p.assign(perm, perm + A->rows);
-    t->chol.allow_local = allow_local != 0;
+    t->chol.allow_local = (allow_local & 1) != 0;
+    t->chol.symmetric = (allow_local & 2) == 0;
     t->chol.factor(A->rows, t->A.off.p, t->A.idx.p, t->A.val.p, p, std::vector<int>(block_sizes, block_sizes + nblocks), 2,
                    st);
     *out = t.release();

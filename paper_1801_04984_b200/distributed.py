@@ -70,9 +70,10 @@ class Comm:
 
 
 class TriSolver:
-    """pdg_tri_*: exact SPD block-tridiagonal solve of a host CSR on the device."""
+    """pdg_tri_*: exact block-tridiagonal solve of a host CSR on the device (SPD:
+    twisted Cholesky; symmetric=False: twisted block LU)."""
 
-    def __init__(self, A, block_sizes, perm=None, allow_local=True, device: int = 0):
+    def __init__(self, A, block_sizes, perm=None, allow_local=True, device: int = 0, symmetric=True):
         import scipy.sparse as sp
 
         A = sp.csr_matrix(A)
@@ -87,7 +88,8 @@ class TriSolver:
         pm = None if perm is None else np.ascontiguousarray(perm, np.int32)
         h = C.c_void_p()
         check(lib().pdg_tri_create(context(device), C.byref(csr), None if pm is None else pm.ctypes.data_as(_lib.IP),
-                                   bs.ctypes.data_as(_lib.IP), len(bs), 1 if allow_local else 0, C.byref(h)))
+                                   bs.ctypes.data_as(_lib.IP), len(bs),
+                                   (1 if allow_local else 0) | (0 if symmetric else 2), C.byref(h)))
         self._h = h
 
     def solve(self, b):
