@@ -320,6 +320,116 @@ std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaS
     return a;
 }
 
+// ---- coupled fixed-stress sweep (fixed_stress.hpp:109-139 with a full Theta) ----
+constexpr int kMaxC = 2;
+struct Mat2 {
+    double a[4];
+};
+// 1 / ((1/M + stab) m_p)
+__global__ void k_dinvc(int np, double s, const double* m_p, double* d) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) d[c] = 1.0 / (s * m_p[c]);
+}
+// S[(i,f),(i2,f2)] = [i==i2] w_i M_q[f,f2] + Gamma_{i,i2} sum_c B[f,c] B[f2,c] / d_c   (Gamma = W Theta^{-1} W)
+__global__ void k_flowc_schur_blocks(int m, int nq, Mat2 w, Mat2 gam, const int* mq_off, const int* mq_idx,
+                                     const double* mq_val, const int* b_off, const int* b_idx, const double* b_val,
+                                     const int* bt_off, const int* bt_idx, const double* bt_val, const double* dinvc,
+                                     const int* inv_perm, const int* blk_of, const int* loc_of, const int* bsz,
+                                     const long long* dD, const long long* dC, const long long* dU, double* dense,
+                                     int* err) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m * nq; t += gridDim.x * blockDim.x) {
+        const int i = t / nq, f = t % nq;
+        const int nr = inv_perm[t], jr = blk_of[nr], lr = loc_of[nr];
+        auto add = [&](int i2, int f2, double v) {
+            const int nc = inv_perm[i2 * nq + f2], jc = blk_of[nc], lc = loc_of[nc];
+            if (jc == jr)
+                dense[dD[jr] + lr + (long long)lc * bsz[jr]] += v;
+            else if (jr == jc + 1)
+                dense[dC[jc] + lr + (long long)lc * bsz[jr]] += v;
+            else if (jc == jr + 1)
+                dense[dU[jr] + lr + (long long)lc * bsz[jr]] += v;
+            else
+                atomicOr(err, 1);
+        };
+        for (int k = mq_off[f]; k < mq_off[f + 1]; ++k) add(i, mq_idx[k], w.a[i] * mq_val[k]);
+        for (int k = b_off[f]; k < b_off[f + 1]; ++k) {
+            const int c = b_idx[k];
+            for (int q = bt_off[c]; q < bt_off[c + 1]; ++q)
+                for (int i2 = 0; i2 < m; ++i2) add(i2, bt_idx[q], gam.a[i * m + i2] * (b_val[k] * bt_val[q]) * dinvc[c]);
+        }
+    }
+}
+// fp_i = r_p_i [+ sum_j Theta_ij (b E^T u_j - stab m_p p_j) from the previous iterate]
+__global__ void k_fsc_fp(int m, int np, int nt, int nu, int nq, const double* __restrict__ xold, Mat2 th, double b,
+                         double stab, const double* __restrict__ r, const int* et_off, const int* et_idx,
+                         const double* et_val, const double* m_p, double* __restrict__ fp) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
+        double pr = r[(long long)i * nt + nu + nq + c];
+        if (xold)
+            for (int j = 0; j < m; ++j) {
+                const double tij = th.a[i * m + j];
+                if (tij == 0.0) continue;
+                double et = 0.0;
+                for (int k = et_off[c]; k < et_off[c + 1]; ++k) et += et_val[k] * xold[(long long)j * nt + et_idx[k]];
+                pr += tij * (b * et - stab * (m_p[c] * xold[(long long)j * nt + nu + nq + c]));
+            }
+        fp[t] = pr;
+    }
+}
+// rq_i[f] = r_q_i[f] + w_i sum_j Thinv_ij sum_{B row f} bv fp_j[c] / d_c
+__global__ void k_fsc_rq(int m, int nq, int np, int nt, int nu, Mat2 w, Mat2 thinv, const double* __restrict__ r,
+                         const double* __restrict__ fp, const int* b_off, const int* b_idx, const double* b_val,
+                         const double* __restrict__ dinvc, double* __restrict__ rq) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nq;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nq), f = static_cast<int>(t % nq);
+        double v = r[(long long)i * nt + nu + f];
+        for (int k = b_off[f]; k < b_off[f + 1]; ++k) {
+            const int c = b_idx[k];
+            double s = 0.0;
+            for (int j = 0; j < m; ++j) s += thinv.a[i * m + j] * fp[(long long)j * np + c];
+            v += w.a[i] * b_val[k] * s * dinvc[c];
+        }
+        rq[t] = v;
+    }
+}
+// q into z, then p_i[c] = -(1/d_c) sum_j Thinv_ij (fp_j[c] - w_j (B^T q_j)[c])
+__global__ void k_fsc_qp(int m, int np, int nq, int nt, int nu, Mat2 w, Mat2 thinv, const double* __restrict__ fp,
+                         const double* __restrict__ q, const int* bt_off, const int* bt_idx, const double* bt_val,
+                         const double* __restrict__ dinvc, double* __restrict__ z) {
+    const long long nqq = (long long)m * nq;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nqq + (long long)m * np;
+         t += (long long)gridDim.x * blockDim.x) {
+        if (t < nqq) {
+            const int i = static_cast<int>(t / nq), f = static_cast<int>(t % nq);
+            z[(long long)i * nt + nu + f] = q[t];
+            continue;
+        }
+        const long long u = t - nqq;
+        const int i = static_cast<int>(u / np), c = static_cast<int>(u % np);
+        double s = 0.0;
+        for (int j = 0; j < m; ++j) {
+            double btq = 0.0;
+            for (int k = bt_off[c]; k < bt_off[c + 1]; ++k) btq += bt_val[k] * q[(long long)j * nq + bt_idx[k]];
+            s += thinv.a[i * m + j] * (fp[(long long)j * np + c] - w.a[j] * btq);
+        }
+        z[(long long)i * nt + nu + nq + c] = -dinvc[c] * s;
+    }
+}
+// mech_i = r_u_i / w_i + b (E p_i)
+__global__ void k_fsc_mech(int m, int nu, int nt, int nq, Mat2 w, double b, const double* __restrict__ r,
+                           const double* __restrict__ z, const int* e_off, const int* e_idx, const double* e_val,
+                           double* __restrict__ mech) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nu;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = static_cast<int>(t / nu), k0 = static_cast<int>(t % nu);
+        double ep = 0.0;
+        for (int k = e_off[k0]; k < e_off[k0 + 1]; ++k) ep += e_val[k] * z[(long long)i * nt + nu + nq + e_idx[k]];
+        mech[t] = r[(long long)i * nt + k0] / w.a[i] + b * ep;
+    }
+}
+
 void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lambda_, double stab_, int sweeps_,
                            std::shared_ptr<ASolver> a_, cudaStream_t st) {
     ops = &o;
@@ -379,6 +489,84 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     if (sweeps > 1) xold.alloc((size_t)m * o.n_total());
 }
 
+void FixedStressPre::setup_coupled(const SpatialOps& o, int m_, double tau_, const double* theta, const double* kappa,
+                                   double stab_, std::shared_ptr<ASolver> a_, cudaStream_t st) {
+    require(m_ >= 1 && m_ <= kMaxC, "fixed-stress: coupled sweep supports up to 2 time components");
+    ops = &o;
+    m = m_;
+    tau = tau_;
+    stab = stab_;
+    sweeps = 1;
+    coupled = true;
+    a = std::move(a_);
+    for (int k = 0; k < m * m; ++k) th[k] = theta[k];
+    for (int i = 0; i < m; ++i) wc[i] = tau * kappa[i];
+    if (m == 1) {
+        require(th[0] != 0.0, "fixed-stress: singular time weight");
+        thinv[0] = 1.0 / th[0];
+    } else {
+        const double det = th[0] * th[3] - th[1] * th[2];
+        require(det != 0.0, "fixed-stress: singular time weight");
+        thinv[0] = th[3] / det;
+        thinv[1] = -th[1] / det;
+        thinv[2] = -th[2] / det;
+        thinv[3] = th[0] / det;
+    }
+    require(o.inv_m + stab > 0.0, "fixed-stress: flow storage block must be negative definite");
+    dinvc.alloc(o.n_p);
+    k_dinvc<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, o.inv_m + stab, o.m_p.p, dinvc.p);
+    PDG_CHECK_LAUNCH();
+    // face-row blocks holding both components: block j = [comp 0 faces of face row j, comp 1 ...]
+    const int nx = o.nx, ny = o.ny;
+    require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
+    std::vector<int> perm, bs;
+    for (int j = 0; j <= ny; ++j) {
+        std::vector<int> faces;
+        for (int i = 0; i < nx; ++i) faces.push_back(j * nx + i);
+        if (j < ny)
+            for (int i = 0; i <= nx; ++i) faces.push_back(nx * (ny + 1) + i * ny + j);
+        for (int c = 0; c < m; ++c)
+            for (int f : faces) perm.push_back(c * o.n_q + f);
+        bs.push_back(static_cast<int>(m * faces.size()));
+    }
+    flow.prof_phase = PROF_FLOW_SOLVE;
+    flow.symmetric = false;
+    flow.layout(m * o.n_q, perm, bs);
+    flow.max_rhs = 1;
+    DBuf<double> dense(flow.dense_total());
+    dense.zero(st);
+    std::vector<long long> dD(flow.nb), dC(flow.nb), dU(flow.nb);
+    for (int j = 0; j < flow.nb; ++j) {
+        dD[j] = flow.dense_d_offset(j);
+        dC[j] = flow.dense_c_offset(j);
+        dU[j] = flow.dense_u_offset(j);
+    }
+    DBuf<long long> ddD, ddC, ddU;
+    ddD.upload(dD, st);
+    ddC.upload(dC, st);
+    ddU.upload(dU, st);
+    Mat2 wm{}, gam{};
+    for (int i = 0; i < m; ++i) wm.a[i] = wc[i];
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) gam.a[i * m + k] = wc[i] * thinv[i * m + k] * wc[k];
+    DBuf<int> err(1);
+    err.zero(st);
+    k_flowc_schur_blocks<<<grid_for((long long)m * o.n_q, 256), 256, 0, st>>>(
+        m, o.n_q, wm, gam, o.M_q.off.p, o.M_q.idx.p, o.M_q.val.p, o.B.off.p, o.B.idx.p, o.B.val.p, o.Bt.off.p,
+        o.Bt.idx.p, o.Bt.val.p, dinvc.p, flow.inv_perm.p, flow.blk_of.p, flow.loc_of.p, flow.d_bsz.p, ddD.p, ddC.p,
+        ddU.p, dense.p, err.p);
+    PDG_CHECK_LAUNCH();
+    int herr = 0;
+    PDG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    require(herr == 0, "fixed-stress: coupled flow Schur complement is not block tridiagonal in face-row order");
+    flow.factor_dense(dense.p, st);
+    rq.alloc((size_t)m * o.n_q);
+    qtmp.alloc((size_t)m * o.n_q);
+    fp.alloc((size_t)m * o.n_p);
+    mech.alloc((size_t)m * o.n_u);
+}
+
 void FixedStressPre::apply(const double* r, double* z, cudaStream_t st) {
     const size_t len = (size_t)m * ops->n_total();
     for (int s = 0; s < sweeps; ++s) {
@@ -392,6 +580,36 @@ void FixedStressPre::apply(const double* r, double* z, cudaStream_t st) {
 void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z, cudaStream_t st) {
     const SpatialOps& o = *ops;
     const int nt = o.n_total(), nu = o.n_u, nq = o.n_q, np = o.n_p;
+    if (coupled) {
+        Mat2 wm{}, tm{}, ti{};
+        for (int i = 0; i < m; ++i) wm.a[i] = wc[i];
+        for (int k = 0; k < m * m; ++k) {
+            tm.a[k] = th[k];
+            ti.a[k] = thinv[k];
+        }
+        {
+            ProfScope prof(PROF_PRE_OTHER, st, 0.0);
+            k_fsc_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, xprev, tm, o.biot_b, stab, r,
+                                                                       o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.m_p.p, fp.p);
+            k_fsc_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, wm, ti, r, fp.p, o.B.off.p,
+                                                                       o.B.idx.p, o.B.val.p, dinvc.p, rq.p);
+            count_launch(2);
+            PDG_CHECK_LAUNCH();
+        }
+        flow.solve(rq.p, (long long)m * nq, qtmp.p, (long long)m * nq, 1, st);
+        {
+            ProfScope prof(PROF_PRE_OTHER, st, 0.0);
+            k_fsc_qp<<<grid_for((long long)m * (nq + np), 256), 256, 0, st>>>(m, np, nq, nt, nu, wm, ti, fp.p, qtmp.p,
+                                                                              o.Bt.off.p, o.Bt.idx.p, o.Bt.val.p,
+                                                                              dinvc.p, z);
+            k_fsc_mech<<<grid_for((long long)m * nu, 256), 256, 0, st>>>(m, nu, nt, nq, wm, o.biot_b, r, z, o.E.off.p,
+                                                                         o.E.idx.p, o.E.val.p, mech.p);
+            count_launch(2);
+            PDG_CHECK_LAUNCH();
+        }
+        a->chol.solve(mech.p, nu, z, nt, m, st);
+        return;
+    }
     const int lag = xprev != nullptr;
     {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (2.0 * np + 2.0 * nq + 3.0 * o.B.nnz));
@@ -638,8 +856,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
 }
 
 void FsSolver::create(const SpatialOps& o, int r, double tau_, double stab, std::shared_ptr<ASolver> a) {
-    require(r == 0, "fixed-stress solver: the device path covers dG(0); dG(r >= 1) couples the time components in "
-                    "the flow block (non-symmetric), not on the device yet");
+    require(r == 0 || r == 1, "fixed-stress solver: dG(r) with r <= 1 on the device");
     require(tau_ > 0.0, "FixedStressSolver: tau must be positive");
     stab = stab < 0.0 ? o.biot_b * o.biot_b / o.k_dr : stab;  // FixedStressConfig::resolve_stab
     require(stab >= 0.0, "fixed-stress: stabilization must be nonnegative");
@@ -649,9 +866,12 @@ void FsSolver::create(const SpatialOps& o, int r, double tau_, double stab, std:
     tau = tau_;
     cudaStream_t st = ctx->stream;
     const TimeConsts tc = time_consts(r);  // Theta = G_hat, kappa = weights (both [1] for r = 0)
-    op.build(o, m, tc.G.data(), tau, st);
+    op.build(o, m, tc.G.data(), tau, st, tc.weights.data());
     if (!a) a = make_a_solver(o, 2, st);
-    pre.setup(o, m, tau, tc.G[0], stab, 1, a, st);
+    if (m == 1)
+        pre.setup(o, m, tau, tc.G[0], stab, 1, a, st);
+    else
+        pre.setup_coupled(o, m, tau, tc.G.data(), tc.weights.data(), stab, a, st);
     const long long n = (long long)m * o.n_total();
     red.setup(n, 1, false, st);
     xa.alloc(n);

@@ -31,6 +31,17 @@ struct FixedStressPre {
                std::shared_ptr<ASolver> a, cudaStream_t st);
     void apply(const double* r, double* z, cudaStream_t st);
     void sweep_once(const double* xprev, const double* r, double* z, cudaStream_t st);
+
+    // Coupled form (the fixed-stress march's untransformed slab block, march.hpp:83-84):
+    // full Theta = G_hat and kappa = Radau weights, m <= 2. The pressure block
+    // -Theta (x) (1/M + stab) M_p is eliminated per cell, the flux Schur complement
+    // W (x) M_q + (W Theta^{-1} W) (x) B D^{-1} B^T couples the components and is
+    // not symmetric: twisted block LU in face-row blocks holding both components.
+    bool coupled = false;
+    double th[4] = {0, 0, 0, 0}, thinv[4] = {0, 0, 0, 0}, wc[2] = {0, 0};
+    DBuf<double> dinvc, qtmp;
+    void setup_coupled(const SpatialOps& ops, int m, double tau, const double* theta, const double* kappa, double stab,
+                       std::shared_ptr<ASolver> a, cudaStream_t st);
 };
 
 struct Gmres {

@@ -17,6 +17,7 @@ namespace {
 
 struct Theta {
     double t[4];
+    double w[2];  // tau * kappa_i per component (fixed_stress.hpp:50; kappa = 1 in the slab solver)
 };
 
 // ---- U class ---------------------------------------------------------------
@@ -30,7 +31,7 @@ __global__ void k_u_count(int n_cells, const int* __restrict__ a_off, const int*
     }
 }
 
-__global__ void k_u_fill(int n_cells, int m, int nt, int nu, int nq, double tau, double mb, const int* __restrict__ a_off,
+__global__ void k_u_fill(int n_cells, int m, int nt, int nu, int nq, Theta th, double mb, const int* __restrict__ a_off,
                          const int* __restrict__ a_idx, const double* __restrict__ a_val, const int* __restrict__ e_off,
                          const int* __restrict__ e_idx, const double* __restrict__ e_val, const long long* __restrict__ u_off,
                          int* u_col, double* u_val, int* err) {
@@ -50,13 +51,13 @@ __global__ void k_u_fill(int n_cells, int m, int nt, int nu, int nq, double tau,
         for (int q = 0; q < la; ++q, ++k) {
             const int col = a_idx[a_off[r] + q];
             if (col != a_idx[a_off[r0] + q]) atomicOr(err, 2);
-            u_val[k * 8 + l] = __dmul_rn(tau, a_val[a_off[r] + q]);
+            u_val[k * 8 + l] = __dmul_rn(th.w[i], a_val[a_off[r] + q]);
             if (l == 0) u_col[k] = i * nt + col;
         }
         for (int q = 0; q < le; ++q, ++k) {
             const int col = e_idx[e_off[r] + q];
             if (col != e_idx[e_off[r0] + q]) atomicOr(err, 2);
-            u_val[k * 8 + l] = __dmul_rn(tau, __dmul_rn(mb, e_val[e_off[r] + q]));
+            u_val[k * 8 + l] = __dmul_rn(th.w[i], __dmul_rn(mb, e_val[e_off[r] + q]));
             if (l == 0) u_col[k] = i * nt + nu + nq + col;
         }
     }
@@ -110,8 +111,8 @@ __global__ void k_s_fill(long long s_rows, int m, int nt, int nu, int nq, int np
         };
         if (loc < nq) {
             const int f = loc;
-            for (int q = mq_off[f]; q < mq_off[f + 1]; ++q) put(i * nt + nu + mq_idx[q], __dmul_rn(tau, mq_val[q]));
-            for (int q = b_off[f]; q < b_off[f + 1]; ++q) put(i * nt + nu + nq + b_idx[q], __dmul_rn(tau, b_val[q]));
+            for (int q = mq_off[f]; q < mq_off[f + 1]; ++q) put(i * nt + nu + mq_idx[q], __dmul_rn(th.w[i], mq_val[q]));
+            for (int q = b_off[f]; q < b_off[f + 1]; ++q) put(i * nt + nu + nq + b_idx[q], __dmul_rn(th.w[i], b_val[q]));
         } else {
             const int c = loc - nq;
             for (int j = 0; j < m; ++j) {
@@ -120,7 +121,8 @@ __global__ void k_s_fill(long long s_rows, int m, int nt, int nu, int nq, int np
                     for (int q = et_off[c]; q < et_off[c + 1]; ++q)
                         put(j * nt + et_idx[q], __dmul_rn(t, __dmul_rn(mb, et_val[q])));
                 if (j == i)
-                    for (int q = bt_off[c]; q < bt_off[c + 1]; ++q) put(i * nt + nu + bt_idx[q], __dmul_rn(tau, bt_val[q]));
+                    for (int q = bt_off[c]; q < bt_off[c + 1]; ++q)
+                        put(i * nt + nu + bt_idx[q], __dmul_rn(th.w[i], bt_val[q]));
                 if (t != 0.0) put(j * nt + nu + nq + c, __dmul_rn(t, __dmul_rn(minv, m_p[c])));
             }
         }
@@ -267,7 +269,8 @@ long long exclusive_scan_ll(const long long* in, long long* out, long long n, cu
 
 }  // namespace
 
-void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, double tau, cudaStream_t st) {
+void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, double tau, cudaStream_t st,
+                        const double* kappa) {
     require(m_ == 1 || m_ == 2, "space-time block: m must be 1 or 2");
     m = m_;
     n_u = ops.n_u;
@@ -278,6 +281,7 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     rows = (long long)m * nt;
     Theta th{};
     for (int k = 0; k < m * m; ++k) th.t[k] = theta[k];
+    for (int i = 0; i < m; ++i) th.w[i] = kappa ? tau * kappa[i] : tau;
     const double mb = -ops.biot_b, minv = -ops.inv_m;
     require(ops.n_u == 8 * ops.n_p, "space-time block: n_u must be 8 * n_cells");
 
@@ -293,7 +297,7 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     u_val.alloc(8 * u_entries);
     DBuf<int> err(1);
     err.zero(st);
-    k_u_fill<<<grid_for(u_groups * 8, 256), 256, 0, st>>>(n_cells, m, nt, n_u, n_q, tau, mb, ops.A.off.p, ops.A.idx.p,
+    k_u_fill<<<grid_for(u_groups * 8, 256), 256, 0, st>>>(n_cells, m, nt, n_u, n_q, th, mb, ops.A.off.p, ops.A.idx.p,
                                                            ops.A.val.p, ops.E.off.p, ops.E.idx.p, ops.E.val.p, u_off.p,
                                                            u_col.p, u_val.p, err.p);
     PDG_CHECK_LAUNCH();

@@ -37,7 +37,10 @@ struct SpaceTimeOp {
     DBuf<int> s_col;        // 32 * s_slots
     DBuf<double> s_val;     // 32 * s_slots
 
-    void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st);
+    // kappa: per-component stationary weights (w_i = tau kappa_i, fixed_stress.hpp:50);
+    // null = 1 (the slab solver, slab.hpp:162)
+    void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st,
+               const double* kappa = nullptr);
     void apply(const double* x, double* y, cudaStream_t st) const;
     // Rows owned by the strip of cell rows [r0, r1) of an nx x ny mesh (multi-GPU
     // row partitioning): displacement and pressure rows of its

@@ -357,7 +357,7 @@ class SlabSolver:
 class FixedStressSolver:
     """FixedStressSolver::solve (fixed_stress.hpp:144-172) of the fixed-stress
     march (march.hpp:80-108): Theta = G_hat, kappa = Radau weights, sweeps on the
-    untransformed slab block from a warm start. Device path: dG(0)."""
+    untransformed slab block from a warm start. Device path: dG(0) and dG(1)."""
 
     def __init__(self, ops: SpatialOperators, r: int, tau: float, cfg: FixedStressConfig | None = None):
         self.ops, self.r, self.tau = ops, r, tau

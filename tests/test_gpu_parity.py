@@ -356,16 +356,19 @@ def test_iteration_log_from_gpu_march():
     assert runlog.slab_line(9, t_points[10], reps[9], run["r"]).startswith("slab    9  t_n=0.2          method=")
 
 
-def test_fixed_stress_march_config0_matches_oracle(oracle):
+@pytest.mark.parametrize("r", [0, 1])
+def test_fixed_stress_march_config0_matches_oracle(oracle, r):
     """Fixed-stress march (march.hpp:80-108, fixed_stress.hpp:144-172) of config
-    0 (dG(0)) on the device vs the oracle: identical sweep counts per slab and
-    per-slab states within 1e-9 (both converge the true residual to 1e-10)."""
+    0 on the device vs the oracle, dG(0) and dG(1) (full Theta = G_hat, Radau
+    weights: the coupled flow Schur complement by twisted block LU): identical
+    sweep counts per slab and per-slab states within 1e-9 (both converge the
+    true residual to 1e-10)."""
     spec = P.config0()
     run = P.RUNS["config0"]
     rp = oracle.RefProblem(spec.to_dict())
-    ref = rp.march_fs(0, run["T"], run["n_slabs"], tol=1e-10, max_sweeps=200, keep_states=True)
+    ref = rp.march_fs(r, run["T"], run["n_slabs"], tol=1e-10, max_sweeps=200, keep_states=True)
     ops = S.SpatialOperators.assemble(spec)
-    reps, states = S.march(ops, 0, run["T"], run["n_slabs"], S.SolveOptions(), keep_states=True,
+    reps, states = S.march(ops, r, run["T"], run["n_slabs"], S.SolveOptions(), keep_states=True,
                            method="fixed-stress")
     for n, rep in enumerate(reps):
         assert rep.converged and rep.iterations == int(ref["sweeps"][n]), (n, rep.iterations, ref["sweeps"][n])
@@ -373,14 +376,14 @@ def test_fixed_stress_march_config0_matches_oracle(oracle):
         assert np.linalg.norm(states[n] - refs) <= SOLVE_RTOL * np.linalg.norm(refs)
 
 
-def test_fixed_stress_solver_errors_and_dg1():
+def test_fixed_stress_solver_errors():
     """Argument errors follow FixedStressConfig::validate (fixed_stress.hpp:29-34);
-    dG(1) is refused on the device with a clear message."""
+    dG(r >= 2) is refused on the device with a clear message."""
     ops = S.SpatialOperators.assemble(P.config0())
     with pytest.raises(S.InvalidArgument):
         S.FixedStressSolver(ops, 0, 0.1, S.FixedStressConfig(tol=2.0))
     with pytest.raises(S.InvalidArgument):
-        S.FixedStressSolver(ops, 1, 0.1)
+        S.FixedStressSolver(ops, 2, 0.1)
     fs = S.FixedStressSolver(ops, 0, 0.1, S.FixedStressConfig(max_sweeps=1, tol=1e-15))
     with pytest.raises(S.SolverError, match="fixed-stress did not converge"):
         fs.solve(P.uniform_vector(5, ops.n_total))
