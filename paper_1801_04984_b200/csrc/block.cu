@@ -309,12 +309,45 @@ std::vector<double> ls_colpiv(std::vector<double> a, int rows, int cols, std::ve
 }  // namespace
 
 // ---------------------------------------------------------------------------
+HCsr csr_download(const DCsr& a, cudaStream_t st) {
+    HCsr h;
+    h.rows = a.rows;
+    h.cols = a.cols;
+    h.off = a.off.download(st);
+    h.idx = a.idx.download(st);
+    h.val = a.val.download(st);
+    return h;
+}
+
+int nd_leaf_dofs(int dflt) {
+    const char* e = std::getenv("PDG_ND_LEAF");
+    return e ? std::max(1, std::atoi(e)) : dflt;
+}
+
 std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st) {
     auto a = std::make_shared<ASolver>();
     // cell-row order: block j = displacement dofs of cell row j (8 nx each)
     require(ops.nx > 0 && ops.ny > 0 && ops.n_u == 8 * ops.nx * ops.ny, "A solver: mesh dimensions do not match n_u");
+    // nd (default): nested dissection; local: twisted block-tridiagonal inverse-Schur sweep;
+    // general: the block-tridiagonal three-matrix recurrence
+    const char* mode = std::getenv("PDG_A_SOLVER");
+    if (!mode || std::string(mode) == "nd") {
+        // nested dissection over cells (row-major, 8 dofs each, centres (i + 1/2, j + 1/2))
+        const HCsr h = csr_download(ops.A, st);
+        const int nc = ops.nx * ops.ny;
+        std::vector<int> node_of(ops.n_u);
+        for (int d = 0; d < ops.n_u; ++d) node_of[d] = d / 8;
+        std::vector<double> cx(nc), cy(nc);
+        for (int c = 0; c < nc; ++c) {
+            cx[c] = c % ops.nx + 0.5;
+            cy[c] = c / ops.nx + 0.5;
+        }
+        a->use_nd = true;
+        a->nd.prof_phase = PROF_A_SOLVE;
+        a->nd.factor(ops.n_u, h.off, h.idx, h.val, node_of, cx, cy, nd_leaf_dofs(128), max_rhs, st);
+        return a;
+    }
     std::vector<int> bs(ops.ny, 8 * ops.nx);
-    const char* mode = std::getenv("PDG_A_SOLVER");  // "general": the three-matrix recurrence path
     a->chol.allow_local = !(mode && std::string(mode) == "general");
     a->chol.factor(ops.n_u, ops.A.off.p, ops.A.idx.p, ops.A.val.p, {}, bs, max_rhs, st);
     return a;
@@ -448,6 +481,54 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     // face-row permutation: level j horizontal faces, then row j vertical faces
     const int nx = o.nx, ny = o.ny;
     require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
+    rq.alloc((size_t)m * o.n_q);
+    fp.alloc((size_t)m * o.n_p);
+    mech.alloc((size_t)m * o.n_u);
+    if (sweeps > 1) xold.alloc((size_t)m * o.n_total());
+    const char* fmode = std::getenv("PDG_FLOW_SOLVER");  // nd (default) | blocktri
+    if ((!fmode || std::string(fmode) == "nd") && !std::getenv("PDG_FLOW_STRIPS")) {
+        // S_q assembled on the host (the entries of k_flow_schur_blocks), nested dissection over
+        // faces: horizontal j*nx+i at (i + 1/2, j), vertical nx(ny+1) + i*ny + j at (i, j + 1/2)
+        const HCsr mq = csr_download(o.M_q, st), bb = csr_download(o.B, st), bt = csr_download(o.Bt, st);
+        const std::vector<double> di = dinv.download(st);
+        std::vector<int> off(o.n_q + 1, 0), idx;
+        std::vector<double> val;
+        for (int f = 0; f < o.n_q; ++f) {
+            std::vector<std::pair<int, double>> row;
+            for (int k = mq.off[f]; k < mq.off[f + 1]; ++k) row.push_back({mq.idx[k], w * mq.val[k]});
+            for (int k = bb.off[f]; k < bb.off[f + 1]; ++k) {
+                const int c = bb.idx[k];
+                const double wa = w * bb.val[k];
+                for (int q = bt.off[c]; q < bt.off[c + 1]; ++q) row.push_back({bt.idx[q], -(wa * (w * bt.val[q])) * di[c]});
+            }
+            std::stable_sort(row.begin(), row.end(), [](auto& a, auto& b) { return a.first < b.first; });
+            for (size_t k = 0; k < row.size();) {
+                double v = 0.0;
+                const int col = row[k].first;
+                for (; k < row.size() && row[k].first == col; ++k) v += row[k].second;
+                idx.push_back(col);
+                val.push_back(v);
+            }
+            off[f + 1] = static_cast<int>(idx.size());
+        }
+        std::vector<int> node_of(o.n_q);
+        std::vector<double> cx(o.n_q), cy(o.n_q);
+        for (int f = 0; f < o.n_q; ++f) {
+            node_of[f] = f;
+            if (f < nx * (ny + 1)) {
+                cx[f] = f % nx + 0.5;
+                cy[f] = f / nx;
+            } else {
+                const int g = f - nx * (ny + 1);
+                cx[f] = g / ny;
+                cy[f] = g % ny + 0.5;
+            }
+        }
+        flow_use_nd = true;
+        flow_nd.prof_phase = PROF_FLOW_SOLVE;
+        flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(64), m, st);
+        return;
+    }
     std::vector<int> perm;
     std::vector<int> bs;
     perm.reserve(o.n_q);
@@ -483,10 +564,6 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     PDG_CUDA(cudaStreamSynchronize(st));
     require(herr == 0, "fixed-stress: flow Schur complement is not block tridiagonal in face-row order");
     flow.factor_dense(dense.p, st);
-    rq.alloc((size_t)m * o.n_q);
-    fp.alloc((size_t)m * o.n_p);
-    mech.alloc((size_t)m * o.n_u);
-    if (sweeps > 1) xold.alloc((size_t)m * o.n_total());
 }
 
 void FixedStressPre::setup_coupled(const SpatialOps& o, int m_, double tau_, const double* theta, const double* kappa,
@@ -607,7 +684,7 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
             count_launch(2);
             PDG_CHECK_LAUNCH();
         }
-        a->chol.solve(mech.p, nu, z, nt, m, st);
+        a->solve(mech.p, nu, z, nt, m, st);
         return;
     }
     const int lag = xprev != nullptr;
@@ -621,7 +698,10 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
         count_launch(2);
         PDG_CHECK_LAUNCH();
     }
-    flow.solve(rq.p, nq, z + nu, nt, m, st);
+    if (flow_use_nd)
+        flow_nd.solve(rq.p, nq, z + nu, nt, m, st);
+    else
+        flow.solve(rq.p, nq, z + nu, nt, m, st);
     {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (3.0 * np + 2.0 * o.Bt.nnz + 2.0 * nu + 2.0 * o.E.nnz));
         k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fp.p, o.Bt.off.p, o.Bt.idx.p,
@@ -631,7 +711,7 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
         count_launch(2);
         PDG_CHECK_LAUNCH();
     }
-    a->chol.solve(mech.p, nu, z, nt, m, st);
+    a->solve(mech.p, nu, z, nt, m, st);
 }
 
 void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {

@@ -6,6 +6,7 @@
 #include <memory>
 
 #include "blocktri.cuh"
+#include "nd.cuh"
 #include "ops.cuh"
 #include "spacetime_op.cuh"
 
@@ -14,7 +15,15 @@ namespace pdg {
 // Shared exact displacement solve (the reference shares one DenseLu of A
 // across all blocks, slab.hpp:155 / fixed_stress.hpp:89-94).
 struct ASolver {
-    BlockTriChol chol;
+    BlockTriChol chol;  // twisted block-tridiagonal (PDG_A_SOLVER=local|general)
+    NdChol nd;          // nested dissection (PDG_A_SOLVER=nd)
+    bool use_nd = false;
+    void solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
+        if (use_nd)
+            nd.solve(b, ldb, x, ldx, nrhs, st);
+        else
+            chol.solve(b, ldb, x, ldx, nrhs, st);
+    }
 };
 std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st);
 
@@ -25,6 +34,8 @@ struct FixedStressPre {
     double tau = 0, lambda = 0, stab = 0, w = 0;
     std::shared_ptr<ASolver> a;
     BlockTriChol flow;  // S_q = w M_q - w^2 B D^{-1} B^T in face-row order
+    NdChol flow_nd;     // the same S_q by nested dissection (PDG_FLOW_SOLVER=nd)
+    bool flow_use_nd = false;
     DBuf<double> dinv;  // 1 / (-(lambda (1/M + stab)) m_p)
     DBuf<double> rq, fp, mech, xold;
     void setup(const SpatialOps& ops, int m, double tau, double lambda, double stab, int sweeps,

@@ -1,0 +1,892 @@
+// Nested-dissection multifrontal Cholesky (see nd.cuh).
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cmath>
+#include <numeric>
+#include <queue>
+#include <string>
+
+#include "blocktri.cuh"
+#include "llsync.cuh"
+#include "nd.cuh"
+
+namespace cg = cooperative_groups;
+
+#define PDG_ND_CUSOLVER(call)                                                                                       \
+    do {                                                                                                            \
+        cusolverStatus_t s_ = (call);                                                                               \
+        if (s_ != CUSOLVER_STATUS_SUCCESS)                                                                          \
+            throw ::pdg::Error(PDG_CUDA_ERROR, std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
+    } while (0)
+#define PDG_ND_CUBLAS(call)                                                                                       \
+    do {                                                                                                          \
+        cublasStatus_t s_ = (call);                                                                               \
+        if (s_ != CUBLAS_STATUS_SUCCESS)                                                                          \
+            throw ::pdg::Error(PDG_CUDA_ERROR, std::string(#call) + ": cublas status " + std::to_string((int)s_)); \
+    } while (0)
+
+namespace pdg {
+
+namespace {
+
+constexpr int kNdThreads = 256;
+constexpr int kNdMaxRhs = 2;
+constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector staging in shared memory)
+
+// ---------------------------------------------------------------------------
+// host: nested dissection
+// ---------------------------------------------------------------------------
+struct HostFront {
+    std::vector<int> snodes, bnodes;
+    int parent = -1, depth = 0;
+    std::vector<int> children;
+};
+
+struct Dissector {
+    const std::vector<int>& aoff;  // node adjacency CSR
+    const std::vector<int>& adj;
+    const std::vector<int>& ndofs;
+    const std::vector<double>& cx;
+    const std::vector<double>& cy;
+    int leaf;
+    std::vector<HostFront> fr;
+    std::vector<int> node_front, mark, seen;
+    int stamp = 0;
+
+    Dissector(const std::vector<int>& o, const std::vector<int>& a, const std::vector<int>& nd,
+              const std::vector<double>& x, const std::vector<double>& y, int lf)
+        : aoff(o), adj(a), ndofs(nd), cx(x), cy(y), leaf(lf) {
+        const int nn = static_cast<int>(nd.size());
+        node_front.assign(nn, -1);
+        mark.assign(nn, 0);
+        seen.assign(nn, 0);
+    }
+
+    // try to cut `nodes` at the line coord == v (axis 0: x, 1: y)
+    bool try_cut(const std::vector<int>& nodes, int axis, double v, int st, std::vector<int>& sep,
+                 std::vector<int>& lo, std::vector<int>& hi) {
+        const std::vector<double>& c = axis == 0 ? cx : cy;
+        sep.clear();
+        lo.clear();
+        hi.clear();
+        for (int u : nodes) {
+            if (c[u] < v)
+                lo.push_back(u);
+            else if (c[u] > v)
+                hi.push_back(u);
+            else
+                sep.push_back(u);
+        }
+        if (lo.empty() || hi.empty() || sep.empty()) return false;
+        for (int u : lo)
+            for (int k = aoff[u]; k < aoff[u + 1]; ++k) {
+                const int w = adj[k];
+                if (mark[w] == st && c[w] > v) return false;
+            }
+        return true;
+    }
+
+    int build(std::vector<int> nodes, int parent, int depth) {
+        const int st = ++stamp;
+        for (int u : nodes) mark[u] = st;
+        std::vector<int> bnd;
+        for (int u : nodes)
+            for (int k = aoff[u]; k < aoff[u + 1]; ++k) {
+                const int w = adj[k];
+                if (mark[w] != st && seen[w] != st) {
+                    seen[w] = st;
+                    if (node_front[w] < 0) throw Error(PDG_INVALID_ARGUMENT, "nested dissection: region boundary outside the ancestor separators");
+                    bnd.push_back(w);
+                }
+            }
+        long long dofs = 0;
+        for (int u : nodes) dofs += ndofs[u];
+        std::vector<int> sep, lo, hi;
+        bool cut = false;
+        if (dofs > leaf && nodes.size() >= 3) {
+            double mn[2] = {1e300, 1e300}, mx[2] = {-1e300, -1e300};
+            for (int u : nodes) {
+                mn[0] = std::min(mn[0], cx[u]);
+                mx[0] = std::max(mx[0], cx[u]);
+                mn[1] = std::min(mn[1], cy[u]);
+                mx[1] = std::max(mx[1], cy[u]);
+            }
+            const int first = (mx[0] - mn[0] >= mx[1] - mn[1]) ? 0 : 1;
+            for (int t = 0; t < 2 && !cut; ++t) {
+                const int axis = t == 0 ? first : 1 - first;
+                const std::vector<double>& c = axis == 0 ? cx : cy;
+                std::vector<double> vals;
+                vals.reserve(nodes.size());
+                for (int u : nodes) vals.push_back(c[u]);
+                std::sort(vals.begin(), vals.end());
+                const double med = vals[vals.size() / 2];
+                vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+                std::vector<double> cand(vals);
+                std::stable_sort(cand.begin(), cand.end(),
+                                 [&](double a, double b) { return std::fabs(a - med) < std::fabs(b - med); });
+                const int tries = std::min<int>(static_cast<int>(cand.size()), 8);
+                for (int k = 0; k < tries && !cut; ++k) cut = try_cut(nodes, axis, cand[k], st, sep, lo, hi);
+            }
+        }
+        const int id = static_cast<int>(fr.size());
+        fr.emplace_back();
+        fr[id].parent = parent;
+        fr[id].depth = depth;
+        fr[id].bnodes = std::move(bnd);
+        fr[id].snodes = cut ? sep : nodes;
+        for (int u : fr[id].snodes) node_front[u] = id;
+        if (cut) {
+            const int a = build(std::move(lo), id, depth + 1);
+            const int b = build(std::move(hi), id, depth + 1);
+            fr[id].children = {a, b};
+        }
+        return id;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// device: numeric factorization helpers (setup)
+// ---------------------------------------------------------------------------
+__global__ void k_nd_scatter(long long nt, const long long* pos, const double* val, double* F) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nt; t += (long long)gridDim.x * blockDim.x)
+        F[pos[t]] = val[t];
+}
+// parent(lower) += child update matrix (lower), both column-major
+__global__ void k_nd_extend_add(double* P, int fp, const double* U, int fc, int bc, const int* map) {
+    const long long tot = (long long)bc * bc;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const int r = static_cast<int>(t % bc), c = static_cast<int>(t / bc);
+        if (r < c) continue;
+        const int pr = map[r], pc = map[c];
+        const int hi = max(pr, pc), lo = min(pr, pc);
+        P[hi + (long long)lo * fp] += U[r + (long long)c * fc];
+    }
+}
+__global__ void k_nd_identity(int s, double* T) {
+    const long long tot = (long long)s * s;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x)
+        T[t] = (t % s == t / s) ? 1.0 : 0.0;
+}
+// M (row-major (s+b) x ldm) and M^T (row-major s x ldt) from Linv (s x s, col-major, ld s)
+// and G = L_BS Linv (b x s, col-major, ld b); padding zero.
+__global__ void k_nd_pack(int s, int b, const double* T, const double* G, double* M, int ldm, double* MT, int ldt) {
+    const long long tot = (long long)(s + b) * ldm;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const int r = static_cast<int>(t / ldm), c = static_cast<int>(t % ldm);
+        double v = 0.0;
+        if (c < s) v = r < s ? T[r + (long long)c * s] : G[(r - s) + (long long)c * b];
+        M[t] = v;
+    }
+    const long long tt = (long long)s * ldt;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tt; t += (long long)gridDim.x * blockDim.x) {
+        const int r = static_cast<int>(t / ldt), c = static_cast<int>(t % ldt);
+        double v = 0.0;
+        if (c < s)
+            v = T[c + (long long)r * s];
+        else if (c < s + b)
+            v = G[(c - s) + (long long)r * b];
+        MT[t] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// device: the solve
+// ---------------------------------------------------------------------------
+struct NdArgs {
+    const NdTask* tasks;
+    const int* ctoff;
+    const int* sdofs;
+    const int* bpos;
+    const int* cm;  // [2][n]: per pivot position, the children's update-vector entry (-1 none)
+    const int* bm;  // [2][nb]: per boundary entry, the children's update-vector entry (-1 none)
+    long long nbtot;
+    const double* store;
+    const double* b;
+    long long ldb;
+    double* x;
+    long long ldx;
+    double* y;
+    double* xpos;
+    double* u;
+    unsigned long long* cnt;
+    unsigned long long call;
+    long long utot;
+    int n, nrhs, stages, vmax, max_tasks, pf;
+    unsigned stage_bytes;
+    unsigned long long* dbg;  // optional: per task, %globaltimer at start (after the wait) and end
+    unsigned long long* prof; // optional: per CTA, ns in [dependency wait, input gather, ring wait, rest] (warp 0)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// 16 per-lane values summed across the warp: on return lane l (< 16) holds the
+// total of index l (reduce-scatter over each half-warp, then the two halves; fixed order)
+__device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o];
+            const double keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+// named barrier of the compute warps (the producer warp never joins)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdThreads) : "memory"); }
+
+// Warps 0-7 compute, warp 8 (one lane) streams the matrix chunks of this CTA's
+// tasks through the ring: full[k] completes on the TMA bytes, empty[k] when all
+// 8 compute warps are done with the slot.
+__global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
+    using namespace dev;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* empty = full + 32;
+    unsigned char* ring = smem + 512;
+    double* v = reinterpret_cast<double*>(ring + (size_t)a.stages * a.stage_bytes);
+    double* wadd = v + (size_t)a.vmax * kNdMaxRhs;  // [rhs][kNdMaxTaskRows]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t0 = a.ctoff[blockIdx.x], nt = a.ctoff[blockIdx.x + 1] - t0;
+    if (tid == 0) {
+        for (int k = 0; k < a.stages; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kNdThreads / 32) {  // producer
+        if (lane == 0) {
+            // two cursors over this CTA's matrix chunks: the ring fill, and an L2
+            // prefetch running pf chunks ahead of it (keeps HBM busy through dependency waits)
+            int ti = 0, tr = 0, pi = 0, pr = 0, seq = 0, pseq = 0;
+            NdTask Ti{}, Tp{};
+            int ti_loaded = -1, pi_loaded = -1;
+            auto next = [&](int& i, int& r, NdTask& T, int& loaded) -> bool {
+                while (i < nt) {
+                    if (loaded != i) {
+                        T = a.tasks[t0 + i];
+                        loaded = i;
+                    }
+                    if (T.type != 0 && r < T.nrows) return true;
+                    ++i;
+                    r = 0;
+                }
+                return false;
+            };
+            while (true) {
+                while (pseq < seq + a.pf && next(pi, pr, Tp, pi_loaded)) {
+                    const int rpc = static_cast<int>(a.stage_bytes / (8u * Tp.ld));
+                    const unsigned bytes = static_cast<unsigned>(min(rpc, Tp.nrows - pr)) * Tp.ld * 8u;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.store + Tp.src + (long long)pr * Tp.ld),
+                                 "r"(bytes)
+                                 : "memory");
+                    pr += rpc;
+                    ++pseq;
+                }
+                if (!next(ti, tr, Ti, ti_loaded)) break;
+                const int rpc = static_cast<int>(a.stage_bytes / (8u * Ti.ld));
+                const int k = seq % a.stages;
+                if (seq >= a.stages) mbar_wait(&empty[k], static_cast<unsigned>(((seq / a.stages) - 1) & 1));
+                const unsigned bytes = static_cast<unsigned>(min(rpc, Ti.nrows - tr)) * Ti.ld * 8u;
+                mbar_arrive_expect_tx(&full[k], bytes);
+                bulk_g2s(ring + (size_t)k * a.stage_bytes, a.store + Ti.src + (long long)tr * Ti.ld, bytes, &full[k]);
+                tr += rpc;
+                ++seq;
+                if (pseq < seq) {  // prefetch cursor never behind the fill
+                    pi = ti;
+                    pr = tr;
+                    pseq = seq;
+                }
+            }
+        }
+        return;
+    }
+    const int nr = a.nrhs;
+    int seq = 0;  // chunks consumed
+    int last_front = -1, last_type = -1;
+    NdTask T = nt > 0 ? a.tasks[t0] : NdTask{};
+    unsigned long long pacc[4] = {0, 0, 0, 0}, pt = a.prof ? globaltimer() : 0;
+    auto mark = [&](int k) {
+        if (a.prof) {
+            const unsigned long long now = globaltimer();
+            pacc[k] += now - pt;
+            pt = now;
+        }
+    };
+    for (int i = 0; i < nt; ++i) {
+        const NdTask Tn = i + 1 < nt ? a.tasks[t0 + i + 1] : T;  // prefetch the next descriptor
+        mark(3);
+        // ---- wait for the dependencies ----
+        if (tid == 0) {
+            if (T.wait0 >= 0) {
+                const unsigned long long tgt = a.call * (unsigned long long)T.need0;
+                while (ld_acquire(a.cnt + T.wait0) < tgt) {
+                }
+            }
+            if (T.wait1 >= 0) {
+                const unsigned long long tgt = a.call * (unsigned long long)T.need1;
+                while (ld_acquire(a.cnt + T.wait1) < tgt) {
+                }
+            }
+        }
+        compute_sync();
+        mark(0);
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 2] = globaltimer();
+        {
+            const int len = T.ncols, lp = T.ld;
+            if (T.front != last_front || T.type != last_type) {
+                for (int c = tid; c < lp * nr; c += kNdThreads) {
+                    const int k = c / lp, cc = c % lp;
+                    double val = 0.0;
+                    if (cc < len) {
+                        if (T.type == 1) {
+                            // b_S minus the children's update vectors (multifrontal forward)
+                            const int pos = T.sdof + cc;
+                            const int m1 = a.cm[pos], m2 = a.cm[a.n + pos];
+                            val = a.b[k * a.ldb + a.sdofs[pos]];
+                            const double w1 = m1 >= 0 ? __ldcg(a.u + k * a.utot + m1) : 0.0;
+                            const double w2 = m2 >= 0 ? __ldcg(a.u + k * a.utot + m2) : 0.0;
+                            if (m1 >= 0) val -= w1;
+                            if (m2 >= 0) val -= w2;
+                        } else if (cc < T.s) {
+                            val = __ldcg(a.y + (long long)k * a.n + T.sdof + cc);
+                        } else {
+                            val = -__ldcg(a.xpos + (long long)k * a.n + a.bpos[T.bdof + cc - T.s]);
+                        }
+                    }
+                    v[k * a.vmax + cc] = val;
+                }
+                last_front = T.front;
+                last_type = T.type;
+            }
+            if (T.type == 1) {  // children's update-vector entries passing through this task's boundary rows
+                const int r_lo = max(T.r0, T.s), r_hi = T.r0 + T.nrows, cnt = max(0, r_hi - r_lo);
+                for (int c = tid; c < cnt * nr; c += kNdThreads) {
+                    const int k = c / cnt, j = r_lo + c % cnt - T.s;
+                    const int m1 = a.bm[T.bdof + j], m2 = a.bm[a.nbtot + T.bdof + j];
+                    const double w1 = m1 >= 0 ? __ldcg(a.u + k * a.utot + m1) : 0.0;
+                    const double w2 = m2 >= 0 ? __ldcg(a.u + k * a.utot + m2) : 0.0;
+                    wadd[k * kNdMaxTaskRows + (r_lo - T.r0) + c % cnt] = w1 + w2;
+                }
+            }
+            compute_sync();
+            mark(1);
+            // chunk j of this CTA's stream is consumed by warp j % 8 alone: groups of 8
+            // rows, lanes over the columns, warp reduce-scatter (no CTA barrier per chunk)
+            const int rpc = static_cast<int>(a.stage_bytes / (8u * T.ld));
+            const int ld2 = T.ld >> 1;
+            for (int rc = 0; rc < T.nrows; rc += rpc, ++seq) {
+                if (seq % (kNdThreads / 32) != warp) continue;
+                const int slot = seq % a.stages;
+                mark(3);
+                mbar_wait(&full[slot], static_cast<unsigned>((seq / a.stages) & 1));
+                mark(2);
+                const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
+                const int nrow = min(rpc, T.nrows - rc);
+                for (int rb = 0; rb < nrow; rb += 8) {
+                    const int rn = min(8, nrow - rb);
+                    double acc[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                    for (int c2 = lane; c2 < ld2; c2 += 32) {
+                        const double v0x = v[2 * c2], v0y = v[2 * c2 + 1];
+                        const double v1x = v[a.vmax + 2 * c2], v1y = v[a.vmax + 2 * c2 + 1];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                            acc[2 * r] = fma(m.y, v0y, fma(m.x, v0x, acc[2 * r]));
+                            acc[2 * r + 1] = fma(m.y, v1y, fma(m.x, v1x, acc[2 * r + 1]));
+                        }
+                    }
+                    const double tot = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
+                    const int r = lane >> 1, k = lane & 1;
+                    if (lane < 16 && r < rn && k < nr) {
+                        const int gr = T.r0 + rc + rb + r;
+                        if (T.type == 2) {
+                            a.xpos[(long long)k * a.n + T.sdof + gr] = tot;
+                            a.x[k * a.ldx + a.sdofs[T.sdof + gr]] = tot;
+                        } else if (gr < T.s) {
+                            a.y[(long long)k * a.n + T.sdof + gr] = tot;
+                        } else {
+                            a.u[k * a.utot + T.uoff + gr - T.s] = tot + wadd[k * kNdMaxTaskRows + gr - T.r0];
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+            }
+        }
+        compute_sync();  // outputs written (and v free)
+        if (tid == 0) red_release_add(a.cnt + T.signal, 1ull);
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 2 + 1] = globaltimer();
+        T = Tn;
+    }
+    mark(3);
+    if (a.prof && tid == 0)
+        for (int k = 0; k < 4; ++k) a.prof[blockIdx.x * 4 + k] = pacc[k];
+}
+
+long long round2(long long v) { return (v + 1) & ~1LL; }
+
+}  // namespace
+
+void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>& idx, const std::vector<double>& val,
+                    const std::vector<int>& node_of, const std::vector<double>& cx, const std::vector<double>& cy,
+                    int leaf_dofs, int max_rhs_, cudaStream_t st) {
+    n = n_;
+    max_rhs = max_rhs_;
+    require(max_rhs >= 1 && max_rhs <= kNdMaxRhs, "nested dissection: at most 2 right-hand sides");
+    require(static_cast<int>(off.size()) == n + 1 && static_cast<int>(node_of.size()) == n, "nested dissection: bad CSR");
+    const int nn = static_cast<int>(cx.size());
+    // ---- node graph ----
+    std::vector<int> ndofs(nn, 0);
+    for (int d = 0; d < n; ++d) {
+        require(node_of[d] >= 0 && node_of[d] < nn, "nested dissection: bad node index");
+        ++ndofs[node_of[d]];
+    }
+    std::vector<int> noff(nn + 1, 0), nlist(n);
+    for (int u = 0; u < nn; ++u) noff[u + 1] = noff[u] + ndofs[u];
+    {
+        std::vector<int> fill(noff.begin(), noff.end() - 1);
+        for (int d = 0; d < n; ++d) nlist[fill[node_of[d]]++] = d;
+    }
+    std::vector<int> aoff(nn + 1, 0), adj;
+    {
+        std::vector<std::vector<int>> nb(nn);
+        for (int d = 0; d < n; ++d)
+            for (int k = off[d]; k < off[d + 1]; ++k) {
+                const int e = node_of[idx[k]];
+                if (e != node_of[d]) nb[node_of[d]].push_back(e);
+            }
+        for (int u = 0; u < nn; ++u) {
+            std::sort(nb[u].begin(), nb[u].end());
+            nb[u].erase(std::unique(nb[u].begin(), nb[u].end()), nb[u].end());
+            aoff[u + 1] = aoff[u] + static_cast<int>(nb[u].size());
+            adj.insert(adj.end(), nb[u].begin(), nb[u].end());
+        }
+    }
+    // ---- dissection ----
+    Dissector ds(aoff, adj, ndofs, cx, cy, leaf_dofs);
+    {
+        std::vector<int> all(nn);
+        std::iota(all.begin(), all.end(), 0);
+        ds.build(std::move(all), -1, 0);
+    }
+    for (int u = 0; u < nn; ++u) require(ds.node_front[u] >= 0, "nested dissection: unassigned node");
+    const int nf = static_cast<int>(ds.fr.size());
+    nfront = nf;
+    maxdepth = 0;
+    for (auto& f : ds.fr) maxdepth = std::max(maxdepth, f.depth);
+    // final order: deepest first (children before parents), stable in build order
+    std::vector<int> order(nf);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ds.fr[a].depth > ds.fr[b].depth; });
+    std::vector<int> newid(nf);
+    for (int k = 0; k < nf; ++k) newid[order[k]] = k;
+    // dof lists
+    std::vector<int> hs, hb;
+    std::vector<int> front_of(n, -1), spos(n, -1);
+    fronts.assign(nf, NdFront{});
+    std::vector<std::vector<int>> children(nf);
+    std::vector<int> parent(nf, -1);
+    for (int k = 0; k < nf; ++k) {
+        const HostFront& h = ds.fr[order[k]];
+        NdFront& F = fronts[k];
+        std::vector<int> sd, bd;
+        for (int u : h.snodes) sd.insert(sd.end(), nlist.begin() + noff[u], nlist.begin() + noff[u + 1]);
+        for (int u : h.bnodes) bd.insert(bd.end(), nlist.begin() + noff[u], nlist.begin() + noff[u + 1]);
+        std::sort(sd.begin(), sd.end());
+        std::sort(bd.begin(), bd.end());
+        F.s = static_cast<int>(sd.size());
+        F.b = static_cast<int>(bd.size());
+        F.sdof = static_cast<int>(hs.size());
+        F.bdof = static_cast<int>(hb.size());
+        F.depth = h.depth;
+        for (int i = 0; i < F.s; ++i) {
+            front_of[sd[i]] = k;
+            spos[sd[i]] = F.sdof + i;
+        }
+        hs.insert(hs.end(), sd.begin(), sd.end());
+        hb.insert(hb.end(), bd.begin(), bd.end());
+        parent[k] = h.parent < 0 ? -1 : newid[h.parent];
+        for (int c : h.children) children[k].push_back(newid[c]);
+    }
+    require(static_cast<int>(hs.size()) == n, "nested dissection: pivots do not cover the matrix");
+    // contribution slots and gather lists (contributors in front order)
+    utot = 0;
+    for (auto& F : fronts) {
+        F.uoff = static_cast<int>(utot);
+        utot += F.b;
+    }
+    // multifrontal update vectors w_F (b_F entries at uoff): w_F = u_F + the children's
+    // w restricted to B_F; the forward input of F is b_S minus the children's w on S_F
+    const long long nbt = static_cast<long long>(hb.size());
+    std::vector<int> hcm(2 * (size_t)n, -1), hbm(2 * (size_t)nbt, -1);
+    {
+        std::vector<int> lc(n, -1);
+        for (int k = 0; k < nf; ++k) {
+            const NdFront& F = fronts[k];
+            for (int i = 0; i < F.s; ++i) lc[hs[F.sdof + i]] = i;
+            for (int i = 0; i < F.b; ++i) lc[hb[F.bdof + i]] = F.s + i;
+            require(children[k].size() <= 2, "nested dissection: more than two children");
+            for (size_t q = 0; q < children[k].size(); ++q) {
+                const NdFront& C = fronts[children[k][q]];
+                for (int i = 0; i < C.b; ++i) {
+                    const int l = lc[hb[C.bdof + i]];
+                    require(l >= 0, "nested dissection: child boundary outside the parent front");
+                    if (l < F.s)
+                        hcm[q * (size_t)n + F.sdof + l] = C.uoff + i;
+                    else
+                        hbm[q * (size_t)nbt + F.bdof + l - F.s] = C.uoff + i;
+                }
+            }
+            for (int i = 0; i < F.s; ++i) lc[hs[F.sdof + i]] = -1;
+            for (int i = 0; i < F.b; ++i) lc[hb[F.bdof + i]] = -1;
+        }
+    }
+    // ---- storage layout ----
+    long long so = 0;
+    factor_bytes = 0.0;
+    vmax = 0;
+    for (auto& F : fronts) {
+        F.ldm = static_cast<int>(round2(F.s));
+        F.ldt = static_cast<int>(round2(F.s + F.b));
+        F.moff = so;
+        so += (long long)(F.s + F.b) * F.ldm;
+        F.mtoff = so;
+        so += (long long)F.s * F.ldt;
+        factor_bytes += 8.0 * ((double)(F.s + F.b) * F.s * 2.0);
+        vmax = std::max(vmax, F.ldt);
+    }
+    store.alloc((size_t)so);
+    // ---- numeric factorization (multifrontal, stream-serial, children first) ----
+    std::vector<long long> fo(nf);
+    long long ftot = 0;
+    int smax = 1, bmax = 1;
+    for (int k = 0; k < nf; ++k) {
+        const long long f = fronts[k].s + fronts[k].b;
+        fo[k] = ftot;
+        ftot += f * f;
+        smax = std::max(smax, fronts[k].s);
+        bmax = std::max(bmax, fronts[k].b);
+    }
+    DBuf<double> dense(ftot);
+    dense.zero(st);
+    std::vector<int> loc(n, -1);
+    {
+        std::vector<long long> tpos;
+        std::vector<double> tval;
+        for (int k = 0; k < nf; ++k) {
+            const NdFront& F = fronts[k];
+            const long long f = F.s + F.b;
+            for (int i = 0; i < F.s; ++i) loc[hs[F.sdof + i]] = i;
+            for (int i = 0; i < F.b; ++i) loc[hb[F.bdof + i]] = F.s + i;
+            for (int i = 0; i < F.s; ++i) {
+                const int d = hs[F.sdof + i];
+                for (int q = off[d]; q < off[d + 1]; ++q) {
+                    const int lj = loc[idx[q]];
+                    if (lj >= i) {
+                        tpos.push_back(fo[k] + lj + (long long)i * f);
+                        tval.push_back(val[q]);
+                    }
+                }
+            }
+            for (int i = 0; i < F.s; ++i) loc[hs[F.sdof + i]] = -1;
+            for (int i = 0; i < F.b; ++i) loc[hb[F.bdof + i]] = -1;
+        }
+        DBuf<long long> dpos;
+        DBuf<double> dval;
+        dpos.upload(tpos, st);
+        dval.upload(tval, st);
+        k_nd_scatter<<<grid_for((long long)tpos.size(), 256), 256, 0, st>>>((long long)tpos.size(), dpos.p, dval.p,
+                                                                           dense.p);
+        PDG_CHECK_LAUNCH();
+        PDG_CUDA(cudaStreamSynchronize(st));
+    }
+    // extend-add maps
+    std::vector<int> hmap;
+    std::vector<long long> mapoff(nf, 0);
+    for (int k = 0; k < nf; ++k) {
+        const NdFront& P = fronts[k];
+        for (int i = 0; i < P.s; ++i) loc[hs[P.sdof + i]] = i;
+        for (int i = 0; i < P.b; ++i) loc[hb[P.bdof + i]] = P.s + i;
+        for (int c : children[k]) {
+            mapoff[c] = static_cast<long long>(hmap.size());
+            for (int i = 0; i < fronts[c].b; ++i) {
+                const int l = loc[hb[fronts[c].bdof + i]];
+                require(l >= 0, "nested dissection: child boundary outside the parent front");
+                hmap.push_back(l);
+            }
+        }
+        for (int i = 0; i < P.s; ++i) loc[hs[P.sdof + i]] = -1;
+        for (int i = 0; i < P.b; ++i) loc[hb[P.bdof + i]] = -1;
+    }
+    DBuf<int> dmap;
+    dmap.upload(hmap, st);
+    LaHandles h(st);
+    int lwork = 0;
+    PDG_ND_CUSOLVER(cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, smax, dense.p, smax, &lwork));
+    DBuf<double> work(std::max(lwork, 1)), T((size_t)smax * smax), G((size_t)smax * bmax);
+    DBuf<int> info(nf);
+    info.zero(st);
+    const double one = 1.0, mone = -1.0, zero = 0.0;
+    for (int k = 0; k < nf; ++k) {
+        const NdFront& F = fronts[k];
+        const int s = F.s, b = F.b, f = s + b;
+        double* Fk = dense.p + fo[k];
+        for (int c : children[k]) {
+            const NdFront& C = fronts[c];
+            const int fc = C.s + C.b;
+            if (C.b == 0) continue;
+            k_nd_extend_add<<<grid_for((long long)C.b * C.b, 256), 256, 0, st>>>(
+                Fk, f, dense.p + fo[c] + C.s + (long long)C.s * fc, fc, C.b, dmap.p + mapoff[c]);
+            PDG_CHECK_LAUNCH();
+        }
+        PDG_ND_CUSOLVER(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, s, Fk, f, work.p, lwork, info.p + k));
+        if (b > 0) {
+            PDG_ND_CUBLAS(cublasDtrsm(h.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                                      CUBLAS_DIAG_NON_UNIT, b, s, &one, Fk, f, Fk + s, f));
+            PDG_ND_CUBLAS(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, b, s, &mone, Fk + s, f, &one,
+                                      Fk + s + (long long)s * f, f));
+        }
+        k_nd_identity<<<grid_for((long long)s * s, 256), 256, 0, st>>>(s, T.p);
+        PDG_CHECK_LAUNCH();
+        PDG_ND_CUBLAS(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                  s, s, &one, Fk, f, T.p, s));
+        if (b > 0)
+            PDG_ND_CUBLAS(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, b, s, s, &one, Fk + s, f, T.p, s, &zero, G.p, b));
+        k_nd_pack<<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store.p + F.moff, F.ldm,
+                                                                      store.p + F.mtoff, F.ldt);
+        PDG_CHECK_LAUNCH();
+    }
+    std::vector<int> hinfo(nf);
+    PDG_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < nf; ++k)
+        if (hinfo[k] != 0) throw Error(PDG_NOT_CONVERGED, "nested dissection: front " + std::to_string(k) + " not positive definite");
+    // ---- solve schedule: tasks in topological order, contiguous per phase on the CTAs ----
+    int dev = 0, nsm = 0;
+    PDG_CUDA(cudaGetDevice(&dev));
+    PDG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int task_chunks = 16;
+    pf = 16;
+    if (const char* e = std::getenv("PDG_ND_PF")) pf = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("PDG_ND_CHUNKS")) task_chunks = std::max(1, std::atoi(e));
+    stages = 16;
+    stage_bytes = static_cast<unsigned>(std::max<long long>(12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
+    if (const char* e = std::getenv("PDG_ND_STAGES")) stages = std::min(32, std::max(2, std::atoi(e)));
+    if (const char* e = std::getenv("PDG_ND_STAGE_KB")) stage_bytes = 1024u * std::max(8, std::atoi(e));
+    int ctas_per_sm = 1;
+    if (const char* e = std::getenv("PDG_ND_CTAS")) ctas_per_sm = std::max(1, std::atoi(e));
+    grid = nsm * ctas_per_sm;
+    for (const auto& F : fronts)
+        require((long long)F.ldt * 8 <= stage_bytes, "nested dissection: front wider than a ring stage");
+    std::vector<int> fwd_tasks(nf, 0), bwd_tasks(nf, 0);
+    std::vector<bool> leaf(nf);
+    for (int k = 0; k < nf; ++k) leaf[k] = children[k].empty();
+    std::vector<std::vector<NdTask>> per_cta(grid);
+    auto place = [&](std::vector<NdTask>& ts) {
+        double wsum = 0.0;
+        for (const auto& t : ts) wsum += 8.0 * t.nrows * t.ld + 64.0 * t.ld;
+        double acc = 0.0;
+        for (const auto& t : ts) {
+            const double w = 8.0 * t.nrows * t.ld + 64.0 * t.ld;
+            int q = static_cast<int>((acc + 0.5 * w) / wsum * grid);
+            q = std::min(std::max(q, 0), grid - 1);
+            per_cta[q].push_back(t);
+            acc += w;
+        }
+    };
+    auto base_task = [&](int k, int type) {
+        const NdFront& F = fronts[k];
+        NdTask t{};
+        t.type = type;
+        t.front = k;
+        t.s = F.s;
+        t.b = F.b;
+        t.sdof = F.sdof;
+        t.bdof = F.bdof;
+        t.uoff = F.uoff;
+        t.wait0 = t.wait1 = -1;
+        t.need0 = t.need1 = 0;
+        t.leaf = leaf[k] ? 1 : 0;
+        return t;
+    };
+    auto level_bytes = [&](int type, int depth) {
+        double by = 0.0;
+        for (const auto& F : fronts)
+            if (F.depth == depth) by += 8.0 * (type == 1 ? (double)(F.s + F.b) * F.ldm : (double)F.s * F.ldt);
+        return by;
+    };
+    auto matrix_tasks = [&](int type, int depth) {
+        std::vector<NdTask> ts;
+        for (int k = 0; k < nf; ++k) {
+            const NdFront& F = fronts[k];
+            if (F.depth != depth) continue;
+            const int rows = type == 1 ? F.s + F.b : F.s;
+            const int ld = type == 1 ? F.ldm : F.ldt;
+            const long long base = type == 1 ? F.moff : F.mtoff;
+            const int rpc = static_cast<int>(stage_bytes / (8u * ld));
+            // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks
+            const int want = static_cast<int>(std::ceil(level_bytes(type, depth) / grid / stage_bytes));
+            const int cap = std::min(kNdMaxTaskRows, rpc * std::max(1, std::min(task_chunks, want)));
+            for (int r0 = 0; r0 < rows; r0 += cap) {
+                NdTask t = base_task(k, type);
+                t.src = base + (long long)r0 * ld;
+                t.r0 = r0;
+                t.nrows = std::min(cap, rows - r0);
+                t.ld = ld;
+                t.ncols = type == 1 ? F.s : F.s + F.b;
+                t.signal = 3 * k + type;
+                ts.push_back(t);
+                (type == 1 ? fwd_tasks : bwd_tasks)[k]++;
+            }
+        }
+        return ts;
+    };
+    std::vector<std::vector<NdTask>> fwd_by_depth(maxdepth + 1), bwd_by_depth(maxdepth + 1);
+    for (int d = maxdepth; d >= 0; --d) fwd_by_depth[d] = matrix_tasks(1, d);
+    for (int d = 0; d <= maxdepth; ++d) bwd_by_depth[d] = matrix_tasks(2, d);
+    // dependencies: forward after both children's forward, backward after the parent's backward
+    for (auto& v : fwd_by_depth)
+        for (auto& t : v) {
+            const auto& ch = children[t.front];
+            if (ch.size() > 0) {
+                t.wait0 = 3 * ch[0] + 1;
+                t.need0 = fwd_tasks[ch[0]];
+            }
+            if (ch.size() > 1) {
+                t.wait1 = 3 * ch[1] + 1;
+                t.need1 = fwd_tasks[ch[1]];
+            }
+        }
+    for (auto& v : bwd_by_depth)
+        for (auto& t : v) {
+            const int p = parent[t.front];
+            if (p >= 0) {
+                t.wait0 = 3 * p + 2;
+                t.need0 = bwd_tasks[p];
+            } else {
+                t.wait0 = 3 * t.front + 1;
+                t.need0 = fwd_tasks[t.front];
+            }
+        }
+    for (int d = maxdepth; d >= 0; --d) place(fwd_by_depth[d]);
+    for (int d = 0; d <= maxdepth; ++d) place(bwd_by_depth[d]);
+    std::vector<NdTask> all;
+    std::vector<int> hct(grid + 1, 0);
+    max_tasks = 0;
+    for (int q = 0; q < grid; ++q) {
+        all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
+        hct[q + 1] = static_cast<int>(all.size());
+        max_tasks = std::max(max_tasks, static_cast<int>(per_cta[q].size()));
+    }
+    const size_t fixed = 512 + (size_t)(vmax + kNdMaxTaskRows) * kNdMaxRhs * sizeof(double);
+    stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed) / stage_bytes));
+    require(stages >= 2, "nested dissection: ring does not fit in shared memory");
+    smem = fixed + (size_t)stages * stage_bytes;
+    require(smem <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
+    static size_t attr_smem = 0;  // one attribute for all instances: the largest
+    if (smem > attr_smem) {
+        PDG_CUDA(cudaFuncSetAttribute(k_nd_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr_smem = smem;
+    }
+    int per_sm = 0;
+    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdThreads + 32, smem));
+    require(per_sm >= 1 && grid <= per_sm * nsm, "nested dissection: solve grid not co-resident");
+    // boundary dofs as pivot positions
+    std::vector<int> hbp(hb.size());
+    for (size_t i = 0; i < hb.size(); ++i) hbp[i] = spos[hb[i]];
+    d_tasks.upload(all, st);
+    ctoff.upload(hct, st);
+    sdofs.upload(hs, st);
+    bpos.upload(hbp, st);
+    cmap.upload(hcm, st);
+    bmap.upload(hbm, st);
+    nbtot = nbt;
+    counters.alloc((size_t)3 * nf);
+    counters.zero(st);
+    call = 0;
+    y.alloc((size_t)n * max_rhs);
+    xpos.alloc((size_t)n * max_rhs);
+    ubuf.alloc((size_t)std::max<long long>(utot, 1) * max_rhs);
+    PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
+    ProfScope prof(prof_phase, st, alg_bytes(nrhs));
+    require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
+    ++call;
+    NdArgs a{d_tasks.p, ctoff.p, sdofs.p, bpos.p, cmap.p,  bmap.p,  nbtot,   store.p, b,     ldb,
+             x,         ldx,     y.p,     xpos.p, ubuf.p,  counters.p, call, utot,   n,     nrhs,
+             stages,    vmax,    max_tasks, pf, stage_bytes, nullptr, nullptr};
+    const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
+    const long long ntask = static_cast<long long>(d_tasks.n);
+    DBuf<unsigned long long> dbg;
+    DBuf<unsigned long long> prof_ns;
+    if (debug) {
+        dbg.alloc((size_t)ntask * 2);
+        dbg.zero(st);
+        a.dbg = dbg.p;
+        prof_ns.alloc((size_t)grid * 4);
+        prof_ns.zero(st);
+        a.prof = prof_ns.p;
+    }
+    void* args[] = {&a};
+    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_nd_solve, grid, kNdThreads + 32, args, smem, st));
+    count_launch(1);
+    PDG_CHECK_LAUNCH();
+    if (debug) {  // per task kind and depth: earliest start, latest end (us from the first start)
+        const std::vector<unsigned long long> h = dbg.download(st);
+        const std::vector<NdTask> ts = d_tasks.download(st);
+        unsigned long long t00 = ~0ull, tend = 0;
+        for (long long i = 0; i < ntask; ++i) {
+            t00 = std::min(t00, h[2 * i]);
+            tend = std::max(tend, h[2 * i + 1]);
+        }
+        std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d total %.2f us\n", n,
+                     nfront, maxdepth, ntask, grid, max_tasks, (tend - t00) * 1e-3);
+        const std::vector<unsigned long long> pn = prof_ns.download(st);
+        double avg[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+        for (int q = 0; q < grid; ++q)
+            for (int k = 0; k < 4; ++k) {
+                avg[k] += pn[q * 4 + k] * 1e-3 / grid;
+                mx[k] = std::max(mx[k], pn[q * 4 + k] * 1e-3);
+            }
+        std::fprintf(stderr, "  per CTA (avg/max us): dep wait %.1f/%.1f  gather %.1f/%.1f  ring wait %.1f/%.1f  rest %.1f/%.1f\n",
+                     avg[0], mx[0], avg[1], mx[1], avg[2], mx[2], avg[3], mx[3]);
+        for (int type = 0; type < 3; ++type)
+            for (int d = maxdepth; d >= 0; --d) {
+                const int dd = type == 2 ? maxdepth - d : d;
+                unsigned long long s0 = ~0ull, e1 = 0, busy = 0;
+                int cntk = 0;
+                for (long long i = 0; i < ntask; ++i)
+                    if (ts[i].type == type && fronts[ts[i].front].depth == dd) {
+                        s0 = std::min(s0, h[2 * i]);
+                        e1 = std::max(e1, h[2 * i + 1]);
+                        busy += h[2 * i + 1] - h[2 * i];
+                        ++cntk;
+                    }
+                if (cntk)
+                    std::fprintf(stderr, "  %s depth %2d tasks %5d  start %8.2f end %8.2f  sum busy %9.2f us\n",
+                                 type == 0 ? "gather  " : type == 1 ? "forward " : "backward", dd, cntk,
+                                 (s0 - t00) * 1e-3, (e1 - t00) * 1e-3, busy * 1e-3);
+            }
+    }
+}
+
+}  // namespace pdg

@@ -1,0 +1,84 @@
+// Nested-dissection multifrontal Cholesky with a level-synchronous persistent
+// solve: the exact SPD inner solves of the fixed-stress preconditioner
+// (fixed_stress.hpp:109-139 applies DenseLu solves, dense.hpp:14-45, of A and of
+// the flow block) at O(n log n) factor storage instead of the block-tridiagonal
+// O(n w^2), and with O(log n) dependent phases per solve instead of O(ny).
+//
+// Ordering: geometric nested dissection of the node graph (a node = the dofs of
+// one cell or one face): a region is cut by the line of nodes at a coordinate
+// value near the median of its longer extent, provided removing that line
+// disconnects the two sides (checked on the graph). Each separator is one front
+// F with pivots S (its dofs) and boundary B (the ancestor dofs adjacent to the
+// region it separates).
+//
+// Factor (setup, cuSOLVER/cuBLAS on dense fronts, multifrontal extend-add):
+//   [L_SS; L_BS] of the front, update F_BB - L_BS L_BS^T to the parent;
+//   stored per front as  M  = [L_SS^{-1}; L_BS L_SS^{-1}]   ((s+b) x s, row-major)
+//                  and   M^T                               (s x (s+b), row-major).
+// Solve (one persistent cooperative kernel, a dataflow without grid barriers):
+//   forward   [y_S; u_F] = M (b_S - w_C1|S - w_C2|S)  once both children's forward
+//             tasks are done, with the update vector w_F = u_F + w_C1|B + w_C2|B
+//             (the children's updates passing through F to its ancestors);
+//   backward  x_S = M^T [y_S; -x_B]      once the parent's backward tasks are done.
+// Tasks are row chunks placed statically on the CTAs in a topological order;
+// each CTA streams the matrix rows of its tasks into a shared-memory ring by
+// cp.async.bulk (TMA) several tasks ahead of the dataflow, and completion
+// counters (monotone across calls) carry the dependencies. Sums are in a fixed
+// order (bit-identical repeats).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace pdg {
+
+struct NdFront {
+    int s, b;             // pivots, boundary dofs
+    int sdof, bdof;       // offsets into the S / B dof lists
+    int uoff, depth;      // contribution slots (b of them), tree depth
+    long long moff, mtoff;  // M and M^T in the store
+    int ldm, ldt;         // row strides (even)
+};
+
+// One unit of the solve dataflow: rows [r0, r0 + nrows) of M (forward) or M^T
+// (backward) at store + src (row stride ld) times the front's gathered input. A
+// task starts when the counters wait0 / wait1 reach call * need0 / need1 and
+// bumps counter `signal` when done.
+struct NdTask {
+    long long src;
+    int type;  // 1 forward, 2 backward
+    int front, r0, nrows, ld, ncols;
+    int s, b, sdof, bdof, uoff;
+    int wait0, wait1, need0, need1, signal;
+    int leaf;  // forward with no contributions: input read from b
+    int pad_;
+};
+
+struct NdChol {
+    int n = 0, max_rhs = 0, nfront = 0, maxdepth = 0;
+    int grid = 0, stages = 3, vmax = 0, max_tasks = 0, pf = 16;
+    unsigned stage_bytes = 24576;
+    unsigned long long call = 0;
+    size_t smem = 0;
+    int prof_phase = PROF_A_SOLVE;
+    double factor_bytes = 0.0;  // bytes of M and M^T read per solve
+    long long utot = 0;
+    DBuf<double> store, y, xpos, ubuf;  // y, xpos in pivot-position order; ubuf: update vectors
+    DBuf<int> sdofs, bpos, cmap, bmap, ctoff;  // bpos: pivot position of each boundary dof
+    long long nbtot = 0;
+    DBuf<unsigned long long> counters;          // [front][-, forward, backward] completed tasks
+    DBuf<NdTask> d_tasks;
+    std::vector<NdFront> fronts;
+
+    // SPD matrix in host CSR (full symmetric pattern, natural numbering);
+    // node_of[dof] groups dofs into graph nodes with coordinates (cx, cy).
+    void factor(int n, const std::vector<int>& off, const std::vector<int>& idx, const std::vector<double>& val,
+                const std::vector<int>& node_of, const std::vector<double>& cx, const std::vector<double>& cy,
+                int leaf_dofs, int max_rhs, cudaStream_t st);
+    // x = A^{-1} b, nrhs <= max_rhs columns at strides ldb / ldx
+    void solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+    double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
+};
+
+}  // namespace pdg

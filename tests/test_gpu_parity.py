@@ -525,3 +525,24 @@ def test_block_tridiagonal_lu_sweep(nb, m):
     assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
     x1 = solver.solve(torch.as_tensor(B[:, 0], device="cuda")).cpu().numpy()
     assert np.linalg.norm(x1 - ref[:, 0]) <= 1e-12 * np.linalg.norm(ref[:, 0])
+
+
+@pytest.mark.parametrize("solver", ["local", "general"])
+def test_nested_dissection_inner_solves_match_block_tridiagonal(monkeypatch, solver):
+    """The nested-dissection multifrontal inner solves (csrc/nd.cu, the default)
+    and the twisted block-tridiagonal ones (PDG_A_SOLVER=local|general,
+    PDG_FLOW_SOLVER=blocktri) are both exact: the preconditioner outputs agree to
+    roundoff, and ND repeats are bit-identical (fixed-order dataflow)."""
+    spec = P.config1(32)
+    ops = S.SpatialOperators.assemble(spec)
+    rng = np.random.default_rng(5)
+    theta = np.array([[1.7]])
+    blk = S.BlockSolver(ops, theta, 0.05)
+    r = rng.standard_normal(blk.rows)
+    z_nd = blk.precondition(r)
+    assert np.array_equal(z_nd, blk.precondition(r))
+    monkeypatch.setenv("PDG_A_SOLVER", solver)
+    monkeypatch.setenv("PDG_FLOW_SOLVER", "blocktri")
+    blk2 = S.BlockSolver(ops, theta, 0.05)
+    z_bt = blk2.precondition(r)
+    assert np.linalg.norm(z_nd - z_bt) <= 1e-11 * np.linalg.norm(z_bt)
