@@ -718,7 +718,11 @@ void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
     n = n_;
     restart = restart_;
     V.alloc((size_t)n * (restart + 1));
-    if (keep_z) Z.alloc((size_t)n * restart);
+    if (keep_z) {
+        Z.alloc((size_t)n * restart);
+        AZ.alloc((size_t)n * restart);
+        r0.alloc(n);
+    }
     w.alloc(n);
     x.alloc(n);
     r.alloc(n);
@@ -854,6 +858,9 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     hist.push_back(true_res);
     const int restart = opts.restart, max_iter = opts.max_iter;
     const bool flexible = opts.candidate == 1;
+    // flexible: the true residual of x + Z y is r0 - (A Z) y, from the op(z_j) products the
+    // Arnoldi step already formed (A linear): no second operator application per iteration
+    const bool arnoldi_res = flexible && !std::getenv("PDG_GMRES_EXPLICIT_RESIDUAL");
     std::vector<double> H;
     bool x_is_zero = true;
     while (total < max_iter) {
@@ -871,12 +878,19 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
         auto h = [&](int i, int j) -> double& { return H[(size_t)j * (mm + 1) + i]; };
         // v_0 = r / beta (beta recomputed on the device by the same fixed tree)
         K.norm_dev(kr.r.p, kr.V.p);
+        if (arnoldi_res) PDG_CUDA(cudaMemcpyAsync(kr.r0.p, kr.r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         bool done = false;
         for (int k = 0; k < mm && !done; ++k) {
             double* vk = kr.V.p + (size_t)k * n;
             double* zk = flexible ? kr.Z.p + (size_t)k * n : kr.cand.p;
             pre.apply(vk, zk, st);
-            op.apply(zk, kr.w.p, st);
+            if (arnoldi_res) {
+                double* azk = kr.AZ.p + (size_t)k * n;
+                op.apply(zk, azk, st);
+                PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            } else {
+                op.apply(zk, kr.w.p, st);
+            }
             // classical Gram-Schmidt, two passes, and the new norm, all on the device;
             // the Hessenberg column comes back in ONE transfer
             for (int pass = 0; pass < 2; ++pass) K.gs_pass(kr.V.p, k + 1, kr.w.p, kr.h_dev.p + (size_t)pass * (k + 1));
@@ -899,9 +913,11 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             e1[0] = beta;
             const std::vector<double> y = ls_colpiv(hk, k + 2, k + 1, e1);
             PDG_CUDA(cudaMemcpyAsync(kr.y_dev.p, y.data(), sizeof(double) * (k + 1), cudaMemcpyHostToDevice, st));
-            if (flexible) {  // cand = x + Z y
-                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
-                count_launch();
+            if (flexible) {  // cand = x + Z y (with the Arnoldi residual: formed when the cycle ends)
+                if (!arnoldi_res) {
+                    { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                    count_launch();
+                }
             } else {  // cand = x + P(V y)   (gmres.hpp:116)
                 { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.V.p, kr.y_dev.p, nullptr, kr.t.p); }
                 count_launch();
@@ -910,11 +926,21 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 count_launch();
             }
             // true residual (gmres.hpp:68-72)
-            op.apply(kr.cand.p, kr.t.p, st);
-            true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+            if (arnoldi_res) {
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.AZ.p, kr.y_dev.p, nullptr, kr.t.p); }
+                count_launch();
+                true_res = K.sub_norm(kr.r0.p, kr.t.p, kr.r.p);
+            } else {
+                op.apply(kr.cand.p, kr.t.p, st);
+                true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+            }
             hist.push_back(true_res);
             const bool ok = true_res / bnorm <= opts.tol;
             if (ok || breakdown || k == mm - 1 || total >= max_iter) {
+                if (arnoldi_res) {
+                    { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                    count_launch();
+                }
                 PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
                 x_is_zero = false;
                 done = true;

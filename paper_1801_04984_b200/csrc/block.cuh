@@ -59,6 +59,7 @@ struct Gmres {
     long long n = 0;
     int restart = 50;
     DBuf<double> V, Z, w, x, r, cand, t, y_dev, h_dev, partial, norm_dev;
+    DBuf<double> AZ, r0;  // flexible: op(z_j) and the cycle's initial residual (Arnoldi-relation residual)
     double* h_host = nullptr;  // pinned
     void setup(long long n, int restart, bool keep_z, cudaStream_t st);
     ~Gmres();
