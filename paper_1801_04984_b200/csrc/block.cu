@@ -934,18 +934,22 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 op.apply(kr.cand.p, kr.t.p, st);
                 true_res = K.sub_norm(b, kr.t.p, kr.r.p);
             }
-            hist.push_back(true_res);
-            const bool ok = true_res / bnorm <= opts.tol;
+            bool ok = true_res / bnorm <= opts.tol;
             if (ok || breakdown || k == mm - 1 || total >= max_iter) {
                 if (arnoldi_res) {
                     { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
                     count_launch();
+                    // the stop is decided on the explicit true residual, as gmres.hpp:68-72
+                    op.apply(kr.cand.p, kr.t.p, st);
+                    true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+                    ok = true_res / bnorm <= opts.tol;
                 }
                 PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
                 x_is_zero = false;
                 done = true;
                 converged = ok;
             }
+            hist.push_back(true_res);
         }
         if (converged) break;
     }
