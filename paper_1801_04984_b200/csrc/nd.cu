@@ -201,9 +201,7 @@ struct NdArgs {
     const int* ctoff;
     const int* sdofs;
     const int* bpos;
-    const int* cm;  // [2][n]: per pivot position, the children's update-vector entry (-1 none)
-    const int* bm;  // [2][nb]: per boundary entry, the children's update-vector entry (-1 none)
-    long long nbtot;
+    const int* cbdst;  // per boundary entry: its slot in the parent's contribution buffer
     const double* store;
     const double* b;
     long long ldb;
@@ -211,14 +209,15 @@ struct NdArgs {
     long long ldx;
     double* y;
     double* xpos;
-    double* u;
+    double* cb;
     unsigned long long* cnt;
     unsigned long long call;
-    long long utot;
+    long long cbtot;
     int n, nrhs, stages, vmax, max_tasks, pf;
     unsigned stage_bytes;
     unsigned long long* dbg;  // optional: per task, %globaltimer at start (after the wait) and end
-    unsigned long long* prof; // optional: per CTA, ns in [dependency wait, input gather, ring wait, rest] (warp 0)
+    unsigned long long* prof; // optional: per warp, ns in [pre-gather, dependency wait, gather, ring wait, compute, end sync]
+    int nodep;                // debug timing only (PDG_ND_NODEP): skip the dependency waits (wrong results)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -247,6 +246,20 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
 // named barrier of the compute warps (the producer warp never joins)
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdThreads) : "memory"); }
 
+// Profiling marks of the solve kernel (PDG_ND_DEBUG): per warp, ns in [pre-gather,
+// dependency wait, gather, ring wait, compute, end sync]
+struct NdProf {
+    unsigned long long acc[6] = {0, 0, 0, 0, 0, 0}, t = 0;
+    bool on = false;
+    __device__ void mark(int k) {
+        if (on) {
+            const unsigned long long now = dev::globaltimer();
+            acc[k] += now - t;
+            t = now;
+        }
+    }
+};
+
 // Warps 0-7 compute, warp 8 (one lane) streams the matrix chunks of this CTA's
 // tasks through the ring: full[k] completes on the TMA bytes, empty[k] when all
 // 8 compute warps are done with the slot.
@@ -258,6 +271,8 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
     unsigned char* ring = smem + 512;
     double* v = reinterpret_cast<double*>(ring + (size_t)a.stages * a.stage_bytes);
     double* wadd = v + (size_t)a.vmax * kNdMaxRhs;  // [rhs][kNdMaxTaskRows]
+    int* bix = reinterpret_cast<int*>(wadd + (size_t)kNdMaxTaskRows * kNdMaxRhs);  // [vmax] backward gather indices
+    int* oix = bix + a.vmax;                                     // [kNdMaxTaskRows] output indices of the task's rows
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t0 = a.ctoff[blockIdx.x], nt = a.ctoff[blockIdx.x + 1] - t0;
     if (tid == 0) {
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
                         T = a.tasks[t0 + i];
                         loaded = i;
                     }
-                    if (T.type != 0 && r < T.nrows) return true;
+                    if (r < T.nrows) return true;
                     ++i;
                     r = 0;
                 }
@@ -318,20 +333,33 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
     const int nr = a.nrhs;
     int seq = 0;  // chunks consumed
     int last_front = -1, last_type = -1;
-    NdTask T = nt > 0 ? a.tasks[t0] : NdTask{};
-    unsigned long long pacc[4] = {0, 0, 0, 0}, pt = a.prof ? globaltimer() : 0;
-    auto mark = [&](int k) {
-        if (a.prof) {
-            const unsigned long long now = globaltimer();
-            pacc[k] += now - pt;
-            pt = now;
+    NdProf pf;
+    pf.on = a.prof != nullptr;
+    if (pf.on) pf.t = globaltimer();
+    for (int i = 0; i < nt;) {
+        const NdTask T = a.tasks[t0 + i];
+        pf.mark(5);
+        const int len = T.ncols, lp = T.ld;
+        const bool fresh = T.front != last_front || T.type != last_type;  // v holds another front's input
+        // ---- input parts that do not depend on the wait (hidden behind it) ----
+        // output scatter indices of this task's rows (x positions / parent contribution slots)
+        for (int r = tid; r < T.nrows; r += kNdThreads) {
+            const int gr = T.r0 + r;
+            oix[r] = T.type == 2 ? a.sdofs[T.sdof + gr] : (gr >= T.s ? a.cbdst[T.bdof + gr - T.s] : 0);
         }
-    };
-    for (int i = 0; i < nt; ++i) {
-        const NdTask Tn = i + 1 < nt ? a.tasks[t0 + i + 1] : T;  // prefetch the next descriptor
-        mark(3);
+        if (fresh) {
+            if (T.type == 1) {  // b_S (and the padding)
+                for (int c = tid; c < lp * nr; c += kNdThreads) {
+                    const int k = c / lp, cc = c % lp;
+                    v[k * a.vmax + cc] = cc < len ? a.b[k * a.ldb + a.sdofs[T.sdof + cc]] : 0.0;
+                }
+            } else {
+                for (int j = tid; j < T.b; j += kNdThreads) bix[j] = a.bpos[T.bdof + j];
+            }
+        }
+        pf.mark(0);
         // ---- wait for the dependencies ----
-        if (tid == 0) {
+        if (tid == 0 && !a.nodep) {
             if (T.wait0 >= 0) {
                 const unsigned long long tgt = a.call * (unsigned long long)T.need0;
                 while (ld_acquire(a.cnt + T.wait0) < tgt) {
@@ -344,100 +372,164 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
             }
         }
         compute_sync();
-        mark(0);
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 2] = globaltimer();
-        {
-            const int len = T.ncols, lp = T.ld;
-            if (T.front != last_front || T.type != last_type) {
-                for (int c = tid; c < lp * nr; c += kNdThreads) {
-                    const int k = c / lp, cc = c % lp;
-                    double val = 0.0;
-                    if (cc < len) {
-                        if (T.type == 1) {
-                            // b_S minus the children's update vectors (multifrontal forward)
-                            const int pos = T.sdof + cc;
-                            const int m1 = a.cm[pos], m2 = a.cm[a.n + pos];
-                            val = a.b[k * a.ldb + a.sdofs[pos]];
-                            const double w1 = m1 >= 0 ? __ldcg(a.u + k * a.utot + m1) : 0.0;
-                            const double w2 = m2 >= 0 ? __ldcg(a.u + k * a.utot + m2) : 0.0;
-                            if (m1 >= 0) val -= w1;
-                            if (m2 >= 0) val -= w2;
-                        } else if (cc < T.s) {
-                            val = __ldcg(a.y + (long long)k * a.n + T.sdof + cc);
-                        } else {
-                            val = -__ldcg(a.xpos + (long long)k * a.n + a.bpos[T.bdof + cc - T.s]);
-                        }
+        pf.mark(1);
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4] = globaltimer();
+        // ---- dependent input: contiguous (forward) or smem-indexed (backward) loads,
+        // issued in batches of 4 per thread so one L2 round trip covers them ----
+        constexpr int kB = 4;
+        if (T.type == 1 && !T.leaf) {
+            const double* c0 = a.cb + T.cboff;
+            const double* c1 = c0 + (T.s + T.b);
+            if (fresh) {  // b_S minus both children's update vectors (multifrontal forward)
+                const int tot = len * nr;
+                for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
+                    double w1[kB], w2[kB];
+#pragma unroll
+                    for (int q = 0; q < kB; ++q) {
+                        const int c = cbase + q * kNdThreads, k = c / len, cc = c % len;
+                        w1[q] = c < tot ? __ldcg(c0 + k * a.cbtot + cc) : 0.0;
+                        w2[q] = c < tot ? __ldcg(c1 + k * a.cbtot + cc) : 0.0;
                     }
-                    v[k * a.vmax + cc] = val;
-                }
-                last_front = T.front;
-                last_type = T.type;
-            }
-            if (T.type == 1) {  // children's update-vector entries passing through this task's boundary rows
-                const int r_lo = max(T.r0, T.s), r_hi = T.r0 + T.nrows, cnt = max(0, r_hi - r_lo);
-                for (int c = tid; c < cnt * nr; c += kNdThreads) {
-                    const int k = c / cnt, j = r_lo + c % cnt - T.s;
-                    const int m1 = a.bm[T.bdof + j], m2 = a.bm[a.nbtot + T.bdof + j];
-                    const double w1 = m1 >= 0 ? __ldcg(a.u + k * a.utot + m1) : 0.0;
-                    const double w2 = m2 >= 0 ? __ldcg(a.u + k * a.utot + m2) : 0.0;
-                    wadd[k * kNdMaxTaskRows + (r_lo - T.r0) + c % cnt] = w1 + w2;
+#pragma unroll
+                    for (int q = 0; q < kB; ++q) {
+                        const int c = cbase + q * kNdThreads, k = c / len, cc = c % len;
+                        if (c < tot) v[k * a.vmax + cc] = v[k * a.vmax + cc] - w1[q] - w2[q];
+                    }
                 }
             }
-            compute_sync();
-            mark(1);
-            // chunk j of this CTA's stream is consumed by warp j % 8 alone: groups of 8
-            // rows, lanes over the columns, warp reduce-scatter (no CTA barrier per chunk)
+            // the children's updates passing through this task's boundary rows
+            const int r_lo = max(T.r0, T.s), r_hi = T.r0 + T.nrows, cnt = max(0, r_hi - r_lo), tot = cnt * nr;
+            for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
+                double w1[kB], w2[kB];
+#pragma unroll
+                for (int q = 0; q < kB; ++q) {
+                    const int c = cbase + q * kNdThreads, k = c / max(cnt, 1), r = r_lo + c % max(cnt, 1);
+                    w1[q] = c < tot ? __ldcg(c0 + k * a.cbtot + r) : 0.0;
+                    w2[q] = c < tot ? __ldcg(c1 + k * a.cbtot + r) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < kB; ++q) {
+                    const int c = cbase + q * kNdThreads;
+                    if (c < tot) wadd[(c / cnt) * kNdMaxTaskRows + (r_lo - T.r0) + c % cnt] = w1[q] + w2[q];
+                }
+            }
+        } else if (T.type == 2 && fresh) {  // [y_S; -x_B]
+            const int tot = lp * nr;
+            for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
+                double w[kB];
+#pragma unroll
+                for (int q = 0; q < kB; ++q) {
+                    const int c = cbase + q * kNdThreads, k = c / lp, cc = c % lp;
+                    w[q] = 0.0;
+                    if (c < tot && cc < len)
+                        w[q] = cc < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + cc)
+                                        : -__ldcg(a.xpos + (long long)k * a.n + bix[cc - T.s]);
+                }
+#pragma unroll
+                for (int q = 0; q < kB; ++q) {
+                    const int c = cbase + q * kNdThreads;
+                    if (c < tot) v[(c / lp) * a.vmax + c % lp] = w[q];
+                }
+            }
+        }
+        last_front = T.front;
+        last_type = T.type;
+        compute_sync();
+        pf.mark(2);
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 2] = globaltimer();
+        // chunk j of this CTA task's stream is consumed by warp j % 8 alone (no CTA
+        // barrier per chunk): two rows at a time share each input load, lanes over the
+        // columns, butterfly over the warp
+        {
             const int rpc = static_cast<int>(a.stage_bytes / (8u * T.ld));
             const int ld2 = T.ld >> 1;
+            const double2* va = reinterpret_cast<const double2*>(v);
+            const double2* vb = va + (a.vmax >> 1);
+            auto write_out = [&](int k, int lr, double tot) {  // row lr of the task, rhs k
+                const int gr = T.r0 + lr;
+                if (T.type == 2) {
+                    a.xpos[(long long)k * a.n + T.sdof + gr] = tot;
+                    a.x[k * a.ldx + oix[lr]] = tot;
+                } else if (gr < T.s) {
+                    a.y[(long long)k * a.n + T.sdof + gr] = tot;
+                } else {  // update vector entry, into the parent's contribution slot
+                    const double w = T.leaf ? 0.0 : wadd[k * kNdMaxTaskRows + lr];
+                    a.cb[k * a.cbtot + oix[lr]] = tot + w;
+                }
+            };
             for (int rc = 0; rc < T.nrows; rc += rpc, ++seq) {
                 if (seq % (kNdThreads / 32) != warp) continue;
                 const int slot = seq % a.stages;
-                mark(3);
+                pf.mark(4);
                 mbar_wait(&full[slot], static_cast<unsigned>((seq / a.stages) & 1));
-                mark(2);
+                pf.mark(3);
                 const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
                 const int nrow = min(rpc, T.nrows - rc);
-                for (int rb = 0; rb < nrow; rb += 8) {
-                    const int rn = min(8, nrow - rb);
-                    double acc[16];
+                if (rpc >= 8) {
+                    // narrow rows: groups of 8 rows share each input load, lanes over the
+                    // columns, warp reduce-scatter of the 16 (row, rhs) sums
+                    for (int rb = 0; rb < nrow; rb += 8) {
+                        const int rn = min(8, nrow - rb);
+                        double acc[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-                    for (int c2 = lane; c2 < ld2; c2 += 32) {
-                        const double v0x = v[2 * c2], v0y = v[2 * c2 + 1];
-                        const double v1x = v[a.vmax + 2 * c2], v1y = v[a.vmax + 2 * c2 + 1];
+                        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                        for (int c2 = lane; c2 < ld2; c2 += 32) {
+                            const double2 pv = va[c2], qv = vb[c2];
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
-                            acc[2 * r] = fma(m.y, v0y, fma(m.x, v0x, acc[2 * r]));
-                            acc[2 * r + 1] = fma(m.y, v1y, fma(m.x, v1x, acc[2 * r + 1]));
+                            for (int r = 0; r < 8; ++r) {
+                                const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                                acc[2 * r] = fma(m.y, pv.y, fma(m.x, pv.x, acc[2 * r]));
+                                acc[2 * r + 1] = fma(m.y, qv.y, fma(m.x, qv.x, acc[2 * r + 1]));
+                            }
                         }
+                        const double tot = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
+                        const int r = lane >> 1, k = lane & 1;
+                        if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, tot);
                     }
-                    const double tot = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
-                    const int r = lane >> 1, k = lane & 1;
-                    if (lane < 16 && r < rn && k < nr) {
-                        const int gr = T.r0 + rc + rb + r;
-                        if (T.type == 2) {
-                            a.xpos[(long long)k * a.n + T.sdof + gr] = tot;
-                            a.x[k * a.ldx + a.sdofs[T.sdof + gr]] = tot;
-                        } else if (gr < T.s) {
-                            a.y[(long long)k * a.n + T.sdof + gr] = tot;
-                        } else {
-                            a.u[k * a.utot + T.uoff + gr - T.s] = tot + wadd[k * kNdMaxTaskRows + gr - T.r0];
+                } else {
+                    // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
+                    // columns, butterfly over the warp
+                    for (int rb = 0; rb < nrow; rb += 2) {
+                        const bool two = rb + 1 < nrow;
+                        const double2* r0p = rows2 + (size_t)rb * ld2;
+                        const double2* r1p = two ? r0p + ld2 : r0p;
+                        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+                        for (int c2 = lane; c2 < ld2; c2 += 32) {
+                            const double2 pv = va[c2], qv = vb[c2], m0 = r0p[c2], m1 = r1p[c2];
+                            acc[0][0] = fma(m0.x, pv.x, acc[0][0]);
+                            acc[0][1] = fma(m0.y, pv.y, acc[0][1]);
+                            acc[0][2] = fma(m0.x, qv.x, acc[0][2]);
+                            acc[0][3] = fma(m0.y, qv.y, acc[0][3]);
+                            acc[1][0] = fma(m1.x, pv.x, acc[1][0]);
+                            acc[1][1] = fma(m1.y, pv.y, acc[1][1]);
+                            acc[1][2] = fma(m1.x, qv.x, acc[1][2]);
+                            acc[1][3] = fma(m1.y, qv.y, acc[1][3]);
                         }
+                        double t4[4] = {acc[0][0] + acc[0][1], acc[0][2] + acc[0][3], acc[1][0] + acc[1][1],
+                                        acc[1][2] + acc[1][3]};
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) t4[u] += __shfl_xor_sync(0xffffffffu, t4[u], o);
+                        // lane 2 r + k writes row rb + r, rhs k
+                        const int r = lane >> 1, k = lane & 1;
+                        if (lane < 4 && (r == 0 || two) && k < nr)
+                            write_out(k, rc + rb + r, lane == 0 ? t4[0] : lane == 1 ? t4[1] : lane == 2 ? t4[2] : t4[3]);
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
             }
         }
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 3] = globaltimer();  // warp 0's chunks done
         compute_sync();  // outputs written (and v free)
         if (tid == 0) red_release_add(a.cnt + T.signal, 1ull);
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 2 + 1] = globaltimer();
-        T = Tn;
+        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 1] = globaltimer();
+        ++i;
     }
-    mark(3);
-    if (a.prof && tid == 0)
-        for (int k = 0; k < 4; ++k) a.prof[blockIdx.x * 4 + k] = pacc[k];
+    pf.mark(5);
+    if (a.prof && lane == 0)
+        for (int k = 0; k < 6; ++k) a.prof[(blockIdx.x * (kNdThreads / 32) + warp) * 6 + k] = pf.acc[k];
 }
 
 long long round2(long long v) { return (v + 1) & ~1LL; }
@@ -526,16 +618,18 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         for (int c : h.children) children[k].push_back(newid[c]);
     }
     require(static_cast<int>(hs.size()) == n, "nested dissection: pivots do not cover the matrix");
-    // contribution slots and gather lists (contributors in front order)
-    utot = 0;
+    // contribution buffers: front F holds [child q][s + b] (per right-hand side); the
+    // update vector w_C of child q of F (its boundary rows: u_C plus the pass-through
+    // of C's own children) is written by C's forward tasks straight into F's slot q at
+    // F's local positions, so F's forward reads contiguous inputs after its wait
+    cbtot = 0;
     for (auto& F : fronts) {
-        F.uoff = static_cast<int>(utot);
-        utot += F.b;
+        F.cboff = static_cast<int>(cbtot);
+        cbtot += 2LL * (F.s + F.b);
     }
-    // multifrontal update vectors w_F (b_F entries at uoff): w_F = u_F + the children's
-    // w restricted to B_F; the forward input of F is b_S minus the children's w on S_F
+    require(cbtot < (1LL << 31), "nested dissection: contribution buffer too large");
     const long long nbt = static_cast<long long>(hb.size());
-    std::vector<int> hcm(2 * (size_t)n, -1), hbm(2 * (size_t)nbt, -1);
+    std::vector<int> hcbdst(std::max<long long>(nbt, 1), -1);
     {
         std::vector<int> lc(n, -1);
         for (int k = 0; k < nf; ++k) {
@@ -548,15 +642,13 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 for (int i = 0; i < C.b; ++i) {
                     const int l = lc[hb[C.bdof + i]];
                     require(l >= 0, "nested dissection: child boundary outside the parent front");
-                    if (l < F.s)
-                        hcm[q * (size_t)n + F.sdof + l] = C.uoff + i;
-                    else
-                        hbm[q * (size_t)nbt + F.bdof + l - F.s] = C.uoff + i;
+                    hcbdst[C.bdof + i] = F.cboff + static_cast<int>(q) * (F.s + F.b) + l;
                 }
             }
             for (int i = 0; i < F.s; ++i) lc[hs[F.sdof + i]] = -1;
             for (int i = 0; i < F.b; ++i) lc[hb[F.bdof + i]] = -1;
         }
+        for (long long i = 0; i < nbt; ++i) require(hcbdst[i] >= 0, "nested dissection: boundary entry without a parent slot");
     }
     // ---- storage layout ----
     long long so = 0;
@@ -720,7 +812,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         t.b = F.b;
         t.sdof = F.sdof;
         t.bdof = F.bdof;
-        t.uoff = F.uoff;
+        t.cboff = F.cboff;
         t.wait0 = t.wait1 = -1;
         t.need0 = t.need1 = 0;
         t.leaf = leaf[k] ? 1 : 0;
@@ -795,7 +887,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         hct[q + 1] = static_cast<int>(all.size());
         max_tasks = std::max(max_tasks, static_cast<int>(per_cta[q].size()));
     }
-    const size_t fixed = 512 + (size_t)(vmax + kNdMaxTaskRows) * kNdMaxRhs * sizeof(double);
+    const size_t fixed = 512 + (size_t)(vmax + kNdMaxTaskRows) * kNdMaxRhs * sizeof(double) +
+                         (size_t)(vmax + kNdMaxTaskRows) * sizeof(int);
     stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed) / stage_bytes));
     require(stages >= 2, "nested dissection: ring does not fit in shared memory");
     smem = fixed + (size_t)stages * stage_bytes;
@@ -815,15 +908,14 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     ctoff.upload(hct, st);
     sdofs.upload(hs, st);
     bpos.upload(hbp, st);
-    cmap.upload(hcm, st);
-    bmap.upload(hbm, st);
-    nbtot = nbt;
+    cbdst.upload(hcbdst, st);
     counters.alloc((size_t)3 * nf);
     counters.zero(st);
     call = 0;
     y.alloc((size_t)n * max_rhs);
     xpos.alloc((size_t)n * max_rhs);
-    ubuf.alloc((size_t)std::max<long long>(utot, 1) * max_rhs);
+    cbuf.alloc((size_t)std::max<long long>(cbtot, 1) * max_rhs);
+    cbuf.zero(st);  // slots no child writes stay zero
     PDG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -831,18 +923,18 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
     ++call;
-    NdArgs a{d_tasks.p, ctoff.p, sdofs.p, bpos.p, cmap.p,  bmap.p,  nbtot,   store.p, b,     ldb,
-             x,         ldx,     y.p,     xpos.p, ubuf.p,  counters.p, call, utot,   n,     nrhs,
-             stages,    vmax,    max_tasks, pf, stage_bytes, nullptr, nullptr};
+    NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
+             y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
+             max_tasks, pf,      stage_bytes, nullptr, nullptr, std::getenv("PDG_ND_NODEP") != nullptr};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;
     DBuf<unsigned long long> prof_ns;
     if (debug) {
-        dbg.alloc((size_t)ntask * 2);
+        dbg.alloc((size_t)ntask * 4);
         dbg.zero(st);
         a.dbg = dbg.p;
-        prof_ns.alloc((size_t)grid * 4);
+        prof_ns.alloc((size_t)grid * (kNdThreads / 32) * 6);
         prof_ns.zero(st);
         a.prof = prof_ns.p;
     }
@@ -855,36 +947,49 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
         const std::vector<NdTask> ts = d_tasks.download(st);
         unsigned long long t00 = ~0ull, tend = 0;
         for (long long i = 0; i < ntask; ++i) {
-            t00 = std::min(t00, h[2 * i]);
-            tend = std::max(tend, h[2 * i + 1]);
+            t00 = std::min(t00, h[4 * i]);
+            tend = std::max(tend, h[4 * i + 1]);
         }
         std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d total %.2f us\n", n,
                      nfront, maxdepth, ntask, grid, max_tasks, (tend - t00) * 1e-3);
         const std::vector<unsigned long long> pn = prof_ns.download(st);
-        double avg[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+        double avg[6] = {}, mx[6] = {}, avgw[6] = {};
+        const int nw = kNdThreads / 32;
         for (int q = 0; q < grid; ++q)
-            for (int k = 0; k < 4; ++k) {
-                avg[k] += pn[q * 4 + k] * 1e-3 / grid;
-                mx[k] = std::max(mx[k], pn[q * 4 + k] * 1e-3);
+            for (int k = 0; k < 6; ++k) {
+                avg[k] += pn[(q * nw) * 6 + k] * 1e-3 / grid;
+                mx[k] = std::max(mx[k], pn[(q * nw) * 6 + k] * 1e-3);
+                for (int w = 0; w < nw; ++w) avgw[k] += pn[(q * nw + w) * 6 + k] * 1e-3 / (grid * nw);
             }
-        std::fprintf(stderr, "  per CTA (avg/max us): dep wait %.1f/%.1f  gather %.1f/%.1f  ring wait %.1f/%.1f  rest %.1f/%.1f\n",
-                     avg[0], mx[0], avg[1], mx[1], avg[2], mx[2], avg[3], mx[3]);
+        std::fprintf(stderr,
+                     "  per CTA, warp 0 (avg/max us): pre-gather %.1f/%.1f  dep wait %.1f/%.1f  gather %.1f/%.1f  ring wait "
+                     "%.1f/%.1f  compute %.1f/%.1f  end sync %.1f/%.1f\n",
+                     avg[0], mx[0], avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], avg[4], mx[4], avg[5], mx[5]);
+        std::fprintf(stderr,
+                     "  per warp (avg us): pre-gather %.1f  dep wait %.1f  gather %.1f  ring wait %.1f  compute %.1f  end sync %.1f\n",
+                     avgw[0], avgw[1], avgw[2], avgw[3], avgw[4], avgw[5]);
         for (int type = 0; type < 3; ++type)
             for (int d = maxdepth; d >= 0; --d) {
                 const int dd = type == 2 ? maxdepth - d : d;
-                unsigned long long s0 = ~0ull, e1 = 0, busy = 0;
+                unsigned long long s0 = ~0ull, e1 = 0, busy = 0, gat = 0, w0 = 0;
+                double mb = 0.0;
                 int cntk = 0;
                 for (long long i = 0; i < ntask; ++i)
                     if (ts[i].type == type && fronts[ts[i].front].depth == dd) {
-                        s0 = std::min(s0, h[2 * i]);
-                        e1 = std::max(e1, h[2 * i + 1]);
-                        busy += h[2 * i + 1] - h[2 * i];
+                        s0 = std::min(s0, h[4 * i]);
+                        e1 = std::max(e1, h[4 * i + 1]);
+                        busy += h[4 * i + 1] - h[4 * i];
+                        gat += h[4 * i + 2] - h[4 * i];
+                        w0 += h[4 * i + 3] - h[4 * i + 2];
+                        mb += 8e-6 * ts[i].nrows * ts[i].ld;
                         ++cntk;
                     }
                 if (cntk)
-                    std::fprintf(stderr, "  %s depth %2d tasks %5d  start %8.2f end %8.2f  sum busy %9.2f us\n",
-                                 type == 0 ? "gather  " : type == 1 ? "forward " : "backward", dd, cntk,
-                                 (s0 - t00) * 1e-3, (e1 - t00) * 1e-3, busy * 1e-3);
+                    std::fprintf(stderr,
+                                 "  %s depth %2d tasks %5d  %7.2f MB  start %8.2f end %8.2f  per task: busy %6.2f gather %6.2f "
+                                 "warp0 chunks %6.2f us\n",
+                                 type == 0 ? "gather  " : type == 1 ? "forward " : "backward", dd, cntk, mb,
+                                 (s0 - t00) * 1e-3, (e1 - t00) * 1e-3, busy * 1e-3 / cntk, gat * 1e-3 / cntk, w0 * 1e-3 / cntk);
             }
     }
 }

@@ -36,7 +36,7 @@ namespace pdg {
 struct NdFront {
     int s, b;             // pivots, boundary dofs
     int sdof, bdof;       // offsets into the S / B dof lists
-    int uoff, depth;      // contribution slots (b of them), tree depth
+    int cboff, depth;     // contribution buffer (2 child slots of s + b), tree depth
     long long moff, mtoff;  // M and M^T in the store
     int ldm, ldt;         // row strides (even)
 };
@@ -49,9 +49,9 @@ struct NdTask {
     long long src;
     int type;  // 1 forward, 2 backward
     int front, r0, nrows, ld, ncols;
-    int s, b, sdof, bdof, uoff;
+    int s, b, sdof, bdof, cboff;
     int wait0, wait1, need0, need1, signal;
-    int leaf;  // forward with no contributions: input read from b
+    int leaf;  // no children: forward input is b_S alone, no pass-through updates
     int pad_;
 };
 
@@ -63,10 +63,11 @@ struct NdChol {
     size_t smem = 0;
     int prof_phase = PROF_A_SOLVE;
     double factor_bytes = 0.0;  // bytes of M and M^T read per solve
-    long long utot = 0;
-    DBuf<double> store, y, xpos, ubuf;  // y, xpos in pivot-position order; ubuf: update vectors
-    DBuf<int> sdofs, bpos, cmap, bmap, ctoff;  // bpos: pivot position of each boundary dof
-    long long nbtot = 0;
+    long long cbtot = 0;
+    // y, xpos in pivot-position order; cbuf: per front, the two children's update vectors
+    // scattered to the front's local positions ([child][s + b], per right-hand side)
+    DBuf<double> store, y, xpos, cbuf;
+    DBuf<int> sdofs, bpos, cbdst, ctoff;  // bpos: pivot position of each boundary dof; cbdst: its slot in the parent's cbuf
     DBuf<unsigned long long> counters;          // [front][-, forward, backward] completed tasks
     DBuf<NdTask> d_tasks;
     std::vector<NdFront> fronts;

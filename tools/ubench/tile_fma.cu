@@ -1,6 +1,7 @@
 // Micro-benchmark: cycles for one warp to multiply an 8-row smem tile (w columns) by a
 // 2-column input (the nested-dissection solve's inner loop), 8 warps per CTA.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 template <int N>
 __device__ __forceinline__ double rs(double (&v)[N], int lane) {
@@ -50,8 +51,8 @@ __global__ void k(int iters, int w2, double* out, long long* cyc) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = keep;
     if (lane == 0) cyc[blockIdx.x * 8 + warp] = c1 - c0;
 }
-int main() {
-    int w2 = 96, iters = 1000;
+int main(int argc, char** argv) {
+    int w2 = argc > 1 ? atoi(argv[1]) : 96, iters = 1000;
     size_t smem = (1536 + 8 * 8 * w2) * sizeof(double2);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     double* out; long long* cyc;
