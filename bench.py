@@ -282,17 +282,17 @@ def main():
         for n in range(args.warmup):
             step(n)
         if keep_rhs:  # rhs of the timed slabs for the e2e leg, collected outside the timed region
-            snap = (u_prev.clone(), p_prev.clone())
+            snap0 = (u_prev.clone(), p_prev.clone())
             for n in range(args.warmup, args.warmup + args.steps):
                 step(n, keep=True)
-            u_prev.copy_(snap[0])
-            p_prev.copy_(snap[1])
+            u_prev.copy_(snap0[0])
+            p_prev.copy_(snap0[1])
+        snap = (u_prev.clone(), p_prev.clone())
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         iters = []
         launches0 = L.pdg_util_launch_count()
-        S.profile(enable=True, reset=True)
         with Clocks(local) as clk:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
@@ -301,11 +301,19 @@ def main():
                 iters.append(step(n).iterations)
             e1.record()
             torch.cuda.synchronize()
-        phases_raw = S.profile(enable=False)
         launches = L.pdg_util_launch_count() - launches0
         ms = e0.elapsed_time(e1) / args.steps
         if world > 1:
             torch.distributed.barrier()
+        # the same K slabs again with the per-phase event profiler on (outside the timed region:
+        # the event pairs add host work between launches)
+        u_prev.copy_(snap[0])
+        p_prev.copy_(snap[1])
+        S.profile(enable=True, reset=True)
+        for n in range(args.warmup, args.warmup + args.steps):
+            step(n)
+        torch.cuda.synchronize()
+        phases_raw = S.profile(enable=False)
         return dict(slab=slab, ms=ms, iters=iters, phases_raw=phases_raw, launches=launches, clocks=clk.summary(),
                     rhs_host=rhs_host)
 
@@ -322,11 +330,17 @@ def main():
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(dom, {}).get("bytes")
+        traffic = tr.get(dom + ("_nd" if (dom == "a_solve" and nd_a) or (dom == "flow_solve" and nd_f) else ""),
+                         {}).get("bytes")
     except Exception:
         pass
-    kernel_of = {"a_solve": "a_solve: k_sweep<16> (displacement solve, one launch per call)",
-                 "flow_solve": "flow_solve: k_sweep_dense (one launch per call)", "spmv": "spmv: k_spmv"}
+    nd_a = os.environ.get("PDG_A_SOLVER", "nd") == "nd"
+    nd_f = os.environ.get("PDG_FLOW_SOLVER", "nd") == "nd" and "PDG_FLOW_STRIPS" not in os.environ
+    kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve (nested-dissection displacement solve" if nd_a else
+                                           "k_sweep<16> (twisted block-tridiagonal displacement solve")
+                 + ", one launch per call)",
+                 "flow_solve": "flow_solve: " + ("k_nd_solve" if nd_f else "k_sweep_dense") + " (one launch per call)",
+                 "spmv": "spmv: k_spmv"}
     roofline = {"bound": "hbm", "kernel": kernel_of.get(dom, dom), "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_kind": peak_kind, "traffic": traffic,
                 "share_of_step": phases[dom]["ms_per_step"] / ms_dev if ms_dev else None,
