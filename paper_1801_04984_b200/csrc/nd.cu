@@ -36,6 +36,10 @@ namespace {
 constexpr int kNdThreads = 256;
 constexpr int kNdMaxRhs = 2;
 constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector staging in shared memory)
+constexpr int kNdComputeWarps = kNdThreads / 32;
+constexpr int kNdPrepWarps = 2;  // input warps
+constexpr int kNdBufs = 3;       // task buffers (staging runs up to two tasks ahead)
+constexpr int kNdBlock = kNdThreads + 32 * (1 + kNdPrepWarps + 1);
 
 // ---------------------------------------------------------------------------
 // host: nested dissection
@@ -215,9 +219,9 @@ struct NdArgs {
     long long cbtot;
     int n, nrhs, stages, vmax, max_tasks, pf;
     unsigned stage_bytes;
-    unsigned long long* dbg;  // optional: per task, %globaltimer at start (after the wait) and end
-    unsigned long long* prof; // optional: per warp, ns in [pre-gather, dependency wait, gather, ring wait, compute, end sync]
+    unsigned long long* dbg;  // optional: per task, %globaltimer at [inputs ready, signalled, prep done, compute done]
     int nodep;                // debug timing only (PDG_ND_NODEP): skip the dependency waits (wrong results)
+    int nomath;               // debug timing only (PDG_ND_NOMATH): consume the matrix chunks without the products
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -243,47 +247,75 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
     }
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
-// named barrier of the compute warps (the producer warp never joins)
+
+// Shared-memory layout of the solve kernel: mbarriers + task descriptors, the TMA
+// ring, then kNdBufs task buffers, each [v: rhs x vmax doubles][oix:
+// kNdMaxTaskRows ints][bix: vmax ints]. v holds the task's input vector; for a
+// forward task the tail v[k][s ..] also carries the children's updates passing
+// through the task's boundary rows.
+constexpr unsigned kNdHeader = 2048;
+__host__ __device__ inline size_t nd_buf_bytes(int vmax) {
+    const size_t by = (size_t)vmax * kNdMaxRhs * sizeof(double) + (size_t)(kNdMaxTaskRows + vmax) * sizeof(int);
+    return (by + 127) / 128 * 128;
+}
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdThreads) : "memory"); }
+__host__ __device__ inline size_t nd_task_bytes(int max_tasks) { return ((size_t)max_tasks * sizeof(NdTask) + 127) / 128 * 128; }
 
-// Profiling marks of the solve kernel (PDG_ND_DEBUG): per warp, ns in [pre-gather,
-// dependency wait, gather, ring wait, compute, end sync]
-struct NdProf {
-    unsigned long long acc[6] = {0, 0, 0, 0, 0, 0}, t = 0;
-    bool on = false;
-    __device__ void mark(int k) {
-        if (on) {
-            const unsigned long long now = dev::globaltimer();
-            acc[k] += now - t;
-            t = now;
-        }
-    }
-};
-
-// Warps 0-7 compute, warp 8 (one lane) streams the matrix chunks of this CTA's
-// tasks through the ring: full[k] completes on the TMA bytes, empty[k] when all
-// 8 compute warps are done with the slot.
-__global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
+// Warp roles (one CTA per SM, a static task list per CTA in topological order):
+//   warps 0-7   compute: per task, the dependency wait and the dependent gather
+//               (children's update vectors, or y / x of the parent) into the task
+//               buffer, then chunk j of the CTA's matrix stream is consumed by warp
+//               j % 8 against that input; outputs to y / cb / x;
+//   warp 8      TMA producer (lane 0): matrix chunks into the ring, L2 prefetch ahead;
+//   warps 9-10  staging (even / odd tasks, independently): for the tasks ahead (up to
+//               kNdBufs - 1), the output indices, the boundary pivot positions and the
+//               right-hand side b_S - everything that does not depend on other tasks -
+//               plus a non-blocking look at the dependency counters;
+//   warp 11     signaller (lane 0): once the compute warps are done with a task,
+//               publishes its completion counter (release).
+// Buffer q cycles staged (staging -> compute), done (compute -> signaller) and free
+// (compute, once the next task's input is built, + signaller -> staging).
+__global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     using namespace dev;
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
-    unsigned long long* empty = full + 32;
-    unsigned char* ring = smem + 512;
-    double* v = reinterpret_cast<double*>(ring + (size_t)a.stages * a.stage_bytes);
-    double* wadd = v + (size_t)a.vmax * kNdMaxRhs;  // [rhs][kNdMaxTaskRows]
-    int* bix = reinterpret_cast<int*>(wadd + (size_t)kNdMaxTaskRows * kNdMaxRhs);  // [vmax] backward gather indices
-    int* oix = bix + a.vmax;                                     // [kNdMaxTaskRows] output indices of the task's rows
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);  // [32]
+    unsigned long long* empty = full + 32;                                   // [32]
+    unsigned long long* staged = empty + 32;                                 // [kNdBufs]
+    unsigned long long* done = staged + kNdBufs;                             // [kNdBufs]
+    unsigned long long* freeb = done + kNdBufs;                              // [kNdBufs]
+    NdTask* tbT = reinterpret_cast<NdTask*>(smem + 1024);                    // [kNdBufs]
+    int* tbOk = reinterpret_cast<int*>(smem + 1024 + kNdBufs * sizeof(NdTask));  // [kNdBufs] dependencies seen met
+    NdTask* tsk = reinterpret_cast<NdTask*>(smem + kNdHeader);  // this CTA's task descriptors
+    unsigned char* ring = smem + kNdHeader + nd_task_bytes(a.max_tasks);
+    unsigned char* bufs = ring + (size_t)a.stages * a.stage_bytes;
+    const size_t bb = nd_buf_bytes(a.vmax);
+    auto vbuf = [&](int q) { return reinterpret_cast<double*>(bufs + q * bb); };
+    auto oixbuf = [&](int q) { return reinterpret_cast<int*>(vbuf(q) + (size_t)a.vmax * kNdMaxRhs); };
+    auto bixbuf = [&](int q) { return oixbuf(q) + kNdMaxTaskRows; };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t0 = a.ctoff[blockIdx.x], nt = a.ctoff[blockIdx.x + 1] - t0;
+    const int nr = a.nrhs, vm = a.vmax;
     if (tid == 0) {
         for (int k = 0; k < a.stages; ++k) {
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], 1);
         }
+        for (int k = 0; k < kNdBufs; ++k) {
+            mbar_init(&staged[k], 1);
+            mbar_init(&done[k], kNdComputeWarps);
+            mbar_init(&freeb[k], 2);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    {
+        static_assert(sizeof(NdTask) % 4 == 0, "NdTask is copied as ints");
+        const int* src = reinterpret_cast<const int*>(a.tasks + t0);
+        int* dst = reinterpret_cast<int*>(tsk);
+        const int words = nt * static_cast<int>(sizeof(NdTask) / 4);
+        for (int w = tid; w < words; w += kNdBlock) dst[w] = src[w];
+    }
     __syncthreads();
-    if (warp == kNdThreads / 32) {  // producer
+    if (warp == kNdComputeWarps) {  // TMA producer
         if (lane == 0) {
             // two cursors over this CTA's matrix chunks: the ring fill, and an L2
             // prefetch running pf chunks ahead of it (keeps HBM busy through dependency waits)
@@ -293,7 +325,7 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
             auto next = [&](int& i, int& r, NdTask& T, int& loaded) -> bool {
                 while (i < nt) {
                     if (loaded != i) {
-                        T = a.tasks[t0 + i];
+                        T = tsk[i];
                         loaded = i;
                     }
                     if (r < T.nrows) return true;
@@ -330,36 +362,103 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
         }
         return;
     }
-    const int nr = a.nrhs;
-    int seq = 0;  // chunks consumed
-    int last_front = -1, last_type = -1;
-    NdProf pf;
-    pf.on = a.prof != nullptr;
-    if (pf.on) pf.t = globaltimer();
-    for (int i = 0; i < nt;) {
-        const NdTask T = a.tasks[t0 + i];
-        pf.mark(5);
-        const int len = T.ncols, lp = T.ld;
-        const bool fresh = T.front != last_front || T.type != last_type;  // v holds another front's input
-        // ---- input parts that do not depend on the wait (hidden behind it) ----
-        // output scatter indices of this task's rows (x positions / parent contribution slots)
-        for (int r = tid; r < T.nrows; r += kNdThreads) {
-            const int gr = T.r0 + r;
-            oix[r] = T.type == 2 ? a.sdofs[T.sdof + gr] : (gr >= T.s ? a.cbdst[T.bdof + gr - T.s] : 0);
-        }
-        if (fresh) {
-            if (T.type == 1) {  // b_S (and the padding)
-                for (int c = tid; c < lp * nr; c += kNdThreads) {
-                    const int k = c / lp, cc = c % lp;
-                    v[k * a.vmax + cc] = cc < len ? a.b[k * a.ldb + a.sdofs[T.sdof + cc]] : 0.0;
-                }
-            } else {
-                for (int j = tid; j < T.b; j += kNdThreads) bix[j] = a.bpos[T.bdof + j];
+    if (warp == kNdBlock / 32 - 1) {  // signaller
+        if (lane == 0)
+            for (int i = 0; i < nt; ++i) {
+                const int q = i % kNdBufs;
+                mbar_wait(&done[q], static_cast<unsigned>((i / kNdBufs) & 1));
+                if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 3] = globaltimer();
+                const int sig = tbT[q].signal;
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                red_release_add(a.cnt + sig, 1ull);
+                if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 1] = globaltimer();
+                mbar_arrive(&freeb[q]);
             }
+        return;
+    }
+    constexpr int kB = 8;  // loads in flight per thread
+    if (warp > kNdComputeWarps) {  // staging warps: warp 9 + w stages the tasks j = w mod kNdPrepWarps
+        const int w = warp - kNdComputeWarps - 1;
+        for (int j = w; j < nt; j += kNdPrepWarps) {
+            const int q = j % kNdBufs;
+            if (j >= kNdBufs) mbar_wait(&freeb[q], static_cast<unsigned>(((j / kNdBufs) - 1) & 1));
+            const NdTask& T = tsk[j];
+            const bool fresh = j == 0 || T.front != tsk[j - 1].front || T.type != tsk[j - 1].type;
+            double* v = vbuf(q);
+            int* oix = oixbuf(q);
+            int* bix = bixbuf(q);
+            const int len = T.ncols, lp = T.ld;
+            // output indices of the task's rows
+            for (int r0 = lane; r0 < T.nrows; r0 += 32 * kB) {
+                int o[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int r = r0 + u * 32, gr = T.r0 + r;
+                    o[u] = r >= T.nrows ? 0
+                                        : T.type == 2 ? a.sdofs[T.sdof + gr] : (gr >= T.s ? a.cbdst[T.bdof + gr - T.s] : 0);
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u)
+                    if (r0 + u * 32 < T.nrows) oix[r0 + u * 32] = o[u];
+            }
+            if (fresh && T.type == 1) {  // b_S (and the padding)
+                const int tot = lp * nr;
+                for (int c0 = lane; c0 < tot; c0 += 32 * kB) {
+                    int d[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = c0 + u * 32, cc = c % lp;
+                        d[u] = (c < tot && cc < len) ? a.sdofs[T.sdof + cc] : -1;
+                    }
+                    double x[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = c0 + u * 32, k = c / lp;
+                        x[u] = d[u] >= 0 ? a.b[k * a.ldb + d[u]] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = c0 + u * 32;
+                        if (c < tot) v[(c / lp) * vm + c % lp] = x[u];
+                    }
+                }
+            } else if (fresh) {  // backward: the boundary's pivot positions
+                for (int c = lane; c < T.b; c += 32) bix[c] = a.bpos[T.bdof + c];
+            }
+            // a look at the dependency counters, after the other loads are issued
+            // (monotone: once met, met for this call)
+            int ok = 1;
+            if (lane == 0) {
+                if (!a.nodep) {
+                    if (T.wait0 >= 0 && ld_acquire(a.cnt + T.wait0) < a.call * (unsigned long long)T.need0) ok = 0;
+                    if (T.wait1 >= 0 && ld_acquire(a.cnt + T.wait1) < a.call * (unsigned long long)T.need1) ok = 0;
+                }
+                tbT[q] = T;
+                tbOk[q] = ok | (fresh ? 2 : 0);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&staged[q]);
         }
-        pf.mark(0);
-        // ---- wait for the dependencies ----
-        if (tid == 0 && !a.nodep) {
+        return;
+    }
+    // ---- compute warps ----
+    int seq = 0;  // chunks of this CTA's stream consumed so far (by all compute warps)
+    for (int i = 0; i < nt; ++i) {
+        const int q = i % kNdBufs, qp = (i + kNdBufs - 1) % kNdBufs;
+        mbar_wait(&staged[q], static_cast<unsigned>((i / kNdBufs) & 1));
+        const NdTask T = tbT[q];
+        const int flags = tbOk[q];
+        const bool fresh = flags & 2;
+        double* v = vbuf(q);
+        const int* oix = oixbuf(q);
+        const int* bix = bixbuf(q);
+        const int len = T.ncols, lp = T.ld, tot = lp * nr;
+        if (!fresh) {  // continuation of the previous task's front: the same input
+            const double* vprev = vbuf(qp);
+            for (int c = tid; c < vm * nr; c += kNdThreads) v[c] = vprev[c];
+        }
+        // ---- the dependency wait ----
+        if (tid == 0 && !a.nodep && !(flags & 1)) {
             if (T.wait0 >= 0) {
                 const unsigned long long tgt = a.call * (unsigned long long)T.need0;
                 while (ld_acquire(a.cnt + T.wait0) < tgt) {
@@ -372,164 +471,151 @@ __global__ void __launch_bounds__(kNdThreads + 32, 1) k_nd_solve(NdArgs a) {
             }
         }
         compute_sync();
-        pf.mark(1);
         if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4] = globaltimer();
-        // ---- dependent input: contiguous (forward) or smem-indexed (backward) loads,
-        // issued in batches of 4 per thread so one L2 round trip covers them ----
-        constexpr int kB = 4;
+        // ---- dependent inputs, one batch of loads ----
         if (T.type == 1 && !T.leaf) {
-            const double* c0 = a.cb + T.cboff;
-            const double* c1 = c0 + (T.s + T.b);
-            if (fresh) {  // b_S minus both children's update vectors (multifrontal forward)
-                const int tot = len * nr;
-                for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
-                    double w1[kB], w2[kB];
-#pragma unroll
-                    for (int q = 0; q < kB; ++q) {
-                        const int c = cbase + q * kNdThreads, k = c / len, cc = c % len;
-                        w1[q] = c < tot ? __ldcg(c0 + k * a.cbtot + cc) : 0.0;
-                        w2[q] = c < tot ? __ldcg(c1 + k * a.cbtot + cc) : 0.0;
-                    }
-#pragma unroll
-                    for (int q = 0; q < kB; ++q) {
-                        const int c = cbase + q * kNdThreads, k = c / len, cc = c % len;
-                        if (c < tot) v[k * a.vmax + cc] = v[k * a.vmax + cc] - w1[q] - w2[q];
-                    }
-                }
-            }
-            // the children's updates passing through this task's boundary rows
-            const int r_lo = max(T.r0, T.s), r_hi = T.r0 + T.nrows, cnt = max(0, r_hi - r_lo), tot = cnt * nr;
-            for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
+            const double* c0p = a.cb + T.cboff;
+            const double* c1p = c0p + (T.s + T.b);
+            // fresh: v[k][cc] -= c0 + c1 for cc < len; every task: the pass-through updates
+            // c0 + c1 of its own boundary rows into the tail v[k][gr], gr in [max(r0, s), r0 + nrows)
+            const int nf = fresh ? len * nr : 0;
+            const int r_lo = max(T.r0, T.s), cnt = max(0, T.r0 + T.nrows - r_lo), tw = cnt * nr;
+            for (int cb0 = tid; cb0 < nf + tw; cb0 += kNdThreads * kB) {
                 double w1[kB], w2[kB];
+                int dst[kB];
 #pragma unroll
-                for (int q = 0; q < kB; ++q) {
-                    const int c = cbase + q * kNdThreads, k = c / max(cnt, 1), r = r_lo + c % max(cnt, 1);
-                    w1[q] = c < tot ? __ldcg(c0 + k * a.cbtot + r) : 0.0;
-                    w2[q] = c < tot ? __ldcg(c1 + k * a.cbtot + r) : 0.0;
+                for (int u = 0; u < kB; ++u) {
+                    const int c = cb0 + u * kNdThreads;
+                    int k = 0, col = 0;
+                    dst[u] = -1;
+                    if (c < nf) {
+                        k = c / len;
+                        col = c % len;
+                        dst[u] = k * vm + col;
+                    } else if (c < nf + tw) {
+                        const int e = c - nf;
+                        k = e / cnt;
+                        col = r_lo + e % cnt;
+                        dst[u] = k * vm + col;
+                    }
+                    w1[u] = dst[u] >= 0 ? __ldcg(c0p + k * a.cbtot + col) : 0.0;
+                    w2[u] = dst[u] >= 0 ? __ldcg(c1p + k * a.cbtot + col) : 0.0;
                 }
 #pragma unroll
-                for (int q = 0; q < kB; ++q) {
-                    const int c = cbase + q * kNdThreads;
-                    if (c < tot) wadd[(c / cnt) * kNdMaxTaskRows + (r_lo - T.r0) + c % cnt] = w1[q] + w2[q];
+                for (int u = 0; u < kB; ++u) {
+                    const int c = cb0 + u * kNdThreads;
+                    if (c < nf)
+                        v[dst[u]] = v[dst[u]] - w1[u] - w2[u];
+                    else if (c < nf + tw)
+                        v[dst[u]] = w1[u] + w2[u];
                 }
             }
         } else if (T.type == 2 && fresh) {  // [y_S; -x_B]
-            const int tot = lp * nr;
-            for (int cbase = tid; cbase < tot; cbase += kNdThreads * kB) {
+            for (int cb0 = tid; cb0 < tot; cb0 += kNdThreads * kB) {
                 double w[kB];
 #pragma unroll
-                for (int q = 0; q < kB; ++q) {
-                    const int c = cbase + q * kNdThreads, k = c / lp, cc = c % lp;
-                    w[q] = 0.0;
+                for (int u = 0; u < kB; ++u) {
+                    const int c = cb0 + u * kNdThreads, k = c / lp, cc = c % lp;
+                    w[u] = 0.0;
                     if (c < tot && cc < len)
-                        w[q] = cc < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + cc)
+                        w[u] = cc < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + cc)
                                         : -__ldcg(a.xpos + (long long)k * a.n + bix[cc - T.s]);
                 }
 #pragma unroll
-                for (int q = 0; q < kB; ++q) {
-                    const int c = cbase + q * kNdThreads;
-                    if (c < tot) v[(c / lp) * a.vmax + c % lp] = w[q];
+                for (int u = 0; u < kB; ++u) {
+                    const int c = cb0 + u * kNdThreads;
+                    if (c < tot) v[(c / lp) * vm + c % lp] = w[u];
                 }
             }
         }
-        last_front = T.front;
-        last_type = T.type;
         compute_sync();
-        pf.mark(2);
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 2] = globaltimer();
-        // chunk j of this CTA task's stream is consumed by warp j % 8 alone (no CTA
-        // barrier per chunk): two rows at a time share each input load, lanes over the
-        // columns, butterfly over the warp
-        {
-            const int rpc = static_cast<int>(a.stage_bytes / (8u * T.ld));
-            const int ld2 = T.ld >> 1;
-            const double2* va = reinterpret_cast<const double2*>(v);
-            const double2* vb = va + (a.vmax >> 1);
-            auto write_out = [&](int k, int lr, double tot) {  // row lr of the task, rhs k
-                const int gr = T.r0 + lr;
-                if (T.type == 2) {
-                    a.xpos[(long long)k * a.n + T.sdof + gr] = tot;
-                    a.x[k * a.ldx + oix[lr]] = tot;
-                } else if (gr < T.s) {
-                    a.y[(long long)k * a.n + T.sdof + gr] = tot;
-                } else {  // update vector entry, into the parent's contribution slot
-                    const double w = T.leaf ? 0.0 : wadd[k * kNdMaxTaskRows + lr];
-                    a.cb[k * a.cbtot + oix[lr]] = tot + w;
-                }
-            };
-            for (int rc = 0; rc < T.nrows; rc += rpc, ++seq) {
-                if (seq % (kNdThreads / 32) != warp) continue;
-                const int slot = seq % a.stages;
-                pf.mark(4);
-                mbar_wait(&full[slot], static_cast<unsigned>((seq / a.stages) & 1));
-                pf.mark(3);
-                const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
-                const int nrow = min(rpc, T.nrows - rc);
-                if (rpc >= 8) {
-                    // narrow rows: groups of 8 rows share each input load, lanes over the
-                    // columns, warp reduce-scatter of the 16 (row, rhs) sums
-                    for (int rb = 0; rb < nrow; rb += 8) {
-                        const int rn = min(8, nrow - rb);
-                        double acc[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-                        for (int c2 = lane; c2 < ld2; c2 += 32) {
-                            const double2 pv = va[c2], qv = vb[c2];
-#pragma unroll
-                            for (int r = 0; r < 8; ++r) {
-                                const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
-                                acc[2 * r] = fma(m.y, pv.y, fma(m.x, pv.x, acc[2 * r]));
-                                acc[2 * r + 1] = fma(m.y, qv.y, fma(m.x, qv.x, acc[2 * r + 1]));
-                            }
-                        }
-                        const double tot = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
-                        const int r = lane >> 1, k = lane & 1;
-                        if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, tot);
-                    }
-                } else {
-                    // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
-                    // columns, butterfly over the warp
-                    for (int rb = 0; rb < nrow; rb += 2) {
-                        const bool two = rb + 1 < nrow;
-                        const double2* r0p = rows2 + (size_t)rb * ld2;
-                        const double2* r1p = two ? r0p + ld2 : r0p;
-                        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-                        for (int c2 = lane; c2 < ld2; c2 += 32) {
-                            const double2 pv = va[c2], qv = vb[c2], m0 = r0p[c2], m1 = r1p[c2];
-                            acc[0][0] = fma(m0.x, pv.x, acc[0][0]);
-                            acc[0][1] = fma(m0.y, pv.y, acc[0][1]);
-                            acc[0][2] = fma(m0.x, qv.x, acc[0][2]);
-                            acc[0][3] = fma(m0.y, qv.y, acc[0][3]);
-                            acc[1][0] = fma(m1.x, pv.x, acc[1][0]);
-                            acc[1][1] = fma(m1.y, pv.y, acc[1][1]);
-                            acc[1][2] = fma(m1.x, qv.x, acc[1][2]);
-                            acc[1][3] = fma(m1.y, qv.y, acc[1][3]);
-                        }
-                        double t4[4] = {acc[0][0] + acc[0][1], acc[0][2] + acc[0][3], acc[1][0] + acc[1][1],
-                                        acc[1][2] + acc[1][3]};
-#pragma unroll
-                        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) t4[u] += __shfl_xor_sync(0xffffffffu, t4[u], o);
-                        // lane 2 r + k writes row rb + r, rhs k
-                        const int r = lane >> 1, k = lane & 1;
-                        if (lane < 4 && (r == 0 || two) && k < nr)
-                            write_out(k, rc + rb + r, lane == 0 ? t4[0] : lane == 1 ? t4[1] : lane == 2 ? t4[2] : t4[3]);
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-            }
+        if (tid == 0) {
+            if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 2] = globaltimer();
+            if (i > 0) mbar_arrive(&freeb[qp]);  // the previous task's buffer is no longer read
         }
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 3] = globaltimer();  // warp 0's chunks done
-        compute_sync();  // outputs written (and v free)
-        if (tid == 0) red_release_add(a.cnt + T.signal, 1ull);
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4 + 1] = globaltimer();
-        ++i;
+        // ---- the matrix stream ----
+        const int type = T.type, r0t = T.r0, nrows = T.nrows, ld = T.ld, s = T.s, sdof = T.sdof, leaf = T.leaf;
+        const int rpc = static_cast<int>(a.stage_bytes / (8u * ld));
+        const int ld2 = ld >> 1;
+        const double2* va = reinterpret_cast<const double2*>(v);
+        const double2* vb = va + (vm >> 1);
+        auto write_out = [&](int k, int lr, double t) {  // row lr of the task, rhs k
+            const int gr = r0t + lr;
+            if (type == 2) {
+                a.xpos[(long long)k * a.n + sdof + gr] = t;
+                a.x[k * a.ldx + oix[lr]] = t;
+            } else if (gr < s) {
+                a.y[(long long)k * a.n + sdof + gr] = t;
+            } else {  // update vector entry (+ the pass-through), into the parent's contribution slot
+                const double w = leaf ? 0.0 : v[k * vm + gr];
+                a.cb[k * a.cbtot + oix[lr]] = t + w;
+            }
+        };
+        for (int rc = 0; rc < nrows; rc += rpc, ++seq) {
+            if (seq % kNdComputeWarps != warp) continue;
+            const int slot = seq % a.stages;
+            mbar_wait(&full[slot], static_cast<unsigned>((seq / a.stages) & 1));
+            const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
+            const int nrow = min(rpc, nrows - rc);
+            if (a.nomath) {
+            } else if (rpc >= 8) {
+                // narrow rows: groups of 8 rows share each input load, lanes over the
+                // columns, warp reduce-scatter of the 16 (row, rhs) sums
+                for (int rb = 0; rb < nrow; rb += 8) {
+                    const int rn = min(8, nrow - rb);
+                    double acc[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                    for (int c2 = lane; c2 < ld2; c2 += 32) {
+                        const double2 pv = va[c2], qv = vb[c2];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                            acc[2 * r] = fma(m.y, pv.y, fma(m.x, pv.x, acc[2 * r]));
+                            acc[2 * r + 1] = fma(m.y, qv.y, fma(m.x, qv.x, acc[2 * r + 1]));
+                        }
+                    }
+                    const double t = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
+                    const int r = lane >> 1, k = lane & 1;
+                    if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, t);
+                }
+            } else {
+                // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
+                // columns, butterfly over the warp
+                for (int rb = 0; rb < nrow; rb += 2) {
+                    const bool two = rb + 1 < nrow;
+                    const double2* r0p = rows2 + (size_t)rb * ld2;
+                    const double2* r1p = two ? r0p + ld2 : r0p;
+                    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+                    for (int c2 = lane; c2 < ld2; c2 += 32) {
+                        const double2 pv = va[c2], qv = vb[c2], m0 = r0p[c2], m1 = r1p[c2];
+                        acc[0][0] = fma(m0.x, pv.x, acc[0][0]);
+                        acc[0][1] = fma(m0.y, pv.y, acc[0][1]);
+                        acc[0][2] = fma(m0.x, qv.x, acc[0][2]);
+                        acc[0][3] = fma(m0.y, qv.y, acc[0][3]);
+                        acc[1][0] = fma(m1.x, pv.x, acc[1][0]);
+                        acc[1][1] = fma(m1.y, pv.y, acc[1][1]);
+                        acc[1][2] = fma(m1.x, qv.x, acc[1][2]);
+                        acc[1][3] = fma(m1.y, qv.y, acc[1][3]);
+                    }
+                    double t4[4] = {acc[0][0] + acc[0][1], acc[0][2] + acc[0][3], acc[1][0] + acc[1][1],
+                                    acc[1][2] + acc[1][3]};
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) t4[u] += __shfl_xor_sync(0xffffffffu, t4[u], o);
+                    // lane 2 r + k writes row rb + r, rhs k
+                    const int r = lane >> 1, k = lane & 1;
+                    if (lane < 4 && (r == 0 || two) && k < nr)
+                        write_out(k, rc + rb + r, lane == 0 ? t4[0] : lane == 1 ? t4[1] : lane == 2 ? t4[2] : t4[3]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[q]);  // this warp's outputs of task i written
     }
-    pf.mark(5);
-    if (a.prof && lane == 0)
-        for (int k = 0; k < 6; ++k) a.prof[(blockIdx.x * (kNdThreads / 32) + warp) * 6 + k] = pf.acc[k];
 }
 
 long long round2(long long v) { return (v + 1) & ~1LL; }
@@ -887,8 +973,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         hct[q + 1] = static_cast<int>(all.size());
         max_tasks = std::max(max_tasks, static_cast<int>(per_cta[q].size()));
     }
-    const size_t fixed = 512 + (size_t)(vmax + kNdMaxTaskRows) * kNdMaxRhs * sizeof(double) +
-                         (size_t)(vmax + kNdMaxTaskRows) * sizeof(int);
+    static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
+    const size_t fixed = kNdHeader + nd_task_bytes(max_tasks) + (size_t)kNdBufs * nd_buf_bytes(vmax);
     stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed) / stage_bytes));
     require(stages >= 2, "nested dissection: ring does not fit in shared memory");
     smem = fixed + (size_t)stages * stage_bytes;
@@ -899,7 +985,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         attr_smem = smem;
     }
     int per_sm = 0;
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdThreads + 32, smem));
+    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdBlock, smem));
     require(per_sm >= 1 && grid <= per_sm * nsm, "nested dissection: solve grid not co-resident");
     // boundary dofs as pivot positions
     std::vector<int> hbp(hb.size());
@@ -925,21 +1011,18 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ++call;
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
-             max_tasks, pf,      stage_bytes, nullptr, nullptr, std::getenv("PDG_ND_NODEP") != nullptr};
+             max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
+             std::getenv("PDG_ND_NOMATH") != nullptr};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;
-    DBuf<unsigned long long> prof_ns;
     if (debug) {
         dbg.alloc((size_t)ntask * 4);
         dbg.zero(st);
         a.dbg = dbg.p;
-        prof_ns.alloc((size_t)grid * (kNdThreads / 32) * 6);
-        prof_ns.zero(st);
-        a.prof = prof_ns.p;
     }
     void* args[] = {&a};
-    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_nd_solve, grid, kNdThreads + 32, args, smem, st));
+    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_nd_solve, grid, kNdBlock, args, smem, st));
     count_launch(1);
     PDG_CHECK_LAUNCH();
     if (debug) {  // per task kind and depth: earliest start, latest end (us from the first start)
@@ -950,24 +1033,8 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
             t00 = std::min(t00, h[4 * i]);
             tend = std::max(tend, h[4 * i + 1]);
         }
-        std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d total %.2f us\n", n,
-                     nfront, maxdepth, ntask, grid, max_tasks, (tend - t00) * 1e-3);
-        const std::vector<unsigned long long> pn = prof_ns.download(st);
-        double avg[6] = {}, mx[6] = {}, avgw[6] = {};
-        const int nw = kNdThreads / 32;
-        for (int q = 0; q < grid; ++q)
-            for (int k = 0; k < 6; ++k) {
-                avg[k] += pn[(q * nw) * 6 + k] * 1e-3 / grid;
-                mx[k] = std::max(mx[k], pn[(q * nw) * 6 + k] * 1e-3);
-                for (int w = 0; w < nw; ++w) avgw[k] += pn[(q * nw + w) * 6 + k] * 1e-3 / (grid * nw);
-            }
-        std::fprintf(stderr,
-                     "  per CTA, warp 0 (avg/max us): pre-gather %.1f/%.1f  dep wait %.1f/%.1f  gather %.1f/%.1f  ring wait "
-                     "%.1f/%.1f  compute %.1f/%.1f  end sync %.1f/%.1f\n",
-                     avg[0], mx[0], avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], avg[4], mx[4], avg[5], mx[5]);
-        std::fprintf(stderr,
-                     "  per warp (avg us): pre-gather %.1f  dep wait %.1f  gather %.1f  ring wait %.1f  compute %.1f  end sync %.1f\n",
-                     avgw[0], avgw[1], avgw[2], avgw[3], avgw[4], avgw[5]);
+        std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d vmax=%d stages=%d x %u B total %.2f us\n", n,
+                     nfront, maxdepth, ntask, grid, max_tasks, vmax, stages, stage_bytes, (tend - t00) * 1e-3);
         for (int type = 0; type < 3; ++type)
             for (int d = maxdepth; d >= 0; --d) {
                 const int dd = type == 2 ? maxdepth - d : d;
@@ -986,8 +1053,8 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
                     }
                 if (cntk)
                     std::fprintf(stderr,
-                                 "  %s depth %2d tasks %5d  %7.2f MB  start %8.2f end %8.2f  per task: busy %6.2f gather %6.2f "
-                                 "warp0 chunks %6.2f us\n",
+                                 "  %s depth %2d tasks %5d  %7.2f MB  inputs ready %8.2f .. signalled %8.2f  per task: ready->signal %6.2f "
+                                 "gather %6.2f  compute %6.2f us\n",
                                  type == 0 ? "gather  " : type == 1 ? "forward " : "backward", dd, cntk, mb,
                                  (s0 - t00) * 1e-3, (e1 - t00) * 1e-3, busy * 1e-3 / cntk, gat * 1e-3 / cntk, w0 * 1e-3 / cntk);
             }
