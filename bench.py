@@ -327,6 +327,8 @@ def main():
               for k, v in main_run["phases_raw"].items()}
     dom = max(phases, key=lambda k: phases[k]["ms_per_step"])
     ach = phases[dom]["achieved_GBs"]
+    nd_a = os.environ.get("PDG_A_SOLVER", "nd") == "nd"
+    nd_f = os.environ.get("PDG_FLOW_SOLVER", "nd") == "nd" and "PDG_FLOW_STRIPS" not in os.environ
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -334,8 +336,6 @@ def main():
                          {}).get("bytes")
     except Exception:
         pass
-    nd_a = os.environ.get("PDG_A_SOLVER", "nd") == "nd"
-    nd_f = os.environ.get("PDG_FLOW_SOLVER", "nd") == "nd" and "PDG_FLOW_STRIPS" not in os.environ
     kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve (nested-dissection displacement solve" if nd_a else
                                            "k_sweep<16> (twisted block-tridiagonal displacement solve")
                  + ", one launch per call)",

@@ -1,5 +1,7 @@
 // Fixed-stress preconditioner, deterministic Krylov kernels and the GMRES
 // driver of one slab block.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -137,6 +139,134 @@ __global__ void k_combine(long long n, int ncols, const double* __restrict__ V, 
         double s = 0.0;
         for (int j = 0; j < ncols; ++j) s += V[(long long)j * n + r] * y[j];
         out[r] = base ? base[r] + s : s;
+    }
+}
+
+// ---- fused Arnoldi kernels (one cooperative launch each, grid = kRedBlocks) ----
+// Same arithmetic, in the same order, as the unfused launch sequences they
+// replace (k_multidot1 / k_red_multiaxpy / k_red_norm_scale / k_combine /
+// k_sub_dot): the grid-stride row order, the per-block partials and the fixed
+// partial-sum tree are unchanged, so results are bit-identical to them. The
+// grid barriers replace kernel boundaries.
+
+// block partials of V_j . w for j < ncols (the k_multidot1 body)
+__device__ __forceinline__ void block_multidot(long long n, int ncols, const double* __restrict__ V,
+                                               const double* w, double* __restrict__ partial) {
+    __shared__ double sh[8][kRedThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j0 = 0; j0 < ncols; j0 += 8) {
+        double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+            const double wr = __ldcg(w + r);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (j0 + q < ncols) a[q] += V[(long long)(j0 + q) * n + r] * wr;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sh[q][warp] = a[q];
+        __syncthreads();
+        if (threadIdx.x < 8 && j0 + threadIdx.x < ncols) {
+            double s = 0.0;
+            for (int i = 0; i < kRedThreads / 32; ++i) s += sh[threadIdx.x][i];
+            partial[(long long)blockIdx.x * ncols + j0 + threadIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// column sums of the partials into hs[ncols] (smem, every block), block 0 copies them to h_out
+__device__ __forceinline__ void block_column_sums(const double* partial, int ncols, double* hs, double* h_out) {
+    __shared__ double sh[32];
+    for (int j = 0; j < ncols; ++j) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(partial + (long long)b * ncols + j);
+        const double s = block_sum(v, sh);
+        if (threadIdx.x == 0) hs[j] = s;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && h_out)
+        for (int j = threadIdx.x; j < ncols; j += blockDim.x) h_out[j] = hs[j];
+}
+
+// Two classical Gram-Schmidt passes of w against V_0..V_{ncols-1}, then
+// h_out[2 ncols] = ||w|| and vnext = w / ||w||. h_out[0..ncols) pass 1, [ncols..2 ncols) pass 2.
+// partial: 3 regions of kRedBlocks * ncols (a region is never rewritten while another block may read it).
+__global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int ncols, const double* __restrict__ V,
+                                                            double* w, double* partial, double* h_out,
+                                                            double* __restrict__ vnext) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double hs[];  // [ncols]
+    double* p1 = partial;
+    double* p2 = partial + (size_t)kRedBlocks * ncols;
+    double* p3 = partial + (size_t)2 * kRedBlocks * ncols;
+    block_multidot(n, ncols, V, w, p1);
+    for (int pass = 0; pass < 2; ++pass) {
+        grid.sync();
+        block_column_sums(pass == 0 ? p1 : p2, ncols, hs, h_out + (size_t)pass * ncols);
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+            double v = __ldcg(w + r);
+            for (int j = 0; j < ncols; ++j) v -= hs[j] * V[(long long)j * n + r];
+            w[r] = v;
+        }
+        __syncthreads();
+        grid.sync();  // w complete before the next pass reads it
+        if (pass == 0)
+            block_multidot(n, ncols, V, w, p2);
+        else
+            block_multidot(n, 1, w, w, p3);
+    }
+    grid.sync();
+    {
+        __shared__ double sh[32];
+        __shared__ double nv;
+        double v = 0.0;
+        for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(p3 + b);
+        const double s = block_sum(v, sh);
+        if (threadIdx.x == 0) nv = sqrt(s);
+        __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0) h_out[2 * ncols] = nv;
+        const double d = nv;
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+            vnext[r] = __ldcg(w + r) / d;
+    }
+}
+
+// r = r0 - sum_j y_j AZ_j (sum from 0.0 in j order), ||r|| into nrm_out
+__global__ void __launch_bounds__(kRedThreads) k_arnoldi_residual(long long n, int ncols, const double* __restrict__ AZ,
+                                                                  const double* __restrict__ y,
+                                                                  const double* __restrict__ r0, double* r,
+                                                                  double* partial, double* nrm_out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < ncols; ++j) s += AZ[(long long)j * n + i] * y[j];
+        const double v = r0[i] - s;
+        r[i] = v;
+        acc += v * v;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sh[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < kRedThreads / 32; ++i) s += sh[i];
+        partial[blockIdx.x] = s;
+    }
+    grid.sync();
+    double v = 0.0;
+    if (blockIdx.x == 0) {
+        for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(partial + b);
+        const double s = block_sum(v, sh);
+        if (threadIdx.x == 0) *nrm_out = sqrt(s);
     }
 }
 
@@ -319,8 +449,8 @@ HCsr csr_download(const DCsr& a, cudaStream_t st) {
     return h;
 }
 
-int nd_leaf_dofs(int dflt) {
-    const char* e = std::getenv("PDG_ND_LEAF");
+int nd_leaf_dofs(int dflt, const char* var = "PDG_ND_LEAF") {
+    const char* e = std::getenv(var);
     return e ? std::max(1, std::atoi(e)) : dflt;
 }
 
@@ -526,7 +656,7 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
         }
         flow_use_nd = true;
         flow_nd.prof_phase = PROF_FLOW_SOLVE;
-        flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(64), m, st);
+        flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(128, "PDG_ND_FLOW_LEAF"), m, st);
         return;
     }
     std::vector<int> perm;
@@ -730,7 +860,7 @@ void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
     t.alloc(n);
     y_dev.alloc(restart + 2);
     h_dev.alloc(2 * (restart + 2));
-    partial.alloc((size_t)kRedBlocks * (restart + 2));
+    partial.alloc((size_t)3 * kRedBlocks * (restart + 2));  // three regions for the fused Arnoldi kernel
     norm_dev.alloc(4);
     if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (2 * restart + 8)));
     (void)st;
@@ -811,6 +941,31 @@ struct KrylovOps {
         norm_dev(v, nullptr);
         return fetch_norm();
     }
+    // both Gram-Schmidt passes + the norm + v_{k+1} = w / ||w|| in ONE cooperative launch
+    // (bit-identical to gs_pass x 2 + norm_dev); h_out[0 .. 2 ncols] as the unfused sequence
+    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext) {
+        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (3.0 * ncols + 6.0));
+        long long n = g.n;
+        double* part = g.partial.p;
+        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext};
+        PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_gs, kRedBlocks, kRedThreads, args, sizeof(double) * ncols, st));
+        count_launch();
+        PDG_CHECK_LAUNCH();
+    }
+    // r = r0 - AZ y and ||r|| (bit-identical to k_combine + sub_norm), on the host
+    double residual_fused(const double* AZ, int ncols, const double* y, const double* r0, double* r) {
+        {
+            ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 2.0));
+            long long n = g.n;
+            double* part = g.partial.p;
+            double* nrm = g.norm_dev.p;
+            void* args[] = {&n, &ncols, (void*)&AZ, (void*)&y, (void*)&r0, &r, &part, &nrm};
+            PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_residual, kRedBlocks, kRedThreads, args, 0, st));
+            count_launch();
+            PDG_CHECK_LAUNCH();
+        }
+        return fetch_norm();
+    }
     double fetch_norm() {
         PDG_CUDA(cudaMemcpyAsync(g.h_host, g.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         PDG_CUDA(cudaStreamSynchronize(st));
@@ -861,6 +1016,9 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     // flexible: the true residual of x + Z y is r0 - (A Z) y, from the op(z_j) products the
     // Arnoldi step already formed (A linear): no second operator application per iteration
     const bool arnoldi_res = flexible && !std::getenv("PDG_GMRES_EXPLICIT_RESIDUAL");
+    // fused cooperative Arnoldi kernels (default); PDG_KRYLOV_UNFUSED=1 selects the launch-per-step
+    // sequence they replace (bit-identical results, kept for the A/B test)
+    const bool fused = !std::getenv("PDG_KRYLOV_UNFUSED");
     std::vector<double> H;
     bool x_is_zero = true;
     while (total < max_iter) {
@@ -893,11 +1051,16 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             }
             // classical Gram-Schmidt, two passes, and the new norm, all on the device;
             // the Hessenberg column comes back in ONE transfer
-            for (int pass = 0; pass < 2; ++pass) K.gs_pass(kr.V.p, k + 1, kr.w.p, kr.h_dev.p + (size_t)pass * (k + 1));
             // h(k+1,k) = ||w|| and v_{k+1} = w / h(k+1,k) (unused when the column breaks down)
-            K.norm_dev(kr.w.p, kr.V.p + (size_t)(k + 1) * n);
-            PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * 2 * (k + 1), cudaMemcpyDeviceToHost, st));
-            PDG_CUDA(cudaMemcpyAsync(kr.h_host + 2 * (k + 1), kr.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (fused) {
+                K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n);
+                PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * (2 * (k + 1) + 1), cudaMemcpyDeviceToHost, st));
+            } else {
+                for (int pass = 0; pass < 2; ++pass) K.gs_pass(kr.V.p, k + 1, kr.w.p, kr.h_dev.p + (size_t)pass * (k + 1));
+                K.norm_dev(kr.w.p, kr.V.p + (size_t)(k + 1) * n);
+                PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * 2 * (k + 1), cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaMemcpyAsync(kr.h_host + 2 * (k + 1), kr.norm_dev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            }
             PDG_CUDA(cudaStreamSynchronize(st));
             for (int pass = 0; pass < 2; ++pass)
                 for (int i = 0; i <= k; ++i) h(i, k) += kr.h_host[(size_t)pass * (k + 1) + i];
@@ -926,7 +1089,9 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 count_launch();
             }
             // true residual (gmres.hpp:68-72)
-            if (arnoldi_res) {
+            if (arnoldi_res && fused) {
+                true_res = K.residual_fused(kr.AZ.p, k + 1, kr.y_dev.p, kr.r0.p, kr.r.p);
+            } else if (arnoldi_res) {
                 { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.AZ.p, kr.y_dev.p, nullptr, kr.t.p); }
                 count_launch();
                 true_res = K.sub_norm(kr.r0.p, kr.t.p, kr.r.p);

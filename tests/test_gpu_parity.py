@@ -548,3 +548,25 @@ def test_nested_dissection_inner_solves_match_block_tridiagonal(monkeypatch, sol
     # both exact; they differ by roundoff amplified by the conditioning of A and S_q
     # (lognormal permeability): ~2e-11 relative measured
     assert np.linalg.norm(z_nd - z_bt) <= 1e-9 * np.linalg.norm(z_bt)
+
+
+@pytest.mark.parametrize("candidate,restart", [("flexible", 50), ("reference", 50), ("flexible", 2)])
+def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
+    """The fused cooperative Arnoldi kernels (both Gram-Schmidt passes + norm +
+    normalisation in one launch; the Arnoldi-relation residual and its norm in
+    one launch) keep the row order, the per-block partials and the partial-sum
+    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1): solutions,
+    residual histories and iteration counts are bit-identical."""
+    spec = P.config1(16)
+    ops = S.SpatialOperators.assemble(spec)
+    t = S.time_constants(1)
+    rhs = np.random.default_rng(11).standard_normal(2 * ops.n_total)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=restart), candidate=candidate)
+    blk = S.BlockSolver(ops, t["T"], 0.05, opt=opt)
+    x_f, rep_f = blk.solve(rhs)
+    monkeypatch.setenv("PDG_KRYLOV_UNFUSED", "1")
+    x_u, rep_u = blk.solve(rhs)
+    assert rep_f.converged and rep_u.converged
+    assert rep_f.iterations == rep_u.iterations
+    assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
+    assert np.array_equal(x_f, x_u)
