@@ -39,7 +39,13 @@ constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector sta
 constexpr int kNdComputeWarps = kNdThreads / 32;
 constexpr int kNdPrepWarps = 2;  // input warps
 constexpr int kNdBufs = 3;       // task buffers (staging runs up to two tasks ahead)
-constexpr int kNdBlock = kNdThreads + 32 * (1 + kNdPrepWarps + 1);
+constexpr int kNdGatherWarps = 4;  // dependency wait + dependent gather, tasks in order
+constexpr int kNdGatherThreads = 32 * kNdGatherWarps;
+constexpr int kNdWarpProducer = kNdComputeWarps;
+constexpr int kNdWarpStage = kNdWarpProducer + 1;
+constexpr int kNdWarpGather = kNdWarpStage + kNdPrepWarps;
+constexpr int kNdWarpSignal = kNdWarpGather + kNdGatherWarps;
+constexpr int kNdBlock = 32 * (kNdWarpSignal + 1);
 
 // ---------------------------------------------------------------------------
 // host: nested dissection
@@ -258,23 +264,28 @@ __host__ __device__ inline size_t nd_buf_bytes(int vmax) {
     const size_t by = (size_t)vmax * kNdMaxRhs * sizeof(double) + (size_t)(kNdMaxTaskRows + vmax) * sizeof(int);
     return (by + 127) / 128 * 128;
 }
-__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdThreads) : "memory"); }
 __host__ __device__ inline size_t nd_task_bytes(int max_tasks) { return ((size_t)max_tasks * sizeof(NdTask) + 127) / 128 * 128; }
 
 // Warp roles (one CTA per SM, a static task list per CTA in topological order):
-//   warps 0-7   compute: per task, the dependency wait and the dependent gather
-//               (children's update vectors, or y / x of the parent) into the task
-//               buffer, then chunk j of the CTA's matrix stream is consumed by warp
-//               j % 8 against that input; outputs to y / cb / x;
+//   warps 0-7   compute: chunk j of the CTA's matrix stream is consumed by warp j % 8
+//               against the task's gathered input; outputs to y / cb / x. No CTA-wide
+//               barrier: a warp moves on to the next task as soon as its chunks are
+//               done and that task's input is gathered (no waiting for stragglers);
 //   warp 8      TMA producer (lane 0): matrix chunks into the ring, L2 prefetch ahead;
 //   warps 9-10  staging (even / odd tasks, independently): for the tasks ahead (up to
 //               kNdBufs - 1), the output indices, the boundary pivot positions and the
 //               right-hand side b_S - everything that does not depend on other tasks -
 //               plus a non-blocking look at the dependency counters;
-//   warp 11     signaller (lane 0): once the compute warps are done with a task,
+//   warps 11-14 gather (tasks in order): the dependency wait and the dependent gather
+//               (children's update vectors, or y / x of the parent) into the task
+//               buffer, while the compute warps still stream the previous tasks;
+//   warp 15     signaller (lane 0): once the compute warps are done with a task,
 //               publishes its completion counter (release).
-// Buffer q cycles staged (staging -> compute), done (compute -> signaller) and free
-// (compute, once the next task's input is built, + signaller -> staging).
+// Buffer q cycles staged (staging -> gather), gathered (gather -> compute), done
+// (compute -> signaller) and free (gather, once the next task's input is built, +
+// signaller -> staging).
+__device__ __forceinline__ void gather_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdGatherThreads) : "memory"); }
+
 __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     using namespace dev;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -283,6 +294,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     unsigned long long* staged = empty + 32;                                 // [kNdBufs]
     unsigned long long* done = staged + kNdBufs;                             // [kNdBufs]
     unsigned long long* freeb = done + kNdBufs;                              // [kNdBufs]
+    unsigned long long* gathered = freeb + kNdBufs;                          // [kNdBufs]
     NdTask* tbT = reinterpret_cast<NdTask*>(smem + 1024);                    // [kNdBufs]
     int* tbOk = reinterpret_cast<int*>(smem + 1024 + kNdBufs * sizeof(NdTask));  // [kNdBufs] dependencies seen met
     NdTask* tsk = reinterpret_cast<NdTask*>(smem + kNdHeader);  // this CTA's task descriptors
@@ -304,6 +316,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
             mbar_init(&staged[k], 1);
             mbar_init(&done[k], kNdComputeWarps);
             mbar_init(&freeb[k], 2);
+            mbar_init(&gathered[k], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -315,7 +328,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         for (int w = tid; w < words; w += kNdBlock) dst[w] = src[w];
     }
     __syncthreads();
-    if (warp == kNdComputeWarps) {  // TMA producer
+    if (warp == kNdWarpProducer) {  // TMA producer
         if (lane == 0) {
             // two cursors over this CTA's matrix chunks: the ring fill, and an L2
             // prefetch running pf chunks ahead of it (keeps HBM busy through dependency waits)
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         }
         return;
     }
-    if (warp == kNdBlock / 32 - 1) {  // signaller
+    if (warp == kNdWarpSignal) {  // signaller
         if (lane == 0)
             for (int i = 0; i < nt; ++i) {
                 const int q = i % kNdBufs;
@@ -377,8 +390,8 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         return;
     }
     constexpr int kB = 8;  // loads in flight per thread
-    if (warp > kNdComputeWarps) {  // staging warps: warp 9 + w stages the tasks j = w mod kNdPrepWarps
-        const int w = warp - kNdComputeWarps - 1;
+    if (warp >= kNdWarpStage && warp < kNdWarpStage + kNdPrepWarps) {  // staging warps: task j = w mod kNdPrepWarps
+        const int w = warp - kNdWarpStage;
         for (int j = w; j < nt; j += kNdPrepWarps) {
             const int q = j % kNdBufs;
             if (j >= kNdBufs) mbar_wait(&freeb[q], static_cast<unsigned>(((j / kNdBufs) - 1) & 1));
@@ -441,180 +454,199 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         }
         return;
     }
-    // ---- compute warps ----
+    if (warp >= kNdWarpGather && warp < kNdWarpGather + kNdGatherWarps) {  // gather warps, tasks in order
+        const int gt = tid - kNdWarpGather * 32;
+        for (int i = 0; i < nt; ++i) {
+            const int q = i % kNdBufs, qp = (i + kNdBufs - 1) % kNdBufs;
+            mbar_wait(&staged[q], static_cast<unsigned>((i / kNdBufs) & 1));
+            const NdTask T = tbT[q];
+            const int flags = tbOk[q];
+            const bool fresh = flags & 2;
+            double* v = vbuf(q);
+            const int* bix = bixbuf(q);
+            const int len = T.ncols, lp = T.ld, tot = lp * nr;
+            if (!fresh) {  // continuation of the previous task's front: the same input
+                const double* vprev = vbuf(qp);
+                for (int c = gt; c < vm * nr; c += kNdGatherThreads) v[c] = vprev[c];
+            }
+            // ---- the dependency wait ----
+            if (gt == 0 && !a.nodep && !(flags & 1)) {
+                if (T.wait0 >= 0) {
+                    const unsigned long long tgt = a.call * (unsigned long long)T.need0;
+                    while (ld_acquire(a.cnt + T.wait0) < tgt) {
+                    }
+                }
+                if (T.wait1 >= 0) {
+                    const unsigned long long tgt = a.call * (unsigned long long)T.need1;
+                    while (ld_acquire(a.cnt + T.wait1) < tgt) {
+                    }
+                }
+            }
+            gather_sync();
+            if (a.dbg && gt == 0) a.dbg[((size_t)(t0 + i)) * 4] = globaltimer();
+            // ---- dependent inputs, one batch of loads ----
+            if (T.type == 1 && !T.leaf) {
+                const double* c0p = a.cb + T.cboff;
+                const double* c1p = c0p + (T.s + T.b);
+                // fresh: v[k][cc] -= c0 + c1 for cc < len; every task: the pass-through updates
+                // c0 + c1 of its own boundary rows into the tail v[k][gr], gr in [max(r0, s), r0 + nrows)
+                const int nf = fresh ? len * nr : 0;
+                const int r_lo = max(T.r0, T.s), cnt = max(0, T.r0 + T.nrows - r_lo), tw = cnt * nr;
+                for (int cb0 = gt; cb0 < nf + tw; cb0 += kNdGatherThreads * kB) {
+                    double w1[kB], w2[kB];
+                    int dst[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = cb0 + u * kNdGatherThreads;
+                        int k = 0, col = 0;
+                        dst[u] = -1;
+                        if (c < nf) {
+                            k = c / len;
+                            col = c % len;
+                            dst[u] = k * vm + col;
+                        } else if (c < nf + tw) {
+                            const int e = c - nf;
+                            k = e / cnt;
+                            col = r_lo + e % cnt;
+                            dst[u] = k * vm + col;
+                        }
+                        w1[u] = dst[u] >= 0 ? __ldcg(c0p + k * a.cbtot + col) : 0.0;
+                        w2[u] = dst[u] >= 0 ? __ldcg(c1p + k * a.cbtot + col) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = cb0 + u * kNdGatherThreads;
+                        if (c < nf)
+                            v[dst[u]] = v[dst[u]] - w1[u] - w2[u];
+                        else if (c < nf + tw)
+                            v[dst[u]] = w1[u] + w2[u];
+                    }
+                }
+            } else if (T.type == 2 && fresh) {  // [y_S; -x_B]
+                for (int cb0 = gt; cb0 < tot; cb0 += kNdGatherThreads * kB) {
+                    double w[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = cb0 + u * kNdGatherThreads, k = c / lp, cc = c % lp;
+                        w[u] = 0.0;
+                        if (c < tot && cc < len)
+                            w[u] = cc < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + cc)
+                                            : -__ldcg(a.xpos + (long long)k * a.n + bix[cc - T.s]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int c = cb0 + u * kNdGatherThreads;
+                        if (c < tot) v[(c / lp) * vm + c % lp] = w[u];
+                    }
+                }
+            }
+            gather_sync();
+            if (gt == 0) {
+                if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 2] = globaltimer();
+                mbar_arrive(&gathered[q]);
+                if (i > 0) mbar_arrive(&freeb[qp]);  // the previous task's buffer is no longer read by the gather
+            }
+        }
+        return;
+    }
+    // ---- compute warps: the matrix stream ----
     int seq = 0;  // chunks of this CTA's stream consumed so far (by all compute warps)
     for (int i = 0; i < nt; ++i) {
-        const int q = i % kNdBufs, qp = (i + kNdBufs - 1) % kNdBufs;
-        mbar_wait(&staged[q], static_cast<unsigned>((i / kNdBufs) & 1));
-        const NdTask T = tbT[q];
-        const int flags = tbOk[q];
-        const bool fresh = flags & 2;
-        double* v = vbuf(q);
-        const int* oix = oixbuf(q);
-        const int* bix = bixbuf(q);
-        const int len = T.ncols, lp = T.ld, tot = lp * nr;
-        if (!fresh) {  // continuation of the previous task's front: the same input
-            const double* vprev = vbuf(qp);
-            for (int c = tid; c < vm * nr; c += kNdThreads) v[c] = vprev[c];
-        }
-        // ---- the dependency wait ----
-        if (tid == 0 && !a.nodep && !(flags & 1)) {
-            if (T.wait0 >= 0) {
-                const unsigned long long tgt = a.call * (unsigned long long)T.need0;
-                while (ld_acquire(a.cnt + T.wait0) < tgt) {
-                }
-            }
-            if (T.wait1 >= 0) {
-                const unsigned long long tgt = a.call * (unsigned long long)T.need1;
-                while (ld_acquire(a.cnt + T.wait1) < tgt) {
-                }
-            }
-        }
-        compute_sync();
-        if (a.dbg && tid == 0) a.dbg[((size_t)(t0 + i)) * 4] = globaltimer();
-        // ---- dependent inputs, one batch of loads ----
-        if (T.type == 1 && !T.leaf) {
-            const double* c0p = a.cb + T.cboff;
-            const double* c1p = c0p + (T.s + T.b);
-            // fresh: v[k][cc] -= c0 + c1 for cc < len; every task: the pass-through updates
-            // c0 + c1 of its own boundary rows into the tail v[k][gr], gr in [max(r0, s), r0 + nrows)
-            const int nf = fresh ? len * nr : 0;
-            const int r_lo = max(T.r0, T.s), cnt = max(0, T.r0 + T.nrows - r_lo), tw = cnt * nr;
-            for (int cb0 = tid; cb0 < nf + tw; cb0 += kNdThreads * kB) {
-                double w1[kB], w2[kB];
-                int dst[kB];
-#pragma unroll
-                for (int u = 0; u < kB; ++u) {
-                    const int c = cb0 + u * kNdThreads;
-                    int k = 0, col = 0;
-                    dst[u] = -1;
-                    if (c < nf) {
-                        k = c / len;
-                        col = c % len;
-                        dst[u] = k * vm + col;
-                    } else if (c < nf + tw) {
-                        const int e = c - nf;
-                        k = e / cnt;
-                        col = r_lo + e % cnt;
-                        dst[u] = k * vm + col;
-                    }
-                    w1[u] = dst[u] >= 0 ? __ldcg(c0p + k * a.cbtot + col) : 0.0;
-                    w2[u] = dst[u] >= 0 ? __ldcg(c1p + k * a.cbtot + col) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < kB; ++u) {
-                    const int c = cb0 + u * kNdThreads;
-                    if (c < nf)
-                        v[dst[u]] = v[dst[u]] - w1[u] - w2[u];
-                    else if (c < nf + tw)
-                        v[dst[u]] = w1[u] + w2[u];
-                }
-            }
-        } else if (T.type == 2 && fresh) {  // [y_S; -x_B]
-            for (int cb0 = tid; cb0 < tot; cb0 += kNdThreads * kB) {
-                double w[kB];
-#pragma unroll
-                for (int u = 0; u < kB; ++u) {
-                    const int c = cb0 + u * kNdThreads, k = c / lp, cc = c % lp;
-                    w[u] = 0.0;
-                    if (c < tot && cc < len)
-                        w[u] = cc < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + cc)
-                                        : -__ldcg(a.xpos + (long long)k * a.n + bix[cc - T.s]);
-                }
-#pragma unroll
-                for (int u = 0; u < kB; ++u) {
-                    const int c = cb0 + u * kNdThreads;
-                    if (c < tot) v[(c / lp) * vm + c % lp] = w[u];
-                }
-            }
-        }
-        compute_sync();
-        if (tid == 0) {
-            if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 2] = globaltimer();
-            if (i > 0) mbar_arrive(&freeb[qp]);  // the previous task's buffer is no longer read
-        }
-        // ---- the matrix stream ----
-        const int type = T.type, r0t = T.r0, nrows = T.nrows, ld = T.ld, s = T.s, sdof = T.sdof, leaf = T.leaf;
+        const int q = i % kNdBufs;
+        const NdTask& Ts = tsk[i];
+        const int type = Ts.type, r0t = Ts.r0, nrows = Ts.nrows, ld = Ts.ld, s = Ts.s, sdof = Ts.sdof, leaf = Ts.leaf;
         const int rpc = static_cast<int>(a.stage_bytes / (8u * ld));
-        const int ld2 = ld >> 1;
-        const double2* va = reinterpret_cast<const double2*>(v);
-        const double2* vb = va + (vm >> 1);
-        auto write_out = [&](int k, int lr, double t) {  // row lr of the task, rhs k
-            const int gr = r0t + lr;
-            if (type == 2) {
-                a.xpos[(long long)k * a.n + sdof + gr] = t;
-                a.x[k * a.ldx + oix[lr]] = t;
-            } else if (gr < s) {
-                a.y[(long long)k * a.n + sdof + gr] = t;
-            } else {  // update vector entry (+ the pass-through), into the parent's contribution slot
-                const double w = leaf ? 0.0 : v[k * vm + gr];
-                a.cb[k * a.cbtot + oix[lr]] = t + w;
-            }
-        };
-        for (int rc = 0; rc < nrows; rc += rpc, ++seq) {
-            if (seq % kNdComputeWarps != warp) continue;
-            const int slot = seq % a.stages;
-            mbar_wait(&full[slot], static_cast<unsigned>((seq / a.stages) & 1));
-            const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
-            const int nrow = min(rpc, nrows - rc);
-            if (a.nomath) {
-            } else if (rpc >= 8) {
-                // narrow rows: groups of 8 rows share each input load, lanes over the
-                // columns, warp reduce-scatter of the 16 (row, rhs) sums
-                for (int rb = 0; rb < nrow; rb += 8) {
-                    const int rn = min(8, nrow - rb);
-                    double acc[16];
+        const int nch = (nrows + rpc - 1) / rpc;
+        // chunks of this task owned by this warp: seq + c with (seq + c) % 8 == warp
+        const int first = (warp - seq % kNdComputeWarps + kNdComputeWarps) % kNdComputeWarps;
+        // every warp waits for every task's input, chunks or not: keeps the warps within one
+        // phase of the gathered / done barriers (a warp skipping tasks could otherwise run a
+        // full buffer cycle ahead and alias a barrier phase)
+        mbar_wait(&gathered[q], static_cast<unsigned>((i / kNdBufs) & 1));
+        if (first < nch) {
+            const double* v = vbuf(q);
+            const int* oix = oixbuf(q);
+            const double2* va = reinterpret_cast<const double2*>(v);
+            const double2* vb = va + (vm >> 1);
+            const int ld2 = ld >> 1;
+            auto write_out = [&](int k, int lr, double t) {  // row lr of the task, rhs k
+                const int gr = r0t + lr;
+                if (type == 2) {
+                    a.xpos[(long long)k * a.n + sdof + gr] = t;
+                    a.x[k * a.ldx + oix[lr]] = t;
+                } else if (gr < s) {
+                    a.y[(long long)k * a.n + sdof + gr] = t;
+                } else {  // update vector entry (+ the pass-through), into the parent's contribution slot
+                    const double w = leaf ? 0.0 : v[k * vm + gr];
+                    a.cb[k * a.cbtot + oix[lr]] = t + w;
+                }
+            };
+            for (int c = first; c < nch; c += kNdComputeWarps) {
+                const int sq = seq + c, rc = c * rpc;
+                const int slot = sq % a.stages;
+                mbar_wait(&full[slot], static_cast<unsigned>((sq / a.stages) & 1));
+                const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
+                const int nrow = min(rpc, nrows - rc);
+                if (a.nomath) {
+                } else if (rpc >= 8) {
+                    // narrow rows: groups of 8 rows share each input load, lanes over the
+                    // columns, warp reduce-scatter of the 16 (row, rhs) sums
+                    for (int rb = 0; rb < nrow; rb += 8) {
+                        const int rn = min(8, nrow - rb);
+                        double acc[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-                    for (int c2 = lane; c2 < ld2; c2 += 32) {
-                        const double2 pv = va[c2], qv = vb[c2];
+                        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                        for (int c2 = lane; c2 < ld2; c2 += 32) {
+                            const double2 pv = va[c2], qv = vb[c2];
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
-                            acc[2 * r] = fma(m.y, pv.y, fma(m.x, pv.x, acc[2 * r]));
-                            acc[2 * r + 1] = fma(m.y, qv.y, fma(m.x, qv.x, acc[2 * r + 1]));
+                            for (int r = 0; r < 8; ++r) {
+                                const double2 m = r < rn ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                                acc[2 * r] = fma(m.y, pv.y, fma(m.x, pv.x, acc[2 * r]));
+                                acc[2 * r + 1] = fma(m.y, qv.y, fma(m.x, qv.x, acc[2 * r + 1]));
+                            }
                         }
+                        const double t = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
+                        const int r = lane >> 1, k = lane & 1;
+                        if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, t);
                     }
-                    const double t = warp_reduce_scatter16(acc, lane);  // lane l < 16: row l/2, rhs l%2
-                    const int r = lane >> 1, k = lane & 1;
-                    if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, t);
-                }
-            } else {
-                // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
-                // columns, butterfly over the warp
-                for (int rb = 0; rb < nrow; rb += 2) {
-                    const bool two = rb + 1 < nrow;
-                    const double2* r0p = rows2 + (size_t)rb * ld2;
-                    const double2* r1p = two ? r0p + ld2 : r0p;
-                    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-                    for (int c2 = lane; c2 < ld2; c2 += 32) {
-                        const double2 pv = va[c2], qv = vb[c2], m0 = r0p[c2], m1 = r1p[c2];
-                        acc[0][0] = fma(m0.x, pv.x, acc[0][0]);
-                        acc[0][1] = fma(m0.y, pv.y, acc[0][1]);
-                        acc[0][2] = fma(m0.x, qv.x, acc[0][2]);
-                        acc[0][3] = fma(m0.y, qv.y, acc[0][3]);
-                        acc[1][0] = fma(m1.x, pv.x, acc[1][0]);
-                        acc[1][1] = fma(m1.y, pv.y, acc[1][1]);
-                        acc[1][2] = fma(m1.x, qv.x, acc[1][2]);
-                        acc[1][3] = fma(m1.y, qv.y, acc[1][3]);
+                } else {
+                    // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
+                    // columns, butterfly over the warp
+                    for (int rb = 0; rb < nrow; rb += 2) {
+                        const bool two = rb + 1 < nrow;
+                        const double2* r0p = rows2 + (size_t)rb * ld2;
+                        const double2* r1p = two ? r0p + ld2 : r0p;
+                        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+                        for (int c2 = lane; c2 < ld2; c2 += 32) {
+                            const double2 pv = va[c2], qv = vb[c2], m0 = r0p[c2], m1 = r1p[c2];
+                            acc[0][0] = fma(m0.x, pv.x, acc[0][0]);
+                            acc[0][1] = fma(m0.y, pv.y, acc[0][1]);
+                            acc[0][2] = fma(m0.x, qv.x, acc[0][2]);
+                            acc[0][3] = fma(m0.y, qv.y, acc[0][3]);
+                            acc[1][0] = fma(m1.x, pv.x, acc[1][0]);
+                            acc[1][1] = fma(m1.y, pv.y, acc[1][1]);
+                            acc[1][2] = fma(m1.x, qv.x, acc[1][2]);
+                            acc[1][3] = fma(m1.y, qv.y, acc[1][3]);
+                        }
+                        double t4[4] = {acc[0][0] + acc[0][1], acc[0][2] + acc[0][3], acc[1][0] + acc[1][1],
+                                        acc[1][2] + acc[1][3]};
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) t4[u] += __shfl_xor_sync(0xffffffffu, t4[u], o);
+                        // lane 2 r + k writes row rb + r, rhs k
+                        const int r = lane >> 1, k = lane & 1;
+                        if (lane < 4 && (r == 0 || two) && k < nr)
+                            write_out(k, rc + rb + r, lane == 0 ? t4[0] : lane == 1 ? t4[1] : lane == 2 ? t4[2] : t4[3]);
                     }
-                    double t4[4] = {acc[0][0] + acc[0][1], acc[0][2] + acc[0][3], acc[1][0] + acc[1][1],
-                                    acc[1][2] + acc[1][3]};
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) t4[u] += __shfl_xor_sync(0xffffffffu, t4[u], o);
-                    // lane 2 r + k writes row rb + r, rhs k
-                    const int r = lane >> 1, k = lane & 1;
-                    if (lane < 4 && (r == 0 || two) && k < nr)
-                        write_out(k, rc + rb + r, lane == 0 ? t4[0] : lane == 1 ? t4[1] : lane == 2 ? t4[2] : t4[3]);
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
         }
+        seq += nch;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&done[q]);  // this warp's outputs of task i written
+        if (lane == 0) mbar_arrive(&done[q]);  // this warp's outputs of task i written (or it had no chunk)
     }
 }
 
