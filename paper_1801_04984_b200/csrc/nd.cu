@@ -38,7 +38,7 @@ constexpr int kNdMaxRhs = 2;
 constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector staging in shared memory)
 constexpr int kNdComputeWarps = kNdThreads / 32;
 constexpr int kNdPrepWarps = 2;  // input warps
-constexpr int kNdBufs = 3;       // task buffers (staging runs up to two tasks ahead)
+constexpr int kNdBufs = 8;       // pipeline slots (barrier sets); task buffers live in a FIFO arena
 constexpr int kNdGatherWarps = 4;  // dependency wait + dependent gather, tasks in order
 constexpr int kNdGatherThreads = 32 * kNdGatherWarps;
 constexpr int kNdWarpProducer = kNdComputeWarps;
@@ -255,13 +255,17 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
 }
 
 // Shared-memory layout of the solve kernel: mbarriers + task descriptors, the TMA
-// ring, then kNdBufs task buffers, each [v: rhs x vmax doubles][oix:
-// kNdMaxTaskRows ints][bix: vmax ints]. v holds the task's input vector; for a
+// ring, then the buffer arena: per task (FIFO, offsets placed on the host so small
+// tasks pack densely and up to kNdBufs tasks are in flight) [v: rhs x vmt doubles]
+// [oix: nrows ints][bix: b ints (backward)]. v holds the task's input vector; for a
 // forward task the tail v[k][s ..] also carries the children's updates passing
 // through the task's boundary rows.
 constexpr unsigned kNdHeader = 2048;
-__host__ __device__ inline size_t nd_buf_bytes(int vmax) {
-    const size_t by = (size_t)vmax * kNdMaxRhs * sizeof(double) + (size_t)(kNdMaxTaskRows + vmax) * sizeof(int);
+long long round2(long long v) { return (v + 1) & ~1LL; }
+// v stride of a task: the row length, and for a non-leaf forward task at least s + b (pass-through tail)
+inline int nd_task_vmt(const NdTask& t) { return static_cast<int>(round2((t.type == 1 && !t.leaf) ? std::max(t.ld, t.s + t.b) : t.ld)); }
+inline size_t nd_task_buf_bytes(const NdTask& t) {
+    const size_t by = (size_t)t.vmt * kNdMaxRhs * sizeof(double) + (size_t)(t.nrows + (t.type == 2 ? t.b : 0)) * sizeof(int);
     return (by + 127) / 128 * 128;
 }
 __host__ __device__ inline size_t nd_task_bytes(int max_tasks) { return ((size_t)max_tasks * sizeof(NdTask) + 127) / 128 * 128; }
@@ -299,14 +303,13 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     int* tbOk = reinterpret_cast<int*>(smem + 1024 + kNdBufs * sizeof(NdTask));  // [kNdBufs] dependencies seen met
     NdTask* tsk = reinterpret_cast<NdTask*>(smem + kNdHeader);  // this CTA's task descriptors
     unsigned char* ring = smem + kNdHeader + nd_task_bytes(a.max_tasks);
-    unsigned char* bufs = ring + (size_t)a.stages * a.stage_bytes;
-    const size_t bb = nd_buf_bytes(a.vmax);
-    auto vbuf = [&](int q) { return reinterpret_cast<double*>(bufs + q * bb); };
-    auto oixbuf = [&](int q) { return reinterpret_cast<int*>(vbuf(q) + (size_t)a.vmax * kNdMaxRhs); };
-    auto bixbuf = [&](int q) { return oixbuf(q) + kNdMaxTaskRows; };
+    unsigned char* arena = ring + (size_t)a.stages * a.stage_bytes;
+    auto vbuf = [&](const NdTask& t) { return reinterpret_cast<double*>(arena + t.boff); };
+    auto oixbuf = [&](const NdTask& t) { return reinterpret_cast<int*>(vbuf(t) + (size_t)t.vmt * kNdMaxRhs); };
+    auto bixbuf = [&](const NdTask& t) { return oixbuf(t) + t.nrows; };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t0 = a.ctoff[blockIdx.x], nt = a.ctoff[blockIdx.x + 1] - t0;
-    const int nr = a.nrhs, vm = a.vmax;
+    const int nr = a.nrhs;
     if (tid == 0) {
         for (int k = 0; k < a.stages; ++k) {
             mbar_init(&full[k], 1);
@@ -394,12 +397,16 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         const int w = warp - kNdWarpStage;
         for (int j = w; j < nt; j += kNdPrepWarps) {
             const int q = j % kNdBufs;
-            if (j >= kNdBufs) mbar_wait(&freeb[q], static_cast<unsigned>(((j / kNdBufs) - 1) & 1));
             const NdTask& T = tsk[j];
+            // the slot's previous task and the arena space (both released in task order;
+            // fdep is monotone and <= j - 2, so this warp's waits never alias a barrier phase)
+            const int wt = max(j - kNdBufs, T.fdep);
+            if (wt >= 0) mbar_wait(&freeb[wt % kNdBufs], static_cast<unsigned>((wt / kNdBufs) & 1));
             const bool fresh = j == 0 || T.front != tsk[j - 1].front || T.type != tsk[j - 1].type;
-            double* v = vbuf(q);
-            int* oix = oixbuf(q);
-            int* bix = bixbuf(q);
+            double* v = vbuf(T);
+            int* oix = oixbuf(T);
+            int* bix = bixbuf(T);
+            const int vm = T.vmt;
             const int len = T.ncols, lp = T.ld;
             // output indices of the task's rows
             for (int r0 = lane; r0 < T.nrows; r0 += 32 * kB) {
@@ -462,11 +469,11 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
             const NdTask T = tbT[q];
             const int flags = tbOk[q];
             const bool fresh = flags & 2;
-            double* v = vbuf(q);
-            const int* bix = bixbuf(q);
-            const int len = T.ncols, lp = T.ld, tot = lp * nr;
-            if (!fresh) {  // continuation of the previous task's front: the same input
-                const double* vprev = vbuf(qp);
+            double* v = vbuf(T);
+            const int* bix = bixbuf(T);
+            const int len = T.ncols, lp = T.ld, tot = lp * nr, vm = T.vmt;
+            if (!fresh) {  // continuation of the previous task's front: the same input (same stride)
+                const double* vprev = vbuf(tsk[i - 1]);
                 for (int c = gt; c < vm * nr; c += kNdGatherThreads) v[c] = vprev[c];
             }
             // ---- the dependency wait ----
@@ -564,8 +571,9 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         // full buffer cycle ahead and alias a barrier phase)
         mbar_wait(&gathered[q], static_cast<unsigned>((i / kNdBufs) & 1));
         if (first < nch) {
-            const double* v = vbuf(q);
-            const int* oix = oixbuf(q);
+            const double* v = vbuf(Ts);
+            const int* oix = oixbuf(Ts);
+            const int vm = Ts.vmt;
             const double2* va = reinterpret_cast<const double2*>(v);
             const double2* vb = va + (vm >> 1);
             const int ld2 = ld >> 1;
@@ -649,8 +657,6 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         if (lane == 0) mbar_arrive(&done[q]);  // this warp's outputs of task i written (or it had no chunk)
     }
 }
-
-long long round2(long long v) { return (v + 1) & ~1LL; }
 
 }  // namespace
 
@@ -997,20 +1003,53 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         }
     for (int d = maxdepth; d >= 0; --d) place(fwd_by_depth[d]);
     for (int d = 0; d <= maxdepth; ++d) place(bwd_by_depth[d]);
+    max_tasks = 0;
+    size_t max_buf = 0;
+    for (auto& v : per_cta) {
+        max_tasks = std::max(max_tasks, static_cast<int>(v.size()));
+        for (auto& t : v) {
+            t.vmt = nd_task_vmt(t);
+            max_buf = std::max(max_buf, nd_task_buf_bytes(t));
+        }
+    }
+    static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
+    // shared memory: header, task list, TMA ring, and the buffer arena (at least three of the
+    // largest task buffers, so a task's buffer never waits on the previous task's)
+    const size_t fixed = kNdHeader + nd_task_bytes(max_tasks);
+    const size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
+    require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
+    stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
+    const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
+    smem = fixed + (size_t)stages * stage_bytes + arena;
+    // FIFO placement of the task buffers in the arena (tasks run and release in order)
+    for (auto& v : per_cta) {
+        size_t head = 0;
+        int prev_dep = -1;
+        for (int j = 0; j < static_cast<int>(v.size()); ++j) {
+            const size_t sz = nd_task_buf_bytes(v[j]);
+            if (head + sz > arena) head = 0;
+            v[j].boff = static_cast<int>(head);
+            int dep = -1;
+            for (int i = j - 1; i >= 0; --i)
+                if ((size_t)v[i].boff < head + sz && head < (size_t)v[i].boff + nd_task_buf_bytes(v[i])) {
+                    dep = i;
+                    break;
+                }
+            dep = std::max(dep, prev_dep);
+            require(dep < 0 || dep <= j - 2, "nested dissection: buffer arena too small (task " + std::to_string(j) + " dep " +
+                                      std::to_string(dep) + " head " + std::to_string(head) + " size " + std::to_string(sz) +
+                                      " arena " + std::to_string(arena) + " prev " + std::to_string(v[j - 1].boff) + "+" +
+                                      std::to_string(nd_task_buf_bytes(v[j - 1])) + ")");
+            v[j].fdep = prev_dep = dep;
+            head += sz;
+        }
+    }
     std::vector<NdTask> all;
     std::vector<int> hct(grid + 1, 0);
-    max_tasks = 0;
     for (int q = 0; q < grid; ++q) {
         all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
         hct[q + 1] = static_cast<int>(all.size());
-        max_tasks = std::max(max_tasks, static_cast<int>(per_cta[q].size()));
     }
-    static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
-    const size_t fixed = kNdHeader + nd_task_bytes(max_tasks) + (size_t)kNdBufs * nd_buf_bytes(vmax);
-    stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed) / stage_bytes));
-    require(stages >= 2, "nested dissection: ring does not fit in shared memory");
-    smem = fixed + (size_t)stages * stage_bytes;
-    require(smem <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
     static size_t attr_smem = 0;  // one attribute for all instances: the largest
     if (smem > attr_smem) {
         PDG_CUDA(cudaFuncSetAttribute(k_nd_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -52,6 +52,10 @@ struct NdTask {
     int s, b, sdof, bdof, cboff;
     int wait0, wait1, need0, need1, signal;
     int leaf;  // no children: forward input is b_S alone, no pass-through updates
+    // task buffer in the CTA's shared-memory arena (FIFO, placed on the host): byte offset,
+    // stride between the right-hand sides of v (doubles), and the newest earlier task of this
+    // CTA whose buffer must be released first (-1: none)
+    int boff, vmt, fdep;
     int pad_;
 };
 
