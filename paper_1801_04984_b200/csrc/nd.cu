@@ -592,6 +592,11 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
             for (int c = first; c < nch; c += kNdComputeWarps) {
                 const int sq = seq + c, rc = c * rpc;
                 const int slot = sq % a.stages;
+                // warps drift apart (no per-task barrier): before waiting for chunk sq to land, wait
+                // until the slot's previous chunk (sq - stages) has been consumed, so a parity wait
+                // can never see an older phase of the slot as this chunk's (needs stages >= 8: this
+                // warp's previous chunk landed, so sq - stages was issued, so sq - 2 stages was consumed)
+                if (sq >= a.stages) mbar_wait(&empty[slot], static_cast<unsigned>(((sq / a.stages) - 1) & 1));
                 mbar_wait(&full[slot], static_cast<unsigned>((sq / a.stages) & 1));
                 const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
                 const int nrow = min(rpc, nrows - rc);
@@ -903,7 +908,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     if (const char* e = std::getenv("PDG_ND_PF")) pf = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("PDG_ND_CHUNKS")) task_chunks = std::max(1, std::atoi(e));
     stages = 16;
-    stage_bytes = static_cast<unsigned>(std::max<long long>(12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
+    // 16 KB stages for wide fronts (rows of up to 8 KB: more rows per chunk), 12 KB otherwise
+    stage_bytes = static_cast<unsigned>(std::max<long long>(vmax >= 1024 ? 16384 : 12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
     if (const char* e = std::getenv("PDG_ND_STAGES")) stages = std::min(32, std::max(2, std::atoi(e)));
     if (const char* e = std::getenv("PDG_ND_STAGE_KB")) stage_bytes = 1024u * std::max(8, std::atoi(e));
     int ctas_per_sm = 1;
@@ -1019,6 +1025,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     const size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
     require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
     stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
+    require(stages >= kNdComputeWarps, "nested dissection: ring shallower than the compute warps (stage size too large)");
     const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
     smem = fixed + (size_t)stages * stage_bytes + arena;
     // FIFO placement of the task buffers in the arena (tasks run and release in order)
