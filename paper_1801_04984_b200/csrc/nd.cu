@@ -228,6 +228,7 @@ struct NdArgs {
     unsigned long long* dbg;  // optional: per task, %globaltimer at [inputs ready, signalled, prep done, compute done]
     int nodep;                // debug timing only (PDG_ND_NODEP): skip the dependency waits (wrong results)
     int nomath;               // debug timing only (PDG_ND_NOMATH): consume the matrix chunks without the products
+    int fence;                // PDG_ND_FENCE: explicit fence.acq_rel.gpu before each completion release
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -385,7 +386,10 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                 mbar_wait(&done[q], static_cast<unsigned>((i / kNdBufs) & 1));
                 if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 3] = globaltimer();
                 const int sig = tbT[q].signal;
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                // the compute warps' outputs reach this thread through the done barrier (release /
+                // acquire at CTA scope); the gpu-scope release below is cumulative over them.
+                // PDG_ND_FENCE (debug): an explicit fence.acq_rel.gpu first
+                if (a.fence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 red_release_add(a.cnt + sig, 1ull);
                 if (a.dbg) a.dbg[((size_t)(t0 + i)) * 4 + 1] = globaltimer();
                 mbar_arrive(&freeb[q]);
@@ -1090,7 +1094,7 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
-             std::getenv("PDG_ND_NOMATH") != nullptr};
+             std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;

@@ -319,11 +319,15 @@ class SlabSolver:
         self._h = h
         self.n = (r + 1) * ops.n_total
 
-    def solve(self, rhs):
-        """rhs: (r+1) * n_total stacked SlabSystem::rhs -> (r+1) * n_total state."""
+    def solve(self, rhs, out=None):
+        """rhs: (r+1) * n_total stacked SlabSystem::rhs -> (r+1) * n_total state
+        (written into `out` when given: a contiguous float64 host array, e.g. pinned)."""
         rhs = np.ascontiguousarray(rhs, np.float64)
         assert rhs.size == self.n
-        out = np.empty_like(rhs)
+        if out is None:
+            out = np.empty_like(rhs)
+        elif out.dtype != np.float64 or out.size != self.n or not out.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument(_lib.PDG_INVALID_ARGUMENT, "slab solve: out must be a contiguous float64 array of the slab size")
         rep, hist = _report(self.opt.gmres.max_iter + 2)
         check(lib().pdg_slab_solve(self._h, _dp(rhs), _dp(out), C.byref(rep)))
         return out, _to_report(rep, hist)
