@@ -10,6 +10,7 @@
 #include <string>
 
 #include "block.cuh"
+#include "gmres_ls.cuh"
 #include "timebasis.hpp"
 
 namespace pdg {
@@ -197,7 +198,8 @@ __device__ __forceinline__ void block_column_sums(const double* partial, int nco
 // partial: 3 regions of kRedBlocks * ncols (a region is never rewritten while another block may read it).
 __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int ncols, const double* __restrict__ V,
                                                             double* w, double* partial, double* h_out,
-                                                            double* __restrict__ vnext) {
+                                                            double* __restrict__ vnext, const GmresDevState* gst) {
+    if (gst && gst->stop) return;  // speculative step after the cycle ended
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double hs[];  // [ncols]
@@ -240,7 +242,11 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
 __global__ void __launch_bounds__(kRedThreads) k_arnoldi_residual(long long n, int ncols, const double* __restrict__ AZ,
                                                                   const double* __restrict__ y,
                                                                   const double* __restrict__ r0, double* r,
-                                                                  double* partial, double* nrm_out) {
+                                                                  double* partial, double* nrm_out, GmresDevState* gst,
+                                                                  double bnorm, double tol) {
+    // gst (device-driven steps): skipped once the cycle ended; sets the step's residual and
+    // the stop decision ok || breakdown (gmres.hpp:68-72, :103) for the next step's kernels
+    if (gst && gst->stop) return;
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
@@ -266,7 +272,14 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_residual(long long n, i
     if (blockIdx.x == 0) {
         for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(partial + b);
         const double s = block_sum(v, sh);
-        if (threadIdx.x == 0) *nrm_out = sqrt(s);
+        if (threadIdx.x == 0) {
+            const double res = sqrt(s);
+            *nrm_out = res;
+            if (gst) {
+                gst->res = res;
+                gst->stop = (res / bnorm <= tol) || gst->brk;
+            }
+        }
     }
 }
 
@@ -279,7 +292,8 @@ __global__ void k_add(long long n, const double* __restrict__ a, const double* _
 // fp_i = r_p_i [+ lambda (b E^T u_i - stab m_p p_i) for sweeps after the first]
 __global__ void k_flow_fp(int m, int np, int nt, int nu, int nq, int lag, double lambda, double b, double stab,
                           const double* __restrict__ r, const double* __restrict__ xold, const int* et_off,
-                          const int* et_idx, const double* et_val, const double* m_p, double* __restrict__ fp) {
+                          const int* et_idx, const double* et_val, const double* m_p, double* __restrict__ fp, const int* __restrict__ stop) {
+    if (stop && *stop) return;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
         double pr = r[(long long)i * nt + nu + nq + c];
@@ -294,7 +308,8 @@ __global__ void k_flow_fp(int m, int np, int nt, int nu, int nq, int lag, double
 // rq_i[f] = r_q_i[f] - sum_{B row f} (w bv) (dinv_c fp_c)
 __global__ void k_flow_rq(int m, int nq, int np, int nt, int nu, double w, const double* __restrict__ r,
                           const double* __restrict__ fp, const int* b_off, const int* b_idx, const double* b_val,
-                          const double* __restrict__ dinv, double* __restrict__ rq) {
+                          const double* __restrict__ dinv, double* __restrict__ rq, const int* __restrict__ stop) {
+    if (stop && *stop) return;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nq; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / nq), f = static_cast<int>(t % nq);
         double v = r[(long long)i * nt + nu + f];
@@ -308,7 +323,8 @@ __global__ void k_flow_rq(int m, int nq, int np, int nt, int nu, double w, const
 // p_i[c] = dinv_c (fp_c - w sum_{B^T row c} bv q_f)   (q already in z)
 __global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const double* __restrict__ fp,
                          const int* bt_off, const int* bt_idx, const double* bt_val, const double* __restrict__ dinv,
-                         double* __restrict__ z) {
+                         double* __restrict__ z, const int* __restrict__ stop) {
+    if (stop && *stop) return;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
         double btq = 0.0;
@@ -319,7 +335,8 @@ __global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const 
 // mech_i = r_u_i / w + b (E p_i)
 __global__ void k_mech_rhs(int m, int nu, int nt, int nq, double w, double b, const double* __restrict__ r,
                            const double* __restrict__ z, const int* e_off, const int* e_idx, const double* e_val,
-                           double* __restrict__ mech) {
+                           double* __restrict__ mech, const int* __restrict__ stop) {
+    if (stop && *stop) return;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nu; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / nu), k0 = static_cast<int>(t % nu);
         double ep = 0.0;
@@ -362,77 +379,9 @@ __global__ void k_dinv(int np, double coef, const double* m_p, double* dinv) {
 // min || beta e1 - H y ||, H (rows x cols) column-major; numerical rank as in
 // a column-pivoted QR with threshold eps * max column norm.
 std::vector<double> ls_colpiv(std::vector<double> a, int rows, int cols, std::vector<double> rhs) {
-    auto A = [&](int i, int j) -> double& { return a[(size_t)j * rows + i]; };
-    const int size = std::min(rows, cols);
-    std::vector<double> tau(size, 0.0), nrm(cols);
+    std::vector<double> tau(cols), nrm(cols), y(cols);
     std::vector<int> piv(cols);
-    for (int j = 0; j < cols; ++j) piv[j] = j;
-    double maxn = 0.0;
-    for (int j = 0; j < cols; ++j) {
-        double s = 0.0;
-        for (int i = 0; i < rows; ++i) s += A(i, j) * A(i, j);
-        nrm[j] = std::sqrt(s);
-        maxn = std::max(maxn, nrm[j]);
-    }
-    const double eps = std::numeric_limits<double>::epsilon();
-    const double thr = (maxn * eps) * (maxn * eps) / rows;
-    int rank = size;
-    for (int k = 0; k < size; ++k) {
-        // exact remaining column norms (rows k..)
-        int best = k;
-        double bestv = -1.0;
-        for (int j = k; j < cols; ++j) {
-            double s = 0.0;
-            for (int i = k; i < rows; ++i) s += A(i, j) * A(i, j);
-            nrm[j] = s;
-            if (s > bestv) {
-                bestv = s;
-                best = j;
-            }
-        }
-        if (rank == size && bestv < thr * (rows - k)) rank = k;
-        if (best != k) {
-            for (int i = 0; i < rows; ++i) std::swap(A(i, k), A(i, best));
-            std::swap(piv[k], piv[best]);
-        }
-        double tail = 0.0;
-        for (int i = k + 1; i < rows; ++i) tail += A(i, k) * A(i, k);
-        const double c0 = A(k, k);
-        double beta;
-        if (tail <= std::numeric_limits<double>::min()) {
-            tau[k] = 0.0;
-            beta = c0;
-            for (int i = k + 1; i < rows; ++i) A(i, k) = 0.0;
-        } else {
-            beta = std::sqrt(c0 * c0 + tail);
-            if (c0 >= 0.0) beta = -beta;
-            for (int i = k + 1; i < rows; ++i) A(i, k) /= (c0 - beta);
-            tau[k] = (beta - c0) / beta;
-        }
-        A(k, k) = beta;
-        if (tau[k] != 0.0)
-            for (int j = k + 1; j < cols; ++j) {
-                double t = A(k, j);
-                for (int i = k + 1; i < rows; ++i) t += A(i, k) * A(i, j);
-                A(k, j) -= tau[k] * t;
-                for (int i = k + 1; i < rows; ++i) A(i, j) -= tau[k] * A(i, k) * t;
-            }
-    }
-    std::vector<double> y(cols, 0.0);
-    if (rank == 0) return y;
-    for (int k = 0; k < rank; ++k) {
-        if (tau[k] == 0.0) continue;
-        double t = rhs[k];
-        for (int i = k + 1; i < rows; ++i) t += A(i, k) * rhs[i];
-        rhs[k] -= tau[k] * t;
-        for (int i = k + 1; i < rows; ++i) rhs[i] -= tau[k] * A(i, k) * t;
-    }
-    for (int i = rank - 1; i >= 0; --i) {
-        double s = rhs[i];
-        for (int j = i + 1; j < rank; ++j) s -= A(i, j) * rhs[j];
-        rhs[i] = s / A(i, i);
-    }
-    for (int i = 0; i < rank; ++i) y[piv[i]] = rhs[i];
+    ls_colpiv_raw(a.data(), rows, cols, rhs.data(), tau.data(), nrm.data(), piv.data(), y.data());
     return y;
 }
 
@@ -822,9 +771,9 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (2.0 * np + 2.0 * nq + 3.0 * o.B.nnz));
         k_flow_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, lag, lambda, o.biot_b, stab, r,
                                                                     xprev, o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.m_p.p,
-                                                                    fp.p);
+                                                                    fp.p, guard);
         k_flow_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, w, r, fp.p, o.B.off.p, o.B.idx.p,
-                                                                    o.B.val.p, dinv.p, rq.p);
+                                                                    o.B.val.p, dinv.p, rq.p, guard);
         count_launch(2);
         PDG_CHECK_LAUNCH();
     }
@@ -835,9 +784,9 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
     {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (3.0 * np + 2.0 * o.Bt.nnz + 2.0 * nu + 2.0 * o.E.nnz));
         k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fp.p, o.Bt.off.p, o.Bt.idx.p,
-                                                                   o.Bt.val.p, dinv.p, z);
+                                                                   o.Bt.val.p, dinv.p, z, guard);
         k_mech_rhs<<<grid_for((long long)m * nu, 256), 256, 0, st>>>(m, nu, nt, nq, w, o.biot_b, r, z, o.E.off.p,
-                                                                     o.E.idx.p, o.E.val.p, mech.p);
+                                                                     o.E.idx.p, o.E.val.p, mech.p, guard);
         count_launch(2);
         PDG_CHECK_LAUNCH();
     }
@@ -863,10 +812,25 @@ void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
     partial.alloc((size_t)3 * kRedBlocks * (restart + 2));  // three regions for the fused Arnoldi kernel
     norm_dev.alloc(4);
     if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (2 * restart + 8)));
+    if (keep_z) {
+        Hd.alloc((size_t)(restart + 1) * restart);
+        hk.alloc((size_t)(restart + 2) * (restart + 1));
+        ls_rhs.alloc(restart + 2);
+        ls_tau.alloc(restart + 1);
+        ls_nrm.alloc(restart + 1);
+        ls_piv.alloc(restart + 1);
+        gst.alloc(2);  // one GmresDevState
+        if (!h_slots) PDG_CUDA(cudaMallocHost(&h_slots, sizeof(GmresDevState) * (restart + 1)));
+        for (auto& e : evs)
+            if (!e) PDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     (void)st;
 }
 Gmres::~Gmres() {
     if (h_host) cudaFreeHost(h_host);
+    if (h_slots) cudaFreeHost(h_slots);
+    for (auto& e : evs)
+        if (e) cudaEventDestroy(e);
 }
 
 void Block::create(const SpatialOps& o, int m_, const double* th, double tau_, double lambda_, const pdg_gmres_opts& op_,
@@ -943,27 +907,29 @@ struct KrylovOps {
     }
     // both Gram-Schmidt passes + the norm + v_{k+1} = w / ||w|| in ONE cooperative launch
     // (bit-identical to gs_pass x 2 + norm_dev); h_out[0 .. 2 ncols] as the unfused sequence
-    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext) {
+    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext, const GmresDevState* gst = nullptr) {
         ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (3.0 * ncols + 6.0));
         long long n = g.n;
         double* part = g.partial.p;
-        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext};
+        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext, (void*)&gst};
         PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_gs, kRedBlocks, kRedThreads, args, sizeof(double) * ncols, st));
         count_launch();
         PDG_CHECK_LAUNCH();
     }
     // r = r0 - AZ y and ||r|| (bit-identical to k_combine + sub_norm), on the host
+    void residual_launch(const double* AZ, int ncols, const double* y, const double* r0, double* r,
+                         GmresDevState* gst = nullptr, double bnorm = 1.0, double tol = 0.0) {
+        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 2.0));
+        long long n = g.n;
+        double* part = g.partial.p;
+        double* nrm = g.norm_dev.p;
+        void* args[] = {&n, &ncols, (void*)&AZ, (void*)&y, (void*)&r0, &r, &part, &nrm, &gst, &bnorm, &tol};
+        PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_residual, kRedBlocks, kRedThreads, args, 0, st));
+        count_launch();
+        PDG_CHECK_LAUNCH();
+    }
     double residual_fused(const double* AZ, int ncols, const double* y, const double* r0, double* r) {
-        {
-            ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 2.0));
-            long long n = g.n;
-            double* part = g.partial.p;
-            double* nrm = g.norm_dev.p;
-            void* args[] = {&n, &ncols, (void*)&AZ, (void*)&y, (void*)&r0, &r, &part, &nrm};
-            PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_residual, kRedBlocks, kRedThreads, args, 0, st));
-            count_launch();
-            PDG_CHECK_LAUNCH();
-        }
+        residual_launch(AZ, ncols, y, r0, r);
         return fetch_norm();
     }
     double fetch_norm() {
@@ -1019,6 +985,16 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     // fused cooperative Arnoldi kernels (default); PDG_KRYLOV_UNFUSED=1 selects the launch-per-step
     // sequence they replace (bit-identical results, kept for the A/B test)
     const bool fused = !std::getenv("PDG_KRYLOV_UNFUSED");
+    // PDG_GMRES_DEVICE_LS=1: device-driven steps (with the fused Arnoldi-relation residual): the
+    // Hessenberg column, breakdown test and least squares run on the device (k_gmres_ls, same
+    // bits as the host), one host round trip per step instead of two. Opt-in: measured slower
+    // at config 1 (4 steps per cycle): the single-block least-squares kernel costs more than
+    // the host round trip it removes.
+    const bool pipelined = arnoldi_res && fused && std::getenv("PDG_GMRES_DEVICE_LS");
+    // PDG_GMRES_LOOKAHEAD=1: queue step k+1 before reading step k's stop flag (speculative
+    // steps exit at entry; measured slower at 4 steps per cycle: the skipped launches cost more
+    // than the host round trip they hide)
+    const bool lookahead = pipelined && std::getenv("PDG_GMRES_LOOKAHEAD") && std::atoi(std::getenv("PDG_GMRES_LOOKAHEAD")) > 0;
     std::vector<double> H;
     bool x_is_zero = true;
     while (total < max_iter) {
@@ -1037,6 +1013,71 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
         // v_0 = r / beta (beta recomputed on the device by the same fixed tree)
         K.norm_dev(kr.r.p, kr.V.p);
         if (arnoldi_res) PDG_CUDA(cudaMemcpyAsync(kr.r0.p, kr.r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        if (pipelined) {
+            GmresDevState* gst = reinterpret_cast<GmresDevState*>(kr.gst.p);
+            GmresDevState* slots = static_cast<GmresDevState*>(kr.h_slots);
+            PDG_CUDA(cudaMemsetAsync(kr.gst.p, 0, sizeof(GmresDevState), st));
+            PDG_CUDA(cudaMemsetAsync(kr.Hd.p, 0, sizeof(double) * (size_t)(mm + 1) * mm, st));
+            auto set_guard = [&](const int* g) {
+                op.guard = g;
+                pre.guard = g;
+                pre.flow_nd.guard = g;
+                if (pre.a) pre.a->nd.guard = g;
+            };
+            set_guard(&gst->stop);
+            auto step = [&](int k) {
+                double* vk = kr.V.p + (size_t)k * n;
+                double* zk = kr.Z.p + (size_t)k * n;
+                double* azk = kr.AZ.p + (size_t)k * n;
+                pre.apply(vk, zk, st);
+                op.apply(zk, azk, st);
+                PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst);
+                {
+                    ProfScope prof_(PROF_KRYLOV, st, 0.0);
+                    gmres_ls_launch(k, mm, beta, kr.h_dev.p, kr.Hd.p, kr.hk.p, kr.ls_rhs.p, kr.ls_tau.p, kr.ls_nrm.p,
+                                    kr.ls_piv.p, kr.y_dev.p, gst, st);
+                }
+                K.residual_launch(kr.AZ.p, k + 1, kr.y_dev.p, kr.r0.p, kr.r.p, gst, bnorm, opts.tol);
+                PDG_CUDA(cudaMemcpyAsync(slots + k, gst, sizeof(GmresDevState), cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaEventRecord(kr.evs[k & 1], st));
+            };
+            int kend = -1;
+            for (int k = 0; k < mm; ++k) {
+                step(k);  // queued behind step k - 1: skipped on the device if k - 1 ended the cycle
+                if (!lookahead) {  // one host round trip per step (the stop flag), no speculative step
+                    PDG_CUDA(cudaEventSynchronize(kr.evs[k & 1]));
+                    if (slots[k].stop) {
+                        kend = k;
+                        break;
+                    }
+                } else if (k >= 1) {
+                    PDG_CUDA(cudaEventSynchronize(kr.evs[(k - 1) & 1]));
+                    if (slots[k - 1].stop) {
+                        kend = k - 1;
+                        break;
+                    }
+                }
+            }
+            if (kend < 0) {
+                PDG_CUDA(cudaEventSynchronize(kr.evs[(mm - 1) & 1]));
+                kend = mm - 1;
+            }
+            set_guard(nullptr);
+            for (int k = 0; k < kend; ++k) hist.push_back(slots[k].res);
+            total += kend + 1;
+            // cand = x + Z y of the last step; the stop is decided on the explicit true residual
+            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, kend + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+            count_launch();
+            op.apply(kr.cand.p, kr.t.p, st);
+            true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+            PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            x_is_zero = false;
+            converged = true_res / bnorm <= opts.tol;
+            hist.push_back(true_res);
+            if (converged) break;
+            continue;
+        }
         bool done = false;
         for (int k = 0; k < mm && !done; ++k) {
             double* vk = kr.V.p + (size_t)k * n;

@@ -38,6 +38,7 @@ struct FixedStressPre {
     bool flow_use_nd = false;
     DBuf<double> dinv;  // 1 / (-(lambda (1/M + stab)) m_p)
     DBuf<double> rq, fp, mech, xold;
+    const int* guard = nullptr;  // skip the sweep's kernels once *guard != 0 (speculative GMRES steps)
     void setup(const SpatialOps& ops, int m, double tau, double lambda, double stab, int sweeps,
                std::shared_ptr<ASolver> a, cudaStream_t st);
     void apply(const double* r, double* z, cudaStream_t st);
@@ -61,6 +62,11 @@ struct Gmres {
     DBuf<double> V, Z, w, x, r, cand, t, y_dev, h_dev, partial, norm_dev;
     DBuf<double> AZ, r0;  // flexible: op(z_j) and the cycle's initial residual (Arnoldi-relation residual)
     double* h_host = nullptr;  // pinned
+    // device-driven steps (flexible candidate): Hessenberg, least-squares scratch, step state
+    DBuf<double> Hd, hk, ls_rhs, ls_tau, ls_nrm, gst;
+    DBuf<int> ls_piv;
+    void* h_slots = nullptr;  // pinned GmresDevState per step
+    cudaEvent_t evs[2] = {nullptr, nullptr};
     void setup(long long n, int restart, bool keep_z, cudaStream_t st);
     ~Gmres();
 };

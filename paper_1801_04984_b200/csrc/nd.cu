@@ -229,6 +229,7 @@ struct NdArgs {
     int nodep;                // debug timing only (PDG_ND_NODEP): skip the dependency waits (wrong results)
     int nomath;               // debug timing only (PDG_ND_NOMATH): consume the matrix chunks without the products
     int fence;                // PDG_ND_FENCE: explicit fence.acq_rel.gpu before each completion release
+    const int* stop;          // skip the solve once *stop != 0 (speculative GMRES steps)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -332,6 +333,10 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         for (int w = tid; w < words; w += kNdBlock) dst[w] = src[w];
     }
     __syncthreads();
+    if (a.stop && *a.stop) {  // skipped call: completion counters advance as if every task ran
+        for (int i = tid; i < nt; i += kNdBlock) atomicAdd(a.cnt + tsk[i].signal, 1ull);
+        return;
+    }
     if (warp == kNdWarpProducer) {  // TMA producer
         if (lane == 0) {
             // two cursors over this CTA's matrix chunks: the ring fill, and an L2
@@ -1094,7 +1099,7 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
-             std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr};
+             std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;

@@ -67,6 +67,7 @@ struct NdChol {
     size_t smem = 0;
     int prof_phase = PROF_A_SOLVE;
     double factor_bytes = 0.0;  // bytes of M and M^T read per solve
+    const int* guard = nullptr;  // skip solves on the device once *guard != 0 (speculative GMRES steps)
     long long cbtot = 0;
     // y, xpos in pivot-position order; cbuf: per front, the two children's update vectors
     // scattered to the front's local positions ([child][s + b], per right-hand side)

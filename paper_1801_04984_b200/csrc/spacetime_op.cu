@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, long l
                                                      const int* __restrict__ u_col, const double* __restrict__ u_val,
                                                      const long long* __restrict__ s_off, const int* __restrict__ s_len,
                                                      const int* __restrict__ s_col, const double* __restrict__ s_val,
-                                                     const double* __restrict__ x, double* __restrict__ y) {
+                                                     const double* __restrict__ x, double* __restrict__ y,
+                                                     const int* __restrict__ stop) {
+    if (stop && *stop) return;
     if (static_cast<int>(blockIdx.x) < gu) {
         const long long stride = (long long)gu * blockDim.x;
         for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
@@ -210,7 +212,9 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_strip(long long u_threads, 
                                                            const int* __restrict__ u_col, const double* __restrict__ u_val,
                                                            const long long* __restrict__ s_off, const int* __restrict__ s_len,
                                                            const int* __restrict__ s_col, const double* __restrict__ s_val,
-                                                           const double* __restrict__ x, double* __restrict__ y) {
+                                                           const double* __restrict__ x, double* __restrict__ y,
+                                                     const int* __restrict__ stop) {
+    if (stop && *stop) return;
     if (static_cast<int>(blockIdx.x) < gu) {
         const long long stride = (long long)gu * blockDim.x;
         for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
@@ -339,7 +343,7 @@ void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     k_spmv<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p, u_val.p,
-                                           s_off.p, s_len.p, s_col.p, s_val.p, x, y);
+                                           s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard);
     count_launch();
     PDG_CHECK_LAUNCH();
 }
@@ -387,7 +391,7 @@ void SpaceTimeOp::apply_strip(const double* x, double* y, cudaStream_t st) const
     ProfScope prof(PROF_SPMV, st, 0.0);
     k_spmv_strip<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, cell0, ncs, gu, ns, strip_slices.p, s_rows, n_cells, nt, n_u, n_q,
                                                  n_p, strip_nx, strip_ny, strip_r0, strip_r1, u_off.p, u_col.p, u_val.p,
-                                                 s_off.p, s_len.p, s_col.p, s_val.p, x, y);
+                                                 s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard);
     count_launch();
     PDG_CHECK_LAUNCH();
 }

@@ -42,6 +42,8 @@ struct SpaceTimeOp {
     void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st,
                const double* kappa = nullptr);
     void apply(const double* x, double* y, cudaStream_t st) const;
+    // when set, apply() is skipped on the device once *guard != 0 (speculative GMRES steps)
+    const int* guard = nullptr;
     // Rows owned by the strip of cell rows [r0, r1) of an nx x ny mesh (multi-GPU
     // row partitioning): displacement and pressure rows of its
     // cells, flux rows of its face rows. Only owned y entries are written; x must

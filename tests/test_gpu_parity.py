@@ -555,18 +555,31 @@ def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
     """The fused cooperative Arnoldi kernels (both Gram-Schmidt passes + norm +
     normalisation in one launch; the Arnoldi-relation residual and its norm in
     one launch) keep the row order, the per-block partials and the partial-sum
-    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1): solutions,
-    residual histories and iteration counts are bit-identical."""
+    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1), and the
+    opt-in device-driven steps (PDG_GMRES_DEVICE_LS: Hessenberg column, breakdown
+    test and least squares on the device; PDG_GMRES_LOOKAHEAD: next step queued
+    speculatively) make the host loop's decisions with the same bits: solutions, residual histories and
+    iteration counts are bit-identical. restart=2 exercises cycle ends without
+    convergence."""
     spec = P.config1(16)
     ops = S.SpatialOperators.assemble(spec)
     t = S.time_constants(1)
     rhs = np.random.default_rng(11).standard_normal(2 * ops.n_total)
     opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=restart), candidate=candidate)
     blk = S.BlockSolver(ops, t["T"], 0.05, opt=opt)
-    x_f, rep_f = blk.solve(rhs)
+    x_f, rep_f = blk.solve(rhs)  # host-driven loop, fused kernels
+    runs = []
+    if candidate == "flexible":
+        monkeypatch.setenv("PDG_GMRES_DEVICE_LS", "1")  # device-driven steps (least squares on the device)
+        runs.append(blk.solve(rhs))
+        monkeypatch.setenv("PDG_GMRES_LOOKAHEAD", "1")  # + speculative next step, skipped on the device
+        runs.append(blk.solve(rhs))
+        monkeypatch.delenv("PDG_GMRES_DEVICE_LS")
+        monkeypatch.delenv("PDG_GMRES_LOOKAHEAD")
     monkeypatch.setenv("PDG_KRYLOV_UNFUSED", "1")
-    x_u, rep_u = blk.solve(rhs)
-    assert rep_f.converged and rep_u.converged
-    assert rep_f.iterations == rep_u.iterations
-    assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
-    assert np.array_equal(x_f, x_u)
+    runs.append(blk.solve(rhs))
+    for x_u, rep_u in runs:
+        assert rep_f.converged and rep_u.converged
+        assert rep_f.iterations == rep_u.iterations
+        assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
+        assert np.array_equal(x_f, x_u)
