@@ -6,6 +6,7 @@
 //   u-row  : tau*a (u_i), tau*((-b)*e) (p_i)
 //   q-row  : tau*mq (q_i), tau*bv (p_i)
 //   p-row  : for j: theta_ij*((-b)*e) (u_j), [j==i] tau*bv (q_i), theta_ij*((-(1/M))*m_p) (p_j)
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "ops.cuh"
@@ -140,7 +141,7 @@ __global__ void k_s_fill(long long s_rows, int m, int nt, int nu, int nq, int np
 // blocks the S class (one thread per row).
 constexpr int kSpmvBlock = 256;
 
-__global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, long long s_rows, int gu, int n_cells, int nt,
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, int u2, long long s_rows, int gu, int n_cells, int nt,
                                                      int nu, int nq, int np, const long long* __restrict__ u_off,
                                                      const int* __restrict__ u_col, const double* __restrict__ u_val,
                                                      const long long* __restrict__ s_off, const int* __restrict__ s_len,
@@ -150,20 +151,44 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, long l
     if (stop && *stop) return;
     if (static_cast<int>(blockIdx.x) < gu) {
         const long long stride = (long long)gu * blockDim.x;
+        if (!u2) {  // one row per thread (large operators: more independent streams in flight)
+            for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
+                const long long g = t >> 3;
+                const int l = static_cast<int>(t & 7);
+                const long long b = __ldg(&u_off[g]), e = __ldg(&u_off[g + 1]);
+                double s = 0.0;
+#pragma unroll 8
+                for (long long k = b; k < e; ++k) {
+                    const double v = __ldcs(&u_val[k * 8 + l]);
+                    const double xv = __ldg(&x[__ldg(&u_col[k])]);
+                    s = __dadd_rn(s, __dmul_rn(v, xv));
+                }
+                const int i = static_cast<int>(g / n_cells);
+                const int c = static_cast<int>(g - (long long)i * n_cells);
+                y[(long long)i * nt + 8 * c + l] = s;
+            }
+            return;
+        }
+        // two rows (2j, 2j+1) of a group per thread (small operators: the grid fits one wave):
+        // one column index and one x load serve both, values as one 16-byte load; each row
+        // still summed alone in stored order
+        const double2* __restrict__ uv2 = reinterpret_cast<const double2*>(u_val);
         for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
-            const long long g = t >> 3;
-            const int l = static_cast<int>(t & 7);
+            const long long g = t >> 2;
+            const int j = static_cast<int>(t & 3);
             const long long b = __ldg(&u_off[g]), e = __ldg(&u_off[g + 1]);
-            double s = 0.0;
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
             for (long long k = b; k < e; ++k) {
-                const double v = __ldcs(&u_val[k * 8 + l]);
+                const double2 v = __ldcs(&uv2[k * 4 + j]);
                 const double xv = __ldg(&x[__ldg(&u_col[k])]);
-                s = __dadd_rn(s, __dmul_rn(v, xv));
+                s0 = __dadd_rn(s0, __dmul_rn(v.x, xv));
+                s1 = __dadd_rn(s1, __dmul_rn(v.y, xv));
             }
             const int i = static_cast<int>(g / n_cells);
             const int c = static_cast<int>(g - (long long)i * n_cells);
-            y[(long long)i * nt + 8 * c + l] = s;
+            y[(long long)i * nt + 8 * c + 2 * j] = s0;
+            y[(long long)i * nt + 8 * c + 2 * j + 1] = s1;
         }
     } else {
         const int bid = blockIdx.x - gu;
@@ -339,10 +364,12 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
 
 void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     ProfScope prof(PROF_SPMV, st, 8.0 * (double)(nnz + 2 * rows));
-    const long long u_threads = u_groups * 8;
+    int u2 = rows <= (2LL << 20);  // two U rows per thread up to 2M rows (256^2 dG(1) and below)
+    if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;  // test override: 1 | 2
+    const long long u_threads = u_groups * (u2 ? 4 : 8);
     const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
-    k_spmv<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p, u_val.p,
+    k_spmv<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p, u_val.p,
                                            s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard);
     count_launch();
     PDG_CHECK_LAUNCH();

@@ -64,10 +64,15 @@ def _upload_from_oracle(rp, spec):
                                      m["inv_m"], m["k_dr"])
 
 
+@pytest.mark.parametrize("rows_per_thread", ["auto", "1", "2"])
 @pytest.mark.parametrize("n,r", [(16, 0), (16, 1), (64, 1)])
-def test_spacetime_operator_and_spmv_bit_identical(oracle, n, r):
+def test_spacetime_operator_and_spmv_bit_identical(oracle, monkeypatch, n, r, rows_per_thread):
     """Canonical space-time CSR and order-fixed SpMV == SparseMatrix::apply on
-    the oracle's canonical CSR (sparse.hpp:30-40), bit for bit."""
+    the oracle's canonical CSR (sparse.hpp:30-40), bit for bit, in both U-class
+    thread mappings (one row per thread for large operators, two rows sharing
+    the column and x loads for small ones; PDG_SPMV_ROWS forces one)."""
+    if rows_per_thread != "auto":
+        monkeypatch.setenv("PDG_SPMV_ROWS", rows_per_thread)
     spec = P.config1(n)
     rp = oracle.RefProblem(spec.to_dict())
     T = oracle.time_constants(r)["T"]
