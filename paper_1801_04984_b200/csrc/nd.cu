@@ -230,6 +230,7 @@ struct NdArgs {
     int nomath;               // debug timing only (PDG_ND_NOMATH): consume the matrix chunks without the products
     int fence;                // PDG_ND_FENCE: explicit fence.acq_rel.gpu before each completion release
     const int* stop;          // skip the solve once *stop != 0 (speculative GMRES steps)
+    int tile8;                // PDG_ND_TILE8: the 8-row / 32-lane narrow-chunk GEMV instead of the 8-lane groups
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -254,6 +255,58 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
         }
     }
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+// Narrow-row chunk GEMV: the warp as 4 groups of 8 lanes, group q owns R rows of each
+// pass (4 R rows per pass), a lane sums its row segment over the columns c2 = lane % 8
+// (mod 8) for both right-hand sides (4 independent FMA chains per row), then an 8-lane
+// reduce-scatter of the 2 R (row, rhs) sums leaves lane l of the group with sum l.
+// Fewer shuffles and more independent chains than the 8-row / 32-lane tile
+// (tools/ubench/chunk_gemv.cu: "G8 R4").
+template <int R, typename Out>
+__device__ __forceinline__ void chunk_g8(const double2* __restrict__ rows2, int nrow, int ld2, const double2* va,
+                                         const double2* vb, int lane, Out out, int nr) {
+    static_assert(R == 2 || R == 4, "rows per lane group");
+    const int lg = lane & 7, grp = lane >> 3;
+    for (int rb = 0; rb < nrow; rb += 4 * R) {
+        const int row0 = rb + grp * R;
+        double acc[R][4];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+        for (int c2 = lg; c2 < ld2; c2 += 8) {
+            const double2 p = va[c2], q = vb[c2];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 m = row0 + r < nrow ? rows2[(size_t)(row0 + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                acc[r][0] = fma(m.x, p.x, acc[r][0]);
+                acc[r][1] = fma(m.y, p.y, acc[r][1]);
+                acc[r][2] = fma(m.x, q.x, acc[r][2]);
+                acc[r][3] = fma(m.y, q.y, acc[r][3]);
+            }
+        }
+        double v[2 * R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            v[2 * r] = acc[r][0] + acc[r][1];
+            v[2 * r + 1] = acc[r][2] + acc[r][3];
+        }
+        // reduce-scatter over the 8 lanes of the group (xor offsets stay inside it)
+#pragma unroll
+        for (int o = R; o >= 1; o >>= 1) {
+            const bool up = lg & o;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+                const double send = up ? v[i] : v[i + o];
+                const double keep = up ? v[i + o] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        double t = v[0];
+        if (R == 2) t += __shfl_xor_sync(0xffffffffu, t, 4);  // 4 values over 8 lanes: pair the halves
+        const int idx = R == 4 ? lg : (lg & 3);  // lane's (row, rhs) index: row idx / 2, rhs idx % 2
+        const int r = idx >> 1, k = idx & 1;
+        if ((R == 4 || lg < 4) && row0 + r < nrow && k < nr) out(k, row0 + r, t);
+    }
 }
 
 // Shared-memory layout of the solve kernel: mbarriers + task descriptors, the TMA
@@ -610,9 +663,13 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                 const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
                 const int nrow = min(rpc, nrows - rc);
                 if (a.nomath) {
+                } else if (rpc >= 16 && !a.tile8) {
+                    chunk_g8<4>(rows2, nrow, ld2, va, vb, lane, [&](int k, int lr, double t) { write_out(k, rc + lr, t); }, nr);
+                } else if (rpc >= 8 && !a.tile8) {
+                    chunk_g8<2>(rows2, nrow, ld2, va, vb, lane, [&](int k, int lr, double t) { write_out(k, rc + lr, t); }, nr);
                 } else if (rpc >= 8) {
                     // narrow rows: groups of 8 rows share each input load, lanes over the
-                    // columns, warp reduce-scatter of the 16 (row, rhs) sums
+                    // columns, warp reduce-scatter of the 16 (row, rhs) sums (PDG_ND_TILE8)
                     for (int rb = 0; rb < nrow; rb += 8) {
                         const int rn = min(8, nrow - rb);
                         double acc[16];
@@ -1099,7 +1156,8 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
-             std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard};
+             std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard,
+             std::getenv("PDG_ND_TILE8") != nullptr};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;
