@@ -309,6 +309,51 @@ __device__ __forceinline__ void chunk_g8(const double2* __restrict__ rows2, int 
     }
 }
 
+// Wide-row chunk GEMV: R rows at a time, all 32 lanes over the columns (stride 32),
+// 4 independent FMA chains per row; reduce-scatter of the 2 R (row, rhs) sums over the
+// low lane bits, then a butterfly over the rest: lane l < 2 R ends with sum l.
+template <int R, typename Out>
+__device__ __forceinline__ void chunk_wide(const double2* __restrict__ rows2, int nrow, int ld2, const double2* va,
+                                           const double2* vb, int lane, Out out, int nr) {
+    for (int rb = 0; rb < nrow; rb += R) {
+        double acc[R][4];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+        for (int c2 = lane; c2 < ld2; c2 += 32) {
+            const double2 p = va[c2], q = vb[c2];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 m = rb + r < nrow ? rows2[(size_t)(rb + r) * ld2 + c2] : make_double2(0.0, 0.0);
+                acc[r][0] = fma(m.x, p.x, acc[r][0]);
+                acc[r][1] = fma(m.y, p.y, acc[r][1]);
+                acc[r][2] = fma(m.x, q.x, acc[r][2]);
+                acc[r][3] = fma(m.y, q.y, acc[r][3]);
+            }
+        }
+        double v[2 * R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            v[2 * r] = acc[r][0] + acc[r][1];
+            v[2 * r + 1] = acc[r][2] + acc[r][3];
+        }
+#pragma unroll
+        for (int o = R; o >= 1; o >>= 1) {
+            const bool up = lane & o;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+                const double send = up ? v[i] : v[i + o];
+                const double keep = up ? v[i + o] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        double t = v[0];
+#pragma unroll
+        for (int o = 2 * R; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        const int r = lane >> 1, k = lane & 1;
+        if (lane < 2 * R && rb + r < nrow && k < nr) out(k, rb + r, t);
+    }
+}
+
 // Shared-memory layout of the solve kernel: mbarriers + task descriptors, the TMA
 // ring, then the buffer arena: per task (FIFO, offsets placed on the host so small
 // tasks pack densely and up to kNdBufs tasks are in flight) [v: rhs x vmt doubles]
@@ -688,6 +733,15 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                         const int r = lane >> 1, k = lane & 1;
                         if (lane < 16 && r < rn && k < nr) write_out(k, rc + rb + r, t);
                     }
+                } else if (!a.tile8) {
+                    // wide rows (fewer than 8 per chunk): R rows at a time over all 32 lanes
+                    auto o = [&](int k, int lr, double t) { write_out(k, rc + lr, t); };
+                    if (rpc >= 4)
+                        chunk_wide<4>(rows2, nrow, ld2, va, vb, lane, o, nr);
+                    else if (rpc >= 2)
+                        chunk_wide<2>(rows2, nrow, ld2, va, vb, lane, o, nr);
+                    else
+                        chunk_wide<1>(rows2, nrow, ld2, va, vb, lane, o, nr);
                 } else {
                     // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
                     // columns, butterfly over the warp
