@@ -13,7 +13,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 os.environ.setdefault("PDG_A_SOLVER", "nd")
 os.environ.setdefault("PDG_FLOW_SOLVER", "nd")
 ops = S.SpatialOperators.assemble(P.config1(n))
-blk = S.BlockSolver(ops, np.array([[1.7]]), 0.05)
+# PDG_DEBUG_M=2: the dG(1) block (2 right-hand sides per inner solve, as the bench)
+theta = S.time_constants(1)["T"] if os.environ.get("PDG_DEBUG_M") == "2" else np.array([[1.7]])
+blk = S.BlockSolver(ops, theta, 0.05)
 r = np.random.default_rng(0).standard_normal(blk.rows)
 z0 = blk.precondition(r)
 os.environ["PDG_ND_DEBUG"] = "1"
