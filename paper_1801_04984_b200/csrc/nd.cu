@@ -1142,11 +1142,14 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     // shared memory: header, task list, TMA ring, and the buffer arena (at least three of the
     // largest task buffers, so a task's buffer never waits on the previous task's)
     const size_t fixed = kNdHeader + nd_task_bytes(max_tasks);
-    const size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
+    size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
+    if (const char* e = std::getenv("PDG_ND_ARENA_KB")) arena_min = 1024 * (size_t)std::max(16, std::atoi(e));
     require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
     stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
     require(stages >= kNdComputeWarps, "nested dissection: ring shallower than the compute warps (stage size too large)");
     const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
+    arena_bytes = arena;
+    max_task_buf = max_buf;
     smem = fixed + (size_t)stages * stage_bytes + arena;
     // FIFO placement of the task buffers in the arena (tasks run and release in order)
     for (auto& v : per_cta) {
@@ -1232,8 +1235,8 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
             t00 = std::min(t00, h[4 * i]);
             tend = std::max(tend, h[4 * i + 1]);
         }
-        std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d vmax=%d stages=%d x %u B total %.2f us\n", n,
-                     nfront, maxdepth, ntask, grid, max_tasks, vmax, stages, stage_bytes, (tend - t00) * 1e-3);
+        std::fprintf(stderr, "nd solve n=%d fronts=%d depth=%d tasks=%lld grid=%d max/cta=%d vmax=%d arena=%zu (max buf %zu) stages=%d x %u B total %.2f us\n", n,
+                     nfront, maxdepth, ntask, grid, max_tasks, vmax, arena_bytes, max_task_buf, stages, stage_bytes, (tend - t00) * 1e-3);
         for (int type = 0; type < 3; ++type)
             for (int d = maxdepth; d >= 0; --d) {
                 const int dd = type == 2 ? maxdepth - d : d;

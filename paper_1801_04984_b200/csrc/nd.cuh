@@ -64,7 +64,7 @@ struct NdChol {
     int grid = 0, stages = 3, vmax = 0, max_tasks = 0, pf = 16;
     unsigned stage_bytes = 24576;
     unsigned long long call = 0;
-    size_t smem = 0;
+    size_t smem = 0, arena_bytes = 0, max_task_buf = 0;
     int prof_phase = PROF_A_SOLVE;
     double factor_bytes = 0.0;  // bytes of M and M^T read per solve
     const int* guard = nullptr;  // skip solves on the device once *guard != 0 (speculative GMRES steps)
