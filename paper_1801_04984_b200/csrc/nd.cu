@@ -231,6 +231,7 @@ struct NdArgs {
     int fence;                // PDG_ND_FENCE: explicit fence.acq_rel.gpu before each completion release
     const int* stop;          // skip the solve once *stop != 0 (speculative GMRES steps)
     int tile8;                // PDG_ND_TILE8: the 8-row / 32-lane narrow-chunk GEMV instead of the 8-lane groups
+    int pairs;                // PDG_ND_PAIRS=1: two warps per chunk (measured slower: 298 vs 287 us at config 1)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -265,10 +266,10 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
 // (tools/ubench/chunk_gemv.cu: "G8 R4").
 template <int R, typename Out>
 __device__ __forceinline__ void chunk_g8(const double2* __restrict__ rows2, int nrow, int ld2, const double2* va,
-                                         const double2* vb, int lane, Out out, int nr) {
-    static_assert(R == 2 || R == 4, "rows per lane group");
+                                         const double2* vb, int lane, Out out, int nr, int start = 0, int step = 1) {
+    static_assert(R == 1 || R == 2 || R == 4, "rows per lane group");
     const int lg = lane & 7, grp = lane >> 3;
-    for (int rb = 0; rb < nrow; rb += 4 * R) {
+    for (int rb = start * 4 * R; rb < nrow; rb += step * 4 * R) {
         const int row0 = rb + grp * R;
         double acc[R][4];
 #pragma unroll
@@ -302,10 +303,11 @@ __device__ __forceinline__ void chunk_g8(const double2* __restrict__ rows2, int 
             }
         }
         double t = v[0];
-        if (R == 2) t += __shfl_xor_sync(0xffffffffu, t, 4);  // 4 values over 8 lanes: pair the halves
-        const int idx = R == 4 ? lg : (lg & 3);  // lane's (row, rhs) index: row idx / 2, rhs idx % 2
+#pragma unroll
+        for (int o = 2 * R; o < 8; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // 2 R values over 8 lanes
+        const int idx = lg & (2 * R - 1);  // lane's (row, rhs) index: row idx / 2, rhs idx % 2
         const int r = idx >> 1, k = idx & 1;
-        if ((R == 4 || lg < 4) && row0 + r < nrow && k < nr) out(k, row0 + r, t);
+        if (lg < 2 * R && row0 + r < nrow && k < nr) out(k, row0 + r, t);
     }
 }
 
@@ -314,8 +316,8 @@ __device__ __forceinline__ void chunk_g8(const double2* __restrict__ rows2, int 
 // low lane bits, then a butterfly over the rest: lane l < 2 R ends with sum l.
 template <int R, typename Out>
 __device__ __forceinline__ void chunk_wide(const double2* __restrict__ rows2, int nrow, int ld2, const double2* va,
-                                           const double2* vb, int lane, Out out, int nr) {
-    for (int rb = 0; rb < nrow; rb += R) {
+                                           const double2* vb, int lane, Out out, int nr, int start = 0, int step = 1) {
+    for (int rb = start * R; rb < nrow; rb += step * R) {
         double acc[R][4];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     if (tid == 0) {
         for (int k = 0; k < a.stages; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], 1);
+            mbar_init(&empty[k], a.pairs ? 2 : 1);
         }
         for (int k = 0; k < kNdBufs; ++k) {
             mbar_init(&staged[k], 1);
@@ -672,7 +674,11 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         const int rpc = static_cast<int>(a.stage_bytes / (8u * ld));
         const int nch = (nrows + rpc - 1) / rpc;
         // chunks of this task owned by this warp: seq + c with (seq + c) % 8 == warp
-        const int first = (warp - seq % kNdComputeWarps + kNdComputeWarps) % kNdComputeWarps;
+        // chunk owners: warp c % 8, or (pairs) the warp pair c % 4 with the chunk's row passes
+        // alternating between the two warps (a consumer then has two ring slots in flight)
+        const int ncons = a.pairs ? kNdComputeWarps / 2 : kNdComputeWarps;
+        const int me = a.pairs ? warp >> 1 : warp, half = a.pairs ? (warp & 1) : 0, npart = a.pairs ? 2 : 1;
+        const int first = (me - seq % ncons + ncons) % ncons;
         // every warp waits for every task's input, chunks or not: keeps the warps within one
         // phase of the gathered / done barriers (a warp skipping tasks could otherwise run a
         // full buffer cycle ahead and alias a barrier phase)
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                     a.cb[k * a.cbtot + oix[lr]] = t + w;
                 }
             };
-            for (int c = first; c < nch; c += kNdComputeWarps) {
+            for (int c = first; c < nch; c += ncons) {
                 const int sq = seq + c, rc = c * rpc;
                 const int slot = sq % a.stages;
                 // warps drift apart (no per-task barrier): before waiting for chunk sq to land, wait
@@ -708,10 +714,15 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                 const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
                 const int nrow = min(rpc, nrows - rc);
                 if (a.nomath) {
-                } else if (rpc >= 16 && !a.tile8) {
-                    chunk_g8<4>(rows2, nrow, ld2, va, vb, lane, [&](int k, int lr, double t) { write_out(k, rc + lr, t); }, nr);
                 } else if (rpc >= 8 && !a.tile8) {
-                    chunk_g8<2>(rows2, nrow, ld2, va, vb, lane, [&](int k, int lr, double t) { write_out(k, rc + lr, t); }, nr);
+                    // rows per pass 4 R, with at least npart passes per chunk
+                    auto o = [&](int k, int lr, double t) { write_out(k, rc + lr, t); };
+                    if (rpc >= 16 * npart)
+                        chunk_g8<4>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
+                    else if (rpc >= 8 * npart)
+                        chunk_g8<2>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
+                    else
+                        chunk_g8<1>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
                 } else if (rpc >= 8) {
                     // narrow rows: groups of 8 rows share each input load, lanes over the
                     // columns, warp reduce-scatter of the 16 (row, rhs) sums (PDG_ND_TILE8)
@@ -736,12 +747,12 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
                 } else if (!a.tile8) {
                     // wide rows (fewer than 8 per chunk): R rows at a time over all 32 lanes
                     auto o = [&](int k, int lr, double t) { write_out(k, rc + lr, t); };
-                    if (rpc >= 4)
-                        chunk_wide<4>(rows2, nrow, ld2, va, vb, lane, o, nr);
-                    else if (rpc >= 2)
-                        chunk_wide<2>(rows2, nrow, ld2, va, vb, lane, o, nr);
+                    if (rpc >= 4 * npart)
+                        chunk_wide<4>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
+                    else if (rpc >= 2 * npart)
+                        chunk_wide<2>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
                     else
-                        chunk_wide<1>(rows2, nrow, ld2, va, vb, lane, o, nr);
+                        chunk_wide<1>(rows2, nrow, ld2, va, vb, lane, o, nr, half, npart);
                 } else {
                     // wide rows (fewer than 8 per chunk): two rows at a time, lanes over the
                     // columns, butterfly over the warp
@@ -1214,7 +1225,8 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
              std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard,
-             std::getenv("PDG_ND_TILE8") != nullptr};
+             std::getenv("PDG_ND_TILE8") != nullptr,
+             std::getenv("PDG_ND_TILE8") == nullptr && std::getenv("PDG_ND_PAIRS") && std::atoi(std::getenv("PDG_ND_PAIRS")) > 0};
     const bool debug = std::getenv("PDG_ND_DEBUG") != nullptr;
     const long long ntask = static_cast<long long>(d_tasks.n);
     DBuf<unsigned long long> dbg;
