@@ -588,3 +588,57 @@ def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
         assert rep_f.iterations == rep_u.iterations
         assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
         assert np.array_equal(x_f, x_u)
+
+
+def test_spmv_config3_256_bit_identical(oracle):
+    """BASELINE config 3 at 256^2 (dG(1), 1.44M rows, 59.6M nnz): the device-built
+    canonical CSR and y = A x (x ~ U(-1,1), seed 4984) equal the oracle's CSR and
+    SparseMatrix::apply on it bit for bit (the two-row thread mapping runs here)."""
+    spec = P.config3(256)
+    T = oracle.time_constants(1)["T"]
+    op = S.SpaceTimeOperator(S.SpatialOperators.assemble(spec), T, 0.05)
+    assert op.rows == 1442816 and op.nnz == 59583488  # SURVEY Appendix B
+    go, gi, gv = op.csr()
+    rp = oracle.RefProblem(spec.to_dict())
+    ro, ri, rv = rp.spacetime_csr(T, 0.05)
+    assert np.array_equal(ro.astype(np.int64), go)
+    assert np.array_equal(ri, gi)
+    assert np.array_equal(rv, gv)
+    del gi, gv
+    import torch
+    x = P.uniform_vector(P.X_SEED, op.rows)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    op.apply_device(xd.data_ptr(), yd.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), oracle.csr_apply(ro, ri, rv, x))
+
+
+def test_spmv_config3_1024_properties(monkeypatch):
+    """BASELINE config 3 at full size (1024^2, 23.1M rows, 955.6M nnz), through
+    size-independent properties: the two U-class thread mappings give the same
+    bits, repeated applications are bit-identical, A (2 x) = 2 A x exactly (a
+    power-of-two scaling commutes with every rounding), and A 0 = 0."""
+    import torch
+    T = S.time_constants(1)["T"]
+    op = S.SpaceTimeOperator(S.SpatialOperators.assemble(P.config3(1024)), T, 0.05)
+    assert op.rows == 23072768 and op.nnz == 955559936  # SURVEY Appendix B
+    x = torch.from_numpy(P.uniform_vector(P.X_SEED, op.rows)).cuda()
+    y1, y2, y3 = (torch.empty_like(x) for _ in range(3))
+    op.apply_device(x.data_ptr(), y1.data_ptr())
+    op.apply_device(x.data_ptr(), y2.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    monkeypatch.setenv("PDG_SPMV_ROWS", "2")
+    op.apply_device(x.data_ptr(), y3.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y3)
+    monkeypatch.delenv("PDG_SPMV_ROWS")
+    x2 = 2.0 * x
+    op.apply_device(x2.data_ptr(), y2.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(y2, 2.0 * y1)
+    x.zero_()
+    op.apply_device(x.data_ptr(), y2.data_ptr())
+    torch.cuda.synchronize()
+    assert not torch.any(y2 != 0)
