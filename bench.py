@@ -148,6 +148,36 @@ def spmv_sweep(sizes, reps, peak):
     return out
 
 
+def spmv_cpu_baseline(n, reps=5):
+    """Config 3 CPU leg ("CPU all-core, not reference"): the oracle's
+    SparseMatrix::apply restatement with all host threads on the canonical CSR of
+    the n x n operator (downloaded from the device build, which is bit-identical to
+    the oracle's), median of `reps`; the result is checked bit for bit against the
+    GPU's y."""
+    import torch
+    from oracle import refcpu
+    from paper_1801_04984_b200 import problem as P, solver as S
+    op = S.SpaceTimeOperator(S.SpatialOperators.assemble(P.config3(n)), S.time_constants(1)["T"], 0.05)
+    off, idx, val = op.csr()
+    x = P.uniform_vector(P.X_SEED, op.rows)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    op.apply_device(xd.data_ptr(), yd.data_ptr())
+    torch.cuda.synchronize()
+    threads = os.cpu_count()
+    refcpu.csr_apply(off, idx, val, x, threads)  # warm-up
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        y = refcpu.csr_apply(off, idx, val, x, threads)
+        ts.append(time.perf_counter() - t0)
+    med = sorted(ts)[len(ts) // 2]
+    return {"n": n, "rows": op.rows, "nnz": op.nnz, "threads": threads, "median_ms": 1e3 * med,
+            "gdof_s": op.rows / med / 1e9, "achieved_GBs": 8.0 * (op.nnz + 2 * op.rows) / med / 1e9,
+            "bit_identical_to_gpu": bool(np.array_equal(y, yd.cpu().numpy())),
+            "label": "CPU all-core CSR SpMV (oracle restatement of SparseMatrix::apply, OpenMP over rows; not the reference)"}
+
+
 def spmv_distributed(n, reps, peak, rank, world, dist):
     """Config 3 at N GPUs, strong scaling: every rank owns a strip of cell rows of
     the n x n operator (parallel.DeviceStripSpMV), one application = NCCL halo
@@ -397,6 +427,12 @@ def main():
                "sample": f"{args.cpu_slabs} slab(s) of config 1 on the host (setup {res['setup_seconds']:.1f} s "
                          "excluded, first slab warm-up); oracle with exact banded sparse-direct inner solves; "
                          "factorisation OpenMP-parallel, triangular solves serial"}
+    spmv_cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.spmv_sizes:
+        try:
+            spmv_cpu = spmv_cpu_baseline(min(int(v) for v in args.spmv_sizes.split(",") if v))
+        except Exception as e:  # report, do not lose the headline line
+            spmv_cpu = {"error": repr(e)[:300]}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": ms_dev, "unit": "ms/slab", "n_gpus": world, "steps": args.steps,
@@ -405,7 +441,7 @@ def main():
             "config": {"workload": WORKLOAD, "rows_per_block": nn * nt,
                        "gmres_candidate": "flexible: x + Z y (the reference's gmres_flexible, gmres.hpp:113-114,"
                                           " 153-158; same iterations, solutions within 1e-9 of gmres)",
-                       "l2": "no flush: per-step working set (displacement-solve matrices 1.07 GB) > 126 MB L2",
+                       "l2": "no flush: per-step working set (nested-dissection factor matrices 0.73 GB) > 126 MB L2",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "setup_s": setup_s},
             "iterations": main_run["iters"],
             "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],
@@ -415,7 +451,7 @@ def main():
             "gpu_launches": int(main_run["launches"]), "roofline": roofline, "spmv_roofline": spmv_roof,
             "phases": phases, "spmv": spmv, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist,
             "clocks": main_run["clocks"],
-            "cpu_baseline": cpu}), flush=True)
+            "cpu_baseline": cpu, "spmv_cpu_baseline": spmv_cpu}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
