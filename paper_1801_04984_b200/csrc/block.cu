@@ -999,9 +999,9 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     bool x_is_zero = true;
     while (total < max_iter) {
         double beta;
-        if (x_is_zero) {  // r = b - op(0) = b exactly
+        if (x_is_zero) {  // r = b - op(0) = b exactly, so ||r|| is ||b|| (same kernels, same bits)
             PDG_CUDA(cudaMemcpyAsync(kr.r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-            beta = K.norm(kr.r.p);
+            beta = bnorm;
         } else {
             op.apply(kr.x.p, kr.t.p, st);
             beta = K.sub_norm(b, kr.t.p, kr.r.p);
