@@ -307,21 +307,22 @@ __global__ void k_flow_fp(int m, int np, int nt, int nu, int nq, int lag, double
 }
 // rq_i[f] = r_q_i[f] - sum_{B row f} (w bv) (dinv_c fp_c)
 __global__ void k_flow_rq(int m, int nq, int np, int nt, int nu, double w, const double* __restrict__ r,
-                          const double* __restrict__ fp, const int* b_off, const int* b_idx, const double* b_val,
-                          const double* __restrict__ dinv, double* __restrict__ rq, const int* __restrict__ stop) {
+                          const double* __restrict__ fp, long long fps, const int* b_off, const int* b_idx,
+                          const double* b_val, const double* __restrict__ dinv, double* __restrict__ rq,
+                          const int* __restrict__ stop) {
     if (stop && *stop) return;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * nq; t += (long long)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(t / nq), f = static_cast<int>(t % nq);
         double v = r[(long long)i * nt + nu + f];
         for (int k = b_off[f]; k < b_off[f + 1]; ++k) {
             const int c = b_idx[k];
-            v -= w * b_val[k] * (dinv[c] * fp[(long long)i * np + c]);
+            v -= w * b_val[k] * (dinv[c] * fp[(long long)i * fps + c]);
         }
         rq[t] = v;
     }
 }
 // p_i[c] = dinv_c (fp_c - w sum_{B^T row c} bv q_f)   (q already in z)
-__global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const double* __restrict__ fp,
+__global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const double* __restrict__ fp, long long fps,
                          const int* bt_off, const int* bt_idx, const double* bt_val, const double* __restrict__ dinv,
                          double* __restrict__ z, const int* __restrict__ stop) {
     if (stop && *stop) return;
@@ -329,7 +330,7 @@ __global__ void k_flow_p(int m, int np, int nt, int nu, int nq, double w, const 
         const int i = static_cast<int>(t / np), c = static_cast<int>(t % np);
         double btq = 0.0;
         for (int k = bt_off[c]; k < bt_off[c + 1]; ++k) btq += bt_val[k] * z[(long long)i * nt + nu + bt_idx[k]];
-        z[(long long)i * nt + nu + nq + c] = dinv[c] * (fp[t] - w * btq);
+        z[(long long)i * nt + nu + nq + c] = dinv[c] * (fp[(long long)i * fps + c] - w * btq);
     }
 }
 // mech_i = r_u_i / w + b (E p_i)
@@ -767,14 +768,22 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
         return;
     }
     const int lag = xprev != nullptr;
+    // first sweep (lag = 0): fp is r_p itself, read in place (no copy kernel)
+    const double* fpb = r + nu + nq;
+    long long fps = nt;
     {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (2.0 * np + 2.0 * nq + 3.0 * o.B.nnz));
-        k_flow_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, lag, lambda, o.biot_b, stab, r,
-                                                                    xprev, o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.m_p.p,
-                                                                    fp.p, guard);
-        k_flow_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, w, r, fp.p, o.B.off.p, o.B.idx.p,
+        if (lag) {
+            k_flow_fp<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, lag, lambda, o.biot_b, stab, r,
+                                                                        xprev, o.Et.off.p, o.Et.idx.p, o.Et.val.p, o.m_p.p,
+                                                                        fp.p, guard);
+            count_launch();
+            fpb = fp.p;
+            fps = np;
+        }
+        k_flow_rq<<<grid_for((long long)m * nq, 256), 256, 0, st>>>(m, nq, np, nt, nu, w, r, fpb, fps, o.B.off.p, o.B.idx.p,
                                                                     o.B.val.p, dinv.p, rq.p, guard);
-        count_launch(2);
+        count_launch();
         PDG_CHECK_LAUNCH();
     }
     if (flow_use_nd)
@@ -783,7 +792,7 @@ void FixedStressPre::sweep_once(const double* xprev, const double* r, double* z,
         flow.solve(rq.p, nq, z + nu, nt, m, st);
     {
         ProfScope prof(PROF_PRE_OTHER, st, 8.0 * m * (3.0 * np + 2.0 * o.Bt.nnz + 2.0 * nu + 2.0 * o.E.nnz));
-        k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fp.p, o.Bt.off.p, o.Bt.idx.p,
+        k_flow_p<<<grid_for((long long)m * np, 256), 256, 0, st>>>(m, np, nt, nu, nq, w, fpb, fps, o.Bt.off.p, o.Bt.idx.p,
                                                                    o.Bt.val.p, dinv.p, z, guard);
         k_mech_rhs<<<grid_for((long long)m * nu, 256), 256, 0, st>>>(m, nu, nt, nq, w, o.biot_b, r, z, o.E.off.p,
                                                                      o.E.idx.p, o.E.val.p, mech.p, guard);
