@@ -33,12 +33,18 @@ namespace pdg {
 
 namespace {
 
-constexpr int kNdThreads = 256;
+#ifndef PDG_ND_THREADS
+#define PDG_ND_THREADS 256
+#endif
+#ifndef PDG_ND_BUFS
+#define PDG_ND_BUFS 8
+#endif
+constexpr int kNdThreads = PDG_ND_THREADS;  // compute threads (tuning: tools/nd_variant_sweep.sh)
 constexpr int kNdMaxRhs = 2;
 constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector staging in shared memory)
 constexpr int kNdComputeWarps = kNdThreads / 32;
 constexpr int kNdPrepWarps = 2;  // input warps
-constexpr int kNdBufs = 8;       // pipeline slots (barrier sets); task buffers live in a FIFO arena
+constexpr int kNdBufs = PDG_ND_BUFS;     // pipeline slots (barrier sets); task buffers live in a FIFO arena
 constexpr int kNdGatherWarps = 4;  // dependency wait + dependent gather, tasks in order
 constexpr int kNdGatherThreads = 32 * kNdGatherWarps;
 constexpr int kNdWarpProducer = kNdComputeWarps;
