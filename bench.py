@@ -300,6 +300,8 @@ def main():
             # W + K > n_slabs): its own start and length, as the reference's march uses them
             t0 = run["T"] * n / run["n_slabs"]
             t1 = run["T"] * (n + 1) / run["n_slabs"]
+            # u_prev / p_prev were written on torch's stream; the library runs on its own
+            torch.cuda.synchronize()
             slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=t1 - t0)
             if keep:
                 rhs_host.append(rhs.cpu().pin_memory().numpy())

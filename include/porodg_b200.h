@@ -103,7 +103,12 @@ const char* pdg_version(void);
 int pdg_ctx_create(int device, pdg_ctx** out);
 void pdg_ctx_destroy(pdg_ctx* ctx);
 
-/* Upload reference-assembled operators (SpatialOperators) from host CSR. */
+/* Structured-mesh dimensions (mesh.hpp:42-60) of reference-assembled operators, from
+ * n_p = nx ny, n_q = nx (ny + 1) + ny (nx + 1) and the cell pair of the first interior
+ * face row of B (which root is nx). dims = {nx, ny}. */
+int pdg_mesh_dims_from_operators(const pdg_csr* B, int n_q, int dims[2]);
+/* Upload reference-assembled operators (SpatialOperators) from host CSR.
+ * nx = ny = 0: infer the mesh with pdg_mesh_dims_from_operators. */
 int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B,
                    const pdg_csr* E, const double* m_p_diag, const signed char* q_constrained, double biot_b,
                    double inv_m, double k_dr, pdg_ops** out);

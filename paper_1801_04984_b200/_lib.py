@@ -72,6 +72,7 @@ _SIGS = {
     "pdg_ops_upload": (C.c_int, [VP, C.c_int, C.c_int, C.POINTER(CSR), C.POINTER(CSR), C.POINTER(CSR),
                                  C.POINTER(CSR), DP, C.POINTER(C.c_byte), C.c_double, C.c_double, C.c_double,
                                  C.POINTER(VP)]),
+    "pdg_mesh_dims_from_operators": (C.c_int, [C.POINTER(CSR), C.c_int, IP]),
     "pdg_ops_assemble": (C.c_int, [VP, C.POINTER(Problem), C.POINTER(VP)]),
     "pdg_ops_sizes": (C.c_int, [VP, LLP]),
     "pdg_ops_download": (C.c_int, [VP, C.c_int, IP, IP, DP]),

@@ -1051,39 +1051,52 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 PDG_CUDA(cudaMemcpyAsync(slots + k, gst, sizeof(GmresDevState), cudaMemcpyDeviceToHost, st));
                 PDG_CUDA(cudaEventRecord(kr.evs[k & 1], st));
             };
-            int kend = -1;
-            for (int k = 0; k < mm; ++k) {
-                step(k);  // queued behind step k - 1: skipped on the device if k - 1 ended the cycle
-                if (!lookahead) {  // one host round trip per step (the stop flag), no speculative step
-                    PDG_CUDA(cudaEventSynchronize(kr.evs[k & 1]));
-                    if (slots[k].stop) {
-                        kend = k;
-                        break;
-                    }
-                } else if (k >= 1) {
-                    PDG_CUDA(cudaEventSynchronize(kr.evs[(k - 1) & 1]));
-                    if (slots[k - 1].stop) {
-                        kend = k - 1;
-                        break;
+            const int left = max_iter - total;  // == mm unless the iteration limit cuts the cycle
+            int k0 = 0;
+            for (;;) {
+                int kend = -1;
+                for (int k = k0; k < mm; ++k) {
+                    step(k);  // queued behind step k - 1: skipped on the device if k - 1 ended the cycle
+                    if (!lookahead) {  // one host round trip per step (the stop flag), no speculative step
+                        PDG_CUDA(cudaEventSynchronize(kr.evs[k & 1]));
+                        if (slots[k].stop) {
+                            kend = k;
+                            break;
+                        }
+                    } else if (k > k0) {
+                        PDG_CUDA(cudaEventSynchronize(kr.evs[(k - 1) & 1]));
+                        if (slots[k - 1].stop) {
+                            kend = k - 1;
+                            break;
+                        }
                     }
                 }
+                if (kend < 0) {
+                    PDG_CUDA(cudaEventSynchronize(kr.evs[(mm - 1) & 1]));
+                    kend = mm - 1;
+                    for (int k = k0; k < mm; ++k)
+                        if (slots[k].stop) { kend = k; break; }
+                }
+                set_guard(nullptr);  // the explicit check below must run with the stop flag set
+                for (int k = k0; k < kend; ++k) hist.push_back(slots[k].res);
+                total += kend + 1 - k0;
+                // cand = x + Z y of the last step; the stop is decided on the explicit true residual
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, kend + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                count_launch();
+                op.apply(kr.cand.p, kr.t.p, st);
+                true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+                converged = true_res / bnorm <= opts.tol;
+                hist.push_back(true_res);
+                const bool cycle_end = slots[kend].brk || kend == mm - 1 || kend + 1 >= left;
+                if (converged || cycle_end) break;
+                // the Arnoldi-relation residual passed but the explicit one did not: the cycle
+                // goes on (gmres.hpp:118-131); re-arm the device state for step kend + 1
+                PDG_CUDA(cudaMemsetAsync(&gst->stop, 0, sizeof(int), st));
+                set_guard(&gst->stop);
+                k0 = kend + 1;
             }
-            if (kend < 0) {
-                PDG_CUDA(cudaEventSynchronize(kr.evs[(mm - 1) & 1]));
-                kend = mm - 1;
-            }
-            set_guard(nullptr);
-            for (int k = 0; k < kend; ++k) hist.push_back(slots[k].res);
-            total += kend + 1;
-            // cand = x + Z y of the last step; the stop is decided on the explicit true residual
-            { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, kend + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
-            count_launch();
-            op.apply(kr.cand.p, kr.t.p, st);
-            true_res = K.sub_norm(b, kr.t.p, kr.r.p);
             PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
             x_is_zero = false;
-            converged = true_res / bnorm <= opts.tol;
-            hist.push_back(true_res);
             if (converged) break;
             continue;
         }
@@ -1150,15 +1163,27 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 true_res = K.sub_norm(b, kr.t.p, kr.r.p);
             }
             bool ok = true_res / bnorm <= opts.tol;
-            if (ok || breakdown || k == mm - 1 || total >= max_iter) {
-                if (arnoldi_res) {
-                    { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
-                    count_launch();
-                    // the stop is decided on the explicit true residual, as gmres.hpp:68-72
-                    op.apply(kr.cand.p, kr.t.p, st);
-                    true_res = K.sub_norm(b, kr.t.p, kr.r.p);
-                    ok = true_res / bnorm <= opts.tol;
-                }
+            const bool cycle_end = breakdown || k == mm - 1 || total >= max_iter;
+            if (ok && arnoldi_res) {
+                // the Arnoldi-relation residual passed: the stop is decided on the explicit
+                // true residual b - op(x + Z y), as gmres.hpp:68-72
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                count_launch();
+                op.apply(kr.cand.p, kr.t.p, st);
+                true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+                ok = true_res / bnorm <= opts.tol;
+            } else if (!ok && cycle_end && arnoldi_res) {
+                // breakdown / full cycle / iteration limit: x = cand (gmres.hpp:123-130) and the
+                // recorded residual is the explicit one
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, k + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                count_launch();
+                op.apply(kr.cand.p, kr.t.p, st);
+                true_res = K.sub_norm(b, kr.t.p, kr.r.p);
+                ok = true_res / bnorm <= opts.tol;
+            }
+            // gmres.hpp:118-131: accept on the true residual; otherwise the cycle goes on
+            // unless it broke down, is full or hit the iteration limit
+            if (ok || cycle_end) {
                 PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
                 x_is_zero = false;
                 done = true;

@@ -199,11 +199,57 @@ void pdg_ctx_destroy(pdg_ctx* ctx) {
     delete ctx;
 }
 
+int pdg_mesh_dims_from_operators(const pdg_csr* B, int n_q, int dims[2]) {
+    API_BEGIN
+    require(B && dims, "pdg_mesh_dims_from_operators: null argument");
+    require(B->rows == n_q && B->cols > 0, "pdg_mesh_dims_from_operators: B must be n_q x n_p");
+    // n_p = nx ny and n_q = nx (ny + 1) + ny (nx + 1), so nx + ny = n_q - 2 n_p and nx, ny are
+    // the roots of t^2 - (nx + ny) t + nx ny
+    const long long np = B->cols, s = (long long)n_q - 2 * np;
+    require(s >= 2 && s * s >= 4 * np, "pdg_mesh_dims_from_operators: sizes do not fit a structured mesh");
+    long long d = (long long)std::llround(std::sqrt((double)(s * s - 4 * np)));
+    while (d * d > s * s - 4 * np) --d;
+    while ((d + 1) * (d + 1) <= s * s - 4 * np) ++d;
+    require(d * d == s * s - 4 * np && (s + d) % 2 == 0, "pdg_mesh_dims_from_operators: sizes do not fit a structured mesh");
+    const int a = (int)((s + d) / 2), b = (int)((s - d) / 2);
+    require(a >= 1 && b >= 1 && (long long)a * b == np, "pdg_mesh_dims_from_operators: sizes do not fit a structured mesh");
+    // interior face rows of B hold exactly the two adjacent cells (no-flux rows only sit on the
+    // boundary): the first interior horizontal face (j = 1, i = 0) is face nx with cells {0, nx};
+    // with ny = 1 the first interior vertical face (i = 1, j = 0) is face 2 nx + 1 with cells {0, 1}
+    auto fits = [&](int nx, int ny) {
+        int face, c1;
+        if (ny >= 2) {
+            face = nx;
+            c1 = nx;
+        } else if (nx >= 2) {
+            face = nx * (ny + 1) + ny;
+            c1 = 1;
+        } else {
+            return true;  // 1 x 1
+        }
+        if (face >= B->rows) return false;
+        const long long o0 = B->row_offsets[face], o1 = B->row_offsets[face + 1];
+        return o1 - o0 == 2 && B->col_indices[o0] == 0 && B->col_indices[o0 + 1] == c1;
+    };
+    const bool fa = fits(a, b), fb = fits(b, a);
+    require(fa || fb, "pdg_mesh_dims_from_operators: B does not match a structured mesh numbering");
+    dims[0] = fa ? a : b;
+    dims[1] = fa ? b : a;
+    API_END
+}
+
 int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B, const pdg_csr* E,
                    const double* m_p_diag, const signed char* q_constrained, double biot_b, double inv_m, double k_dr,
                    pdg_ops** out) {
     API_BEGIN
     require(ctx && A && M_q && B && E && m_p_diag && out, "pdg_ops_upload: null argument");
+    if (nx <= 0 && ny <= 0) {  // infer the structured mesh from the operators (mesh.hpp:42-60)
+        int dims[2];
+        const int rc = pdg_mesh_dims_from_operators(B, M_q->rows, dims);
+        if (rc != PDG_OK) return rc;
+        nx = dims[0];
+        ny = dims[1];
+    }
     require(nx > 0 && ny > 0, "pdg_ops_upload: mesh dimensions must be positive");
     PDG_CUDA(cudaSetDevice(ctx->c.device));
     cudaStream_t st = ctx->c.stream;
@@ -579,6 +625,9 @@ int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev
                                                                            s->rhs_p.p, s->djump.p, rhs_dev);
     count_launch(2);
     PDG_CHECK_LAUNCH();
+    // like every other *_device entry point: rhs_dev is complete when the call returns, so a
+    // caller on another stream (torch's) may read it without a library-stream dependency
+    PDG_CUDA(cudaStreamSynchronize(st));
     API_END
 }
 

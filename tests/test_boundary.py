@@ -5,6 +5,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 from paper_1801_04984_b200 import _lib, problem as P
 
@@ -57,3 +58,23 @@ def test_missing_gpu_is_loud():
     h = ctypes.c_void_p()
     rc = _lib.lib().pdg_ctx_create(0, ctypes.byref(h))
     assert rc != 0
+
+
+@pytest.mark.parametrize("nx,ny", [(12, 7), (7, 12), (16, 16), (5, 1), (1, 5), (1, 1), (3, 2)])
+def test_mesh_dims_inferred_from_reference_operators(oracle, nx, ny):
+    """pdg_ops_upload(nx = ny = 0) infers the structured mesh (mesh.hpp:42-60)
+    from reference-assembled operators, so the slab.hpp adapter
+    needs nothing beyond SpatialOperators. Host-only, no GPU."""
+    spec = P.config1(4)
+    spec.nx, spec.ny = nx, ny
+    spec.k_perm_cells = P.lognormal_field(P.K_SEED, nx * ny)
+    rp = oracle.RefProblem(spec.to_dict())
+    off, idx, val = rp.csr("B")
+    off = np.ascontiguousarray(off, np.int32)
+    idx = np.ascontiguousarray(idx, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    csr = _lib.CSR(rp.n_q, rp.n_p, len(val), off.ctypes.data_as(_lib.IP), idx.ctypes.data_as(_lib.IP),
+                   val.ctypes.data_as(_lib.DP))
+    dims = (ctypes.c_int * 2)()
+    _lib.check(_lib.lib().pdg_mesh_dims_from_operators(ctypes.byref(csr), rp.n_q, dims))
+    assert (dims[0], dims[1]) == (nx, ny)
