@@ -1036,12 +1036,33 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     PDG_CUDA(cudaStreamSynchronize(st));
     for (int k = 0; k < nf; ++k)
         if (hinfo[k] != 0) throw Error(PDG_NOT_CONVERGED, "nested dissection: front " + std::to_string(k) + " not positive definite");
+    // boundary dofs as pivot positions; buffers shared by both solve kernels
+    std::vector<int> hbp(hb.size());
+    for (size_t i = 0; i < hb.size(); ++i) hbp[i] = spos[hb[i]];
+    sdofs.upload(hs, st);
+    bpos.upload(hbp, st);
+    cbdst.upload(hcbdst, st);
+    counters.alloc((size_t)3 * nf);
+    counters.zero(st);
+    call = 0;
+    y.alloc((size_t)n * max_rhs);
+    xpos.alloc((size_t)n * max_rhs);
+    cbuf.alloc((size_t)std::max<long long>(cbtot, 1) * max_rhs);
+    cbuf.zero(st);  // slots no child writes stay zero
+    tiles = nd_tile_default();
+    if (tiles) {
+        build_tiles(children, parent, hs, hbp, hcbdst, st);
+        store.release();  // the tile store replaces the row-major one
+        return;
+    }
     // ---- solve schedule: tasks in topological order, contiguous per phase on the CTAs ----
     int dev = 0, nsm = 0;
     PDG_CUDA(cudaGetDevice(&dev));
     PDG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int task_chunks = 16;
-    pf = 16;
+    // no L2 prefetch cursor by default: measured 278 vs 291 us (pf 16) for the config-1
+    // displacement solve (tools/nd_sweep.sh, profiles/round2_nd_sweeps.txt)
+    pf = 0;
     if (const char* e = std::getenv("PDG_ND_PF")) pf = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("PDG_ND_CHUNKS")) task_chunks = std::max(1, std::atoi(e));
     stages = 16;
@@ -1091,6 +1112,34 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             if (F.depth == depth) by += 8.0 * (type == 1 ? (double)(F.s + F.b) * F.ldm : (double)F.s * F.ldt);
         return by;
     };
+    // subtree mapping: the fronts at depth >= local_depth form subtrees that run entirely on one
+    // CTA each (their dependencies stay inside the CTA, in task order); the levels above are
+    // spread over all CTAs. Default: the deepest level with no more fronts than CTAs.
+    int local_depth = maxdepth + 1;
+    {
+        std::vector<int> per_depth(maxdepth + 1, 0);
+        for (const auto& F : fronts) per_depth[F.depth]++;
+        for (int d = maxdepth; d >= 0; --d)
+            if (per_depth[d] <= grid) {
+                local_depth = d;
+                break;
+            }
+        if (const char* e = std::getenv("PDG_ND_LOCAL_DEPTH")) {
+            const int v = std::atoi(e);
+            local_depth = v < 0 ? maxdepth + 1 : std::min(v, maxdepth + 1);
+        }
+    }
+    std::vector<int> cta_of(nf, -1);  // CTA of a local front
+    {
+        std::vector<int> roots;
+        for (int k = 0; k < nf; ++k)
+            if (fronts[k].depth == local_depth) roots.push_back(k);
+        const int nr = static_cast<int>(roots.size());
+        for (int j = 0; j < nr; ++j) cta_of[roots[j]] = static_cast<int>((long long)j * grid / std::max(nr, 1));
+        for (int d = local_depth + 1; d <= maxdepth; ++d)
+            for (int k = 0; k < nf; ++k)
+                if (fronts[k].depth == d && parent[k] >= 0) cta_of[k] = cta_of[parent[k]];
+    }
     auto matrix_tasks = [&](int type, int depth) {
         std::vector<NdTask> ts;
         for (int k = 0; k < nf; ++k) {
@@ -1100,9 +1149,11 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             const int ld = type == 1 ? F.ldm : F.ldt;
             const long long base = type == 1 ? F.moff : F.mtoff;
             const int rpc = static_cast<int>(stage_bytes / (8u * ld));
-            // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks
+            // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks;
+            // a local front (one CTA runs its whole subtree) in as few tasks as the buffers allow
             const int want = static_cast<int>(std::ceil(level_bytes(type, depth) / grid / stage_bytes));
-            const int cap = std::min(kNdMaxTaskRows, rpc * std::max(1, std::min(task_chunks, want)));
+            const int cap = depth >= local_depth ? kNdMaxTaskRows
+                                                 : std::min(kNdMaxTaskRows, rpc * std::max(1, std::min(task_chunks, want)));
             for (int r0 = 0; r0 < rows; r0 += cap) {
                 NdTask t = base_task(k, type);
                 t.src = base + (long long)r0 * ld;
@@ -1144,8 +1195,21 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 t.need0 = fwd_tasks[t.front];
             }
         }
-    for (int d = maxdepth; d >= 0; --d) place(fwd_by_depth[d]);
-    for (int d = 0; d <= maxdepth; ++d) place(bwd_by_depth[d]);
+    auto place_local = [&](std::vector<NdTask>& ts) {
+        for (const auto& t : ts) per_cta[cta_of[t.front]].push_back(t);
+    };
+    for (int d = maxdepth; d >= 0; --d) {
+        if (d >= local_depth)
+            place_local(fwd_by_depth[d]);
+        else
+            place(fwd_by_depth[d]);
+    }
+    for (int d = 0; d <= maxdepth; ++d) {
+        if (d >= local_depth)
+            place_local(bwd_by_depth[d]);
+        else
+            place(bwd_by_depth[d]);
+    }
     max_tasks = 0;
     size_t max_buf = 0;
     for (auto& v : per_cta) {
@@ -1197,29 +1261,17 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
         hct[q + 1] = static_cast<int>(all.size());
     }
-    static size_t attr_smem = 0;  // one attribute for all instances: the largest
-    if (smem > attr_smem) {
+    // the attribute is per device and only ever raised: set the largest seen on this device
+    static size_t attr_smem[64] = {};
+    if (smem > attr_smem[dev % 64]) {
         PDG_CUDA(cudaFuncSetAttribute(k_nd_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr_smem = smem;
+        attr_smem[dev % 64] = smem;
     }
     int per_sm = 0;
     PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdBlock, smem));
     require(per_sm >= 1 && grid <= per_sm * nsm, "nested dissection: solve grid not co-resident");
-    // boundary dofs as pivot positions
-    std::vector<int> hbp(hb.size());
-    for (size_t i = 0; i < hb.size(); ++i) hbp[i] = spos[hb[i]];
     d_tasks.upload(all, st);
     ctoff.upload(hct, st);
-    sdofs.upload(hs, st);
-    bpos.upload(hbp, st);
-    cbdst.upload(hcbdst, st);
-    counters.alloc((size_t)3 * nf);
-    counters.zero(st);
-    call = 0;
-    y.alloc((size_t)n * max_rhs);
-    xpos.alloc((size_t)n * max_rhs);
-    cbuf.alloc((size_t)std::max<long long>(cbtot, 1) * max_rhs);
-    cbuf.zero(st);  // slots no child writes stay zero
     PDG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -1227,6 +1279,10 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
     ++call;
+    if (tiles) {
+        solve_tiles(b, ldb, x, ldx, nrhs, st);
+        return;
+    }
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,

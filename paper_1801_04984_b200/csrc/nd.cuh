@@ -59,6 +59,21 @@ struct NdTask {
     int pad_;
 };
 
+// One task of the tile-streaming solve (nd_tile.cu): rows [r0, r0 + nrows) of a
+// front pass (type 1: M, type 2: M^T), ntiles tiles of rb complete rows each at
+// tstore + src, the row output indices at toix + oix_off, the task buffer at byte
+// boff of the CTA's arena (free once CTA-local task fdep is done).
+struct NdTileTask {
+    long long src;
+    int type, front, r0, nrows, cp, ncols, rb, ntiles, tile_d2, kt, nchunks;  // kt tiles per ring chunk
+    int s, b, sdof, bdof, cboff, leaf;
+    int wait0, wait1, need0, need1, signal;
+    int oix_off, boff, fdep, tail_lo, tail_n;
+    int cgather;  // the compute warps gather the dependent inputs (shared levels)
+    int l2keep;   // tiles loaded with L2 evict_last (top levels)
+};
+bool nd_tile_default();
+
 struct NdChol {
     int n = 0, max_rhs = 0, nfront = 0, maxdepth = 0;
     int grid = 0, stages = 3, vmax = 0, max_tasks = 0, pf = 16;
@@ -84,6 +99,20 @@ struct NdChol {
                 int leaf_dofs, int max_rhs, cudaStream_t st);
     // x = A^{-1} b, nrhs <= max_rhs columns at strides ldb / ldx
     void solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+
+    // tile-streaming solve (nd_tile.cu, default)
+    bool tiles = false;
+    int tgrid = 0, tstages = 8, tmax_tasks = 0;
+    unsigned tstage_bytes = 32768;
+    size_t ttask_bytes = 0, tarena = 0, tsmem = 0;
+    double tile_bytes = 0.0;  // bytes of the tile store (the factor plus tile padding)
+    DBuf<double> tstore;
+    DBuf<NdTileTask> d_ttasks;
+    DBuf<int> tctoff, d_toix;
+    void build_tiles(const std::vector<std::vector<int>>& children, const std::vector<int>& parent,
+                     const std::vector<int>& hs, const std::vector<int>& hbp, const std::vector<int>& hcbdst,
+                     cudaStream_t st);
+    void solve_tiles(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };
 
