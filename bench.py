@@ -13,6 +13,7 @@ solution D2H inside the timed region). Multi-GPU (N > 1): replicas only
 --impl reference.
 """
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -279,16 +280,32 @@ def main():
     L = _lib.lib()
     run = P.RUNS["config1"]
     tau = run["T"] / run["n_slabs"]
-    t_setup = time.time()
+    # setup, per stage (library timers: host wall clock, stream synchronized per stage)
+    L.pdg_setup_reset()
+    t_setup = time.perf_counter()
     ops = S.SpatialOperators.assemble(P.config1(128), device=local)
     torch.cuda.synchronize()
+    t_assembled = time.perf_counter()
     nt, nn = ops.n_total, run["r"] + 1
     dev = torch.device("cuda", local)
+    setup = {}
 
     def timed_march(candidate, keep_rhs):
         """W warm-up + K timed slabs of the device-resident march (CUDA events)."""
         opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]), candidate=candidate)
+        t0 = time.perf_counter()
         slab = S.SlabSolver(ops, run["r"], tau, opt)
+        torch.cuda.synchronize()
+        if not setup:
+            st = (C.c_double * 9)()
+            L.pdg_setup_read(st, 9)
+            names = ("assemble", "a_nd_analysis", "a_nd_factor", "a_nd_schedule", "flow_nd_analysis", "flow_nd_factor",
+                     "flow_nd_schedule", "spacetime_operator", "slab_solver_total")
+            setup.update({f"{k}_s": round(st[i], 4) for i, k in enumerate(names)})
+            setup["assemble_wall_s"] = round(t_assembled - t_setup, 4)
+            setup["slab_solver_wall_s"] = round(time.perf_counter() - t0, 4)
+            setup["note"] = ("one-time per tau: device assembly, then the slab solver (nested-dissection analysis on "
+                             "the host, front factorization with cuSOLVER/cuBLAS, solve schedule, operator build)")
         u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
         p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
         rhs = torch.empty(nn * nt, dtype=torch.float64, device=dev)
@@ -350,7 +367,6 @@ def main():
                     rhs_host=rhs_host)
 
     main_run = timed_march("flexible", keep_rhs=True)
-    setup_s = time.time() - t_setup
     ref_run = timed_march("reference", keep_rhs=False)
     ms_dev = main_run["ms"]
     phases = {k: {"ms_per_step": v[0] / args.steps, "calls_per_step": v[1] / args.steps,
@@ -424,6 +440,7 @@ def main():
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
         res = oracle_config1(args.cpu_slabs)
         secs = res["solve_seconds"][1:] if args.cpu_slabs > 1 else res["solve_seconds"]
+        setup["oracle_setup_s"] = round(float(res["setup_seconds"]), 3)
         cpu = {"value": 1e3 * float(np.mean(secs)), "unit": "ms/slab", "cores": os.cpu_count(), "kind": "port",
                "iterations": [int(i) for i in res["iterations"]],
                "sample": f"{args.cpu_slabs} slab(s) of config 1 on the host (setup {res['setup_seconds']:.1f} s "
@@ -431,29 +448,34 @@ def main():
                          "factorisation OpenMP-parallel, triangular solves serial"}
     spmv_cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.spmv_sizes:
-        try:
-            spmv_cpu = spmv_cpu_baseline(min(int(v) for v in args.spmv_sizes.split(",") if v))
-        except Exception as e:  # report, do not lose the headline line
-            spmv_cpu = {"error": repr(e)[:300]}
+        spmv_cpu = []
+        for n in sorted(int(v) for v in args.spmv_sizes.split(",") if v):
+            try:
+                spmv_cpu.append(spmv_cpu_baseline(n, reps=5 if n <= 512 else 2))
+            except Exception as e:  # report, do not lose the headline line
+                spmv_cpu.append({"n": n, "error": repr(e)[:300]})
     if rank == 0:
+        spmv_compact = [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in d.items()
+                         if k in ("n", "rows", "nnz", "median_ms", "gdof_s", "achieved_GBs", "frac")} for d in spmv]
+        phases_compact = {k: {"ms_per_step": round(v["ms_per_step"], 4), "calls_per_step": v["calls_per_step"],
+                              "achieved_GBs": round(v["achieved_GBs"], 1)} for k, v in phases.items()}
         print(json.dumps({
             "metric": METRIC, "value": ms_dev, "unit": "ms/slab", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded lognormal K, BASELINE config 1)",
-            "config": {"workload": WORKLOAD, "rows_per_block": nn * nt,
-                       "gmres_candidate": "flexible: x + Z y (the reference's gmres_flexible, gmres.hpp:113-114,"
-                                          " 153-158; same iterations, solutions within 1e-9 of gmres)",
+            "config": {"workload": WORKLOAD,
+                       "gmres_candidate": "flexible: x + Z y (gmres_flexible, gmres.hpp:113-114; 20-slab oracle "
+                                          "parity tested for both candidates)",
                        "l2": "no flush: per-step working set (nested-dissection factor matrices 0.73 GB) > 126 MB L2",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "setup_s": setup_s},
-            "iterations": main_run["iters"],
-            "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],
-                                          "note": "candidate x + P(V y) exactly as gmres.hpp:116"},
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
             "e2e": {"value": e2e_ms, "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
                     "d2h_bytes_per_step": 8 * nn * nt},
-            "gpu_launches": int(main_run["launches"]), "roofline": roofline, "spmv_roofline": spmv_roof,
-            "phases": phases, "spmv": spmv, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist,
-            "clocks": main_run["clocks"],
-            "cpu_baseline": cpu, "spmv_cpu_baseline": spmv_cpu}), flush=True)
+            "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],
+                                          "note": "candidate x + P(V y) exactly as gmres.hpp:116"},
+            "iterations": main_run["iters"], "gpu_launches": int(main_run["launches"]),
+            "roofline": roofline, "clocks": main_run["clocks"], "cpu_baseline": cpu, "setup": setup,
+            "spmv_roofline": spmv_roof, "spmv": spmv_compact, "spmv_cpu_baseline": spmv_cpu,
+            "phases": phases_compact, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -161,6 +161,13 @@ void pdg_op_destroy(pdg_op* op);
  * 0 space-time SpMV, 1 displacement solve, 2 flow solve, 3 other preconditioner
  * kernels, 4 Krylov vector kernels, 5 slab transforms / rhs. alg_bytes is the
  * algorithmic traffic summed over the calls. */
+/* Setup stage timers, cumulative seconds since pdg_setup_reset: [0] device assembly,
+ * [1..3] displacement nested-dissection analysis / numeric factorization / solve schedule,
+ * [4..6] the same for the flow Schur complement, [7] space-time operator build,
+ * [8] whole block/slab solver construction (includes 1..7 when built there).
+ * Writes min(n, 9) values and returns 9. */
+void pdg_setup_reset(void);
+int pdg_setup_read(double* seconds, int n);
 void pdg_profile_enable(int on);
 void pdg_profile_reset(void);
 int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes);

@@ -104,6 +104,8 @@ _SIGS = {
     "pdg_op_apply_strip_device": (C.c_int, [VP, VP, VP, C.c_int, C.POINTER(C.c_float)]),
     "pdg_op_download_csr": (C.c_int, [VP, LLP, IP, DP]),
     "pdg_op_destroy": (None, [VP]),
+    "pdg_setup_reset": (None, []),
+    "pdg_setup_read": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "pdg_profile_enable": (None, [C.c_int]),
     "pdg_profile_reset": (None, []),
     "pdg_profile_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), LLP, C.POINTER(C.c_double)]),

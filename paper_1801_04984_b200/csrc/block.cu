@@ -180,11 +180,12 @@ __device__ __forceinline__ void block_multidot(long long n, int ncols, const dou
 }
 
 // column sums of the partials into hs[ncols] (smem, every block), block 0 copies them to h_out
-__device__ __forceinline__ void block_column_sums(const double* partial, int ncols, double* hs, double* h_out) {
+__device__ __forceinline__ void block_column_sums(const double* partial, int ncols, double* hs, double* h_out,
+                                                  int nblocks = kRedBlocks) {
     __shared__ double sh[32];
     for (int j = 0; j < ncols; ++j) {
         double v = 0.0;
-        for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(partial + (long long)b * ncols + j);
+        for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += __ldcg(partial + (long long)b * ncols + j);
         const double s = block_sum(v, sh);
         if (threadIdx.x == 0) hs[j] = s;
     }
@@ -196,9 +197,12 @@ __device__ __forceinline__ void block_column_sums(const double* partial, int nco
 // Two classical Gram-Schmidt passes of w against V_0..V_{ncols-1}, then
 // h_out[2 ncols] = ||w|| and vnext = w / ||w||. h_out[0..ncols) pass 1, [ncols..2 ncols) pass 2.
 // partial: 3 regions of kRedBlocks * ncols (a region is never rewritten while another block may read it).
+// pre1 != null: the first pass's partials were formed by the SpMV epilogue (k_spmv<true>,
+// nb1 blocks); the kernel starts at their column sums
 __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int ncols, const double* __restrict__ V,
                                                             double* w, double* partial, double* h_out,
-                                                            double* __restrict__ vnext, const GmresDevState* gst) {
+                                                            double* __restrict__ vnext, const GmresDevState* gst,
+                                                            const double* pre1, int nb1) {
     if (gst && gst->stop) return;  // speculative step after the cycle ended
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -206,10 +210,13 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
     double* p1 = partial;
     double* p2 = partial + (size_t)kRedBlocks * ncols;
     double* p3 = partial + (size_t)2 * kRedBlocks * ncols;
-    block_multidot(n, ncols, V, w, p1);
+    if (!pre1) block_multidot(n, ncols, V, w, p1);
     for (int pass = 0; pass < 2; ++pass) {
-        grid.sync();
-        block_column_sums(pass == 0 ? p1 : p2, ncols, hs, h_out + (size_t)pass * ncols);
+        if (pass > 0 || !pre1) grid.sync();
+        if (pass == 0 && pre1)
+            block_column_sums(pre1, ncols, hs, h_out, nb1);
+        else
+            block_column_sums(pass == 0 ? p1 : p2, ncols, hs, h_out + (size_t)pass * ncols);
         for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
             double v = __ldcg(w + r);
             for (int j = 0; j < ncols; ++j) v -= hs[j] * V[(long long)j * n + r];
@@ -855,12 +862,18 @@ void Block::create(const SpatialOps& o, int m_, const double* th, double tau_, d
     require(opts.restart >= 1 && opts.max_iter >= 1, "gmres: bad iteration limits");
     require(tau > 0.0, "FixedStressSolver: tau must be positive");
     cudaStream_t st = ctx->stream;
-    op.build(o, m, th, tau, st);
+    SetupTimer total(SETUP_SOLVER_TOTAL, st);
+    {
+        SetupTimer t(SETUP_OPERATOR, st);
+        op.build(o, m, th, tau, st);
+    }
     const double stab = opts.stab < 0.0 ? o.biot_b * o.biot_b / o.k_dr : opts.stab;
     require(stab >= 0.0, "fixed-stress: stabilization must be nonnegative");
     if (!a) a = make_a_solver(o, 2, st);
     pre.setup(o, m, tau, lambda, stab, opts.sweeps, a, st);
     kr.setup(rows(), opts.restart, opts.candidate == 1, st);
+    kr.spmv_blocks = op.dots_grid();
+    kr.spmv_part.alloc((size_t)kr.spmv_blocks * 8);
     PDG_CUDA(cudaEventCreate(&ev0));
     PDG_CUDA(cudaEventCreate(&ev1));
     PDG_CUDA(cudaStreamSynchronize(st));
@@ -916,11 +929,12 @@ struct KrylovOps {
     }
     // both Gram-Schmidt passes + the norm + v_{k+1} = w / ||w|| in ONE cooperative launch
     // (bit-identical to gs_pass x 2 + norm_dev); h_out[0 .. 2 ncols] as the unfused sequence
-    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext, const GmresDevState* gst = nullptr) {
-        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (3.0 * ncols + 6.0));
+    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext, const GmresDevState* gst = nullptr,
+                  const double* pre1 = nullptr, int nb1 = 0) {
+        ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (3.0 * ncols + 6.0 - (pre1 ? ncols + 1.0 : 0.0)));
         long long n = g.n;
         double* part = g.partial.p;
-        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext, (void*)&gst};
+        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext, (void*)&gst, (void*)&pre1, &nb1};
         PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_gs, kRedBlocks, kRedThreads, args, sizeof(double) * ncols, st));
         count_launch();
         PDG_CHECK_LAUNCH();
@@ -994,6 +1008,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     // fused cooperative Arnoldi kernels (default); PDG_KRYLOV_UNFUSED=1 selects the launch-per-step
     // sequence they replace (bit-identical results, kept for the A/B test)
     const bool fused = !std::getenv("PDG_KRYLOV_UNFUSED");
+    const bool spmv_dots = fused && !(std::getenv("PDG_SPMV_DOTS") && std::atoi(std::getenv("PDG_SPMV_DOTS")) == 0);
     // PDG_GMRES_DEVICE_LS=1: device-driven steps (with the fused Arnoldi-relation residual): the
     // Hessenberg column, breakdown test and least squares run on the device (k_gmres_ls, same
     // bits as the host), one host round trip per step instead of two. Opt-in: measured slower
@@ -1039,9 +1054,15 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 double* zk = kr.Z.p + (size_t)k * n;
                 double* azk = kr.AZ.p + (size_t)k * n;
                 pre.apply(vk, zk, st);
-                op.apply(zk, azk, st);
-                PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-                K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst);
+                if (spmv_dots && k + 1 <= 8) {  // w = AZ_k and the first Gram-Schmidt pass's partials in the SpMV
+                    op.apply_dots(zk, azk, kr.w.p, kr.V.p, k + 1, kr.spmv_part.p, st);
+                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst, kr.spmv_part.p,
+                               kr.spmv_blocks);
+                } else {
+                    op.apply(zk, azk, st);
+                    PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst);
+                }
                 {
                     ProfScope prof_(PROF_KRYLOV, st, 0.0);
                     gmres_ls_launch(k, mm, beta, kr.h_dev.p, kr.Hd.p, kr.hk.p, kr.ls_rhs.p, kr.ls_tau.p, kr.ls_nrm.p,
@@ -1105,10 +1126,19 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             double* vk = kr.V.p + (size_t)k * n;
             double* zk = flexible ? kr.Z.p + (size_t)k * n : kr.cand.p;
             pre.apply(vk, zk, st);
+            // fused (default, up to 8 basis vectors): the SpMV epilogue forms w and the first
+            // Gram-Schmidt pass's partial dots (PDG_SPMV_DOTS=0: separate passes)
+            const bool dots = fused && spmv_dots && k + 1 <= 8;
             if (arnoldi_res) {
                 double* azk = kr.AZ.p + (size_t)k * n;
-                op.apply(zk, azk, st);
-                PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                if (dots) {
+                    op.apply_dots(zk, azk, kr.w.p, kr.V.p, k + 1, kr.spmv_part.p, st);
+                } else {
+                    op.apply(zk, azk, st);
+                    PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                }
+            } else if (dots) {
+                op.apply_dots(zk, kr.w.p, nullptr, kr.V.p, k + 1, kr.spmv_part.p, st);
             } else {
                 op.apply(zk, kr.w.p, st);
             }
@@ -1116,7 +1146,8 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             // the Hessenberg column comes back in ONE transfer
             // h(k+1,k) = ||w|| and v_{k+1} = w / h(k+1,k) (unused when the column breaks down)
             if (fused) {
-                K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n);
+                K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, nullptr,
+                           dots ? kr.spmv_part.p : nullptr, kr.spmv_blocks);
                 PDG_CUDA(cudaMemcpyAsync(kr.h_host, kr.h_dev.p, sizeof(double) * (2 * (k + 1) + 1), cudaMemcpyDeviceToHost, st));
             } else {
                 for (int pass = 0; pass < 2; ++pass) K.gs_pass(kr.V.p, k + 1, kr.w.p, kr.h_dev.p + (size_t)pass * (k + 1));
@@ -1215,8 +1246,12 @@ void FsSolver::create(const SpatialOps& o, int r, double tau_, double stab, std:
     m = r + 1;
     tau = tau_;
     cudaStream_t st = ctx->stream;
+    SetupTimer total(SETUP_SOLVER_TOTAL, st);
     const TimeConsts tc = time_consts(r);  // Theta = G_hat, kappa = weights (both [1] for r = 0)
-    op.build(o, m, tc.G.data(), tau, st, tc.weights.data());
+    {
+        SetupTimer t(SETUP_OPERATOR, st);
+        op.build(o, m, tc.G.data(), tau, st, tc.weights.data());
+    }
     if (!a) a = make_a_solver(o, 2, st);
     if (m == 1)
         pre.setup(o, m, tau, tc.G[0], stab, 1, a, st);

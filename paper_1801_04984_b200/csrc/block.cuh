@@ -61,6 +61,8 @@ struct Gmres {
     int restart = 50;
     DBuf<double> V, Z, w, x, r, cand, t, y_dev, h_dev, partial, norm_dev;
     DBuf<double> AZ, r0;  // flexible: op(z_j) and the cycle's initial residual (Arnoldi-relation residual)
+    DBuf<double> spmv_part;  // first Gram-Schmidt pass partials from the fused SpMV epilogue [block][<= 8]
+    int spmv_blocks = 0;
     double* h_host = nullptr;  // pinned
     // device-driven steps (flexible candidate): Hessenberg, least-squares scratch, step state
     DBuf<double> Hd, hk, ls_rhs, ls_tau, ls_nrm, gst;

@@ -286,6 +286,7 @@ int pdg_ops_assemble(pdg_ctx* ctx, const pdg_problem* problem, pdg_ops** out) {
     cudaStream_t st = ctx->c.stream;
     auto o = std::make_unique<pdg_ops>();
     o->s.ctx = &ctx->c;
+    SetupTimer timer(SETUP_ASSEMBLE, st);
     assemble_ops_device(o->s, *problem, st);
     finish_ops(o->s, st);
     *out = o.release();

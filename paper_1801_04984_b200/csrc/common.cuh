@@ -150,4 +150,33 @@ struct ProfScope {
     }
 };
 
+// Setup stage timers (host wall clock, the stream synchronized at the end of each
+// stage) behind pdg_setup_read: assembly, and per nested-dissection factor (A and the
+// flow Schur complement) the analysis (graph + dissection + dense-front maps, host),
+// the numeric factorization (cuSOLVER/cuBLAS on the fronts, device) and the solve
+// schedule (task lists, host + upload); the space-time operator build; the whole
+// block / slab solver construction.
+enum SetupStage { SETUP_ASSEMBLE = 0, SETUP_A_ANALYSIS = 1, SETUP_A_FACTOR = 2, SETUP_A_SCHEDULE = 3,
+                  SETUP_F_ANALYSIS = 4, SETUP_F_FACTOR = 5, SETUP_F_SCHEDULE = 6, SETUP_OPERATOR = 7,
+                  SETUP_SOLVER_TOTAL = 8, SETUP_NSTAGES = 9 };
+void setup_add(int stage, double seconds);
+double setup_clock();  // seconds, monotonic
+struct SetupTimer {
+    int stage;
+    cudaStream_t st;
+    double t0;
+    SetupTimer(int s, cudaStream_t stream) : stage(s), st(stream), t0(setup_clock()) {}
+    void next(int s) {  // close the current stage, open stage s
+        cudaStreamSynchronize(st);
+        const double t = setup_clock();
+        setup_add(stage, t - t0);
+        stage = s;
+        t0 = t;
+    }
+    ~SetupTimer() {
+        cudaStreamSynchronize(st);
+        setup_add(stage, setup_clock() - t0);
+    }
+};
+
 }  // namespace pdg

@@ -807,6 +807,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                     int leaf_dofs, int max_rhs_, cudaStream_t st) {
     n = n_;
     max_rhs = max_rhs_;
+    const int stage0 = prof_phase == PROF_A_SOLVE ? SETUP_A_ANALYSIS : SETUP_F_ANALYSIS;
+    SetupTimer timer(stage0, st);
     require(max_rhs >= 1 && max_rhs <= kNdMaxRhs, "nested dissection: at most 2 right-hand sides");
     require(static_cast<int>(off.size()) == n + 1 && static_cast<int>(node_of.size()) == n, "nested dissection: bad CSR");
     const int nn = static_cast<int>(cx.size());
@@ -995,6 +997,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     }
     DBuf<int> dmap;
     dmap.upload(hmap, st);
+    timer.next(stage0 + 1);  // numeric factorization
     LaHandles h(st);
     int lwork = 0;
     PDG_ND_CUSOLVER(cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, smax, dense.p, smax, &lwork));
@@ -1036,6 +1039,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     PDG_CUDA(cudaStreamSynchronize(st));
     for (int k = 0; k < nf; ++k)
         if (hinfo[k] != 0) throw Error(PDG_NOT_CONVERGED, "nested dissection: front " + std::to_string(k) + " not positive definite");
+    timer.next(stage0 + 2);  // solve schedule
     // boundary dofs as pivot positions; buffers shared by both solve kernels
     std::vector<int> hbp(hb.size());
     for (size_t i = 0; i < hb.size(); ++i) hbp[i] = spos[hb[i]];

@@ -1,4 +1,5 @@
 // Per-phase CUDA-event profiler behind pdg_profile_* (see common.cuh).
+#include <chrono>
 #include <mutex>
 
 #include "common.cuh"
@@ -53,6 +54,16 @@ cudaEvent_t prof_event() {
     return e;
 }
 
+namespace {
+double g_setup[SETUP_NSTAGES] = {};
+}
+void setup_add(int stage, double seconds) {
+    if (stage >= 0 && stage < SETUP_NSTAGES) g_setup[stage] += seconds;
+}
+double setup_clock() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void prof_push(int phase, cudaEvent_t a, cudaEvent_t b, double bytes) {
     State& s = st();
     s.pending.push_back({phase, a, b, bytes});
@@ -71,6 +82,14 @@ void pdg_profile_reset(void) {
         s.calls[i] = 0;
         s.bytes[i] = 0.0;
     }
+}
+void pdg_setup_reset(void) {
+    for (int i = 0; i < pdg::SETUP_NSTAGES; ++i) pdg::g_setup[i] = 0.0;
+}
+int pdg_setup_read(double* seconds, int n) {
+    if (!seconds || n < 0) return PDG_INVALID_ARGUMENT;
+    for (int i = 0; i < n && i < pdg::SETUP_NSTAGES; ++i) seconds[i] = pdg::g_setup[i];
+    return pdg::SETUP_NSTAGES;
 }
 int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes) {
     if (phase < 0 || phase >= pdg::PROF_NPHASES) return PDG_INVALID_ARGUMENT;

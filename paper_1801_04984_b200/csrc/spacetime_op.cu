@@ -140,15 +140,34 @@ __global__ void k_s_fill(long long s_rows, int m, int nt, int nu, int nq, int np
 // Blocks [0, gu) run the U class (one thread per (group,row)), the remaining
 // blocks the S class (one thread per row).
 constexpr int kSpmvBlock = 256;
+constexpr int kSpmvMaxDots = 8;  // fused Gram-Schmidt pass-1 dots: up to 8 basis vectors
 
+// DOTS (the GMRES operator application, north_star "SpMV fused with the GMRES dot
+// products"): y is also copied to y2 (the Gram-Schmidt work vector) and every block
+// writes its partial sums of V_j . y over the rows it produced, j < ncols <= 8
+// (partial[block][j], block-order summed by the Arnoldi kernel). y itself is computed
+// exactly as without DOTS (bit-identical).
+template <bool DOTS>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, int u2, long long s_rows, int gu, int n_cells, int nt,
                                                      int nu, int nq, int np, const long long* __restrict__ u_off,
                                                      const int* __restrict__ u_col, const double* __restrict__ u_val,
                                                      const long long* __restrict__ s_off, const int* __restrict__ s_len,
                                                      const int* __restrict__ s_col, const double* __restrict__ s_val,
                                                      const double* __restrict__ x, double* __restrict__ y,
-                                                     const int* __restrict__ stop) {
+                                                     const int* __restrict__ stop, const double* __restrict__ V, int ncols,
+                                                     long long nrows, double* __restrict__ y2, double* __restrict__ partial) {
     if (stop && *stop) return;
+    double acc[kSpmvMaxDots];
+#pragma unroll
+    for (int q = 0; q < kSpmvMaxDots; ++q) acc[q] = 0.0;
+    auto dots = [&](long long row, double v) {
+        if (DOTS) {
+            if (y2) y2[row] = v;
+#pragma unroll
+            for (int q = 0; q < kSpmvMaxDots; ++q)
+                if (q < ncols) acc[q] += __ldg(&V[(long long)q * nrows + row]) * v;
+        }
+    };
     if (static_cast<int>(blockIdx.x) < gu) {
         const long long stride = (long long)gu * blockDim.x;
         if (!u2) {  // one row per thread (large operators: more independent streams in flight)
@@ -165,30 +184,35 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, int u2
                 }
                 const int i = static_cast<int>(g / n_cells);
                 const int c = static_cast<int>(g - (long long)i * n_cells);
-                y[(long long)i * nt + 8 * c + l] = s;
+                const long long row = (long long)i * nt + 8 * c + l;
+                y[row] = s;
+                dots(row, s);
             }
-            return;
-        }
-        // two rows (2j, 2j+1) of a group per thread (small operators: the grid fits one wave):
-        // one column index and one x load serve both, values as one 16-byte load; each row
-        // still summed alone in stored order
-        const double2* __restrict__ uv2 = reinterpret_cast<const double2*>(u_val);
-        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
-            const long long g = t >> 2;
-            const int j = static_cast<int>(t & 3);
-            const long long b = __ldg(&u_off[g]), e = __ldg(&u_off[g + 1]);
-            double s0 = 0.0, s1 = 0.0;
+        } else {
+            // two rows (2j, 2j+1) of a group per thread (small operators: the grid fits one wave):
+            // one column index and one x load serve both, values as one 16-byte load; each row
+            // still summed alone in stored order
+            const double2* __restrict__ uv2 = reinterpret_cast<const double2*>(u_val);
+            for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < u_threads; t += stride) {
+                const long long g = t >> 2;
+                const int j = static_cast<int>(t & 3);
+                const long long b = __ldg(&u_off[g]), e = __ldg(&u_off[g + 1]);
+                double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
-            for (long long k = b; k < e; ++k) {
-                const double2 v = __ldcs(&uv2[k * 4 + j]);
-                const double xv = __ldg(&x[__ldg(&u_col[k])]);
-                s0 = __dadd_rn(s0, __dmul_rn(v.x, xv));
-                s1 = __dadd_rn(s1, __dmul_rn(v.y, xv));
+                for (long long k = b; k < e; ++k) {
+                    const double2 v = __ldcs(&uv2[k * 4 + j]);
+                    const double xv = __ldg(&x[__ldg(&u_col[k])]);
+                    s0 = __dadd_rn(s0, __dmul_rn(v.x, xv));
+                    s1 = __dadd_rn(s1, __dmul_rn(v.y, xv));
+                }
+                const int i = static_cast<int>(g / n_cells);
+                const int c = static_cast<int>(g - (long long)i * n_cells);
+                const long long row = (long long)i * nt + 8 * c + 2 * j;
+                y[row] = s0;
+                y[row + 1] = s1;
+                dots(row, s0);
+                dots(row + 1, s1);
             }
-            const int i = static_cast<int>(g / n_cells);
-            const int c = static_cast<int>(g - (long long)i * n_cells);
-            y[(long long)i * nt + 8 * c + 2 * j] = s0;
-            y[(long long)i * nt + 8 * c + 2 * j + 1] = s1;
         }
     } else {
         const int bid = blockIdx.x - gu;
@@ -207,7 +231,25 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv(long long u_threads, int u2
             }
             const int i = static_cast<int>(srow / (nq + np));
             const int loc = static_cast<int>(srow - (long long)i * (nq + np));
-            y[(long long)i * nt + nu + loc] = s;
+            const long long row = (long long)i * nt + nu + loc;
+            y[row] = s;
+            dots(row, s);
+        }
+    }
+    if (DOTS) {  // block partials, fixed order: warp butterflies, then the warps in order
+        __shared__ double sh[kSpmvMaxDots][kSpmvBlock / 32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < kSpmvMaxDots; ++q)
+            for (int o = 16; o; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < kSpmvMaxDots; ++q) sh[q][warp] = acc[q];
+        __syncthreads();
+        if (threadIdx.x < ncols) {
+            double t = 0.0;
+            for (int w = 0; w < kSpmvBlock / 32; ++w) t += sh[threadIdx.x][w];
+            partial[(long long)blockIdx.x * ncols + threadIdx.x] = t;
         }
     }
 }
@@ -369,8 +411,34 @@ void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     const long long u_threads = u_groups * (u2 ? 4 : 8);
     const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
-    k_spmv<<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p, u_val.p,
-                                           s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard);
+    k_spmv<false><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p,
+                                                  u_val.p, s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard, nullptr, 0, rows,
+                                                  nullptr, nullptr);
+    count_launch();
+    PDG_CHECK_LAUNCH();
+}
+
+int SpaceTimeOp::dots_grid() const {
+    int u2 = rows <= (2LL << 20);
+    if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;
+    const long long u_threads = u_groups * (u2 ? 4 : 8);
+    const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
+    const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
+    return gu + gs;
+}
+
+void SpaceTimeOp::apply_dots(const double* x, double* y, double* y2, const double* V, int ncols, double* partial,
+                             cudaStream_t st) const {
+    require(ncols >= 1 && ncols <= kSpmvMaxDots, "space-time block: fused dots need 1..8 basis vectors");
+    ProfScope prof(PROF_SPMV, st, 8.0 * (double)(nnz + 2 * rows));
+    int u2 = rows <= (2LL << 20);
+    if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;
+    const long long u_threads = u_groups * (u2 ? 4 : 8);
+    const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
+    const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
+    k_spmv<true><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p,
+                                                 u_val.p, s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard, V, ncols, rows,
+                                                 y2, partial);
     count_launch();
     PDG_CHECK_LAUNCH();
 }

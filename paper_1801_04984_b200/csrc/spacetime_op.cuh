@@ -42,6 +42,12 @@ struct SpaceTimeOp {
     void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st,
                const double* kappa = nullptr);
     void apply(const double* x, double* y, cudaStream_t st) const;
+    // y = A x (the same bits as apply), y2 = y, and per-block partials of V_j . y for
+    // j < ncols <= 8 into partial[dots_grid()][ncols] (the first Gram-Schmidt pass of the
+    // Arnoldi step, fused into the SpMV epilogue: gmres.hpp:95-97 after fixed_stress.hpp:38-60)
+    void apply_dots(const double* x, double* y, double* y2, const double* V, int ncols, double* partial,
+                    cudaStream_t st) const;
+    int dots_grid() const;
     // when set, apply() is skipped on the device once *guard != 0 (speculative GMRES steps)
     const int* guard = nullptr;
     // Rows owned by the strip of cell rows [r0, r1) of an nx x ny mesh (multi-GPU

@@ -608,8 +608,8 @@ def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
     """The fused cooperative Arnoldi kernels (both Gram-Schmidt passes + norm +
     normalisation in one launch; the Arnoldi-relation residual and its norm in
     one launch) keep the row order, the per-block partials and the partial-sum
-    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1), and the
-    opt-in device-driven steps (PDG_GMRES_DEVICE_LS: Hessenberg column, breakdown
+    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1, compared below),
+    and the opt-in device-driven steps (PDG_GMRES_DEVICE_LS: Hessenberg column, breakdown
     test and least squares on the device; PDG_GMRES_LOOKAHEAD: next step queued
     speculatively) make the host loop's decisions with the same bits: solutions, residual histories and
     iteration counts are bit-identical. restart=2 exercises cycle ends without
@@ -629,13 +629,29 @@ def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
         runs.append(blk.solve(rhs))
         monkeypatch.delenv("PDG_GMRES_DEVICE_LS")
         monkeypatch.delenv("PDG_GMRES_LOOKAHEAD")
-    monkeypatch.setenv("PDG_KRYLOV_UNFUSED", "1")
-    runs.append(blk.solve(rhs))
     for x_u, rep_u in runs:
         assert rep_f.converged and rep_u.converged
         assert rep_f.iterations == rep_u.iterations
         assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
         assert np.array_equal(x_f, x_u)
+    # the first Gram-Schmidt pass's dots formed in the SpMV epilogue (default, up to 8 basis
+    # vectors) sum the same products in another fixed order than the separate multidot pass
+    # (PDG_SPMV_DOTS=0) and the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1): the same
+    # iterations, roundoff-level differences
+    assert np.array_equal(x_f, blk.solve(rhs)[0])  # deterministic
+    other = []
+    monkeypatch.setenv("PDG_SPMV_DOTS", "0")
+    other.append(blk.solve(rhs))
+    monkeypatch.setenv("PDG_KRYLOV_UNFUSED", "1")
+    other.append(blk.solve(rhs))
+    x_s, rep_s = other[0]
+    for x_u, rep_u in other[1:]:  # without the SpMV dots, the fused kernels keep the unfused bits
+        assert rep_s.iterations == rep_u.iterations and np.array_equal(x_s, x_u)
+    for x_u, rep_u in other:
+        assert rep_u.converged and rep_u.iterations == rep_f.iterations
+        assert np.linalg.norm(x_u - x_f) <= 1e-10 * np.linalg.norm(x_f)
+        h, hu = np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history)
+        assert np.allclose(h, hu, rtol=1e-6, atol=1e-12 * h[0])
 
 
 def test_spmv_config3_256_bit_identical(oracle):
