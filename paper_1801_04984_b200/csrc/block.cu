@@ -4,13 +4,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
 
 #include "block.cuh"
-#include "gmres_ls.cuh"
+#include "gmres_ls.cuh"  // ls_colpiv_raw (host least squares)
 #include "timebasis.hpp"
 
 namespace pdg {
@@ -199,11 +200,54 @@ __device__ __forceinline__ void block_column_sums(const double* partial, int nco
 // partial: 3 regions of kRedBlocks * ncols (a region is never rewritten while another block may read it).
 // pre1 != null: the first pass's partials were formed by the SpMV epilogue (k_spmv<true>,
 // nb1 blocks); the kernel starts at their column sums
+// Device-driven GMRES steps (LoopState, flexible candidate): after the norm, block 0 stores
+// the Hessenberg column H(0..k+1, k) = (0 + pass 1) + pass 2, ||w|| (as the host assembles
+// it) into Hcol, runs the breakdown test of gmres.hpp:103, applies the cycle's Givens
+// rotations and forms the next one; |g_{k+1}| = || beta e1 - H y || is the step's residual
+// estimate. stop = estimate <= tol ||b|| || breakdown || last step of the cycle.
+struct LoopState {
+    int stop, brk;
+    double res;
+};
+__device__ __forceinline__ void givens_step(int k, int mm, const double* h1, const double* h2, double nv,
+                                            double* Hcol, double* cs, double* sn, double* g, double tolb,
+                                            LoopState* ls) {
+    double cn = 0.0;
+    for (int i = 0; i <= k; ++i) {
+        const double v = (0.0 + h1[i]) + h2[i];
+        Hcol[i] = v;
+        cn += v * v;
+    }
+    Hcol[k + 1] = nv;
+    cn += nv * nv;
+    const int brk = nv <= 1e-14 * sqrt(cn);
+    // rotate the column by the previous rotations, then annihilate H(k+1, k)
+    double hk = Hcol[0];
+    for (int i = 0; i < k; ++i) {
+        const double hn = Hcol[i + 1];
+        const double t = cs[i] * hk + sn[i] * hn;
+        hk = -sn[i] * hk + cs[i] * hn;
+        (void)t;
+    }
+    // (the rotated entries above the diagonal are not needed: only the residual estimate is)
+    const double r = hypot(hk, nv);
+    const double c = r == 0.0 ? 1.0 : hk / r, sg = r == 0.0 ? 0.0 : nv / r;
+    cs[k] = c;
+    sn[k] = sg;
+    g[k + 1] = -sg * g[k];
+    g[k] = c * g[k];
+    const double res = fabs(g[k + 1]);
+    ls->res = res;
+    ls->brk = brk;
+    ls->stop = (res <= tolb) || brk || (k == mm - 1);
+}
+
 __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int ncols, const double* __restrict__ V,
                                                             double* w, double* partial, double* h_out,
-                                                            double* __restrict__ vnext, const GmresDevState* gst,
-                                                            const double* pre1, int nb1) {
-    if (gst && gst->stop) return;  // speculative step after the cycle ended
+                                                            double* __restrict__ vnext, LoopState* ls,
+                                                            const double* pre1, int nb1, double* Hcol, double* cs,
+                                                            double* sn, double* g, int mm, double tolb) {
+    if (ls && ls->stop) return;  // speculative step after the cycle ended
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double hs[];  // [ncols]
@@ -238,7 +282,10 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
         const double s = block_sum(v, sh);
         if (threadIdx.x == 0) nv = sqrt(s);
         __syncthreads();
-        if (blockIdx.x == 0 && threadIdx.x == 0) h_out[2 * ncols] = nv;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            h_out[2 * ncols] = nv;
+            if (ls) givens_step(ncols - 1, mm, h_out, h_out + ncols, nv, Hcol, cs, sn, g, tolb, ls);
+        }
         const double d = nv;
         for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
             vnext[r] = __ldcg(w + r) / d;
@@ -249,11 +296,7 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
 __global__ void __launch_bounds__(kRedThreads) k_arnoldi_residual(long long n, int ncols, const double* __restrict__ AZ,
                                                                   const double* __restrict__ y,
                                                                   const double* __restrict__ r0, double* r,
-                                                                  double* partial, double* nrm_out, GmresDevState* gst,
-                                                                  double bnorm, double tol) {
-    // gst (device-driven steps): skipped once the cycle ended; sets the step's residual and
-    // the stop decision ok || breakdown (gmres.hpp:68-72, :103) for the next step's kernels
-    if (gst && gst->stop) return;
+                                                                  double* partial, double* nrm_out) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
@@ -279,14 +322,7 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_residual(long long n, i
     if (blockIdx.x == 0) {
         for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(partial + b);
         const double s = block_sum(v, sh);
-        if (threadIdx.x == 0) {
-            const double res = sqrt(s);
-            *nrm_out = res;
-            if (gst) {
-                gst->res = res;
-                gst->stop = (res / bnorm <= tol) || gst->brk;
-            }
-        }
+        if (threadIdx.x == 0) *nrm_out = sqrt(s);
     }
 }
 
@@ -830,13 +866,9 @@ void Gmres::setup(long long n_, int restart_, bool keep_z, cudaStream_t st) {
     if (!h_host) PDG_CUDA(cudaMallocHost(&h_host, sizeof(double) * (2 * restart + 8)));
     if (keep_z) {
         Hd.alloc((size_t)(restart + 1) * restart);
-        hk.alloc((size_t)(restart + 2) * (restart + 1));
-        ls_rhs.alloc(restart + 2);
-        ls_tau.alloc(restart + 1);
-        ls_nrm.alloc(restart + 1);
-        ls_piv.alloc(restart + 1);
-        gst.alloc(2);  // one GmresDevState
-        if (!h_slots) PDG_CUDA(cudaMallocHost(&h_slots, sizeof(GmresDevState) * (restart + 1)));
+        lstate.alloc(2);  // one LoopState
+        givens.alloc((size_t)3 * (restart + 1));  // cs, sn, g
+        if (!h_slots) PDG_CUDA(cudaMallocHost(&h_slots, sizeof(LoopState) * (restart + 1)));
         for (auto& e : evs)
             if (!e) PDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
@@ -929,24 +961,25 @@ struct KrylovOps {
     }
     // both Gram-Schmidt passes + the norm + v_{k+1} = w / ||w|| in ONE cooperative launch
     // (bit-identical to gs_pass x 2 + norm_dev); h_out[0 .. 2 ncols] as the unfused sequence
-    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext, const GmresDevState* gst = nullptr,
-                  const double* pre1 = nullptr, int nb1 = 0) {
+    void gs_fused(const double* V, int ncols, double* w, double* h_out, double* vnext, LoopState* ls = nullptr,
+                  const double* pre1 = nullptr, int nb1 = 0, double* Hcol = nullptr, double* cs = nullptr,
+                  double* sn = nullptr, double* gv = nullptr, int mm = 0, double tolb = 0.0) {
         ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (3.0 * ncols + 6.0 - (pre1 ? ncols + 1.0 : 0.0)));
         long long n = g.n;
         double* part = g.partial.p;
-        void* args[] = {&n, &ncols, (void*)&V, &w, &part, &h_out, &vnext, (void*)&gst, (void*)&pre1, &nb1};
+        void* args[] = {&n,   &ncols,       (void*)&V, &w,  &part, &h_out, &vnext, (void*)&ls,
+                        (void*)&pre1, &nb1, &Hcol,     &cs, &sn,   &gv,    &mm,    &tolb};
         PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_gs, kRedBlocks, kRedThreads, args, sizeof(double) * ncols, st));
         count_launch();
         PDG_CHECK_LAUNCH();
     }
     // r = r0 - AZ y and ||r|| (bit-identical to k_combine + sub_norm), on the host
-    void residual_launch(const double* AZ, int ncols, const double* y, const double* r0, double* r,
-                         GmresDevState* gst = nullptr, double bnorm = 1.0, double tol = 0.0) {
+    void residual_launch(const double* AZ, int ncols, const double* y, const double* r0, double* r) {
         ProfScope prof(PROF_KRYLOV, st, 8.0 * (double)g.n * (ncols + 2.0));
         long long n = g.n;
         double* part = g.partial.p;
         double* nrm = g.norm_dev.p;
-        void* args[] = {&n, &ncols, (void*)&AZ, (void*)&y, (void*)&r0, &r, &part, &nrm, &gst, &bnorm, &tol};
+        void* args[] = {&n, &ncols, (void*)&AZ, (void*)&y, (void*)&r0, &r, &part, &nrm};
         PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_arnoldi_residual, kRedBlocks, kRedThreads, args, 0, st));
         count_launch();
         PDG_CHECK_LAUNCH();
@@ -1009,16 +1042,10 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
     // sequence they replace (bit-identical results, kept for the A/B test)
     const bool fused = !std::getenv("PDG_KRYLOV_UNFUSED");
     const bool spmv_dots = fused && !(std::getenv("PDG_SPMV_DOTS") && std::atoi(std::getenv("PDG_SPMV_DOTS")) == 0);
-    // PDG_GMRES_DEVICE_LS=1: device-driven steps (with the fused Arnoldi-relation residual): the
-    // Hessenberg column, breakdown test and least squares run on the device (k_gmres_ls, same
-    // bits as the host), one host round trip per step instead of two. Opt-in: measured slower
-    // at config 1 (4 steps per cycle): the single-block least-squares kernel costs more than
-    // the host round trip it removes.
-    const bool pipelined = arnoldi_res && fused && std::getenv("PDG_GMRES_DEVICE_LS");
-    // PDG_GMRES_LOOKAHEAD=1: queue step k+1 before reading step k's stop flag (speculative
-    // steps exit at entry; measured slower at 4 steps per cycle: the skipped launches cost more
-    // than the host round trip they hide)
-    const bool lookahead = pipelined && std::getenv("PDG_GMRES_LOOKAHEAD") && std::atoi(std::getenv("PDG_GMRES_LOOKAHEAD")) > 0;
+    // flexible candidate (default): device-driven steps with the Givens residual estimate
+    // (below); PDG_GMRES_HOST_LOOP=1 selects the host-driven loop (Arnoldi-relation residual
+    // per step, two host round trips per step), also used by the reference candidate
+    const bool devloop = flexible && fused && !(std::getenv("PDG_GMRES_HOST_LOOP") && std::atoi(std::getenv("PDG_GMRES_HOST_LOOP")) > 0);
     std::vector<double> H;
     bool x_is_zero = true;
     while (total < max_iter) {
@@ -1036,40 +1063,49 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
         auto h = [&](int i, int j) -> double& { return H[(size_t)j * (mm + 1) + i]; };
         // v_0 = r / beta (beta recomputed on the device by the same fixed tree)
         K.norm_dev(kr.r.p, kr.V.p);
-        if (arnoldi_res) PDG_CUDA(cudaMemcpyAsync(kr.r0.p, kr.r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        if (pipelined) {
-            GmresDevState* gst = reinterpret_cast<GmresDevState*>(kr.gst.p);
-            GmresDevState* slots = static_cast<GmresDevState*>(kr.h_slots);
-            PDG_CUDA(cudaMemsetAsync(kr.gst.p, 0, sizeof(GmresDevState), st));
+        if (arnoldi_res && !devloop) PDG_CUDA(cudaMemcpyAsync(kr.r0.p, kr.r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        if (devloop) {
+            // Device-driven steps: step k (preconditioner, SpMV + first-pass dots, Gram-Schmidt
+            // with the Givens residual estimate) is queued before step k - 1's stop flag is read,
+            // so the GPU never waits for the host inside a cycle; a step queued after the cycle
+            // ended exits at entry on the device (guard). At the stop, the host solves the
+            // least squares (ColPivHouseholderQR, gmres.hpp:111) on the downloaded Hessenberg
+            // columns and confirms on the explicit true residual (gmres.hpp:68-72); if that
+            // fails before the cycle's end, the cycle goes on (gmres.hpp:118-131).
+            LoopState* lsd = reinterpret_cast<LoopState*>(kr.lstate.p);
+            LoopState* slots = static_cast<LoopState*>(kr.h_slots);
+            double* cs = kr.givens.p;
+            double* sn = cs + (restart + 1);
+            double* gv = sn + (restart + 1);
+            PDG_CUDA(cudaMemsetAsync(kr.lstate.p, 0, sizeof(LoopState), st));
+            // the columns are written down to the subdiagonal only: the rest of H is zero
             PDG_CUDA(cudaMemsetAsync(kr.Hd.p, 0, sizeof(double) * (size_t)(mm + 1) * mm, st));
-            auto set_guard = [&](const int* g) {
-                op.guard = g;
-                pre.guard = g;
-                pre.flow_nd.guard = g;
-                if (pre.a) pre.a->nd.guard = g;
+            kr.h_host[0] = beta;
+            PDG_CUDA(cudaMemcpyAsync(gv, kr.h_host, sizeof(double), cudaMemcpyHostToDevice, st));
+            auto set_guard = [&](const int* gp) {
+                op.guard = gp;
+                pre.guard = gp;
+                pre.flow_nd.guard = gp;
+                if (pre.a) pre.a->nd.guard = gp;
             };
-            set_guard(&gst->stop);
+            set_guard(&lsd->stop);
+            const double tolb = opts.tol * bnorm;
+            const bool no_lookahead = std::getenv("PDG_GMRES_NO_LOOKAHEAD") != nullptr;
             auto step = [&](int k) {
                 double* vk = kr.V.p + (size_t)k * n;
                 double* zk = kr.Z.p + (size_t)k * n;
-                double* azk = kr.AZ.p + (size_t)k * n;
                 pre.apply(vk, zk, st);
-                if (spmv_dots && k + 1 <= 8) {  // w = AZ_k and the first Gram-Schmidt pass's partials in the SpMV
-                    op.apply_dots(zk, azk, kr.w.p, kr.V.p, k + 1, kr.spmv_part.p, st);
-                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst, kr.spmv_part.p,
-                               kr.spmv_blocks);
+                double* Hcol = kr.Hd.p + (size_t)k * (mm + 1);
+                if (spmv_dots && k + 1 <= 8) {  // w and the first Gram-Schmidt pass's partials in the SpMV
+                    op.apply_dots(zk, kr.w.p, nullptr, kr.V.p, k + 1, kr.spmv_part.p, st);
+                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, lsd, kr.spmv_part.p,
+                               kr.spmv_blocks, Hcol, cs, sn, gv, mm, tolb);
                 } else {
-                    op.apply(zk, azk, st);
-                    PDG_CUDA(cudaMemcpyAsync(kr.w.p, azk, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, gst);
+                    op.apply(zk, kr.w.p, st);
+                    K.gs_fused(kr.V.p, k + 1, kr.w.p, kr.h_dev.p, kr.V.p + (size_t)(k + 1) * n, lsd, nullptr, 0, Hcol,
+                               cs, sn, gv, mm, tolb);
                 }
-                {
-                    ProfScope prof_(PROF_KRYLOV, st, 0.0);
-                    gmres_ls_launch(k, mm, beta, kr.h_dev.p, kr.Hd.p, kr.hk.p, kr.ls_rhs.p, kr.ls_tau.p, kr.ls_nrm.p,
-                                    kr.ls_piv.p, kr.y_dev.p, gst, st);
-                }
-                K.residual_launch(kr.AZ.p, k + 1, kr.y_dev.p, kr.r0.p, kr.r.p, gst, bnorm, opts.tol);
-                PDG_CUDA(cudaMemcpyAsync(slots + k, gst, sizeof(GmresDevState), cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaMemcpyAsync(slots + k, lsd, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
                 PDG_CUDA(cudaEventRecord(kr.evs[k & 1], st));
             };
             const int left = max_iter - total;  // == mm unless the iteration limit cuts the cycle
@@ -1078,7 +1114,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 int kend = -1;
                 for (int k = k0; k < mm; ++k) {
                     step(k);  // queued behind step k - 1: skipped on the device if k - 1 ended the cycle
-                    if (!lookahead) {  // one host round trip per step (the stop flag), no speculative step
+                    if (no_lookahead) {
                         PDG_CUDA(cudaEventSynchronize(kr.evs[k & 1]));
                         if (slots[k].stop) {
                             kend = k;
@@ -1094,26 +1130,43 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                 }
                 if (kend < 0) {
                     PDG_CUDA(cudaEventSynchronize(kr.evs[(mm - 1) & 1]));
-                    kend = mm - 1;
                     for (int k = k0; k < mm; ++k)
-                        if (slots[k].stop) { kend = k; break; }
+                        if (slots[k].stop) {
+                            kend = k;
+                            break;
+                        }
+                    if (kend < 0) kend = mm - 1;
                 }
                 set_guard(nullptr);  // the explicit check below must run with the stop flag set
                 for (int k = k0; k < kend; ++k) hist.push_back(slots[k].res);
                 total += kend + 1 - k0;
-                // cand = x + Z y of the last step; the stop is decided on the explicit true residual
-                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, kend + 1, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
+                // least squares on the Hessenberg columns 0..kend (host, as gmres.hpp:110-111)
+                const int kk = kend + 1;
+                std::vector<double> hk((size_t)(kk + 1) * kk);
+                PDG_CUDA(cudaMemcpy2DAsync(hk.data(), sizeof(double) * (kk + 1), kr.Hd.p, sizeof(double) * (mm + 1),
+                                           sizeof(double) * (kk + 1), kk, cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaStreamSynchronize(st));
+                std::vector<double> e1(kk + 1, 0.0);
+                e1[0] = beta;
+                const std::vector<double> y = ls_colpiv(hk, kk + 1, kk, e1);
+                PDG_CUDA(cudaMemcpyAsync(kr.y_dev.p, y.data(), sizeof(double) * kk, cudaMemcpyHostToDevice, st));
+                { ProfScope prof_(PROF_KRYLOV, st, 0.0); k_combine<<<gr, 256, 0, st>>>(n, kk, kr.Z.p, kr.y_dev.p, kr.x.p, kr.cand.p); }
                 count_launch();
                 op.apply(kr.cand.p, kr.t.p, st);
                 true_res = K.sub_norm(b, kr.t.p, kr.r.p);
                 converged = true_res / bnorm <= opts.tol;
                 hist.push_back(true_res);
                 const bool cycle_end = slots[kend].brk || kend == mm - 1 || kend + 1 >= left;
+                if (std::getenv("PDG_GMRES_TRACE")) {
+                    std::fprintf(stderr, "gmres devloop: k0 %d kend %d mm %d beta %.6e bnorm %.6e |", k0, kend, mm, beta, bnorm);
+                    for (int k = k0; k <= kend; ++k) std::fprintf(stderr, " %.3e", slots[k].res / bnorm);
+                    std::fprintf(stderr, " | explicit %.3e brk %d", true_res / bnorm, slots[kend].brk);
+                    std::fprintf(stderr, "\n");
+                }
                 if (converged || cycle_end) break;
-                // the Arnoldi-relation residual passed but the explicit one did not: the cycle
-                // goes on (gmres.hpp:118-131); re-arm the device state for step kend + 1
-                PDG_CUDA(cudaMemsetAsync(&gst->stop, 0, sizeof(int), st));
-                set_guard(&gst->stop);
+                // the estimate passed but the explicit residual did not: the cycle goes on
+                PDG_CUDA(cudaMemsetAsync(&lsd->stop, 0, sizeof(int), st));
+                set_guard(&lsd->stop);
                 k0 = kend + 1;
             }
             PDG_CUDA(cudaMemcpyAsync(kr.x.p, kr.cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));

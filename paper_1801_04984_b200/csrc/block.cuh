@@ -64,10 +64,10 @@ struct Gmres {
     DBuf<double> spmv_part;  // first Gram-Schmidt pass partials from the fused SpMV epilogue [block][<= 8]
     int spmv_blocks = 0;
     double* h_host = nullptr;  // pinned
-    // device-driven steps (flexible candidate): Hessenberg, least-squares scratch, step state
-    DBuf<double> Hd, hk, ls_rhs, ls_tau, ls_nrm, gst;
-    DBuf<int> ls_piv;
-    void* h_slots = nullptr;  // pinned GmresDevState per step
+    // device-driven steps (flexible candidate): Hessenberg columns, Givens state (cs, sn, g),
+    // step state
+    DBuf<double> Hd, givens, lstate;
+    void* h_slots = nullptr;  // pinned LoopState per step
     cudaEvent_t evs[2] = {nullptr, nullptr};
     void setup(long long n, int restart, bool keep_z, cudaStream_t st);
     ~Gmres();

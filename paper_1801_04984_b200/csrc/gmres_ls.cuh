@@ -3,9 +3,8 @@
 // published algorithm: column norms, pivot = largest remaining norm, Householder
 // vectors as makeHouseholder, numerical rank from the threshold eps * max norm).
 //
-// One implementation for the host (block.cu) and the device (gmres_ls.cu, one
-// thread, compiled with --fmad=false): no contraction on either side, IEEE sqrt
-// and division, so both produce the same bits.
+// Host implementation (block.cu): x86-64 code without -mfma (no contraction), IEEE
+// sqrt and division.
 #pragma once
 
 #include <cfloat>
@@ -96,17 +95,5 @@ __host__ __device__ inline void ls_colpiv_raw(double* a, int rows, int cols, dou
     for (int i = 0; i < rank; ++i) y[piv[i]] = rhs[i];
 #undef PDG_A
 }
-
-// One GMRES step's host decisions on the device (one thread): Hessenberg column k
-// from the two Gram-Schmidt passes and the norm (hd = [pass 0 | pass 1 | norm]),
-// the breakdown test h(k+1,k) <= 1e-14 ||H(:,k)|| (gmres.hpp:103) and the least
-// squares y of the (k+2) x (k+1) leading block (gmres.hpp:111).
-struct GmresDevState {
-    int stop;  // the step's candidate ends the cycle (converged or breakdown)
-    int brk;   // breakdown
-    double res;  // Arnoldi-relation true residual of the step
-};
-void gmres_ls_launch(int k, int mm, double beta, const double* hd, double* H, double* hk, double* rhs, double* tau,
-                     double* nrm, int* piv, double* y, GmresDevState* gs, cudaStream_t st);
 
 }  // namespace pdg

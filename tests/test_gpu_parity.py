@@ -604,54 +604,46 @@ def test_nested_dissection_inner_solves_match_block_tridiagonal(monkeypatch, sol
 
 
 @pytest.mark.parametrize("candidate,restart", [("flexible", 50), ("reference", 50), ("flexible", 2)])
-def test_fused_arnoldi_kernels_bit_identical(monkeypatch, candidate, restart):
-    """The fused cooperative Arnoldi kernels (both Gram-Schmidt passes + norm +
-    normalisation in one launch; the Arnoldi-relation residual and its norm in
-    one launch) keep the row order, the per-block partials and the partial-sum
-    tree of the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1, compared below),
-    and the opt-in device-driven steps (PDG_GMRES_DEVICE_LS: Hessenberg column, breakdown
-    test and least squares on the device; PDG_GMRES_LOOKAHEAD: next step queued
-    speculatively) make the host loop's decisions with the same bits: solutions, residual histories and
-    iteration counts are bit-identical. restart=2 exercises cycle ends without
-    convergence."""
+def test_gmres_loop_variants_agree(monkeypatch, candidate, restart):
+    """The GMRES loop variants on one dG(1) block (16^2, lognormal K):
+    - default, flexible: device-driven steps (the Gram-Schmidt kernel applies the
+      Givens rotations and decides the stop from || beta e1 - H y ||; the next step is
+      queued before the host reads the stop flag, and skipped on the device);
+    - PDG_GMRES_HOST_LOOP=1: the host-driven loop (Arnoldi-relation residual
+      r0 - (A Z) y each step), the reference candidate's loop;
+    - PDG_SPMV_DOTS=0: the first Gram-Schmidt pass as its own multidot instead of
+      the SpMV epilogue; PDG_KRYLOV_UNFUSED=1: the launch-per-step sequence.
+    The fused cooperative kernels keep the partial-sum order of the launch-per-step
+    sequence (bit-identical once the SpMV dots are off); every variant is
+    deterministic and takes the same iterations, solutions within 1e-10.
+    restart=2 exercises cycle ends without convergence."""
     spec = P.config1(16)
     ops = S.SpatialOperators.assemble(spec)
     t = S.time_constants(1)
     rhs = np.random.default_rng(11).standard_normal(2 * ops.n_total)
     opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=restart), candidate=candidate)
     blk = S.BlockSolver(ops, t["T"], 0.05, opt=opt)
-    x_f, rep_f = blk.solve(rhs)  # host-driven loop, fused kernels
+    x_f, rep_f = blk.solve(rhs)
+    x_r, rep_r = blk.solve(rhs)
+    assert rep_f.converged and np.array_equal(x_f, x_r)
+    assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_r.residual_history))
     runs = []
-    if candidate == "flexible":
-        monkeypatch.setenv("PDG_GMRES_DEVICE_LS", "1")  # device-driven steps (least squares on the device)
+    for env in ({"PDG_GMRES_HOST_LOOP": "1"}, {"PDG_GMRES_HOST_LOOP": "1", "PDG_SPMV_DOTS": "0"},
+                {"PDG_GMRES_HOST_LOOP": "1", "PDG_SPMV_DOTS": "0", "PDG_KRYLOV_UNFUSED": "1"}):
+        for k in ("PDG_GMRES_HOST_LOOP", "PDG_SPMV_DOTS", "PDG_KRYLOV_UNFUSED"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         runs.append(blk.solve(rhs))
-        monkeypatch.setenv("PDG_GMRES_LOOKAHEAD", "1")  # + speculative next step, skipped on the device
-        runs.append(blk.solve(rhs))
-        monkeypatch.delenv("PDG_GMRES_DEVICE_LS")
-        monkeypatch.delenv("PDG_GMRES_LOOKAHEAD")
-    for x_u, rep_u in runs:
-        assert rep_f.converged and rep_u.converged
-        assert rep_f.iterations == rep_u.iterations
-        assert np.array_equal(np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history))
-        assert np.array_equal(x_f, x_u)
-    # the first Gram-Schmidt pass's dots formed in the SpMV epilogue (default, up to 8 basis
-    # vectors) sum the same products in another fixed order than the separate multidot pass
-    # (PDG_SPMV_DOTS=0) and the launch-per-step sequence (PDG_KRYLOV_UNFUSED=1): the same
-    # iterations, roundoff-level differences
-    assert np.array_equal(x_f, blk.solve(rhs)[0])  # deterministic
-    other = []
-    monkeypatch.setenv("PDG_SPMV_DOTS", "0")
-    other.append(blk.solve(rhs))
-    monkeypatch.setenv("PDG_KRYLOV_UNFUSED", "1")
-    other.append(blk.solve(rhs))
-    x_s, rep_s = other[0]
-    for x_u, rep_u in other[1:]:  # without the SpMV dots, the fused kernels keep the unfused bits
-        assert rep_s.iterations == rep_u.iterations and np.array_equal(x_s, x_u)
-    for x_u, rep_u in other:
-        assert rep_u.converged and rep_u.iterations == rep_f.iterations
-        assert np.linalg.norm(x_u - x_f) <= 1e-10 * np.linalg.norm(x_f)
-        h, hu = np.asarray(rep_f.residual_history), np.asarray(rep_u.residual_history)
-        assert np.allclose(h, hu, rtol=1e-6, atol=1e-12 * h[0])
+    (x_s, rep_s), (x_u, rep_u) = runs[1], runs[2]
+    assert rep_s.iterations == rep_u.iterations and np.array_equal(x_s, x_u)
+    assert np.array_equal(np.asarray(rep_s.residual_history), np.asarray(rep_u.residual_history))
+    for x_v, rep_v in runs:
+        assert rep_v.converged and rep_v.iterations == rep_f.iterations, (rep_v.iterations, rep_f.iterations)
+        assert len(rep_v.residual_history) == len(rep_f.residual_history) == rep_f.iterations + 1
+        assert np.linalg.norm(x_v - x_f) <= 1e-10 * np.linalg.norm(x_f)
+        h, hv = np.asarray(rep_f.residual_history), np.asarray(rep_v.residual_history)
+        assert np.allclose(h, hv, rtol=1e-6, atol=1e-12 * h[0])
 
 
 def test_spmv_config3_256_bit_identical(oracle):
