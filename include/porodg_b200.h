@@ -161,6 +161,37 @@ void pdg_op_destroy(pdg_op* op);
  * 0 space-time SpMV, 1 displacement solve, 2 flow solve, 3 other preconditioner
  * kernels, 4 Krylov vector kernels, 5 slab transforms / rhs. alg_bytes is the
  * algorithmic traffic summed over the calls. */
+/* ---- Multi-GPU: one process per GPU, strips of cell rows ----
+ * A communicator per rank: NCCL (rank 0 creates the id with pdg_nccl_unique_id and the
+ * caller distributes it, e.g. by torch.distributed or MPI), or host-staged collectives
+ * through caller callbacks (blocking; tests with several ranks on one GPU). The
+ * distributed block is the transformed slab block of pdg_block_create (slab.hpp:154-171,
+ * :220-234) with its rows owned by strips: every rank passes the whole operators (ops)
+ * and its rows of the right-hand side; pdg_dblock_owned_rows gives their global indices. */
+typedef struct pdg_comm pdg_comm;
+typedef struct pdg_dblock pdg_dblock;
+/* recv[r * count + j] = (send of rank r)[j]; return 0 on success */
+typedef int (*pdg_host_allgather_fn)(void* user, const double* send, double* recv, long long count);
+/* to peers[i]: send[i] (scount[i] doubles); from peers[i]: recv[i] (rcount[i]); 0 on success */
+typedef int (*pdg_host_exchange_fn)(void* user, int npeers, const int* peers, const double* const* send,
+                                    const long long* scount, double* const* recv, const long long* rcount);
+int pdg_nccl_unique_id(unsigned char id[128]);
+int pdg_comm_create_nccl(pdg_ctx* ctx, int nranks, int rank, const unsigned char id[128], pdg_comm** out);
+int pdg_comm_create_host(pdg_ctx* ctx, int nranks, int rank, pdg_host_allgather_fn allgather,
+                         pdg_host_exchange_fn exchange, void* user, pdg_comm** out);
+void pdg_comm_destroy(pdg_comm* comm);
+int pdg_dblock_create(pdg_ops* ops, pdg_comm* comm, int m, const double* theta_mxm, double tau, double lambda_pre,
+                      const pdg_gmres_opts* opts, pdg_dblock** out);
+/* rows owned here and rows of the whole block (m * n_total) */
+int pdg_dblock_rows(const pdg_dblock* blk, long long* n_owned, long long* n_global);
+int pdg_dblock_owned_rows(const pdg_dblock* blk, long long* rows);
+/* GMRES across the ranks (collective: every rank calls it), owned rows, device pointers */
+int pdg_dblock_solve_device(pdg_dblock* blk, const double* rhs_owned, double* x_owned, pdg_report* rep);
+/* the operator rows and the preconditioner (collective), owned rows, device pointers */
+int pdg_dblock_apply_device(pdg_dblock* blk, const double* x_owned, double* y_owned);
+int pdg_dblock_precondition_device(pdg_dblock* blk, const double* r_owned, double* z_owned);
+void pdg_dblock_destroy(pdg_dblock* blk);
+
 /* Setup stage timers, cumulative seconds since pdg_setup_reset: [0] device assembly,
  * [1..3] displacement nested-dissection analysis / numeric factorization / solve schedule,
  * [4..6] the same for the flow Schur complement, [7] space-time operator build,

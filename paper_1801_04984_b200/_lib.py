@@ -104,6 +104,17 @@ _SIGS = {
     "pdg_op_apply_strip_device": (C.c_int, [VP, VP, VP, C.c_int, C.POINTER(C.c_float)]),
     "pdg_op_download_csr": (C.c_int, [VP, LLP, IP, DP]),
     "pdg_op_destroy": (None, [VP]),
+    "pdg_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+    "pdg_comm_create_nccl": (C.c_int, [VP, C.c_int, C.c_int, C.POINTER(C.c_ubyte), C.POINTER(VP)]),
+    "pdg_comm_create_host": (C.c_int, [VP, C.c_int, C.c_int, C.c_void_p, C.c_void_p, VP, C.POINTER(VP)]),
+    "pdg_comm_destroy": (None, [VP]),
+    "pdg_dblock_create": (C.c_int, [VP, VP, C.c_int, DP, C.c_double, C.c_double, C.POINTER(GmresOpts), C.POINTER(VP)]),
+    "pdg_dblock_rows": (C.c_int, [VP, LLP, LLP]),
+    "pdg_dblock_owned_rows": (C.c_int, [VP, LLP]),
+    "pdg_dblock_solve_device": (C.c_int, [VP, VP, VP, C.POINTER(Report)]),
+    "pdg_dblock_apply_device": (C.c_int, [VP, VP, VP]),
+    "pdg_dblock_precondition_device": (C.c_int, [VP, VP, VP]),
+    "pdg_dblock_destroy": (None, [VP]),
     "pdg_setup_reset": (None, []),
     "pdg_setup_read": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "pdg_profile_enable": (None, [C.c_int]),

@@ -442,7 +442,51 @@ HCsr csr_download(const DCsr& a, cudaStream_t st) {
     return h;
 }
 
-int nd_leaf_dofs(int dflt, const char* var = "PDG_ND_LEAF") {
+HCsr flow_schur_host(const SpatialOps& o, double w, const std::vector<double>& di, cudaStream_t st) {
+    // S_q = w M_q - w^2 B D^{-1} B^T, rows in face order, columns ascending; each entry summed
+    // in the order of k_flow_schur_blocks (M_q term, then the B D^{-1} B^T products)
+    const HCsr mq = csr_download(o.M_q, st), bb = csr_download(o.B, st), bt = csr_download(o.Bt, st);
+    HCsr h;
+    h.rows = h.cols = o.n_q;
+    h.off.assign(o.n_q + 1, 0);
+    for (int f = 0; f < o.n_q; ++f) {
+        std::vector<std::pair<int, double>> row;
+        for (int k = mq.off[f]; k < mq.off[f + 1]; ++k) row.push_back({mq.idx[k], w * mq.val[k]});
+        for (int k = bb.off[f]; k < bb.off[f + 1]; ++k) {
+            const int c = bb.idx[k];
+            const double wa = w * bb.val[k];
+            for (int q = bt.off[c]; q < bt.off[c + 1]; ++q) row.push_back({bt.idx[q], -(wa * (w * bt.val[q])) * di[c]});
+        }
+        std::stable_sort(row.begin(), row.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        for (size_t k = 0; k < row.size();) {
+            double v = 0.0;
+            const int col = row[k].first;
+            for (; k < row.size() && row[k].first == col; ++k) v += row[k].second;
+            h.idx.push_back(col);
+            h.val.push_back(v);
+        }
+        h.off[f + 1] = static_cast<int>(h.idx.size());
+    }
+    return h;
+}
+
+void face_coords(int nx, int ny, std::vector<double>& cx, std::vector<double>& cy) {
+    const int nq = nx * (ny + 1) + (nx + 1) * ny;
+    cx.assign(nq, 0.0);
+    cy.assign(nq, 0.0);
+    for (int f = 0; f < nq; ++f) {
+        if (f < nx * (ny + 1)) {
+            cx[f] = f % nx + 0.5;
+            cy[f] = f / nx;
+        } else {
+            const int g = f - nx * (ny + 1);
+            cx[f] = g / ny;
+            cy[f] = g % ny + 0.5;
+        }
+    }
+}
+
+int nd_leaf_dofs(int dflt, const char* var) {
     const char* e = std::getenv(var);
     return e ? std::max(1, std::atoi(e)) : dflt;
 }
@@ -612,41 +656,14 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     if ((!fmode || std::string(fmode) == "nd") && !std::getenv("PDG_FLOW_STRIPS")) {
         // S_q assembled on the host (the entries of k_flow_schur_blocks), nested dissection over
         // faces: horizontal j*nx+i at (i + 1/2, j), vertical nx(ny+1) + i*ny + j at (i, j + 1/2)
-        const HCsr mq = csr_download(o.M_q, st), bb = csr_download(o.B, st), bt = csr_download(o.Bt, st);
-        const std::vector<double> di = dinv.download(st);
-        std::vector<int> off(o.n_q + 1, 0), idx;
-        std::vector<double> val;
-        for (int f = 0; f < o.n_q; ++f) {
-            std::vector<std::pair<int, double>> row;
-            for (int k = mq.off[f]; k < mq.off[f + 1]; ++k) row.push_back({mq.idx[k], w * mq.val[k]});
-            for (int k = bb.off[f]; k < bb.off[f + 1]; ++k) {
-                const int c = bb.idx[k];
-                const double wa = w * bb.val[k];
-                for (int q = bt.off[c]; q < bt.off[c + 1]; ++q) row.push_back({bt.idx[q], -(wa * (w * bt.val[q])) * di[c]});
-            }
-            std::stable_sort(row.begin(), row.end(), [](auto& a, auto& b) { return a.first < b.first; });
-            for (size_t k = 0; k < row.size();) {
-                double v = 0.0;
-                const int col = row[k].first;
-                for (; k < row.size() && row[k].first == col; ++k) v += row[k].second;
-                idx.push_back(col);
-                val.push_back(v);
-            }
-            off[f + 1] = static_cast<int>(idx.size());
-        }
+        const HCsr sq = flow_schur_host(o, w, dinv.download(st), st);
+        const std::vector<int>& off = sq.off;
+        const std::vector<int>& idx = sq.idx;
+        const std::vector<double>& val = sq.val;
         std::vector<int> node_of(o.n_q);
-        std::vector<double> cx(o.n_q), cy(o.n_q);
-        for (int f = 0; f < o.n_q; ++f) {
-            node_of[f] = f;
-            if (f < nx * (ny + 1)) {
-                cx[f] = f % nx + 0.5;
-                cy[f] = f / nx;
-            } else {
-                const int g = f - nx * (ny + 1);
-                cx[f] = g / ny;
-                cy[f] = g % ny + 0.5;
-            }
-        }
+        std::vector<double> cx, cy;
+        face_coords(nx, ny, cx, cy);
+        for (int f = 0; f < o.n_q; ++f) node_of[f] = f;
         flow_use_nd = true;
         flow_nd.prof_phase = PROF_FLOW_SOLVE;
         flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(128, "PDG_ND_FLOW_LEAF"), m, st);

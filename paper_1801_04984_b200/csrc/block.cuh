@@ -26,6 +26,12 @@ struct ASolver {
     }
 };
 std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st);
+HCsr csr_download(const DCsr& a, cudaStream_t st);
+// flux Schur complement S_q = w M_q - w^2 B D^{-1} B^T (host CSR, face order), dinv = D^{-1}
+HCsr flow_schur_host(const SpatialOps& o, double w, const std::vector<double>& dinv, cudaStream_t st);
+// face centres (mesh.hpp:59-60 numbering) in cell units: the nested-dissection coordinates
+void face_coords(int nx, int ny, std::vector<double>& cx, std::vector<double>& cy);
+int nd_leaf_dofs(int dflt, const char* var = "PDG_ND_LEAF");
 
 // FixedStressSolver(lambda) :: precondition for each of the m components.
 struct FixedStressPre {

@@ -4,6 +4,7 @@
 #include <random>
 
 #include "block.cuh"
+#include "dist.cuh"
 #include "timebasis.hpp"
 
 namespace pdg {
@@ -39,6 +40,12 @@ struct pdg_fs {
     FsSolver fs;
     pdg_fs_opts opts{};
     DBuf<double> io_a, io_b, io_c;
+};
+struct pdg_comm {
+    std::unique_ptr<Comm> c;
+};
+struct pdg_dblock {
+    DistBlock b;
 };
 struct pdg_slab {
     pdg_ops* ops = nullptr;
@@ -198,6 +205,86 @@ void pdg_ctx_destroy(pdg_ctx* ctx) {
     if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
 }
+
+int pdg_nccl_unique_id(unsigned char id[128]) {
+    API_BEGIN
+    require(id != nullptr, "pdg_nccl_unique_id: null argument");
+    nccl_unique_id(id);
+    API_END
+}
+
+int pdg_comm_create_nccl(pdg_ctx* ctx, int nranks, int rank, const unsigned char id[128], pdg_comm** out) {
+    API_BEGIN
+    require(ctx && id && out, "pdg_comm_create_nccl: null argument");
+    auto c = std::make_unique<pdg_comm>();
+    c->c = make_nccl_comm(nranks, rank, id, ctx->c.device);
+    *out = c.release();
+    API_END
+}
+
+int pdg_comm_create_host(pdg_ctx* ctx, int nranks, int rank, pdg_host_allgather_fn allgather,
+                         pdg_host_exchange_fn exchange, void* user, pdg_comm** out) {
+    API_BEGIN
+    require(ctx && out, "pdg_comm_create_host: null argument");
+    auto c = std::make_unique<pdg_comm>();
+    c->c = make_host_comm(nranks, rank, allgather, exchange, user);
+    *out = c.release();
+    API_END
+}
+
+void pdg_comm_destroy(pdg_comm* comm) { delete comm; }
+
+int pdg_dblock_create(pdg_ops* ops, pdg_comm* comm, int m, const double* theta, double tau, double lambda_pre,
+                      const pdg_gmres_opts* opts, pdg_dblock** out) {
+    API_BEGIN
+    require(ops && comm && theta && opts && out, "pdg_dblock_create: null argument");
+    PDG_CUDA(cudaSetDevice(ops->s.ctx->device));
+    auto b = std::make_unique<pdg_dblock>();
+    b->b.create(ops->s, comm->c.get(), m, theta, tau, lambda_pre, *opts, ops->s.ctx->stream);
+    *out = b.release();
+    API_END
+}
+
+int pdg_dblock_rows(const pdg_dblock* blk, long long* n_owned, long long* n_global) {
+    API_BEGIN
+    require(blk && n_owned && n_global, "pdg_dblock_rows: null argument");
+    *n_owned = blk->b.nown;
+    *n_global = blk->b.nglob;
+    API_END
+}
+
+int pdg_dblock_owned_rows(const pdg_dblock* blk, long long* rows) {
+    API_BEGIN
+    require(blk && rows, "pdg_dblock_owned_rows: null argument");
+    std::copy(blk->b.own_rows_h.begin(), blk->b.own_rows_h.end(), rows);
+    API_END
+}
+
+int pdg_dblock_solve_device(pdg_dblock* blk, const double* rhs, double* x, pdg_report* rep) {
+    API_BEGIN
+    require(blk && rhs && x, "pdg_dblock_solve_device: null argument");
+    blk->b.solve(rhs, x, rep);
+    PDG_CUDA(cudaStreamSynchronize(blk->b.ctx->stream));
+    API_END
+}
+
+int pdg_dblock_apply_device(pdg_dblock* blk, const double* x, double* y) {
+    API_BEGIN
+    require(blk && x && y, "pdg_dblock_apply_device: null argument");
+    blk->b.apply(x, y, blk->b.ctx->stream);
+    PDG_CUDA(cudaStreamSynchronize(blk->b.ctx->stream));
+    API_END
+}
+
+int pdg_dblock_precondition_device(pdg_dblock* blk, const double* r, double* z) {
+    API_BEGIN
+    require(blk && r && z, "pdg_dblock_precondition_device: null argument");
+    blk->b.precondition(r, z, blk->b.ctx->stream);
+    PDG_CUDA(cudaStreamSynchronize(blk->b.ctx->stream));
+    API_END
+}
+
+void pdg_dblock_destroy(pdg_dblock* blk) { delete blk; }
 
 int pdg_mesh_dims_from_operators(const pdg_csr* B, int n_q, int dims[2]) {
     API_BEGIN

@@ -1,9 +1,14 @@
-"""The device path of the multi-GPU block solve (distributed.py) run as two
-ranks sharing one GPU over gloo: no kernel waits on another rank's kernel
-(every exchange is a host-level collective), so this exercises the real code
-(strip SpMV + halo, substructured exact inner solves with the library's
-sweeps, rank-ordered Krylov sums) without a second GPU. Bar: the single-GPU
-solve's iteration count (+-1) and its solution within 1e-9."""
+"""The library's multi-GPU block solve (csrc/dist.cu, pdg_dblock_*): strip-owned
+operator rows with a halo exchange, rank-ordered Krylov sums and exact inner
+solves by substructuring, all inside libporodg_b200.
+
+- one rank through an NCCL communicator (the NCCL code path on one GPU);
+- 2 and 3 ranks sharing one GPU through the host-staged communicator (gloo
+  callbacks): no kernel waits on another rank's kernel, every exchange is a
+  host-level collective. 3 ranks exercise a middle strip (two separators).
+Bars: the distributed operator is the single-GPU SpMV bit for bit; the
+preconditioner agrees to roundoff; the solve takes the single-GPU iteration
+count (+-1) and matches its solution within 1e-9."""
 import os
 import socket
 
@@ -23,6 +28,37 @@ def _free_port():
     return p
 
 
+def _single_gpu(n, candidate):
+    from paper_1801_04984_b200 import solver as S
+
+    ops = S.SpatialOperators.assemble(P.config1(n))
+    T = S.time_constants(1)["T"]
+    blk = S.BlockSolver(ops, T, 0.05, opt=S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate))
+    rhs = P.uniform_vector(P.X_SEED, blk.rows)
+    x, rep = blk.solve(rhs)
+    return blk, rhs, x, rep
+
+
+@pytest.mark.parametrize("candidate", ["reference", "flexible"])
+def test_distributed_block_one_rank_nccl(candidate):
+    from paper_1801_04984_b200 import distributed as D, solver as S
+
+    n = 16
+    blk, rhs, x_ref, rep_ref = _single_gpu(n, candidate)
+    comm = D.nccl_comm(None, 0, 1)
+    ops = S.SpatialOperators.assemble(P.config1(n))
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate)
+    db = D.DistributedBlock(ops, comm, S.time_constants(1)["T"], 0.05, opt)
+    assert db.n_owned == db.n_global == blk.rows and np.array_equal(db.owned, np.arange(blk.rows))
+    v = P.uniform_vector(7, blk.rows)
+    assert np.array_equal(db.apply(v), blk.apply(v))
+    z, zr = db.precondition(v), blk.precondition(v)
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    x, rep = db.solve(rhs)
+    assert rep.converged and abs(rep.iterations - rep_ref.iterations) <= 1
+    assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
+
+
 def _rank(rank, world, port, n, candidate, q):
     import torch
     import torch.distributed as dist
@@ -34,46 +70,48 @@ def _rank(rank, world, port, n, candidate, q):
         from paper_1801_04984_b200 import distributed as D, solver as S
 
         torch.cuda.set_device(0)
-        comm = D.Comm(dist, rank, world, stage_on_host=True)
-        T = S.time_constants(1)["T"]
-        blk = D.DeviceDistributedBlock(P.config1(n), T, 0.05, rank, comm, device=0, candidate=candidate)
-        rhs = P.uniform_vector(P.X_SEED, 2 * blk.nt)
-        owned = blk.owned.cpu().numpy()
-        x, rep = blk.solve(torch.as_tensor(rhs[owned], device="cuda"))
-        q.put((rank, owned, x.cpu().numpy(), rep["iterations"], rep["converged"]))
+        comm = D.host_comm(dist, rank, world)
+        ops = S.SpatialOperators.assemble(P.config1(n))
+        opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate)
+        db = D.DistributedBlock(ops, comm, S.time_constants(1)["T"], 0.05, opt)
+        own = db.owned
+        v = P.uniform_vector(7, db.n_global)
+        y = db.apply(v[own])
+        z = db.precondition(v[own])
+        rhs = P.uniform_vector(P.X_SEED, db.n_global)
+        x, rep = db.solve(rhs[own])
+        q.put((rank, own, y, z, x, rep.iterations, rep.converged))
     except Exception:  # pragma: no cover
         import traceback
-        q.put((rank, traceback.format_exc(), None, None, None))
+        q.put((rank, traceback.format_exc(), None, None, None, None, None))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("candidate", ["reference", "flexible"])
-def test_distributed_block_solve_two_ranks_one_gpu(candidate):
+@pytest.mark.parametrize("world,candidate", [(2, "flexible"), (2, "reference"), (3, "flexible")])
+def test_distributed_block_ranks_share_one_gpu(world, candidate):
     import multiprocessing as mp
 
-    from paper_1801_04984_b200 import solver as S
-
-    n, world = 16, 2
+    n = 16
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_rank, args=(r, world, port, n, candidate, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in procs]
+    res = [q.get(timeout=900) for _ in procs]
     for p in procs:
         p.join(timeout=120)
     for r in res:
         assert not isinstance(r[1], str), r[1]
-    ops = S.SpatialOperators.assemble(P.config1(n))
-    blk = S.BlockSolver(ops, S.time_constants(1)["T"], 0.05,
-                        opt=S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate))
-    rhs = P.uniform_vector(P.X_SEED, blk.rows)
-    x_ref, rep_ref = blk.solve(rhs)
-    x = np.full(blk.rows, np.nan)
-    for rank, owned, xo, its, conv in res:
+    blk, rhs, x_ref, rep_ref = _single_gpu(n, candidate)
+    v = P.uniform_vector(7, blk.rows)
+    y_ref, z_ref = blk.apply(v), blk.precondition(v)
+    y, z, x = (np.full(blk.rows, np.nan) for _ in range(3))
+    for rank, own, yo, zo, xo, its, conv in res:
         assert conv and abs(its - rep_ref.iterations) <= 1, (rank, its, rep_ref.iterations)
-        x[owned] = xo
+        y[own], z[own], x[own] = yo, zo, xo
     assert not np.isnan(x).any()
+    assert np.array_equal(y, y_ref)  # every row summed as on one GPU
+    assert np.linalg.norm(z - z_ref) <= 1e-10 * np.linalg.norm(z_ref)  # exact substructured inner solves
     assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
