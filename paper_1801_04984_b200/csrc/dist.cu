@@ -259,23 +259,53 @@ __global__ void k_d_collect(long long nown, const long long* __restrict__ rows, 
         z[k] = l < nu ? u[(long long)i * nu + l] : l < nu + nq ? q[(long long)i * nq + l - nu] : p[(long long)i * np + l - nu - nq];
     }
 }
-// deterministic local dots: one block per column j of V (n x ncols, ld n) against w
 constexpr int kDotThreads = 256;
-__global__ void __launch_bounds__(kDotThreads) k_col_dots(long long n, const double* __restrict__ V, const double* __restrict__ w,
-                                                          double* __restrict__ out) {
-    __shared__ double sh[kDotThreads / 32];
-    const double* v = V + (long long)blockIdx.x * n;
-    double a = 0.0;
-    for (long long r = threadIdx.x; r < n; r += blockDim.x) a += v[r] * w[r];
-    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < kDotThreads / 32; ++i) s += sh[i];
-        out[blockIdx.x] = s;
+// deterministic multi-block dots: partials[blk][j] of V_j . w over a fixed grid-stride row
+// set, then out[j] = the partials summed in block order (one thread per column)
+constexpr int kDotBlocks = 148;
+__global__ void __launch_bounds__(kDotThreads) k_dot_partials(long long n, int ncols, const double* __restrict__ V,
+                                                              const double* __restrict__ w, double* __restrict__ part) {
+    __shared__ double sh[8][kDotThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j0 = 0; j0 < ncols; j0 += 8) {
+        double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+            const double wr = w[r];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (j0 + q < ncols) a[q] += V[(long long)(j0 + q) * n + r] * wr;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sh[q][warp] = a[q];
+        __syncthreads();
+        if (threadIdx.x < 8 && j0 + threadIdx.x < ncols) {
+            double t = 0.0;
+            for (int i = 0; i < kDotThreads / 32; ++i) t += sh[threadIdx.x][i];
+            part[(long long)blockIdx.x * ncols + j0 + threadIdx.x] = t;
+        }
+        __syncthreads();
     }
 }
+__global__ void k_dot_final(int nblk, int ncols, const double* __restrict__ part, double* __restrict__ out) {
+    for (int j = threadIdx.x; j < ncols; j += blockDim.x) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t += part[(long long)b * ncols + j];
+        out[j] = t;
+    }
+}
+__global__ void k_sqrt_scale(long long n, const double* __restrict__ nrm2, const double* __restrict__ w, double* __restrict__ v,
+                             double* __restrict__ nrm_out) {
+    const double d = sqrt(nrm2[0]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) nrm_out[0] = d;
+    if (!v) return;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        v[r] = w[r] / d;
+}
+
 // w -= V h (h on the device), out = base + V y
 __global__ void k_sub_vh(long long n, int ncols, const double* __restrict__ V, const double* __restrict__ h, double* __restrict__ w) {
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
@@ -811,8 +841,8 @@ void DistBlock::create(const SpatialOps& o, Comm* c, int m_, const double* theta
     for (auto* b : {&wv, &x, &r, &cand, &t}) b->alloc(nown);
     ydev.alloc(rs + 2);
     dots.alloc(rs + 2);
-    dsum.alloc(rs + 2);
-    if (!hhost) PDG_CUDA(cudaMallocHost(&hhost, sizeof(double) * (rs + 4)));
+    dsum.alloc(2 * rs + 4);
+    if (!hhost) PDG_CUDA(cudaMallocHost(&hhost, sizeof(double) * (2 * rs + 4)));
     PDG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -859,21 +889,22 @@ void DistBlock::precondition(const double* r_own, double* z_own, cudaStream_t st
     PDG_CHECK_LAUNCH();
 }
 
+// ordered sums over the ranks of the local dots V_j . w, j < ncols, into out (device): no
+// host round trip (NCCL runs on the stream; the host backend synchronizes inside)
+void DistBlock::multidot_dev(const double* Vb, int ncols, const double* wv_, double* out, cudaStream_t st) {
+    if (part.n < (size_t)kDotBlocks * ncols) part.alloc((size_t)kDotBlocks * ncols);
+    k_dot_partials<<<kDotBlocks, kDotThreads, 0, st>>>(nown, ncols, Vb, wv_, part.p);
+    k_dot_final<<<1, 64, 0, st>>>(kDotBlocks, ncols, part.p, dots.p);
+    count_launch(2);
+    PDG_CHECK_LAUNCH();
+    ordered_allreduce(*comm, dots.p, out, ncols, gbuf, st);
+}
+
 double DistBlock::dot_sum(const double* a, const double* b, cudaStream_t st) {
-    k_col_dots<<<1, kDotThreads, 0, st>>>(nown, a, b, dots.p);
-    count_launch();
-    ordered_allreduce(*comm, dots.p, dsum.p, 1, gbuf, st);
+    multidot_dev(a, 1, b, dsum.p, st);
     PDG_CUDA(cudaMemcpyAsync(hhost, dsum.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     PDG_CUDA(cudaStreamSynchronize(st));
     return hhost[0];
-}
-
-void DistBlock::multidot(const double* Vb, int ncols, const double* wv_, double* h_host, cudaStream_t st) {
-    k_col_dots<<<ncols, kDotThreads, 0, st>>>(nown, Vb, wv_, dots.p);
-    count_launch();
-    ordered_allreduce(*comm, dots.p, dsum.p, ncols, gbuf, st);
-    PDG_CUDA(cudaMemcpyAsync(h_host, dsum.p, sizeof(double) * ncols, cudaMemcpyDeviceToHost, st));
-    PDG_CUDA(cudaStreamSynchronize(st));
 }
 
 // GMRES (gmres.hpp:40-139) on the owned rows; every reduction is a rank-ordered sum, so all
@@ -921,27 +952,46 @@ void DistBlock::solve(const double* b, double* x_out, pdg_report* rep) {
             k_axpby<<<gr, 256, 0, st>>>(n, 1.0 / beta, r.p, 0.0, nullptr, V.p);
             count_launch();
             bool done = false;
+            double* hd = dsum.p;  // [h pass 1 (k+1) | h pass 2 (k+1) | ||w||^2, ||w||]
+            std::vector<double> cs(mm), sn(mm), gq(mm + 1, 0.0);
+            gq[0] = beta;
             for (int k = 0; k < mm && !done; ++k) {
                 double* vk = V.p + (size_t)k * n;
                 double* zk = flexible ? Z.p + (size_t)k * n : cand.p;
                 precondition(vk, zk, st);
                 apply(zk, wv.p, st);
-                for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, two passes
-                    multidot(V.p, k + 1, wv.p, hhost, st);
-                    PDG_CUDA(cudaMemcpyAsync(ydev.p, hhost, sizeof(double) * (k + 1), cudaMemcpyHostToDevice, st));
-                    k_sub_vh<<<gr, 256, 0, st>>>(n, k + 1, V.p, ydev.p, wv.p);
+                // classical Gram-Schmidt, two passes, and the norm: rank-ordered sums on the stream,
+                // the Hessenberg column comes back in one transfer
+                for (int pass = 0; pass < 2; ++pass) {
+                    multidot_dev(V.p, k + 1, wv.p, hd + (size_t)pass * (k + 1), st);
+                    k_sub_vh<<<gr, 256, 0, st>>>(n, k + 1, V.p, hd + (size_t)pass * (k + 1), wv.p);
                     count_launch();
-                    for (int i = 0; i <= k; ++i) h(i, k) += hhost[i];
                 }
-                h(k + 1, k) = nrm(wv.p);
+                multidot_dev(wv.p, 1, wv.p, hd + 2 * (k + 1), st);
+                k_sqrt_scale<<<gr, 256, 0, st>>>(n, hd + 2 * (k + 1), wv.p, V.p + (size_t)(k + 1) * n, hd + 2 * (k + 1) + 1);
+                count_launch();
+                PDG_CUDA(cudaMemcpyAsync(hhost, hd, sizeof(double) * (2 * (k + 1) + 2), cudaMemcpyDeviceToHost, st));
+                PDG_CUDA(cudaStreamSynchronize(st));
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int i = 0; i <= k; ++i) h(i, k) += hhost[(size_t)pass * (k + 1) + i];
+                h(k + 1, k) = hhost[2 * (k + 1) + 1];
                 double cn = 0.0;
                 for (int i = 0; i <= mm; ++i) cn += h(i, k) * h(i, k);
                 const bool breakdown = h(k + 1, k) <= 1e-14 * std::sqrt(cn);
-                if (!breakdown) {
-                    k_axpby<<<gr, 256, 0, st>>>(n, 1.0 / h(k + 1, k), wv.p, 0.0, nullptr, V.p + (size_t)(k + 1) * n);
-                    count_launch();
-                }
                 ++total;
+                // residual estimate || beta e1 - H y || by Givens rotations (flexible candidate)
+                double hk_ = h(0, k);
+                for (int i = 0; i < k; ++i) hk_ = -sn[i] * hk_ + cs[i] * h(i + 1, k);
+                const double rr = std::hypot(hk_, h(k + 1, k));
+                cs[k] = rr == 0.0 ? 1.0 : hk_ / rr;
+                sn[k] = rr == 0.0 ? 0.0 : h(k + 1, k) / rr;
+                gq[k + 1] = -sn[k] * gq[k];
+                gq[k] = cs[k] * gq[k];
+                const bool cycle_end = breakdown || k == mm - 1 || total >= max_iter;
+                if (flexible && std::fabs(gq[k + 1]) > opts.tol * bnorm && !cycle_end) {
+                    hist.push_back(std::fabs(gq[k + 1]));  // estimate; the stop is confirmed explicitly
+                    continue;
+                }
                 std::vector<double> hk((size_t)(k + 2) * (k + 1));
                 for (int j = 0; j <= k; ++j)
                     for (int i = 0; i < k + 2; ++i) hk[(size_t)j * (k + 2) + i] = h(i, j);
@@ -960,13 +1010,14 @@ void DistBlock::solve(const double* b, double* x_out, pdg_report* rep) {
                     k_axpby<<<gr, 256, 0, st>>>(n, 1.0, x.p, 1.0, r.p, cand.p);
                     count_launch();
                 }
+                // the true residual (gmres.hpp:68-72)
                 apply(cand.p, t.p, st);
                 k_axpby<<<gr, 256, 0, st>>>(n, 1.0, b, -1.0, t.p, r.p);
                 count_launch();
                 true_res = nrm(r.p);
                 hist.push_back(true_res);
                 const bool ok = true_res / bnorm <= opts.tol;
-                if (ok || breakdown || k == mm - 1 || total >= max_iter) {
+                if (ok || cycle_end) {  // else the cycle goes on (gmres.hpp:118-131)
                     PDG_CUDA(cudaMemcpyAsync(x.p, cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
                     x_zero = false;
                     done = true;

@@ -101,7 +101,7 @@ struct DistBlock {
     DBuf<double> dinv, fp, rq, qf, pf, mech, uf, rfull, zfull;
     DistSub flow, mech_solver;
     // GMRES
-    DBuf<double> V, Z, wv, x, r, cand, t, ydev, dots, dsum, gbuf;
+    DBuf<double> V, Z, wv, x, r, cand, t, ydev, dots, dsum, gbuf, part;
     double* hhost = nullptr;
     void create(const SpatialOps& o, Comm* c, int m, const double* theta, double tau, double lambda,
                 const pdg_gmres_opts& op, cudaStream_t st);
@@ -112,7 +112,7 @@ struct DistBlock {
 
   private:
     double dot_sum(const double* a, const double* b, cudaStream_t st);
-    void multidot(const double* Vb, int ncols, const double* wv_, double* h_host, cudaStream_t st);
+    void multidot_dev(const double* Vb, int ncols, const double* wv_, double* out, cudaStream_t st);
 };
 
 }  // namespace pdg
