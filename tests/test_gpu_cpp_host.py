@@ -30,3 +30,27 @@ def test_cpp_host_layer_solves_config0_slab(tmp_path):
     assert "fixed-stress: converged=1" in out.stdout
     worst = float(out.stdout.split("max|res|/scale=")[1].split()[0])
     assert worst < 1e-8
+
+
+def _build_adapter(tmp_path):
+    exe = str(tmp_path / "adapter_main")
+    lib = os.path.join(ROOT, "paper_1801_04984_b200", "_lib")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "integration", "adapter_main.cpp"), "-L", lib, "-lporodg_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    return exe
+
+
+def test_reference_binding_compiles_and_links(tmp_path):
+    """integration/porodg_gpu_slab.hpp (the slab.hpp binding of INTEGRATION.md) against
+    stand-ins with the reference's member names."""
+    assert os.path.exists(_build_adapter(tmp_path))
+
+
+@pytest.mark.gpu
+def test_reference_binding_solves_config0_slab_bitwise(tmp_path):
+    """Reference-shaped operators -> pdg_ops_upload (mesh inferred) -> GPU slab solve:
+    the same bits as the solve on the device-assembled operators."""
+    out = subprocess.run([_build_adapter(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "mesh 16x16" in out.stdout and "bitwise 1" in out.stdout
