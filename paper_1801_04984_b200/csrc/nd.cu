@@ -409,7 +409,13 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
     unsigned long long* gathered = freeb + kNdBufs;                          // [kNdBufs]
     NdTask* tbT = reinterpret_cast<NdTask*>(smem + 1024);                    // [kNdBufs]
     int* tbOk = reinterpret_cast<int*>(smem + 1024 + kNdBufs * sizeof(NdTask));  // [kNdBufs] dependencies seen met
-    NdTask* tsk = reinterpret_cast<NdTask*>(smem + kNdHeader);  // this CTA's task descriptors
+    // this CTA's task descriptors: copied into shared memory when they fit the budget the
+    // host planned (a.max_tasks > 0), read from global memory (L1-cached) otherwise, so the
+    // shared-memory plan does not grow with the mesh
+    const bool tsk_smem = a.max_tasks > 0;
+    NdTask* tsk_s = reinterpret_cast<NdTask*>(smem + kNdHeader);
+    const int t0_ = a.ctoff[blockIdx.x];
+    const NdTask* tsk = tsk_smem ? tsk_s : a.tasks + t0_;
     unsigned char* ring = smem + kNdHeader + nd_task_bytes(a.max_tasks);
     unsigned char* arena = ring + (size_t)a.stages * a.stage_bytes;
     auto vbuf = [&](const NdTask& t) { return reinterpret_cast<double*>(arena + t.boff); };
@@ -431,10 +437,10 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    {
+    if (tsk_smem) {
         static_assert(sizeof(NdTask) % 4 == 0, "NdTask is copied as ints");
         const int* src = reinterpret_cast<const int*>(a.tasks + t0);
-        int* dst = reinterpret_cast<int*>(tsk);
+        int* dst = reinterpret_cast<int*>(tsk_s);
         const int words = nt * static_cast<int>(sizeof(NdTask) / 4);
         for (int w = tid; w < words; w += kNdBlock) dst[w] = src[w];
     }
@@ -1054,242 +1060,264 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     cbuf.alloc((size_t)std::max<long long>(cbtot, 1) * max_rhs);
     cbuf.zero(st);  // slots no child writes stay zero
     tiles = nd_tile_default();
+    levels = nd_levels_default();
     if (tiles) {
         build_tiles(children, parent, hs, hbp, hcbdst, st);
         store.release();  // the tile store replaces the row-major one
         return;
     }
     // ---- solve schedule: tasks in topological order, contiguous per phase on the CTAs ----
-    int dev = 0, nsm = 0;
-    PDG_CUDA(cudaGetDevice(&dev));
-    PDG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    int task_chunks = 16;
-    // no L2 prefetch cursor by default: measured 278 vs 291 us (pf 16) for the config-1
-    // displacement solve (tools/nd_sweep.sh, profiles/round2_nd_sweeps.txt)
-    pf = 0;
-    if (const char* e = std::getenv("PDG_ND_PF")) pf = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("PDG_ND_CHUNKS")) task_chunks = std::max(1, std::atoi(e));
-    stages = 16;
-    // 16 KB stages for wide fronts (rows of up to 8 KB: more rows per chunk), 12 KB otherwise
-    stage_bytes = static_cast<unsigned>(std::max<long long>(vmax >= 1024 ? 16384 : 12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
-    if (const char* e = std::getenv("PDG_ND_STAGES")) stages = std::min(32, std::max(2, std::atoi(e)));
-    if (const char* e = std::getenv("PDG_ND_STAGE_KB")) stage_bytes = 1024u * std::max(8, std::atoi(e));
-    int ctas_per_sm = 1;
-    if (const char* e = std::getenv("PDG_ND_CTAS")) ctas_per_sm = std::max(1, std::atoi(e));
-    grid = nsm * ctas_per_sm;
-    for (const auto& F : fronts)
-        require((long long)F.ldt * 8 <= stage_bytes, "nested dissection: front wider than a ring stage");
-    std::vector<int> fwd_tasks(nf, 0), bwd_tasks(nf, 0);
-    std::vector<bool> leaf(nf);
-    for (int k = 0; k < nf; ++k) leaf[k] = children[k].empty();
-    std::vector<std::vector<NdTask>> per_cta(grid);
-    auto place = [&](std::vector<NdTask>& ts) {
-        double wsum = 0.0;
-        for (const auto& t : ts) wsum += 8.0 * t.nrows * t.ld + 64.0 * t.ld;
-        double acc = 0.0;
-        for (const auto& t : ts) {
-            const double w = 8.0 * t.nrows * t.ld + 64.0 * t.ld;
-            int q = static_cast<int>((acc + 0.5 * w) / wsum * grid);
-            q = std::min(std::max(q, 0), grid - 1);
-            per_cta[q].push_back(t);
-            acc += w;
-        }
-    };
-    auto base_task = [&](int k, int type) {
-        const NdFront& F = fronts[k];
-        NdTask t{};
-        t.type = type;
-        t.front = k;
-        t.s = F.s;
-        t.b = F.b;
-        t.sdof = F.sdof;
-        t.bdof = F.bdof;
-        t.cboff = F.cboff;
-        t.wait0 = t.wait1 = -1;
-        t.need0 = t.need1 = 0;
-        t.leaf = leaf[k] ? 1 : 0;
-        return t;
-    };
-    auto level_bytes = [&](int type, int depth) {
-        double by = 0.0;
+    // (wide fronts of large meshes do not fit the ring / arena of this kernel: the
+    // level-synchronous tile kernels, which stream tiles from global memory, take over)
+    auto schedule_chunks = [&]() {
+        int dev = 0, nsm = 0;
+        PDG_CUDA(cudaGetDevice(&dev));
+        PDG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        int task_chunks = 16;
+        // no L2 prefetch cursor by default: measured 278 vs 291 us (pf 16) for the config-1
+        // displacement solve (tools/nd_sweep.sh, profiles/round2_nd_sweeps.txt)
+        pf = 0;
+        if (const char* e = std::getenv("PDG_ND_PF")) pf = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("PDG_ND_CHUNKS")) task_chunks = std::max(1, std::atoi(e));
+        stages = 16;
+        // 16 KB stages for wide fronts (rows of up to 8 KB: more rows per chunk), 12 KB otherwise
+        stage_bytes = static_cast<unsigned>(std::max<long long>(vmax >= 1024 ? 16384 : 12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
+        if (const char* e = std::getenv("PDG_ND_STAGES")) stages = std::min(32, std::max(2, std::atoi(e)));
+        if (const char* e = std::getenv("PDG_ND_STAGE_KB")) stage_bytes = 1024u * std::max(8, std::atoi(e));
+        int ctas_per_sm = 1;
+        if (const char* e = std::getenv("PDG_ND_CTAS")) ctas_per_sm = std::max(1, std::atoi(e));
+        grid = nsm * ctas_per_sm;
         for (const auto& F : fronts)
-            if (F.depth == depth) by += 8.0 * (type == 1 ? (double)(F.s + F.b) * F.ldm : (double)F.s * F.ldt);
-        return by;
-    };
-    // subtree mapping: the fronts at depth >= local_depth form subtrees that run entirely on one
-    // CTA each (their dependencies stay inside the CTA, in task order); the levels above are
-    // spread over all CTAs. Default: the deepest level with no more fronts than CTAs.
-    int local_depth = maxdepth + 1;
-    {
-        std::vector<int> per_depth(maxdepth + 1, 0);
-        for (const auto& F : fronts) per_depth[F.depth]++;
-        for (int d = maxdepth; d >= 0; --d)
-            if (per_depth[d] <= grid) {
-                local_depth = d;
-                break;
+            require((long long)F.ldt * 8 <= stage_bytes, "nested dissection: front wider than a ring stage");
+        std::vector<int> fwd_tasks(nf, 0), bwd_tasks(nf, 0);
+        std::vector<bool> leaf(nf);
+        for (int k = 0; k < nf; ++k) leaf[k] = children[k].empty();
+        std::vector<std::vector<NdTask>> per_cta(grid);
+        auto place = [&](std::vector<NdTask>& ts) {
+            double wsum = 0.0;
+            for (const auto& t : ts) wsum += 8.0 * t.nrows * t.ld + 64.0 * t.ld;
+            double acc = 0.0;
+            for (const auto& t : ts) {
+                const double w = 8.0 * t.nrows * t.ld + 64.0 * t.ld;
+                int q = static_cast<int>((acc + 0.5 * w) / wsum * grid);
+                q = std::min(std::max(q, 0), grid - 1);
+                per_cta[q].push_back(t);
+                acc += w;
             }
-        if (const char* e = std::getenv("PDG_ND_LOCAL_DEPTH")) {
-            const int v = std::atoi(e);
-            local_depth = v < 0 ? maxdepth + 1 : std::min(v, maxdepth + 1);
-        }
-    }
-    std::vector<int> cta_of(nf, -1);  // CTA of a local front
-    {
-        std::vector<int> roots;
-        for (int k = 0; k < nf; ++k)
-            if (fronts[k].depth == local_depth) roots.push_back(k);
-        const int nr = static_cast<int>(roots.size());
-        for (int j = 0; j < nr; ++j) cta_of[roots[j]] = static_cast<int>((long long)j * grid / std::max(nr, 1));
-        for (int d = local_depth + 1; d <= maxdepth; ++d)
-            for (int k = 0; k < nf; ++k)
-                if (fronts[k].depth == d && parent[k] >= 0) cta_of[k] = cta_of[parent[k]];
-    }
-    auto matrix_tasks = [&](int type, int depth) {
-        std::vector<NdTask> ts;
-        for (int k = 0; k < nf; ++k) {
+        };
+        auto base_task = [&](int k, int type) {
             const NdFront& F = fronts[k];
-            if (F.depth != depth) continue;
-            const int rows = type == 1 ? F.s + F.b : F.s;
-            const int ld = type == 1 ? F.ldm : F.ldt;
-            const long long base = type == 1 ? F.moff : F.mtoff;
-            const int rpc = static_cast<int>(stage_bytes / (8u * ld));
-            // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks;
-            // a local front (one CTA runs its whole subtree) in as few tasks as the buffers allow
-            const int want = static_cast<int>(std::ceil(level_bytes(type, depth) / grid / stage_bytes));
-            const int cap = depth >= local_depth ? kNdMaxTaskRows
-                                                 : std::min(kNdMaxTaskRows, rpc * std::max(1, std::min(task_chunks, want)));
-            for (int r0 = 0; r0 < rows; r0 += cap) {
-                NdTask t = base_task(k, type);
-                t.src = base + (long long)r0 * ld;
-                t.r0 = r0;
-                t.nrows = std::min(cap, rows - r0);
-                t.ld = ld;
-                t.ncols = type == 1 ? F.s : F.s + F.b;
-                t.signal = 3 * k + type;
-                ts.push_back(t);
-                (type == 1 ? fwd_tasks : bwd_tasks)[k]++;
-            }
-        }
-        return ts;
-    };
-    std::vector<std::vector<NdTask>> fwd_by_depth(maxdepth + 1), bwd_by_depth(maxdepth + 1);
-    for (int d = maxdepth; d >= 0; --d) fwd_by_depth[d] = matrix_tasks(1, d);
-    for (int d = 0; d <= maxdepth; ++d) bwd_by_depth[d] = matrix_tasks(2, d);
-    // dependencies: forward after both children's forward, backward after the parent's backward
-    for (auto& v : fwd_by_depth)
-        for (auto& t : v) {
-            const auto& ch = children[t.front];
-            if (ch.size() > 0) {
-                t.wait0 = 3 * ch[0] + 1;
-                t.need0 = fwd_tasks[ch[0]];
-            }
-            if (ch.size() > 1) {
-                t.wait1 = 3 * ch[1] + 1;
-                t.need1 = fwd_tasks[ch[1]];
-            }
-        }
-    for (auto& v : bwd_by_depth)
-        for (auto& t : v) {
-            const int p = parent[t.front];
-            if (p >= 0) {
-                t.wait0 = 3 * p + 2;
-                t.need0 = bwd_tasks[p];
-            } else {
-                t.wait0 = 3 * t.front + 1;
-                t.need0 = fwd_tasks[t.front];
-            }
-        }
-    auto place_local = [&](std::vector<NdTask>& ts) {
-        for (const auto& t : ts) per_cta[cta_of[t.front]].push_back(t);
-    };
-    for (int d = maxdepth; d >= 0; --d) {
-        if (d >= local_depth)
-            place_local(fwd_by_depth[d]);
-        else
-            place(fwd_by_depth[d]);
-    }
-    for (int d = 0; d <= maxdepth; ++d) {
-        if (d >= local_depth)
-            place_local(bwd_by_depth[d]);
-        else
-            place(bwd_by_depth[d]);
-    }
-    max_tasks = 0;
-    size_t max_buf = 0;
-    for (auto& v : per_cta) {
-        max_tasks = std::max(max_tasks, static_cast<int>(v.size()));
-        for (auto& t : v) {
-            t.vmt = nd_task_vmt(t);
-            max_buf = std::max(max_buf, nd_task_buf_bytes(t));
-        }
-    }
-    static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
-    // shared memory: header, task list, TMA ring, and the buffer arena (at least three of the
-    // largest task buffers, so a task's buffer never waits on the previous task's)
-    const size_t fixed = kNdHeader + nd_task_bytes(max_tasks);
-    size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
-    if (const char* e = std::getenv("PDG_ND_ARENA_KB")) arena_min = 1024 * (size_t)std::max(16, std::atoi(e));
-    require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
-    stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
-    require(stages >= kNdComputeWarps, "nested dissection: ring shallower than the compute warps (stage size too large)");
-    const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
-    arena_bytes = arena;
-    max_task_buf = max_buf;
-    smem = fixed + (size_t)stages * stage_bytes + arena;
-    // FIFO placement of the task buffers in the arena (tasks run and release in order)
-    for (auto& v : per_cta) {
-        size_t head = 0;
-        int prev_dep = -1;
-        for (int j = 0; j < static_cast<int>(v.size()); ++j) {
-            const size_t sz = nd_task_buf_bytes(v[j]);
-            if (head + sz > arena) head = 0;
-            v[j].boff = static_cast<int>(head);
-            int dep = -1;
-            for (int i = j - 1; i >= 0; --i)
-                if ((size_t)v[i].boff < head + sz && head < (size_t)v[i].boff + nd_task_buf_bytes(v[i])) {
-                    dep = i;
+            NdTask t{};
+            t.type = type;
+            t.front = k;
+            t.s = F.s;
+            t.b = F.b;
+            t.sdof = F.sdof;
+            t.bdof = F.bdof;
+            t.cboff = F.cboff;
+            t.wait0 = t.wait1 = -1;
+            t.need0 = t.need1 = 0;
+            t.leaf = leaf[k] ? 1 : 0;
+            return t;
+        };
+        auto level_bytes = [&](int type, int depth) {
+            double by = 0.0;
+            for (const auto& F : fronts)
+                if (F.depth == depth) by += 8.0 * (type == 1 ? (double)(F.s + F.b) * F.ldm : (double)F.s * F.ldt);
+            return by;
+        };
+        // subtree mapping: the fronts at depth >= local_depth form subtrees that run entirely on one
+        // CTA each (their dependencies stay inside the CTA, in task order); the levels above are
+        // spread over all CTAs. Default: the deepest level with no more fronts than CTAs.
+        int local_depth = maxdepth + 1;
+        {
+            std::vector<int> per_depth(maxdepth + 1, 0);
+            for (const auto& F : fronts) per_depth[F.depth]++;
+            for (int d = maxdepth; d >= 0; --d)
+                if (per_depth[d] <= grid) {
+                    local_depth = d;
                     break;
                 }
-            dep = std::max(dep, prev_dep);
-            require(dep < 0 || dep <= j - 2, "nested dissection: buffer arena too small (task " + std::to_string(j) + " dep " +
-                                      std::to_string(dep) + " head " + std::to_string(head) + " size " + std::to_string(sz) +
-                                      " arena " + std::to_string(arena) + " prev " + std::to_string(v[j - 1].boff) + "+" +
-                                      std::to_string(nd_task_buf_bytes(v[j - 1])) + ")");
-            v[j].fdep = prev_dep = dep;
-            head += sz;
+            if (const char* e = std::getenv("PDG_ND_LOCAL_DEPTH")) {
+                const int v = std::atoi(e);
+                local_depth = v < 0 ? maxdepth + 1 : std::min(v, maxdepth + 1);
+            }
         }
-    }
-    std::vector<NdTask> all;
-    std::vector<int> hct(grid + 1, 0);
-    for (int q = 0; q < grid; ++q) {
-        all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
-        hct[q + 1] = static_cast<int>(all.size());
-    }
-    // the attribute is per device and only ever raised: set the largest seen on this device
-    static size_t attr_smem[64] = {};
-    if (smem > attr_smem[dev % 64]) {
-        PDG_CUDA(cudaFuncSetAttribute(k_nd_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr_smem[dev % 64] = smem;
-    }
-    int per_sm = 0;
-    PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdBlock, smem));
-    require(per_sm >= 1 && grid <= per_sm * nsm, "nested dissection: solve grid not co-resident");
+        std::vector<int> cta_of(nf, -1);  // CTA of a local front
+        {
+            std::vector<int> roots;
+            for (int k = 0; k < nf; ++k)
+                if (fronts[k].depth == local_depth) roots.push_back(k);
+            const int nr = static_cast<int>(roots.size());
+            for (int j = 0; j < nr; ++j) cta_of[roots[j]] = static_cast<int>((long long)j * grid / std::max(nr, 1));
+            for (int d = local_depth + 1; d <= maxdepth; ++d)
+                for (int k = 0; k < nf; ++k)
+                    if (fronts[k].depth == d && parent[k] >= 0) cta_of[k] = cta_of[parent[k]];
+        }
+        auto matrix_tasks = [&](int type, int depth) {
+            std::vector<NdTask> ts;
+            for (int k = 0; k < nf; ++k) {
+                const NdFront& F = fronts[k];
+                if (F.depth != depth) continue;
+                const int rows = type == 1 ? F.s + F.b : F.s;
+                const int ld = type == 1 ? F.ldm : F.ldt;
+                const long long base = type == 1 ? F.moff : F.mtoff;
+                const int rpc = static_cast<int>(stage_bytes / (8u * ld));
+                // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks;
+                // a local front (one CTA runs its whole subtree) in as few tasks as the buffers allow
+                const int want = static_cast<int>(std::ceil(level_bytes(type, depth) / grid / stage_bytes));
+                const int cap = depth >= local_depth ? kNdMaxTaskRows
+                                                     : std::min(kNdMaxTaskRows, rpc * std::max(1, std::min(task_chunks, want)));
+                for (int r0 = 0; r0 < rows; r0 += cap) {
+                    NdTask t = base_task(k, type);
+                    t.src = base + (long long)r0 * ld;
+                    t.r0 = r0;
+                    t.nrows = std::min(cap, rows - r0);
+                    t.ld = ld;
+                    t.ncols = type == 1 ? F.s : F.s + F.b;
+                    t.signal = 3 * k + type;
+                    ts.push_back(t);
+                    (type == 1 ? fwd_tasks : bwd_tasks)[k]++;
+                }
+            }
+            return ts;
+        };
+        std::vector<std::vector<NdTask>> fwd_by_depth(maxdepth + 1), bwd_by_depth(maxdepth + 1);
+        for (int d = maxdepth; d >= 0; --d) fwd_by_depth[d] = matrix_tasks(1, d);
+        for (int d = 0; d <= maxdepth; ++d) bwd_by_depth[d] = matrix_tasks(2, d);
+        // dependencies: forward after both children's forward, backward after the parent's backward
+        for (auto& v : fwd_by_depth)
+            for (auto& t : v) {
+                const auto& ch = children[t.front];
+                if (ch.size() > 0) {
+                    t.wait0 = 3 * ch[0] + 1;
+                    t.need0 = fwd_tasks[ch[0]];
+                }
+                if (ch.size() > 1) {
+                    t.wait1 = 3 * ch[1] + 1;
+                    t.need1 = fwd_tasks[ch[1]];
+                }
+            }
+        for (auto& v : bwd_by_depth)
+            for (auto& t : v) {
+                const int p = parent[t.front];
+                if (p >= 0) {
+                    t.wait0 = 3 * p + 2;
+                    t.need0 = bwd_tasks[p];
+                } else {
+                    t.wait0 = 3 * t.front + 1;
+                    t.need0 = fwd_tasks[t.front];
+                }
+            }
+        auto place_local = [&](std::vector<NdTask>& ts) {
+            for (const auto& t : ts) per_cta[cta_of[t.front]].push_back(t);
+        };
+        for (int d = maxdepth; d >= 0; --d) {
+            if (d >= local_depth)
+                place_local(fwd_by_depth[d]);
+            else
+                place(fwd_by_depth[d]);
+        }
+        for (int d = 0; d <= maxdepth; ++d) {
+            if (d >= local_depth)
+                place_local(bwd_by_depth[d]);
+            else
+                place(bwd_by_depth[d]);
+        }
+        max_tasks = 0;
+        size_t max_buf = 0;
+        for (auto& v : per_cta) {
+            max_tasks = std::max(max_tasks, static_cast<int>(v.size()));
+            for (auto& t : v) {
+                t.vmt = nd_task_vmt(t);
+                max_buf = std::max(max_buf, nd_task_buf_bytes(t));
+            }
+        }
+        static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
+        // shared memory: header, task list, TMA ring, and the buffer arena (at least three of the
+        // largest task buffers, so a task's buffer never waits on the previous task's)
+        // descriptors in shared memory only up to 12 KB (config 1: 49 tasks = 4.7 KB); beyond it
+        // (large meshes) the kernel reads them from global memory
+        if (nd_task_bytes(max_tasks) > 12 * 1024 || std::getenv("PDG_ND_TASKS_GLOBAL")) smem_tasks = 0;
+        else smem_tasks = max_tasks;
+        const size_t fixed = kNdHeader + nd_task_bytes(smem_tasks);
+        size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
+        if (const char* e = std::getenv("PDG_ND_ARENA_KB")) arena_min = 1024 * (size_t)std::max(16, std::atoi(e));
+        require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
+        stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
+        require(stages >= kNdComputeWarps, "nested dissection: ring shallower than the compute warps (stage size too large)");
+        const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
+        arena_bytes = arena;
+        max_task_buf = max_buf;
+        smem = fixed + (size_t)stages * stage_bytes + arena;
+        // FIFO placement of the task buffers in the arena (tasks run and release in order)
+        for (auto& v : per_cta) {
+            size_t head = 0;
+            int prev_dep = -1;
+            for (int j = 0; j < static_cast<int>(v.size()); ++j) {
+                const size_t sz = nd_task_buf_bytes(v[j]);
+                if (head + sz > arena) head = 0;
+                v[j].boff = static_cast<int>(head);
+                int dep = -1;
+                for (int i = j - 1; i >= 0; --i)
+                    if ((size_t)v[i].boff < head + sz && head < (size_t)v[i].boff + nd_task_buf_bytes(v[i])) {
+                        dep = i;
+                        break;
+                    }
+                dep = std::max(dep, prev_dep);
+                require(dep < 0 || dep <= j - 2, "nested dissection: buffer arena too small (task " + std::to_string(j) + " dep " +
+                                          std::to_string(dep) + " head " + std::to_string(head) + " size " + std::to_string(sz) +
+                                          " arena " + std::to_string(arena) + " prev " + std::to_string(v[j - 1].boff) + "+" +
+                                          std::to_string(nd_task_buf_bytes(v[j - 1])) + ")");
+                v[j].fdep = prev_dep = dep;
+                head += sz;
+            }
+        }
+        std::vector<NdTask> all;
+        std::vector<int> hct(grid + 1, 0);
+        for (int q = 0; q < grid; ++q) {
+            all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
+            hct[q + 1] = static_cast<int>(all.size());
+        }
+        // the attribute is per device and only ever raised: set the largest seen on this device
+        static size_t attr_smem[64] = {};
+        if (smem > attr_smem[dev % 64]) {
+            PDG_CUDA(cudaFuncSetAttribute(k_nd_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            attr_smem[dev % 64] = smem;
+        }
+        int per_sm = 0;
+        PDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_solve, kNdBlock, smem));
+        require(per_sm >= 1 && grid <= per_sm * nsm, "nested dissection: solve grid not co-resident");
     d_tasks.upload(all, st);
-    ctoff.upload(hct, st);
-    PDG_CUDA(cudaStreamSynchronize(st));
+        ctoff.upload(hct, st);
+        PDG_CUDA(cudaStreamSynchronize(st));
+    };
+    try {
+        schedule_chunks();
+    } catch (const Error& e) {
+        if (e.status != PDG_INVALID_ARGUMENT || std::getenv("PDG_ND_STRICT")) throw;
+        fallback_reason = e.what();
+        tiles = levels = true;
+        build_tiles(children, parent, hs, hbp, hcbdst, st);
+        store.release();
+    }
 }
 
 void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
     ++call;
+    if (levels) {
+        solve_levels(b, ldb, x, ldx, nrhs, st);
+        return;
+    }
     if (tiles) {
         solve_tiles(b, ldb, x, ldx, nrhs, st);
         return;
     }
     NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
-             max_tasks, pf,      stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
+             smem_tasks, pf,     stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
              std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard,
              std::getenv("PDG_ND_TILE8") != nullptr,
              std::getenv("PDG_ND_TILE8") == nullptr && std::getenv("PDG_ND_PAIRS") && std::atoi(std::getenv("PDG_ND_PAIRS")) > 0};

@@ -27,6 +27,7 @@
 // order (bit-identical repeats).
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -73,10 +74,11 @@ struct NdTileTask {
     int l2keep;   // tiles loaded with L2 evict_last (top levels)
 };
 bool nd_tile_default();
+bool nd_levels_default();
 
 struct NdChol {
     int n = 0, max_rhs = 0, nfront = 0, maxdepth = 0;
-    int grid = 0, stages = 3, vmax = 0, max_tasks = 0, pf = 16;
+    int grid = 0, stages = 3, vmax = 0, max_tasks = 0, smem_tasks = 0, pf = 16;
     unsigned stage_bytes = 24576;
     unsigned long long call = 0;
     size_t smem = 0, arena_bytes = 0, max_task_buf = 0;
@@ -113,6 +115,12 @@ struct NdChol {
                      const std::vector<int>& hs, const std::vector<int>& hbp, const std::vector<int>& hcbdst,
                      cudaStream_t st);
     void solve_tiles(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+    // level-synchronous solve (PDG_ND_LEVELS): per level and pass a unit range and its buffer size
+    bool levels = false;
+    std::string fallback_reason;  // why the chunk kernel's schedule did not fit (levels used instead)
+    std::vector<int> lvl_off;
+    std::vector<size_t> lvl_smem;
+    void solve_levels(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };
 

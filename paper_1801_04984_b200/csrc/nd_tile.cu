@@ -446,6 +446,130 @@ __global__ void __launch_bounds__(kTBlock, 1) k_nd_tile_solve(TileArgs a) {
     }
 }
 
+// ---- level-synchronous solve (PDG_ND_LEVELS): one launch per tree level and pass ----
+// All fronts of a level are independent: every block takes units (a front's row range),
+// gathers the front's input vector into shared memory (all 256 threads, one round of
+// loads), and its 8 warps stream the unit's tiles straight from global memory (coalesced
+// 512 B warp loads, the lane-per-row layout above). The levels are chained with
+// programmatic dependent launch: a level's blocks start (and prefetch their tiles into L2)
+// while the previous level runs, then wait (griddepcontrol.wait) for its results.
+constexpr int kLvlThreads = 256;
+__global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, int u1, int prefetch) {
+    extern __shared__ __align__(16) unsigned char lsm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nr = a.nrhs;
+    if (prefetch)  // static data: the factor tiles of this block's units, into L2
+        for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+            const NdTileTask& T = a.tasks[u];
+            const long long bytes = (long long)T.ntiles * T.tile_d2 * 16;
+            for (long long off = (long long)tid * 16384; off < bytes; off += (long long)kLvlThreads * 16384) {
+                const unsigned n = static_cast<unsigned>(min(16384LL, bytes - off));
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(a.tstore + T.src) + off),
+                             "r"(n)
+                             : "memory");
+            }
+        }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
+    for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+        const NdTileTask T = a.tasks[u];
+        unsigned char* buf = lsm;
+        double* v = reinterpret_cast<double*>(buf);
+        int* oix = reinterpret_cast<int*>(buf + tb_oix(T));
+        int* bix = reinterpret_cast<int*>(buf + tb_bix(T));
+        // static inputs: output indices, b_S (forward) / boundary positions (backward), padding
+        for (int r = tid; r < T.nrows; r += kLvlThreads) oix[r] = __ldg(a.toix + T.oix_off + r);
+        if (T.type == 1) {
+            const int tot = kTMaxRhs * T.cp;
+            for (int c0 = tid; c0 < tot; c0 += kLvlThreads * 8) {
+                double xv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int c = c0 + q * kLvlThreads, k = c / T.cp, cc = c - k * T.cp;
+                    xv[q] = (c < tot && k < nr && cc < T.s) ? a.b[k * a.ldb + __ldg(a.sdofs + T.sdof + cc)] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (c0 + q * kLvlThreads < tot) v[c0 + q * kLvlThreads] = xv[q];
+            }
+        } else {
+            for (int c = tid; c < T.b; c += kLvlThreads) bix[c] = __ldg(a.bpos + T.bdof + c);
+            for (int k = 0; k < kTMaxRhs; ++k)
+                for (int c = (k < nr ? T.ncols : 0) + tid; c < T.cp; c += kLvlThreads) v[k * T.cp + c] = 0.0;
+        }
+        __syncthreads();
+        gather_dependent<kLvlThreads>(a, T, buf, tid);
+        __syncthreads();
+        const double* tail = reinterpret_cast<const double*>(buf + tb_tail(T));
+        const int rb = T.rb, J = 32 / rb, jl = lane / rb, rl = lane - jl * rb;
+        const int nslab = T.tile_d2 >> 5;
+        const double2* v0 = reinterpret_cast<const double2*>(v);
+        const double2* v1 = reinterpret_cast<const double2*>(v + T.cp);
+        for (int q = warp; q < T.ntiles; q += kLvlThreads / 32) {
+            const double2* tile = reinterpret_cast<const double2*>(a.tstore + T.src) + (size_t)q * T.tile_d2 + lane;
+            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, q0 = 0.0, qq1 = 0.0, q2 = 0.0, q3 = 0.0;
+            int t = 0;
+            for (; t + 3 < nslab; t += 4) {
+                const double2 m0 = __ldcs(tile + t * 32), m1 = __ldcs(tile + (t + 1) * 32);
+                const double2 m2 = __ldcs(tile + (t + 2) * 32), m3 = __ldcs(tile + (t + 3) * 32);
+                const double2 a0 = v0[t * J + jl], b0 = v1[t * J + jl], a1 = v0[(t + 1) * J + jl], b1 = v1[(t + 1) * J + jl];
+                const double2 a2 = v0[(t + 2) * J + jl], b2 = v1[(t + 2) * J + jl], a3 = v0[(t + 3) * J + jl],
+                              b3 = v1[(t + 3) * J + jl];
+                p0 = fma(m0.x, a0.x, p0);
+                p1 = fma(m0.y, a0.y, p1);
+                q0 = fma(m0.x, b0.x, q0);
+                qq1 = fma(m0.y, b0.y, qq1);
+                p2 = fma(m1.x, a1.x, p2);
+                p3 = fma(m1.y, a1.y, p3);
+                q2 = fma(m1.x, b1.x, q2);
+                q3 = fma(m1.y, b1.y, q3);
+                p0 = fma(m2.x, a2.x, p0);
+                p1 = fma(m2.y, a2.y, p1);
+                q0 = fma(m2.x, b2.x, q0);
+                qq1 = fma(m2.y, b2.y, qq1);
+                p2 = fma(m3.x, a3.x, p2);
+                p3 = fma(m3.y, a3.y, p3);
+                q2 = fma(m3.x, b3.x, q2);
+                q3 = fma(m3.y, b3.y, q3);
+            }
+            for (; t < nslab; ++t) {
+                const double2 m0 = __ldcs(tile + t * 32);
+                const double2 a0 = v0[t * J + jl], b0 = v1[t * J + jl];
+                p0 = fma(m0.x, a0.x, p0);
+                p1 = fma(m0.y, a0.y, p1);
+                q0 = fma(m0.x, b0.x, q0);
+                qq1 = fma(m0.y, b0.y, qq1);
+            }
+            double s0 = (p0 + p1) + (p2 + p3), s1 = (q0 + qq1) + (q2 + q3);
+            for (int o = rb; o < 32; o <<= 1) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            }
+            const int row = q * rb + rl;
+            if (jl == 0 && row < T.nrows) {
+                const int gr = T.r0 + row;
+                if (T.type == 2) {
+                    a.xpos[T.sdof + gr] = s0;
+                    a.x[oix[row]] = s0;
+                    if (nr > 1) {
+                        a.xpos[(long long)a.n + T.sdof + gr] = s1;
+                        a.x[a.ldx + oix[row]] = s1;
+                    }
+                } else if (gr < T.s) {
+                    a.y[T.sdof + gr] = s0;
+                    if (nr > 1) a.y[(long long)a.n + T.sdof + gr] = s1;
+                } else {
+                    const int ti = gr - T.tail_lo;
+                    a.cb[oix[row]] = s0 + (T.leaf ? 0.0 : tail[ti]);
+                    if (nr > 1) a.cb[a.cbtot + oix[row]] = s1 + (T.leaf ? 0.0 : tail[T.tail_n + ti]);
+                }
+            }
+        }
+        __syncthreads();  // the buffer is reused by the next unit
+    }
+}
+
 // tile store from the row-major M / M^T store: one block per tile
 struct TilePack {
     long long dst;  // doubles
@@ -471,10 +595,15 @@ __global__ void k_nd_tile_pack(const TilePack* __restrict__ jobs, const double* 
 
 }  // namespace
 
+bool nd_levels_default() {
+    const char* e = std::getenv("PDG_ND_LEVELS");
+    return e && std::atoi(e) > 0;
+}
+
 bool nd_tile_default() {
     // opt-in (PDG_ND_TILES=1): measured no faster than the row-chunk kernel at config 1
     const char* e = std::getenv("PDG_ND_TILES");
-    return e && std::atoi(e) > 0;
+    return (e && std::atoi(e) > 0) || nd_levels_default();
 }
 
 void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const std::vector<int>& parent,
@@ -499,7 +628,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
     const long long wide = ((long long)(cmax + 63) / 64 * 64) * 8;  // one row of the widest pass
     tile_cap = static_cast<unsigned>(std::max<long long>(tile_cap, wide));
     tstage_bytes = std::max(tstage_bytes, tile_cap);
-    require(tstage_bytes <= 65536, "nested dissection: front too wide for the tile ring");
+    require(levels || tstage_bytes <= 65536, "nested dissection: front too wide for the tile ring");
     // subtree mapping (see the file comment)
     int local_depth = maxdepth + 1;
     {
@@ -646,6 +775,56 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
             }
         }
     };
+    if (levels) {  // level-synchronous units: fwd levels deepest first, then bwd levels
+        std::vector<NdTileTask> units;
+        lvl_off.clear();
+        lvl_smem.clear();
+        int min_rows = 8;
+        if (const char* e = std::getenv("PDG_ND_LVL_MINROWS")) min_rows = std::max(1, std::atoi(e));
+        auto add_level = [&](int type, int depth) {
+            const double want = level_bytes(type, depth) / (2.0 * tgrid);
+            size_t smax = 0;
+            lvl_off.push_back(static_cast<int>(units.size()));
+            for (int k = 0; k < nf; ++k) {
+                if (fronts[k].depth != depth) continue;
+                const NdFront& F = fronts[k];
+                const int cols = type == 1 ? F.s : F.s + F.b;
+                const int rows = type == 1 ? F.s + F.b : F.s;
+                const int rpt = std::max(min_rows, static_cast<int>(std::ceil(want / (8.0 * std::max(cols, 1)))));
+                for (auto& t : make_tasks(k, type, std::min(rows, rpt))) {
+                    smax = std::max(smax, tb_size(t));
+                    units.push_back(t);
+                }
+            }
+            lvl_smem.push_back(a16(smax));
+        };
+        for (int d = maxdepth; d >= 0; --d) add_level(1, d);
+        for (int d = 0; d <= maxdepth; ++d) add_level(2, d);
+        lvl_off.push_back(static_cast<int>(units.size()));
+        size_t smax = 0;
+        for (size_t v : lvl_smem) smax = std::max(smax, v);
+        require(smax <= 227 * 1024, "nested dissection: level unit buffer exceeds shared memory");
+        tstore.alloc((size_t)std::max<long long>(toff, 1));
+        {
+            DBuf<TilePack> dp;
+            dp.upload(packs, st);
+            const long long np = static_cast<long long>(packs.size());
+            for (long long o = 0; o < np; o += 65535) {
+                const unsigned g = static_cast<unsigned>(std::min<long long>(65535, np - o));
+                k_nd_tile_pack<<<g, 256, 0, st>>>(dp.p + o, store.p, tstore.p);
+                PDG_CHECK_LAUNCH();
+            }
+            PDG_CUDA(cudaStreamSynchronize(st));
+        }
+        tile_bytes = 8.0 * (double)toff;
+        d_ttasks.upload(units, st);
+        d_toix.upload(oix, st);
+        PDG_CUDA(cudaFuncSetAttribute(k_nd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PDG_CUDA(cudaStreamSynchronize(st));
+        (void)hbp;
+        (void)cta_of;
+        return;
+    }
     for (int d = maxdepth; d >= 0; --d) place_level(1, d);
     for (int d = 0; d <= maxdepth; ++d) place_level(2, d);
     // dependencies: forward after both children's forward, backward after the parent's backward
@@ -742,6 +921,48 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
     require(per_sm >= 1 && tgrid <= per_sm * nsm, "nested dissection: tile solve grid not co-resident");
     (void)hbp;
     PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void NdChol::solve_levels(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
+    TileArgs a{};
+    a.tasks = d_ttasks.p;
+    a.toix = d_toix.p;
+    a.sdofs = sdofs.p;
+    a.bpos = bpos.p;
+    a.tstore = tstore.p;
+    a.b = b;
+    a.ldb = ldb;
+    a.x = x;
+    a.ldx = ldx;
+    a.y = y.p;
+    a.xpos = xpos.p;
+    a.cb = cbuf.p;
+    a.cbtot = cbtot;
+    a.n = n;
+    a.nrhs = nrhs;
+    a.stop = guard;
+    static const int pf = !(std::getenv("PDG_ND_LVL_PF") && std::atoi(std::getenv("PDG_ND_LVL_PF")) == 0);
+    static const int bpsm = std::getenv("PDG_ND_LVL_BLOCKS") ? std::max(1, std::atoi(std::getenv("PDG_ND_LVL_BLOCKS"))) : 2;
+    static const int use_pdl = !(std::getenv("PDG_ND_LVL_PDL") && std::atoi(std::getenv("PDG_ND_LVL_PDL")) == 0);
+    const int nl = static_cast<int>(lvl_smem.size());
+    for (int l = 0; l < nl; ++l) {
+        int u0 = lvl_off[l], u1 = lvl_off[l + 1];
+        if (u1 <= u0) continue;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(std::min(u1 - u0, bpsm * tgrid)));
+        cfg.blockDim = dim3(kLvlThreads);
+        cfg.dynamicSmemBytes = lvl_smem[l];
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = use_pdl ? 1 : 0;
+        int p = pf;
+        PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level, a, u0, u1, p));
+        count_launch(1);
+    }
+    PDG_CHECK_LAUNCH();
 }
 
 void NdChol::solve_tiles(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {

@@ -150,9 +150,12 @@ class SpaceTimeOperator:
         return [buf[i] for i in range(repeats)] if times else None
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.pdg_op_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.pdg_op_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def profile(enable: bool | None = None, reset: bool = False):
@@ -239,9 +242,12 @@ class SpatialOperators:
         return res, sc.value
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.pdg_ops_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.pdg_ops_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class BlockSolver:
@@ -301,9 +307,12 @@ class BlockSolver:
         return off, idx, val
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.pdg_block_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.pdg_block_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class SlabSolver:
@@ -353,9 +362,12 @@ class SlabSolver:
         return sc.value
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.pdg_slab_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.pdg_slab_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class FixedStressSolver:
@@ -388,9 +400,12 @@ class FixedStressSolver:
         return _to_report(rep, hist)
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.pdg_fs_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.pdg_fs_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def uniform_partition(T: float, n_slabs: int):

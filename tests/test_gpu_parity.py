@@ -751,3 +751,32 @@ def test_spmv_config3_1024_properties(monkeypatch):
     op.apply_device(x.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
     assert not torch.any(y2 != 0)
+
+
+def test_nd_level_kernels_match_chunk_kernel(monkeypatch):
+    """The level-synchronous nested-dissection solve (PDG_ND_LEVELS=1; the automatic
+    fallback when the chunk kernel's ring / arena do not fit wide fronts) against the
+    default chunk kernel: the same exact solves to roundoff, repeats bit-identical."""
+    spec = P.config1(32)
+    ops = S.SpatialOperators.assemble(spec)
+    r = np.random.default_rng(9).standard_normal(2 * ops.n_total)
+    T = S.time_constants(1)["T"]
+    z_chunk = S.BlockSolver(ops, T, 0.05).precondition(r)
+    monkeypatch.setenv("PDG_ND_LEVELS", "1")
+    blk = S.BlockSolver(ops, T, 0.05)
+    z_lvl = blk.precondition(r)
+    assert np.array_equal(z_lvl, blk.precondition(r))
+    assert np.linalg.norm(z_lvl - z_chunk) <= 1e-10 * np.linalg.norm(z_chunk)
+
+
+@pytest.mark.parametrize("n", [192, 256])
+def test_large_mesh_slab_solve(n):
+    """Meshes whose top separator fronts are too wide for the chunk kernel (the level
+    kernels take over): the dG(1) march converges in the config-1 iteration counts
+    with the local mass balance of the 128^2 runs."""
+    ops = S.SpatialOperators.assemble(P.config3(n))
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
+    reps, _ = S.march(ops, 1, 0.1, 2, opt, mass_check=True)
+    for rep in reps:
+        assert rep.converged and 3 <= rep.iterations <= 6
+        assert rep.mass_rel < 1e-7
