@@ -454,54 +454,111 @@ __global__ void __launch_bounds__(kTBlock, 1) k_nd_tile_solve(TileArgs a) {
 // programmatic dependent launch: a level's blocks start (and prefetch their tiles into L2)
 // while the previous level runs, then wait (griddepcontrol.wait) for its results.
 constexpr int kLvlThreads = 256;
-__global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, int u1, int prefetch) {
+// level unit buffer: the task buffer (tb_size) plus, forward, the b_S gather indices
+__host__ __device__ inline size_t lvl_sidx(const NdTileTask& t) { return tb_size(t); }
+__host__ __device__ inline size_t lvl_size(const NdTileTask& t) {
+    return tb_size(t) + (t.type == 1 ? (((size_t)t.s * 4 + 15) / 16) * 16 : 0);
+}
+
+__global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, int u1, int prefetch, int lvl) {
     extern __shared__ __align__(16) unsigned char lsm[];
+    __shared__ NdTileTask Ts;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nr = a.nrhs;
-    if (prefetch)  // static data: the factor tiles of this block's units, into L2
-        for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
-            const NdTileTask& T = a.tasks[u];
+    bool waited = false;
+    for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
+        if (tid < (int)(sizeof(NdTileTask) / 4))
+            reinterpret_cast<int*>(&Ts)[tid] = __ldg(reinterpret_cast<const int*>(a.tasks + u) + tid);
+        __syncthreads();
+        const NdTileTask& T = Ts;
+        unsigned char* buf = lsm;
+        double* v = reinterpret_cast<double*>(buf);
+        double* tail = reinterpret_cast<double*>(buf + tb_tail(T));
+        int* oix = reinterpret_cast<int*>(buf + tb_oix(T));
+        int* bix = reinterpret_cast<int*>(buf + tb_bix(T));
+        int* sidx = reinterpret_cast<int*>(buf + lvl_sidx(T));
+        // ---- static data (before the dependency wait): the unit's tiles into L2, the index lists ----
+        if (prefetch) {
             const long long bytes = (long long)T.ntiles * T.tile_d2 * 16;
             for (long long off = (long long)tid * 16384; off < bytes; off += (long long)kLvlThreads * 16384) {
-                const unsigned n = static_cast<unsigned>(min(16384LL, bytes - off));
+                const unsigned nb = static_cast<unsigned>(min(16384LL, bytes - off));
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(a.tstore + T.src) + off),
-                             "r"(n)
+                             "r"(nb)
                              : "memory");
             }
         }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
-    for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
-        const NdTileTask T = a.tasks[u];
-        unsigned char* buf = lsm;
-        double* v = reinterpret_cast<double*>(buf);
-        int* oix = reinterpret_cast<int*>(buf + tb_oix(T));
-        int* bix = reinterpret_cast<int*>(buf + tb_bix(T));
-        // static inputs: output indices, b_S (forward) / boundary positions (backward), padding
         for (int r = tid; r < T.nrows; r += kLvlThreads) oix[r] = __ldg(a.toix + T.oix_off + r);
+        if (T.type == 1)
+            for (int c = tid; c < T.s; c += kLvlThreads) sidx[c] = __ldg(a.sdofs + T.sdof + c);
+        else
+            for (int c = tid; c < T.b; c += kLvlThreads) bix[c] = __ldg(a.bpos + T.bdof + c);
+        if (!waited) {  // the previous level's results (and b) are visible past this point
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+        __syncthreads();
+        if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
+        if (a.dbg && tid == 0) {  // PDG_ND_DEBUG: per level [first start past the wait, last end, launch seen]
+            atomicMin(a.dbg + 3 * lvl, dev::globaltimer());
+        }
+        // ---- the input vector in one round of loads ----
         if (T.type == 1) {
-            const int tot = kTMaxRhs * T.cp;
-            for (int c0 = tid; c0 < tot; c0 += kLvlThreads * 8) {
-                double xv[8];
+            const double* c0p = a.cb + T.cboff;
+            const double* c1p = c0p + (T.s + T.b);
+            const bool inner = !T.leaf;
+            const int tot = kTMaxRhs * T.cp, nt2 = nr * T.tail_n;
+            for (int e0 = tid; e0 < tot + nt2; e0 += kLvlThreads * 8) {
+                double w0[8], w1[8], bv[8];
+                int dst[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const int c = c0 + q * kLvlThreads, k = c / T.cp, cc = c - k * T.cp;
-                    xv[q] = (c < tot && k < nr && cc < T.s) ? a.b[k * a.ldb + __ldg(a.sdofs + T.sdof + cc)] : 0.0;
+                    const int e = e0 + q * kLvlThreads;
+                    int k = 0, col = 0;
+                    dst[q] = -1;
+                    bv[q] = 0.0;
+                    if (e < tot) {
+                        k = e / T.cp;
+                        col = e - k * T.cp;
+                        dst[q] = e;
+                        if (k < nr && col < T.s) bv[q] = a.b[k * a.ldb + sidx[col]];
+                    } else if (e < tot + nt2) {
+                        const int f = e - tot;
+                        k = f / T.tail_n;
+                        const int ti = f - k * T.tail_n;
+                        col = T.tail_lo + ti;
+                        dst[q] = -2 - (k * T.tail_n + ti);
+                    }
+                    const bool ld = inner && ((dst[q] >= 0 && k < nr && col < T.s) || dst[q] <= -2);
+                    w0[q] = ld ? __ldcg(c0p + k * a.cbtot + col) : 0.0;
+                    w1[q] = ld ? __ldcg(c1p + k * a.cbtot + col) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (dst[q] >= 0)
+                        v[dst[q]] = inner ? (bv[q] - w0[q]) - w1[q] : bv[q];
+                    else if (dst[q] <= -2)
+                        tail[-2 - dst[q]] = w0[q] + w1[q];
+                }
+            }
+        } else {
+            const int len = T.s + T.b, tot = kTMaxRhs * T.cp;
+            for (int e0 = tid; e0 < tot; e0 += kLvlThreads * 8) {
+                double w[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = e0 + q * kLvlThreads, k = e / T.cp, c = e - k * T.cp;
+                    w[q] = 0.0;
+                    if (e < tot && k < nr && c < len)
+                        w[q] = c < T.s ? __ldcg(a.y + (long long)k * a.n + T.sdof + c)
+                                       : -__ldcg(a.xpos + (long long)k * a.n + bix[c - T.s]);
                 }
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
-                    if (c0 + q * kLvlThreads < tot) v[c0 + q * kLvlThreads] = xv[q];
+                    if (e0 + q * kLvlThreads < tot) v[e0 + q * kLvlThreads] = w[q];
             }
-        } else {
-            for (int c = tid; c < T.b; c += kLvlThreads) bix[c] = __ldg(a.bpos + T.bdof + c);
-            for (int k = 0; k < kTMaxRhs; ++k)
-                for (int c = (k < nr ? T.ncols : 0) + tid; c < T.cp; c += kLvlThreads) v[k * T.cp + c] = 0.0;
         }
         __syncthreads();
-        gather_dependent<kLvlThreads>(a, T, buf, tid);
-        __syncthreads();
-        const double* tail = reinterpret_cast<const double*>(buf + tb_tail(T));
         const int rb = T.rb, J = 32 / rb, jl = lane / rb, rl = lane - jl * rb;
         const int nslab = T.tile_d2 >> 5;
         const double2* v0 = reinterpret_cast<const double2*>(v);
@@ -566,7 +623,12 @@ __global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, in
                 }
             }
         }
-        __syncthreads();  // the buffer is reused by the next unit
+        __syncthreads();  // the buffers are reused by the next unit
+        if (a.dbg && tid == 0) atomicMax(a.dbg + 3 * lvl + 1, dev::globaltimer());
+    }
+    if (!waited) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
     }
 }
 
@@ -781,8 +843,10 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         lvl_smem.clear();
         int min_rows = 8;
         if (const char* e = std::getenv("PDG_ND_LVL_MINROWS")) min_rows = std::max(1, std::atoi(e));
+        double upb = 2.0;  // units per CTA slot of the grid, for the levels large enough to split
+        if (const char* e = std::getenv("PDG_ND_LVL_UPB")) upb = std::max(0.25, std::atof(e));
         auto add_level = [&](int type, int depth) {
-            const double want = level_bytes(type, depth) / (2.0 * tgrid);
+            const double want = level_bytes(type, depth) / (upb * tgrid);
             size_t smax = 0;
             lvl_off.push_back(static_cast<int>(units.size()));
             for (int k = 0; k < nf; ++k) {
@@ -792,7 +856,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
                 const int rows = type == 1 ? F.s + F.b : F.s;
                 const int rpt = std::max(min_rows, static_cast<int>(std::ceil(want / (8.0 * std::max(cols, 1)))));
                 for (auto& t : make_tasks(k, type, std::min(rows, rpt))) {
-                    smax = std::max(smax, tb_size(t));
+                    smax = std::max(smax, lvl_size(t));
                     units.push_back(t);
                 }
             }
@@ -803,7 +867,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         lvl_off.push_back(static_cast<int>(units.size()));
         size_t smax = 0;
         for (size_t v : lvl_smem) smax = std::max(smax, v);
-        require(smax <= 227 * 1024, "nested dissection: level unit buffer exceeds shared memory");
+        require(smax <= 226 * 1024, "nested dissection: level unit buffer exceeds shared memory");
         tstore.alloc((size_t)std::max<long long>(toff, 1));
         {
             DBuf<TilePack> dp;
@@ -819,7 +883,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         tile_bytes = 8.0 * (double)toff;
         d_ttasks.upload(units, st);
         d_toix.upload(oix, st);
-        PDG_CUDA(cudaFuncSetAttribute(k_nd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PDG_CUDA(cudaFuncSetAttribute(k_nd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         PDG_CUDA(cudaStreamSynchronize(st));
         (void)hbp;
         (void)cta_of;
@@ -942,9 +1006,17 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
     a.nrhs = nrhs;
     a.stop = guard;
     static const int pf = !(std::getenv("PDG_ND_LVL_PF") && std::atoi(std::getenv("PDG_ND_LVL_PF")) == 0);
-    static const int bpsm = std::getenv("PDG_ND_LVL_BLOCKS") ? std::max(1, std::atoi(std::getenv("PDG_ND_LVL_BLOCKS"))) : 2;
+    static const int bpsm = std::getenv("PDG_ND_LVL_BLOCKS") ? std::max(1, std::atoi(std::getenv("PDG_ND_LVL_BLOCKS"))) : 8;
     static const int use_pdl = !(std::getenv("PDG_ND_LVL_PDL") && std::atoi(std::getenv("PDG_ND_LVL_PDL")) == 0);
     const int nl = static_cast<int>(lvl_smem.size());
+    const bool dbg_on = std::getenv("PDG_ND_DEBUG") != nullptr;
+    DBuf<unsigned long long> dbg;
+    if (dbg_on) {
+        std::vector<unsigned long long> init(3 * nl, 0ull);
+        for (int l = 0; l < nl; ++l) init[3 * l] = ~0ull;
+        dbg.upload(init, st);
+        a.dbg = dbg.p;
+    }
     for (int l = 0; l < nl; ++l) {
         int u0 = lvl_off[l], u1 = lvl_off[l + 1];
         if (u1 <= u0) continue;
@@ -959,10 +1031,24 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
         cfg.attrs = attr;
         cfg.numAttrs = use_pdl ? 1 : 0;
         int p = pf;
-        PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level, a, u0, u1, p));
+        PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level, a, u0, u1, p, l));
         count_launch(1);
     }
     PDG_CHECK_LAUNCH();
+    if (dbg_on) {
+        const std::vector<unsigned long long> h = dbg.download(st);
+        unsigned long long t00 = ~0ull;
+        for (int l = 0; l < nl; ++l) t00 = std::min(t00, h[3 * l]);
+        std::fprintf(stderr, "nd level solve n=%d levels=%d\n", n, nl);
+        for (int l = 0; l < nl; ++l) {
+            double mb = 0.0;
+            const std::vector<NdTileTask> ts = d_ttasks.download(st);
+            for (int u = lvl_off[l]; u < lvl_off[l + 1]; ++u) mb += 16e-6 * ts[u].ntiles * ts[u].tile_d2;
+            std::fprintf(stderr, "  level %2d units %5d %7.2f MB  start %8.2f  end %8.2f  (%6.2f us)\n", l,
+                         lvl_off[l + 1] - lvl_off[l], mb, (h[3 * l] - t00) * 1e-3, (h[3 * l + 1] - t00) * 1e-3,
+                         (h[3 * l + 1] - h[3 * l]) * 1e-3);
+        }
+    }
 }
 
 void NdChol::solve_tiles(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
