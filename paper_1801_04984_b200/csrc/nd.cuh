@@ -120,6 +120,9 @@ struct NdChol {
     std::string fallback_reason;  // why the chunk kernel's schedule did not fit (levels used instead)
     std::vector<int> lvl_off;
     std::vector<size_t> lvl_smem;
+    unsigned lvl_stage_bytes = 0;  // TMA staging region for a unit's tiles
+    bool lvl_staged = false;
+    int lvl_pf = 1;
     void solve_levels(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };

@@ -460,25 +460,43 @@ __host__ __device__ inline size_t lvl_size(const NdTileTask& t) {
     return tb_size(t) + (t.type == 1 ? (((size_t)t.s * 4 + 15) / 16) * 16 : 0);
 }
 
+// prefetch: 0 none, 1 L2 prefetch of the unit's tiles, 2 the tiles themselves into shared
+// memory by TMA bulk copies (stage_bytes = the staging region), issued before the wait
+template <bool STAGED>
 __global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, int u1, int prefetch, int lvl) {
-    extern __shared__ __align__(16) unsigned char lsm[];
+    extern __shared__ __align__(128) unsigned char lsm[];
     __shared__ NdTileTask Ts;
+    __shared__ __align__(8) unsigned long long tbar;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nr = a.nrhs;
+    constexpr bool staged = STAGED;
+    unsigned char* stage = lsm;  // staged tiles (prefetch 2)
     bool waited = false;
+    unsigned phase = 0;
+    if (staged && tid == 0) {
+        dev::mbar_init(&tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
         if (tid < (int)(sizeof(NdTileTask) / 4))
             reinterpret_cast<int*>(&Ts)[tid] = __ldg(reinterpret_cast<const int*>(a.tasks + u) + tid);
         __syncthreads();
         const NdTileTask& T = Ts;
-        unsigned char* buf = lsm;
+        unsigned char* buf = lsm + (staged ? a.stage_bytes : 0);
         double* v = reinterpret_cast<double*>(buf);
         double* tail = reinterpret_cast<double*>(buf + tb_tail(T));
         int* oix = reinterpret_cast<int*>(buf + tb_oix(T));
         int* bix = reinterpret_cast<int*>(buf + tb_bix(T));
         int* sidx = reinterpret_cast<int*>(buf + lvl_sidx(T));
+        const long long tbytes = (long long)T.ntiles * T.tile_d2 * 16;
+        if (staged && tid == 0) {  // the unit's tiles (static) into shared memory, in flight during the wait
+            dev::mbar_arrive_expect_tx(&tbar, static_cast<unsigned>(tbytes));
+            for (long long off = 0; off < tbytes; off += 32768)
+                dev::bulk_g2s(stage + off, reinterpret_cast<const char*>(a.tstore + T.src) + off,
+                              static_cast<unsigned>(min(32768LL, tbytes - off)), &tbar);
+        }
         // ---- static data (before the dependency wait): the unit's tiles into L2, the index lists ----
-        if (prefetch) {
+        if (prefetch == 1) {
             const long long bytes = (long long)T.ntiles * T.tile_d2 * 16;
             for (long long off = (long long)tid * 16384; off < bytes; off += (long long)kLvlThreads * 16384) {
                 const unsigned nb = static_cast<unsigned>(min(16384LL, bytes - off));
@@ -498,7 +516,10 @@ __global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, in
             waited = true;
         }
         __syncthreads();
-        if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
+        if (a.stop && *a.stop) {  // speculative GMRES step after the cycle ended
+            if (staged) dev::mbar_wait(&tbar, phase);  // no bulk copy may outlive the CTA
+            return;
+        }
         if (a.dbg && tid == 0) {  // PDG_ND_DEBUG: per level [first start past the wait, last end, launch seen]
             atomicMin(a.dbg + 3 * lvl, dev::globaltimer());
         }
@@ -563,13 +584,25 @@ __global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, in
         const int nslab = T.tile_d2 >> 5;
         const double2* v0 = reinterpret_cast<const double2*>(v);
         const double2* v1 = reinterpret_cast<const double2*>(v + T.cp);
+        if (staged) {
+            dev::mbar_wait(&tbar, phase);
+            phase ^= 1u;
+        }
+        const double2* tiles = staged ? reinterpret_cast<const double2*>(stage)
+                                      : reinterpret_cast<const double2*>(a.tstore + T.src);
         for (int q = warp; q < T.ntiles; q += kLvlThreads / 32) {
-            const double2* tile = reinterpret_cast<const double2*>(a.tstore + T.src) + (size_t)q * T.tile_d2 + lane;
+            const double2* tile = tiles + (size_t)q * T.tile_d2 + lane;
             double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, q0 = 0.0, qq1 = 0.0, q2 = 0.0, q3 = 0.0;
+            auto ld = [&](const double2* p_) {
+                if constexpr (STAGED)
+                    return *p_;
+                else
+                    return __ldcs(p_);
+            };
             int t = 0;
             for (; t + 3 < nslab; t += 4) {
-                const double2 m0 = __ldcs(tile + t * 32), m1 = __ldcs(tile + (t + 1) * 32);
-                const double2 m2 = __ldcs(tile + (t + 2) * 32), m3 = __ldcs(tile + (t + 3) * 32);
+                const double2 m0 = ld(tile + t * 32), m1 = ld(tile + (t + 1) * 32);
+                const double2 m2 = ld(tile + (t + 2) * 32), m3 = ld(tile + (t + 3) * 32);
                 const double2 a0 = v0[t * J + jl], b0 = v1[t * J + jl], a1 = v0[(t + 1) * J + jl], b1 = v1[(t + 1) * J + jl];
                 const double2 a2 = v0[(t + 2) * J + jl], b2 = v1[(t + 2) * J + jl], a3 = v0[(t + 3) * J + jl],
                               b3 = v1[(t + 3) * J + jl];
@@ -591,7 +624,7 @@ __global__ void __launch_bounds__(kLvlThreads) k_nd_level(TileArgs a, int u0, in
                 q3 = fma(m3.y, b3.y, q3);
             }
             for (; t < nslab; ++t) {
-                const double2 m0 = __ldcs(tile + t * 32);
+                const double2 m0 = ld(tile + t * 32);
                 const double2 a0 = v0[t * J + jl], b0 = v1[t * J + jl];
                 p0 = fma(m0.x, a0.x, p0);
                 p1 = fma(m0.y, a0.y, p1);
@@ -845,8 +878,15 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         if (const char* e = std::getenv("PDG_ND_LVL_MINROWS")) min_rows = std::max(1, std::atoi(e));
         double upb = 2.0;  // units per CTA slot of the grid, for the levels large enough to split
         if (const char* e = std::getenv("PDG_ND_LVL_UPB")) upb = std::max(0.25, std::atof(e));
+        // PDG_ND_LVL_PF: 1 (default) L2 prefetch of a unit's tiles before the dependency wait;
+        // 2 the tiles staged in shared memory by TMA bulk copies (units capped to the staging
+        // region; measured slower at config 1: 352 vs 276 us); 0 none
+        lvl_pf = std::getenv("PDG_ND_LVL_PF") ? std::atoi(std::getenv("PDG_ND_LVL_PF")) : 1;
+        long long lvl_stage = lvl_pf == 2 ? 96 * 1024 : (1LL << 40);  // staging region of a unit's tiles
+        if (const char* e = std::getenv("PDG_ND_LVL_STAGE_KB")) lvl_stage = 1024LL * std::max(16, std::atoi(e));
+        long long stage_max = 0;
         auto add_level = [&](int type, int depth) {
-            const double want = level_bytes(type, depth) / (upb * tgrid);
+            const double want = std::min(level_bytes(type, depth) / (upb * tgrid), (double)lvl_stage);
             size_t smax = 0;
             lvl_off.push_back(static_cast<int>(units.size()));
             for (int k = 0; k < nf; ++k) {
@@ -854,9 +894,13 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
                 const NdFront& F = fronts[k];
                 const int cols = type == 1 ? F.s : F.s + F.b;
                 const int rows = type == 1 ? F.s + F.b : F.s;
-                const int rpt = std::max(min_rows, static_cast<int>(std::ceil(want / (8.0 * std::max(cols, 1)))));
+                int rpt = std::max(min_rows, static_cast<int>(std::ceil(want / (8.0 * std::max(cols, 1)))));
+                // staged tiles: a unit's tiles must fit the staging region
+                const int rb_cols = std::max(1, cols);
+                while (rpt > 1 && (double)rpt * rb_cols * 8.0 > lvl_stage * 0.98) rpt = (rpt + 1) / 2;
                 for (auto& t : make_tasks(k, type, std::min(rows, rpt))) {
                     smax = std::max(smax, lvl_size(t));
+                    stage_max = std::max<long long>(stage_max, (long long)t.ntiles * t.tile_d2 * 16);
                     units.push_back(t);
                 }
             }
@@ -865,8 +909,10 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         for (int d = maxdepth; d >= 0; --d) add_level(1, d);
         for (int d = 0; d <= maxdepth; ++d) add_level(2, d);
         lvl_off.push_back(static_cast<int>(units.size()));
+        lvl_stage_bytes = static_cast<unsigned>((stage_max + 127) / 128 * 128);
         size_t smax = 0;
         for (size_t v : lvl_smem) smax = std::max(smax, v);
+        lvl_staged = lvl_pf == 2 && smax + lvl_stage_bytes <= 226 * 1024;  // else tiles come from global memory
         require(smax <= 226 * 1024, "nested dissection: level unit buffer exceeds shared memory");
         tstore.alloc((size_t)std::max<long long>(toff, 1));
         {
@@ -883,7 +929,8 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
         tile_bytes = 8.0 * (double)toff;
         d_ttasks.upload(units, st);
         d_toix.upload(oix, st);
-        PDG_CUDA(cudaFuncSetAttribute(k_nd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        PDG_CUDA(cudaFuncSetAttribute(k_nd_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        PDG_CUDA(cudaFuncSetAttribute(k_nd_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         PDG_CUDA(cudaStreamSynchronize(st));
         (void)hbp;
         (void)cta_of;
@@ -1005,7 +1052,8 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
     a.n = n;
     a.nrhs = nrhs;
     a.stop = guard;
-    static const int pf = !(std::getenv("PDG_ND_LVL_PF") && std::atoi(std::getenv("PDG_ND_LVL_PF")) == 0);
+    const int pf = lvl_pf == 2 && !lvl_staged ? 1 : lvl_pf;
+    a.stage_bytes = pf == 2 ? lvl_stage_bytes : 0;
     static const int bpsm = std::getenv("PDG_ND_LVL_BLOCKS") ? std::max(1, std::atoi(std::getenv("PDG_ND_LVL_BLOCKS"))) : 8;
     static const int use_pdl = !(std::getenv("PDG_ND_LVL_PDL") && std::atoi(std::getenv("PDG_ND_LVL_PDL")) == 0);
     const int nl = static_cast<int>(lvl_smem.size());
@@ -1023,7 +1071,7 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(std::min(u1 - u0, bpsm * tgrid)));
         cfg.blockDim = dim3(kLvlThreads);
-        cfg.dynamicSmemBytes = lvl_smem[l];
+        cfg.dynamicSmemBytes = lvl_smem[l] + a.stage_bytes;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1031,7 +1079,10 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
         cfg.attrs = attr;
         cfg.numAttrs = use_pdl ? 1 : 0;
         int p = pf;
-        PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level, a, u0, u1, p, l));
+        if (p == 2)
+            PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level<true>, a, u0, u1, p, l));
+        else
+            PDG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_level<false>, a, u0, u1, p, l));
         count_launch(1);
     }
     PDG_CHECK_LAUNCH();
