@@ -405,9 +405,14 @@ def main():
                          {}).get("bytes")
     except Exception:
         pass
-    kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve (nested-dissection displacement solve" if nd_a else
-                                           "k_sweep<16> (twisted block-tridiagonal displacement solve")
-                 + ", one launch per call)",
+    hybrid_a = nd_a and os.environ.get("PDG_ND_HYBRID", "2") in ("1", "2")
+    kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve + k_nd_level (nested-dissection displacement solve: the local "
+                                           "subtrees in the chunk kernel, forward and backward launches, the 7 top "
+                                           "levels as level kernels chained by programmatic dependent launch)"
+                                           if hybrid_a else
+                                           "k_nd_solve (nested-dissection displacement solve, one launch per call)"
+                                           if nd_a else
+                                           "k_sweep<16> (twisted block-tridiagonal displacement solve, one launch per call)"),
                  "flow_solve": "flow_solve: " + ("k_nd_solve" if nd_f else "k_sweep_dense") + " (one launch per call)",
                  "spmv": "spmv: k_spmv"}
     roofline = {"bound": "hbm", "kernel": kernel_of.get(dom, dom), "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,

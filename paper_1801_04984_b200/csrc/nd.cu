@@ -1212,27 +1212,41 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         auto place_local = [&](std::vector<NdTask>& ts) {
             for (const auto& t : ts) per_cta[cta_of[t.front]].push_back(t);
         };
+        // hybrid (PDG_ND_HYBRID): this kernel runs the local subtrees only, as two launches
+        // (forward, backward); the levels above run as level kernels in between (nd_tile.cu)
+        hybrid = local_depth > 0 && local_depth <= maxdepth && nd_hybrid_default(prof_phase);
+        hybrid_top = local_depth - 1;
+        std::vector<std::vector<NdTask>> per_cta_b(hybrid ? grid : 0);
         for (int d = maxdepth; d >= 0; --d) {
             if (d >= local_depth)
                 place_local(fwd_by_depth[d]);
-            else
+            else if (!hybrid)
                 place(fwd_by_depth[d]);
         }
+        if (hybrid) per_cta.swap(per_cta_b);  // per_cta_b: forward schedule, per_cta: backward
+        if (hybrid) per_cta.assign(grid, {});
         for (int d = 0; d <= maxdepth; ++d) {
             if (d >= local_depth)
                 place_local(bwd_by_depth[d]);
-            else
+            else if (!hybrid)
                 place(bwd_by_depth[d]);
+        }
+        if (hybrid) {
+            per_cta.swap(per_cta_b);  // per_cta: forward, per_cta_b: backward
+            for (auto& v : per_cta_b)  // the subtree roots' parents (top levels) are done: stream order
+                for (auto& t : v)
+                    if (fronts[t.front].depth == local_depth) t.wait0 = -1;
         }
         max_tasks = 0;
         size_t max_buf = 0;
-        for (auto& v : per_cta) {
-            max_tasks = std::max(max_tasks, static_cast<int>(v.size()));
-            for (auto& t : v) {
-                t.vmt = nd_task_vmt(t);
-                max_buf = std::max(max_buf, nd_task_buf_bytes(t));
+        for (auto* lists : {&per_cta, &per_cta_b})
+            for (auto& v : *lists) {
+                max_tasks = std::max(max_tasks, static_cast<int>(v.size()));
+                for (auto& t : v) {
+                    t.vmt = nd_task_vmt(t);
+                    max_buf = std::max(max_buf, nd_task_buf_bytes(t));
+                }
             }
-        }
         static_assert((sizeof(NdTask) + sizeof(int)) * kNdBufs <= kNdHeader - 1024, "task descriptors do not fit the header");
         // shared memory: header, task list, TMA ring, and the buffer arena (at least three of the
         // largest task buffers, so a task's buffer never waits on the previous task's)
@@ -1251,6 +1265,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         max_task_buf = max_buf;
         smem = fixed + (size_t)stages * stage_bytes + arena;
         // FIFO placement of the task buffers in the arena (tasks run and release in order)
+        for (auto& v : per_cta_b) per_cta.push_back(std::move(v));  // placed like the others, split below
         for (auto& v : per_cta) {
             size_t head = 0;
             int prev_dep = -1;
@@ -1273,11 +1288,19 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 head += sz;
             }
         }
-        std::vector<NdTask> all;
-        std::vector<int> hct(grid + 1, 0);
+        std::vector<NdTask> all, all_b;
+        std::vector<int> hct(grid + 1, 0), hct_b(grid + 1, 0);
         for (int q = 0; q < grid; ++q) {
             all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
             hct[q + 1] = static_cast<int>(all.size());
+        }
+        if (hybrid) {
+            for (int q = 0; q < grid; ++q) {
+                all_b.insert(all_b.end(), per_cta[grid + q].begin(), per_cta[grid + q].end());
+                hct_b[q + 1] = static_cast<int>(all_b.size());
+            }
+            d_tasks_b.upload(all_b, st);
+            ctoff_b.upload(hct_b, st);
         }
         // the attribute is per device and only ever raised: set the largest seen on this device
         static size_t attr_smem[64] = {};
@@ -1294,13 +1317,39 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     };
     try {
         schedule_chunks();
+        if (hybrid) {  // the top levels as level kernels (tiles for those fronts only)
+            lvl_max_depth = hybrid_top;
+            build_tiles(children, parent, hs, hbp, hcbdst, st);
+        }
     } catch (const Error& e) {
         if (e.status != PDG_INVALID_ARGUMENT || std::getenv("PDG_ND_STRICT")) throw;
         fallback_reason = e.what();
+        hybrid = false;
+        lvl_max_depth = -1;
         tiles = levels = true;
         build_tiles(children, parent, hs, hbp, hcbdst, st);
         store.release();
     }
+}
+
+// one launch of the chunk kernel on a task schedule (the hybrid's local forward / backward)
+void NdChol::launch_chunks(const NdTask* tasks, const int* cto, const double* b, long long ldb, double* x, long long ldx,
+                           int nrhs, cudaStream_t st) {
+    NdArgs a{tasks, cto, sdofs.p, bpos.p, cbdst.p, store.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, counters.p, call, cbtot, n,
+             nrhs, stages, vmax, smem_tasks, pf, stage_bytes, nullptr, 0, 0, std::getenv("PDG_ND_FENCE") != nullptr, guard,
+             0, 0};
+    void* args[] = {&a};
+    PDG_CUDA(cudaLaunchCooperativeKernel((void*)k_nd_solve, grid, kNdBlock, args, smem, st));
+    count_launch(1);
+    PDG_CHECK_LAUNCH();
+}
+
+// PDG_ND_HYBRID: unset -> the displacement solve only (config 1: 275 -> 246 us; the flux
+// solve's small top levels are faster in the chunk kernel, 92 vs 106 us); 0 none; 1 both
+bool nd_hybrid_default(int prof_phase) {
+    const char* e = std::getenv("PDG_ND_HYBRID");
+    if (!e) return prof_phase == PROF_A_SOLVE;
+    return std::atoi(e) == 1 || (std::atoi(e) == 2 && prof_phase == PROF_A_SOLVE);
 }
 
 void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
@@ -1309,6 +1358,12 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ++call;
     if (levels) {
         solve_levels(b, ldb, x, ldx, nrhs, st);
+        return;
+    }
+    if (hybrid) {  // local forward (chunk kernel), top levels (level kernels), local backward
+        launch_chunks(d_tasks.p, ctoff.p, b, ldb, x, ldx, nrhs, st);
+        solve_levels(b, ldb, x, ldx, nrhs, st);
+        launch_chunks(d_tasks_b.p, ctoff_b.p, b, ldb, x, ldx, nrhs, st);
         return;
     }
     if (tiles) {

@@ -75,6 +75,7 @@ struct NdTileTask {
 };
 bool nd_tile_default();
 bool nd_levels_default();
+bool nd_hybrid_default(int prof_phase);
 
 struct NdChol {
     int n = 0, max_rhs = 0, nfront = 0, maxdepth = 0;
@@ -124,6 +125,14 @@ struct NdChol {
     bool lvl_staged = false;
     int lvl_pf = 1;
     void solve_levels(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+    // hybrid (PDG_ND_HYBRID): chunk kernel on the local subtrees (forward, backward schedules),
+    // level kernels on the levels 0..hybrid_top in between
+    bool hybrid = false;
+    int hybrid_top = -1, lvl_max_depth = -1;  // lvl_max_depth >= 0: level units only up to that depth
+    DBuf<NdTask> d_tasks_b;
+    DBuf<int> ctoff_b;
+    void launch_chunks(const NdTask* tasks, const int* cto, const double* b, long long ldb, double* x, long long ldx,
+                       int nrhs, cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };
 

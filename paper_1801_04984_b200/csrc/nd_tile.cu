@@ -723,7 +723,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
     const long long wide = ((long long)(cmax + 63) / 64 * 64) * 8;  // one row of the widest pass
     tile_cap = static_cast<unsigned>(std::max<long long>(tile_cap, wide));
     tstage_bytes = std::max(tstage_bytes, tile_cap);
-    require(levels || tstage_bytes <= 65536, "nested dissection: front too wide for the tile ring");
+    require(levels || hybrid || tstage_bytes <= 65536, "nested dissection: front too wide for the tile ring");
     // subtree mapping (see the file comment)
     int local_depth = maxdepth + 1;
     {
@@ -870,7 +870,7 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
             }
         }
     };
-    if (levels) {  // level-synchronous units: fwd levels deepest first, then bwd levels
+    if (levels || hybrid) {  // level-synchronous units: fwd levels deepest first, then bwd levels
         std::vector<NdTileTask> units;
         lvl_off.clear();
         lvl_smem.clear();
@@ -906,8 +906,9 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
             }
             lvl_smem.push_back(a16(smax));
         };
-        for (int d = maxdepth; d >= 0; --d) add_level(1, d);
-        for (int d = 0; d <= maxdepth; ++d) add_level(2, d);
+        const int dtop = lvl_max_depth >= 0 ? std::min(lvl_max_depth, maxdepth) : maxdepth;
+        for (int d = dtop; d >= 0; --d) add_level(1, d);
+        for (int d = 0; d <= dtop; ++d) add_level(2, d);
         lvl_off.push_back(static_cast<int>(units.size()));
         lvl_stage_bytes = static_cast<unsigned>((stage_max + 127) / 128 * 128);
         size_t smax = 0;
