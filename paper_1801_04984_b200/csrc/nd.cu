@@ -892,6 +892,15 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         for (int c : h.children) children[k].push_back(newid[c]);
     }
     require(static_cast<int>(hs.size()) == n, "nested dissection: pivots do not cover the matrix");
+    // dense top (nd_top.cu): the deepest front level it covers, lowered until |T| fits
+    top_depth = std::min(nd_top_default(prof_phase), maxdepth - 1);
+    while (top_depth >= 0) {
+        long long nt = 0;
+        for (const auto& F : fronts)
+            if (F.depth <= top_depth) nt += F.s;
+        if (nt <= nd_top_cap()) break;
+        --top_depth;
+    }
     // contribution buffers: front F holds [child q][s + b] (per right-hand side); the
     // update vector w_C of child q of F (its boundary rows: u_C plus the pass-through
     // of C's own children) is written by C's forward tasks straight into F's slot q at
@@ -1061,6 +1070,9 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     cbuf.zero(st);  // slots no child writes stay zero
     tiles = nd_tile_default();
     levels = nd_levels_default();
+    if (tiles && !levels) top_depth = -1;  // the opt-in dataflow tile kernel solves every front
+    if (top_depth >= 0) build_top(hs, hbp, children, fo, dense.p, st);
+    lvl_min_depth = top_depth + 1;
     if (tiles) {
         build_tiles(children, parent, hs, hbp, hcbdst, st);
         store.release();  // the tile store replaces the row-major one
@@ -1214,28 +1226,38 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         };
         // hybrid (PDG_ND_HYBRID): this kernel runs the local subtrees only, as two launches
         // (forward, backward); the levels above run as level kernels in between (nd_tile.cu)
-        hybrid = local_depth > 0 && local_depth <= maxdepth && nd_hybrid_default(prof_phase);
+        // with a dense top (top_depth >= 0) the fronts of depth <= top_depth get no tasks
+        hybrid = local_depth > 0 && local_depth <= maxdepth && nd_hybrid_default(prof_phase) &&
+                 local_depth - 1 > top_depth;
         hybrid_top = local_depth - 1;
-        std::vector<std::vector<NdTask>> per_cta_b(hybrid ? grid : 0);
+        split = hybrid || top_depth >= 0;
+        auto in_chunks = [&](int d) { return d > top_depth && (d >= local_depth || !hybrid); };
+        std::vector<std::vector<NdTask>> per_cta_b(split ? grid : 0);
         for (int d = maxdepth; d >= 0; --d) {
+            if (!in_chunks(d)) continue;
             if (d >= local_depth)
                 place_local(fwd_by_depth[d]);
-            else if (!hybrid)
+            else
                 place(fwd_by_depth[d]);
         }
-        if (hybrid) per_cta.swap(per_cta_b);  // per_cta_b: forward schedule, per_cta: backward
-        if (hybrid) per_cta.assign(grid, {});
+        if (split) per_cta.swap(per_cta_b);  // per_cta_b: forward schedule, per_cta: backward
+        if (split) per_cta.assign(grid, {});
         for (int d = 0; d <= maxdepth; ++d) {
+            if (!in_chunks(d)) continue;
             if (d >= local_depth)
                 place_local(bwd_by_depth[d]);
-            else if (!hybrid)
+            else
                 place(bwd_by_depth[d]);
         }
-        if (hybrid) {
+        if (split) {
             per_cta.swap(per_cta_b);  // per_cta: forward, per_cta_b: backward
-            for (auto& v : per_cta_b)  // the subtree roots' parents (top levels) are done: stream order
-                for (auto& t : v)
-                    if (fronts[t.front].depth == local_depth) t.wait0 = -1;
+            // backward tasks whose parent is solved outside this launch (level kernels, dense
+            // top, or none): their inputs are complete in stream order
+            for (auto& v : per_cta_b)
+                for (auto& t : v) {
+                    const int p = parent[t.front];
+                    if (p < 0 || !in_chunks(fronts[p].depth)) t.wait0 = -1;
+                }
         }
         max_tasks = 0;
         size_t max_buf = 0;
@@ -1294,7 +1316,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             all.insert(all.end(), per_cta[q].begin(), per_cta[q].end());
             hct[q + 1] = static_cast<int>(all.size());
         }
-        if (hybrid) {
+        if (split) {
             for (int q = 0; q < grid; ++q) {
                 all_b.insert(all_b.end(), per_cta[grid + q].begin(), per_cta[grid + q].end());
                 hct_b[q + 1] = static_cast<int>(all_b.size());
@@ -1324,7 +1346,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     } catch (const Error& e) {
         if (e.status != PDG_INVALID_ARGUMENT || std::getenv("PDG_ND_STRICT")) throw;
         fallback_reason = e.what();
-        hybrid = false;
+        hybrid = split = false;
         lvl_max_depth = -1;
         tiles = levels = true;
         build_tiles(children, parent, hs, hbp, hcbdst, st);
@@ -1356,13 +1378,20 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
     ++call;
-    if (levels) {
-        solve_levels(b, ldb, x, ldx, nrhs, st);
+    const int nl = static_cast<int>(lvl_smem.size());
+    if (levels) {  // forward levels, the dense top, backward levels
+        solve_levels_range(b, ldb, x, ldx, nrhs, 0, top_depth >= 0 ? nl / 2 : nl, st);
+        if (top_depth >= 0) {
+            solve_top(b, ldb, x, ldx, nrhs, st);
+            solve_levels_range(b, ldb, x, ldx, nrhs, nl / 2, nl, st);
+        }
         return;
     }
-    if (hybrid) {  // local forward (chunk kernel), top levels (level kernels), local backward
+    if (split) {  // local forward (chunk kernel), level kernels, dense top, level kernels, local backward
         launch_chunks(d_tasks.p, ctoff.p, b, ldb, x, ldx, nrhs, st);
-        solve_levels(b, ldb, x, ldx, nrhs, st);
+        if (hybrid) solve_levels_range(b, ldb, x, ldx, nrhs, 0, nl / 2, st);
+        if (top_depth >= 0) solve_top(b, ldb, x, ldx, nrhs, st);
+        if (hybrid) solve_levels_range(b, ldb, x, ldx, nrhs, nl / 2, nl, st);
         launch_chunks(d_tasks_b.p, ctoff_b.p, b, ldb, x, ldx, nrhs, st);
         return;
     }

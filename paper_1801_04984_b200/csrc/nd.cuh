@@ -76,6 +76,8 @@ struct NdTileTask {
 bool nd_tile_default();
 bool nd_levels_default();
 bool nd_hybrid_default(int prof_phase);
+int nd_top_default(int prof_phase);
+int nd_top_cap();
 
 struct NdChol {
     int n = 0, max_rhs = 0, nfront = 0, maxdepth = 0;
@@ -133,6 +135,19 @@ struct NdChol {
     DBuf<int> ctoff_b;
     void launch_chunks(const NdTask* tasks, const int* cto, const double* b, long long ldb, double* x, long long ldx,
                        int nrhs, cudaStream_t st);
+    // dense top (PDG_ND_TOP): the fronts of depth <= top_depth (pivot positions [top0, n)) are
+    // not solved front by front; their Schur complement inverse G = S_TT^{-1} (= (A^{-1})_TT)
+    // is applied as one GEMV between the forward and backward passes of the fronts below
+    int top_depth = -1, ntop = 0, top0 = 0, ldg = 0;
+    int lvl_min_depth = 0;       // level kernels for depths lvl_min_depth..lvl_max_depth
+    bool split = false;          // two chunk launches (forward, backward) around the top / levels
+    DBuf<double> gtop, ctop;     // G (ntop x ldg, row-major), the top right-hand sides [rhs][ldg]
+    DBuf<int> top_coff, top_clist;  // per top position: the contribution-buffer entries to subtract
+    void build_top(const std::vector<int>& hs, const std::vector<int>& hbp, const std::vector<std::vector<int>>& children,
+                   const std::vector<long long>& fo, const double* dense, cudaStream_t st);
+    void solve_top(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
+    void solve_levels_range(const double* b, long long ldb, double* x, long long ldx, int nrhs, int l0, int l1,
+                            cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };
 

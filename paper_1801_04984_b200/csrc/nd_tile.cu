@@ -907,8 +907,8 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
             lvl_smem.push_back(a16(smax));
         };
         const int dtop = lvl_max_depth >= 0 ? std::min(lvl_max_depth, maxdepth) : maxdepth;
-        for (int d = dtop; d >= 0; --d) add_level(1, d);
-        for (int d = 0; d <= dtop; ++d) add_level(2, d);
+        for (int d = dtop; d >= lvl_min_depth; --d) add_level(1, d);
+        for (int d = lvl_min_depth; d <= dtop; ++d) add_level(2, d);
         lvl_off.push_back(static_cast<int>(units.size()));
         lvl_stage_bytes = static_cast<unsigned>((stage_max + 127) / 128 * 128);
         size_t smax = 0;
@@ -1036,6 +1036,12 @@ void NdChol::build_tiles(const std::vector<std::vector<int>>& children, const st
 }
 
 void NdChol::solve_levels(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
+    solve_levels_range(b, ldb, x, ldx, nrhs, 0, static_cast<int>(lvl_smem.size()), st);
+}
+
+// level kernels l0..l1-1 (the forward levels are the first half of the list, the backward the second)
+void NdChol::solve_levels_range(const double* b, long long ldb, double* x, long long ldx, int nrhs, int l0, int l1,
+                                cudaStream_t st) {
     TileArgs a{};
     a.tasks = d_ttasks.p;
     a.toix = d_toix.p;
@@ -1066,7 +1072,7 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
         dbg.upload(init, st);
         a.dbg = dbg.p;
     }
-    for (int l = 0; l < nl; ++l) {
+    for (int l = l0; l < l1; ++l) {
         int u0 = lvl_off[l], u1 = lvl_off[l + 1];
         if (u1 <= u0) continue;
         cudaLaunchConfig_t cfg{};
@@ -1090,9 +1096,9 @@ void NdChol::solve_levels(const double* b, long long ldb, double* x, long long l
     if (dbg_on) {
         const std::vector<unsigned long long> h = dbg.download(st);
         unsigned long long t00 = ~0ull;
-        for (int l = 0; l < nl; ++l) t00 = std::min(t00, h[3 * l]);
-        std::fprintf(stderr, "nd level solve n=%d levels=%d\n", n, nl);
-        for (int l = 0; l < nl; ++l) {
+        for (int l = l0; l < l1; ++l) t00 = std::min(t00, h[3 * l]);
+        std::fprintf(stderr, "nd level solve n=%d levels=%d (%d..%d)\n", n, nl, l0, l1 - 1);
+        for (int l = l0; l < l1; ++l) {
             double mb = 0.0;
             const std::vector<NdTileTask> ts = d_ttasks.download(st);
             for (int u = lvl_off[l]; u < lvl_off[l + 1]; ++u) mb += 16e-6 * ts[u].ntiles * ts[u].tile_d2;
