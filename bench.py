@@ -406,9 +406,11 @@ def main():
     except Exception:
         pass
     hybrid_a = nd_a and os.environ.get("PDG_ND_HYBRID", "2") in ("1", "2")
-    kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve + k_nd_level (nested-dissection displacement solve: the local "
-                                           "subtrees in the chunk kernel, forward and backward launches, the 7 top "
-                                           "levels as level kernels chained by programmatic dependent launch)"
+    kernel_of = {"a_solve": "a_solve: " + ("k_nd_solve + k_nd_level + k_nd_top_gemv (nested-dissection displacement "
+                                           "solve: the local subtrees in the chunk kernel, forward and backward "
+                                           "launches; front levels 3-6 as level kernels chained by programmatic "
+                                           "dependent launch; the top separators (levels 0-2, 4096 dofs) as one "
+                                           "dense GEMV with their Schur complement inverse)"
                                            if hybrid_a else
                                            "k_nd_solve (nested-dissection displacement solve, one launch per call)"
                                            if nd_a else
