@@ -1108,6 +1108,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             set_guard(&lsd->stop);
             const double tolb = opts.tol * bnorm;
             const bool no_lookahead = std::getenv("PDG_GMRES_NO_LOOKAHEAD") != nullptr;
+            static const bool predict = !(std::getenv("PDG_GMRES_PREDICT") && std::atoi(std::getenv("PDG_GMRES_PREDICT")) == 0);
             auto step = [&](int k) {
                 double* vk = kr.V.p + (size_t)k * n;
                 double* zk = kr.Z.p + (size_t)k * n;
@@ -1129,6 +1130,7 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
             int k0 = 0;
             for (;;) {
                 int kend = -1;
+                const double beta_k0 = k0 > 0 ? slots[k0 - 1].res : beta;  // residual estimate before step k0
                 for (int k = k0; k < mm; ++k) {
                     step(k);  // queued behind step k - 1: skipped on the device if k - 1 ended the cycle
                     if (no_lookahead) {
@@ -1142,6 +1144,20 @@ void Block::solve(const double* b, double* x_out, pdg_report* rep, int block_ind
                         if (slots[k - 1].stop) {
                             kend = k - 1;
                             break;
+                        }
+                        // predicted stop: when the residual estimate extrapolated from the last two
+                        // steps reaches the tolerance at step k, wait for step k instead of queuing
+                        // step k + 1 speculatively (a skipped step still costs its launches on the
+                        // GPU; a wrong prediction costs one host round trip). Same iterates either way.
+                        if (predict && k + 1 < mm) {
+                            const double r1 = slots[k - 1].res, r0 = k - 1 > k0 ? slots[k - 2].res : beta_k0;
+                            if (r0 > 0.0 && r1 * (r1 / r0) <= 4.0 * tolb) {
+                                PDG_CUDA(cudaEventSynchronize(kr.evs[k & 1]));
+                                if (slots[k].stop) {
+                                    kend = k;
+                                    break;
+                                }
+                            }
                         }
                     }
                 }

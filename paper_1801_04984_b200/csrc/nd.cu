@@ -1071,7 +1071,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     tiles = nd_tile_default();
     levels = nd_levels_default();
     if (tiles && !levels) top_depth = -1;  // the opt-in dataflow tile kernel solves every front
-    if (top_depth >= 0) build_top(hs, hbp, children, fo, dense.p, st);
+    if (top_depth >= 0) build_top(hbp, children, fo, dense.p, h, st);
     lvl_min_depth = top_depth + 1;
     if (tiles) {
         build_tiles(children, parent, hs, hbp, hcbdst, st);

@@ -34,6 +34,8 @@
 
 namespace pdg {
 
+struct LaHandles;
+
 struct NdFront {
     int s, b;             // pivots, boundary dofs
     int sdof, bdof;       // offsets into the S / B dof lists
@@ -143,8 +145,8 @@ struct NdChol {
     bool split = false;          // two chunk launches (forward, backward) around the top / levels
     DBuf<double> gtop, ctop;     // G (ntop x ldg, row-major), the top right-hand sides [rhs][ldg]
     DBuf<int> top_coff, top_clist;  // per top position: the contribution-buffer entries to subtract
-    void build_top(const std::vector<int>& hs, const std::vector<int>& hbp, const std::vector<std::vector<int>>& children,
-                   const std::vector<long long>& fo, const double* dense, cudaStream_t st);
+    void build_top(const std::vector<int>& hbp, const std::vector<std::vector<int>>& children,
+                   const std::vector<long long>& fo, const double* dense, LaHandles& la, cudaStream_t st);
     void solve_top(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     void solve_levels_range(const double* b, long long ldb, double* x, long long ldx, int nrhs, int l0, int l1,
                             cudaStream_t st);

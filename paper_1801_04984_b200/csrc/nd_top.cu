@@ -178,9 +178,8 @@ int nd_top_default(int prof_phase) {
     return prof_phase == PROF_A_SOLVE ? 2 : 5;
 }
 
-void NdChol::build_top(const std::vector<int>& hs, const std::vector<int>& hbp,
-                       const std::vector<std::vector<int>>& children, const std::vector<long long>& fo,
-                       const double* dense, cudaStream_t st) {
+void NdChol::build_top(const std::vector<int>& hbp, const std::vector<std::vector<int>>& children,
+                       const std::vector<long long>& fo, const double* dense, LaHandles& h, cudaStream_t st) {
     const int nf = static_cast<int>(fronts.size());
     int kt = nf;
     while (kt > 0 && fronts[kt - 1].depth <= top_depth) --kt;
@@ -200,7 +199,6 @@ void NdChol::build_top(const std::vector<int>& hs, const std::vector<int>& hbp,
         PDG_CHECK_LAUNCH();
     }
     {
-        LaHandles h(st);
         int lwork = 0;
         if (cusolverDnDpotri_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, ntop, L.p, ntop, &lwork) != CUSOLVER_STATUS_SUCCESS)
             throw Error(PDG_CUDA_ERROR, "nested dissection: potri workspace query failed");
@@ -243,7 +241,6 @@ void NdChol::build_top(const std::vector<int>& hs, const std::vector<int>& hbp,
     factor_bytes = 0.0;
     for (int k = 0; k < kt; ++k) factor_bytes += 16.0 * (double)(fronts[k].s + fronts[k].b) * fronts[k].s;
     factor_bytes += 8.0 * (double)ntop * ntop;
-    (void)hs;
     // the attribute is per device and only ever raised: the largest seen on this device
     static size_t attr[64] = {};
     int dev = 0;
