@@ -327,7 +327,9 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_strip(long long u_threads, 
     }
 }
 
-long long exclusive_scan_ll(const long long* in, long long* out, long long n, cudaStream_t st) {
+}  // namespace
+
+long long scan_ll(const long long* in, long long* out, long long n, cudaStream_t st) {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, st);
     DBuf<unsigned char> buf(tmp + 1);
@@ -337,8 +339,6 @@ long long exclusive_scan_ll(const long long* in, long long* out, long long n, cu
     PDG_CUDA(cudaStreamSynchronize(st));
     return total;
 }
-
-}  // namespace
 
 void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, double tau, cudaStream_t st,
                         const double* kappa) {
@@ -355,15 +355,18 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     for (int i = 0; i < m; ++i) th.w[i] = kappa ? tau * kappa[i] : tau;
     const double mb = -ops.biot_b, minv = -ops.inv_m;
     require(ops.n_u == 8 * ops.n_p, "space-time block: n_u must be 8 * n_cells");
+    u_groups = (long long)m * n_cells;
+    s_rows = (long long)m * (n_q + n_p);
+    s_slices = (s_rows + 31) / 32;
+    if (build_kp(ops, th.t, th.w, st)) return;
 
     // U class
-    u_groups = (long long)m * n_cells;
     DBuf<long long> cnt(u_groups + 1);
     cnt.zero(st);
     k_u_count<<<grid_for(u_groups, 256), 256, 0, st>>>(n_cells, ops.A.off.p, ops.E.off.p, m, cnt.p);
     PDG_CHECK_LAUNCH();
     u_off.alloc(u_groups + 1);
-    u_entries = exclusive_scan_ll(cnt.p, u_off.p, u_groups, st);
+    u_entries = scan_ll(cnt.p, u_off.p, u_groups, st);
     u_col.alloc(u_entries);
     u_val.alloc(8 * u_entries);
     DBuf<int> err(1);
@@ -374,8 +377,6 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     PDG_CHECK_LAUNCH();
 
     // S class
-    s_rows = (long long)m * (n_q + n_p);
-    s_slices = (s_rows + 31) / 32;
     s_len.alloc(s_rows);
     k_s_len<<<grid_for(s_rows, 256), 256, 0, st>>>(s_rows, m, n_q, n_p, th, ops.M_q.off.p, ops.B.off.p, ops.Et.off.p,
                                                     ops.Bt.off.p, s_len.p);
@@ -385,7 +386,7 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     k_s_slice_width<<<grid_for(s_slices, 256), 256, 0, st>>>(s_rows, s_slices, s_len.p, w.p);
     PDG_CHECK_LAUNCH();
     s_off.alloc(s_slices + 1);
-    s_slots = exclusive_scan_ll(w.p, s_off.p, s_slices, st);
+    s_slots = scan_ll(w.p, s_off.p, s_slices, st);
     s_col.alloc(32 * s_slots);
     s_val.alloc(32 * s_slots);
     k_s_fill<<<grid_for(s_rows, 256), 256, 0, st>>>(s_rows, m, nt, n_u, n_q, n_p, tau, mb, minv, th, ops.M_q.off.p,
@@ -406,6 +407,10 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
 
 void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     ProfScope prof(PROF_SPMV, st, 8.0 * (double)(nnz + 2 * rows));
+    if (kp) {
+        kp_launch(x, y, nullptr, nullptr, 0, nullptr, false, st);
+        return;
+    }
     int u2 = rows <= (2LL << 20);  // two U rows per thread up to 2M rows (256^2 dG(1) and below)
     if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;  // test override: 1 | 2
     const long long u_threads = u_groups * (u2 ? 4 : 8);
@@ -419,6 +424,7 @@ void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
 }
 
 int SpaceTimeOp::dots_grid() const {
+    if (kp) return kp_grid(false);
     int u2 = rows <= (2LL << 20);
     if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;
     const long long u_threads = u_groups * (u2 ? 4 : 8);
@@ -431,6 +437,10 @@ void SpaceTimeOp::apply_dots(const double* x, double* y, double* y2, const doubl
                              cudaStream_t st) const {
     require(ncols >= 1 && ncols <= kSpmvMaxDots, "space-time block: fused dots need 1..8 basis vectors");
     ProfScope prof(PROF_SPMV, st, 8.0 * (double)(nnz + 2 * rows));
+    if (kp) {
+        kp_launch(x, y, y2, V, ncols, partial, false, st);
+        return;
+    }
     int u2 = rows <= (2LL << 20);
     if (const char* e = std::getenv("PDG_SPMV_ROWS")) u2 = std::atoi(e) == 2;
     const long long u_threads = u_groups * (u2 ? 4 : 8);
@@ -450,8 +460,25 @@ void SpaceTimeOp::set_strip(int nx, int ny, int r0, int r1, cudaStream_t st) {
     strip_ny = ny;
     strip_r0 = r0;
     strip_r1 = r1;
-    // S slices holding an owned row (host scan of the row -> owner rule)
     const int nh = nx * (ny + 1);
+    if (kp) {  // QK slices holding an owned face
+        std::vector<long long> sl;
+        for (long long s = 0; s < qk_slices; ++s) {
+            bool any = false;
+            for (int l = 0; l < 32 && !any; ++l) {
+                const long long f = s * 32 + l;
+                if (f >= n_q) break;
+                const int row = f < nh ? std::min(static_cast<int>(f) / nx, ny - 1) : static_cast<int>((f - nh) % ny);
+                any = row >= r0 && row < r1;
+            }
+            if (any) sl.push_back(s);
+        }
+        strip_qslices.upload(sl, st);
+        strip_qslices.n = sl.size();
+        PDG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    // S slices holding an owned row (host scan of the row -> owner rule)
     auto owned = [&](long long srow) {
         const int loc = static_cast<int>(srow % (n_q + n_p));
         int row;
@@ -477,6 +504,11 @@ void SpaceTimeOp::set_strip(int nx, int ny, int r0, int r1, cudaStream_t st) {
 
 void SpaceTimeOp::apply_strip(const double* x, double* y, cudaStream_t st) const {
     require(strip_nx > 0, "space-time block: no strip set");
+    if (kp) {
+        ProfScope prof(PROF_SPMV, st, 0.0);
+        kp_launch(x, y, nullptr, nullptr, 0, nullptr, true, st);
+        return;
+    }
     const int cell0 = strip_r0 * strip_nx, ncs = (strip_r1 - strip_r0) * strip_nx;
     const long long u_threads = (long long)m * ncs * 8;
     const long long ns = static_cast<long long>(strip_slices.n);
@@ -493,6 +525,10 @@ void SpaceTimeOp::apply_strip(const double* x, double* y, cudaStream_t st) const
 
 void SpaceTimeOp::to_csr(std::vector<long long>& off, std::vector<int>& idx, std::vector<double>& val,
                          cudaStream_t st) const {
+    if (kp) {
+        kp_to_csr(off, idx, val, st);
+        return;
+    }
     const auto uo = u_off.download(st);
     const auto uc = u_col.download(st);
     const auto uv = u_val.download(st);

@@ -37,6 +37,45 @@ struct SpaceTimeOp {
     DBuf<int> s_col;        // 32 * s_slots
     DBuf<double> s_val;     // 32 * s_slots
 
+    // Kronecker-paired layout (the default when the structure allows it; `kp` true):
+    // the M = m rows that share one spatial row pattern are kept together, one
+    // thread per pattern, so a column list and the x reuse serve all M rows and the
+    // M values of an entry are one 16-byte load (m = 2). Column lists keep one index
+    // per run of 8 consecutive displacement columns (cell blocks of A and of E^T).
+    //  UK : one pattern per cell (its 8 displacement rows x M components); per cell
+    //       a header [A run starts..., E columns...], values [cell][entry k][row l][i].
+    //  PK : one pattern per cell (its M pressure rows), SELL-32 over cells; header
+    //       per lane [counts, E^T run starts..., B^T faces...], slots of M values:
+    //       for j: E^T u_j entries (row i: theta_ij*((-b)*e)), B^T q_j pairs of
+    //       consecutive entries of row j only (w_j*bv), the p_j entry of every row.
+    //  QK : one pattern per face (its M flux rows), SELL-32 over faces; one int32
+    //       column (offset within [q p]) and one slot of M values per entry.
+    // Each row is still summed alone in ascending column order with
+    // __dmul_rn/__dadd_rn: the same bits as the SELL layout and as
+    // SparseMatrix::apply (sparse.hpp:30-40) on the canonical CSR.
+    bool kp = false;
+    long long kp_u_entries = 0, kp_u_hdr = 0;  // per-cell entries / header ints (sums)
+    DBuf<long long> uk_voff;                   // n_cells + 1 (entry offset per cell)
+    DBuf<long long> uk_hoff;                   // n_cells + 1 (header offset per cell)
+    DBuf<int> uk_na;                           // n_cells: A runs (entries 8 * na), then E columns
+    DBuf<int> uk_hdr;
+    DBuf<double> uk_val;                       // 8 * M * kp_u_entries
+    long long pk_slices = 0, pk_slots = 0, pk_hslots = 0;
+    DBuf<long long> pk_voff, pk_hoff;          // pk_slices + 1
+    DBuf<int> pk_hdr;                          // 32 * pk_hslots
+    DBuf<double> pk_val;                       // 32 * M * pk_slots
+    long long qk_slices = 0, qk_slots = 0;
+    DBuf<long long> qk_off;                    // qk_slices + 1
+    DBuf<int> qk_len;                          // n_q
+    DBuf<int> qk_col;                          // 32 * qk_slots
+    DBuf<double> qk_val;                       // 32 * M * qk_slots
+    DBuf<long long> strip_qslices;             // kp strips: QK slices holding an owned face
+    bool build_kp(const SpatialOps& ops, const double* theta, const double* w, cudaStream_t st);
+    void kp_launch(const double* x, double* y, double* y2, const double* V, int ncols, double* partial, bool strip,
+                   cudaStream_t st) const;
+    int kp_grid(bool strip) const;
+    void kp_to_csr(std::vector<long long>& off, std::vector<int>& idx, std::vector<double>& val, cudaStream_t st) const;
+
     // kappa: per-component stationary weights (w_i = tau kappa_i, fixed_stress.hpp:50);
     // null = 1 (the slab solver, slab.hpp:162)
     void build(const SpatialOps& ops, int m, const double* theta, double tau, cudaStream_t st,
@@ -62,6 +101,9 @@ struct SpaceTimeOp {
     // canonical CSR download (tests / CPU bitwise check)
     void to_csr(std::vector<long long>& off, std::vector<int>& idx, std::vector<double>& val, cudaStream_t st) const;
 };
+
+// exclusive prefix sum of in[0..n) into out[0..n] (out[n] = total, returned)
+long long scan_ll(const long long* in, long long* out, long long n, cudaStream_t st);
 
 void spmv_csr_device(int rows, const long long* off, const int* idx, const double* val, const double* x, double* y,
                      cudaStream_t st);

@@ -64,15 +64,19 @@ def _upload_from_oracle(rp, spec):
                                      m["inv_m"], m["k_dr"])
 
 
-@pytest.mark.parametrize("rows_per_thread", ["auto", "1", "2"])
+@pytest.mark.parametrize("layout", ["kp", "sell", "sell1", "sell2"])
 @pytest.mark.parametrize("n,r", [(16, 0), (16, 1), (64, 1)])
-def test_spacetime_operator_and_spmv_bit_identical(oracle, monkeypatch, n, r, rows_per_thread):
+def test_spacetime_operator_and_spmv_bit_identical(oracle, monkeypatch, n, r, layout):
     """Canonical space-time CSR and order-fixed SpMV == SparseMatrix::apply on
-    the oracle's canonical CSR (sparse.hpp:30-40), bit for bit, in both U-class
-    thread mappings (one row per thread for large operators, two rows sharing
-    the column and x loads for small ones; PDG_SPMV_ROWS forces one)."""
-    if rows_per_thread != "auto":
-        monkeypatch.setenv("PDG_SPMV_ROWS", rows_per_thread)
+    the oracle's canonical CSR (sparse.hpp:30-40), bit for bit, in every device
+    layout: the Kronecker-paired layout (default: the m rows of one spatial
+    pattern on one thread, one index per run of 8 displacement columns) and the
+    SELL layout (PDG_SPMV_FORMAT=sell) in both U-class thread mappings (one row
+    per thread, two rows sharing the column and x loads; PDG_SPMV_ROWS)."""
+    if layout != "kp":
+        monkeypatch.setenv("PDG_SPMV_FORMAT", "sell")
+    if layout in ("sell1", "sell2"):
+        monkeypatch.setenv("PDG_SPMV_ROWS", layout[-1])
     spec = P.config1(n)
     rp = oracle.RefProblem(spec.to_dict())
     T = oracle.time_constants(r)["T"]
@@ -725,12 +729,14 @@ def test_spmv_config3_1024_bit_identical_to_cpu(oracle):
 
 def test_spmv_config3_1024_properties(monkeypatch):
     """BASELINE config 3 at full size (1024^2, 23.1M rows, 955.6M nnz), through
-    size-independent properties: the two U-class thread mappings give the same
-    bits, repeated applications are bit-identical, A (2 x) = 2 A x exactly (a
-    power-of-two scaling commutes with every rounding), and A 0 = 0."""
+    size-independent properties: the Kronecker-paired layout and both SELL-layout
+    U-class thread mappings give the same bits, repeated applications are
+    bit-identical, A (2 x) = 2 A x exactly (a power-of-two scaling commutes with
+    every rounding), and A 0 = 0."""
     import torch
     T = S.time_constants(1)["T"]
-    op = S.SpaceTimeOperator(S.SpatialOperators.assemble(P.config3(1024)), T, 0.05)
+    ops = S.SpatialOperators.assemble(P.config3(1024))
+    op = S.SpaceTimeOperator(ops, T, 0.05)
     assert op.rows == 23072768 and op.nnz == 955559936  # SURVEY Appendix B
     x = torch.from_numpy(P.uniform_vector(P.X_SEED, op.rows)).cuda()
     y1, y2, y3 = (torch.empty_like(x) for _ in range(3))
@@ -738,11 +744,18 @@ def test_spmv_config3_1024_properties(monkeypatch):
     op.apply_device(x.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
-    monkeypatch.setenv("PDG_SPMV_ROWS", "2")
-    op.apply_device(x.data_ptr(), y3.data_ptr())
-    torch.cuda.synchronize()
-    assert torch.equal(y1, y3)
+    monkeypatch.setenv("PDG_SPMV_FORMAT", "sell")
+    op_sell = S.SpaceTimeOperator(ops, T, 0.05)
+    assert op_sell.nnz == op.nnz
+    for rows in ("1", "2"):
+        monkeypatch.setenv("PDG_SPMV_ROWS", rows)
+        y3.fill_(1.0)
+        op_sell.apply_device(x.data_ptr(), y3.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y3)
+    del op_sell
     monkeypatch.delenv("PDG_SPMV_ROWS")
+    monkeypatch.delenv("PDG_SPMV_FORMAT")
     x2 = 2.0 * x
     op.apply_device(x2.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
