@@ -75,6 +75,22 @@ typedef struct {
     double flow_data[4];        /* constant boundary pressure */
 } pdg_problem;
 
+/* 3D extension (BASELINE configs 2 and 4; the reference is 2D only): structured
+ * nx x ny x nz mesh of hexahedra with the reference's element pair generalised (discontinuous
+ * trilinear SIPG displacement, 24 dofs per cell; one normal-velocity flux dof per face; constant
+ * pressure per cell). Cell c = (k ny + j) nx + i; boundary tags xlo, xhi, ylo, yhi, zlo, zhi. */
+typedef struct {
+    int nx, ny, nz;
+    double lx, ly, lz;
+    double lambda, mu, k_perm, eta, biot_m, biot_b;
+    const double* k_perm_cells; /* NULL or nx*ny*nz values */
+    double penalty;
+    int disp_kind[6];           /* 0 fixed 1 traction 2 roller_x 3 roller_y 4 roller_z */
+    double disp_data[6][3];     /* constant Dirichlet value / traction vector */
+    int flow_kind[6];           /* 0 pressure, 1 no_flow */
+    double flow_data[6];        /* constant boundary pressure */
+} pdg_problem3;
+
 /* GmresOptions (gmres.hpp:24-28) + FixedStressConfig (fixed_stress.hpp:17-22). */
 typedef struct {
     double tol;     /* relative true residual, default 1e-10 */
@@ -114,6 +130,14 @@ int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr
                    double inv_m, double k_dr, pdg_ops** out);
 /* Assemble the operators on the device (one thread block per cell / face). */
 int pdg_ops_assemble(pdg_ctx* ctx, const pdg_problem* problem, pdg_ops** out);
+/* 3D: assemble on the device / upload host CSR blocks of an nx x ny x nz mesh (n_u = 24 n_p;
+ * the dimensions locate cells and faces for the nested-dissection orderings). Every handle
+ * built on such operators (pdg_block, pdg_slab, pdg_op, pdg_fs for r = 0) works unchanged;
+ * strips (pdg_op_set_strip, pdg_dblock) are 2D only. */
+int pdg_ops_assemble3(pdg_ctx* ctx, const pdg_problem3* problem, pdg_ops** out);
+int pdg_ops_upload3(pdg_ctx* ctx, int nx, int ny, int nz, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B,
+                    const pdg_csr* E, const double* m_p_diag, const signed char* q_constrained, double biot_b,
+                    double inv_m, double k_dr, pdg_ops** out);
 /* Sizes: n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E). */
 int pdg_ops_sizes(const pdg_ops* ops, long long sizes[7]);
 /* Download block `which` (0 A, 1 M_q, 2 B, 3 E) as CSR into caller buffers. */

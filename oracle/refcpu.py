@@ -42,6 +42,16 @@ class _Problem(C.Structure):
     ]
 
 
+class _Problem3(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
+        ("lam", C.c_double), ("mu", C.c_double), ("k_perm", C.c_double), ("eta", C.c_double),
+        ("biot_m", C.c_double), ("biot_b", C.c_double), ("k_perm_cells", C.POINTER(C.c_double)),
+        ("penalty", C.c_double), ("disp_kind", C.c_int * 6), ("disp_data", (C.c_double * 3) * 6),
+        ("flow_kind", C.c_int * 6), ("flow_data", C.c_double * 6),
+    ]
+
+
 class _Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int), ("max_iter", C.c_int), ("sweeps", C.c_int),
                 ("stab", C.c_double), ("backend", C.c_int), ("flexible", C.c_int)]
@@ -69,9 +79,10 @@ def _ip(a):
     return a.ctypes.data_as(C.POINTER(C.c_int))
 
 
-DISP = {"fixed": 0, "traction": 1, "roller_x": 2, "roller_y": 3}
+DISP = {"fixed": 0, "traction": 1, "roller_x": 2, "roller_y": 3, "roller_z": 4}
 FLOW = {"pressure": 0, "no_flow": 1}
 TAGS = ("left", "right", "bottom", "top")
+TAGS3 = ("xlo", "xhi", "ylo", "yhi", "zlo", "zhi")
 
 
 class RefProblem:
@@ -79,24 +90,28 @@ class RefProblem:
     paper_1801_04984_b200.problem.ProblemSpec.to_dict for the fields)."""
 
     def __init__(self, spec: dict):
-        p = _Problem()
+        three_d = spec.get("nz") is not None
+        p = _Problem3() if three_d else _Problem()
         p.nx, p.ny, p.lx, p.ly = spec["nx"], spec["ny"], spec["lx"], spec["ly"]
+        if three_d:
+            p.nz, p.lz = spec["nz"], spec["lz"]
         p.lam, p.mu, p.k_perm, p.eta = spec["lam"], spec["mu"], spec["k_perm"], spec["eta"]
         p.biot_m, p.biot_b, p.penalty = spec["biot_m"], spec["biot_b"], spec["penalty"]
         self._k = None
         if spec.get("k_perm_cells") is not None:
             self._k = np.ascontiguousarray(spec["k_perm_cells"], dtype=np.float64)
             p.k_perm_cells = _dp(self._k)
-        for s, tag in enumerate(TAGS):
+        for s, tag in enumerate(TAGS3 if three_d else TAGS):
             kind, data = spec["disp"][tag]
             p.disp_kind[s] = DISP[kind]
-            p.disp_data[s][0], p.disp_data[s][1] = data
+            for k, v in enumerate(data):
+                p.disp_data[s][k] = v
             fk, fd = spec["flow"][tag]
             p.flow_kind[s] = FLOW[fk]
             p.flow_data[s] = fd
         self.spec = spec
         h = C.c_void_p()
-        _check(lib().refcpu_create(C.byref(p), C.byref(h)))
+        _check((lib().refcpu_create3 if three_d else lib().refcpu_create)(C.byref(p), C.byref(h)))
         self._h = h
         sz = (C.c_longlong * 8)()
         _check(lib().refcpu_sizes(self._h, sz))

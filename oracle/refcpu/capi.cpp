@@ -8,6 +8,7 @@
 #include <random>
 
 #include "solver.hpp"
+#include "fem3d.hpp"
 
 using namespace refcpu;
 
@@ -33,7 +34,17 @@ struct Handle {
     SpatialOperators ops;
     VolumeData data;
     std::string err;
+    // 3D extension (fem3d.hpp; no reference counterpart): dim == 3 uses mesh3 / bc3
+    int dim = 2;
+    Mesh3 mesh3;
+    BoundarySpec3 bc3;
 };
+
+// assemble_rhs of either dimension
+static FieldVecs rhs_at(Handle* h, double t) {
+    if (h->dim == 3) return assemble_rhs3(h->mesh3, h->ops.mat, h->ops, h->bc3, t);
+    return assemble_rhs(h->mesh, h->dofs, h->ops.mat, h->ops, h->data, t);
+}
 
 static thread_local std::string g_err;
 
@@ -94,6 +105,46 @@ int refcpu_create(const refcpu_problem* p, void** out) {
     GUARD_END
 }
 
+// 3D problem (fem3d.hpp): tags xlo, xhi, ylo, yhi, zlo, zhi; displacement kinds 0 fixed,
+// 1 traction, 2 / 3 / 4 roller fixing the x / y / z component; constant data.
+typedef struct {
+    int nx, ny, nz;
+    double lx, ly, lz;
+    double lambda, mu, k_perm, eta, biot_m, biot_b;
+    const double* k_perm_cells;  // nullptr or nx*ny*nz values (cell c = (k*ny + j)*nx + i)
+    double penalty;
+    int disp_kind[6];
+    double disp_data[6][3];
+    int flow_kind[6];  // 0 pressure, 1 no_flow
+    double flow_data[6];
+} refcpu_problem3;
+
+int refcpu_create3(const refcpu_problem3* p, void** out) {
+    GUARD_BEGIN
+    auto h = std::make_unique<Handle>();
+    h->dim = 3;
+    h->mesh3 = build_mesh3(p->nx, p->ny, p->nz, p->lx, p->ly, p->lz);
+    MaterialParameters mat = material_from_lame3(p->lambda, p->mu, p->k_perm, p->eta, p->biot_m, p->biot_b);
+    if (p->k_perm_cells) mat.k_perm_cells.assign(p->k_perm_cells, p->k_perm_cells + (size_t)p->nx * p->ny * p->nz);
+    for (int s = 0; s < 6; ++s) {
+        DisplacementBC3& d = h->bc3.displacement[s];
+        const int kind = p->disp_kind[s];
+        if (kind < 0 || kind > 4) throw std::invalid_argument("bad displacement kind");
+        d.dirichlet = {kind == 0 || kind == 2, kind == 0 || kind == 3, kind == 0 || kind == 4};
+        for (int k = 0; k < 3; ++k) {
+            // dirichlet data only for fixed(); rollers and traction faces carry traction data
+            d.dirichlet_data[k] = kind == 0 ? p->disp_data[s][k] : 0.0;
+            d.traction_data[k] = kind == 0 ? 0.0 : p->disp_data[s][k];
+        }
+        if (p->flow_kind[s] != 0 && p->flow_kind[s] != 1) throw std::invalid_argument("bad flow kind");
+        h->bc3.flow[s].no_flow = p->flow_kind[s] == 1;
+        h->bc3.flow[s].pressure = p->flow_data[s];
+    }
+    h->ops = assemble_operators3(h->mesh3, mat, p->penalty, h->bc3);
+    *out = h.release();
+    GUARD_END
+}
+
 void refcpu_destroy(void* h) { delete static_cast<Handle*>(h); }
 
 // sizes[0..] = n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E), nnz(M_p)
@@ -148,7 +199,7 @@ int refcpu_export_misc(void* hp, double* m_p_diag, signed char* q_constrained, d
 int refcpu_assemble_rhs(void* hp, double t, double* u, double* q, double* p) {
     GUARD_BEGIN
     auto* h = static_cast<Handle*>(hp);
-    const FieldVecs r = assemble_rhs(h->mesh, h->dofs, h->ops.mat, h->ops, h->data, t);
+    const FieldVecs r = rhs_at(h, t);
     std::memcpy(u, r.u.data(), sizeof(double) * r.u.size());
     std::memcpy(q, r.q.data(), sizeof(double) * r.q.size());
     std::memcpy(p, r.p.data(), sizeof(double) * r.p.size());
@@ -319,7 +370,7 @@ int refcpu_march(void* hp, int r, double T, int n_slabs, const refcpu_solve_opts
         const double tau = part.slab_length(n), t0 = part.t_begin(n);
         std::vector<FieldVecs> nodal(basis.n_nodes());
         for (int i = 0; i < basis.n_nodes(); ++i)
-            nodal[i] = assemble_rhs(h->mesh, h->dofs, ops.mat, ops, h->data, t0 + basis.nodes[i] * tau);
+            nodal[i] = rhs_at(h, t0 + basis.nodes[i] * tau);
         const SlabSystem sys = build_slab_system(ops, basis, tau, nodal, u_prev, p_prev);
         const bool rebuild = cached_tau < 0.0 || std::abs(tau - cached_tau) > 1e-12 * tau;
         try {
@@ -395,7 +446,7 @@ int refcpu_march_fs(void* hp, int r, double T, int n_slabs, double tol, int max_
         const double tau = part.slab_length(n), t0 = part.t_begin(n);
         std::vector<FieldVecs> nodal(nn);
         for (int i = 0; i < nn; ++i)
-            nodal[i] = assemble_rhs(h->mesh, h->dofs, ops.mat, ops, h->data, t0 + basis.nodes[i] * tau);
+            nodal[i] = rhs_at(h, t0 + basis.nodes[i] * tau);
         const SlabSystem sys = build_slab_system(ops, basis, tau, nodal, u_prev, p_prev);
         const bool rebuild = cached_tau < 0.0 || std::abs(tau - cached_tau) > 1e-12 * tau;
         try {
@@ -440,7 +491,7 @@ int refcpu_slab_rhs(void* hp, int r, double t0, double tau, const double* u_prev
     const TimeBasis basis = time_matrices(r);
     std::vector<FieldVecs> nodal(basis.n_nodes());
     for (int i = 0; i < basis.n_nodes(); ++i)
-        nodal[i] = assemble_rhs(h->mesh, h->dofs, h->ops.mat, h->ops, h->data, t0 + basis.nodes[i] * tau);
+        nodal[i] = rhs_at(h, t0 + basis.nodes[i] * tau);
     const SlabSystem sys = build_slab_system(h->ops, basis, tau, nodal, Vec(u_prev, u_prev + h->ops.n_u),
                                              Vec(p_prev, p_prev + h->ops.n_p));
     for (int i = 0; i < basis.n_nodes(); ++i) std::copy(sys.rhs[i].begin(), sys.rhs[i].end(), out + i * h->ops.n_total());

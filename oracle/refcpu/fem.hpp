@@ -523,6 +523,9 @@ struct SpatialOperators {
     std::vector<char> q_constrained;
     std::vector<Triplet> mq_bc, b_bc;
     Vec rhs_ref_u;  // A u0 - b E p0 - E sigma_v0 : zero (no reference-state fields in scope)
+    // oracle-only: banded ordering of the faces for the sparse-direct flow backend when the
+    // mesh is not the 2D structured one (fem3d.hpp); empty = the 2D face-row order
+    std::vector<int> face_band_perm;
     int n_u = 0, n_q = 0, n_p = 0;
     int n_total() const { return n_u + n_q + n_p; }
 };

@@ -281,12 +281,14 @@ public:
             for (auto& a : cell_faces[c])
                 for (auto& bb : cell_faces[c]) ts.push_back({a.first, bb.first, -(w * a.second) * (w * bb.second) * dinv_[c]});
         const SparseMatrix S = csr_from_triplets(nq_, nq_, ts);
-        std::vector<int> perm;
-        perm.reserve(nq_);
-        for (int j = 0; j <= ny; ++j) {
-            for (int i = 0; i < nx; ++i) perm.push_back(j * nx + i);
-            if (j < ny)
-                for (int i = 0; i <= nx; ++i) perm.push_back(nx * (ny + 1) + i * ny + j);
+        std::vector<int> perm = ops.face_band_perm;
+        if (perm.empty()) {
+            perm.reserve(nq_);
+            for (int j = 0; j <= ny; ++j) {
+                for (int i = 0; i < nx; ++i) perm.push_back(j * nx + i);
+                if (j < ny)
+                    for (int i = 0; i <= nx; ++i) perm.push_back(nx * (ny + 1) + i * ny + j);
+            }
         }
         chol_ = std::make_unique<BandCholesky>(S, perm);
     }

@@ -44,6 +44,14 @@ class Problem(C.Structure):
                 ("flow_kind", C.c_int * 4), ("flow_data", C.c_double * 4)]
 
 
+class Problem3(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("lx", C.c_double), ("ly", C.c_double),
+                ("lz", C.c_double), ("lam", C.c_double), ("mu", C.c_double), ("k_perm", C.c_double),
+                ("eta", C.c_double), ("biot_m", C.c_double), ("biot_b", C.c_double),
+                ("k_perm_cells", C.POINTER(C.c_double)), ("penalty", C.c_double), ("disp_kind", C.c_int * 6),
+                ("disp_data", (C.c_double * 3) * 6), ("flow_kind", C.c_int * 6), ("flow_data", C.c_double * 6)]
+
+
 class GmresOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int), ("max_iter", C.c_int), ("sweeps", C.c_int),
                 ("stab", C.c_double), ("candidate", C.c_int)]
@@ -74,6 +82,10 @@ _SIGS = {
                                  C.POINTER(VP)]),
     "pdg_mesh_dims_from_operators": (C.c_int, [C.POINTER(CSR), C.c_int, IP]),
     "pdg_ops_assemble": (C.c_int, [VP, C.POINTER(Problem), C.POINTER(VP)]),
+    "pdg_ops_assemble3": (C.c_int, [VP, C.POINTER(Problem3), C.POINTER(VP)]),
+    "pdg_ops_upload3": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.POINTER(CSR), C.POINTER(CSR), C.POINTER(CSR),
+                                  C.POINTER(CSR), DP, C.POINTER(C.c_byte), C.c_double, C.c_double, C.c_double,
+                                  C.POINTER(VP)]),
     "pdg_ops_sizes": (C.c_int, [VP, LLP]),
     "pdg_ops_download": (C.c_int, [VP, C.c_int, IP, IP, DP]),
     "pdg_ops_rhs": (C.c_int, [VP, C.c_double, DP, DP, DP]),

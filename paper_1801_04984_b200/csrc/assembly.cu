@@ -676,6 +676,7 @@ void assemble_ops_device(SpatialOps& s, const pdg_problem& p, cudaStream_t st) {
 }
 
 void assemble_rhs_device(const SpatialOps& s, double t, double* u, double* q, double* p, cudaStream_t st) {
+    if (s.nz > 0) return assemble_rhs_device3(s, t, u, q, p, st);
     (void)t;  // constant boundary data: time-independent
     const Geo g = make_geo(s.prob);
     k_rhs_u<<<grid_for(8LL * s.n_p, 256), 256, 0, st>>>(g, u);

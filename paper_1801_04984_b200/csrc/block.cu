@@ -491,8 +491,52 @@ int nd_leaf_dofs(int dflt, const char* var) {
     return e ? std::max(1, std::atoi(e)) : dflt;
 }
 
+// 3D face centres (assembly3d.cu numbering): z-normal (i + 1/2, j + 1/2, k), y-normal
+// (i + 1/2, j, k + 1/2), x-normal (i, j + 1/2, k + 1/2)
+void face_coords3(int nx, int ny, int nz, std::vector<double>& cx, std::vector<double>& cy, std::vector<double>& cz) {
+    const int nzf = nx * ny * (nz + 1), nyf = nx * (ny + 1) * nz, nq = nzf + nyf + (nx + 1) * ny * nz;
+    cx.assign(nq, 0.0);
+    cy.assign(nq, 0.0);
+    cz.assign(nq, 0.0);
+    for (int f = 0; f < nq; ++f) {
+        if (f < nzf) {
+            cx[f] = f % nx + 0.5;
+            cy[f] = (f / nx) % ny + 0.5;
+            cz[f] = f / (nx * ny);
+        } else if (f < nzf + nyf) {
+            const int g = f - nzf;
+            cx[f] = g % nx + 0.5;
+            cz[f] = (g / nx) % nz + 0.5;
+            cy[f] = g / (nx * nz);
+        } else {
+            const int g = f - nzf - nyf;
+            cy[f] = g % ny + 0.5;
+            cz[f] = (g / ny) % nz + 0.5;
+            cx[f] = g / (ny * nz);
+        }
+    }
+}
+
 std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st) {
     auto a = std::make_shared<ASolver>();
+    if (ops.nz > 0) {
+        // 3D: nested dissection over cells (24 dofs each, centres (i + 1/2, j + 1/2, k + 1/2))
+        const long long nc = (long long)ops.nx * ops.ny * ops.nz;
+        require(ops.nx > 0 && ops.ny > 0 && ops.n_u == 24 * nc, "A solver: mesh dimensions do not match n_u");
+        const HCsr h = csr_download(ops.A, st);
+        std::vector<int> node_of(ops.n_u);
+        for (int d = 0; d < ops.n_u; ++d) node_of[d] = d / 24;
+        std::vector<double> cx(nc), cy(nc), cz(nc);
+        for (int c = 0; c < nc; ++c) {
+            cx[c] = c % ops.nx + 0.5;
+            cy[c] = (c / ops.nx) % ops.ny + 0.5;
+            cz[c] = c / (ops.nx * ops.ny) + 0.5;
+        }
+        a->use_nd = true;
+        a->nd.prof_phase = PROF_A_SOLVE;
+        a->nd.factor(ops.n_u, h.off, h.idx, h.val, node_of, cx, cy, nd_leaf_dofs(192), max_rhs, st, &cz);
+        return a;
+    }
     // cell-row order: block j = displacement dofs of cell row j (8 nx each)
     require(ops.nx > 0 && ops.ny > 0 && ops.n_u == 8 * ops.nx * ops.ny, "A solver: mesh dimensions do not match n_u");
     // nd (default): nested dissection; local: twisted block-tridiagonal inverse-Schur sweep;
@@ -647,13 +691,17 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
     PDG_CHECK_LAUNCH();
     // face-row permutation: level j horizontal faces, then row j vertical faces
     const int nx = o.nx, ny = o.ny;
-    require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
+    if (o.nz > 0)
+        require(o.n_q == nx * ny * (o.nz + 1) + nx * (ny + 1) * o.nz + (nx + 1) * ny * o.nz,
+                "fixed-stress: face count does not match the mesh");
+    else
+        require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
     rq.alloc((size_t)m * o.n_q);
     fp.alloc((size_t)m * o.n_p);
     mech.alloc((size_t)m * o.n_u);
     if (sweeps > 1) xold.alloc((size_t)m * o.n_total());
     const char* fmode = std::getenv("PDG_FLOW_SOLVER");  // nd (default) | blocktri
-    if ((!fmode || std::string(fmode) == "nd") && !std::getenv("PDG_FLOW_STRIPS")) {
+    if (o.nz > 0 || ((!fmode || std::string(fmode) == "nd") && !std::getenv("PDG_FLOW_STRIPS"))) {
         // S_q assembled on the host (the entries of k_flow_schur_blocks), nested dissection over
         // faces: horizontal j*nx+i at (i + 1/2, j), vertical nx(ny+1) + i*ny + j at (i, j + 1/2)
         const HCsr sq = flow_schur_host(o, w, dinv.download(st), st);
@@ -661,12 +709,16 @@ void FixedStressPre::setup(const SpatialOps& o, int m_, double tau_, double lamb
         const std::vector<int>& idx = sq.idx;
         const std::vector<double>& val = sq.val;
         std::vector<int> node_of(o.n_q);
-        std::vector<double> cx, cy;
-        face_coords(nx, ny, cx, cy);
+        std::vector<double> cx, cy, cz;
+        if (o.nz > 0)
+            face_coords3(nx, ny, o.nz, cx, cy, cz);
+        else
+            face_coords(nx, ny, cx, cy);
         for (int f = 0; f < o.n_q; ++f) node_of[f] = f;
         flow_use_nd = true;
         flow_nd.prof_phase = PROF_FLOW_SOLVE;
-        flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(128, "PDG_ND_FLOW_LEAF"), m, st);
+        flow_nd.factor(o.n_q, off, idx, val, node_of, cx, cy, nd_leaf_dofs(128, "PDG_ND_FLOW_LEAF"), m, st,
+                       o.nz > 0 ? &cz : nullptr);
         return;
     }
     std::vector<int> perm;
@@ -735,6 +787,7 @@ void FixedStressPre::setup_coupled(const SpatialOps& o, int m_, double tau_, con
     PDG_CHECK_LAUNCH();
     // face-row blocks holding both components: block j = [comp 0 faces of face row j, comp 1 ...]
     const int nx = o.nx, ny = o.ny;
+    require(o.nz == 0, "fixed-stress march with coupled components: 2D meshes only");
     require(o.n_q == nx * (ny + 1) + (nx + 1) * ny, "fixed-stress: face count does not match the mesh");
     std::vector<int> perm, bs;
     for (int j = 0; j <= ny; ++j) {

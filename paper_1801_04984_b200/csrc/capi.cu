@@ -380,6 +380,58 @@ int pdg_ops_assemble(pdg_ctx* ctx, const pdg_problem* problem, pdg_ops** out) {
     API_END
 }
 
+int pdg_ops_assemble3(pdg_ctx* ctx, const pdg_problem3* problem, pdg_ops** out) {
+    API_BEGIN
+    require(ctx && problem && out, "pdg_ops_assemble3: null argument");
+    PDG_CUDA(cudaSetDevice(ctx->c.device));
+    cudaStream_t st = ctx->c.stream;
+    auto o = std::make_unique<pdg_ops>();
+    o->s.ctx = &ctx->c;
+    SetupTimer timer(SETUP_ASSEMBLE, st);
+    assemble_ops_device3(o->s, *problem, st);
+    finish_ops(o->s, st);
+    *out = o.release();
+    API_END
+}
+
+int pdg_ops_upload3(pdg_ctx* ctx, int nx, int ny, int nz, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B,
+                    const pdg_csr* E, const double* m_p_diag, const signed char* q_constrained, double biot_b,
+                    double inv_m, double k_dr, pdg_ops** out) {
+    API_BEGIN
+    require(ctx && A && M_q && B && E && m_p_diag && out, "pdg_ops_upload3: null argument");
+    require(nx > 0 && ny > 0 && nz > 0, "pdg_ops_upload3: mesh dimensions must be positive");
+    PDG_CUDA(cudaSetDevice(ctx->c.device));
+    cudaStream_t st = ctx->c.stream;
+    auto o = std::make_unique<pdg_ops>();
+    SpatialOps& s = o->s;
+    s.ctx = &ctx->c;
+    s.nx = nx;
+    s.ny = ny;
+    s.nz = nz;
+    s.n_u = A->rows;
+    s.n_q = M_q->rows;
+    s.n_p = B->cols;
+    require(A->cols == s.n_u && E->rows == s.n_u && E->cols == s.n_p && B->rows == s.n_q && M_q->cols == s.n_q,
+            "pdg_ops_upload3: block dimensions are inconsistent");
+    const long long nc = (long long)nx * ny * nz;
+    require(s.n_u == 24 * nc && s.n_p == nc &&
+                s.n_q == (long long)nx * ny * (nz + 1) + (long long)nx * (ny + 1) * nz + (long long)(nx + 1) * ny * nz,
+            "pdg_ops_upload3: sizes do not match an nx x ny x nz mesh");
+    s.biot_b = biot_b;
+    s.inv_m = inv_m;
+    s.k_dr = k_dr;
+    csr_upload(s.A, *A, st);
+    csr_upload(s.M_q, *M_q, st);
+    csr_upload(s.B, *B, st);
+    csr_upload(s.E, *E, st);
+    s.m_p.upload(m_p_diag, s.n_p, st);
+    s.q_constrained.alloc(s.n_q);
+    if (q_constrained) s.q_constrained.upload(q_constrained, s.n_q, st);
+    finish_ops(s, st);
+    *out = o.release();
+    API_END
+}
+
 int pdg_ops_sizes(const pdg_ops* ops, long long sizes[7]) {
     API_BEGIN
     require(ops && sizes, "pdg_ops_sizes: null argument");

@@ -66,26 +66,27 @@ struct Dissector {
     const std::vector<int>& aoff;  // node adjacency CSR
     const std::vector<int>& adj;
     const std::vector<int>& ndofs;
-    const std::vector<double>& cx;
-    const std::vector<double>& cy;
+    std::vector<const std::vector<double>*> cs;  // node coordinates per axis (2 or 3 axes)
     int leaf;
     std::vector<HostFront> fr;
     std::vector<int> node_front, mark, seen;
     int stamp = 0;
 
     Dissector(const std::vector<int>& o, const std::vector<int>& a, const std::vector<int>& nd,
-              const std::vector<double>& x, const std::vector<double>& y, int lf)
-        : aoff(o), adj(a), ndofs(nd), cx(x), cy(y), leaf(lf) {
+              const std::vector<double>& x, const std::vector<double>& y, const std::vector<double>* z, int lf)
+        : aoff(o), adj(a), ndofs(nd), leaf(lf) {
+        cs = {&x, &y};
+        if (z) cs.push_back(z);
         const int nn = static_cast<int>(nd.size());
         node_front.assign(nn, -1);
         mark.assign(nn, 0);
         seen.assign(nn, 0);
     }
 
-    // try to cut `nodes` at the line coord == v (axis 0: x, 1: y)
+    // try to cut `nodes` at the line / plane coord == v (axis 0: x, 1: y, 2: z)
     bool try_cut(const std::vector<int>& nodes, int axis, double v, int st, std::vector<int>& sep,
                  std::vector<int>& lo, std::vector<int>& hi) {
-        const std::vector<double>& c = axis == 0 ? cx : cy;
+        const std::vector<double>& c = *cs[axis];
         sep.clear();
         lo.clear();
         hi.clear();
@@ -124,17 +125,19 @@ struct Dissector {
         std::vector<int> sep, lo, hi;
         bool cut = false;
         if (dofs > leaf && nodes.size() >= 3) {
-            double mn[2] = {1e300, 1e300}, mx[2] = {-1e300, -1e300};
-            for (int u : nodes) {
-                mn[0] = std::min(mn[0], cx[u]);
-                mx[0] = std::max(mx[0], cx[u]);
-                mn[1] = std::min(mn[1], cy[u]);
-                mx[1] = std::max(mx[1], cy[u]);
-            }
-            const int first = (mx[0] - mn[0] >= mx[1] - mn[1]) ? 0 : 1;
-            for (int t = 0; t < 2 && !cut; ++t) {
-                const int axis = t == 0 ? first : 1 - first;
-                const std::vector<double>& c = axis == 0 ? cx : cy;
+            const int nax = static_cast<int>(cs.size());
+            double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+            for (int u : nodes)
+                for (int a = 0; a < nax; ++a) {
+                    mn[a] = std::min(mn[a], (*cs[a])[u]);
+                    mx[a] = std::max(mx[a], (*cs[a])[u]);
+                }
+            // axes by decreasing extent (ties: the lower axis first)
+            int order[3] = {0, 1, 2};
+            std::stable_sort(order, order + nax, [&](int a, int b) { return mx[a] - mn[a] > mx[b] - mn[b]; });
+            for (int t = 0; t < nax && !cut; ++t) {
+                const int axis = order[t];
+                const std::vector<double>& c = *cs[axis];
                 std::vector<double> vals;
                 vals.reserve(nodes.size());
                 for (int u : nodes) vals.push_back(c[u]);
@@ -810,7 +813,7 @@ __global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
 
 void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>& idx, const std::vector<double>& val,
                     const std::vector<int>& node_of, const std::vector<double>& cx, const std::vector<double>& cy,
-                    int leaf_dofs, int max_rhs_, cudaStream_t st) {
+                    int leaf_dofs, int max_rhs_, cudaStream_t st, const std::vector<double>* cz) {
     n = n_;
     max_rhs = max_rhs_;
     const int stage0 = prof_phase == PROF_A_SOLVE ? SETUP_A_ANALYSIS : SETUP_F_ANALYSIS;
@@ -846,7 +849,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         }
     }
     // ---- dissection ----
-    Dissector ds(aoff, adj, ndofs, cx, cy, leaf_dofs);
+    Dissector ds(aoff, adj, ndofs, cx, cy, cz, leaf_dofs);
     {
         std::vector<int> all(nn);
         std::iota(all.begin(), all.end(), 0);

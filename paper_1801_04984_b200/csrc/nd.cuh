@@ -100,10 +100,10 @@ struct NdChol {
     std::vector<NdFront> fronts;
 
     // SPD matrix in host CSR (full symmetric pattern, natural numbering);
-    // node_of[dof] groups dofs into graph nodes with coordinates (cx, cy).
+    // node_of[dof] groups dofs into graph nodes with coordinates (cx, cy[, cz]).
     void factor(int n, const std::vector<int>& off, const std::vector<int>& idx, const std::vector<double>& val,
                 const std::vector<int>& node_of, const std::vector<double>& cx, const std::vector<double>& cy,
-                int leaf_dofs, int max_rhs, cudaStream_t st);
+                int leaf_dofs, int max_rhs, cudaStream_t st, const std::vector<double>* cz = nullptr);
     // x = A^{-1} b, nrhs <= max_rhs columns at strides ldb / ldx
     void solve(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
 

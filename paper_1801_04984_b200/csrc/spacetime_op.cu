@@ -354,16 +354,20 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     for (int k = 0; k < m * m; ++k) th.t[k] = theta[k];
     for (int i = 0; i < m; ++i) th.w[i] = kappa ? tau * kappa[i] : tau;
     const double mb = -ops.biot_b, minv = -ops.inv_m;
-    require(ops.n_u == 8 * ops.n_p, "space-time block: n_u must be 8 * n_cells");
-    u_groups = (long long)m * n_cells;
+    // U groups: 8 consecutive displacement rows sharing one column list (a 2D cell, or a third
+    // of a 3D cell's 24 rows)
+    require(ops.n_u % 8 == 0 && (ops.n_u == 8 * ops.n_p || ops.n_u == 24 * ops.n_p),
+            "space-time block: n_u must be 8 or 24 times n_cells");
+    n_ug = ops.n_u / 8;
+    u_groups = (long long)m * n_ug;
     s_rows = (long long)m * (n_q + n_p);
     s_slices = (s_rows + 31) / 32;
-    if (build_kp(ops, th.t, th.w, st)) return;
+    if (ops.n_u == 8 * ops.n_p && build_kp(ops, th.t, th.w, st)) return;
 
     // U class
     DBuf<long long> cnt(u_groups + 1);
     cnt.zero(st);
-    k_u_count<<<grid_for(u_groups, 256), 256, 0, st>>>(n_cells, ops.A.off.p, ops.E.off.p, m, cnt.p);
+    k_u_count<<<grid_for(u_groups, 256), 256, 0, st>>>(n_ug, ops.A.off.p, ops.E.off.p, m, cnt.p);
     PDG_CHECK_LAUNCH();
     u_off.alloc(u_groups + 1);
     u_entries = scan_ll(cnt.p, u_off.p, u_groups, st);
@@ -371,7 +375,7 @@ void SpaceTimeOp::build(const SpatialOps& ops, int m_, const double* theta, doub
     u_val.alloc(8 * u_entries);
     DBuf<int> err(1);
     err.zero(st);
-    k_u_fill<<<grid_for(u_groups * 8, 256), 256, 0, st>>>(n_cells, m, nt, n_u, n_q, th, mb, ops.A.off.p, ops.A.idx.p,
+    k_u_fill<<<grid_for(u_groups * 8, 256), 256, 0, st>>>(n_ug, m, nt, n_u, n_q, th, mb, ops.A.off.p, ops.A.idx.p,
                                                            ops.A.val.p, ops.E.off.p, ops.E.idx.p, ops.E.val.p, u_off.p,
                                                            u_col.p, u_val.p, err.p);
     PDG_CHECK_LAUNCH();
@@ -416,7 +420,7 @@ void SpaceTimeOp::apply(const double* x, double* y, cudaStream_t st) const {
     const long long u_threads = u_groups * (u2 ? 4 : 8);
     const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
-    k_spmv<false><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p,
+    k_spmv<false><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_ug, nt, n_u, n_q, n_p, u_off.p, u_col.p,
                                                   u_val.p, s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard, nullptr, 0, rows,
                                                   nullptr, nullptr);
     count_launch();
@@ -446,7 +450,7 @@ void SpaceTimeOp::apply_dots(const double* x, double* y, double* y2, const doubl
     const long long u_threads = u_groups * (u2 ? 4 : 8);
     const int gu = static_cast<int>(std::min<long long>((u_threads + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
     const int gs = static_cast<int>(std::min<long long>((s_rows + kSpmvBlock - 1) / kSpmvBlock, (long long)num_sms() * 16));
-    k_spmv<true><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_cells, nt, n_u, n_q, n_p, u_off.p, u_col.p,
+    k_spmv<true><<<gu + gs, kSpmvBlock, 0, st>>>(u_threads, u2, s_rows, gu, n_ug, nt, n_u, n_q, n_p, u_off.p, u_col.p,
                                                  u_val.p, s_off.p, s_len.p, s_col.p, s_val.p, x, y, guard, V, ncols, rows,
                                                  y2, partial);
     count_launch();
@@ -454,7 +458,8 @@ void SpaceTimeOp::apply_dots(const double* x, double* y, double* y2, const doubl
 }
 
 void SpaceTimeOp::set_strip(int nx, int ny, int r0, int r1, cudaStream_t st) {
-    require(nx > 0 && ny > 0 && (long long)nx * ny == n_cells, "space-time block: strip mesh does not match the operator");
+    require(nx > 0 && ny > 0 && (long long)nx * ny == n_cells && n_u == 8 * n_p,
+            "space-time block: strip mesh does not match the operator (strips are 2D only)");
     require(0 <= r0 && r0 < r1 && r1 <= ny, "space-time block: bad strip rows");
     strip_nx = nx;
     strip_ny = ny;
@@ -538,7 +543,7 @@ void SpaceTimeOp::to_csr(std::vector<long long>& off, std::vector<int>& idx, std
     const auto sv = s_val.download(st);
     std::vector<int> len(rows, 0);
     for (long long g = 0; g < u_groups; ++g) {
-        const int i = static_cast<int>(g / n_cells), c = static_cast<int>(g % n_cells);
+        const int i = static_cast<int>(g / n_ug), c = static_cast<int>(g % n_ug);
         for (int l = 0; l < 8; ++l) len[(long long)i * nt + 8 * c + l] = static_cast<int>(uo[g + 1] - uo[g]);
     }
     for (long long s = 0; s < s_rows; ++s) {
@@ -550,7 +555,7 @@ void SpaceTimeOp::to_csr(std::vector<long long>& off, std::vector<int>& idx, std
     idx.resize(off[rows]);
     val.resize(off[rows]);
     for (long long g = 0; g < u_groups; ++g) {
-        const int i = static_cast<int>(g / n_cells), c = static_cast<int>(g % n_cells);
+        const int i = static_cast<int>(g / n_ug), c = static_cast<int>(g % n_ug);
         for (int l = 0; l < 8; ++l) {
             long long o = off[(long long)i * nt + 8 * c + l];
             for (long long k = uo[g]; k < uo[g + 1]; ++k, ++o) {

@@ -24,6 +24,7 @@ struct SpaceTimeOp {
     int m = 1;           // time components in the block
     int nt = 0;          // n_u + n_q + n_p
     int n_u = 0, n_q = 0, n_p = 0, n_cells = 0;
+    int n_ug = 0;        // U groups per component (n_u / 8: one per 2D cell, three per 3D cell)
     long long rows = 0, nnz = 0;
     // U class
     long long u_groups = 0, u_entries = 0;  // entries counted per group (x8 values)

@@ -179,9 +179,9 @@ PROFILE_PHASES = ("spmv", "a_solve", "flow_solve", "precond_other", "krylov", "s
 class SpatialOperators:
     """Device-resident A, M_q, B, E, m_p (SpatialOperators, assembly.hpp:38-52)."""
 
-    def __init__(self, handle, nx, ny):
+    def __init__(self, handle, nx, ny, nz=0):
         self._h = handle
-        self.nx, self.ny = nx, ny
+        self.nx, self.ny, self.nz = nx, ny, nz  # nz > 0: 3D extension (24 displacement dofs per cell)
         sz = (C.c_longlong * 7)()
         check(lib().pdg_ops_sizes(self._h, sz))
         self.n_u, self.n_q, self.n_p = sz[0], sz[1], sz[2]
@@ -193,15 +193,22 @@ class SpatialOperators:
         """assemble_operators (assembly.hpp:177-395) on the device."""
         p, keep = spec.to_struct()
         h = C.c_void_p()
+        if isinstance(p, _lib.Problem3):  # 3D extension (assembly3d.cu)
+            check(lib().pdg_ops_assemble3(context(device), C.byref(p), C.byref(h)))
+            return cls(h, spec.nx, spec.ny, spec.nz)
         check(lib().pdg_ops_assemble(context(device), C.byref(p), C.byref(h)))
         del keep
         return cls(h, spec.nx, spec.ny)
 
     @classmethod
-    def upload(cls, nx, ny, blocks, m_p_diag, q_constrained, biot_b, inv_m, k_dr, device: int = 0):
-        """Upload host CSR blocks {'A','M_q','B','E': (off, idx, val)}."""
-        n_u, n_p = 8 * nx * ny, nx * ny
-        n_q = nx * (ny + 1) + (nx + 1) * ny
+    def upload(cls, nx, ny, blocks, m_p_diag, q_constrained, biot_b, inv_m, k_dr, device: int = 0, nz: int = 0):
+        """Upload host CSR blocks {'A','M_q','B','E': (off, idx, val)} (nz > 0: a 3D mesh)."""
+        if nz > 0:
+            n_u, n_p = 24 * nx * ny * nz, nx * ny * nz
+            n_q = nx * ny * (nz + 1) + nx * (ny + 1) * nz + (nx + 1) * ny * nz
+        else:
+            n_u, n_p = 8 * nx * ny, nx * ny
+            n_q = nx * (ny + 1) + (nx + 1) * ny
         dims = dict(A=(n_u, n_u), M_q=(n_q, n_q), B=(n_q, n_p), E=(n_u, n_p))
         structs, keep = {}, []
         for k, (r, c) in dims.items():
@@ -210,6 +217,11 @@ class SpatialOperators:
         mp = np.ascontiguousarray(m_p_diag, np.float64)
         qc = np.ascontiguousarray(q_constrained, np.int8)
         h = C.c_void_p()
+        if nz > 0:
+            check(lib().pdg_ops_upload3(context(device), nx, ny, nz, C.byref(structs["A"]), C.byref(structs["M_q"]),
+                                        C.byref(structs["B"]), C.byref(structs["E"]), _dp(mp),
+                                        qc.ctypes.data_as(C.POINTER(C.c_byte)), biot_b, inv_m, k_dr, C.byref(h)))
+            return cls(h, nx, ny, nz)
         check(lib().pdg_ops_upload(context(device), nx, ny, C.byref(structs["A"]), C.byref(structs["M_q"]),
                                    C.byref(structs["B"]), C.byref(structs["E"]), _dp(mp),
                                    qc.ctypes.data_as(C.POINTER(C.c_byte)), biot_b, inv_m, k_dr, C.byref(h)))

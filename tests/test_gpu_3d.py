@@ -1,0 +1,172 @@
+"""GPU tests of the 3D extension (BASELINE configs 2 / 4).
+
+The reference is 2D only, so there is no reference arithmetic for
+these configurations: PARITY UNPINNED. The checker is the 3D CPU restatement
+oracle/refcpu/fem3d.hpp (pinned by its own properties, tests/test_oracle3d.py)
+driving the same oracle solver stack as the 2D configurations. Bars: bit-exact
+for the assembled operators, the right-hand side and the order-fixed SpMV;
+GMRES iterations within +-1 and per-slab relative L2 <= 1e-9 for the solves;
+at sizes the oracle cannot reach, the discrete mass balance and linearity."""
+import numpy as np
+import pytest
+
+from paper_1801_04984_b200 import problem as P
+from paper_1801_04984_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+SOLVE_RTOL = 1e-9
+
+
+def _variants():
+    out = []
+    a = P.config2(3)
+    a.nx, a.ny, a.nz = 3, 4, 2
+    a.lx, a.ly, a.lz = 1.3, 0.9, 0.7
+    a.k_perm_cells = P.lognormal_field(11, 24)
+    out.append(a)
+    b = P.config2(4)
+    out.append(b)
+    c = P.config2(3)
+    c.nx, c.ny, c.nz = 2, 3, 3
+    c.k_perm_cells = None
+    c.disp = {"xlo": ("fixed", (0.1, 0.0, -0.2)), "xhi": ("roller_x", (0.0, 0.3, 0.1)),
+              "ylo": ("roller_y", (0.2, 0.0, 0.4)), "yhi": ("traction", (0.1, -1.0, 0.5)),
+              "zlo": ("roller_z", (0.3, -0.1, 0.0)), "zhi": ("fixed", (0.0, 0.0, 0.05))}
+    c.flow = {"xlo": ("pressure", 0.5), "xhi": ("no_flow", 0.0), "ylo": ("no_flow", 0.0), "yhi": ("pressure", -0.25),
+              "zlo": ("pressure", 0.0), "zhi": ("no_flow", 0.0)}
+    out.append(c)
+    d = P.config2(1)
+    d.nx = d.ny = d.nz = 1
+    d.k_perm_cells = None
+    out.append(d)
+    e = P.config2(5)
+    e.nx, e.ny, e.nz = 5, 1, 2
+    e.k_perm_cells = None
+    e.disp = {t: ("fixed", (0.0, 0.0, 0.0)) for t in P.TAGS3}
+    e.flow = {t: ("pressure", 0.0) for t in P.TAGS3}
+    out.append(e)
+    return out
+
+
+@pytest.mark.parametrize("spec", _variants(), ids=lambda s: f"{s.nx}x{s.ny}x{s.nz}")
+def test_device_assembly3_bit_identical(oracle, spec):
+    """pdg_ops_assemble3 (one thread block per cell, one thread per face) == the 3D CPU
+    restatement's triplet assembly merged in push order, bit for bit, and the constant-data
+    right-hand side likewise."""
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    assert (ops.n_u, ops.n_q, ops.n_p) == (rp.n_u, rp.n_q, rp.n_p) == spec.sizes
+    for name in ("A", "M_q", "B", "E"):
+        ro, ri, rv = rp.csr(name)
+        go, gi, gv = ops.download(name)
+        assert np.array_equal(ro, go), name
+        assert np.array_equal(ri, gi), name
+        assert np.array_equal(rv, gv), name
+    u, q, p = rp.assemble_rhs(0.3)
+    gu, gq, gp = ops.rhs(0.3)
+    assert np.array_equal(u, gu) and np.array_equal(q, gq) and np.array_equal(p, gp)
+
+
+@pytest.mark.parametrize("r", [0, 1])
+def test_spacetime_operator3_bit_identical(oracle, r):
+    """Canonical space-time CSR of the 3D operators and its order-fixed SpMV == the oracle's
+    canonical CSR and SparseMatrix::apply (sparse.hpp:30-40) on it, bit for bit."""
+    spec = _variants()[0]
+    rp = oracle.RefProblem(spec.to_dict())
+    T = oracle.time_constants(r)["T"]
+    tau = 0.1
+    ops = S.SpatialOperators.assemble(spec)
+    op = S.SpaceTimeOperator(ops, T, tau)
+    ro, ri, rv = rp.spacetime_csr(T, tau)
+    go, gi, gv = op.csr()
+    assert np.array_equal(ro.astype(np.int64), go)
+    assert np.array_equal(ri, gi)
+    assert np.array_equal(rv, gv)
+    import torch
+    x = P.uniform_vector(P.X_SEED, op.rows)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    torch.cuda.synchronize()
+    op.apply_device(xd.data_ptr(), yd.data_ptr())
+    assert np.array_equal(yd.cpu().numpy(), oracle.csr_apply(ro, ri, rv, x))
+    # matrix-free form of the reference (fixed_stress.hpp:38-60) on the 3D blocks: roundoff only
+    y_mf = rp.apply_block(T, tau, x)
+    assert np.linalg.norm(yd.cpu().numpy() - y_mf) <= 1e-12 * np.linalg.norm(y_mf)
+
+
+def test_preconditioner3_matches_oracle(oracle):
+    """One truncated fixed-stress sweep (fixed_stress.hpp:109-139) with the exact nested-dissection
+    inner solves on the 3D operators against the oracle's dense-LU sweep; linear and repeatable."""
+    spec = P.config2(4)
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    tau, lam = 0.1, 1.0
+    blk = S.BlockSolver(ops, [[lam]], tau)
+    r = P.uniform_vector(5, rp.n_total)
+    z = blk.precondition(r)
+    zr = rp.precondition(lam, tau, r, sweeps=1, backend=0)
+    assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+    assert np.array_equal(z, blk.precondition(r))
+    r2 = P.uniform_vector(6, rp.n_total)
+    lin = blk.precondition(2.0 * r - 3.0 * r2) - (2.0 * z - 3.0 * blk.precondition(r2))
+    assert np.abs(lin).max() <= 1e-11 * np.abs(z).max()
+
+
+@pytest.mark.parametrize("candidate", ["reference", "flexible"])
+@pytest.mark.parametrize("n", [4, 6])
+def test_march_config2_type_parity(oracle, n, candidate):
+    """dG(0) march of config 2 at n^3 (layered permeability over 8 layers, fixed bottom, loaded
+    drained top): GMRES iterations within +-1 of the oracle and per-slab relative L2 <= 1e-9."""
+    spec = P.config2(n)
+    rp = oracle.RefProblem(spec.to_dict())
+    n_slabs = 3
+    ref = rp.march(0, 0.3, n_slabs, tol=1e-10, restart=50, backend=1, flexible=candidate == "flexible",
+                   keep_states=True)
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate)
+    reps, states = S.march(ops, 0, 0.3, n_slabs, opt, keep_states=True, mass_check=True)
+    for s in range(n_slabs):
+        assert reps[s].converged
+        assert abs(reps[s].iterations - int(ref["iterations"][s])) <= 1, (s, reps[s].iterations, ref["iterations"])
+        d = np.linalg.norm(states[s] - ref["states"][s].ravel()) / np.linalg.norm(ref["states"][s])
+        assert d <= SOLVE_RTOL, (s, d)
+        assert reps[s].mass_rel <= 1e-9
+
+
+def test_upload3_matches_device_assembly(oracle):
+    """Operators assembled by the CPU restatement and uploaded (pdg_ops_upload3) give the same
+    slab solve, bit for bit, as the device-assembled ones."""
+    spec = P.config2(4)
+    rp = oracle.RefProblem(spec.to_dict())
+    m = rp.misc()
+    blocks = {k: rp.csr(k) for k in ("A", "M_q", "B", "E")}
+    up = S.SpatialOperators.upload(spec.nx, spec.ny, blocks, m["m_p_diag"], m["q_constrained"], m["biot_b"],
+                                   m["inv_m"], m["k_dr"], nz=spec.nz)
+    dev = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
+    rhs = rp.slab_rhs(0, 0.0, 0.1, np.zeros(rp.n_u), np.zeros(rp.n_p))
+    xa, ra = S.SlabSolver(up, 0, 0.1, opt).solve(rhs)
+    xb, rb = S.SlabSolver(dev, 0, 0.1, opt).solve(rhs)
+    assert ra.iterations == rb.iterations and np.array_equal(xa, xb)
+    with pytest.raises(S.InvalidArgument):
+        S.SpatialOperators.upload(spec.nx, spec.ny, blocks, m["m_p_diag"], m["q_constrained"], m["biot_b"],
+                                  m["inv_m"], m["k_dr"], nz=spec.nz + 1)
+
+
+def test_march_config2_12cubed_properties():
+    """Beyond the oracle's reach (12^3: 41,472 displacement dofs): every slab converges, the
+    per-cell discrete mass balance closes (slab.hpp:292-318 on the device), the iteration count
+    stays that of the small meshes, and repeats are bit-identical."""
+    spec = P.config2(12)
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
+    reps, states = S.march(ops, 0, 0.2, 2, opt, keep_states=True, mass_check=True)
+    reps2, states2 = S.march(ops, 0, 0.2, 2, opt, keep_states=True)
+    for s in range(2):
+        assert reps[s].converged and reps[s].iterations <= 20
+        assert reps[s].final_relative_residual <= 1e-10
+        assert reps[s].mass_rel <= 1e-7  # GMRES tol 1e-10 times the conditioning (2D config 1 uses the same bar)
+        assert np.array_equal(states[s], states2[s])
+    nu = ops.n_u
+    uz = states[-1][:nu].reshape(-1, 8, 3)[:, :, 2]
+    assert uz.min() < 0.0 and uz.min() > -1.0  # the loaded top settles, by less than the domain height

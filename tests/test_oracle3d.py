@@ -1,0 +1,203 @@
+"""Self-validation of the 3D extension of the oracle (oracle/refcpu/fem3d.hpp).
+
+The reference is 2D only, so BASELINE configs 2 and 4 have no
+reference arithmetic: parity is UNPINNED for them. These tests pin the 3D CPU
+restatement by the properties a correct dQ1-SIPG / RT0 / dQ0 discretisation on
+hexahedra must have; the device 3D assembly is then checked bit for bit against
+it (tests/test_gpu_3d.py)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import refcpu
+
+TAGS3 = refcpu.TAGS3
+
+
+def spec3(nx, ny, nz, lx=1.0, ly=1.0, lz=1.0, disp=None, flow=None, lam=2.0, mu=1.5, k_cells=None, **kw):
+    disp = disp or {t: ("traction", (0.0, 0.0, 0.0)) for t in TAGS3}
+    flow = flow or {t: ("pressure", 0.0) for t in TAGS3}
+    d = dict(nx=nx, ny=ny, nz=nz, lx=lx, ly=ly, lz=lz, lam=lam, mu=mu, k_perm=1.0, eta=1.0, biot_m=10.0, biot_b=0.8,
+             penalty=10.0, k_perm_cells=k_cells, disp=disp, flow=flow)
+    d.update(kw)
+    return d
+
+
+def csr(rp, name, shape):
+    off, idx, val = rp.csr(name)
+    return sp.csr_matrix((val, idx, off), shape=shape)
+
+
+def nodal_field(spec, fn):
+    """dQ1 nodal interpolant of fn(x, y, z) -> (3,), dof = 24 c + 3 a + comp, a = 4 az + 2 ay + ax."""
+    nx, ny, nz = spec["nx"], spec["ny"], spec["nz"]
+    hx, hy, hz = spec["lx"] / nx, spec["ly"] / ny, spec["lz"] / nz
+    u = np.zeros(24 * nx * ny * nz)
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                c = (k * ny + j) * nx + i
+                for a in range(8):
+                    ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+                    u[24 * c + 3 * a:24 * c + 3 * a + 3] = fn((i + ax) * hx, (j + ay) * hy, (k + az) * hz)
+    return u
+
+
+def test_sizes_and_symmetry():
+    s = spec3(3, 2, 4, lx=1.5, ly=1.0, lz=2.0)
+    rp = refcpu.RefProblem(s)
+    n = 3 * 2 * 4
+    assert (rp.n_u, rp.n_p) == (24 * n, n)
+    assert rp.n_q == 3 * 2 * 5 + 3 * 3 * 4 + 4 * 2 * 4
+    A = csr(rp, "A", (rp.n_u, rp.n_u))
+    assert abs(A - A.T).max() <= 1e-12 * abs(A).max()
+    # every row of a cell couples to the cell and its face neighbours, 24 columns each
+    off = rp.csr("A")[0]
+    lens = np.diff(off).reshape(n, 24)
+    assert (lens == lens[:, :1]).all() and set(np.unique(lens // 24)) <= {4, 5, 6, 7}
+    Mq = csr(rp, "M_q", (rp.n_q, rp.n_q))
+    assert abs(Mq - Mq.T).max() <= 1e-14
+    mp = rp.misc()["m_p_diag"]
+    assert np.allclose(mp, (1.5 / 3) * (1.0 / 2) * (2.0 / 4), rtol=1e-15)
+    assert rp.misc()["k_dr"] == pytest.approx(2.0 + 2.0 * 1.5 / 3.0, rel=1e-15)
+
+
+def test_rigid_body_modes_in_the_null_space():
+    s = spec3(3, 3, 2, lx=1.0, ly=1.2, lz=0.7)
+    rp = refcpu.RefProblem(s)
+    A = csr(rp, "A", (rp.n_u, rp.n_u))
+    scale = abs(A).max()
+    modes = [lambda x, y, z: (1.0, 0.0, 0.0), lambda x, y, z: (0.0, 1.0, 0.0), lambda x, y, z: (0.0, 0.0, 1.0),
+             lambda x, y, z: (-y, x, 0.0), lambda x, y, z: (0.0, -z, y), lambda x, y, z: (z, 0.0, -x)]
+    for m in modes:
+        u = nodal_field(s, m)
+        assert abs(A @ u).max() <= 1e-11 * scale * abs(u).max()
+    # and nothing else: with one fixed face the matrix is positive definite
+    disp = {t: ("traction", (0.0, 0.0, 0.0)) for t in TAGS3}
+    disp["zlo"] = ("fixed", (0.0, 0.0, 0.0))
+    rp2 = refcpu.RefProblem(spec3(3, 3, 2, lx=1.0, ly=1.2, lz=0.7, disp=disp))
+    A2 = csr(rp2, "A", (rp2.n_u, rp2.n_u)).toarray()
+    w = np.linalg.eigvalsh(0.5 * (A2 + A2.T))
+    assert w[0] > 1e-6 * w[-1]
+    wn = np.linalg.eigvalsh(0.5 * (A.toarray() + A.toarray().T))
+    assert (abs(wn[:6]) <= 1e-10 * wn[-1]).all() and wn[6] > 1e-6 * wn[-1]
+
+
+def test_patch_test_constant_strain():
+    """a(u_lin, v) = int_{boundary} (sigma n) . v for a globally linear u (no jumps, div sigma = 0): the cell
+    term, the face consistency term and the traction load of assemble_rhs3 agree."""
+    lam, mu = 2.0, 1.5
+    G = np.array([[0.3, -0.2, 0.5], [0.1, 0.4, -0.6], [-0.7, 0.25, 0.15]])
+    eps = 0.5 * (G + G.T)
+    sig = 2 * mu * eps + lam * np.trace(eps) * np.eye(3)
+    normals = {"xlo": (-1, 0, 0), "xhi": (1, 0, 0), "ylo": (0, -1, 0), "yhi": (0, 1, 0), "zlo": (0, 0, -1),
+               "zhi": (0, 0, 1)}
+    disp = {t: ("traction", tuple(sig @ np.array(nv, float))) for t, nv in normals.items()}
+    s = spec3(3, 2, 3, lx=0.9, ly=1.1, lz=1.3, disp=disp, lam=lam, mu=mu)
+    rp = refcpu.RefProblem(s)
+    A = csr(rp, "A", (rp.n_u, rp.n_u))
+    u = nodal_field(s, lambda x, y, z: tuple(G @ np.array([x, y, z]) + np.array([0.2, -0.1, 0.05])))
+    ru, rq, rpp = rp.assemble_rhs(0.0)
+    assert abs(A @ u - ru).max() <= 1e-11 * abs(ru).max()
+    # divergence identity: (E^T u)_c = int_c div u for a continuous field
+    E = csr(rp, "E", (rp.n_u, rp.n_p))
+    vol = (0.9 / 3) * (1.1 / 2) * (1.3 / 3)
+    assert np.allclose(E.T @ u, np.trace(G) * vol, rtol=1e-11)
+    assert abs(rq).max() == 0.0 and abs(rpp).max() == 0.0
+
+
+def test_uniaxial_compression_is_reproduced_exactly():
+    """Fixed bottom, rollers on the sides, unit load on top: u = (0, 0, -z / (lambda + 2 mu)) is linear, and
+    the Nitsche form is consistent, so the discrete solution equals it."""
+    lam, mu = 2.0, 1.5
+    disp = {"xlo": ("roller_x", (0, 0, 0)), "xhi": ("roller_x", (0, 0, 0)), "ylo": ("roller_y", (0, 0, 0)),
+            "yhi": ("roller_y", (0, 0, 0)), "zlo": ("fixed", (0, 0, 0)), "zhi": ("traction", (0.0, 0.0, -1.0))}
+    s = spec3(2, 3, 3, lx=1.0, ly=0.8, lz=1.5, disp=disp, lam=lam, mu=mu)
+    rp = refcpu.RefProblem(s)
+    A = csr(rp, "A", (rp.n_u, rp.n_u)).toarray()
+    ru = rp.assemble_rhs(0.0)[0]
+    u = np.linalg.solve(A, ru)
+    ex = nodal_field(s, lambda x, y, z: (0.0, 0.0, -z / (lam + 2 * mu)))
+    assert abs(u - ex).max() <= 1e-10 * abs(ex).max()
+    # Dirichlet data: lift the bottom by a constant; the solution shifts rigidly
+    disp["zlo"] = ("fixed", (0.0, 0.0, 0.25))
+    rp2 = refcpu.RefProblem(spec3(2, 3, 3, lx=1.0, ly=0.8, lz=1.5, disp=disp, lam=lam, mu=mu))
+    u2 = np.linalg.solve(csr(rp2, "A", (rp2.n_u, rp2.n_u)).toarray(), rp2.assemble_rhs(0.0)[0])
+    assert abs(u2 - (ex + nodal_field(s, lambda x, y, z: (0.0, 0.0, 0.25)))).max() <= 1e-10
+
+
+def test_flux_blocks():
+    nx, ny, nz = 3, 2, 2
+    lx, ly, lz = 1.2, 1.0, 0.8
+    s = spec3(nx, ny, nz, lx=lx, ly=ly, lz=lz)
+    rp = refcpu.RefProblem(s)
+    Mq = csr(rp, "M_q", (rp.n_q, rp.n_q))
+    B = csr(rp, "B", (rp.n_q, rp.n_p))
+    hx, hy, hz = lx / nx, ly / ny, lz / nz
+    nzf, nyf = nx * ny * (nz + 1), nx * (ny + 1) * nz
+
+    def flux_of(v):  # q_f = v(face centre) . n_f, n_f the stored normal (outward on the boundary)
+        q = np.zeros(rp.n_q)
+        for k in range(nz + 1):
+            for j in range(ny):
+                for i in range(nx):
+                    n = -1.0 if k == 0 else 1.0
+                    q[(k * ny + j) * nx + i] = n * v((i + .5) * hx, (j + .5) * hy, k * hz)[2]
+        for j in range(ny + 1):
+            for k in range(nz):
+                for i in range(nx):
+                    n = -1.0 if j == 0 else 1.0
+                    q[nzf + (j * nz + k) * nx + i] = n * v((i + .5) * hx, j * hy, (k + .5) * hz)[1]
+        for i in range(nx + 1):
+            for k in range(nz):
+                for j in range(ny):
+                    n = -1.0 if i == 0 else 1.0
+                    q[nzf + nyf + (i * nz + k) * ny + j] = n * v(i * hx, (j + .5) * hy, (k + .5) * hz)[0]
+        return q
+
+    vol = hx * hy * hz
+    qc = flux_of(lambda x, y, z: (0.7, -0.3, 0.2))
+    assert abs(B.T @ qc).max() <= 1e-14                      # div of a constant field
+    assert qc @ (Mq @ qc) == pytest.approx((0.49 + 0.09 + 0.04) * lx * ly * lz, rel=1e-13)
+    ql = flux_of(lambda x, y, z: (x, 2 * y, -0.5 * z))
+    assert np.allclose(B.T @ ql, -(1 + 2 - 0.5) * vol, rtol=1e-13)  # B^T q = -int div v
+    # per-cell permeability scales the cell's mass contribution by eta / K_c
+    k_cells = np.linspace(0.5, 2.0, nx * ny * nz)
+    rp2 = refcpu.RefProblem(spec3(nx, ny, nz, lx=lx, ly=ly, lz=lz, k_cells=k_cells))
+    Mq2 = csr(rp2, "M_q", (rp2.n_q, rp2.n_q))
+    f = nzf + nyf + (1 * nz + 0) * ny + 0   # interior x face between cells (0,0,0) and (1,0,0)
+    assert Mq2[f, f] == pytest.approx(vol / 3 * (1 / k_cells[0] + 1 / k_cells[1]), rel=1e-14)
+    # no-flow faces are eliminated: identity rows, no B entries
+    flow = {t: ("no_flow", 0.0) for t in TAGS3}
+    flow["zhi"] = ("pressure", 0.0)
+    rp3 = refcpu.RefProblem(spec3(nx, ny, nz, flow=flow))
+    qcn = rp3.misc()["q_constrained"].astype(bool)
+    assert qcn.sum() == 2 * (ny * nz + nx * nz) + nx * ny
+    Mq3 = csr(rp3, "M_q", (rp3.n_q, rp3.n_q)).toarray()
+    B3 = csr(rp3, "B", (rp3.n_q, rp3.n_p)).toarray()
+    assert (Mq3[qcn] == np.eye(rp3.n_q)[qcn]).all() and (Mq3[:, qcn] == np.eye(rp3.n_q)[:, qcn]).all()
+    assert abs(B3[qcn]).max() == 0.0
+
+
+def test_config2_type_march_converges_and_conserves_mass():
+    """dG(0) march of a small config-2-type problem through the oracle's solver stack (dense and banded
+    inner solves agree); the per-cell discrete mass balance closes."""
+    from paper_1801_04984_b200 import problem as P
+    spec = P.config2(4).to_dict()
+    rp = refcpu.RefProblem(spec)
+    a = rp.march(0, 0.3, 3, tol=1e-10, restart=50, backend=0, keep_states=True)
+    b = rp.march(0, 0.3, 3, tol=1e-10, restart=50, backend=1, keep_states=True)
+    assert (a["iterations"] == b["iterations"]).all() and (a["iterations"] <= 12).all()
+    for s in range(3):
+        d = np.linalg.norm(a["states"][s] - b["states"][s]) / np.linalg.norm(a["states"][s])
+        assert d <= 1e-9
+    u_prev, p_prev = np.zeros(rp.n_u), np.zeros(rp.n_p)
+    for s in range(3):
+        rhs = rp.slab_rhs(0, 0.1 * s, 0.1, u_prev, p_prev)
+        res, scale = rp.mass_residual(0, 0.1, rhs, a["states"][s].ravel())
+        assert res.max() <= 1e-9 * scale
+        st = a["states"][s][-1]
+        u_prev, p_prev = st[:rp.n_u], st[rp.n_u + rp.n_q:]
+    # the column settles: top displacement is downwards, pressure positive below the drained top
+    uz_top = a["states"][-1][-1][:rp.n_u].reshape(-1, 8, 3)[-16:, 4:, 2]
+    assert (uz_top < 0).all()
