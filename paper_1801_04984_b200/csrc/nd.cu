@@ -953,7 +953,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     store.alloc((size_t)so);
     // ---- numeric factorization (multifrontal, stream-serial, children first) ----
     std::vector<long long> fo(nf);
-    long long ftot = 0;
+    long long ftot = 0, sbmax = 1;
     int smax = 1, bmax = 1;
     for (int k = 0; k < nf; ++k) {
         const long long f = fronts[k].s + fronts[k].b;
@@ -961,10 +961,23 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         ftot += f * f;
         smax = std::max(smax, fronts[k].s);
         bmax = std::max(bmax, fronts[k].b);
+        sbmax = std::max(sbmax, (long long)fronts[k].s * fronts[k].b);
     }
-    DBuf<double> dense(ftot);
+    // streaming mode (nd_stream.cu): wide fronts (the level kernels hold a front's input vector,
+    // s + b doubles per right-hand side plus index lists, in shared memory) or more than 8 GB of
+    // dense fronts (3D meshes)
+    stream = vmax > 10000 || 8.0 * (double)ftot > 8e9;
+    if (const char* e = std::getenv("PDG_ND_STREAM")) stream = std::atoi(e) != 0;
+    if (stream) {
+        top_depth = -1;
+        for (auto& o : fo) o = 0;  // front-relative positions: every front has its own allocation
+    }
+    DBuf<double> dense(stream ? 1 : ftot);
     dense.zero(st);
+    std::vector<long long> tstart(nf + 1, 0);  // streaming: the scatter entries of front k
     std::vector<int> loc(n, -1);
+    DBuf<long long> dpos;
+    DBuf<double> dval;
     {
         std::vector<long long> tpos;
         std::vector<double> tval;
@@ -985,14 +998,15 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             }
             for (int i = 0; i < F.s; ++i) loc[hs[F.sdof + i]] = -1;
             for (int i = 0; i < F.b; ++i) loc[hb[F.bdof + i]] = -1;
+            tstart[k + 1] = static_cast<long long>(tpos.size());
         }
-        DBuf<long long> dpos;
-        DBuf<double> dval;
         dpos.upload(tpos, st);
         dval.upload(tval, st);
-        k_nd_scatter<<<grid_for((long long)tpos.size(), 256), 256, 0, st>>>((long long)tpos.size(), dpos.p, dval.p,
-                                                                           dense.p);
-        PDG_CHECK_LAUNCH();
+        if (!stream) {
+            k_nd_scatter<<<grid_for((long long)tpos.size(), 256), 256, 0, st>>>((long long)tpos.size(), dpos.p, dval.p,
+                                                                               dense.p);
+            PDG_CHECK_LAUNCH();
+        }
         PDG_CUDA(cudaStreamSynchronize(st));
     }
     // extend-add maps
@@ -1019,21 +1033,65 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     LaHandles h(st);
     int lwork = 0;
     PDG_ND_CUSOLVER(cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, smax, dense.p, smax, &lwork));
-    DBuf<double> work(std::max(lwork, 1)), T((size_t)smax * smax), G((size_t)smax * bmax);
+    DBuf<double> work(std::max(lwork, 1)), T((size_t)smax * smax), G(stream ? (size_t)sbmax : (size_t)smax * bmax);
     DBuf<int> info(nf);
     info.zero(st);
     const double one = 1.0, mone = -1.0, zero = 0.0;
-    for (int k = 0; k < nf; ++k) {
+    // processing order: by index (deepest level first), or in streaming mode the postorder of the
+    // tree, so that only the update matrices on the current root path are alive
+    std::vector<int> porder;
+    std::vector<double*> fptr(nf, nullptr);
+    if (stream) {
+        std::vector<std::pair<int, size_t>> stk;
+        for (int k = 0; k < nf; ++k)
+            if (parent[k] < 0) stk.push_back({k, 0});
+        while (!stk.empty()) {
+            auto& [k, ci] = stk.back();
+            if (ci < children[k].size()) {
+                const int c = children[k][ci++];
+                stk.push_back({c, 0});
+            } else {
+                porder.push_back(k);
+                stk.pop_back();
+            }
+        }
+        cudaMemPool_t pool;
+        int dev = 0;
+        PDG_CUDA(cudaGetDevice(&dev));
+        PDG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        unsigned long long keep = ~0ULL;  // reuse freed front matrices instead of returning them to the driver
+        PDG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    } else {
+        porder.resize(nf);
+        std::iota(porder.begin(), porder.end(), 0);
+    }
+    for (int k : porder) {
         const NdFront& F = fronts[k];
         const int s = F.s, b = F.b, f = s + b;
         double* Fk = dense.p + fo[k];
+        if (stream) {
+            PDG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&Fk), sizeof(double) * (size_t)f * f, st));
+            fptr[k] = Fk;
+            PDG_CUDA(cudaMemsetAsync(Fk, 0, sizeof(double) * (size_t)f * f, st));
+            const long long cnt = tstart[k + 1] - tstart[k];
+            if (cnt > 0) {
+                k_nd_scatter<<<grid_for(cnt, 256), 256, 0, st>>>(cnt, dpos.p + tstart[k], dval.p + tstart[k], Fk);
+                PDG_CHECK_LAUNCH();
+            }
+        }
         for (int c : children[k]) {
             const NdFront& C = fronts[c];
             const int fc = C.s + C.b;
-            if (C.b == 0) continue;
-            k_nd_extend_add<<<grid_for((long long)C.b * C.b, 256), 256, 0, st>>>(
-                Fk, f, dense.p + fo[c] + C.s + (long long)C.s * fc, fc, C.b, dmap.p + mapoff[c]);
-            PDG_CHECK_LAUNCH();
+            const double* Fc = stream ? fptr[c] : dense.p + fo[c];
+            if (C.b > 0) {
+                k_nd_extend_add<<<grid_for((long long)C.b * C.b, 256), 256, 0, st>>>(
+                    Fk, f, Fc + C.s + (long long)C.s * fc, fc, C.b, dmap.p + mapoff[c]);
+                PDG_CHECK_LAUNCH();
+            }
+            if (stream) {
+                PDG_CUDA(cudaFreeAsync(fptr[c], st));
+                fptr[c] = nullptr;
+            }
         }
         PDG_ND_CUSOLVER(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, s, Fk, f, work.p, lwork, info.p + k));
         if (b > 0) {
@@ -1051,6 +1109,16 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         k_nd_pack<<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store.p + F.moff, F.ldm,
                                                                       store.p + F.mtoff, F.ldt);
         PDG_CHECK_LAUNCH();
+    }
+    if (stream) {  // the roots' front matrices, then the pool's cached blocks back to the driver
+        for (int k = 0; k < nf; ++k)
+            if (fptr[k]) PDG_CUDA(cudaFreeAsync(fptr[k], st));
+        PDG_CUDA(cudaStreamSynchronize(st));
+        cudaMemPool_t pool;
+        int dev = 0;
+        PDG_CUDA(cudaGetDevice(&dev));
+        PDG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        PDG_CUDA(cudaMemPoolTrimTo(pool, 0));
     }
     std::vector<int> hinfo(nf);
     PDG_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
@@ -1071,6 +1139,11 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     xpos.alloc((size_t)n * max_rhs);
     cbuf.alloc((size_t)std::max<long long>(cbtot, 1) * max_rhs);
     cbuf.zero(st);  // slots no child writes stay zero
+    if (stream) {
+        tiles = levels = hybrid = split = false;
+        build_stream(st);
+        return;
+    }
     tiles = nd_tile_default();
     levels = nd_levels_default();
     if (tiles && !levels) top_depth = -1;  // the opt-in dataflow tile kernel solves every front
@@ -1381,6 +1454,10 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
     ProfScope prof(prof_phase, st, alg_bytes(nrhs));
     require(nrhs >= 1 && nrhs <= max_rhs, "nested dissection solve: bad nrhs");
     ++call;
+    if (stream) {
+        solve_stream(b, ldb, x, ldx, nrhs, st);
+        return;
+    }
     const int nl = static_cast<int>(lvl_smem.size());
     if (levels) {  // forward levels, the dense top, backward levels
         solve_levels_range(b, ldb, x, ldx, nrhs, 0, top_depth >= 0 ? nl / 2 : nl, st);

@@ -75,6 +75,13 @@ struct NdTileTask {
     int cgather;  // the compute warps gather the dependent inputs (shared levels)
     int l2keep;   // tiles loaded with L2 evict_last (top levels)
 };
+// One unit of the streaming solve (nd_stream.cu): rows [r0, r0 + nrows) of a front's M
+// (type 1, forward) or M^T (type 2, backward) at store + src, row stride ld.
+struct NdStreamUnit {
+    long long src;
+    int type, r0, nrows, ncols, ld;
+    int s, b, sdof, bdof, cboff;
+};
 bool nd_tile_default();
 bool nd_levels_default();
 bool nd_hybrid_default(int prof_phase);
@@ -150,6 +157,15 @@ struct NdChol {
     void solve_top(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     void solve_levels_range(const double* b, long long ldb, double* x, long long ldx, int nrhs, int l0, int l1,
                             cudaStream_t st);
+    // streaming mode (nd_stream.cu): fronts too wide for the shared-memory kernels, or dense
+    // fronts too large to hold all at once (3D). Numeric factorization in postorder with one
+    // front matrix alive per pending update; one level kernel per depth and pass on the
+    // row-major store. PDG_ND_STREAM=1/0 forces / forbids it.
+    bool stream = false;
+    std::vector<int> stream_off;
+    DBuf<NdStreamUnit> d_sunits;
+    void build_stream(cudaStream_t st);
+    void solve_stream(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     double alg_bytes(int nrhs) const { return factor_bytes + 16.0 * n * nrhs; }
 };
 

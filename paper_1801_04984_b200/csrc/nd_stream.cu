@@ -1,0 +1,200 @@
+// Streaming mode of the nested-dissection solve (NdChol::stream): for factors whose
+// fronts are too wide for the shared-memory dataflow kernels (nd.cu, nd_tile.cu) -- the
+// 3D meshes of BASELINE config 2, where the top separator of 32^3 cells has 24,576 dofs
+// and the factor is ~80 GB. Same math as the other solve paths (the exact inner solves of
+// fixed_stress.hpp:109-139):
+//   forward   [y_S; u_F] = M (b_S - w_C1|S - w_C2|S),  w_F = u_F + w_C1|B + w_C2|B
+//   backward  x_S = M^T [y_S; -x_B]
+// One launch per tree level and pass (stream order carries the dependencies; at these
+// sizes a level streams 1-15 GB, so launch gaps are noise). A CTA takes a unit = 64 rows
+// of one front's M (or M^T), read straight from the row-major factor store with 16-byte
+// streaming loads, 8 rows per warp in flight at once; the front's input vector is formed
+// on the fly (right-hand side minus the children's update vectors, or [y_S; -x_B]) and
+// staged through shared memory in tiles of 2048 columns shared by the CTA's 64 rows, so
+// its L2 traffic is 1/64 of the factor traffic. Sums run in a fixed order: repeats are
+// bit-identical. HBM-bound: algorithmic bytes = the factor once per pass.
+#include <algorithm>
+
+#include "nd.cuh"
+
+namespace pdg {
+
+namespace {
+
+constexpr int kSRows = 64;     // rows per unit (8 warps x 8 rows)
+constexpr int kSTile = 2048;   // columns per shared-memory tile
+constexpr int kSThreads = 256;
+
+struct StreamArgs {
+    const NdStreamUnit* units;
+    const int* sdofs;
+    const int* bpos;
+    const int* cbdst;
+    const double* store;
+    const double* b;
+    long long ldb;
+    double* x;
+    long long ldx;
+    double* y;
+    double* xpos;
+    double* cb;
+    long long cbtot;
+    int n;
+    const int* stop;
+};
+
+template <int NR>
+__global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
+    if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
+    __shared__ double vs[NR][kSTile];
+    __shared__ NdStreamUnit Us;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid < (int)(sizeof(NdStreamUnit) / 4))
+        reinterpret_cast<int*>(&Us)[tid] = __ldg(reinterpret_cast<const int*>(a.units + u0 + blockIdx.x) + tid);
+    __syncthreads();
+    const NdStreamUnit& U = Us;
+    const int fwd = U.type == 1;
+    const int sb = U.s + U.b;
+    double acc[8][NR];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) acc[j][k] = 0.0;
+    const int rw = warp * 8;  // this warp's first row within the unit
+    const double* rowp = a.store + U.src + (long long)(U.r0 + rw) * U.ld;
+    for (int c0 = 0; c0 < U.ncols; c0 += kSTile) {
+        const int nc = min(kSTile, U.ncols - c0);
+        // ---- the input vector tile ----
+        for (int c = tid; c < ((nc + 1) & ~1); c += kSThreads) {
+            const int gc = c0 + c;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                double v = 0.0;
+                if (c < nc) {
+                    if (fwd) {
+                        const double* cbk = a.cb + k * a.cbtot + U.cboff;
+                        v = (a.b[k * a.ldb + __ldg(a.sdofs + U.sdof + gc)] - __ldcg(cbk + gc)) - __ldcg(cbk + sb + gc);
+                    } else {
+                        v = gc < U.s ? __ldcg(a.y + (long long)k * a.n + U.sdof + gc)
+                                     : -__ldcg(a.xpos + (long long)k * a.n + __ldg(a.bpos + U.bdof + gc - U.s));
+                    }
+                }
+                vs[k][c] = v;
+            }
+        }
+        __syncthreads();
+        // ---- 8 rows per warp against the tile ----
+        const int np = (nc + 1) >> 1;
+        const int nrw = min(8, U.nrows - rw);  // rows of this warp (<= 0: none)
+        if (nrw == 8) {
+            for (int p = lane; p < np; p += 32) {
+                double2 m[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) m[j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * p]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j][k] = fma(m[j].y, v.y, fma(m[j].x, v.x, acc[j][k]));
+                }
+            }
+        } else if (nrw > 0) {
+            for (int p = lane; p < np; p += 32) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j < nrw) {
+                        const double2 mv = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
+#pragma unroll
+                        for (int k = 0; k < NR; ++k) {
+                            const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * p]);
+                            acc[j][k] = fma(mv.y, v.y, fma(mv.x, v.x, acc[j][k]));
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // ---- row sums (fixed butterfly) and outputs ----
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            double s = acc[j][k];
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            acc[j][k] = s;
+        }
+    if (lane < 8 && rw + lane < U.nrows) {
+        const int gr = U.r0 + rw + lane;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j == lane) s = acc[j][k];
+            if (!fwd) {
+                a.xpos[(long long)k * a.n + U.sdof + gr] = s;
+                a.x[k * a.ldx + __ldg(a.sdofs + U.sdof + gr)] = s;
+            } else if (gr < U.s) {
+                a.y[(long long)k * a.n + U.sdof + gr] = s;
+            } else {  // update vector entry plus the children's pass-through, into the parent's slot
+                const double* cbk = a.cb + k * a.cbtot + U.cboff;
+                const double tail = __ldcg(cbk + gr) + __ldcg(cbk + sb + gr);
+                a.cb[k * a.cbtot + __ldg(a.cbdst + U.bdof + gr - U.s)] = s + tail;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// Units per (pass, depth): forward levels deepest first, then backward levels root first.
+void NdChol::build_stream(cudaStream_t st) {
+    std::vector<NdStreamUnit> units;
+    stream_off.clear();
+    auto add_level = [&](int type, int depth) {
+        stream_off.push_back(static_cast<int>(units.size()));
+        for (int k = 0; k < nfront; ++k) {
+            const NdFront& F = fronts[k];
+            if (F.depth != depth) continue;
+            const int rows = type == 1 ? F.s + F.b : F.s;
+            for (int r0 = 0; r0 < rows; r0 += kSRows) {
+                NdStreamUnit u{};
+                u.src = type == 1 ? F.moff : F.mtoff;
+                u.type = type;
+                u.r0 = r0;
+                u.nrows = std::min(kSRows, rows - r0);
+                u.ncols = type == 1 ? F.s : F.s + F.b;
+                u.ld = type == 1 ? F.ldm : F.ldt;
+                u.s = F.s;
+                u.b = F.b;
+                u.sdof = F.sdof;
+                u.bdof = F.bdof;
+                u.cboff = F.cboff;
+                units.push_back(u);
+            }
+        }
+    };
+    for (int d = maxdepth; d >= 0; --d) add_level(1, d);
+    for (int d = 0; d <= maxdepth; ++d) add_level(2, d);
+    stream_off.push_back(static_cast<int>(units.size()));
+    d_sunits.upload(units, st);
+    PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void NdChol::solve_stream(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
+    StreamArgs a{d_sunits.p, sdofs.p, bpos.p, cbdst.p, store.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, cbtot, n, guard};
+    const int nl = static_cast<int>(stream_off.size()) - 1;
+    for (int l = 0; l < nl; ++l) {
+        const int u0 = stream_off[l], nu = stream_off[l + 1] - u0;
+        if (nu == 0) continue;
+        if (nrhs == 1)
+            k_nd_stream<1><<<nu, kSThreads, 0, st>>>(a, u0);
+        else
+            k_nd_stream<2><<<nu, kSThreads, 0, st>>>(a, u0);
+        count_launch(1);
+    }
+    PDG_CHECK_LAUNCH();
+}
+
+}  // namespace pdg

@@ -133,6 +133,37 @@ def test_march_config2_type_parity(oracle, n, candidate):
         assert reps[s].mass_rel <= 1e-9
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_nd_streaming_mode_matches_default(oracle, monkeypatch, dim):
+    """The streaming mode of the nested-dissection solves (nd_stream.cu: postorder numeric
+    factorization with one front matrix per pending update, one level kernel per depth and pass on
+    the row-major factor; selected automatically for wide 3D fronts, forced here by
+    PDG_ND_STREAM=1) is the same exact solve as the default kernels: preconditioner within
+    roundoff, same GMRES iterations, solution within 1e-9 of the oracle."""
+    spec = P.config1(32) if dim == 2 else P.config2(6)
+    r = 1 if dim == 2 else 0
+    rp = oracle.RefProblem(spec.to_dict())
+    T = oracle.time_constants(r)["T"]
+    tau = 0.05
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
+    blk = S.BlockSolver(ops, T, tau, opt=opt)
+    monkeypatch.setenv("PDG_ND_STREAM", "1")
+    blk_s = S.BlockSolver(ops, T, tau, opt=opt)
+    monkeypatch.delenv("PDG_ND_STREAM")
+    rvec = P.uniform_vector(9, blk.rows)
+    z, zs = blk.precondition(rvec), blk_s.precondition(rvec)
+    assert np.linalg.norm(z - zs) <= 1e-11 * np.linalg.norm(z)
+    assert np.array_equal(zs, blk_s.precondition(rvec))
+    rhs = P.uniform_vector(10, blk.rows)
+    x, rep = blk.solve(rhs)
+    xs, reps = blk_s.solve(rhs)
+    assert rep.iterations == reps.iterations
+    assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(x)
+    xr, _ = rp.block_solve(r, tau, rhs, tol=1e-10, restart=50, backend=1, flexible=True)
+    assert np.linalg.norm(xs - xr) <= SOLVE_RTOL * np.linalg.norm(xr)
+
+
 def test_upload3_matches_device_assembly(oracle):
     """Operators assembled by the CPU restatement and uploaded (pdg_ops_upload3) give the same
     slab solve, bit for bit, as the device-assembled ones."""
