@@ -81,6 +81,7 @@ struct NdStreamUnit {
     long long src;
     int type, r0, nrows, ncols, ld;
     int s, b, sdof, bdof, cboff;
+    int cbeg;  // first column read (even); columns [cbeg, ncols)
 };
 bool nd_tile_default();
 bool nd_levels_default();
@@ -162,7 +163,7 @@ struct NdChol {
     // front matrix alive per pending update; one level kernel per depth and pass on the
     // row-major store. PDG_ND_STREAM=1/0 forces / forbids it.
     bool stream = false;
-    std::vector<int> stream_off;
+    std::vector<int> stream_off, stream_rpw;  // per level: first unit, rows per warp (8 | 4 | 2)
     DBuf<NdStreamUnit> d_sunits;
     void build_stream(cudaStream_t st);
     void solve_stream(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);

@@ -11,9 +11,11 @@
 // streaming loads, 8 rows per warp in flight at once; the front's input vector is formed
 // on the fly (right-hand side minus the children's update vectors, or [y_S; -x_B]) and
 // staged through shared memory in tiles of 2048 columns shared by the CTA's 64 rows, so
-// its L2 traffic is 1/64 of the factor traffic. Sums run in a fixed order: repeats are
-// bit-identical. HBM-bound: algorithmic bytes = the factor once per pass.
+// its L2 traffic is 1/64 of the factor traffic. The zero triangle of L_SS^{-1} is skipped
+// (per unit a column range). Sums run in a fixed order: repeats are bit-identical.
+// HBM-bound: algorithmic bytes = the nonzero part of the factor once per pass.
 #include <algorithm>
+#include <cstdlib>
 
 #include "nd.cuh"
 
@@ -43,7 +45,9 @@ struct StreamArgs {
     const int* stop;
 };
 
-template <int NR>
+// RPW rows per warp: a unit has up to 8 * RPW rows (64 by default; 32 or 16 on levels with few
+// units, where more CTAs keep more bytes in flight)
+template <int NR, int RPW>
 __global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
     if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
     __shared__ double vs[NR][kSTile];
@@ -55,14 +59,14 @@ __global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
     const NdStreamUnit& U = Us;
     const int fwd = U.type == 1;
     const int sb = U.s + U.b;
-    double acc[8][NR];
+    double acc[RPW][NR];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < RPW; ++j)
 #pragma unroll
         for (int k = 0; k < NR; ++k) acc[j][k] = 0.0;
-    const int rw = warp * 8;  // this warp's first row within the unit
+    const int rw = warp * RPW;  // this warp's first row within the unit
     const double* rowp = a.store + U.src + (long long)(U.r0 + rw) * U.ld;
-    for (int c0 = 0; c0 < U.ncols; c0 += kSTile) {
+    for (int c0 = U.cbeg; c0 < U.ncols; c0 += kSTile) {
         const int nc = min(kSTile, U.ncols - c0);
         // ---- the input vector tile ----
         for (int c = tid; c < ((nc + 1) & ~1); c += kSThreads) {
@@ -83,25 +87,44 @@ __global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
             }
         }
         __syncthreads();
-        // ---- 8 rows per warp against the tile ----
+        // ---- RPW rows per warp against the tile ----
         const int np = (nc + 1) >> 1;
-        const int nrw = min(8, U.nrows - rw);  // rows of this warp (<= 0: none)
-        if (nrw == 8) {
-            for (int p = lane; p < np; p += 32) {
-                double2 m[8];
+        const int nrw = min(RPW, U.nrows - rw);  // rows of this warp (<= 0: none)
+        if (nrw == RPW) {
+            constexpr int UN = 8 / RPW;  // 8 16-byte loads in flight per lane
+            int p = lane;
+            if constexpr (UN > 1)
+            for (; p + 32 * (UN - 1) < np; p += 32 * UN) {
+                double2 m[UN][RPW];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) m[j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
+                for (int q = 0; q < UN; ++q)
+#pragma unroll
+                    for (int j = 0; j < RPW; ++j)
+                        m[q][j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p + 32 * q);
+#pragma unroll
+                for (int q = 0; q < UN; ++q)
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) {
+                        const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * (p + 32 * q)]);
+#pragma unroll
+                        for (int j = 0; j < RPW; ++j) acc[j][k] = fma(m[q][j].y, v.y, fma(m[q][j].x, v.x, acc[j][k]));
+                    }
+            }
+            for (; p < np; p += 32) {
+                double2 m[RPW];
+#pragma unroll
+                for (int j = 0; j < RPW; ++j) m[j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
                     const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * p]);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[j][k] = fma(m[j].y, v.y, fma(m[j].x, v.x, acc[j][k]));
+                    for (int j = 0; j < RPW; ++j) acc[j][k] = fma(m[j].y, v.y, fma(m[j].x, v.x, acc[j][k]));
                 }
             }
         } else if (nrw > 0) {
             for (int p = lane; p < np; p += 32) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < RPW; ++j) {
                     if (j < nrw) {
                         const double2 mv = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
 #pragma unroll
@@ -117,20 +140,20 @@ __global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
     }
     // ---- row sums (fixed butterfly) and outputs ----
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < RPW; ++j)
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             double s = acc[j][k];
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             acc[j][k] = s;
         }
-    if (lane < 8 && rw + lane < U.nrows) {
+    if (lane < RPW && rw + lane < U.nrows) {
         const int gr = U.r0 + rw + lane;
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < RPW; ++j)
                 if (j == lane) s = acc[j][k];
             if (!fwd) {
                 a.xpos[(long long)k * a.n + U.sdof + gr] = s;
@@ -151,20 +174,34 @@ __global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
 // Units per (pass, depth): forward levels deepest first, then backward levels root first.
 void NdChol::build_stream(cudaStream_t st) {
     std::vector<NdStreamUnit> units;
+    double read_bytes = 0.0;
     stream_off.clear();
+    stream_rpw.clear();
+    const int want = std::getenv("PDG_ND_STREAM_UNITS") ? std::atoi(std::getenv("PDG_ND_STREAM_UNITS")) : 3000;
     auto add_level = [&](int type, int depth) {
         stream_off.push_back(static_cast<int>(units.size()));
+        // rows per unit: 64, or 32 / 16 while the level has fewer than `want` units
+        long long rows_tot = 0;
+        for (int k = 0; k < nfront; ++k)
+            if (fronts[k].depth == depth) rows_tot += type == 1 ? fronts[k].s + fronts[k].b : fronts[k].s;
+        int rpu = kSRows;
+        while (rpu > 16 && rows_tot / rpu < want) rpu /= 2;
+        stream_rpw.push_back(rpu / 8);
         for (int k = 0; k < nfront; ++k) {
             const NdFront& F = fronts[k];
             if (F.depth != depth) continue;
             const int rows = type == 1 ? F.s + F.b : F.s;
-            for (int r0 = 0; r0 < rows; r0 += kSRows) {
+            for (int r0 = 0; r0 < rows; r0 += rpu) {
                 NdStreamUnit u{};
                 u.src = type == 1 ? F.moff : F.mtoff;
                 u.type = type;
                 u.r0 = r0;
-                u.nrows = std::min(kSRows, rows - r0);
-                u.ncols = type == 1 ? F.s : F.s + F.b;
+                u.nrows = std::min(rpu, rows - r0);
+                // L_SS^{-1} is lower triangular: a forward row r < s has entries in columns <= r, a
+                // backward row r (of L_SS^{-T} | G^T) in columns >= r; the exact zeros are not read
+                u.ncols = type == 1 ? (r0 + u.nrows <= F.s ? r0 + u.nrows : F.s) : F.s + F.b;
+                u.cbeg = type == 1 ? 0 : (r0 & ~1);
+                read_bytes += 8.0 * u.nrows * (u.ncols - u.cbeg);
                 u.ld = type == 1 ? F.ldm : F.ldt;
                 u.s = F.s;
                 u.b = F.b;
@@ -178,6 +215,7 @@ void NdChol::build_stream(cudaStream_t st) {
     for (int d = maxdepth; d >= 0; --d) add_level(1, d);
     for (int d = 0; d <= maxdepth; ++d) add_level(2, d);
     stream_off.push_back(static_cast<int>(units.size()));
+    factor_bytes = read_bytes;  // what a solve streams: the nonzero parts of M and M^T once each
     d_sunits.upload(units, st);
     PDG_CUDA(cudaStreamSynchronize(st));
 }
@@ -188,10 +226,16 @@ void NdChol::solve_stream(const double* b, long long ldb, double* x, long long l
     for (int l = 0; l < nl; ++l) {
         const int u0 = stream_off[l], nu = stream_off[l + 1] - u0;
         if (nu == 0) continue;
-        if (nrhs == 1)
-            k_nd_stream<1><<<nu, kSThreads, 0, st>>>(a, u0);
-        else
-            k_nd_stream<2><<<nu, kSThreads, 0, st>>>(a, u0);
+        const int rpw = stream_rpw[l];
+        if (nrhs == 1) {
+            if (rpw == 8) k_nd_stream<1, 8><<<nu, kSThreads, 0, st>>>(a, u0);
+            else if (rpw == 4) k_nd_stream<1, 4><<<nu, kSThreads, 0, st>>>(a, u0);
+            else k_nd_stream<1, 2><<<nu, kSThreads, 0, st>>>(a, u0);
+        } else {
+            if (rpw == 8) k_nd_stream<2, 8><<<nu, kSThreads, 0, st>>>(a, u0);
+            else if (rpw == 4) k_nd_stream<2, 4><<<nu, kSThreads, 0, st>>>(a, u0);
+            else k_nd_stream<2, 2><<<nu, kSThreads, 0, st>>>(a, u0);
+        }
         count_launch(1);
     }
     PDG_CHECK_LAUNCH();
