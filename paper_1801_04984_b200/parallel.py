@@ -115,22 +115,31 @@ def local_spmv(plan: HaloPlan, x_ext: np.ndarray) -> np.ndarray:
     return y
 
 
+def _p2p(dist, sends, recvs):
+    """All sends and receives of one exchange as ONE batch (dist.batch_isend_irecv): with NCCL the
+    ops of a batch are grouped, so neighbours that both send first cannot block each other once a
+    halo outgrows the p2p buffering. sends / recvs: lists of (tensor, peer)."""
+    ops = [dist.P2POp(dist.isend, t, peer) for t, peer in sends]
+    ops += [dist.P2POp(dist.irecv, t, peer) for t, peer in recvs]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
 def exchange_halo(plan: HaloPlan, x_global_owned: dict, dist, device="cpu"):
     """Point-to-point halo exchange with torch.distributed: returns the halo
     values in plan.ext_cols order (after the owned rows)."""
     import torch
 
-    reqs = []
+    sends, recvs = [], []
     bufs = {}
     for dst, cols in sorted(plan.send_to.items()):
-        t = torch.from_numpy(np.ascontiguousarray(x_global_owned["fn"](cols))).to(device)
-        reqs.append(dist.isend(t, dst))
+        sends.append((torch.from_numpy(np.ascontiguousarray(x_global_owned["fn"](cols))).to(device), dst))
     for src, cols in sorted(plan.recv_from.items()):
         b = torch.empty(len(cols), dtype=torch.float64, device=device)
         bufs[src] = b
-        reqs.append(dist.irecv(b, src))
-    for r in reqs:
-        r.wait()
+        recvs.append((b, src))
+    _p2p(dist, sends, recvs)
     # the halo part of ext_cols is sorted by global index, which interleaves the
     # sources (vertical faces are numbered column-major): place by position
     ext = plan.ext_cols[len(plan.rows):]
@@ -345,14 +354,13 @@ def exchange(vec, plan, dist):
     """Fill the halo entries of vec (global numbering) from their owners."""
     import torch
 
-    reqs, bufs = [], {}
+    sends, recvs, bufs = [], [], {}
     for dst, sel in sorted(plan["send"].items()):
-        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(vec[sel])), dst))
+        sends.append((torch.from_numpy(np.ascontiguousarray(vec[sel])), dst))
     for src, sel in sorted(plan["recv"].items()):
         bufs[src] = torch.empty(len(sel), dtype=torch.float64)
-        reqs.append(dist.irecv(bufs[src], src))
-    for r in reqs:
-        r.wait()
+        recvs.append((bufs[src], src))
+    _p2p(dist, sends, recvs)
     for src, sel in plan["recv"].items():
         vec[sel] = bufs[src].numpy()
 
@@ -609,14 +617,9 @@ class StripHalo:
         """Fill x's halo entries from the neighbours."""
         if self.dist is None or self.nranks == 1:
             return
-        reqs = []
         for k, idx in sorted(self.send.items()):
             torch_index_select(x, idx, self.sbuf[k])
-            reqs.append(self.dist.isend(self.sbuf[k], k))
-        for k in sorted(self.recv):
-            reqs.append(self.dist.irecv(self.rbuf[k], k))
-        for r in reqs:
-            r.wait()
+        _p2p(self.dist, [(self.sbuf[k], k) for k in sorted(self.send)], [(self.rbuf[k], k) for k in sorted(self.recv)])
         for k, idx in self.recv.items():
             x.index_copy_(0, idx, self.rbuf[k])
 
