@@ -235,8 +235,18 @@ int pdg_profile_read(int phase, double* ms, long long* calls, double* alg_bytes)
 int pdg_debug_recurrence_timing(pdg_block* blk, int which, unsigned long long* out, long long cap, int* ctas,
                                 int* nsteps);
 
-/* Slab solver for dG(r), r <= 1 (SlabSolver, slab.hpp:133-274). */
+/* Slab solver for dG(r), 0 <= r <= 5 (SlabSolver, slab.hpp:133-274): one block solver per
+ * diagonal block of the ordered real Schur form (1x1: a real eigenvalue, 2x2: a standardized
+ * complex pair), sharing the displacement factorisation (slab.hpp:155); solve() transforms,
+ * back-substitutes through the T_ij D y_j couplings in descending block order
+ * (slab.hpp:194-203), solves each block by preconditioned GMRES and transforms back. The
+ * report handed back is that of the block with the most iterations (final_rel_res the maximum
+ * over the blocks, device time and launches summed); pdg_slab_block_reports gives every
+ * block's iterations and final relative residual of the last solve (BlockReport, slab.hpp:113-119).
+ * Non-convergence: PDG_NOT_CONVERGED with "slab block g: GMRES did not converge (rel res ...)". */
 int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts, pdg_slab** out);
+int pdg_slab_block_reports(const pdg_slab* slab, int* n_blocks, int* block_sizes, int* iterations,
+                           double* final_rel_res);
 /* rhs: (r+1) * n_total stacked per Radau node (SlabSystem::rhs); out: (r+1) * n_total solution comps. */
 int pdg_slab_solve(pdg_slab* slab, const double* rhs, double* out, pdg_report* rep);
 int pdg_slab_solve_device(pdg_slab* slab, const double* rhs_dev, double* out_dev, pdg_report* rep);
@@ -252,8 +262,9 @@ void pdg_slab_destroy(pdg_slab* slab);
 int pdg_spmv_csr_device(int rows, const long long* row_offsets_dev, const int* col_indices_dev,
                         const double* values_dev, const double* x_dev, double* y_dev);
 
-/* dG(r) time constants, r <= 1 (time_matrices + real_schur, time_basis.hpp:135-182,
- * schur.hpp:101-173): nodes, weights, phi(0) [r+1], T and Q [(r+1)^2 row-major]. */
+/* dG(r) time constants, 0 <= r <= 5 (time_matrices + real_schur, time_basis.hpp:135-182,
+ * schur.hpp:101-173): nodes, weights, phi(0) [r+1], T and Q [(r+1)^2 row-major]; blocks of T
+ * ordered by ascending (Re, |Im|) of their eigenvalues, 2x2 blocks standardized. */
 /* Fixed-stress solver of the fixed-stress march (FixedStressSolver::solve,
  * fixed_stress.hpp:144-172, as built at march.hpp:83-84: Theta = G_hat, kappa =
  * the Radau weights): sweeps on the untransformed slab block from x0 (null =
@@ -300,6 +311,9 @@ int pdg_mass_residual_device(pdg_ops* ops, int r, double tau, const double* rhs_
                              double* residual_dev, double* scale);
 
 int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, double* T, double* Q);
+/* The diagonal blocks of T (sizes 1 | 2, first rows; up to r + 1 entries) and G_hat [(r+1)^2]
+ * (any output may be NULL except n_blocks). */
+int pdg_time_schur_blocks(int r, int* n_blocks, int* block_sizes, int* block_starts, double* G_hat);
 
 /* Seeded workload generators (Inputs). */
 void pdg_util_uniform(unsigned long long seed, long long n, double* out);

@@ -183,6 +183,7 @@ class RefProblem:
 
     def block_solve(self, r, tau, rhs, tol=1e-10, restart=50, max_iter=400, sweeps=1, stab=-1.0, backend=0,
                     flexible=False):
+        ensure_schur(r)
         o = self._opts(tol, restart, max_iter, sweeps, stab, backend, flexible)
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
         x = np.empty_like(rhs)
@@ -194,8 +195,21 @@ class RefProblem:
                        final_rel_res=rep.final_rel_res, history=hist[:rep.history_len].copy(),
                        setup_seconds=rep.setup_seconds, solve_seconds=rep.solve_seconds)
 
+    def block_solve_theta(self, theta, tau, rhs, tol=1e-10, restart=50, max_iter=400, sweeps=1, stab=-1.0, backend=0,
+                          flexible=False):
+        """GMRES solve of one transformed diagonal block given its theta (m x m) directly."""
+        theta = np.ascontiguousarray(np.atleast_2d(theta), dtype=np.float64)
+        o = self._opts(tol, restart, max_iter, sweeps, stab, backend, flexible)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty_like(rhs)
+        rep = _Report()
+        _check(lib().refcpu_block_solve_theta(self._h, theta.shape[0], _dp(theta), C.c_double(tau), C.byref(o),
+                                              _dp(rhs), _dp(x), C.byref(rep)))
+        return x, dict(converged=bool(rep.converged), iterations=rep.iterations, final_rel_res=rep.final_rel_res)
+
     def march(self, r, T, n_slabs, tol=1e-10, restart=50, max_iter=400, sweeps=1, stab=-1.0, backend=0,
               flexible=False, keep_states=False, max_slabs=0):
+        ensure_schur(r)
         o = self._opts(tol, restart, max_iter, sweeps, stab, backend, flexible)
         its = np.zeros(n_slabs, np.int32)
         res = np.zeros(n_slabs)
@@ -231,6 +245,7 @@ class RefProblem:
         return out
 
     def schur_forward(self, r, R):
+        ensure_schur(r)
         R = np.ascontiguousarray(R, np.float64)
         out = np.empty_like(R)
         _check(lib().refcpu_schur_forward(self._h, r, _dp(R), _dp(out)))
@@ -245,7 +260,35 @@ class RefProblem:
         return out, sc.value
 
 
+_raw_schur_done = set()
+
+
+def ensure_schur(r):
+    """r >= 2: register the raw real Schur form of W = M_hat^{-1} G_hat, computed by LAPACK
+    (scipy.linalg.schur), which the C++ restatement orders and standardizes as the reference
+    does with Eigen::RealSchur's (solver.hpp real_schur)."""
+    if r < 2 or r in _raw_schur_done:
+        return
+    import scipy.linalg as sl
+    n = r + 1
+    nodes, w, phi, G = np.empty(n), np.empty(n), np.empty(n), np.empty((n, n))
+    _check(lib().refcpu_time_basis(r, _dp(nodes), _dp(w), _dp(phi), _dp(G)))
+    T, Q = sl.schur(G / w[:, None], output="real")
+    T, Q = np.ascontiguousarray(T), np.ascontiguousarray(Q)
+    _check(lib().refcpu_set_raw_schur(r, _dp(T), _dp(Q)))
+    _raw_schur_done.add(r)
+
+
+def schur_blocks(r):
+    ensure_schur(r)
+    nb = C.c_int()
+    sizes, starts = np.zeros(r + 1, np.int32), np.zeros(r + 1, np.int32)
+    _check(lib().refcpu_schur_blocks(r, C.byref(nb), _ip(sizes), _ip(starts)))
+    return sizes[:nb.value].copy(), starts[:nb.value].copy()
+
+
 def time_constants(r):
+    ensure_schur(r)
     n = r + 1
     nodes, w, phi = np.empty(n), np.empty(n), np.empty(n)
     G, T, Q = np.empty((n, n)), np.empty((n, n)), np.empty((n, n))

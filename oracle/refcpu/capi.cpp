@@ -226,6 +226,44 @@ int refcpu_time_constants(int r, double* nodes, double* weights, double* phi0, d
     GUARD_END
 }
 
+// dG(r) basis alone (no Schur form): nodes, weights, phi(0) [r+1], G_hat [(r+1)^2].
+int refcpu_time_basis(int r, double* nodes, double* weights, double* phi0, double* G_hat) {
+    GUARD_BEGIN
+    const TimeBasis b = time_matrices(r);
+    const int n = r + 1;
+    for (int i = 0; i < n; ++i) {
+        nodes[i] = b.nodes[i];
+        weights[i] = b.weights[i];
+        phi0[i] = b.phi_at0[i];
+    }
+    for (int i = 0; i < n * n; ++i) G_hat[i] = b.G_hat[i];
+    GUARD_END
+}
+
+// Register the raw (unordered) real Schur form W = Q T Q^T of the (r+1) x (r+1) time operator,
+// r >= 2, computed by LAPACK (solver.hpp real_schur).
+int refcpu_set_raw_schur(int r, const double* T, const double* Q) {
+    GUARD_BEGIN
+    const int n = r + 1;
+    RawSchur rs;
+    rs.T.assign(T, T + n * n);
+    rs.Q.assign(Q, Q + n * n);
+    raw_schur_registry()[n] = rs;
+    GUARD_END
+}
+
+// Diagonal blocks of the ordered Schur form of degree r.
+int refcpu_schur_blocks(int r, int* n_blocks, int* sizes, int* starts) {
+    GUARD_BEGIN
+    const SchurForm s = real_schur(time_matrices(r));
+    *n_blocks = s.n_blocks();
+    for (int g = 0; g < s.n_blocks(); ++g) {
+        sizes[g] = s.block_sizes[g];
+        starts[g] = s.block_starts[g];
+    }
+    GUARD_END
+}
+
 struct StCsr {
     SparseMatrix s;
 };
@@ -343,6 +381,32 @@ int refcpu_block_solve(void* hp, int r, double tau, const refcpu_solve_opts* o, 
     rep->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
     rep->solve_seconds = std::chrono::duration<double>(t2 - t1).count();
     for (int i = 0; i < std::min(history_cap, rep->history_len); ++i) history[i] = br.report.residual_history[i];
+    GUARD_END
+}
+
+// GMRES solve of one transformed diagonal block given its theta (m x m, m <= 2) directly
+// (slab.hpp:154-171, :220-234): operator FixedStressSolver(theta), preconditioner
+// FixedStressSolver(theta(0,0)) per component. Used for the blocks of r >= 2.
+int refcpu_block_solve_theta(void* hp, int m, const double* theta, double tau, const refcpu_solve_opts* o,
+                             const double* rhs, double* x, refcpu_report* rep) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    SchurForm one;
+    one.n = m;
+    one.T.assign(theta, theta + m * m);
+    one.block_sizes = {m};
+    one.block_starts = {0};
+    const TimeBasis basis = time_matrices(m - 1);  // only its size is read by solve_block
+    SlabSolver solver(h->ops, basis, one, tau, to_opts(o), h->mesh.nx, h->mesh.ny);
+    Vec b(rhs, rhs + static_cast<size_t>(m) * h->ops.n_total());
+    BlockReport br;
+    const Vec sol = solver.solve_block(0, b, br);
+    std::copy(sol.begin(), sol.end(), x);
+    rep->converged = br.report.converged;
+    rep->iterations = br.report.iterations;
+    rep->history_len = static_cast<int>(br.report.residual_history.size());
+    rep->final_rel_res = br.report.final_relative_residual;
+    rep->setup_seconds = rep->solve_seconds = 0.0;
     GUARD_END
 }
 

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <complex>
+#include <map>
 
 #include "linalg.hpp"
 
@@ -156,9 +157,117 @@ struct SchurForm {
         return {re, std::sqrt(std::max(0.0, -disc))};
     }
 };
+// r >= 2: the reference calls Eigen::RealSchur (schur.hpp:108-114), an unvendored dependency
+// (Eigen >= 3.3, version unpinned). Its published algorithm is the Hessenberg + Francis
+// double-shift QR iteration of LAPACK dhseqr / EISPACK hqr2, so the oracle takes the RAW real
+// Schur form from LAPACK (scipy.linalg.schur in oracle/refcpu.py, registered per matrix size
+// through refcpu_set_raw_schur) and restates everything the reference does with it: block
+// detection, ordering by ascending (Re, |Im|) with direct adjacent swaps (schur.hpp:47-85),
+// standardization of the 2x2 blocks (schur.hpp:87-97), cleaning and the sanity checks
+// (schur.hpp:163-170). A real Schur form is unique only up to rotations of its invariant
+// subspaces, so T and Q are compared through their invariants, the slab solution directly.
+struct RawSchur {
+    std::vector<double> T, Q;  // row-major n x n
+};
+inline std::map<int, RawSchur>& raw_schur_registry() {
+    static std::map<int, RawSchur> reg;
+    return reg;
+}
+
+namespace schur_detail {
+// schur.hpp:47-85 (direct swap): A11 X - X A22 = -A12 by PartialPivLU, [X; I] = QR by
+// HouseholderQR (full Q), window rotated by Q, new strictly-lower part set to zero
+inline void swap_adjacent_blocks(int n, std::vector<double>& t, std::vector<double>& q, int i, int p, int pq) {
+    const int qs = pq - p, ns = p * qs;
+    std::vector<double> sys(static_cast<size_t>(ns) * ns, 0.0), rhs(ns);
+    for (int cc = 0; cc < qs; ++cc)
+        for (int rr = 0; rr < p; ++rr) {
+            const int eq = cc * p + rr;
+            for (int k = 0; k < p; ++k) sys[eq * ns + cc * p + k] += t[(i + rr) * n + i + k];
+            for (int k = 0; k < qs; ++k) sys[eq * ns + k * p + rr] -= t[(i + p + k) * n + i + p + cc];
+            rhs[eq] = -t[(i + rr) * n + i + p + cc];
+        }
+    std::vector<double> xv(ns);
+    DenseLu(sys, ns).solve(rhs.data(), xv.data());
+    // Householder QR of stack = [X; I] (pq x qs), Q_full = H_0 ... H_{qs-1} (makeHouseholder:
+    // beta = -sign(c0) ||x||, v = x / (c0 - beta) with v_0 = 1, tau = (beta - c0) / beta)
+    std::vector<double> st(static_cast<size_t>(pq) * qs, 0.0), qr(static_cast<size_t>(pq) * pq, 0.0);
+    for (int cc = 0; cc < qs; ++cc) {
+        for (int rr = 0; rr < p; ++rr) st[rr * qs + cc] = xv[cc * p + rr];
+        st[(p + cc) * qs + cc] = 1.0;
+    }
+    for (int k = 0; k < pq; ++k) qr[k * pq + k] = 1.0;
+    for (int k = 0; k < qs; ++k) {
+        double tail = 0.0;
+        for (int r2 = k + 1; r2 < pq; ++r2) tail += st[r2 * qs + k] * st[r2 * qs + k];
+        const double c0 = st[k * qs + k];
+        if (tail == 0.0) continue;
+        double beta = std::sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        std::vector<double> v(pq, 0.0);
+        v[k] = 1.0;
+        for (int r2 = k + 1; r2 < pq; ++r2) v[r2] = st[r2 * qs + k] / (c0 - beta);
+        const double tau = (beta - c0) / beta;
+        for (int c2 = 0; c2 < qs; ++c2) {  // st <- (I - tau v v^T) st
+            double d = 0.0;
+            for (int r2 = k; r2 < pq; ++r2) d += v[r2] * st[r2 * qs + c2];
+            for (int r2 = k; r2 < pq; ++r2) st[r2 * qs + c2] -= tau * d * v[r2];
+        }
+        for (int r2 = 0; r2 < pq; ++r2) {  // qr <- qr (I - tau v v^T)
+            double d = 0.0;
+            for (int c2 = k; c2 < pq; ++c2) d += qr[r2 * pq + c2] * v[c2];
+            for (int c2 = k; c2 < pq; ++c2) qr[r2 * pq + c2] -= tau * d * v[c2];
+        }
+    }
+    auto right = [&](std::vector<double>& m) {
+        for (int r2 = 0; r2 < n; ++r2) {
+            std::vector<double> o(pq, 0.0);
+            for (int c2 = 0; c2 < pq; ++c2)
+                for (int k = 0; k < pq; ++k) o[c2] += m[r2 * n + i + k] * qr[k * pq + c2];
+            for (int c2 = 0; c2 < pq; ++c2) m[r2 * n + i + c2] = o[c2];
+        }
+    };
+    right(t);
+    for (int c2 = 0; c2 < n; ++c2) {
+        std::vector<double> o(pq, 0.0);
+        for (int r2 = 0; r2 < pq; ++r2)
+            for (int k = 0; k < pq; ++k) o[r2] += qr[k * pq + r2] * t[(i + k) * n + c2];
+        for (int r2 = 0; r2 < pq; ++r2) t[(i + r2) * n + c2] = o[r2];
+    }
+    right(q);
+    for (int rr = qs; rr < pq; ++rr)
+        for (int cc = 0; cc < qs; ++cc) t[(i + rr) * n + i + cc] = 0.0;
+    if (qs == 2 && std::abs(t[(i + 1) * n + i]) < 1e-13) t[(i + 1) * n + i] = 0.0;
+    if (p == 2) {
+        const int j = i + qs;
+        if (std::abs(t[(j + 1) * n + j]) < 1e-13) t[(j + 1) * n + j] = 0.0;
+    }
+}
+// schur.hpp:87-97
+inline void standardize_block(int n, std::vector<double>& t, std::vector<double>& q, int i) {
+    const double a = t[i * n + i], b = t[i * n + i + 1], c = t[(i + 1) * n + i], d = t[(i + 1) * n + i + 1];
+    if (a == d) return;
+    const double theta = 0.5 * std::atan2(a - d, b + c);
+    const double cs = std::cos(theta), sn = std::sin(theta);
+    auto right = [&](std::vector<double>& m) {  // m.middleCols(i, 2) = m.middleCols(i, 2) * [cs sn; -sn cs]
+        for (int r2 = 0; r2 < n; ++r2) {
+            const double x = m[r2 * n + i], y = m[r2 * n + i + 1];
+            m[r2 * n + i] = x * cs - y * sn;
+            m[r2 * n + i + 1] = x * sn + y * cs;
+        }
+    };
+    right(t);
+    for (int c2 = 0; c2 < n; ++c2) {  // rows <- g^T rows
+        const double x = t[i * n + c2], y = t[(i + 1) * n + c2];
+        t[i * n + c2] = cs * x - sn * y;
+        t[(i + 1) * n + c2] = sn * x + cs * y;
+    }
+    right(q);
+}
+}  // namespace schur_detail
+
 inline SchurForm real_schur(const TimeBasis& basis) {
     const int n = basis.n_nodes();
-    if (n > 2) throw std::invalid_argument("real_schur: oracle restatement covers r <= 1 only");
     SchurForm s;
     s.n = n;
     s.W.assign(n * n, 0.0);
@@ -166,7 +275,67 @@ inline SchurForm real_schur(const TimeBasis& basis) {
         for (int j = 0; j < n; ++j) s.W[i * n + j] = (1.0 / basis.weights[i]) * basis.G_hat[i * n + j];
     s.Q.assign(n * n, 0.0);
     for (int i = 0; i < n; ++i) s.Q[i * n + i] = 1.0;
-    if (n == 1) {
+    if (n > 2) {
+        const auto it = raw_schur_registry().find(n);
+        if (it == raw_schur_registry().end())
+            throw std::invalid_argument("real_schur: no raw Schur form registered for r = " + std::to_string(n - 1) +
+                                        " (refcpu_set_raw_schur)");
+        s.T = it->second.T;
+        s.Q = it->second.Q;
+        auto detect = [&]() {  // schur.hpp:117-129
+            s.block_sizes.clear();
+            s.block_starts.clear();
+            int i = 0;
+            while (i < n) {
+                const bool two = (i + 1 < n) && std::abs(s.t(i + 1, i)) > 1e-12 * (std::abs(s.t(i, i)) + std::abs(s.t(i + 1, i + 1)));
+                s.block_starts.push_back(i);
+                s.block_sizes.push_back(two ? 2 : 1);
+                i += two ? 2 : 1;
+            }
+        };
+        detect();
+        auto key_less = [&](int g1, int g2) {  // schur.hpp:133-137
+            const auto e1 = s.block_eigenvalue(g1), e2 = s.block_eigenvalue(g2);
+            if (std::abs(e1.real() - e2.real()) > 1e-12 * (1.0 + std::abs(e1.real()))) return e1.real() < e2.real();
+            return std::abs(e1.imag()) < std::abs(e2.imag());
+        };
+        bool swapped = true;
+        while (swapped) {
+            swapped = false;
+            for (int g = 0; g + 1 < s.n_blocks(); ++g)
+                if (key_less(g + 1, g)) {
+                    const int i = s.block_starts[g], p = s.block_sizes[g];
+                    schur_detail::swap_adjacent_blocks(n, s.T, s.Q, i, p, p + s.block_sizes[g + 1]);
+                    detect();
+                    swapped = true;
+                    break;
+                }
+        }
+        for (int g = 0; g < s.n_blocks(); ++g)
+            if (s.block_sizes[g] == 2) schur_detail::standardize_block(n, s.T, s.Q, s.block_starts[g]);
+        for (int g = 0; g < s.n_blocks(); ++g) {
+            const int i = s.block_starts[g], bs = s.block_sizes[g];
+            for (int rr = i; rr < i + bs; ++rr)
+                for (int cc = 0; cc < i; ++cc) s.T[rr * n + cc] = 0.0;
+            if (bs == 1 && i + 1 < n) s.T[(i + 1) * n + i] = 0.0;
+        }
+        double orth = 0.0, resid = 0.0, wmax = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                double qq = 0.0, rec = 0.0;
+                for (int k = 0; k < n; ++k) {
+                    qq += s.q(k, i) * s.q(k, j);
+                    double tq = 0.0;
+                    for (int l = 0; l < n; ++l) tq += s.t(k, l) * s.q(j, l);
+                    rec += s.q(i, k) * tq;
+                }
+                orth = std::max(orth, std::abs(qq - (i == j ? 1.0 : 0.0)));
+                resid = std::max(resid, std::abs(rec - s.W[i * n + j]));
+                wmax = std::max(wmax, std::abs(s.W[i * n + j]));
+            }
+        if (orth > 1e-12) throw SolverError("real_schur: Q lost orthogonality");
+        if (resid > 1e-10 * (1.0 + wmax)) throw SolverError("real_schur: factorization residual too large");
+    } else if (n == 1) {
         s.T = s.W;
         s.block_sizes = {1};
         s.block_starts = {0};

@@ -103,6 +103,7 @@ _SIGS = {
     "pdg_slab_solve": (C.c_int, [VP, DP, DP, C.POINTER(Report)]),
     "pdg_slab_solve_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
     "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "pdg_slab_block_reports": (C.c_int, [VP, IP, IP, IP, DP]),
     "pdg_slab_destroy": (None, [VP]),
     "pdg_fs_create": (C.c_int, [VP, C.c_int, C.c_double, C.POINTER(FsOpts), C.POINTER(VP)]),
     "pdg_fs_solve": (C.c_int, [VP, DP, DP, DP, C.POINTER(Report)]),
@@ -138,6 +139,7 @@ _SIGS = {
     "pdg_mass_residual": (C.c_int, [VP, C.c_int, C.c_double, DP, DP, DP, DP]),
     "pdg_mass_residual_device": (C.c_int, [VP, C.c_int, C.c_double, VP, VP, VP, DP]),
     "pdg_time_constants": (C.c_int, [C.c_int, DP, DP, DP, DP, DP]),
+    "pdg_time_schur_blocks": (C.c_int, [C.c_int, IP, IP, IP, DP]),
     "pdg_debug_recurrence_timing": (C.c_int, [VP, C.c_int, C.POINTER(C.c_ulonglong), C.c_longlong, IP, IP]),
     "pdg_util_uniform": (None, [C.c_ulonglong, C.c_longlong, DP]),
     "pdg_util_lognormal": (None, [C.c_ulonglong, C.c_longlong, C.c_double, DP]),

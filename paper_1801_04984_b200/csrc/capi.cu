@@ -51,8 +51,13 @@ struct pdg_slab {
     pdg_ops* ops = nullptr;
     TimeConsts tc;
     double tau = 0;
-    std::unique_ptr<pdg_block> blk;
+    // one solver per diagonal Schur block (slab.hpp:154-171), solved in descending order with the
+    // T_ij D y_j couplings of the blocks above (slab.hpp:194-203); r <= 1: a single block
+    std::vector<std::unique_ptr<pdg_block>> blks;
+    std::vector<int> blk_iterations;        // per block, last solve (BlockReport::gmres_iterations)
+    std::vector<double> blk_final_rel_res;  // per block, last solve
     DBuf<double> d_Q, d_w, d_phi0, shat, ysol, io_a, io_b, rhs_u, rhs_q, rhs_p, djump, et_u;
+    DBuf<double> dpt;  // D y_j (p rows) of the solved components, n x n_p
 };
 
 #define API_BEGIN try {
@@ -141,7 +146,7 @@ __global__ void k_slab_rhs(int nn, int nu, int nq, int np, double tau, const dou
 // res += (storage + flux) - src, scale += (|storage| + |flux|) + |src|.
 // Writes |res| per cell; the scale maximum is an order-free atomic max on the
 // (non-negative) double bits. Same operation order as the reference, no FMA.
-constexpr int kMaxNodes = 4;
+constexpr int kMaxNodes = kMaxTimeDegree + 1;
 __global__ void k_mass_residual(int np, int nu, int nq, int n, const double* __restrict__ G, const double* __restrict__ w,
                                 double tau, double mb, double im, const double* __restrict__ m_p, const int* et_off,
                                 const int* et_idx, const double* et_val, const int* bt_off, const int* bt_idx,
@@ -171,6 +176,21 @@ __global__ void k_mass_residual(int np, int nu, int nq, int n, const double* __r
         }
         residual[c] = fabs(res);
         atomicMax(scale_bits, static_cast<unsigned long long>(__double_as_longlong(sc)));
+    }
+}
+
+// rhs_i (p rows) -= sum_{j >= j0} T(i, j) D y_j for the rows i of one Schur block (slab.hpp:197-200)
+__global__ void k_schur_backsub(int np, int n, int i0, int m, int j0, const double* __restrict__ T,
+                                const double* __restrict__ dp, long long nt, long long poff, double* shat) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * np;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int bi = static_cast<int>(t / np), c = static_cast<int>(t % np);
+        double r = shat[(i0 + bi) * nt + poff + c];
+        for (int j = j0; j < n; ++j) {
+            const double tij = T[(i0 + bi) * n + j];
+            if (tij != 0.0) r = __dsub_rn(r, __dmul_rn(tij, dp[(long long)j * np + c]));
+        }
+        shat[(i0 + bi) * nt + poff + c] = r;
     }
 }
 
@@ -683,18 +703,28 @@ void pdg_op_destroy(pdg_op* op) {
 int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts, pdg_slab** out) {
     API_BEGIN
     require(ops && opts && out, "pdg_slab_create: null argument");
-    require(r == 0 || r == 1, "pdg_slab_create: r must be 0 or 1");
+    require(r >= 0 && r <= kMaxTimeDegree, "pdg_slab_create: r must be in [0, 5]");
     require(tau > 0.0, "build_slab_system: tau must be positive");
     auto s = std::make_unique<pdg_slab>();
     s->ops = ops;
     s->tc = time_consts(r);
     s->tau = tau;
     const int nn = r + 1;
-    pdg_block* b = nullptr;
-    const int rc = pdg_block_create(ops, nn, s->tc.T.data(), tau, s->tc.T[0], opts, &b);
-    if (rc != PDG_OK) return rc;
-    s->blk.reset(b);
+    for (int g = 0; g < s->tc.n_blocks(); ++g) {
+        const int m = s->tc.block_sizes[g], i0 = s->tc.block_starts[g];
+        double theta[4];
+        for (int a = 0; a < m; ++a)
+            for (int c = 0; c < m; ++c) theta[a * m + c] = s->tc.T[(i0 + a) * nn + i0 + c];
+        pdg_block* b = nullptr;
+        // per-time-component preconditioner lambda = T_gg(0,0) (2x2 blocks are standardized, slab.hpp:166-169)
+        const int rc = pdg_block_create(ops, m, theta, tau, theta[0], opts, &b);
+        if (rc != PDG_OK) return rc;
+        s->blks.emplace_back(b);
+    }
+    s->blk_iterations.assign(s->tc.n_blocks(), 0);
+    s->blk_final_rel_res.assign(s->tc.n_blocks(), 0.0);
     cudaStream_t st = ops->s.ctx->stream;
+    if (s->tc.n_blocks() > 1) s->dpt.alloc((size_t)nn * ops->s.n_p);
     s->d_Q.upload(s->tc.Q, st);
     s->d_w.upload(s->tc.weights, st);
     s->d_phi0.upload(s->tc.phi0, st);
@@ -717,7 +747,67 @@ int pdg_slab_solve_device(pdg_slab* s, const double* rhs_dev, double* out_dev, p
     k_schur_fwd<<<grid_for(nn * nt, 256), 256, 0, st>>>(nn, nt, s->d_Q.p, s->d_w.p, rhs_dev, s->shat.p); }
     count_launch();
     PDG_CHECK_LAUNCH();
-    s->blk->b.solve(s->shat.p, s->ysol.p, rep, 0);
+    const int nb = s->tc.n_blocks();
+    if (nb == 1) {
+        s->blks[0]->b.solve(s->shat.p, s->ysol.p, rep, 0);
+        if (rep) {
+            s->blk_iterations[0] = rep->iterations;
+            s->blk_final_rel_res[0] = rep->final_rel_res;
+        }
+    } else {
+        // blocks in descending order (slab.hpp:194-235); the report handed back is the block
+        // with the most iterations (march.hpp logs the maximum), device time and launches summed
+        const SpatialOps& o = s->ops->s;
+        DBuf<double> dT;
+        dT.upload(s->tc.T, st);
+        pdg_report best{};
+        double ms = 0.0;
+        int launches = 0;
+        bool have = false;
+        for (int g = nb - 1; g >= 0; --g) {
+            const int m = s->tc.block_sizes[g], i0 = s->tc.block_starts[g];
+            if (i0 + m < nn) {
+                k_schur_backsub<<<grid_for((long long)m * o.n_p, 256), 256, 0, st>>>(o.n_p, nn, i0, m, i0 + m, dT.p, s->dpt.p,
+                                                                                     nt, (long long)o.n_u + o.n_q, s->shat.p);
+                count_launch();
+                PDG_CHECK_LAUNCH();
+            }
+            pdg_report br{};
+            if (rep) {
+                br.history = rep->history;  // the last solved block's history ends up in the caller's buffer
+                br.history_cap = rep->history_cap;
+            }
+            s->blks[g]->b.solve(s->shat.p + (long long)i0 * nt, s->ysol.p + (long long)i0 * nt, &br, g);
+            s->blk_iterations[g] = br.iterations;
+            s->blk_final_rel_res[g] = br.final_rel_res;
+            ms += br.device_ms;
+            launches += br.kernel_launches;
+            if (!have || br.iterations > best.iterations) best = br;
+            have = true;
+            if (g > 0)
+                for (int bi = 0; bi < m; ++bi) {
+                    const double* yj = s->ysol.p + (long long)(i0 + bi) * nt;
+                    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p,
+                                                                             o.Et.val.p, o.m_p.p, yj, yj + o.n_u + o.n_q,
+                                                                             s->dpt.p + (size_t)(i0 + bi) * o.n_p);
+                    count_launch();
+                    PDG_CHECK_LAUNCH();
+                }
+        }
+        if (rep) {
+            double worst = 0.0;
+            for (double v : s->blk_final_rel_res) worst = std::max(worst, v);
+            double* hist = rep->history;
+            const int cap = rep->history_cap;
+            *rep = best;
+            rep->history = hist;
+            rep->history_cap = cap;
+            rep->final_rel_res = worst;
+            rep->device_ms = ms;
+            rep->kernel_launches = launches;
+        }
+        PDG_CUDA(cudaStreamSynchronize(st));  // dT is released at scope exit
+    }
     { ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * nt);
     k_schur_bwd<<<grid_for(nn * nt, 256), 256, 0, st>>>(nn, nt, s->d_Q.p, s->ysol.p, out_dev); }
     count_launch();
@@ -768,6 +858,18 @@ int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev
     // like every other *_device entry point: rhs_dev is complete when the call returns, so a
     // caller on another stream (torch's) may read it without a library-stream dependency
     PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+int pdg_slab_block_reports(const pdg_slab* s, int* n_blocks, int* block_sizes, int* iterations, double* final_rel_res) {
+    API_BEGIN
+    require(s && n_blocks, "pdg_slab_block_reports: null argument");
+    *n_blocks = s->tc.n_blocks();
+    for (int g = 0; g < s->tc.n_blocks(); ++g) {
+        if (block_sizes) block_sizes[g] = s->tc.block_sizes[g];
+        if (iterations) iterations[g] = s->blk_iterations[g];
+        if (final_rel_res) final_rel_res[g] = s->blk_final_rel_res[g];
+    }
     API_END
 }
 
@@ -910,6 +1012,20 @@ int pdg_time_constants(int r, double* nodes, double* weights, double* phi0, doub
         T[i] = tc.T[i];
         Q[i] = tc.Q[i];
     }
+    API_END
+}
+
+int pdg_time_schur_blocks(int r, int* n_blocks, int* block_sizes, int* block_starts, double* G_hat) {
+    API_BEGIN
+    require(n_blocks != nullptr, "pdg_time_schur_blocks: null argument");
+    const TimeConsts tc = time_consts(r);
+    *n_blocks = tc.n_blocks();
+    for (int g = 0; g < tc.n_blocks(); ++g) {
+        if (block_sizes) block_sizes[g] = tc.block_sizes[g];
+        if (block_starts) block_starts[g] = tc.block_starts[g];
+    }
+    if (G_hat)
+        for (int i = 0; i < tc.n * tc.n; ++i) G_hat[i] = tc.G[i];
     API_END
 }
 

@@ -112,7 +112,11 @@ def time_constants(r: int):
     nodes, w, phi = np.empty(n), np.empty(n), np.empty(n)
     T, Q = np.empty((n, n)), np.empty((n, n))
     check(lib().pdg_time_constants(r, _dp(nodes), _dp(w), _dp(phi), _dp(T), _dp(Q)))
-    return dict(nodes=nodes, weights=w, phi_at0=phi, T=T, Q=Q)
+    nb = C.c_int()
+    sizes, starts, G = np.zeros(n, np.int32), np.zeros(n, np.int32), np.empty((n, n))
+    check(lib().pdg_time_schur_blocks(r, C.byref(nb), _ip(sizes), _ip(starts), _dp(G)))
+    return dict(nodes=nodes, weights=w, phi_at0=phi, T=T, Q=Q, G_hat=G, block_sizes=sizes[:nb.value].copy(),
+                block_starts=starts[:nb.value].copy())
 
 
 class SpaceTimeOperator:
@@ -328,8 +332,9 @@ class BlockSolver:
 
 
 class SlabSolver:
-    """SlabSolver (slab.hpp:133-274) for dG(r), r in {0, 1}: Schur transform,
-    GMRES block solve and back-transform on the device."""
+    """SlabSolver (slab.hpp:133-274) for dG(r), 0 <= r <= 5: Schur transform, one GMRES
+    solve per diagonal Schur block with the back-substitution couplings, and the
+    back-transform, all on the device."""
 
     def __init__(self, ops: SpatialOperators, r: int, tau: float, opt: SolveOptions | None = None):
         self.ops, self.r, self.tau = ops, r, tau
@@ -357,6 +362,15 @@ class SlabSolver:
         rep, hist = _report(self.opt.gmres.max_iter + 2)
         check(lib().pdg_slab_solve_device(self._h, rhs_ptr, out_ptr, C.byref(rep)))
         return _to_report(rep, hist)
+
+    def block_reports(self):
+        """Per Schur block of the last solve: (block size, GMRES iterations, final relative
+        residual), blocks in ascending order (BlockReport, slab.hpp:113-119)."""
+        nb = C.c_int()
+        n = self.r + 1
+        sizes, its, res = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n)
+        check(lib().pdg_slab_block_reports(self._h, C.byref(nb), _ip(sizes), _ip(its), _dp(res)))
+        return [(int(sizes[g]), int(its[g]), float(res[g])) for g in range(nb.value)]
 
     def rhs_device(self, t0: float, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int, tau: float | None = None):
         """build_slab_system on the device for the slab [t0, t0 + tau] (tau defaults

@@ -793,3 +793,63 @@ def test_large_mesh_slab_solve(n):
     for rep in reps:
         assert rep.converged and 3 <= rep.iterations <= 6
         assert rep.mass_rel < 1e-7
+
+
+# ---- dG(r), r >= 2: several Schur blocks (slab.hpp:194-203, schur.hpp:101-173) ----
+@pytest.mark.parametrize("r", [2, 3, 4, 5])
+def test_time_constants_high_order(oracle, r):
+    """pdg_time_constants for r >= 2 (Hessenberg + Francis QR in the library where the reference
+    calls Eigen::RealSchur; the oracle takes LAPACK's): the basis constants agree to roundoff, the
+    ordered block structure is the same, Q is orthogonal, Q T Q^T = W, and the diagonal blocks
+    carry the same eigenvalues in the same standardized form. (T's off-block entries and Q are
+    unique only up to rotations of the invariant subspaces.)"""
+    lib, ref = S.time_constants(r), oracle.time_constants(r)
+    n = r + 1
+    for k in ("nodes", "weights", "phi_at0", "G_hat"):
+        assert np.allclose(lib[k], ref[k], rtol=1e-13, atol=1e-14), k
+    sizes, starts = oracle.schur_blocks(r)
+    assert np.array_equal(lib["block_sizes"], sizes) and np.array_equal(lib["block_starts"], starts)
+    W = lib["G_hat"] / lib["weights"][:, None]
+    T, Q = lib["T"], lib["Q"]
+    assert abs(Q.T @ Q - np.eye(n)).max() <= 1e-12
+    assert abs(Q @ T @ Q.T - W).max() <= 1e-10 * (1 + abs(W).max())
+    for s, i in zip(sizes, starts):
+        assert np.allclose(np.diag(T)[i:i + s], np.diag(ref["T"])[i:i + s], rtol=1e-11)
+        if s == 2:
+            assert T[i, i] == pytest.approx(T[i + 1, i + 1], rel=1e-13)
+            assert T[i, i + 1] * T[i + 1, i] == pytest.approx(ref["T"][i, i + 1] * ref["T"][i + 1, i], rel=1e-10)
+            assert (T[i + 2:, i:i + 2] == 0.0).all()
+        else:
+            assert (T[i + 1:, i] == 0.0).all()
+
+
+@pytest.mark.parametrize("candidate", ["reference", "flexible"])
+@pytest.mark.parametrize("r", [2, 3])
+def test_march_high_order_parity(oracle, r, candidate):
+    """dG(2) / dG(3) march of a config-0-type problem: one GMRES solve per Schur block in descending
+    order with the T_ij D y_j couplings on the device (slab.hpp:194-235). Per slab: the maximum
+    block iteration count within +-1 of the oracle's and the state within 1e-9."""
+    spec = P.config0()
+    rp = oracle.RefProblem(spec.to_dict())
+    n_slabs = 3
+    ref = rp.march(r, 0.3, n_slabs, tol=1e-10, restart=50, backend=0, flexible=candidate == "flexible",
+                   keep_states=True)
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate)
+    reps, states = S.march(ops, r, 0.3, n_slabs, opt, keep_states=True, mass_check=True)
+    for s in range(n_slabs):
+        assert reps[s].converged
+        assert abs(reps[s].iterations - int(ref["iterations"][s])) <= 1, (s, reps[s].iterations, ref["iterations"])
+        d = np.linalg.norm(states[s] - ref["states"][s].ravel()) / np.linalg.norm(ref["states"][s])
+        assert d <= SOLVE_RTOL, (s, d)
+        assert reps[s].mass_rel <= 1e-7
+    slab = S.SlabSolver(ops, r, 0.1, opt)
+    rhs = rp.slab_rhs(r, 0.0, 0.1, np.zeros(rp.n_u), np.zeros(rp.n_p))
+    x, rep = slab.solve(rhs)
+    blocks = slab.block_reports()
+    sizes, _ = oracle.schur_blocks(r)
+    assert [b[0] for b in blocks] == list(sizes)
+    assert rep.iterations == max(b[1] for b in blocks) and all(b[2] <= 1e-10 for b in blocks)
+    assert np.linalg.norm(x - ref["states"][0].ravel()) <= SOLVE_RTOL * np.linalg.norm(ref["states"][0])
+    with pytest.raises(S.InvalidArgument):
+        S.SlabSolver(ops, 6, 0.1, opt)
