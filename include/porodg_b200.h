@@ -144,6 +144,27 @@ int pdg_ops_sizes(const pdg_ops* ops, long long sizes[7]);
 int pdg_ops_download(const pdg_ops* ops, int which, int* row_offsets, int* col_indices, double* values);
 /* assemble_rhs (assembly.hpp:467-563) for constant boundary data at time t. */
 int pdg_ops_rhs(const pdg_ops* ops, double t, double* u, double* q, double* p);
+/* assemble_rhs in full (assembly.hpp:467-563): VolumeData (assembly.hpp:24-28) and time- / space-
+ * dependent boundary functions (boundary.hpp:12-13). std::function callbacks cannot cross the ABI,
+ * so the caller evaluates its fields at the quadrature points for the time t it wants and passes
+ * the samples (host arrays); the device accumulates them in the reference's order (bit-identical).
+ * Sample points (pdg_rhs_sample_points returns them): per cell c the 6 x 6 Gauss points
+ * (x0 + g_i hx, y0 + g_j hy), index c*36 + i*6 + j; per boundary face, in ascending face index
+ * (bottom row, top row, left column, right column: 2 nx + 2 ny faces), the 6 Gauss points
+ * x0 + g_k (x1 - x0). momentum / darcy / mass may be NULL (absent field, assembly.hpp:485);
+ * traction / dirichlet / flow hold eval_or_zero of the face's traction_data, dirichlet_data and
+ * flow data (prescribed pressure, or prescribed normal flux on no-flow-kind faces). 2D only. */
+typedef struct {
+    const double* momentum;  /* [n_cells][36][2] */
+    const double* darcy;     /* [n_cells][36][2] */
+    const double* mass;      /* [n_cells][36] */
+    const double* traction;  /* [n_bfaces][6][2] */
+    const double* dirichlet; /* [n_bfaces][6][2] */
+    const double* flow;      /* [n_bfaces][6] */
+} pdg_rhs_samples;
+/* cell_xy [n_cells][36][2], bface_ids [2 nx + 2 ny], bface_xy [n_bfaces][6][2] (any may be NULL) */
+int pdg_rhs_sample_points(const pdg_ops* ops, double* cell_xy, int* bface_ids, double* bface_xy);
+int pdg_ops_rhs_sampled(const pdg_ops* ops, const pdg_rhs_samples* samples, double* u, double* q, double* p);
 void pdg_ops_destroy(pdg_ops* ops);
 
 /* One transformed diagonal block: theta is m x m row-major (T_gg), lambda_pre
@@ -256,6 +277,10 @@ int pdg_slab_solve_device(pdg_slab* slab, const double* rhs_dev, double* out_dev
  * ((r+1) * n_total). */
 int pdg_slab_rhs_device(pdg_slab* slab, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
                         double* rhs_dev);
+/* The same with sampled data: samples[i] holds the fields at the slab's Radau node i,
+ * t = t0 + nodes[i] * tau (r + 1 entries; pdg_time_constants gives the nodes). */
+int pdg_slab_rhs_sampled_device(pdg_slab* slab, double tau, const pdg_rhs_samples* samples, const double* u_prev_dev,
+                                const double* p_prev_dev, double* rhs_dev);
 void pdg_slab_destroy(pdg_slab* slab);
 
 /* Order-fixed CSR SpMV (SparseMatrix::apply) on device buffers. */

@@ -147,6 +147,25 @@ class RefProblem:
         _check(lib().refcpu_assemble_rhs(self._h, C.c_double(t), _dp(u), _dp(q), _dp(p)))
         return u, q, p
 
+    def set_test_fields(self, kind=1):
+        """Install (1) or clear (0) the analytic, time-dependent VolumeData and boundary functions."""
+        _check(lib().refcpu_set_test_fields(self._h, kind))
+
+    def sample_rhs_data(self, t):
+        """The installed fields at assemble_rhs's quadrature points at time t, as the dict
+        paper_1801_04984_b200.solver.SpatialOperators.rhs_sampled takes."""
+        nc, nb = self.n_p, 2 * (self.spec["nx"] + self.spec["ny"])
+        out = dict(momentum=np.empty((nc, 36, 2)), darcy=np.empty((nc, 36, 2)), mass=np.empty((nc, 36)),
+                   traction=np.empty((nb, 6, 2)), dirichlet=np.empty((nb, 6, 2)), flow=np.empty((nb, 6)))
+        present = (C.c_int * 3)()
+        _check(lib().refcpu_sample_rhs_data(self._h, C.c_double(t), _dp(out["momentum"]), _dp(out["darcy"]),
+                                            _dp(out["mass"]), _dp(out["traction"]), _dp(out["dirichlet"]),
+                                            _dp(out["flow"]), present))
+        for k, name in enumerate(("momentum", "darcy", "mass")):
+            if not present[k]:
+                out[name] = None
+        return out
+
     def spacetime_csr(self, theta, tau):
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         m = theta.shape[0]
@@ -294,6 +313,12 @@ def time_constants(r):
     G, T, Q = np.empty((n, n)), np.empty((n, n)), np.empty((n, n))
     _check(lib().refcpu_time_constants(r, _dp(nodes), _dp(w), _dp(phi), _dp(G), _dp(T), _dp(Q)))
     return dict(nodes=nodes, weights=w, phi_at0=phi, G_hat=G, T=T, Q=Q)
+
+
+def gauss_points(n):
+    pts, wts = np.empty(n), np.empty(n)
+    _check(lib().refcpu_gauss(n, _dp(pts), _dp(wts)))
+    return pts
 
 
 def csr_apply(off, idx, val, x, threads=1):

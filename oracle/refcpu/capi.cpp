@@ -145,6 +145,94 @@ int refcpu_create3(const refcpu_problem3* p, void** out) {
     GUARD_END
 }
 
+// Smooth, time-dependent analytic test fields for the full assemble_rhs path (VolumeData and
+// boundary functions, assembly.hpp:24-28, boundary.hpp:12-13): kind 0 clears them, kind 1
+// installs momentum / Darcy / mass sources and, on every tag, traction, Dirichlet and flow data
+// (prescribed pressure, or a nonzero prescribed normal flux on no-flow-kind faces). 2D.
+int refcpu_set_test_fields(void* hp, int kind) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    if (h->dim != 2) throw std::invalid_argument("test fields: 2D only");
+    const FaceTag tags[4] = {FaceTag::left, FaceTag::right, FaceTag::bottom, FaceTag::top};
+    if (kind == 0) {
+        h->data = VolumeData{};
+        for (FaceTag t : tags) {
+            h->ops.bc.displacement[BoundarySpec::slot(t)]->dirichlet_data = {};
+            h->ops.bc.displacement[BoundarySpec::slot(t)]->traction_data = {};
+            h->ops.bc.flow[BoundarySpec::slot(t)]->data = {};
+        }
+    } else {
+        h->data.momentum = [](double x, double y, double t) {
+            return std::array<double, 2>{std::sin(1.3 * x + 0.7 * y) * (1.0 + 0.5 * t), x * y - 0.3 * t};
+        };
+        h->data.darcy = [](double x, double y, double t) {
+            return std::array<double, 2>{std::cos(2.0 * x) * y + t, 0.25 + x - y * y * t};
+        };
+        h->data.mass = [](double x, double y, double t) { return std::exp(-t) * (1.0 + x) * std::sin(3.0 * y); };
+        int k = 0;
+        for (FaceTag t : tags) {
+            const double a = 0.1 * (++k);
+            h->ops.bc.displacement[BoundarySpec::slot(t)]->dirichlet_data = [a](double x, double y, double tt) {
+                return std::array<double, 2>{a * std::sin(x + 2.0 * y + tt), a * (x - y) * (1.0 + tt)};
+            };
+            h->ops.bc.displacement[BoundarySpec::slot(t)]->traction_data = [a](double x, double y, double tt) {
+                return std::array<double, 2>{a + x * tt, -1.0 + a * std::cos(y - tt)};
+            };
+            h->ops.bc.flow[BoundarySpec::slot(t)]->data = [a](double x, double y, double tt) {
+                return a * (1.0 + x * y) + 0.2 * std::sin(tt + x - y);
+            };
+        }
+    }
+    GUARD_END
+}
+
+// The installed fields evaluated at assemble_rhs's quadrature points at time t (what a host
+// binding passes to pdg_ops_rhs_sampled): per cell the 6 x 6 points (xi outer), per boundary
+// face in ascending face index the 6 points. vol_present[3]: momentum, darcy, mass set?
+int refcpu_sample_rhs_data(void* hp, double t, double* momentum, double* darcy, double* mass, double* traction,
+                           double* dirichlet, double* flow, int* vol_present) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    const Mesh& mesh = h->mesh;
+    const QuadratureRule gq = gauss_legendre(kDataQuadOrder);
+    vol_present[0] = static_cast<bool>(h->data.momentum);
+    vol_present[1] = static_cast<bool>(h->data.darcy);
+    vol_present[2] = static_cast<bool>(h->data.mass);
+    for (int c = 0; c < mesh.n_cells(); ++c) {
+        const Cell& cell = mesh.cells[c];
+        for (size_t i = 0; i < 6; ++i)
+            for (size_t j = 0; j < 6; ++j) {
+                const double x = cell.x0 + gq.points[i] * cell.hx, y = cell.y0 + gq.points[j] * cell.hy;
+                const size_t k = static_cast<size_t>(c) * 36 + i * 6 + j;
+                const auto fm = eval_or_zero(h->data.momentum, x, y, t), fd = eval_or_zero(h->data.darcy, x, y, t);
+                momentum[2 * k] = fm[0];
+                momentum[2 * k + 1] = fm[1];
+                darcy[2 * k] = fd[0];
+                darcy[2 * k + 1] = fd[1];
+                mass[k] = eval_or_zero(h->data.mass, x, y, t);
+            }
+    }
+    size_t b = 0;
+    for (int f = 0; f < mesh.n_faces(); ++f) {
+        const Face& face = mesh.faces[f];
+        if (!face.is_boundary()) continue;
+        const DisplacementBC& dbc = h->ops.bc.displacement_on(face.tag);
+        const FlowBC& fbc = h->ops.bc.flow_on(face.tag);
+        for (size_t q = 0; q < 6; ++q) {
+            const double s = gq.points[q];
+            const double x = face.x0 + s * (face.x1 - face.x0), y = face.y0 + s * (face.y1 - face.y0);
+            const auto tn = eval_or_zero(dbc.traction_data, x, y, t), ud = eval_or_zero(dbc.dirichlet_data, x, y, t);
+            traction[(b * 6 + q) * 2] = tn[0];
+            traction[(b * 6 + q) * 2 + 1] = tn[1];
+            dirichlet[(b * 6 + q) * 2] = ud[0];
+            dirichlet[(b * 6 + q) * 2 + 1] = ud[1];
+            flow[b * 6 + q] = eval_or_zero(fbc.data, x, y, t);
+        }
+        ++b;
+    }
+    GUARD_END
+}
+
 void refcpu_destroy(void* h) { delete static_cast<Handle*>(h); }
 
 // sizes[0..] = n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E), nnz(M_p)
@@ -595,6 +683,17 @@ int refcpu_mass_residual(void* hp, int r, double tau, const double* rhs, const d
     const MassResidual mr = local_mass_residual(h->ops, basis, tau, R, comps);
     std::copy(mr.residual.begin(), mr.residual.end(), residual);
     *scale = mr.scale;
+    GUARD_END
+}
+
+// gauss_legendre(n) on [0, 1] (quadrature.hpp:33-54)
+int refcpu_gauss(int n, double* pts, double* wts) {
+    GUARD_BEGIN
+    const QuadratureRule g = gauss_legendre(n);
+    for (int i = 0; i < n; ++i) {
+        pts[i] = g.points[i];
+        wts[i] = g.weights[i];
+    }
     GUARD_END
 }
 

@@ -52,6 +52,12 @@ class Problem3(C.Structure):
                 ("disp_data", (C.c_double * 3) * 6), ("flow_kind", C.c_int * 6), ("flow_data", C.c_double * 6)]
 
 
+class RhsSamples(C.Structure):
+    _fields_ = [("momentum", C.POINTER(C.c_double)), ("darcy", C.POINTER(C.c_double)), ("mass", C.POINTER(C.c_double)),
+                ("traction", C.POINTER(C.c_double)), ("dirichlet", C.POINTER(C.c_double)),
+                ("flow", C.POINTER(C.c_double))]
+
+
 class GmresOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int), ("max_iter", C.c_int), ("sweeps", C.c_int),
                 ("stab", C.c_double), ("candidate", C.c_int)]
@@ -89,6 +95,8 @@ _SIGS = {
     "pdg_ops_sizes": (C.c_int, [VP, LLP]),
     "pdg_ops_download": (C.c_int, [VP, C.c_int, IP, IP, DP]),
     "pdg_ops_rhs": (C.c_int, [VP, C.c_double, DP, DP, DP]),
+    "pdg_rhs_sample_points": (C.c_int, [VP, DP, IP, DP]),
+    "pdg_ops_rhs_sampled": (C.c_int, [VP, C.POINTER(RhsSamples), DP, DP, DP]),
     "pdg_ops_destroy": (None, [VP]),
     "pdg_block_create": (C.c_int, [VP, C.c_int, DP, C.c_double, C.c_double, C.POINTER(GmresOpts), C.POINTER(VP)]),
     "pdg_block_rows": (C.c_int, [VP, LLP, LLP]),
@@ -104,6 +112,7 @@ _SIGS = {
     "pdg_slab_solve_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
     "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_block_reports": (C.c_int, [VP, IP, IP, IP, DP]),
+    "pdg_slab_rhs_sampled_device": (C.c_int, [VP, C.c_double, C.POINTER(RhsSamples), C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_destroy": (None, [VP]),
     "pdg_fs_create": (C.c_int, [VP, C.c_int, C.c_double, C.POINTER(FsOpts), C.POINTER(VP)]),
     "pdg_fs_solve": (C.c_int, [VP, DP, DP, DP, C.POINTER(Report)]),

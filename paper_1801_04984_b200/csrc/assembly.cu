@@ -547,6 +547,167 @@ __global__ void k_rhs_qp(Geo g, int nq, int np, const signed char* qc, double* q
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) p[c] = 0.0;
 }
 
+// ---- assemble_rhs with sampled data (assembly.hpp:467-563 in full: VolumeData and time- /
+// space-dependent boundary functions). The host evaluates its fields at the quadrature points
+// (6 x 6 Gauss per cell, xi outer; 6 Gauss per boundary face) and the kernels accumulate in the
+// reference's order: per dof the volume points (i, j) in order, then the cell's boundary
+// faces in ascending face index; per flux row the adjacent cells in ascending index, then the
+// boundary term, then the eliminated couplings (mq_bc, b_bc) in push order.
+struct Samples {
+    const double* momentum;   // [cell][36][2] or null
+    const double* darcy;      // [cell][36][2] or null
+    const double* mass;       // [cell][36] or null
+    const double* traction;   // [bface][6][2]
+    const double* dirichlet;  // [bface][6][2]
+    const double* flow;       // [bface][6]
+};
+
+// index of boundary face f in the ascending list of boundary faces
+__device__ __forceinline__ int bface_index(const Geo& g, int f) {
+    const int nh = g.nx * (g.ny + 1);
+    if (f < g.nx) return f;
+    if (f < nh) return g.nx + (f - g.ny * g.nx);
+    if (f < nh + g.ny) return 2 * g.nx + (f - nh);
+    return 2 * g.nx + g.ny + (f - nh - g.nx * g.ny);
+}
+
+__global__ void k_rhs_u_s(Geo g, Samples sm, double* u) {
+    const int n = g.nx * g.ny;
+    const double area = g.hx * g.hy;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 8LL * n; t += (long long)gridDim.x * blockDim.x) {
+        const int c = static_cast<int>(t / 8), l = static_cast<int>(t % 8);
+        const int i = c % g.nx, j = c / g.nx;
+        const int cf[4] = {hface(g, i, j), hface(g, i, j + 1), vface(g, i, j), vface(g, i + 1, j)};
+        const int a = l / 2, comp = l % 2;
+        double r = 0.0;
+        if (sm.momentum)
+            for (int qi = 0; qi < 6; ++qi)
+                for (int qj = 0; qj < 6; ++qj) {
+                    const double w = g.g6w[qi] * g.g6w[qj] * area;
+                    const double nv = shp(a, g.g6p[qi], g.g6p[qj]);
+                    r += w * nv * sm.momentum[((long long)c * 36 + qi * 6 + qj) * 2 + comp];
+                }
+        for (int q = 0; q < 4; ++q) {
+            const FaceInfo F = face_info(g, cf[q]);
+            if (!F.boundary) continue;
+            const int* dir = g.disp_dir[F.tag - 1];
+            const double gamma_f = sipg(g, F);
+            const long long bf = bface_index(g, cf[q]);
+            for (int qk = 0; qk < 6; ++qk) {
+                const double s = g.g6p[qk];
+                const double w = g.g6w[qk] * F.measure;
+                double xi, eta;
+                ref_point(g, F, c, s, xi, eta);
+                const double tn0 = sm.traction[(bf * 6 + qk) * 2], tn1 = sm.traction[(bf * 6 + qk) * 2 + 1];
+                const double ud0 = sm.dirichlet[(bf * 6 + qk) * 2], ud1 = sm.dirichlet[(bf * 6 + qk) * 2 + 1];
+                const double mud0 = dir[0] ? ud0 : 0.0, mud1 = dir[1] ? ud1 : 0.0;
+                const double nv = shp(a, xi, eta);
+                if (!dir[comp]) r += w * nv * (comp == 0 ? tn0 : tn1);
+                if (dir[comp]) r += w * gamma_f * nv * (comp == 0 ? mud0 : mud1);
+                double tv0, tv1;
+                traction(g, a, comp, xi, eta, F.nx, F.ny, tv0, tv1);
+                r -= w * (tv0 * mud0 + tv1 * mud1);
+            }
+        }
+        u[t] = r + 0.0;
+    }
+}
+
+// prescribed normal-flux values of the constrained faces: q_values[f] = sum_k (w_k / |F|) data_k
+__global__ void k_rhs_qvalues(Geo g, int nq, const signed char* qc, Samples sm, double* qv) {
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nq; f += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (qc[f]) {
+            const FaceInfo F = face_info(g, f);
+            const long long bf = bface_index(g, f);
+            for (int qk = 0; qk < 6; ++qk) {
+                const double w = g.g6w[qk] * F.measure;
+                v += w / F.measure * sm.flow[bf * 6 + qk];
+            }
+        }
+        qv[f] = v;
+    }
+}
+
+__global__ void k_rhs_qp_s(Geo g, int nq, int np, const double* __restrict__ kcells, const signed char* qc, Samples sm,
+                           const double* __restrict__ qv, double* q, double* p) {
+    const double area = g.hx * g.hy;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nq; f += gridDim.x * blockDim.x) {
+        const FaceInfo F = face_info(g, f);
+        if (qc[f]) {  // essential value (assembly.hpp:554)
+            q[f] = qv[f];
+            continue;
+        }
+        double r = 0.0;
+        if (sm.darcy)
+            for (int side = 0; side < 2; ++side) {
+                const int c = side ? F.cp : F.cm;
+                if (c < 0) continue;
+                const int i = c % g.nx, j = c / g.nx;
+                // local face of c: W, E (vertical) or S, N (horizontal), and its normal sign
+                const bool low = F.vertical ? (f == vface(g, i, j)) : (f == hface(g, i, j));
+                const double sg = F.vertical ? F.nx : F.ny;
+                for (int qi = 0; qi < 6; ++qi)
+                    for (int qj = 0; qj < 6; ++qj) {
+                        const double xi = g.g6p[qi], eta = g.g6p[qj];
+                        const double w = g.g6w[qi] * g.g6w[qj] * area;
+                        const double t = F.vertical ? xi : eta;
+                        const double wf = low ? sg * (1.0 - t) : sg * t;
+                        r += w * wf * sm.darcy[((long long)c * 36 + qi * 6 + qj) * 2 + (F.vertical ? 0 : 1)];
+                    }
+            }
+        if (F.boundary) {  // pressure condition (assembly.hpp:549-550)
+            const long long bf = bface_index(g, f);
+            for (int qk = 0; qk < 6; ++qk) {
+                const double w = g.g6w[qk] * F.measure;
+                r -= w * sm.flow[bf * 6 + qk];
+            }
+        }
+        // eliminated couplings to constrained faces (mq_bc, assembly.hpp:250-258, :556)
+        for (int side = 0; side < 2; ++side) {
+            const int c = side ? F.cp : F.cm;
+            if (c < 0) continue;
+            const int i = c % g.nx, j = c / g.nx;
+            int f0, f1;
+            if (F.vertical) {
+                f0 = vface(g, i, j);
+                f1 = vface(g, i + 1, j);
+            } else {
+                f0 = hface(g, i, j);
+                f1 = hface(g, i, j + 1);
+            }
+            const int opp = (f == f0) ? f1 : f0;
+            if (!qc[opp]) continue;
+            const double keff = g.eta / (kcells ? kcells[c] : g.kperm);
+            const double d6 = keff * area / 6.0;
+            const double cross = d6 * axis_sign(face_info(g, f0)) * axis_sign(face_info(g, f1));
+            r -= cross * qv[opp];
+        }
+        q[f] = r;
+    }
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
+        double r = 0.0;
+        if (sm.mass)
+            for (int qi = 0; qi < 6; ++qi)
+                for (int qj = 0; qj < 6; ++qj) {
+                    const double w = g.g6w[qi] * g.g6w[qj] * area;
+                    r -= w * sm.mass[(long long)c * 36 + qi * 6 + qj];
+                }
+        // b_bc (assembly.hpp:270-273, :557): the cell's constrained faces in the order W, E, S, N
+        const int i = c % g.nx, j = c / g.nx;
+        const int cfo[4] = {vface(g, i, j), vface(g, i + 1, j), hface(g, i, j), hface(g, i, j + 1)};
+        for (int k = 0; k < 4; ++k) {
+            const int f = cfo[k];
+            if (!qc[f]) continue;
+            const FaceInfo F = face_info(g, f);
+            const double sout = F.boundary ? 1.0 : (c == F.cm ? 1.0 : -1.0);
+            const double v = -sout * F.measure;
+            r -= v * qv[f];
+        }
+        p[c] = r;
+    }
+}
+
 Geo make_geo(const pdg_problem& p) {
     Geo g{};
     g.nx = p.nx;
@@ -673,6 +834,42 @@ void assemble_ops_device(SpatialOps& s, const pdg_problem& p, cudaStream_t st) {
     k_mp<<<grid_for(n, 256), 256, 0, st>>>(g, n, s.m_p.p);
     PDG_CHECK_LAUNCH();
     PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void assemble_rhs_sampled_device(const SpatialOps& s, const pdg_rhs_samples& h, double* u, double* q, double* p,
+                                 cudaStream_t st) {
+    require(s.nz == 0, "pdg_ops_rhs_sampled: 2D meshes only");
+    require(h.traction && h.dirichlet && h.flow, "pdg_ops_rhs_sampled: boundary samples must be given");
+    const Geo g = make_geo(s.prob);
+    const size_t nc = (size_t)s.n_p, nbf = 2 * ((size_t)s.nx + s.ny);
+    DBuf<double> mom, dar, mas, tra, dir, flo, kc, qv(s.n_q);
+    Samples sm{};
+    if (h.momentum) {
+        mom.upload(h.momentum, nc * 72, st);
+        sm.momentum = mom.p;
+    }
+    if (h.darcy) {
+        dar.upload(h.darcy, nc * 72, st);
+        sm.darcy = dar.p;
+    }
+    if (h.mass) {
+        mas.upload(h.mass, nc * 36, st);
+        sm.mass = mas.p;
+    }
+    tra.upload(h.traction, nbf * 12, st);
+    dir.upload(h.dirichlet, nbf * 12, st);
+    flo.upload(h.flow, nbf * 6, st);
+    sm.traction = tra.p;
+    sm.dirichlet = dir.p;
+    sm.flow = flo.p;
+    if (!s.k_cells.empty()) kc.upload(s.k_cells, st);
+    k_rhs_u_s<<<grid_for(8LL * s.n_p, 256), 256, 0, st>>>(g, sm, u);
+    k_rhs_qvalues<<<grid_for(s.n_q, 256), 256, 0, st>>>(g, s.n_q, s.q_constrained.p, sm, qv.p);
+    k_rhs_qp_s<<<grid_for(std::max(s.n_q, s.n_p), 256), 256, 0, st>>>(g, s.n_q, s.n_p, kc.n ? kc.p : nullptr,
+                                                                       s.q_constrained.p, sm, qv.p, q, p);
+    count_launch(3);
+    PDG_CHECK_LAUNCH();
+    PDG_CUDA(cudaStreamSynchronize(st));  // the staging buffers are released at scope exit
 }
 
 void assemble_rhs_device(const SpatialOps& s, double t, double* u, double* q, double* p, cudaStream_t st) {

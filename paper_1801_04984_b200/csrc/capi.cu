@@ -497,6 +497,57 @@ int pdg_ops_rhs(const pdg_ops* ops, double t, double* u, double* q, double* p) {
     API_END
 }
 
+int pdg_rhs_sample_points(const pdg_ops* ops, double* cell_xy, int* bface_ids, double* bface_xy) {
+    API_BEGIN
+    require(ops != nullptr, "pdg_rhs_sample_points: null ops");
+    const SpatialOps& s = ops->s;
+    require(s.has_problem && s.nz == 0, "pdg_rhs_sample_points: needs a 2D problem description (pdg_ops_assemble)");
+    const int nx = s.nx, ny = s.ny;
+    const double hx = s.prob.lx / nx, hy = s.prob.ly / ny;
+    std::vector<double> pts, wts;
+    tc_gauss(6, pts, wts);
+    if (cell_xy)
+        for (int c = 0; c < nx * ny; ++c) {
+            const double x0 = (c % nx) * hx, y0 = (c / nx) * hy;
+            for (int i = 0; i < 6; ++i)
+                for (int j = 0; j < 6; ++j) {
+                    cell_xy[((size_t)c * 36 + i * 6 + j) * 2] = x0 + pts[i] * hx;
+                    cell_xy[((size_t)c * 36 + i * 6 + j) * 2 + 1] = y0 + pts[j] * hy;
+                }
+        }
+    const int nh = nx * (ny + 1);
+    int k = 0;
+    auto face = [&](int f, double x0, double y0, double x1, double y1) {
+        if (bface_ids) bface_ids[k] = f;
+        if (bface_xy)
+            for (int q = 0; q < 6; ++q) {
+                bface_xy[((size_t)k * 6 + q) * 2] = x0 + pts[q] * (x1 - x0);
+                bface_xy[((size_t)k * 6 + q) * 2 + 1] = y0 + pts[q] * (y1 - y0);
+            }
+        ++k;
+    };
+    for (int i = 0; i < nx; ++i) face(i, i * hx, 0 * hy, (i + 1) * hx, 0 * hy);
+    for (int i = 0; i < nx; ++i) face(ny * nx + i, i * hx, ny * hy, (i + 1) * hx, ny * hy);
+    for (int j = 0; j < ny; ++j) face(nh + j, 0 * hx, j * hy, 0 * hx, (j + 1) * hy);
+    for (int j = 0; j < ny; ++j) face(nh + nx * ny + j, nx * hx, j * hy, nx * hx, (j + 1) * hy);
+    API_END
+}
+
+int pdg_ops_rhs_sampled(const pdg_ops* ops, const pdg_rhs_samples* samples, double* u, double* q, double* p) {
+    API_BEGIN
+    require(ops && samples && u && q && p, "pdg_ops_rhs_sampled: null argument");
+    const SpatialOps& s = ops->s;
+    require(s.has_problem, "pdg_ops_rhs_sampled: operators were uploaded without a problem description");
+    cudaStream_t st = s.ctx->stream;
+    DBuf<double> du(s.n_u), dq(s.n_q), dp(s.n_p);
+    assemble_rhs_sampled_device(s, *samples, du.p, dq.p, dp.p, st);
+    PDG_CUDA(cudaMemcpyAsync(u, du.p, sizeof(double) * s.n_u, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(q, dq.p, sizeof(double) * s.n_q, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaMemcpyAsync(p, dp.p, sizeof(double) * s.n_p, cudaMemcpyDeviceToHost, st));
+    PDG_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
 void pdg_ops_destroy(pdg_ops* ops) { delete ops; }
 
 int pdg_block_create(pdg_ops* ops, int m, const double* theta, double tau, double lambda_pre,
@@ -870,6 +921,35 @@ int pdg_slab_block_reports(const pdg_slab* s, int* n_blocks, int* block_sizes, i
         if (iterations) iterations[g] = s->blk_iterations[g];
         if (final_rel_res) final_rel_res[g] = s->blk_final_rel_res[g];
     }
+    API_END
+}
+
+int pdg_slab_rhs_sampled_device(pdg_slab* s, double tau, const pdg_rhs_samples* samples, const double* u_prev_dev,
+                                const double* p_prev_dev, double* rhs_dev) {
+    API_BEGIN
+    require(s && samples && u_prev_dev && p_prev_dev && rhs_dev, "pdg_slab_rhs_sampled_device: null argument");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
+    const SpatialOps& o = s->ops->s;
+    require(o.has_problem, "pdg_slab_rhs_sampled_device: operators were uploaded without a problem description");
+    cudaStream_t st = o.ctx->stream;
+    const int nn = s->tc.n;
+    if (!s->rhs_u.n) {
+        s->rhs_u.alloc((size_t)nn * o.n_u);
+        s->rhs_q.alloc((size_t)nn * o.n_q);
+        s->rhs_p.alloc((size_t)nn * o.n_p);
+        s->djump.alloc(o.n_p);
+    }
+    for (int i = 0; i < nn; ++i)
+        assemble_rhs_sampled_device(o, samples[i], s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
+                                    s->rhs_p.p + (size_t)i * o.n_p, st);
+    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
+                                                             o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
+    k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, tau, s->d_w.p,
+                                                                           s->d_phi0.p, s->rhs_u.p, s->rhs_q.p,
+                                                                           s->rhs_p.p, s->djump.p, rhs_dev);
+    count_launch(2);
+    PDG_CHECK_LAUNCH();
+    PDG_CUDA(cudaStreamSynchronize(st));
     API_END
 }
 

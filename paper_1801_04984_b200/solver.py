@@ -244,6 +244,34 @@ class SpatialOperators:
         check(lib().pdg_ops_rhs(self._h, t, _dp(u), _dp(q), _dp(p)))
         return u, q, p
 
+    def sample_points(self):
+        """Quadrature points at which assemble_rhs evaluates its data (pdg_rhs_sample_points):
+        cell points (n_cells, 36, 2), boundary face ids (2 nx + 2 ny,), face points (n_bfaces, 6, 2)."""
+        nb = 2 * (self.nx + self.ny)
+        cxy, ids, fxy = np.empty((self.n_p, 36, 2)), np.empty(nb, np.int32), np.empty((nb, 6, 2))
+        check(lib().pdg_rhs_sample_points(self._h, _dp(cxy), _ip(ids), _dp(fxy)))
+        return cxy, ids, fxy
+
+    @staticmethod
+    def _samples_struct(samples):
+        """samples: dict with 'traction', 'dirichlet', 'flow' and optionally 'momentum', 'darcy', 'mass'."""
+        st, keep = _lib.RhsSamples(), []
+        for k in ("momentum", "darcy", "mass", "traction", "dirichlet", "flow"):
+            v = samples.get(k)
+            if v is not None:
+                a = np.ascontiguousarray(v, np.float64)
+                keep.append(a)
+                setattr(st, k, _dp(a))
+        return st, keep
+
+    def rhs_sampled(self, samples):
+        """assemble_rhs (assembly.hpp:467-563) from fields sampled at sample_points()."""
+        st, keep = self._samples_struct(samples)
+        u, q, p = np.empty(self.n_u), np.empty(self.n_q), np.empty(self.n_p)
+        check(lib().pdg_ops_rhs_sampled(self._h, C.byref(st), _dp(u), _dp(q), _dp(p)))
+        del keep
+        return u, q, p
+
     def mass_residual(self, r, tau, rhs, state):
         """local_mass_residual (slab.hpp:292-318) of one slab on the GPU: rhs and
         state are (r+1, n_total) (slab right-hand side and solution per Radau
@@ -377,6 +405,20 @@ class SlabSolver:
         to the solver's)."""
         check(lib().pdg_slab_rhs_device(self._h, t0, self.tau if tau is None else tau, u_prev_ptr, p_prev_ptr,
                                         rhs_ptr))
+
+    def rhs_sampled_device(self, samples_per_node, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int,
+                           tau: float | None = None):
+        """build_slab_system from sampled data: samples_per_node[i] = the fields at t0 + nodes[i] tau."""
+        assert len(samples_per_node) == self.r + 1
+        arr = (_lib.RhsSamples * (self.r + 1))()
+        keep = []
+        for i, sm in enumerate(samples_per_node):
+            st, k = SpatialOperators._samples_struct(sm)
+            arr[i] = st
+            keep.append(k)
+        check(lib().pdg_slab_rhs_sampled_device(self._h, self.tau if tau is None else tau, arr, u_prev_ptr, p_prev_ptr,
+                                                rhs_ptr))
+        del keep
 
     def mass_residual_device(self, rhs_ptr: int, state_ptr: int, residual_ptr: int, tau: float | None = None) -> float:
         """local_mass_residual (slab.hpp:292-318) of a device slab system/state

@@ -853,3 +853,89 @@ def test_march_high_order_parity(oracle, r, candidate):
     assert np.linalg.norm(x - ref["states"][0].ravel()) <= SOLVE_RTOL * np.linalg.norm(ref["states"][0])
     with pytest.raises(S.InvalidArgument):
         S.SlabSolver(ops, 6, 0.1, opt)
+
+
+# ---- assemble_rhs in full: VolumeData and time-/space-dependent boundary functions ----
+def _rhs_variants():
+    a = P.config0()
+    a.nx, a.ny = 5, 3
+    b = P.config1(6)
+    b.disp = {"left": ("fixed", (0.0, 0.0)), "right": ("roller_x", (0.0, 0.0)),
+              "bottom": ("roller_y", (0.0, 0.0)), "top": ("traction", (0.0, 0.0))}
+    b.flow = {"left": ("pressure", 0.0), "right": ("no_flow", 0.0), "bottom": ("no_flow", 0.0), "top": ("pressure", 0.0)}
+    b.lx, b.ly = 1.3, 0.9
+    c = P.config0()
+    c.nx, c.ny = 1, 1
+    return [a, b, c]
+
+
+@pytest.mark.parametrize("spec", _rhs_variants(), ids=lambda s: f"{s.nx}x{s.ny}")
+def test_rhs_sampled_bit_identical(oracle, spec):
+    """pdg_ops_rhs_sampled == assemble_rhs (assembly.hpp:467-563) with momentum / Darcy / mass
+    sources and time- and space-dependent traction, Dirichlet, pressure and prescribed-flux data
+    (the eliminated couplings mq_bc / b_bc included), bit for bit: the fields are sampled at the
+    quadrature points by the host (here the oracle) and accumulated on the device in the
+    reference's order. Sample points as the library documents them; absent fields skipped."""
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    rp.set_test_fields(1)
+    for t in (0.0, 0.37):
+        sm = rp.sample_rhs_data(t)
+        u, q, p = rp.assemble_rhs(t)
+        gu, gq, gp = ops.rhs_sampled(sm)
+        assert np.array_equal(u, gu) and np.array_equal(q, gq) and np.array_equal(p, gp)
+        assert np.abs(q).max() > 0 and np.abs(p).max() > 0
+    # the documented sample points are the ones the reference evaluates at
+    cxy, ids, fxy = ops.sample_points()
+    hx, hy = spec.lx / spec.nx, spec.ly / spec.ny
+    g6 = oracle.gauss_points(6)
+    assert np.array_equal(cxy[0, :, 0].reshape(6, 6)[:, 0], 0 * hx + g6 * hx)
+    assert np.array_equal(cxy[-1, :, 1].reshape(6, 6)[0, :], (spec.ny - 1) * hy + g6 * hy)
+    assert len(ids) == 2 * (spec.nx + spec.ny) and (np.diff(ids) > 0).all()
+    # boundary data only (no volume fields): the volume loops are skipped as in the reference
+    rp.set_test_fields(1)
+    sm = rp.sample_rhs_data(0.2)
+    sm0 = dict(sm, momentum=None, darcy=None, mass=None)
+    zero = {k: np.zeros_like(v) for k, v in sm.items()}
+    gu0, gq0, gp0 = ops.rhs_sampled(dict(sm0))
+    gu1, gq1, gp1 = ops.rhs_sampled(dict(zero, traction=sm["traction"], dirichlet=sm["dirichlet"], flow=sm["flow"]))
+    assert np.array_equal(gu0, gu1) and np.array_equal(gq0, gq1) and np.array_equal(gp0, gp1)
+    # constant data through the sampled path == the constant-data kernels == the oracle
+    rp2 = oracle.RefProblem(spec.to_dict())
+    sm = rp2.sample_rhs_data(0.0)
+    assert sm["momentum"] is None and sm["darcy"] is None and sm["mass"] is None
+    cu, cq, cp = ops.rhs(0.0)
+    su, sq, sp_ = ops.rhs_sampled(sm)
+    ru, rq, rpp = rp2.assemble_rhs(0.0)
+    for a_, b_, c_ in ((ru, cu, su), (rq, cq, sq), (rpp, cp, sp_)):
+        assert np.array_equal(a_, b_) and np.array_equal(a_, c_)
+
+
+def test_march_with_sampled_data(oracle):
+    """A dG(1) slab built from sampled, time-dependent data on the device
+    (pdg_slab_rhs_sampled_device) equals the oracle's build_slab_system bit for bit, and its
+    solve matches the oracle's."""
+    import torch
+    spec = _rhs_variants()[1]
+    rp = oracle.RefProblem(spec.to_dict())
+    rp.set_test_fields(1)
+    ops = S.SpatialOperators.assemble(spec)
+    r, tau, t0 = 1, 0.05, 0.1
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50))
+    slab = S.SlabSolver(ops, r, tau, opt)
+    nodes = S.time_constants(r)["nodes"]
+    u_prev = 0.01 * P.uniform_vector(3, ops.n_u)
+    p_prev = 0.01 * P.uniform_vector(4, ops.n_p)
+    ref_rhs = rp.slab_rhs(r, t0, tau, u_prev, p_prev)
+    samples = [rp.sample_rhs_data(t0 + c * tau) for c in nodes]
+    ud, pd = torch.from_numpy(u_prev).cuda(), torch.from_numpy(p_prev).cuda()
+    rhs = torch.empty((r + 1) * ops.n_total, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    slab.rhs_sampled_device(samples, ud.data_ptr(), pd.data_ptr(), rhs.data_ptr())
+    assert np.array_equal(rhs.cpu().numpy(), ref_rhs)
+    x, rep = slab.solve(ref_rhs)
+    T = oracle.time_constants(r)
+    xr, rr = rp.block_solve(r, tau, rp.schur_forward(r, ref_rhs), tol=1e-10, restart=50, backend=1)
+    y = (T["Q"] @ xr.reshape(r + 1, -1)).ravel()
+    assert abs(rep.iterations - rr["iterations"]) <= 1
+    assert np.linalg.norm(x - y) <= SOLVE_RTOL * np.linalg.norm(y)
