@@ -164,6 +164,26 @@ def test_nd_streaming_mode_matches_default(oracle, monkeypatch, dim):
     assert np.linalg.norm(xs - xr) <= SOLVE_RTOL * np.linalg.norm(xr)
 
 
+@pytest.mark.parametrize("candidate", ["reference", "flexible"])
+def test_march_3d_dg1_parity(oracle, candidate):
+    """dG(1) in 3D (the element pair of config 4 at a size the oracle reaches, 4^3): the 2x2
+    Schur block with two right-hand sides per inner solve; iterations within +-1, states within
+    1e-9 of the oracle."""
+    spec = P.config2(4)
+    spec.k_perm_cells = P.lognormal_field(7, 64, 1.5)
+    rp = oracle.RefProblem(spec.to_dict())
+    ref = rp.march(1, 0.25, 2, tol=1e-10, restart=50, backend=1, flexible=candidate == "flexible", keep_states=True)
+    ops = S.SpatialOperators.assemble(spec)
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate=candidate)
+    reps, states = S.march(ops, 1, 0.25, 2, opt, keep_states=True, mass_check=True)
+    for s in range(2):
+        assert reps[s].converged
+        assert abs(reps[s].iterations - int(ref["iterations"][s])) <= 1
+        d = np.linalg.norm(states[s] - ref["states"][s].ravel()) / np.linalg.norm(ref["states"][s])
+        assert d <= SOLVE_RTOL, (s, d)
+        assert reps[s].mass_rel <= 1e-7
+
+
 def test_upload3_matches_device_assembly(oracle):
     """Operators assembled by the CPU restatement and uploaded (pdg_ops_upload3) give the same
     slab solve, bit for bit, as the device-assembled ones."""
