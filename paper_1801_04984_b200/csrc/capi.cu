@@ -58,6 +58,7 @@ struct pdg_slab {
     std::vector<double> blk_final_rel_res;  // per block, last solve
     DBuf<double> d_Q, d_w, d_phi0, shat, ysol, io_a, io_b, rhs_u, rhs_q, rhs_p, djump, et_u;
     DBuf<double> dpt;  // D y_j (p rows) of the solved components, n x n_p
+    DBuf<double> d_T;  // the Schur form's T on the device (back-substitution couplings)
 };
 
 #define API_BEGIN try {
@@ -775,7 +776,10 @@ int pdg_slab_create(pdg_ops* ops, int r, double tau, const pdg_gmres_opts* opts,
     s->blk_iterations.assign(s->tc.n_blocks(), 0);
     s->blk_final_rel_res.assign(s->tc.n_blocks(), 0.0);
     cudaStream_t st = ops->s.ctx->stream;
-    if (s->tc.n_blocks() > 1) s->dpt.alloc((size_t)nn * ops->s.n_p);
+    if (s->tc.n_blocks() > 1) {
+        s->dpt.alloc((size_t)nn * ops->s.n_p);
+        s->d_T.upload(s->tc.T, st);
+    }
     s->d_Q.upload(s->tc.Q, st);
     s->d_w.upload(s->tc.weights, st);
     s->d_phi0.upload(s->tc.phi0, st);
@@ -809,8 +813,7 @@ int pdg_slab_solve_device(pdg_slab* s, const double* rhs_dev, double* out_dev, p
         // blocks in descending order (slab.hpp:194-235); the report handed back is the block
         // with the most iterations (march.hpp logs the maximum), device time and launches summed
         const SpatialOps& o = s->ops->s;
-        DBuf<double> dT;
-        dT.upload(s->tc.T, st);
+        DBuf<double>& dT = s->d_T;
         pdg_report best{};
         double ms = 0.0;
         int launches = 0;
@@ -857,7 +860,6 @@ int pdg_slab_solve_device(pdg_slab* s, const double* rhs_dev, double* out_dev, p
             rep->device_ms = ms;
             rep->kernel_launches = launches;
         }
-        PDG_CUDA(cudaStreamSynchronize(st));  // dT is released at scope exit
     }
     { ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * nt);
     k_schur_bwd<<<grid_for(nn * nt, 256), 256, 0, st>>>(nn, nt, s->d_Q.p, s->ysol.p, out_dev); }

@@ -184,6 +184,20 @@ def test_march_3d_dg1_parity(oracle, candidate):
         assert reps[s].mass_rel <= 1e-7
 
 
+def test_fixed_stress_march_3d(oracle):
+    """The fixed-stress branch of the march (march.hpp:80-108, dG(0)) on the 3D operators: sweep
+    counts identical to the oracle's, states within 1e-8 (the iteration stops at tol 1e-10)."""
+    spec = P.config2(4)
+    rp = oracle.RefProblem(spec.to_dict())
+    ref = rp.march_fs(0, 0.3, 3, tol=1e-10, backend=1, keep_states=True)
+    ops = S.SpatialOperators.assemble(spec)
+    reps, states = S.march(ops, 0, 0.3, 3, S.SolveOptions(), keep_states=True, method="fixed-stress")
+    assert [r.iterations for r in reps] == [int(v) for v in ref["sweeps"]]
+    for s in range(3):
+        d = np.linalg.norm(states[s] - ref["states"][s].ravel()) / np.linalg.norm(ref["states"][s])
+        assert d <= 1e-8, (s, d)
+
+
 def test_upload3_matches_device_assembly(oracle):
     """Operators assembled by the CPU restatement and uploaded (pdg_ops_upload3) give the same
     slab solve, bit for bit, as the device-assembled ones."""
