@@ -21,16 +21,35 @@ namespace pdg {
             throw ::pdg::Error(PDG_CUDA_ERROR, std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
     } while (0)
 
+// cuBLAS / cuSOLVER handles are expensive to create (tens of ms each): one pair per host thread
+// and device, created on first use and reused by every factorization (handles are not
+// thread-safe, hence thread_local; they are released with the thread).
+namespace {
+struct HandleCache {
+    cublasHandle_t blas[64] = {};
+    cusolverDnHandle_t solver[64] = {};
+    ~HandleCache() {
+        for (int d = 0; d < 64; ++d) {
+            if (blas[d]) cublasDestroy(blas[d]);
+            if (solver[d]) cusolverDnDestroy(solver[d]);
+        }
+    }
+};
+thread_local HandleCache g_handles;
+}  // namespace
+
 LaHandles::LaHandles(cudaStream_t st) {
-    PDG_CUBLAS(cublasCreate(&blas));
+    int dev = 0;
+    PDG_CUDA(cudaGetDevice(&dev));
+    dev %= 64;
+    if (!g_handles.blas[dev]) PDG_CUBLAS(cublasCreate(&g_handles.blas[dev]));
+    if (!g_handles.solver[dev]) PDG_CUSOLVER(cusolverDnCreate(&g_handles.solver[dev]));
+    blas = g_handles.blas[dev];
+    solver = g_handles.solver[dev];
     PDG_CUBLAS(cublasSetStream(blas, st));
-    PDG_CUSOLVER(cusolverDnCreate(&solver));
     PDG_CUSOLVER(cusolverDnSetStream(solver, st));
 }
-LaHandles::~LaHandles() {
-    if (blas) cublasDestroy(blas);
-    if (solver) cusolverDnDestroy(solver);
-}
+LaHandles::~LaHandles() {}
 
 namespace {
 

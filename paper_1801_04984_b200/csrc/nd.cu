@@ -212,6 +212,90 @@ __global__ void k_nd_pack(int s, int b, const double* T, const double* G, double
     }
 }
 
+// Batched factorization of one tree level (setup): one CTA per front does what the cuSOLVER /
+// cuBLAS sequence does per front (extend-add of the children's update matrices, partial
+// Cholesky of the s pivots with the Schur complement left in F_BB for the parent,
+// T = L_SS^{-1}, G = L_BS T, M / M^T packed into the store), so a level of hundreds of small
+// fronts is ONE launch instead of ~10 library calls per front (the setup was launch-bound:
+// config 1, 2047 + 1023 fronts). Fronts are dense column-major (ld = f), lower triangle.
+struct NdFactorDesc {
+    long long fo, moff, mtoff;
+    long long cfo[2], cmap[2];
+    int s, b, ldm, ldt, nchild, front;
+    int cs[2], cb[2];
+};
+constexpr int kFactorThreads = 256;
+__global__ void __launch_bounds__(kFactorThreads) k_nd_factor_batch(const NdFactorDesc* descs, double* dense, const int* maps,
+                                                                   double* store, int* info) {
+    const NdFactorDesc D = descs[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kFactorThreads / 32;
+    const int s = D.s, b = D.b, f = s + b;
+    double* F = dense + D.fo;
+    // 1. extend-add, children in order (their maps are injective: no two entries collide)
+    for (int q = 0; q < D.nchild; ++q) {
+        const int bc = D.cb[q], fc = D.cs[q] + bc;
+        const double* U = dense + D.cfo[q] + D.cs[q] + (long long)D.cs[q] * fc;
+        const int* map = maps + D.cmap[q];
+        for (long long t = tid; t < (long long)bc * bc; t += kFactorThreads) {
+            const int r = static_cast<int>(t % bc), c = static_cast<int>(t / bc);
+            if (r < c) continue;
+            const int pr = map[r], pc = map[c];
+            const int hi = max(pr, pc), lo = min(pr, pc);
+            F[hi + (long long)lo * f] += U[r + (long long)c * fc];
+        }
+        __syncthreads();
+    }
+    // 2. right-looking partial Cholesky: pivots 0..s-1, updates reach the whole lower triangle
+    for (int k = 0; k < s; ++k) {
+        if (tid == 0) {
+            double d = F[k + (long long)k * f];
+            if (!(d > 0.0)) {
+                if (info[D.front] == 0) info[D.front] = k + 1;
+                d = 1.0;
+            }
+            F[k + (long long)k * f] = sqrt(d);
+        }
+        __syncthreads();
+        const double dk = F[k + (long long)k * f];
+        for (int i = k + 1 + tid; i < f; i += kFactorThreads) F[i + (long long)k * f] /= dk;
+        __syncthreads();
+        for (int j = k + 1 + warp; j < f; j += nw) {
+            const double ljk = F[j + (long long)k * f];
+            for (int i = j + lane; i < f; i += 32) F[i + (long long)j * f] -= F[i + (long long)k * f] * ljk;
+        }
+        __syncthreads();
+    }
+    // 3. T = L_SS^{-1} straight into M (row-major, ld = ldm): thread j owns column j
+    double* M = store + D.moff;
+    double* MT = store + D.mtoff;
+    for (int j = tid; j < D.ldm; j += kFactorThreads) {
+        for (int i = 0; i < s; ++i) {
+            double acc = 0.0;
+            if (j < s && i >= j) {
+                acc = i == j ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) acc -= F[i + (long long)k * f] * M[(long long)k * D.ldm + j];
+                acc /= F[i + (long long)i * f];
+            }
+            M[(long long)i * D.ldm + j] = acc;
+        }
+    }
+    __syncthreads();
+    // 4. G = L_BS T into the rows s.. of M
+    for (long long t = tid; t < (long long)b * D.ldm; t += kFactorThreads) {
+        const int r = static_cast<int>(t / D.ldm), c = static_cast<int>(t % D.ldm);
+        double acc = 0.0;
+        if (c < s)
+            for (int k = c; k < s; ++k) acc += F[(s + r) + (long long)k * f] * M[(long long)k * D.ldm + c];
+        M[(long long)(s + r) * D.ldm + c] = acc;
+    }
+    __syncthreads();
+    // 5. M^T (s x ldt)
+    for (long long t = tid; t < (long long)s * D.ldt; t += kFactorThreads) {
+        const int r = static_cast<int>(t / D.ldt), c = static_cast<int>(t % D.ldt);
+        MT[t] = c < f ? M[(long long)c * D.ldm + r] : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // device: the solve
 // ---------------------------------------------------------------------------
@@ -1065,9 +1149,69 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         porder.resize(nf);
         std::iota(porder.begin(), porder.end(), 0);
     }
+    // levels of many small fronts: one batched launch per level (k_nd_factor_batch); the few
+    // large fronts near the root (and everything in streaming mode) go through cuSOLVER / cuBLAS
+    std::vector<char> batched(nf, 0);
+    std::vector<int> level_first(maxdepth + 2, -1), level_count(maxdepth + 2, 0);
+    bool batch_on = !stream;
+    if (const char* e = std::getenv("PDG_ND_FACTOR_BATCH")) batch_on = batch_on && std::atoi(e) != 0;
+    for (int k = 0; k < nf; ++k) {
+        const int d = fronts[k].depth;
+        if (level_first[d] < 0) level_first[d] = k;
+        ++level_count[d];
+    }
+    DBuf<NdFactorDesc> d_descs;
+    if (batch_on) {
+        std::vector<NdFactorDesc> descs;
+        std::vector<int> level_desc0(maxdepth + 2, 0);
+        for (int d = maxdepth; d >= 0; --d) {
+            level_desc0[d] = static_cast<int>(descs.size());
+            int fmax = 0;
+            for (int k = level_first[d]; k >= 0 && k < level_first[d] + level_count[d]; ++k)
+                fmax = std::max(fmax, fronts[k].s + fronts[k].b);
+            if (level_count[d] < 32 || fmax > 1536) continue;
+            for (int k = level_first[d]; k < level_first[d] + level_count[d]; ++k) {
+                require(fronts[k].depth == d, "nested dissection: fronts of a level are not contiguous");
+                NdFactorDesc D{};
+                D.fo = fo[k];
+                D.moff = fronts[k].moff;
+                D.mtoff = fronts[k].mtoff;
+                D.s = fronts[k].s;
+                D.b = fronts[k].b;
+                D.ldm = fronts[k].ldm;
+                D.ldt = fronts[k].ldt;
+                D.front = k;
+                D.nchild = 0;
+                for (int c : children[k]) {
+                    if (fronts[c].b == 0) continue;
+                    D.cfo[D.nchild] = fo[c];
+                    D.cmap[D.nchild] = mapoff[c];
+                    D.cs[D.nchild] = fronts[c].s;
+                    D.cb[D.nchild] = fronts[c].b;
+                    ++D.nchild;
+                }
+                descs.push_back(D);
+                batched[k] = 1;
+            }
+        }
+        d_descs.upload(descs, st);
+        // launches happen in the loop below, when the level's first front comes up
+        for (int d = 0; d <= maxdepth; ++d)
+            if (level_first[d] >= 0 && batched[level_first[d]]) level_first[d] = -2 - level_desc0[d];
+    }
     for (int k : porder) {
         const NdFront& F = fronts[k];
         const int s = F.s, b = F.b, f = s + b;
+        if (batched[k]) {
+            const int d = F.depth;
+            if (level_first[d] <= -2) {  // first front of a batched level: the whole level in one launch
+                const int d0 = -2 - level_first[d];
+                k_nd_factor_batch<<<level_count[d], kFactorThreads, 0, st>>>(d_descs.p + d0, dense.p, dmap.p, store.p, info.p);
+                PDG_CHECK_LAUNCH();
+                level_first[d] = -1;
+            }
+            continue;
+        }
         double* Fk = dense.p + fo[k];
         if (stream) {
             PDG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&Fk), sizeof(double) * (size_t)f * f, st));
