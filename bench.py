@@ -342,6 +342,12 @@ def config2_leg(n, steps, warmup, peak, local):
                      "alg_GB_per_call": round(per_call / 1e9, 3),
                      "achieved_GBs": round(per_call * real * steps / (v[0] * 1e-3) / 1e9, 1) if v[0] else 0.0}
     a = phases["a_solve"]
+    traffic = None
+    try:
+        if n == 32:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["a_solve_stream_config2"]["bytes"]
+    except Exception:
+        pass
     return {"workload": f"config2: 3D Biot {n}^3 hexahedra, dG(0), tau={tau}, GMRES(50) tol 1e-10, 1 fixed-stress sweep, "
                         "8 permeability layers (3D extension: the reference is 2D only, parity unpinned; checked "
                         "against the 3D CPU restatement at 4^3 and 6^3 and by the discrete mass balance here)",
@@ -355,7 +361,7 @@ def config2_leg(n, steps, warmup, peak, local):
                                                    "mode: one level kernel per depth and pass on the row-major factor)",
                          "achieved": a["achieved_GBs"], "peak": peak, "unit": "GB/s", "frac": a["achieved_GBs"] / peak,
                          "algorithmic_bytes_per_call": a["alg_GB_per_call"] * 1e9,
-                         "share_of_step": a["ms_per_step"] / ms if ms else None, "traffic": None},
+                         "share_of_step": a["ms_per_step"] / ms if ms else None, "traffic": traffic},
             "phases": phases,
             "setup": {"assemble_wall_s": round(t1 - t0, 3), "slab_solver_wall_s": round(t2 - t1, 3),
                       "a_nd_analysis_s": round(st[1], 3), "a_nd_factor_s": round(st[2], 3),
@@ -567,16 +573,34 @@ def main():
     ms_dev, e2e_ms, ms_ref = float(t[0]), float(t[1]), float(t[2])
 
     spmv_dist = solve_dist = None
+    hung = False
+
+    def guarded(fn, seconds, *a):
+        """Run a distributed leg in a worker thread: an exception or a stuck collective (this path
+        has only ever run on one GPU) must not lose the headline line. After a timeout no further
+        collective is issued and the process leaves through os._exit."""
+        import threading
+        box = {}
+
+        def work():
+            try:
+                torch.cuda.set_device(local)
+                box["out"] = fn(*a)
+            except Exception as e:  # report, do not lose the headline line
+                box["out"] = {"error": repr(e)[:300]}
+
+        th = threading.Thread(target=work, daemon=True)
+        th.start()
+        th.join(seconds)
+        if th.is_alive():
+            return {"error": f"no result within {seconds} s (distributed leg abandoned)"}, True
+        return box["out"], False
+
     if world > 1 and args.spmv_sizes:
-        try:
-            spmv_dist = spmv_distributed(int(args.spmv_sizes.split(",")[-1]), 20, peak, rank, world, torch.distributed)
-        except Exception as e:  # report, do not lose the headline line
-            spmv_dist = {"error": repr(e)[:300]}
-    if world > 1:
-        try:
-            solve_dist = solve_distributed(args.steps, args.warmup, rank, world, torch.distributed, local)
-        except Exception as e:
-            solve_dist = {"error": repr(e)[:300]}
+        spmv_dist, hung = guarded(spmv_distributed, 240, int(args.spmv_sizes.split(",")[-1]), 20, peak, rank, world,
+                                  torch.distributed)
+    if world > 1 and not hung:
+        solve_dist, hung = guarded(solve_distributed, 240, args.steps, args.warmup, rank, world, torch.distributed, local)
     # N > 1: the headline is the strong-scaled distributed solve (north_star); the replicas of
     # the 1-GPU march stay beside it (and are the fallback if the distributed leg failed)
     scaling, parallelism, value, e2e_line = "weak", "1 GPU", ms_dev, {
@@ -660,6 +684,9 @@ def main():
             "phases": phases_compact, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist,
             "config2": cfg2}), flush=True)
     if world > 1:
+        if hung:
+            sys.stdout.flush()
+            os._exit(0)
         torch.distributed.destroy_process_group()
 
 
