@@ -27,7 +27,11 @@
  *       SparseMatrix::apply (sparse.hpp:30-40), order-fixed (bit-identical)
  *
  * Conventions: plain pointers and sizes, caller-owned HOST buffers (copied
- * inside the call) unless a function name ends in _device. Every function
+ * inside the call) unless a function name ends in _device. _device functions
+ * run on the context's own non-blocking stream, which no other stream orders:
+ * their device inputs must be complete when the call is made (synchronize the
+ * stream that produced them), and their outputs are complete when it returns.
+ * Every function
  * returns a pdg_status; the message of the last failure on the calling
  * thread is pdg_last_error(). Handles are not thread-safe; destroy order is
  * block/slab -> ops -> ctx.

@@ -750,6 +750,7 @@ def test_spmv_config3_1024_properties(monkeypatch):
     for rows in ("1", "2"):
         monkeypatch.setenv("PDG_SPMV_ROWS", rows)
         y3.fill_(1.0)
+        torch.cuda.synchronize()  # torch's stream and the library's do not order each other
         op_sell.apply_device(x.data_ptr(), y3.data_ptr())
         torch.cuda.synchronize()
         assert torch.equal(y1, y3)
@@ -757,10 +758,12 @@ def test_spmv_config3_1024_properties(monkeypatch):
     monkeypatch.delenv("PDG_SPMV_ROWS")
     monkeypatch.delenv("PDG_SPMV_FORMAT")
     x2 = 2.0 * x
+    torch.cuda.synchronize()
     op.apply_device(x2.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
     assert torch.equal(y2, 2.0 * y1)
     x.zero_()
+    torch.cuda.synchronize()
     op.apply_device(x.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
     assert not torch.any(y2 != 0)
