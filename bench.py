@@ -264,19 +264,19 @@ def solve_distributed(steps, warmup, rank, world, dist, local):
                     "device time per solve (CUDA events on the library stream), max over ranks"}
 
 
-def config2_leg(n, steps, warmup, peak, local):
+def config2_leg(n, steps, warmup, peak, local, which="config2"):
     """BASELINE config 2 (3D extension, no reference counterpart): n^3 hexahedra, dG(0), 10 slabs of
     T = 1, layered permeability; device-resident march, CUDA events, then a profiled pass for the
     per-phase roofline. The inner solves run in the nested-dissection streaming mode (nd_stream.cu)."""
     import torch
     from paper_1801_04984_b200 import _lib, problem as P, solver as S
     L = _lib.lib()
-    run = P.RUNS["config2"]
+    run = P.RUNS[which]
     tau = run["T"] / run["n_slabs"]
     dev = torch.device("cuda", local)
     L.pdg_setup_reset()
     t0 = time.perf_counter()
-    ops = S.SpatialOperators.assemble(P.config2(n), device=local)
+    ops = S.SpatialOperators.assemble(P.config2(n) if which == "config2" else P.config4(n), device=local)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     opt = S.SolveOptions(gmres=S.GmresOptions(tol=run["tol"], restart=run["restart"]), candidate="flexible")
@@ -287,9 +287,10 @@ def config2_leg(n, steps, warmup, peak, local):
     L.pdg_setup_read(st, 9)
     free, total = torch.cuda.mem_get_info(local)
     nt = ops.n_total
+    nn = run["r"] + 1
     u_prev = torch.zeros(ops.n_u, dtype=torch.float64, device=dev)
     p_prev = torch.zeros(ops.n_p, dtype=torch.float64, device=dev)
-    rhs = torch.empty(nt, dtype=torch.float64, device=dev)
+    rhs = torch.empty(nn * nt, dtype=torch.float64, device=dev)
     out = torch.empty_like(rhs)
     res = torch.empty(ops.n_p, dtype=torch.float64, device=dev)
 
@@ -298,8 +299,9 @@ def config2_leg(n, steps, warmup, peak, local):
         torch.cuda.synchronize()
         slab.rhs_device(a, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=b - a)
         rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
-        u_prev.copy_(out[:ops.n_u])
-        p_prev.copy_(out[ops.n_u + ops.n_q:])
+        end = out[run["r"] * nt:(run["r"] + 1) * nt]
+        u_prev.copy_(end[:ops.n_u])
+        p_prev.copy_(end[ops.n_u + ops.n_q:])
         return rep
 
     for k in range(warmup):
@@ -319,7 +321,7 @@ def config2_leg(n, steps, warmup, peak, local):
     mass = float(res.max().item()) / scale if scale > 0 else 0.0
     # e2e through pdg_slab_solve with pinned host buffers
     rhs_h = rhs.cpu().pin_memory().numpy()
-    out_h = torch.empty(nt, dtype=torch.float64).pin_memory().numpy()
+    out_h = torch.empty(nn * nt, dtype=torch.float64).pin_memory().numpy()
     e2e = []
     for _ in range(3):
         t = time.perf_counter()
@@ -344,16 +346,19 @@ def config2_leg(n, steps, warmup, peak, local):
     a = phases["a_solve"]
     traffic = None
     try:
-        if n == 32:
+        if n == 32 and which == "config2":
             traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["a_solve_stream_config2"]["bytes"]
     except Exception:
         pass
-    return {"workload": f"config2: 3D Biot {n}^3 hexahedra, dG(0), tau={tau}, GMRES(50) tol 1e-10, 1 fixed-stress sweep, "
-                        "8 permeability layers (3D extension: the reference is 2D only, parity unpinned; checked "
+    what = ("8 permeability layers" if which == "config2" else
+            "i.i.d. lognormal permeability (sigma 1.5); BASELINE config 4 at a REDUCED size: the exact "
+            "preconditioner does not exist at 96^3 (DESIGN.md section 8)")
+    return {"workload": f"{which}: 3D Biot {n}^3 hexahedra, dG({run['r']}), tau={tau}, GMRES(50) tol 1e-10, 1 fixed-stress sweep, "
+                        f"{what} (3D extension: the reference is 2D only, parity unpinned; checked "
                         "against the 3D CPU restatement at 4^3 and 6^3 and by the discrete mass balance here)",
             "value": ms, "unit": "ms/slab", "steps": steps, "warmup": warmup,
-            "e2e": {"value": float(np.mean(e2e[1:])), "unit": "ms/slab", "h2d_bytes_per_step": 8 * nt,
-                    "d2h_bytes_per_step": 8 * nt},
+            "e2e": {"value": float(np.mean(e2e[1:])), "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
+                    "d2h_bytes_per_step": 8 * nn * nt},
             "iterations": [r.iterations for r in reps], "final_rel_res_max": max(r.final_relative_residual for r in reps),
             "mass_balance_rel": mass, "gpu_launches": int(launches),
             "sizes": {"n_u": ops.n_u, "n_q": ops.n_q, "n_p": ops.n_p, "nnz_A": ops.nnz["A"]},
@@ -408,6 +413,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-slabs", type=int, default=2)
     ap.add_argument("--config2-n", type=int, default=32, help="cells per edge of the 3D config-2 leg (0: skip)")
+    ap.add_argument("--config4-n", type=int, default=24, help="cells per edge of the reduced 3D dG(1) config-4 leg (0: skip)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -660,6 +666,13 @@ def main():
                 cfg2["cpu_baseline_small"] = config2_cpu_small(12, local)
             except Exception as e:
                 cfg2["cpu_baseline_small"] = {"error": repr(e)[:300]}
+    cfg4 = None
+    if rank == 0 and world == 1 and args.config4_n > 0:
+        try:
+            cfg4 = config2_leg(args.config4_n, 8, 1, peak, local, which="config4")
+            cfg4.pop("cpu_baseline_note", None)
+        except Exception as e:
+            cfg4 = {"error": repr(e)[:300]}
     if rank == 0:
         spmv_compact = [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in d.items()
                          if k in ("n", "rows", "nnz", "median_ms", "gdof_s", "achieved_GBs", "frac")} for d in spmv]
@@ -682,7 +695,7 @@ def main():
             "roofline": roofline, "clocks": main_run["clocks"], "cpu_baseline": cpu, "setup": setup,
             "spmv_roofline": spmv_roof, "spmv": spmv_compact, "spmv_cpu_baseline": spmv_cpu,
             "phases": phases_compact, "spmv_distributed": spmv_dist, "solve_distributed": solve_dist,
-            "config2": cfg2}), flush=True)
+            "config2": cfg2, "config4_reduced": cfg4}), flush=True)
     if world > 1:
         if hung:
             sys.stdout.flush()
