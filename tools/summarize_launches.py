@@ -6,7 +6,7 @@ import re
 import sys
 
 SETUP = re.compile(r"cusolver|cublas|potrf|trsm|syrk|gemm|getrf|Kernel<|k_nd_pack|k_nd_extend_add|k_nd_identity|"
-                   r"k_nd_scatter|k_assemble|k_row_lengths|k_cell|k_face|k_csr|DeviceScan|DeviceRadix|DeviceReduce|"
+                   r"k_nd_scatter|k_nd_tile_pack|trtri|copy_info|k_nd_factor_batch|k_nd_top_scatter|k_nd_top_sym|k_uk_|k_pk_|k_qk_|k_slice_max|k_assemble|k_row_lengths|k_cell|k_face|k_csr|DeviceScan|DeviceRadix|DeviceReduce|"
                    r"k_u_count|k_u_fill|k_s_len|k_s_slice_width|k_s_fill|k_flux|k_qc|k_mp|k_dinv|k_flow_schur|"
                    r"elementwise|at::|xxtrf|trsv|k_sort_rows|k_count_cols|k_blk|k_fill|k_step|k_sweep_setup|k_pack|k_transpose|k_copy_tri|k_scatter",
                    re.I)
