@@ -67,6 +67,35 @@ def test_device_assembly3_bit_identical(oracle, spec):
     assert np.array_equal(u, gu) and np.array_equal(q, gq) and np.array_equal(p, gp)
 
 
+def test_device_assembly3_random_specs(oracle):
+    """Seeded random 3D problems (mesh dimensions 1..4 per axis incl. single-cell directions, edge
+    lengths, Lame parameters, penalty, per-cell permeability, every displacement / flow boundary
+    kind with nonzero data): operators and right-hand side bit-identical to the CPU restatement."""
+    rng = np.random.default_rng(20240611)
+    kinds = ["fixed", "traction", "roller_x", "roller_y", "roller_z"]
+    for case in range(12):
+        nx, ny, nz = (int(v) for v in rng.integers(1, 5, 3))
+        spec = P.config2(1)
+        spec.nx, spec.ny, spec.nz = nx, ny, nz
+        spec.lx, spec.ly, spec.lz = (float(v) for v in rng.uniform(0.5, 2.0, 3))
+        spec.lam, spec.mu = float(rng.uniform(0.5, 5e3)), float(rng.uniform(0.5, 4e3))
+        spec.penalty = float(rng.uniform(5.0, 40.0))
+        spec.eta, spec.biot_m, spec.biot_b = float(rng.uniform(0.5, 2)), float(rng.uniform(1, 1e3)), float(rng.uniform(0.3, 1))
+        spec.k_perm = float(rng.uniform(0.1, 3.0))
+        spec.k_perm_cells = rng.lognormal(0.0, 1.0, nx * ny * nz) if case % 3 else None
+        spec.disp = {t: (kinds[int(rng.integers(0, 5))], tuple(float(v) for v in rng.uniform(-1, 1, 3))) for t in P.TAGS3}
+        spec.flow = {t: (("pressure", float(rng.uniform(-1, 1))) if rng.random() < 0.6 else ("no_flow", 0.0))
+                     for t in P.TAGS3}
+        rp = oracle.RefProblem(spec.to_dict())
+        ops = S.SpatialOperators.assemble(spec)
+        for name in ("A", "M_q", "B", "E"):
+            ro, ri, rv = rp.csr(name)
+            go, gi, gv = ops.download(name)
+            assert np.array_equal(ro, go) and np.array_equal(ri, gi) and np.array_equal(rv, gv), (case, name)
+        for a, b in zip(rp.assemble_rhs(0.1), ops.rhs(0.1)):
+            assert np.array_equal(a, b), case
+
+
 @pytest.mark.parametrize("r", [0, 1])
 def test_spacetime_operator3_bit_identical(oracle, r):
     """Canonical space-time CSR of the 3D operators and its order-fixed SpMV == the oracle's

@@ -57,6 +57,33 @@ def test_device_assembly_bit_identical(oracle, spec):
     assert np.array_equal(u, gu) and np.array_equal(q, gq) and np.array_equal(p, gp)
 
 
+def test_device_assembly_random_specs(oracle):
+    """Seeded random 2D problems (mesh dimensions 1..7, edge lengths, material, penalty, per-cell
+    permeability, every boundary kind with nonzero data): bit-identical operators and rhs."""
+    rng = np.random.default_rng(1801)
+    kinds = ["fixed", "traction", "roller_x", "roller_y"]
+    for case in range(16):
+        spec = P.config0()
+        spec.nx, spec.ny = (int(v) for v in rng.integers(1, 8, 2))
+        spec.lx, spec.ly = (float(v) for v in rng.uniform(0.5, 2.0, 2))
+        spec.lam, spec.mu = float(rng.uniform(0.5, 5e3)), float(rng.uniform(0.5, 4e3))
+        spec.penalty = float(rng.uniform(5.0, 40.0))
+        spec.eta, spec.biot_m, spec.biot_b = float(rng.uniform(0.5, 2)), float(rng.uniform(1, 1e3)), float(rng.uniform(0.3, 1))
+        spec.k_perm = float(rng.uniform(0.1, 3.0))
+        spec.k_perm_cells = rng.lognormal(0.0, 1.0, spec.nx * spec.ny) if case % 3 else None
+        spec.disp = {t: (kinds[int(rng.integers(0, 4))], tuple(float(v) for v in rng.uniform(-1, 1, 2))) for t in P.TAGS}
+        spec.flow = {t: (("pressure", float(rng.uniform(-1, 1))) if rng.random() < 0.6 else ("no_flow", 0.0))
+                     for t in P.TAGS}
+        rp = oracle.RefProblem(spec.to_dict())
+        ops = S.SpatialOperators.assemble(spec)
+        for name in ("A", "M_q", "B", "E"):
+            ro, ri, rv = rp.csr(name)
+            go, gi, gv = ops.download(name)
+            assert np.array_equal(ro, go) and np.array_equal(ri, gi) and np.array_equal(rv, gv), (case, name)
+        for a, b in zip(rp.assemble_rhs(0.1), ops.rhs(0.1)):
+            assert np.array_equal(a, b), case
+
+
 def _upload_from_oracle(rp, spec):
     m = rp.misc()
     blocks = {k: rp.csr(k) for k in ("A", "M_q", "B", "E")}
