@@ -48,7 +48,7 @@ struct StreamArgs {
 // RPW rows per warp: a unit has up to 8 * RPW rows (64 by default; 32 or 16 on levels with few
 // units, where more CTAs keep more bytes in flight)
 template <int NR, int RPW>
-__global__ void __launch_bounds__(kSThreads) k_nd_stream(StreamArgs a, int u0) {
+__global__ void __launch_bounds__(kSThreads, 4) k_nd_stream(StreamArgs a, int u0) {
     if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
     __shared__ double vs[NR][kSTile];
     __shared__ NdStreamUnit Us;
