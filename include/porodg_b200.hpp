@@ -94,6 +94,8 @@ public:
     }
     // Assemble on the device from a structured-mesh problem description.
     SpatialOperators(Context& ctx, const pdg_problem& p) { check(pdg_ops_assemble(ctx.get(), &p, &h_)); }
+    // 3D extension (BASELINE config 2; no reference counterpart): nx x ny x nz hexahedra.
+    SpatialOperators(Context& ctx, const pdg_problem3& p) { check(pdg_ops_assemble3(ctx.get(), &p, &h_)); }
     ~SpatialOperators() { pdg_ops_destroy(h_); }
     SpatialOperators(const SpatialOperators&) = delete;
     SpatialOperators& operator=(const SpatialOperators&) = delete;

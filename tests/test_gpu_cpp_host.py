@@ -32,6 +32,29 @@ def test_cpp_host_layer_solves_config0_slab(tmp_path):
     assert worst < 1e-8
 
 
+def _build3d(tmp_path):
+    exe = str(tmp_path / "slab_solve3d")
+    lib = os.path.join(ROOT, "paper_1801_04984_b200", "_lib")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "slab_solve3d.cpp"), "-L", lib, "-lporodg_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_host_layer_3d_compiles_and_links(tmp_path):
+    assert os.path.exists(_build3d(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_host_layer_solves_3d_slab(tmp_path):
+    """examples/slab_solve3d.cpp: pdg_ops_assemble3 + SlabSolver through the C++ layer (config-2 type, 8^3)."""
+    out = subprocess.run([_build3d(tmp_path), "8"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "iterations=4" in out.stdout
+    assert float(out.stdout.split("max|res|/scale=")[1].split()[0]) < 1e-8
+    assert float(out.stdout.split("min u_z=")[1].split()[0]) < 0.0
+
+
 def _build_adapter(tmp_path):
     exe = str(tmp_path / "adapter_main")
     lib = os.path.join(ROOT, "paper_1801_04984_b200", "_lib")
