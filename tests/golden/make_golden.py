@@ -10,6 +10,12 @@ config1_k_perm.npy         -- per-cell permeability of config 1 (seed 1801),
 config0_oracle.npz         -- oracle march of config 0 (dense inner solves):
                               iterations, final residuals, all slab states.
 terzaghi_oracle.npz        -- oracle march of the recorded Terzaghi run.
+config2_small_oracle.npz   -- 3D extension (no reference counterpart; oracle/refcpu/fem3d.hpp):
+                              oracle march of config 2 at 4^3 (3 slabs) with the sums of the
+                              operator values and of the right-hand side, pinning the 3D
+                              restatement against accidental edits.
+highorder_oracle.npz       -- oracle marches of config 0 at 6^2 with dG(2) and dG(3)
+                              (multi-block Schur back-substitution): iterations and states.
 """
 import csv
 import json
@@ -46,6 +52,25 @@ def main():
                        keep_states=True)
         np.savez_compressed(os.path.join(HERE, f"{name}_oracle.npz"), iterations=res["iterations"],
                             final_res=res["final_res"], states=res["states"])
+
+
+    spec = P.config2(4)
+    rp = refcpu.RefProblem(spec.to_dict())
+    res = rp.march(0, 0.3, 3, tol=1e-10, restart=50, backend=0, keep_states=True)
+    sums = {nm: np.array([rp.csr(nm)[2].sum(), np.abs(rp.csr(nm)[2]).sum()]) for nm in ("A", "M_q", "B", "E")}
+    ru, rq, rpp = rp.assemble_rhs(0.0)
+    np.savez_compressed(os.path.join(HERE, "config2_small_oracle.npz"), iterations=res["iterations"],
+                        final_res=res["final_res"], states=res["states"], k_perm=spec.k_perm_cells,
+                        rhs_sums=np.array([ru.sum(), rq.sum(), rpp.sum()]), **{f"sum_{k}": v for k, v in sums.items()})
+    spec = P.config0()
+    spec.nx = spec.ny = 6
+    rp = refcpu.RefProblem(spec.to_dict())
+    out = {}
+    for r in (2, 3):
+        res = rp.march(r, 0.3, 2, tol=1e-10, restart=50, backend=0, keep_states=True)
+        out[f"iterations_r{r}"] = res["iterations"]
+        out[f"states_r{r}"] = res["states"]
+    np.savez_compressed(os.path.join(HERE, "highorder_oracle.npz"), **out)
 
 
 if __name__ == "__main__":

@@ -309,3 +309,28 @@ def test_config2_full_size_32cubed():
     op.apply_device(x2.data_ptr(), y2.data_ptr())
     torch.cuda.synchronize()
     assert torch.equal(y2, 2.0 * y)
+
+
+def test_gpu_against_committed_golden_vectors():
+    """The GPU march against the committed fixtures (no oracle call): config 2 at 4^3
+    (tests/golden/config2_small_oracle.npz) and dG(2) / dG(3) at 6^2 (highorder_oracle.npz)."""
+    import os
+    golden = os.path.join(os.path.dirname(__file__), "golden")
+    g = np.load(os.path.join(golden, "config2_small_oracle.npz"))
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50))
+    ops = S.SpatialOperators.assemble(P.config2(4))
+    reps, states = S.march(ops, 0, 0.3, 3, opt, keep_states=True)
+    for s in range(3):
+        assert abs(reps[s].iterations - int(g["iterations"][s])) <= 1
+        ref = g["states"][s].ravel()
+        assert np.linalg.norm(states[s] - ref) <= SOLVE_RTOL * np.linalg.norm(ref)
+    h = np.load(os.path.join(golden, "highorder_oracle.npz"))
+    spec = P.config0()
+    spec.nx = spec.ny = 6
+    ops2 = S.SpatialOperators.assemble(spec)
+    for r in (2, 3):
+        reps, states = S.march(ops2, r, 0.3, 2, opt, keep_states=True)
+        for s in range(2):
+            assert abs(reps[s].iterations - int(h[f"iterations_r{r}"][s])) <= 1
+            ref = h[f"states_r{r}"][s].ravel()
+            assert np.linalg.norm(states[s] - ref) <= SOLVE_RTOL * np.linalg.norm(ref)

@@ -201,3 +201,23 @@ def test_config2_type_march_converges_and_conserves_mass():
     # the column settles: top displacement is downwards, pressure positive below the drained top
     uz_top = a["states"][-1][-1][:rp.n_u].reshape(-1, 8, 3)[-16:, 4:, 2]
     assert (uz_top < 0).all()
+
+
+def test_config2_small_golden():
+    """The committed fixture tests/golden/config2_small_oracle.npz (tests/golden/make_golden.py): the
+    3D restatement reproduces its recorded operator sums, right-hand side, iteration counts and slab
+    states for config 2 at 4^3, so an accidental edit of fem3d.hpp shows up here."""
+    import os
+    from paper_1801_04984_b200 import problem as P
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "config2_small_oracle.npz"))
+    spec = P.config2(4)
+    assert np.array_equal(spec.k_perm_cells, g["k_perm"])
+    rp = refcpu.RefProblem(spec.to_dict())
+    for nm in ("A", "M_q", "B", "E"):
+        v = rp.csr(nm)[2]
+        assert np.allclose([v.sum(), np.abs(v).sum()], g[f"sum_{nm}"], rtol=1e-13, atol=1e-9)
+    ru, rq, rpp = rp.assemble_rhs(0.0)
+    assert np.allclose([ru.sum(), rq.sum(), rpp.sum()], g["rhs_sums"], rtol=1e-13, atol=1e-15)
+    res = rp.march(0, 0.3, 3, tol=1e-10, restart=50, backend=0, keep_states=True)
+    assert np.array_equal(res["iterations"], g["iterations"])
+    assert np.allclose(res["states"], g["states"], rtol=1e-11, atol=1e-16)

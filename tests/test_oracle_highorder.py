@@ -99,3 +99,18 @@ def test_spectral_slab_solve_matches_monolithic(r):
     x0 = spla.spsolve(full, R0)
     res = rp.march(r, tau, 1, tol=1e-12, restart=100, backend=0, keep_states=True)
     assert np.linalg.norm(res["states"][0].ravel() - x0) <= 1e-9 * np.linalg.norm(x0)
+
+
+def test_highorder_golden():
+    """tests/golden/highorder_oracle.npz: dG(2) / dG(3) marches of config 0 at 6^2 (the raw Schur form
+    comes from the local LAPACK, so states are compared to roundoff, not bitwise)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "highorder_oracle.npz"))
+    spec = P.config0()
+    spec.nx = spec.ny = 6
+    rp = refcpu.RefProblem(spec.to_dict())
+    for r in (2, 3):
+        res = rp.march(r, 0.3, 2, tol=1e-10, restart=50, backend=0, keep_states=True)
+        assert np.array_equal(res["iterations"], g[f"iterations_r{r}"])
+        ref = g[f"states_r{r}"]
+        assert np.linalg.norm(res["states"] - ref) <= 1e-9 * np.linalg.norm(ref)
