@@ -157,7 +157,11 @@ int pdg_ops_rhs(const pdg_ops* ops, double t, double* u, double* q, double* p);
  * (bottom row, top row, left column, right column: 2 nx + 2 ny faces), the 6 Gauss points
  * x0 + g_k (x1 - x0). momentum / darcy / mass may be NULL (absent field, assembly.hpp:485);
  * traction / dirichlet / flow hold eval_or_zero of the face's traction_data, dirichlet_data and
- * flow data (prescribed pressure, or prescribed normal flux on no-flow-kind faces). 2D only. */
+ * flow data (prescribed pressure, or prescribed normal flux on no-flow-kind faces).
+ * 3D operators (pdg_ops_assemble3): the same call with 6 x 6 x 6 points per cell, index
+ * c*216 + (i*6 + j)*6 + k, vectors of 3 components ([n_cells][216][3], mass [n_cells][216]), and
+ * 6 x 6 points per boundary face in ascending face index (first tangential axis outer):
+ * [n_bfaces][36][3], flow [n_bfaces][36], n_bfaces = 2 (nx ny + nx nz + ny nz). */
 typedef struct {
     const double* momentum;  /* [n_cells][36][2] */
     const double* darcy;     /* [n_cells][36][2] */
@@ -166,7 +170,8 @@ typedef struct {
     const double* dirichlet; /* [n_bfaces][6][2] */
     const double* flow;      /* [n_bfaces][6] */
 } pdg_rhs_samples;
-/* cell_xy [n_cells][36][2], bface_ids [2 nx + 2 ny], bface_xy [n_bfaces][6][2] (any may be NULL) */
+/* cell_xy [n_cells][36][2], bface_ids [2 nx + 2 ny], bface_xy [n_bfaces][6][2] (any may be NULL);
+ * 3D: [n_cells][216][3], [n_bfaces], [n_bfaces][36][3] */
 int pdg_rhs_sample_points(const pdg_ops* ops, double* cell_xy, int* bface_ids, double* bface_xy);
 int pdg_ops_rhs_sampled(const pdg_ops* ops, const pdg_rhs_samples* samples, double* u, double* q, double* p);
 void pdg_ops_destroy(pdg_ops* ops);

@@ -166,6 +166,23 @@ class RefProblem:
                 out[name] = None
         return out
 
+    def sample_points3(self):
+        """3D: the quadrature points of assemble_rhs3_sampled: cells (n_cells, 216, 3), boundary
+        face ids, face points (n_bfaces, 36, 3)."""
+        nx, ny, nz = self.spec["nx"], self.spec["ny"], self.spec["nz"]
+        nb = 2 * (nx * ny + nx * nz + ny * nz)
+        cxyz, ids, fxyz = np.empty((self.n_p, 216, 3)), np.empty(nb, np.int32), np.empty((nb, 36, 3))
+        _check(lib().refcpu_rhs3_sample_points(self._h, _dp(cxyz), _ip(ids), _dp(fxyz)))
+        return cxyz, ids, fxyz
+
+    def rhs3_sampled(self, traction, dirichlet, flow, momentum=None, darcy=None, mass=None):
+        """3D assemble_rhs with sampled volume sources and boundary data (fem3d.hpp)."""
+        arrs = [None if a is None else np.ascontiguousarray(a, np.float64) for a in (momentum, darcy, mass, traction,
+                                                                                      dirichlet, flow)]
+        u, q, p = np.empty(self.n_u), np.empty(self.n_q), np.empty(self.n_p)
+        _check(lib().refcpu_rhs3_sampled(self._h, *[None if a is None else _dp(a) for a in arrs], _dp(u), _dp(q), _dp(p)))
+        return u, q, p
+
     def spacetime_csr(self, theta, tau):
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         m = theta.shape[0]

@@ -233,6 +233,33 @@ int refcpu_sample_rhs_data(void* hp, double t, double* momentum, double* darcy, 
     GUARD_END
 }
 
+// 3D: assemble_rhs3_sampled and its sample points (fem3d.hpp). n_bfaces = 2 (nx ny + nx nz + ny nz).
+int refcpu_rhs3_sample_points(void* hp, double* cell_xyz, int* bface_ids, double* bface_xyz) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    if (h->dim != 3) throw std::invalid_argument("rhs3 sample points: 3D only");
+    rhs3_sample_points(h->mesh3, cell_xyz, bface_ids, bface_xyz);
+    GUARD_END
+}
+int refcpu_rhs3_sampled(void* hp, const double* momentum, const double* darcy, const double* mass, const double* traction,
+                        const double* dirichlet, const double* flow, double* u, double* q, double* p) {
+    GUARD_BEGIN
+    auto* h = static_cast<Handle*>(hp);
+    if (h->dim != 3) throw std::invalid_argument("rhs3 sampled: 3D only");
+    RhsSamples3 sm;
+    sm.momentum = momentum;
+    sm.darcy = darcy;
+    sm.mass = mass;
+    sm.traction = traction;
+    sm.dirichlet = dirichlet;
+    sm.flow = flow;
+    const FieldVecs r = assemble_rhs3_sampled(h->mesh3, h->ops.mat, h->ops, h->bc3, sm);
+    std::memcpy(u, r.u.data(), sizeof(double) * r.u.size());
+    std::memcpy(q, r.q.data(), sizeof(double) * r.q.size());
+    std::memcpy(p, r.p.data(), sizeof(double) * r.p.size());
+    GUARD_END
+}
+
 void refcpu_destroy(void* h) { delete static_cast<Handle*>(h); }
 
 // sizes[0..] = n_u, n_q, n_p, nnz(A), nnz(M_q), nnz(B), nnz(E), nnz(M_p)

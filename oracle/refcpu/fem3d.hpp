@@ -481,4 +481,133 @@ inline FieldVecs assemble_rhs3(const Mesh3& mesh, const MaterialParameters& mat,
     return r;
 }
 
+// assemble_rhs3 with sampled data: the 3D analogue of assembly.hpp:467-563 in full (volume
+// sources and space- / time-dependent boundary data), the fields given at the quadrature points
+// (6 x 6 x 6 Gauss per cell, xi outermost; 6 x 6 per boundary face in ascending face index, first
+// tangential axis outer). null = absent field (the volume loop is skipped as in the reference).
+struct RhsSamples3 {
+    const double* momentum = nullptr;   // [cell][216][3]
+    const double* darcy = nullptr;      // [cell][216][3]
+    const double* mass = nullptr;       // [cell][216]
+    const double* traction = nullptr;   // [bface][36][3]
+    const double* dirichlet = nullptr;  // [bface][36][3]
+    const double* flow = nullptr;       // [bface][36]  prescribed pressure, or normal flux on no-flow-kind faces
+};
+inline FieldVecs assemble_rhs3_sampled(const Mesh3& mesh, const MaterialParameters& mat, const SpatialOperators& ops,
+                                       const BoundarySpec3& bc, const RhsSamples3& sm) {
+    FieldVecs r;
+    r.u.assign(ops.n_u, 0.0);
+    r.q.assign(ops.n_q, 0.0);
+    r.p.assign(ops.n_p, 0.0);
+    const QuadratureRule gq = gauss_legendre(kDataQuadOrder);
+    if (sm.momentum || sm.darcy || sm.mass) {
+        for (int c = 0; c < mesh.n_cells(); ++c) {
+            const Cell3& cell = mesh.cells[c];
+            const double vol = cell.volume();
+            const auto cf = mesh.cell_faces(c);
+            std::array<double, 6> sgn{};
+            for (int k = 0; k < 6; ++k) {
+                const Face3& f = mesh.faces[cf[k]];
+                sgn[k] = f.n[f.axis];
+            }
+            for (size_t i = 0; i < 6; ++i)
+                for (size_t j = 0; j < 6; ++j)
+                    for (size_t k = 0; k < 6; ++k) {
+                        const double ref[3] = {gq.points[i], gq.points[j], gq.points[k]};
+                        const double w = gq.weights[i] * gq.weights[j] * gq.weights[k] * vol;
+                        const size_t sp = static_cast<size_t>(c) * 216 + (i * 6 + j) * 6 + k;
+                        if (sm.momentum)
+                            for (int a = 0; a < 8; ++a) {
+                                const double nv = shapes3::n(a, ref[0], ref[1], ref[2]);
+                                for (int comp = 0; comp < 3; ++comp)
+                                    r.u[24 * c + 3 * a + comp] += w * nv * sm.momentum[3 * sp + comp];
+                            }
+                        if (sm.darcy)
+                            for (int axis = 0; axis < 3; ++axis) {
+                                const int flo = cf[2 * axis], fhi = cf[2 * axis + 1];
+                                const double wl = sgn[2 * axis] * (1.0 - ref[axis]), wh = sgn[2 * axis + 1] * ref[axis];
+                                if (!ops.q_constrained[flo]) r.q[flo] += w * wl * sm.darcy[3 * sp + axis];
+                                if (!ops.q_constrained[fhi]) r.q[fhi] += w * wh * sm.darcy[3 * sp + axis];
+                            }
+                        if (sm.mass) r.p[c] -= w * sm.mass[sp];
+                    }
+        }
+    }
+    Vec q_values(ops.n_q, 0.0);
+    size_t bf = 0;
+    for (int f = 0; f < mesh.n_faces(); ++f) {
+        const Face3& face = mesh.faces[f];
+        if (!face.is_boundary()) continue;
+        const int c = face.cell_minus;
+        const Cell3& cell = mesh.cells[c];
+        const DisplacementBC3& dbc = bc.displacement[face.tag - 1];
+        const FlowBC3& fbc = bc.flow[face.tag - 1];
+        const double gamma_f = sipg_face_coefficient3(mesh, mat, ops.penalty, f);
+        for (size_t qa = 0; qa < 6; ++qa)
+            for (size_t qb = 0; qb < 6; ++qb) {
+                const double w = gq.weights[qa] * gq.weights[qb] * face.measure;
+                const auto rp = face_ref_point3(mesh, f, c, gq.points[qa], gq.points[qb]);
+                const size_t sp = bf * 36 + qa * 6 + qb;
+                const std::array<double, 3> tn = {sm.traction[3 * sp], sm.traction[3 * sp + 1], sm.traction[3 * sp + 2]};
+                const std::array<double, 3> mud = {dbc.dirichlet[0] ? sm.dirichlet[3 * sp] : 0.0,
+                                                   dbc.dirichlet[1] ? sm.dirichlet[3 * sp + 1] : 0.0,
+                                                   dbc.dirichlet[2] ? sm.dirichlet[3 * sp + 2] : 0.0};
+                for (int l = 0; l < 24; ++l) {
+                    const int a = l / 3, comp = l % 3;
+                    const double nv = shapes3::n(a, rp[0], rp[1], rp[2]);
+                    const int gi = 24 * c + l;
+                    if (!dbc.dirichlet[comp]) r.u[gi] += w * nv * tn[comp];
+                    if (dbc.dirichlet[comp]) r.u[gi] += w * gamma_f * nv * mud[comp];
+                    const auto tv = shapes3::traction(cell, mat, a, comp, rp[0], rp[1], rp[2], face.n);
+                    r.u[gi] -= w * dot3(tv, mud);
+                }
+                if (!fbc.no_flow)
+                    r.q[f] -= w * sm.flow[sp];
+                else
+                    q_values[f] += w / face.measure * sm.flow[sp];
+            }
+        if (fbc.no_flow) r.q[f] = q_values[f];
+        ++bf;
+    }
+    for (const Triplet& tr : ops.mq_bc) r.q[tr.row] -= tr.value * q_values[tr.col];
+    for (const Triplet& tr : ops.b_bc) r.p[tr.col] -= tr.value * q_values[tr.row];
+    for (int i = 0; i < ops.n_u; ++i) r.u[i] += ops.rhs_ref_u[i];
+    return r;
+}
+
+// the sample points of assemble_rhs3_sampled
+inline void rhs3_sample_points(const Mesh3& mesh, double* cell_xyz, int* bface_ids, double* bface_xyz) {
+    const QuadratureRule gq = gauss_legendre(kDataQuadOrder);
+    if (cell_xyz)
+        for (int c = 0; c < mesh.n_cells(); ++c) {
+            const Cell3& cell = mesh.cells[c];
+            for (size_t i = 0; i < 6; ++i)
+                for (size_t j = 0; j < 6; ++j)
+                    for (size_t k = 0; k < 6; ++k) {
+                        double* o = cell_xyz + (static_cast<size_t>(c) * 216 + (i * 6 + j) * 6 + k) * 3;
+                        o[0] = cell.x0 + gq.points[i] * cell.hx;
+                        o[1] = cell.y0 + gq.points[j] * cell.hy;
+                        o[2] = cell.z0 + gq.points[k] * cell.hz;
+                    }
+        }
+    size_t bf = 0;
+    for (int f = 0; f < mesh.n_faces(); ++f) {
+        const Face3& face = mesh.faces[f];
+        if (!face.is_boundary()) continue;
+        if (bface_ids) bface_ids[bf] = f;
+        if (bface_xyz) {
+            const Cell3& cell = mesh.cells[face.cell_minus];
+            for (size_t qa = 0; qa < 6; ++qa)
+                for (size_t qb = 0; qb < 6; ++qb) {
+                    const auto rp = face_ref_point3(mesh, f, face.cell_minus, gq.points[qa], gq.points[qb]);
+                    double* o = bface_xyz + (bf * 36 + qa * 6 + qb) * 3;
+                    o[0] = cell.x0 + rp[0] * cell.hx;
+                    o[1] = cell.y0 + rp[1] * cell.hy;
+                    o[2] = cell.z0 + rp[2] * cell.hz;
+                }
+        }
+        ++bf;
+    }
+}
+
 }  // namespace refcpu

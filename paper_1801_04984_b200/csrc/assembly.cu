@@ -838,7 +838,7 @@ void assemble_ops_device(SpatialOps& s, const pdg_problem& p, cudaStream_t st) {
 
 void assemble_rhs_sampled_device(const SpatialOps& s, const pdg_rhs_samples& h, double* u, double* q, double* p,
                                  cudaStream_t st) {
-    require(s.nz == 0, "pdg_ops_rhs_sampled: 2D meshes only");
+    if (s.nz > 0) return assemble_rhs_sampled_device3(s, h, u, q, p, st);
     require(h.traction && h.dirichlet && h.flow, "pdg_ops_rhs_sampled: boundary samples must be given");
     const Geo g = make_geo(s.prob);
     const size_t nc = (size_t)s.n_p, nbf = 2 * ((size_t)s.nx + s.ny);

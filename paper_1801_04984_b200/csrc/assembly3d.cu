@@ -580,6 +580,161 @@ __global__ void k_rhs_qp3(Geo3 g, int nq, int np, double* q, double* p) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) p[c] = 0.0;
 }
 
+// ---- assemble_rhs with sampled data in 3D (the 3D form of assembly.hpp:467-563 in full; the
+// oracle's assemble_rhs3_sampled): volume sources at the 6 x 6 x 6 Gauss points per cell (xi
+// outermost), boundary data at the 6 x 6 points per boundary face (ascending face index, first
+// tangential axis outer); accumulation order as in assembly.cu's 2D kernels.
+struct Samples3 {
+    const double* momentum;   // [cell][216][3] or null
+    const double* darcy;      // [cell][216][3] or null
+    const double* mass;       // [cell][216] or null
+    const double* traction;   // [bface][36][3]
+    const double* dirichlet;  // [bface][36][3]
+    const double* flow;       // [bface][36]
+};
+
+__device__ __forceinline__ int bface_index3(const Geo3& g, int f) {
+    const int nxy = g.nx * g.ny, nxz = g.nx * g.nz, nyz = g.ny * g.nz, a = nzf(g), b = nyf(g);
+    if (f < nxy) return f;
+    if (f < a) return nxy + (f - g.nz * nxy);
+    if (f < a + nxz) return 2 * nxy + (f - a);
+    if (f < a + b) return 2 * nxy + nxz + (f - a - g.ny * nxz);
+    if (f < a + b + nyz) return 2 * nxy + 2 * nxz + (f - a - b);
+    return 2 * nxy + 2 * nxz + nyz + (f - a - b - g.nx * nyz);
+}
+
+__global__ void k_rhs_u_s3(Geo3 g, Samples3 sm, double* u) {
+    const int n = g.nx * g.ny * g.nz;
+    const double vol = g.h[0] * g.h[1] * g.h[2];
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 24LL * n; t += (long long)gridDim.x * blockDim.x) {
+        const int c = static_cast<int>(t / 24), l = static_cast<int>(t % 24);
+        int cf[6];
+        cell_faces_asc(g, c, cf);
+        const int a = l / 3, comp = l % 3;
+        double r = 0.0;
+        if (sm.momentum)
+            for (int qi = 0; qi < 6; ++qi)
+                for (int qj = 0; qj < 6; ++qj)
+                    for (int qk = 0; qk < 6; ++qk) {
+                        const double ref[3] = {g.g6p[qi], g.g6p[qj], g.g6p[qk]};
+                        const double w = g.g6w[qi] * g.g6w[qj] * g.g6w[qk] * vol;
+                        r += w * shp(a, ref) * sm.momentum[((long long)c * 216 + (qi * 6 + qj) * 6 + qk) * 3 + comp];
+                    }
+        for (int q = 0; q < 6; ++q) {
+            const Face3 F = face_info(g, cf[q]);
+            if (!F.boundary) continue;
+            const int* dir = g.disp_dir[F.tag - 1];
+            const double gamma_f = sipg(g, F);
+            const long long bf = bface_index3(g, cf[q]);
+            for (int qa = 0; qa < 6; ++qa)
+                for (int qb = 0; qb < 6; ++qb) {
+                    const double w = g.g6w[qa] * g.g6w[qb] * F.measure;
+                    const long long sp = (bf * 36 + qa * 6 + qb) * 3;
+                    double rp[3], tv[3], mud[3];
+                    ref_point(g, F, c, g.g6p[qa], g.g6p[qb], rp);
+                    for (int d = 0; d < 3; ++d) mud[d] = dir[d] ? sm.dirichlet[sp + d] : 0.0;
+                    const double nv = shp(a, rp);
+                    if (!dir[comp]) r += w * nv * sm.traction[sp + comp];
+                    if (dir[comp]) r += w * gamma_f * nv * mud[comp];
+                    traction(g, a, comp, rp, F.n, tv);
+                    r -= w * dot3(tv, mud);
+                }
+        }
+        u[t] = r + 0.0;
+    }
+}
+
+__global__ void k_rhs_qvalues3(Geo3 g, int nq, const signed char* qc, Samples3 sm, double* qv) {
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nq; f += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (qc[f]) {
+            const Face3 F = face_info(g, f);
+            const long long bf = bface_index3(g, f);
+            for (int qa = 0; qa < 6; ++qa)
+                for (int qb = 0; qb < 6; ++qb) {
+                    const double w = g.g6w[qa] * g.g6w[qb] * F.measure;
+                    v += w / F.measure * sm.flow[bf * 36 + qa * 6 + qb];
+                }
+        }
+        qv[f] = v;
+    }
+}
+
+__global__ void k_rhs_qp_s3(Geo3 g, int nq, int np, const double* __restrict__ kcells, const signed char* qc, Samples3 sm,
+                            const double* __restrict__ qv, double* q, double* p) {
+    const double vol = g.h[0] * g.h[1] * g.h[2];
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nq; f += gridDim.x * blockDim.x) {
+        const Face3 F = face_info(g, f);
+        if (qc[f]) {
+            q[f] = qv[f];
+            continue;
+        }
+        double r = 0.0;
+        if (sm.darcy)
+            for (int side = 0; side < 2; ++side) {
+                const int c = side ? F.cp : F.cm;
+                if (c < 0) continue;
+                int f0, f1;
+                axis_faces(g, c, F.axis, f0, f1);
+                const bool low = f == f0;
+                const double sg = F.n[F.axis];
+                for (int qi = 0; qi < 6; ++qi)
+                    for (int qj = 0; qj < 6; ++qj)
+                        for (int qk = 0; qk < 6; ++qk) {
+                            const double ref[3] = {g.g6p[qi], g.g6p[qj], g.g6p[qk]};
+                            const double w = g.g6w[qi] * g.g6w[qj] * g.g6w[qk] * vol;
+                            const double wf = low ? sg * (1.0 - ref[F.axis]) : sg * ref[F.axis];
+                            r += w * wf * sm.darcy[((long long)c * 216 + (qi * 6 + qj) * 6 + qk) * 3 + F.axis];
+                        }
+            }
+        if (F.boundary) {
+            const long long bf = bface_index3(g, f);
+            for (int qa = 0; qa < 6; ++qa)
+                for (int qb = 0; qb < 6; ++qb) {
+                    const double w = g.g6w[qa] * g.g6w[qb] * F.measure;
+                    r -= w * sm.flow[bf * 36 + qa * 6 + qb];
+                }
+        }
+        for (int side = 0; side < 2; ++side) {  // eliminated couplings to constrained faces (mq_bc)
+            const int c = side ? F.cp : F.cm;
+            if (c < 0) continue;
+            int f0, f1;
+            axis_faces(g, c, F.axis, f0, f1);
+            const int opp = (f == f0) ? f1 : f0;
+            if (!qc[opp]) continue;
+            const double keff = g.eta / (kcells ? kcells[c] : g.kperm);
+            const double d6 = keff * vol / 6.0;
+            const Face3 F0 = face_info(g, f0), F1 = face_info(g, f1);
+            const double cross = d6 * F0.n[F.axis] * F1.n[F.axis];
+            r -= cross * qv[opp];
+        }
+        q[f] = r;
+    }
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
+        double r = 0.0;
+        if (sm.mass)
+            for (int qi = 0; qi < 6; ++qi)
+                for (int qj = 0; qj < 6; ++qj)
+                    for (int qk = 0; qk < 6; ++qk) {
+                        const double w = g.g6w[qi] * g.g6w[qj] * g.g6w[qk] * vol;
+                        r -= w * sm.mass[(long long)c * 216 + (qi * 6 + qj) * 6 + qk];
+                    }
+        // b_bc: the cell's constrained faces in the order xlo, xhi, ylo, yhi, zlo, zhi
+        for (int axis = 0; axis < 3; ++axis) {
+            int ff[2];
+            axis_faces(g, c, axis, ff[0], ff[1]);
+            for (int e = 0; e < 2; ++e) {
+                if (!qc[ff[e]]) continue;
+                const Face3 F = face_info(g, ff[e]);
+                const double sout = F.boundary ? 1.0 : (c == F.cm ? 1.0 : -1.0);
+                const double v = -sout * F.measure;
+                r -= v * qv[ff[e]];
+            }
+        }
+        p[c] = r;
+    }
+}
+
 Geo3 make_geo3(const pdg_problem3& p) {
     Geo3 g{};
     g.nx = p.nx;
@@ -709,6 +864,42 @@ void assemble_ops_device3(SpatialOps& s, const pdg_problem3& p, cudaStream_t st)
     k_mp3<<<grid_for(n, 256), 256, 0, st>>>(g, n, s.m_p.p);
     PDG_CHECK_LAUNCH();
     PDG_CUDA(cudaStreamSynchronize(st));
+}
+
+void assemble_rhs_sampled_device3(const SpatialOps& s, const pdg_rhs_samples& h, double* u, double* q, double* p,
+                                  cudaStream_t st) {
+    require(h.traction && h.dirichlet && h.flow, "pdg_ops_rhs_sampled: boundary samples must be given");
+    const Geo3 g = make_geo3(s.prob3);
+    const size_t nc = (size_t)s.n_p;
+    const size_t nbf = 2 * ((size_t)s.nx * s.ny + (size_t)s.nx * s.nz + (size_t)s.ny * s.nz);
+    DBuf<double> mom, dar, mas, tra, dir, flo, kc, qv(s.n_q);
+    Samples3 sm{};
+    if (h.momentum) {
+        mom.upload(h.momentum, nc * 648, st);
+        sm.momentum = mom.p;
+    }
+    if (h.darcy) {
+        dar.upload(h.darcy, nc * 648, st);
+        sm.darcy = dar.p;
+    }
+    if (h.mass) {
+        mas.upload(h.mass, nc * 216, st);
+        sm.mass = mas.p;
+    }
+    tra.upload(h.traction, nbf * 108, st);
+    dir.upload(h.dirichlet, nbf * 108, st);
+    flo.upload(h.flow, nbf * 36, st);
+    sm.traction = tra.p;
+    sm.dirichlet = dir.p;
+    sm.flow = flo.p;
+    if (!s.k_cells.empty()) kc.upload(s.k_cells, st);
+    k_rhs_u_s3<<<grid_for(24LL * s.n_p, 256), 256, 0, st>>>(g, sm, u);
+    k_rhs_qvalues3<<<grid_for(s.n_q, 256), 256, 0, st>>>(g, s.n_q, s.q_constrained.p, sm, qv.p);
+    k_rhs_qp_s3<<<grid_for(std::max(s.n_q, s.n_p), 256), 256, 0, st>>>(g, s.n_q, s.n_p, kc.n ? kc.p : nullptr,
+                                                                        s.q_constrained.p, sm, qv.p, q, p);
+    count_launch(3);
+    PDG_CHECK_LAUNCH();
+    PDG_CUDA(cudaStreamSynchronize(st));  // the staging buffers are released at scope exit
 }
 
 void assemble_rhs_device3(const SpatialOps& s, double t, double* u, double* q, double* p, cudaStream_t st) {

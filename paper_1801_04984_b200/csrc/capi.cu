@@ -502,7 +502,51 @@ int pdg_rhs_sample_points(const pdg_ops* ops, double* cell_xy, int* bface_ids, d
     API_BEGIN
     require(ops != nullptr, "pdg_rhs_sample_points: null ops");
     const SpatialOps& s = ops->s;
-    require(s.has_problem && s.nz == 0, "pdg_rhs_sample_points: needs a 2D problem description (pdg_ops_assemble)");
+    require(s.has_problem, "pdg_rhs_sample_points: needs a problem description (pdg_ops_assemble / pdg_ops_assemble3)");
+    if (s.nz > 0) {  // 3D: [cell][216][3], boundary faces ascending, [bface][36][3]
+        const int nx = s.nx, ny = s.ny, nz = s.nz;
+        const double h[3] = {s.prob3.lx / nx, s.prob3.ly / ny, s.prob3.lz / nz};
+        std::vector<double> pts, wts;
+        tc_gauss(6, pts, wts);
+        if (cell_xy)
+            for (int c = 0; c < nx * ny * nz; ++c) {
+                const double o[3] = {(c % nx) * h[0], ((c / nx) % ny) * h[1], (c / (nx * ny)) * h[2]};
+                for (int i = 0; i < 6; ++i)
+                    for (int j = 0; j < 6; ++j)
+                        for (int k = 0; k < 6; ++k) {
+                            double* d = cell_xy + ((size_t)c * 216 + (i * 6 + j) * 6 + k) * 3;
+                            d[0] = o[0] + pts[i] * h[0];
+                            d[1] = o[1] + pts[j] * h[1];
+                            d[2] = o[2] + pts[k] * h[2];
+                        }
+            }
+        const int nzf = nx * ny * (nz + 1), nyf = nx * (ny + 1) * nz;
+        size_t b = 0;
+        // axis: normal axis; (ci, cj, ck): the adjacent cell; fixed: reference coordinate of the face in it
+        auto face = [&](int f, int axis, int ci, int cj, int ck, double fixed) {
+            if (bface_ids) bface_ids[b] = f;
+            if (bface_xy)
+                for (int qa = 0; qa < 6; ++qa)
+                    for (int qb = 0; qb < 6; ++qb) {
+                        double rp[3];
+                        if (axis == 0) { rp[0] = fixed; rp[1] = pts[qa]; rp[2] = pts[qb]; }
+                        else if (axis == 1) { rp[0] = pts[qa]; rp[1] = fixed; rp[2] = pts[qb]; }
+                        else { rp[0] = pts[qa]; rp[1] = pts[qb]; rp[2] = fixed; }
+                        double* d = bface_xy + (b * 36 + qa * 6 + qb) * 3;
+                        d[0] = ci * h[0] + rp[0] * h[0];
+                        d[1] = cj * h[1] + rp[1] * h[1];
+                        d[2] = ck * h[2] + rp[2] * h[2];
+                    }
+            ++b;
+        };
+        for (int j = 0; j < ny; ++j) for (int i = 0; i < nx; ++i) face((0 * ny + j) * nx + i, 2, i, j, 0, 0.0);
+        for (int j = 0; j < ny; ++j) for (int i = 0; i < nx; ++i) face((nz * ny + j) * nx + i, 2, i, j, nz - 1, 1.0);
+        for (int k = 0; k < nz; ++k) for (int i = 0; i < nx; ++i) face(nzf + (0 * nz + k) * nx + i, 1, i, 0, k, 0.0);
+        for (int k = 0; k < nz; ++k) for (int i = 0; i < nx; ++i) face(nzf + (ny * nz + k) * nx + i, 1, i, ny - 1, k, 1.0);
+        for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) face(nzf + nyf + (0 * nz + k) * ny + j, 0, 0, j, k, 0.0);
+        for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) face(nzf + nyf + (nx * nz + k) * ny + j, 0, nx - 1, j, k, 1.0);
+        return PDG_OK;
+    }
     const int nx = s.nx, ny = s.ny;
     const double hx = s.prob.lx / nx, hy = s.prob.ly / ny;
     std::vector<double> pts, wts;

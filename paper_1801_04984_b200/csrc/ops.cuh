@@ -37,6 +37,8 @@ void csr_spmv(const DCsr& a, const double* x, double* y, cudaStream_t st);  // o
 void assemble_ops_device(SpatialOps& ops, const pdg_problem& p, cudaStream_t st);
 void assemble_ops_device3(SpatialOps& ops, const pdg_problem3& p, cudaStream_t st);
 void assemble_rhs_device3(const SpatialOps& ops, double t, double* u, double* q, double* p, cudaStream_t st);
+void assemble_rhs_sampled_device3(const SpatialOps& ops, const pdg_rhs_samples& samples, double* u, double* q, double* p,
+                                  cudaStream_t st);
 void assemble_rhs_sampled_device(const SpatialOps& ops, const pdg_rhs_samples& samples, double* u, double* q, double* p,
                                  cudaStream_t st);
 void assemble_rhs_device(const SpatialOps& ops, double t, double* u, double* q, double* p, cudaStream_t st);

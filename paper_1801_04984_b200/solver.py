@@ -247,8 +247,12 @@ class SpatialOperators:
     def sample_points(self):
         """Quadrature points at which assemble_rhs evaluates its data (pdg_rhs_sample_points):
         cell points (n_cells, 36, 2), boundary face ids (2 nx + 2 ny,), face points (n_bfaces, 6, 2)."""
-        nb = 2 * (self.nx + self.ny)
-        cxy, ids, fxy = np.empty((self.n_p, 36, 2)), np.empty(nb, np.int32), np.empty((nb, 6, 2))
+        if self.nz > 0:
+            nb = 2 * (self.nx * self.ny + self.nx * self.nz + self.ny * self.nz)
+            cxy, ids, fxy = np.empty((self.n_p, 216, 3)), np.empty(nb, np.int32), np.empty((nb, 36, 3))
+        else:
+            nb = 2 * (self.nx + self.ny)
+            cxy, ids, fxy = np.empty((self.n_p, 36, 2)), np.empty(nb, np.int32), np.empty((nb, 6, 2))
         check(lib().pdg_rhs_sample_points(self._h, _dp(cxy), _ip(ids), _dp(fxy)))
         return cxy, ids, fxy
 

@@ -334,3 +334,40 @@ def test_gpu_against_committed_golden_vectors():
             assert abs(reps[s].iterations - int(h[f"iterations_r{r}"][s])) <= 1
             ref = h[f"states_r{r}"][s].ravel()
             assert np.linalg.norm(states[s] - ref) <= SOLVE_RTOL * np.linalg.norm(ref)
+
+
+def test_rhs_sampled3_bit_identical(oracle):
+    """pdg_ops_rhs_sampled on 3D operators == the oracle's assemble_rhs3_sampled, bit for bit, for
+    seeded random volume sources and boundary data (Dirichlet, traction, pressure and prescribed
+    nonzero normal flux, eliminated couplings included); the library's sample points are the
+    oracle's; absent volume fields are skipped; constant data through the sampled path equals the
+    constant-data kernels."""
+    spec = _variants()[2]  # every boundary kind
+    rp = oracle.RefProblem(spec.to_dict())
+    ops = S.SpatialOperators.assemble(spec)
+    cxyz, ids, fxyz = rp.sample_points3()
+    gc, gi, gf = ops.sample_points()
+    assert np.array_equal(cxyz, gc) and np.array_equal(ids, gi) and np.array_equal(fxyz, gf)
+    rng = np.random.default_rng(7)
+    sm = dict(momentum=rng.standard_normal(cxyz.shape), darcy=rng.standard_normal(cxyz.shape),
+              mass=rng.standard_normal(cxyz.shape[:2]), traction=rng.standard_normal(fxyz.shape),
+              dirichlet=rng.standard_normal(fxyz.shape), flow=rng.standard_normal(fxyz.shape[:2]))
+    for drop in ((), ("momentum",), ("darcy", "mass"), ("momentum", "darcy", "mass")):
+        cur = {k: (None if k in drop else v) for k, v in sm.items()}
+        ref = rp.rhs3_sampled(cur["traction"], cur["dirichlet"], cur["flow"], momentum=cur["momentum"],
+                              darcy=cur["darcy"], mass=cur["mass"])
+        got = ops.rhs_sampled(cur)
+        for a, b in zip(ref, got):
+            assert np.array_equal(a, b), drop
+    # constant boundary data as samples == the constant-data right-hand side
+    const = dict(traction=np.zeros(fxyz.shape), dirichlet=np.zeros(fxyz.shape), flow=np.zeros(fxyz.shape[:2]))
+    nx, ny, nz = spec.nx, spec.ny, spec.nz
+    nzf, nyf = nx * ny * (nz + 1), nx * (ny + 1) * nz
+    for b, f in enumerate(ids):
+        tag = (("zlo" if f < nx * ny else "zhi") if f < nzf else
+               (("ylo" if f - nzf < nz * nx else "yhi") if f < nzf + nyf else ("xlo" if f - nzf - nyf < nz * ny else "xhi")))
+        kind, data = spec.disp[tag]
+        (const["dirichlet"] if kind == "fixed" else const["traction"])[b, :, :] = data
+        const["flow"][b, :] = spec.flow[tag][1]
+    for a, b in zip(ops.rhs(0.0), ops.rhs_sampled(const)):
+        assert np.array_equal(a, b)
