@@ -371,3 +371,89 @@ def test_rhs_sampled3_bit_identical(oracle):
         const["flow"][b, :] = spec.flow[tag][1]
     for a, b in zip(ops.rhs(0.0), ops.rhs_sampled(const)):
         assert np.array_equal(a, b)
+
+
+def test_mms_poroelastic_march_converges_on_device():
+    """End-to-end manufactured solution of the coupled 3D Biot system on the GPU (device assembly,
+    sampled time-dependent sources and boundary data, dG(1) slabs, GMRES with the exact fixed-stress
+    preconditioner): u(x, t) = U(x)(1 + t), p(x, t) = P(x)(1 + t/2), q = -(K/eta) grad p, with
+    f = -div(sigma(u) - b p I) and g = d/dt(b div u + p/M) + div q. The solution is linear in time, so
+    dG(1) is exact in time and the error at the end of the march is the spatial one: second order in
+    the nodal displacement, at least first order in the piecewise-constant pressure (measured:
+    2.2 / 2.2 and 2.7 / 1.4 under n = 2, 4, 8). Parity is unpinned in 3D; this pins the whole device
+    path against the continuous problem."""
+    import sympy as sy
+    import torch
+    x, y, z, t = sy.symbols("x y z t")
+    lam, mu, bb, MM, eta, kperm = 2.0, 1.5, 0.8, 10.0, 1.0, 1.0
+    U = sy.Matrix([sy.sin(sy.pi * x / 2) * sy.cos(y) * (1 + z), x * y * sy.exp(-z), sy.cos(x) * z * z + x * y * z]) * sy.Rational(1, 10)
+    P_ = sy.sin(sy.pi * x / 2) * sy.cos(y) * (1 + z * z) + x * y
+    u = U * (1 + t)
+    p = P_ * (1 + t / 2)
+    grad = u.jacobian([x, y, z])
+    eps = (grad + grad.T) / 2
+    sig = 2 * mu * eps + lam * eps.trace() * sy.eye(3) - bb * p * sy.eye(3)
+    fm = -sy.Matrix([sum(sy.diff(sig[i, j], (x, y, z)[j]) for j in range(3)) for i in range(3)])
+    q = -(kperm / eta) * sy.Matrix([sy.diff(p, v) for v in (x, y, z)])
+    g = sy.diff(bb * eps.trace() + p / MM, t) + sum(sy.diff(q[i], (x, y, z)[i]) for i in range(3))
+    L = lambda e: sy.lambdify((x, y, z, t), e, "numpy")  # noqa: E731
+    u_f, p_f, fm_f, g_f = L(u), L(p), L(fm), L(g)
+
+    def vec(fn, X, Y, Z, tt):
+        out = fn(X, Y, Z, tt)
+        return np.stack([np.broadcast_to(np.asarray(out[i][0], float), X.shape) for i in range(3)], axis=-1)
+
+    def sca(fn, X, Y, Z, tt):
+        return np.broadcast_to(np.asarray(fn(X, Y, Z, tt), float), X.shape).copy()
+
+    r, n_slabs, T = 1, 2, 0.5
+    tau = T / n_slabs
+    nodes = S.time_constants(r)["nodes"]
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-12, restart=50), candidate="flexible")
+    eu, ep = [], []
+    for n in (2, 4, 8):
+        spec = P.config2(n)
+        spec.lam, spec.mu, spec.biot_b, spec.biot_m, spec.eta, spec.k_perm = lam, mu, bb, MM, eta, kperm
+        spec.k_perm_cells = None
+        spec.disp = {tg: ("fixed", (0.0, 0.0, 0.0)) for tg in P.TAGS3}
+        spec.flow = {tg: ("pressure", 0.0) for tg in P.TAGS3}
+        ops = S.SpatialOperators.assemble(spec)
+        cxyz, ids, fxyz = ops.sample_points()
+        h = 1.0 / n
+        # initial data: nodal interpolant of u(0), cell-centre value of p(0)
+        nod = np.array([[((i + (a & 1)) * h, (j + ((a >> 1) & 1)) * h, (k + (a >> 2)) * h) for a in range(8)]
+                        for k in range(n) for j in range(n) for i in range(n)])
+        cc = np.array([((i + .5) * h, (j + .5) * h, (k + .5) * h) for k in range(n) for j in range(n) for i in range(n)])
+        u_prev = torch.from_numpy(vec(u_f, nod[..., 0], nod[..., 1], nod[..., 2], 0.0).reshape(-1).copy()).cuda()
+        p_prev = torch.from_numpy(sca(p_f, cc[:, 0], cc[:, 1], cc[:, 2], 0.0)).cuda()
+        slab = S.SlabSolver(ops, r, tau, opt)
+        nt = ops.n_total
+        rhs = torch.empty((r + 1) * nt, dtype=torch.float64, device="cuda")
+        out = torch.empty_like(rhs)
+        for s_ in range(n_slabs):
+            t0 = s_ * tau
+            samples = []
+            for c in nodes:
+                tt = t0 + c * tau
+                samples.append(dict(
+                    momentum=vec(fm_f, cxyz[..., 0], cxyz[..., 1], cxyz[..., 2], tt),
+                    mass=sca(g_f, cxyz[..., 0], cxyz[..., 1], cxyz[..., 2], tt),
+                    traction=np.zeros(fxyz.shape), dirichlet=vec(u_f, fxyz[..., 0], fxyz[..., 1], fxyz[..., 2], tt),
+                    flow=sca(p_f, fxyz[..., 0], fxyz[..., 1], fxyz[..., 2], tt)))
+            torch.cuda.synchronize()
+            slab.rhs_sampled_device(samples, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+            rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+            assert rep.converged
+            end = out[r * nt:(r + 1) * nt]
+            u_prev.copy_(end[:ops.n_u])
+            p_prev.copy_(end[ops.n_u + ops.n_q:])
+            torch.cuda.synchronize()
+        ue = vec(u_f, nod[..., 0], nod[..., 1], nod[..., 2], T).reshape(-1)
+        pe = sca(p_f, cc[:, 0], cc[:, 1], cc[:, 2], T)
+        eu.append(float(np.sqrt(np.mean((u_prev.cpu().numpy() - ue) ** 2))))
+        ep.append(float(np.sqrt(np.mean((p_prev.cpu().numpy() - pe) ** 2))))
+    ru = [np.log2(eu[i] / eu[i + 1]) for i in range(2)]
+    rp_ = [np.log2(ep[i] / ep[i + 1]) for i in range(2)]
+    print("MMS 3D march: u errors", eu, "rates", ru, "p errors", ep, "rates", rp_)
+    assert eu[2] < eu[1] < eu[0] and ep[2] < ep[1] < ep[0]
+    assert ru[1] > 1.7 and rp_[1] > 0.9, (eu, ru, ep, rp_)
