@@ -969,3 +969,95 @@ def test_march_with_sampled_data(oracle):
     y = (T["Q"] @ xr.reshape(r + 1, -1)).ravel()
     assert abs(rep.iterations - rr["iterations"]) <= 1
     assert np.linalg.norm(x - y) <= SOLVE_RTOL * np.linalg.norm(y)
+
+
+def test_mms_poroelastic_march_2d_on_device():
+    """The reference's MMS-type use of assemble_rhs (volume sources and space- / time-dependent
+    boundary functions, assembly.hpp:467-563) end to end on the GPU in 2D: u = U(x)(1 + t),
+    p = P(x)(1 + t/2), q = -(K/eta) grad p, f = -div(sigma(u) - b p I), g = d/dt(b div u + p/M) +
+    div q, Nitsche displacement data on left / bottom, traction data on right / top, pressure data
+    on left / top and prescribed normal flux on right / bottom; dG(1) (exact in time for this
+    solution), two slabs. Nodal displacement error second order, cell pressure at least first order
+    under n = 4, 8, 16."""
+    import sympy as sy
+    import torch
+    x, y, t = sy.symbols("x y t")
+    lam, mu, bb, MM, eta, kperm = 2.0, 1.5, 0.8, 10.0, 1.0, 1.0
+    U = sy.Matrix([sy.sin(sy.pi * x / 2) * sy.cos(y), x * y + sy.sin(x) * y * y]) * sy.Rational(1, 10)
+    P_ = sy.sin(sy.pi * x / 2) * sy.cos(y) + x * y
+    u = U * (1 + t)
+    p = P_ * (1 + t / 2)
+    grad = u.jacobian([x, y])
+    eps = (grad + grad.T) / 2
+    sig_e = 2 * mu * eps + lam * eps.trace() * sy.eye(2)
+    sig = sig_e - bb * p * sy.eye(2)
+    fm = -sy.Matrix([sum(sy.diff(sig[i, j], (x, y)[j]) for j in range(2)) for i in range(2)])
+    q = -(kperm / eta) * sy.Matrix([sy.diff(p, v) for v in (x, y)])
+    g = sy.diff(bb * eps.trace() + p / MM, t) + sum(sy.diff(q[i], (x, y)[i]) for i in range(2))
+    L = lambda e: sy.lambdify((x, y, t), e, "numpy")  # noqa: E731
+    u_f, p_f, fm_f, g_f, q_f, sg_f = L(u), L(p), L(fm), L(g), L(q), L(sig)
+
+    def vec(fn, X, Y, tt):
+        out = fn(X, Y, tt)
+        return np.stack([np.broadcast_to(np.asarray(out[i][0], float), X.shape) for i in range(2)], axis=-1)
+
+    def sca(fn, X, Y, tt):
+        return np.broadcast_to(np.asarray(fn(X, Y, tt), float), X.shape).copy()
+
+    r, n_slabs, T = 1, 2, 0.5
+    tau = T / n_slabs
+    nodes = S.time_constants(r)["nodes"]
+    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-12, restart=50), candidate="flexible")
+    normals = {"left": (-1.0, 0.0), "right": (1.0, 0.0), "bottom": (0.0, -1.0), "top": (0.0, 1.0)}
+    eu, ep = [], []
+    for n in (4, 8, 16):
+        spec = P.config0()
+        spec.nx = spec.ny = n
+        spec.lam, spec.mu, spec.biot_b, spec.biot_m, spec.eta, spec.k_perm = lam, mu, bb, MM, eta, kperm
+        spec.disp = {"left": ("fixed", (0.0, 0.0)), "bottom": ("fixed", (0.0, 0.0)),
+                     "right": ("traction", (0.0, 0.0)), "top": ("traction", (0.0, 0.0))}
+        spec.flow = {"left": ("pressure", 0.0), "top": ("pressure", 0.0), "right": ("no_flow", 0.0),
+                     "bottom": ("no_flow", 0.0)}
+        ops = S.SpatialOperators.assemble(spec)
+        cxy, ids, fxy = ops.sample_points()
+        nh = n * (n + 1)
+        tags = ["bottom" if f < n else "top" if f < nh else "left" if f < nh + n else "right" for f in ids]
+        h = 1.0 / n
+        nod = np.array([[((i + (a & 1)) * h, (j + (a >> 1)) * h) for a in range(4)] for j in range(n) for i in range(n)])
+        cc = np.array([((i + .5) * h, (j + .5) * h) for j in range(n) for i in range(n)])
+        u_prev = torch.from_numpy(vec(u_f, nod[..., 0], nod[..., 1], 0.0).reshape(-1).copy()).cuda()
+        p_prev = torch.from_numpy(sca(p_f, cc[:, 0], cc[:, 1], 0.0)).cuda()
+        slab = S.SlabSolver(ops, r, tau, opt)
+        nt = ops.n_total
+        rhs = torch.empty((r + 1) * nt, dtype=torch.float64, device="cuda")
+        out = torch.empty_like(rhs)
+        for s_ in range(n_slabs):
+            samples = []
+            for c in nodes:
+                tt = s_ * tau + c * tau
+                X, Y = fxy[..., 0], fxy[..., 1]
+                SG, Q = sg_f(X, Y, tt), q_f(X, Y, tt)
+                trac, flow = np.zeros(fxy.shape), sca(p_f, X, Y, tt)
+                for b_, tg in enumerate(tags):
+                    nv = normals[tg]
+                    for i in range(2):
+                        trac[b_, :, i] = sum(np.broadcast_to(np.asarray(SG[i][j], float), X.shape)[b_] * nv[j] for j in range(2))
+                    if tg in ("right", "bottom"):
+                        flow[b_] = sum(np.broadcast_to(np.asarray(Q[j][0], float), X.shape)[b_] * nv[j] for j in range(2))
+                samples.append(dict(momentum=vec(fm_f, cxy[..., 0], cxy[..., 1], tt), mass=sca(g_f, cxy[..., 0], cxy[..., 1], tt),
+                                    traction=trac, dirichlet=vec(u_f, X, Y, tt), flow=flow))
+            torch.cuda.synchronize()
+            slab.rhs_sampled_device(samples, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr())
+            rep = slab.solve_device(rhs.data_ptr(), out.data_ptr())
+            assert rep.converged
+            end = out[r * nt:(r + 1) * nt]
+            u_prev.copy_(end[:ops.n_u])
+            p_prev.copy_(end[ops.n_u + ops.n_q:])
+            torch.cuda.synchronize()
+        eu.append(float(np.sqrt(np.mean((u_prev.cpu().numpy() - vec(u_f, nod[..., 0], nod[..., 1], T).reshape(-1)) ** 2))))
+        ep.append(float(np.sqrt(np.mean((p_prev.cpu().numpy() - sca(p_f, cc[:, 0], cc[:, 1], T)) ** 2))))
+    ru = [np.log2(eu[i] / eu[i + 1]) for i in range(2)]
+    rp_ = [np.log2(ep[i] / ep[i + 1]) for i in range(2)]
+    print("MMS 2D march: u errors", eu, "rates", ru, "p errors", ep, "rates", rp_)
+    assert eu[2] < eu[1] < eu[0] and ep[2] < ep[1] < ep[0]
+    assert ru[1] > 1.7 and rp_[1] > 0.9, (eu, ru, ep, rp_)
