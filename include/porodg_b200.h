@@ -121,6 +121,10 @@ const char* pdg_last_error(void);
 const char* pdg_version(void);
 
 int pdg_ctx_create(int device, pdg_ctx** out);
+/* One context per listed device (pdg_ctx_create(const int* devices, int n, ...)):
+ * out[i] is the context of devices[i]. The multi-GPU solve itself is one process (or host
+ * thread) per GPU: each binds its context to a pdg_comm (below). On failure nothing is kept. */
+int pdg_ctx_create_devices(const int* devices, int n, pdg_ctx** out);
 void pdg_ctx_destroy(pdg_ctx* ctx);
 
 /* Structured-mesh dimensions (mesh.hpp:42-60) of reference-assembled operators, from

@@ -82,6 +82,7 @@ _SIGS = {
     "pdg_last_error": (C.c_char_p, []),
     "pdg_version": (C.c_char_p, []),
     "pdg_ctx_create": (C.c_int, [C.c_int, C.POINTER(VP)]),
+    "pdg_ctx_create_devices": (C.c_int, [IP, C.c_int, C.POINTER(VP)]),
     "pdg_ctx_destroy": (None, [VP]),
     "pdg_ops_upload": (C.c_int, [VP, C.c_int, C.c_int, C.POINTER(CSR), C.POINTER(CSR), C.POINTER(CSR),
                                  C.POINTER(CSR), DP, C.POINTER(C.c_byte), C.c_double, C.c_double, C.c_double,

@@ -346,6 +346,23 @@ int pdg_mesh_dims_from_operators(const pdg_csr* B, int n_q, int dims[2]) {
     API_END
 }
 
+int pdg_ctx_create_devices(const int* devices, int n, pdg_ctx** out) {
+    API_BEGIN
+    require(devices && out && n >= 1, "pdg_ctx_create_devices: bad arguments");
+    for (int i = 0; i < n; ++i) out[i] = nullptr;
+    for (int i = 0; i < n; ++i) {
+        const int rc = pdg_ctx_create(devices[i], &out[i]);
+        if (rc != PDG_OK) {
+            for (int j = 0; j < i; ++j) {
+                pdg_ctx_destroy(out[j]);
+                out[j] = nullptr;
+            }
+            return rc;
+        }
+    }
+    API_END
+}
+
 int pdg_ops_upload(pdg_ctx* ctx, int nx, int ny, const pdg_csr* A, const pdg_csr* M_q, const pdg_csr* B, const pdg_csr* E,
                    const double* m_p_diag, const signed char* q_constrained, double biot_b, double inv_m, double k_dr,
                    pdg_ops** out) {

@@ -60,6 +60,24 @@ def test_missing_gpu_is_loud():
     assert rc != 0
 
 
+def test_ctx_device_list_argument_errors():
+    """pdg_ctx_create_devices (SURVEY 8(b) signature): null / empty lists are invalid arguments;
+    without a GPU every listed device fails loudly and nothing is kept."""
+    import torch
+    L = _lib.lib()
+    out = (ctypes.c_void_p * 2)()
+    assert L.pdg_ctx_create_devices(None, 1, out) == _lib.PDG_INVALID_ARGUMENT
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert L.pdg_ctx_create_devices(devs, 0, out) == _lib.PDG_INVALID_ARGUMENT
+    rc = L.pdg_ctx_create_devices(devs, 2, out)
+    if torch.cuda.is_available():
+        assert rc == 0 and out[0] and out[1]
+        L.pdg_ctx_destroy(out[0])
+        L.pdg_ctx_destroy(out[1])
+    else:
+        assert rc != 0 and not out[0] and not out[1]
+
+
 @pytest.mark.parametrize("nx,ny", [(12, 7), (7, 12), (16, 16), (5, 1), (1, 5), (1, 1), (3, 2)])
 def test_mesh_dims_inferred_from_reference_operators(oracle, nx, ny):
     """pdg_ops_upload(nx = ny = 0) infers the structured mesh (mesh.hpp:42-60)
