@@ -255,6 +255,54 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
     double* p2 = partial + (size_t)kRedBlocks * ncols;
     double* p3 = partial + (size_t)2 * kRedBlocks * ncols;
     if (!pre1) block_multidot(n, ncols, V, w, p1);
+    if (ncols <= 8) {
+        // Fused passes (up to 8 basis vectors): a thread updates its rows of w and accumulates the
+        // next pass's partial dots from the values it just formed, in the same row order and with
+        // the same partial-sum tree as the separate loops, so the bits are those of the unfused
+        // sequence; only the partials cross blocks: two grid barriers fewer, half the sweeps.
+        __shared__ double shd[8][kRedThreads / 32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass > 0 || !pre1) grid.sync();
+            if (pass == 0 && pre1)
+                block_column_sums(pre1, ncols, hs, h_out, nb1);
+            else
+                block_column_sums(pass == 0 ? p1 : p2, ncols, hs, h_out + (size_t)pass * ncols);
+            double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+                double v = __ldcg(w + r);
+                double vj[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < ncols) {
+                        vj[j] = V[(long long)j * n + r];
+                        v -= hs[j] * vj[j];
+                    }
+                w[r] = v;
+                if (pass == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < ncols) a[q] += vj[q] * v;
+                } else {
+                    a[0] += v * v;
+                }
+            }
+            const int nq = pass == 0 ? ncols : 1;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) shd[q][warp] = a[q];
+            __syncthreads();
+            if (threadIdx.x < 8 && threadIdx.x < nq) {
+                double sacc = 0.0;
+                for (int i = 0; i < kRedThreads / 32; ++i) sacc += shd[threadIdx.x][i];
+                (pass == 0 ? p2 : p3)[(long long)blockIdx.x * nq + threadIdx.x] = sacc;
+            }
+            __syncthreads();
+        }
+    } else {
     for (int pass = 0; pass < 2; ++pass) {
         if (pass > 0 || !pre1) grid.sync();
         if (pass == 0 && pre1)
@@ -272,6 +320,7 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
             block_multidot(n, ncols, V, w, p2);
         else
             block_multidot(n, 1, w, w, p3);
+    }
     }
     grid.sync();
     {
