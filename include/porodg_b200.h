@@ -290,6 +290,13 @@ int pdg_slab_solve_device(pdg_slab* slab, const double* rhs_dev, double* out_dev
  * ((r+1) * n_total). */
 int pdg_slab_rhs_device(pdg_slab* slab, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
                         double* rhs_dev);
+/* One step of the march's slab loop on the device (march.hpp:62-79 for the monolithic-spectral
+ * branch): build_slab_system for [t0, t0 + tau] from the previous end trace prev_state_dev
+ * ([u q p], n_total doubles; NULL = zero initial data) and solve it into out_dev ((r+1) n_total),
+ * with ONE synchronization at the end. prev_state_dev must not alias out_dev (use two output
+ * buffers alternately and pass the last component of the previous one). Constant boundary data. */
+int pdg_slab_step_device(pdg_slab* slab, double t0, double tau, const double* prev_state_dev, double* out_dev,
+                         pdg_report* rep);
 /* The same with sampled data: samples[i] holds the fields at the slab's Radau node i,
  * t = t0 + nodes[i] * tau (r + 1 entries; pdg_time_constants gives the nodes). */
 int pdg_slab_rhs_sampled_device(pdg_slab* slab, double tau, const pdg_rhs_samples* samples, const double* u_prev_dev,

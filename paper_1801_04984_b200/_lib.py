@@ -113,6 +113,7 @@ _SIGS = {
     "pdg_slab_solve_device": (C.c_int, [VP, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
     "pdg_slab_rhs_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_block_reports": (C.c_int, [VP, IP, IP, IP, DP]),
+    "pdg_slab_step_device": (C.c_int, [VP, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
     "pdg_slab_rhs_sampled_device": (C.c_int, [VP, C.c_double, C.POINTER(RhsSamples), C.c_void_p, C.c_void_p, C.c_void_p]),
     "pdg_slab_destroy": (None, [VP]),
     "pdg_fs_create": (C.c_int, [VP, C.c_int, C.c_double, C.POINTER(FsOpts), C.POINTER(VP)]),

@@ -59,6 +59,7 @@ struct pdg_slab {
     DBuf<double> d_Q, d_w, d_phi0, shat, ysol, io_a, io_b, rhs_u, rhs_q, rhs_p, djump, et_u;
     DBuf<double> dpt;  // D y_j (p rows) of the solved components, n x n_p
     DBuf<double> d_T;  // the Schur form's T on the device (back-substitution couplings)
+    DBuf<double> zero_state;  // n_total zeros: the initial data of pdg_slab_step_device(prev = NULL)
 };
 
 #define API_BEGIN try {
@@ -943,13 +944,11 @@ int pdg_slab_solve(pdg_slab* s, const double* rhs, double* out, pdg_report* rep)
     API_END
 }
 
-int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
-                        double* rhs_dev) {
-    API_BEGIN
-    require(s && u_prev_dev && p_prev_dev && rhs_dev, "pdg_slab_rhs_device: null argument");
-    require(tau > 0.0, "build_slab_system: tau must be positive");
+namespace {
+// build_slab_system (slab.hpp:58-87) on the slab's stream, constant boundary data; no synchronize
+void slab_rhs_enqueue(pdg_slab* s, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
+                      double* rhs_dev) {
     const SpatialOps& o = s->ops->s;
-    require(o.has_problem, "pdg_slab_rhs_device: operators were uploaded without a problem description");
     cudaStream_t st = o.ctx->stream;
     const int nn = s->tc.n;
     if (!s->rhs_u.n) {
@@ -969,9 +968,41 @@ int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev
                                                                            s->rhs_p.p, s->djump.p, rhs_dev);
     count_launch(2);
     PDG_CHECK_LAUNCH();
+}
+}  // namespace
+
+int pdg_slab_rhs_device(pdg_slab* s, double t0, double tau, const double* u_prev_dev, const double* p_prev_dev,
+                        double* rhs_dev) {
+    API_BEGIN
+    require(s && u_prev_dev && p_prev_dev && rhs_dev, "pdg_slab_rhs_device: null argument");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
+    require(s->ops->s.has_problem, "pdg_slab_rhs_device: operators were uploaded without a problem description");
+    slab_rhs_enqueue(s, t0, tau, u_prev_dev, p_prev_dev, rhs_dev);
     // like every other *_device entry point: rhs_dev is complete when the call returns, so a
     // caller on another stream (torch's) may read it without a library-stream dependency
-    PDG_CUDA(cudaStreamSynchronize(st));
+    PDG_CUDA(cudaStreamSynchronize(s->ops->s.ctx->stream));
+    API_END
+}
+
+int pdg_slab_step_device(pdg_slab* s, double t0, double tau, const double* prev_state_dev, double* out_dev,
+                         pdg_report* rep) {
+    API_BEGIN
+    require(s && out_dev, "pdg_slab_step_device: null argument");
+    require(tau > 0.0, "build_slab_system: tau must be positive");
+    const SpatialOps& o = s->ops->s;
+    require(o.has_problem, "pdg_slab_step_device: operators were uploaded without a problem description");
+    cudaStream_t st = o.ctx->stream;
+    const long long nt = o.n_total();
+    if (!s->zero_state.n) {
+        s->zero_state.alloc(nt);
+        s->zero_state.zero(st);
+    }
+    const double* prev = prev_state_dev ? prev_state_dev : s->zero_state.p;
+    // the right-hand side is consumed (Schur transform) before the solve writes out_dev, all in
+    // stream order: prev_state_dev may be the last component of the previous call's out_dev only
+    // if that is a different buffer than this call's out_dev
+    slab_rhs_enqueue(s, t0, tau, prev, prev + o.n_u + o.n_q, s->io_a.p);
+    return pdg_slab_solve_device(s, s->io_a.p, out_dev, rep);
     API_END
 }
 

@@ -410,6 +410,14 @@ class SlabSolver:
         check(lib().pdg_slab_rhs_device(self._h, t0, self.tau if tau is None else tau, u_prev_ptr, p_prev_ptr,
                                         rhs_ptr))
 
+    def step_device(self, t0: float, prev_state_ptr: int | None, out_ptr: int, tau: float | None = None):
+        """One slab of the march on the device (pdg_slab_step_device): right-hand side from the
+        previous end trace (None = zero initial data) and solve, one synchronization."""
+        rep, hist = _report(self.opt.gmres.max_iter + 2)
+        check(lib().pdg_slab_step_device(self._h, t0, self.tau if tau is None else tau, prev_state_ptr, out_ptr,
+                                         C.byref(rep)))
+        return _to_report(rep, hist)
+
     def rhs_sampled_device(self, samples_per_node, u_prev_ptr: int, p_prev_ptr: int, rhs_ptr: int,
                            tau: float | None = None):
         """build_slab_system from sampled data: samples_per_node[i] = the fields at t0 + nodes[i] tau."""
@@ -514,6 +522,12 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
     out = torch.empty_like(rhs)
     reports, states = [], []
     x0 = None
+    # monolithic branch without the mass check: one library call per slab (pdg_slab_step_device:
+    # right-hand side from the previous end trace + solve, one synchronization), two output
+    # buffers used alternately so the previous end trace never aliases the current output
+    fused = method == "monolithic-spectral" and not mass_check
+    outs = (out, torch.empty_like(out)) if fused else (out, out)
+    prev_ptr = None
     for n in range(n_slabs):
         # the slab's own length and start (march.hpp:63-64); the solver is rebuilt
         # only when tau changes by more than 1e-12 tau (march.hpp:72)
@@ -522,6 +536,17 @@ def march(ops: SpatialOperators, r: int, T: float, n_slabs: int, opt: SolveOptio
             slab = SlabSolver(ops, r, tau, opt)
             fs = FixedStressSolver(ops, r, tau, opt.fs) if method == "fixed-stress" else None
         cached_tau = tau
+        out = outs[n % 2]
+        if fused:
+            try:
+                rep = slab.step_device(t0, prev_ptr, out.data_ptr(), tau=tau)
+            except SolverError as e:
+                raise SolverError(e.status, f"slab {n} (t_n = {t_points[n + 1]:f}): {e}") from None
+            reports.append(rep)
+            prev_ptr = out.data_ptr() + 8 * r * nt
+            if keep_states:
+                states.append(out.cpu().numpy().copy())
+            continue
         torch.cuda.synchronize()
         slab.rhs_device(t0, u_prev.data_ptr(), p_prev.data_ptr(), rhs.data_ptr(), tau=tau)
         try:
