@@ -96,3 +96,17 @@ def test_mesh_dims_inferred_from_reference_operators(oracle, nx, ny):
     dims = (ctypes.c_int * 2)()
     _lib.check(_lib.lib().pdg_mesh_dims_from_operators(ctypes.byref(csr), rp.n_q, dims))
     assert (dims[0], dims[1]) == (nx, ny)
+
+
+def test_library_real_schur_on_random_matrices(tmp_path):
+    """The library's Hessenberg + Francis double-shift QR (csrc/timebasis.hpp), which stands where
+    the reference calls Eigen::RealSchur for r >= 2, on 360 seeded random matrices (n = 2..7, a
+    third of them symmetric so that every 2x2 block has to split): Q orthogonal and Q T Q^T = A to
+    1e-12, T quasi-upper-triangular, 2x2 blocks only for complex pairs. Host-only."""
+    import subprocess
+    exe = str(tmp_path / "schur_check")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "paper_1801_04984_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "integration", "schur_check.cpp"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "cases 360" in out.stdout and "bad_blocks 0" in out.stdout
