@@ -497,6 +497,10 @@ __global__ void k_rhs_u(Geo g, double* u) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 8LL * n; t += (long long)gridDim.x * blockDim.x) {
         const int c = static_cast<int>(t / 8), l = static_cast<int>(t % 8);
         const int i = c % g.nx, j = c / g.nx;
+        if (i > 0 && i < g.nx - 1 && j > 0 && j < g.ny - 1) {  // interior cell: no boundary face
+            u[t] = 0.0;
+            continue;
+        }
         const int cf[4] = {hface(g, i, j), hface(g, i, j + 1), vface(g, i, j), vface(g, i + 1, j)};
         const int a = l / 2, comp = l % 2;
         double r = 0.0;

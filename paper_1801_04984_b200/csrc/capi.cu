@@ -117,10 +117,28 @@ __device__ __forceinline__ double time_derivative_p(int c, double mb, double im,
     for (int k = et_off[c]; k < et_off[c + 1]; ++k) s = __dadd_rn(s, __dmul_rn(et_val[k], u[et_idx[k]]));
     return __dsub_rn(__dmul_rn(mb, s), __dmul_rn(im, __dmul_rn(m_p[c], p[c])));
 }
+// 8 lanes per cell: the lanes load the products e_k u_k of the cell's E^T row in parallel, lane 0
+// adds them in ascending k (the sequential sum of apply_transpose, same bits as one thread)
 __global__ void k_time_derivative(int np, double mb, double im, const int* et_off, const int* et_idx, const double* et_val,
                                   const double* m_p, const double* u, const double* p, double* out) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < np; c += gridDim.x * blockDim.x) {
-        out[c] = time_derivative_p(c, mb, im, et_off, et_idx, et_val, m_p, u, p);
+    const int sub = threadIdx.x & 7;
+    const unsigned gmask = 0xffu << (threadIdx.x & 24);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 8LL * ((np + 3) / 4 * 4);
+         t += (long long)gridDim.x * blockDim.x) {
+        const int c = static_cast<int>(t >> 3);
+        const bool live = c < np;
+        const int b = live ? et_off[c] : 0, e = live ? et_off[c + 1] : 0;
+        double s = 0.0;
+        for (int k0 = b; __any_sync(gmask, k0 < e); k0 += 8) {
+            const int k = k0 + sub;
+            const double prod = k < e ? __dmul_rn(et_val[k], u[et_idx[k]]) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double v = __shfl_sync(gmask, prod, (threadIdx.x & 24) + q);
+                if (k0 + q < e) s = __dadd_rn(s, v);
+            }
+        }
+        if (live && sub == 0) out[c] = __dsub_rn(__dmul_rn(mb, s), __dmul_rn(im, __dmul_rn(m_p[c], p[c])));
     }
 }
 // R_i = (tau w_i) [u;q;p]_i + phi0_i djump (p rows)   (slab.hpp:76-84)
@@ -903,7 +921,7 @@ int pdg_slab_solve_device(pdg_slab* s, const double* rhs_dev, double* out_dev, p
             if (g > 0)
                 for (int bi = 0; bi < m; ++bi) {
                     const double* yj = s->ysol.p + (long long)(i0 + bi) * nt;
-                    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p,
+                    k_time_derivative<<<grid_for(8LL * o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p,
                                                                              o.Et.val.p, o.m_p.p, yj, yj + o.n_u + o.n_q,
                                                                              s->dpt.p + (size_t)(i0 + bi) * o.n_p);
                     count_launch();
@@ -961,7 +979,7 @@ void slab_rhs_enqueue(pdg_slab* s, double t0, double tau, const double* u_prev_d
     for (int i = 0; i < nn; ++i)
         assemble_rhs_device(o, t0 + s->tc.nodes[i] * tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
                             s->rhs_p.p + (size_t)i * o.n_p, st);
-    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
+    k_time_derivative<<<grid_for(8LL * o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
                                                              o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
     k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, tau, s->d_w.p,
                                                                            s->d_phi0.p, s->rhs_u.p, s->rhs_q.p,
@@ -1036,7 +1054,7 @@ int pdg_slab_rhs_sampled_device(pdg_slab* s, double tau, const pdg_rhs_samples* 
     for (int i = 0; i < nn; ++i)
         assemble_rhs_sampled_device(o, samples[i], s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
                                     s->rhs_p.p + (size_t)i * o.n_p, st);
-    k_time_derivative<<<grid_for(o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
+    k_time_derivative<<<grid_for(8LL * o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
                                                              o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
     k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, tau, s->d_w.p,
                                                                            s->d_phi0.p, s->rhs_u.p, s->rhs_q.p,
