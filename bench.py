@@ -637,8 +637,9 @@ def main():
                         "d2h_bytes_per_step": solve_dist["h2d_bytes_per_step"]}
         else:
             parallelism = f"replicas x{world} (distributed leg failed)"
+    # (after an abandoned distributed leg the device may be blocked by a stuck collective: no more GPU work)
     spmv = spmv_sweep([int(s) for s in args.spmv_sizes.split(",") if s], args.spmv_reps, peak) \
-        if rank == 0 and args.spmv_sizes else []
+        if rank == 0 and args.spmv_sizes and not hung else []
     spmv_roof = None
     if spmv:
         big = spmv[-1]
