@@ -110,3 +110,44 @@ def test_library_real_schur_on_random_matrices(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "cases 360" in out.stdout and "bad_blocks 0" in out.stdout
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 3, 4, 5])
+def test_library_time_constants_match_oracle_host_only(oracle, r):
+    """pdg_time_constants / pdg_time_schur_blocks are host code: checked here without a GPU. Nodes,
+    weights, phi(0), G_hat agree with the oracle to roundoff (bit for bit for r <= 1, where T and Q
+    are compared directly too); for r >= 2 the ordered block structure and the block eigenvalues
+    agree and Q T Q^T = W."""
+    from paper_1801_04984_b200 import solver as S
+    lib, ref = S.time_constants(r), oracle.time_constants(r)
+    n = r + 1
+    for k in ("nodes", "weights", "phi_at0", "G_hat"):
+        assert np.allclose(lib[k], ref[k], rtol=1e-13, atol=1e-14), k
+    if r <= 1:
+        for k in ("nodes", "weights", "phi_at0", "T", "Q"):
+            assert np.array_equal(lib[k], ref[k]), k
+    sizes, starts = oracle.schur_blocks(r) if r >= 2 else (np.array([n]), np.array([0]))
+    assert np.array_equal(lib["block_sizes"], sizes) and np.array_equal(lib["block_starts"], starts)
+    W = lib["G_hat"] / lib["weights"][:, None]
+    assert abs(lib["Q"].T @ lib["Q"] - np.eye(n)).max() <= 1e-12
+    assert abs(lib["Q"] @ lib["T"] @ lib["Q"].T - W).max() <= 1e-10 * (1 + abs(W).max())
+    assert np.allclose(np.diag(lib["T"]), np.diag(ref["T"]), rtol=1e-11)
+
+
+def test_new_entry_points_reject_bad_arguments():
+    """Argument errors of the round-2 entry points surface as PDG_INVALID_ARGUMENT with a message,
+    before any device work (no GPU needed)."""
+    L = _lib.lib()
+    rep = _lib.Report()
+    assert L.pdg_slab_step_device(None, 0.0, 0.1, None, None, ctypes.byref(rep)) == _lib.PDG_INVALID_ARGUMENT
+    assert b"null" in L.pdg_last_error()
+    assert L.pdg_ops_assemble3(None, None, None) == _lib.PDG_INVALID_ARGUMENT
+    assert L.pdg_ops_upload3(None, 2, 2, 2, None, None, None, None, None, None, 0.8, 0.1, 2.0, None) == _lib.PDG_INVALID_ARGUMENT
+    assert L.pdg_ops_rhs_sampled(None, None, None, None, None) == _lib.PDG_INVALID_ARGUMENT
+    assert L.pdg_rhs_sample_points(None, None, None, None) == _lib.PDG_INVALID_ARGUMENT
+    nb = ctypes.c_int()
+    assert L.pdg_slab_block_reports(None, ctypes.byref(nb), None, None, None) == _lib.PDG_INVALID_ARGUMENT
+    buf = (ctypes.c_double * 64)()
+    assert L.pdg_time_constants(6, buf, buf, buf, buf, buf) == _lib.PDG_INVALID_ARGUMENT
+    assert L.pdg_time_constants(-1, buf, buf, buf, buf, buf) == _lib.PDG_INVALID_ARGUMENT
+    assert L.pdg_time_schur_blocks(2, None, None, None, None) == _lib.PDG_INVALID_ARGUMENT
