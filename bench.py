@@ -351,19 +351,18 @@ def config2_leg(n, steps, warmup, peak, local, which="config2"):
     except Exception:
         pass
     what = ("8 permeability layers" if which == "config2" else
-            "i.i.d. lognormal permeability (sigma 1.5); BASELINE config 4 at a REDUCED size: the exact "
-            "preconditioner does not exist at 96^3 (DESIGN.md section 8)")
-    return {"workload": f"{which}: 3D Biot {n}^3 hexahedra, dG({run['r']}), tau={tau}, GMRES(50) tol 1e-10, 1 fixed-stress sweep, "
-                        f"{what} (3D extension: the reference is 2D only, parity unpinned; checked "
-                        "against the 3D CPU restatement at 4^3 and 6^3 and by the discrete mass balance here)",
+            "lognormal K (sigma 1.5); config 4 at a REDUCED size (96^3 is out of reach of exact inner solves)")
+    phases = {k: {"ms": v["ms_per_step"], "GBs": v["achieved_GBs"]} for k, v in phases.items()
+              if k in ("spmv", "a_solve", "flow_solve")}
+    return {"workload": f"{which}: 3D Biot {n}^3 hexahedra, dG({run['r']}), tau={tau}, GMRES(50) tol 1e-10, {what}; "
+                        "3D extension, parity unpinned (DESIGN.md 3a)",
             "value": ms, "unit": "ms/slab", "steps": steps, "warmup": warmup,
             "e2e": {"value": float(np.mean(e2e[1:])), "unit": "ms/slab", "h2d_bytes_per_step": 8 * nn * nt,
                     "d2h_bytes_per_step": 8 * nn * nt},
             "iterations": [r.iterations for r in reps], "final_rel_res_max": max(r.final_relative_residual for r in reps),
             "mass_balance_rel": mass, "gpu_launches": int(launches),
             "sizes": {"n_u": ops.n_u, "n_q": ops.n_q, "n_p": ops.n_p, "nnz_A": ops.nnz["A"]},
-            "roofline": {"bound": "hbm", "kernel": "a_solve: k_nd_stream (nested-dissection displacement solve, streaming "
-                                                   "mode: one level kernel per depth and pass on the row-major factor)",
+            "roofline": {"bound": "hbm", "kernel": "a_solve: k_nd_stream (nested-dissection displacement solve, streaming mode)",
                          "achieved": a["achieved_GBs"], "peak": peak, "unit": "GB/s", "frac": a["achieved_GBs"] / peak,
                          "algorithmic_bytes_per_call": a["alg_GB_per_call"] * 1e9,
                          "share_of_step": a["ms_per_step"] / ms if ms else None, "traffic": traffic},
@@ -373,8 +372,7 @@ def config2_leg(n, steps, warmup, peak, local, which="config2"):
                       "flow_nd_analysis_s": round(st[4], 3), "flow_nd_factor_s": round(st[5], 3),
                       "device_memory_GiB": round((total - free) / 2**30, 1)},
             "cpu_baseline": None,
-            "cpu_baseline_note": "the oracle's exact inner solves do not reach 32^3 on the host (banded Cholesky of A: "
-                                 "154 GB); cpu_baseline_small times both sides on the same configuration at a size it reaches"}
+            "cpu_baseline_note": "the oracle cannot reach 32^3 (banded Cholesky of A: 154 GB); see cpu_baseline_small"}
 
 
 def config2_cpu_small(n, local):
@@ -398,8 +396,7 @@ def config2_cpu_small(n, local):
             "iterations": [int(i) for i in ref["iterations"]],
             "gpu_same_size_ms_per_slab": float(np.mean([r.device_ms for r in reps[1:]])),
             "gpu_iterations": [r.iterations for r in reps], "max_rel_l2_gpu_vs_oracle": diff,
-            "sample": f"3 slabs of config 2 at {n}^3 (first as warm-up; the oracle cannot reach 32^3), "
-                      "oracle = 3D CPU restatement with exact banded sparse-direct inner solves"}
+            "sample": f"3 slabs of config 2 at {n}^3 (first as warm-up), oracle = 3D CPU restatement, banded inner solves"}
 
 
 def main():
