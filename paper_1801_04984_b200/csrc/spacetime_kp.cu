@@ -175,6 +175,8 @@ struct KpArgs {
     int n_cells, nt, nu, nq;
     int cell0, cell1, tile0;  // cells [cell0, cell1) computed; tiles start at tile0 (multiple of 256)
     int per, qpt;             // blocks per tile (9 + qpt), QK blocks per tile
+    int pkfirst;
+    int heavy;                // > 0: the tiles' 9 UK / PK blocks come first in the grid (heavy = 9 tiles), the QK blocks after them
     long long nqs;            // QK slices scheduled (all, or the strip's list)
     const long long* qlist;   // strip: QK slice list
     int nx, ny, r0, r1;       // strip: face-row ownership of the flux rows
@@ -210,8 +212,21 @@ __device__ __forceinline__ void ld_slot(const double* __restrict__ p, long long 
 
 __device__ __forceinline__ double mac(double s, double v, double x) { return __dadd_rn(s, __dmul_rn(v, x)); }
 
-template <int M, bool DOTS, bool STRIP>
-__global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
+// PF (default; PDG_SPMV_PF=0 turns it off): the column headers of a thread's rows are loaded in
+// one batch up front, and the pressure entries of a displacement row in one batch, so a thread's
+// dependent-load chain is offsets -> headers -> one round per 8-column run instead of two rounds
+// per run and per entry; registers capped at 64 (4 CTAs per SM). The sums keep their order. With
+// the QK blocks at the end of the grid (and, on meshes whose x stays in L2 anyway, the PK
+// blocks - the longest threads - at its start), measured on B200: config 1 (128^2, one wave of
+// 768 CTAs) 45 -> 33 us per application, 256^2 0.81 -> 0.93, 512^2 0.84 -> 0.93, 1024^2 0.95 of HBM.
+constexpr int kPfRuns = 6, kPfEnt = 6, kPfFaces = 4;  // batch sizes (the 2D operator: 5 runs, 5 entries, 4 faces)
+constexpr int kKpPkFirstCells = 100000;               // PK blocks first up to this many cells
+#ifndef KP_MINB
+#define KP_MINB 4
+#endif
+
+template <int M, bool DOTS, bool STRIP, bool PF>
+__global__ void __launch_bounds__(kKpBlock, PF ? KP_MINB : 1) k_spmv_kp(const KpArgs a) {
     if (a.stop && *a.stop) return;
     double acc[kKpMaxDots];
 #pragma unroll
@@ -225,7 +240,22 @@ __global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
                 if (q < a.ncols) acc[q] += __ldg(&a.V[(long long)q * a.nrows + row]) * v;
         }
     };
-    const int tile = blockIdx.x / a.per, part = blockIdx.x - tile * a.per;
+    int tile, part;
+    if (a.heavy == 0) {
+        tile = blockIdx.x / a.per;
+        part = blockIdx.x - tile * a.per;
+    } else if ((int)blockIdx.x < a.heavy / 9 && a.pkfirst) {  // the PK blocks (longest threads) first
+        tile = blockIdx.x;
+        part = 8;
+    } else if ((int)blockIdx.x < a.heavy) {
+        const int ub = a.pkfirst ? blockIdx.x - a.heavy / 9 : blockIdx.x;
+        tile = a.pkfirst ? ub >> 3 : ub / 9;
+        part = a.pkfirst ? ub & 7 : ub - tile * 9;
+    } else {
+        const int qb = blockIdx.x - a.heavy;
+        tile = qb / a.qpt;
+        part = 9 + qb - tile * a.qpt;
+    }
     const int tbase = a.tile0 + tile * kKpTileCells;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* __restrict__ x = a.x;
@@ -241,8 +271,7 @@ __global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
 #pragma unroll
             for (int i = 0; i < M; ++i) s[i] = 0.0;
             const long long sb = vo * 8 + l;  // slot of entry k: sb + 8 k
-            for (int r = 0; r < na; ++r) {
-                const int base = __ldg(&a.uk_hdr[ho + r]);
+            auto run = [&](int r, int base) {
                 double v[8][M];
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) ld_slot<M>(a.uk_val, sb + 8LL * (8 * r + kk), v[kk]);
@@ -250,14 +279,41 @@ __global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
                 for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
                     for (int i = 0; i < M; ++i) s[i] = mac(s[i], v[kk][i], __ldg(&x[(long long)i * a.nt + base + kk]));
-            }
-            const int* __restrict__ ecol = a.uk_hdr + ho + na;
-            for (int e = 0; e < ne; ++e) {
+            };
+            auto ent = [&](int e, int col) {
                 double v[M];
                 ld_slot<M>(a.uk_val, sb + 8LL * (8 * na + e), v);
-                const int col = __ldg(&ecol[e]) + a.nu + a.nq;
 #pragma unroll
-                for (int i = 0; i < M; ++i) s[i] = mac(s[i], v[i], __ldg(&x[(long long)i * a.nt + col]));
+                for (int i = 0; i < M; ++i) s[i] = mac(s[i], v[i], __ldg(&x[(long long)i * a.nt + a.nu + a.nq + col]));
+            };
+            const int* __restrict__ hp = a.uk_hdr + ho;
+            if constexpr (PF) {
+                int hb[kPfRuns], ec[kPfEnt];
+#pragma unroll
+                for (int r = 0; r < kPfRuns; ++r) hb[r] = r < na ? __ldg(hp + r) : 0;
+#pragma unroll
+                for (int e = 0; e < kPfEnt; ++e) ec[e] = e < ne ? __ldg(hp + na + e) : 0;
+#pragma unroll
+                for (int r = 0; r < kPfRuns; ++r)
+                    if (r < na) run(r, hb[r]);
+                for (int r = kPfRuns; r < na; ++r) run(r, __ldg(hp + r));
+                double ev[kPfEnt][M], ex[kPfEnt][M];
+#pragma unroll
+                for (int e = 0; e < kPfEnt; ++e)
+                    if (e < ne) {
+                        ld_slot<M>(a.uk_val, sb + 8LL * (8 * na + e), ev[e]);
+#pragma unroll
+                        for (int i = 0; i < M; ++i) ex[e][i] = __ldg(&x[(long long)i * a.nt + a.nu + a.nq + ec[e]]);
+                    }
+#pragma unroll
+                for (int e = 0; e < kPfEnt; ++e)
+                    if (e < ne)
+#pragma unroll
+                        for (int i = 0; i < M; ++i) s[i] = mac(s[i], ev[e][i], ex[e][i]);
+                for (int e = kPfEnt; e < ne; ++e) ent(e, __ldg(hp + na + e));
+            } else {
+                for (int r = 0; r < na; ++r) run(r, __ldg(hp + r));
+                for (int e = 0; e < ne; ++e) ent(e, __ldg(hp + na + e));
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) out((long long)i * a.nt + 8 * c + l, s[i]);
@@ -275,11 +331,18 @@ __global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
 #pragma unroll
             for (int i = 0; i < M; ++i) s[i] = 0.0;
             long long k = vb * 32 + lane;  // slot index, advances by 32 per slot
+            int pb[kPfRuns], pf[kPfFaces];
+            if constexpr (PF) {
+#pragma unroll
+                for (int r = 0; r < kPfRuns; ++r) pb[r] = r < ne8 ? __ldcs(&hdr[32 * (1 + r)]) : 0;
+#pragma unroll
+                for (int b = 0; b < kPfFaces; ++b) pf[b] = b < nb ? __ldcs(&hdr[32 * (1 + ne8 + b)]) : 0;
+            }
+            const int* __restrict__ fc = hdr + 32 * (1 + ne8);
 #pragma unroll
             for (int j = 0; j < M; ++j) {
                 const double* __restrict__ xj = x + (long long)j * a.nt;
-                for (int r = 0; r < ne8; ++r) {
-                    const int base = __ldcs(&hdr[32 * (1 + r)]);
+                auto run = [&](int base) {
                     double v[8][M];
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) ld_slot<M>(a.pk_val, k + 32LL * kk, v[kk]);
@@ -290,22 +353,45 @@ __global__ void __launch_bounds__(kKpBlock) k_spmv_kp(const KpArgs a) {
 #pragma unroll
                         for (int i = 0; i < M; ++i) s[i] = mac(s[i], v[kk][i], xv);
                     }
-                }
-                const int* __restrict__ fc = hdr + 32 * (1 + ne8);
-                if constexpr (M == 2) {
-                    for (int b = 0; b < nb; b += 2) {
-                        double v[2];
-                        ld_slot<2>(a.pk_val, k, v);
-                        k += 32;
-                        s[j] = mac(s[j], v[0], __ldg(&xj[a.nu + __ldcs(&fc[32 * b])]));
-                        if (b + 1 < nb) s[j] = mac(s[j], v[1], __ldg(&xj[a.nu + __ldcs(&fc[32 * (b + 1)])]));
+                };
+                // the B^T entries of component j: row j only (m = 2: two entries per slot)
+                auto faces2 = [&](int b, int c0, int c1) {
+                    double v[2];
+                    ld_slot<2>(a.pk_val, k, v);
+                    k += 32;
+                    s[j] = mac(s[j], v[0], __ldg(&xj[a.nu + c0]));
+                    if (b + 1 < nb) s[j] = mac(s[j], v[1], __ldg(&xj[a.nu + c1]));
+                };
+                auto face1 = [&](int c0) {
+                    double v[1];
+                    ld_slot<1>(a.pk_val, k, v);
+                    k += 32;
+                    s[0] = mac(s[0], v[0], __ldg(&xj[a.nu + c0]));
+                };
+                if constexpr (PF) {
+#pragma unroll
+                    for (int r = 0; r < kPfRuns; ++r)
+                        if (r < ne8) run(pb[r]);
+                    for (int r = kPfRuns; r < ne8; ++r) run(__ldcs(&hdr[32 * (1 + r)]));
+                    if constexpr (M == 2) {
+#pragma unroll
+                        for (int b = 0; b < kPfFaces; b += 2)
+                            if (b < nb) faces2(b, pf[b], pf[b + 1]);
+                        for (int b = kPfFaces; b < nb; b += 2)
+                            faces2(b, __ldcs(&fc[32 * b]), b + 1 < nb ? __ldcs(&fc[32 * (b + 1)]) : 0);
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < kPfFaces; ++b)
+                            if (b < nb) face1(pf[b]);
+                        for (int b = kPfFaces; b < nb; ++b) face1(__ldcs(&fc[32 * b]));
                     }
                 } else {
-                    for (int b = 0; b < nb; ++b) {
-                        double v[1];
-                        ld_slot<1>(a.pk_val, k, v);
-                        k += 32;
-                        s[0] = mac(s[0], v[0], __ldg(&xj[a.nu + __ldcs(&fc[32 * b])]));
+                    for (int r = 0; r < ne8; ++r) run(__ldcs(&hdr[32 * (1 + r)]));
+                    if constexpr (M == 2) {
+                        for (int b = 0; b < nb; b += 2)
+                            faces2(b, __ldcs(&fc[32 * b]), b + 1 < nb ? __ldcs(&fc[32 * (b + 1)]) : 0);
+                    } else {
+                        for (int b = 0; b < nb; ++b) face1(__ldcs(&fc[32 * b]));
                     }
                 }
                 {
@@ -530,21 +616,36 @@ void SpaceTimeOp::kp_launch(const double* x, double* y, double* y2, const double
     a.partial = partial;
     const int grid = tiles * a.per;
     const bool dots = partial != nullptr;
+    static const int pf_env = std::getenv("PDG_SPMV_PF") ? std::atoi(std::getenv("PDG_SPMV_PF")) : 1;
+    const bool pf = pf_env != 0;
+    static const int ql_env = std::getenv("PDG_SPMV_QLAST") ? std::atoi(std::getenv("PDG_SPMV_QLAST")) : -1;
+    a.heavy = (ql_env >= 0 ? ql_env != 0 : pf) ? 9 * tiles : 0;
+    // PK blocks first while x stays in L2 anyway (measured: 256^2 0.855 -> 0.93 of HBM, 1024^2 0.954 -> 0.938)
+    static const int pk_env = std::getenv("PDG_SPMV_PKFIRST") ? std::atoi(std::getenv("PDG_SPMV_PKFIRST")) : -1;
+    a.pkfirst = pk_env >= 0 ? pk_env : (n_cells <= kKpPkFirstCells ? 1 : 0);
+#define PDG_KP_LAUNCH(M_, D_, S_)                                          \
+    do {                                                                   \
+        if (pf)                                                            \
+            k_spmv_kp<M_, D_, S_, true><<<grid, kKpBlock, 0, st>>>(a);     \
+        else                                                               \
+            k_spmv_kp<M_, D_, S_, false><<<grid, kKpBlock, 0, st>>>(a);    \
+    } while (0)
     if (m == 2) {
         if (strip)
-            k_spmv_kp<2, false, true><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(2, false, true);
         else if (dots)
-            k_spmv_kp<2, true, false><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(2, true, false);
         else
-            k_spmv_kp<2, false, false><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(2, false, false);
     } else {
         if (strip)
-            k_spmv_kp<1, false, true><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(1, false, true);
         else if (dots)
-            k_spmv_kp<1, true, false><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(1, true, false);
         else
-            k_spmv_kp<1, false, false><<<grid, kKpBlock, 0, st>>>(a);
+            PDG_KP_LAUNCH(1, false, false);
     }
+#undef PDG_KP_LAUNCH
     count_launch();
     PDG_CHECK_LAUNCH();
 }
