@@ -43,9 +43,18 @@ constexpr int kNdThreads = PDG_ND_THREADS;  // compute threads (tuning: tools/nd
 constexpr int kNdMaxRhs = 2;
 constexpr int kNdMaxTaskRows = 1024;  // rows of one task (the update-vector staging in shared memory)
 constexpr int kNdComputeWarps = kNdThreads / 32;
-constexpr int kNdPrepWarps = 2;  // input warps
+#ifndef PDG_ND_PREP
+#define PDG_ND_PREP 2
+#endif
+#ifndef PDG_ND_GATHER
+#define PDG_ND_GATHER 4
+#endif
+#ifndef PDG_ND_MINB
+#define PDG_ND_MINB 1
+#endif
+constexpr int kNdPrepWarps = PDG_ND_PREP;  // input warps
 constexpr int kNdBufs = PDG_ND_BUFS;     // pipeline slots (barrier sets); task buffers live in a FIFO arena
-constexpr int kNdGatherWarps = 4;  // dependency wait + dependent gather, tasks in order
+constexpr int kNdGatherWarps = PDG_ND_GATHER;  // dependency wait + dependent gather, tasks in order
 constexpr int kNdGatherThreads = 32 * kNdGatherWarps;
 constexpr int kNdWarpProducer = kNdComputeWarps;
 constexpr int kNdWarpStage = kNdWarpProducer + 1;
@@ -485,7 +494,7 @@ __host__ __device__ inline size_t nd_task_bytes(int max_tasks) { return ((size_t
 // signaller -> staging).
 __device__ __forceinline__ void gather_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNdGatherThreads) : "memory"); }
 
-__global__ void __launch_bounds__(kNdBlock, 1) k_nd_solve(NdArgs a) {
+__global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
     using namespace dev;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);  // [32]
@@ -1316,11 +1325,9 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         stage_bytes = static_cast<unsigned>(std::max<long long>(vmax >= 1024 ? 16384 : 12288, ((long long)vmax * 8 + 1023) / 1024 * 1024));
         if (const char* e = std::getenv("PDG_ND_STAGES")) stages = std::min(32, std::max(2, std::atoi(e)));
         if (const char* e = std::getenv("PDG_ND_STAGE_KB")) stage_bytes = 1024u * std::max(8, std::atoi(e));
-        int ctas_per_sm = 1;
+        int ctas_per_sm = PDG_ND_MINB;
         if (const char* e = std::getenv("PDG_ND_CTAS")) ctas_per_sm = std::max(1, std::atoi(e));
         grid = nsm * ctas_per_sm;
-        for (const auto& F : fronts)
-            require((long long)F.ldt * 8 <= stage_bytes, "nested dissection: front wider than a ring stage");
         std::vector<int> fwd_tasks(nf, 0), bwd_tasks(nf, 0);
         std::vector<bool> leaf(nf);
         for (int k = 0; k < nf; ++k) leaf[k] = children[k].empty();
@@ -1381,10 +1388,19 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             for (int k = 0; k < nf; ++k)
                 if (fronts[k].depth == local_depth) roots.push_back(k);
             const int nr = static_cast<int>(roots.size());
-            for (int j = 0; j < nr; ++j) cta_of[roots[j]] = static_cast<int>((long long)j * grid / std::max(nr, 1));
+            // PDG_ND_SPLIT_LOCAL: a local subtree on two CTAs (the root and its first child's subtree
+            // on one, the second child's subtree on the other) when the grid has room for it
+            const bool split_local = std::getenv("PDG_ND_SPLIT_LOCAL") && std::atoi(std::getenv("PDG_ND_SPLIT_LOCAL")) && 2 * nr <= grid;
+            const int slots = split_local ? grid / 2 : grid;
+            for (int j = 0; j < nr; ++j)
+                cta_of[roots[j]] = (split_local ? 2 : 1) * static_cast<int>((long long)j * slots / std::max(nr, 1));
             for (int d = local_depth + 1; d <= maxdepth; ++d)
                 for (int k = 0; k < nf; ++k)
-                    if (fronts[k].depth == d && parent[k] >= 0) cta_of[k] = cta_of[parent[k]];
+                    if (fronts[k].depth == d && parent[k] >= 0) {
+                        const int pk = parent[k];
+                        const bool second = split_local && d == local_depth + 1 && children[pk].size() > 1 && children[pk][1] == k;
+                        cta_of[k] = cta_of[pk] + (second ? 1 : 0);
+                    }
         }
         auto matrix_tasks = [&](int type, int depth) {
             std::vector<NdTask> ts;
@@ -1394,7 +1410,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 const int rows = type == 1 ? F.s + F.b : F.s;
                 const int ld = type == 1 ? F.ldm : F.ldt;
                 const long long base = type == 1 ? F.moff : F.mtoff;
-                const int rpc = static_cast<int>(stage_bytes / (8u * ld));
+                const int rpc = std::max(1, static_cast<int>(stage_bytes / (8u * ld)));  // (fronts outside this kernel may be wider)
                 // balanced over the CTAs: about level bytes / grid per task, 1..task_chunks chunks;
                 // a local front (one CTA runs its whole subtree) in as few tasks as the buffers allow
                 const int want = static_cast<int>(std::ceil(level_bytes(type, depth) / grid / stage_bytes));
@@ -1452,6 +1468,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         hybrid_top = local_depth - 1;
         split = hybrid || top_depth >= 0;
         auto in_chunks = [&](int d) { return d > top_depth && (d >= local_depth || !hybrid); };
+        for (const auto& F : fronts)
+            if (in_chunks(F.depth)) require((long long)F.ldt * 8 <= stage_bytes, "nested dissection: front wider than a ring stage");
         std::vector<std::vector<NdTask>> per_cta_b(split ? grid : 0);
         for (int d = maxdepth; d >= 0; --d) {
             if (!in_chunks(d)) continue;
@@ -1499,10 +1517,11 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         const size_t fixed = kNdHeader + nd_task_bytes(smem_tasks);
         size_t arena_min = std::max<size_t>(3 * max_buf, 48 * 1024);
         if (const char* e = std::getenv("PDG_ND_ARENA_KB")) arena_min = 1024 * (size_t)std::max(16, std::atoi(e));
-        require(fixed + arena_min + 2 * (size_t)stage_bytes <= 227 * 1024, "nested dissection: ring does not fit in shared memory");
-        stages = std::min<int>(stages, static_cast<int>((227 * 1024 - fixed - arena_min) / stage_bytes));
+        const size_t smem_cap = ctas_per_sm == 1 ? 227 * 1024 : (228 * 1024 / ctas_per_sm - 1024) / 128 * 128;
+        require(fixed + arena_min + 2 * (size_t)stage_bytes <= smem_cap, "nested dissection: ring does not fit in shared memory");
+        stages = std::min<int>(stages, static_cast<int>((smem_cap - fixed - arena_min) / stage_bytes));
         require(stages >= kNdComputeWarps, "nested dissection: ring shallower than the compute warps (stage size too large)");
-        const size_t arena = (227 * 1024 - fixed - (size_t)stages * stage_bytes) / 128 * 128;
+        const size_t arena = (smem_cap - fixed - (size_t)stages * stage_bytes) / 128 * 128;
         arena_bytes = arena;
         max_task_buf = max_buf;
         smem = fixed + (size_t)stages * stage_bytes + arena;
