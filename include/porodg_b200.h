@@ -103,6 +103,12 @@ typedef struct {
     int sweeps;     /* truncated fixed-stress sweeps per preconditioner call, default 1 */
     double stab;    /* < 0: b^2 / K_dr (fixed_stress.hpp:23-27) */
     int candidate;  /* 0: x + P(V y) as gmres.hpp:116 (reference); 1: x + Z y (gmres_flexible, gmres.hpp:113-114) */
+    int mode;       /* 0 parity (default): exact fp64 inner solves, as the reference's sparse-direct LU.
+                     * 1 fast (SURVEY 8(b) SolveOptions mode): the displacement factor of the streaming
+                     * nested-dissection solve (3D meshes) is STORED in fp32 - half the bytes of the
+                     * HBM-bound solve; sums stay fp64 and GMRES still iterates to the fp64 true-residual
+                     * tolerance, so the solution meets the same acceptance test while the iterates differ
+                     * from the reference's at the 1e-7 level of the preconditioner. No effect on 2D. */
 } pdg_gmres_opts;
 
 /* SolverReport (gmres.hpp:15-20) plus timings. */

@@ -44,6 +44,7 @@ struct SolveOptions {  // slab.hpp:123-127 (+ fixed_stress.hpp:17-22)
     int truncation_sweeps = 1;
     double stab = -1.0;      // < 0: b^2 / K_dr
     bool flexible = false;   // candidate x + Z y (gmres_flexible) instead of x + P(V y)
+    bool fast = false;       // pdg_gmres_opts.mode 1: fp32-stored displacement factor on 3D meshes
     pdg_gmres_opts c() const {
         pdg_gmres_opts o{};
         o.tol = gmres.tol;
@@ -52,6 +53,7 @@ struct SolveOptions {  // slab.hpp:123-127 (+ fixed_stress.hpp:17-22)
         o.sweeps = truncation_sweeps;
         o.stab = stab;
         o.candidate = flexible ? 1 : 0;
+        o.mode = fast ? 1 : 0;
         return o;
     }
 };

@@ -60,7 +60,7 @@ class RhsSamples(C.Structure):
 
 class GmresOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int), ("max_iter", C.c_int), ("sweeps", C.c_int),
-                ("stab", C.c_double), ("candidate", C.c_int)]
+                ("stab", C.c_double), ("candidate", C.c_int), ("mode", C.c_int)]
 
 
 class FsOpts(C.Structure):

@@ -566,7 +566,7 @@ void face_coords3(int nx, int ny, int nz, std::vector<double>& cx, std::vector<d
     }
 }
 
-std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st) {
+std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st, bool fp32_factor) {
     auto a = std::make_shared<ASolver>();
     if (ops.nz > 0) {
         // 3D: nested dissection over cells (24 dofs each, centres (i + 1/2, j + 1/2, k + 1/2))
@@ -583,6 +583,7 @@ std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaS
         }
         a->use_nd = true;
         a->nd.prof_phase = PROF_A_SOLVE;
+        a->nd.fp32_req = fp32_factor;
         a->nd.factor(ops.n_u, h.off, h.idx, h.val, node_of, cx, cy, nd_leaf_dofs(192), max_rhs, st, &cz);
         return a;
     }

@@ -25,7 +25,8 @@ struct ASolver {
             chol.solve(b, ldb, x, ldx, nrhs, st);
     }
 };
-std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st);
+// fp32_factor: fast mode (pdg_gmres_opts.mode 1), honoured by the streaming nested-dissection solve only
+std::shared_ptr<ASolver> make_a_solver(const SpatialOps& ops, int max_rhs, cudaStream_t st, bool fp32_factor = false);
 HCsr csr_download(const DCsr& a, cudaStream_t st);
 // flux Schur complement S_q = w M_q - w^2 B D^{-1} B^T (host CSR, face order), dinv = D^{-1}
 HCsr flow_schur_host(const SpatialOps& o, double w, const std::vector<double>& dinv, cudaStream_t st);

@@ -20,6 +20,7 @@ struct pdg_ctx {
 struct pdg_ops {
     SpatialOps s;
     std::shared_ptr<ASolver> a;  // shared displacement factorisation (slab.hpp:155)
+    std::shared_ptr<ASolver> a_fast;  // the same with the fp32-stored factor (pdg_gmres_opts.mode 1)
 };
 struct pdg_block {
     Block b;
@@ -636,9 +637,11 @@ int pdg_block_create(pdg_ops* ops, int m, const double* theta, double tau, doubl
     API_BEGIN
     require(ops && theta && opts && out, "pdg_block_create: null argument");
     PDG_CUDA(cudaSetDevice(ops->s.ctx->device));
-    if (!ops->a) ops->a = make_a_solver(ops->s, 2, ops->s.ctx->stream);
+    require(opts->mode == 0 || opts->mode == 1, "pdg_block_create: mode must be 0 (parity) or 1 (fast)");
+    auto& aslot = opts->mode == 1 ? ops->a_fast : ops->a;
+    if (!aslot) aslot = make_a_solver(ops->s, 2, ops->s.ctx->stream, opts->mode == 1);
     auto b = std::make_unique<pdg_block>();
-    b->b.create(ops->s, m, theta, tau, lambda_pre, *opts, ops->a);
+    b->b.create(ops->s, m, theta, tau, lambda_pre, *opts, aslot);
     const long long n = b->b.rows();
     b->io_a.alloc(n);
     b->io_b.alloc(n);

@@ -201,13 +201,14 @@ __global__ void k_nd_identity(int s, double* T) {
 }
 // M (row-major (s+b) x ldm) and M^T (row-major s x ldt) from Linv (s x s, col-major, ld s)
 // and G = L_BS Linv (b x s, col-major, ld b); padding zero.
-__global__ void k_nd_pack(int s, int b, const double* T, const double* G, double* M, int ldm, double* MT, int ldt) {
+template <typename OutT>
+__global__ void k_nd_pack(int s, int b, const double* T, const double* G, OutT* M, int ldm, OutT* MT, int ldt) {
     const long long tot = (long long)(s + b) * ldm;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
         const int r = static_cast<int>(t / ldm), c = static_cast<int>(t % ldm);
         double v = 0.0;
         if (c < s) v = r < s ? T[r + (long long)c * s] : G[(r - s) + (long long)c * b];
-        M[t] = v;
+        M[t] = static_cast<OutT>(v);
     }
     const long long tt = (long long)s * ldt;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tt; t += (long long)gridDim.x * blockDim.x) {
@@ -217,7 +218,7 @@ __global__ void k_nd_pack(int s, int b, const double* T, const double* G, double
             v = T[c + (long long)r * s];
         else if (c < s + b)
             v = G[(c - s) + (long long)r * b];
-        MT[t] = v;
+        MT[t] = static_cast<OutT>(v);
     }
 }
 
@@ -1034,8 +1035,9 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     factor_bytes = 0.0;
     vmax = 0;
     for (auto& F : fronts) {
-        F.ldm = static_cast<int>(round2(F.s));
-        F.ldt = static_cast<int>(round2(F.s + F.b));
+        // rows start on 16-byte boundaries: even lengths in fp64, multiples of 4 for an fp32 store
+        F.ldm = static_cast<int>(fp32_req ? (F.s + 3LL) & ~3LL : round2(F.s));
+        F.ldt = static_cast<int>(fp32_req ? (F.s + F.b + 3LL) & ~3LL : round2(F.s + F.b));
         F.moff = so;
         so += (long long)(F.s + F.b) * F.ldm;
         F.mtoff = so;
@@ -1043,7 +1045,6 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         factor_bytes += 8.0 * ((double)(F.s + F.b) * F.s * 2.0);
         vmax = std::max(vmax, F.ldt);
     }
-    store.alloc((size_t)so);
     // ---- numeric factorization (multifrontal, stream-serial, children first) ----
     std::vector<long long> fo(nf);
     long long ftot = 0, sbmax = 1;
@@ -1065,6 +1066,11 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         top_depth = -1;
         for (auto& o : fo) o = 0;  // front-relative positions: every front has its own allocation
     }
+    fp32 = fp32_req && stream;
+    if (fp32)
+        store32.alloc((size_t)so);
+    else
+        store.alloc((size_t)so);
     DBuf<double> dense(stream ? 1 : ftot);
     dense.zero(st);
     std::vector<long long> tstart(nf + 1, 0);  // streaming: the scatter entries of front k
@@ -1259,8 +1265,12 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                                   s, s, &one, Fk, f, T.p, s));
         if (b > 0)
             PDG_ND_CUBLAS(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, b, s, s, &one, Fk + s, f, T.p, s, &zero, G.p, b));
-        k_nd_pack<<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store.p + F.moff, F.ldm,
-                                                                      store.p + F.mtoff, F.ldt);
+        if (fp32)
+            k_nd_pack<float><<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store32.p + F.moff, F.ldm,
+                                                                                 store32.p + F.mtoff, F.ldt);
+        else
+            k_nd_pack<double><<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store.p + F.moff, F.ldm,
+                                                                                  store.p + F.mtoff, F.ldt);
         PDG_CHECK_LAUNCH();
     }
     if (stream) {  // the roots' front matrices, then the pool's cached blocks back to the driver

@@ -163,6 +163,10 @@ struct NdChol {
     // front matrix alive per pending update; one level kernel per depth and pass on the
     // row-major store. PDG_ND_STREAM=1/0 forces / forbids it.
     bool stream = false;
+    // fast mode (pdg_gmres_opts.mode 1): the streamed factor stored in fp32 (half the bytes); the
+    // factorization and all sums stay fp64. fp32 = fp32_req && stream.
+    bool fp32_req = false, fp32 = false;
+    DBuf<float> store32;
     std::vector<int> stream_off, stream_rpw;  // per level: first unit, rows per warp (8 | 4 | 2)
     DBuf<NdStreamUnit> d_sunits;
     void build_stream(cudaStream_t st);

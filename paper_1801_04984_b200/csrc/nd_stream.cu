@@ -33,6 +33,7 @@ struct StreamArgs {
     const int* bpos;
     const int* cbdst;
     const double* store;
+    const float* store32;  // fast mode: the factor stored in fp32 (store is null)
     const double* b;
     long long ldb;
     double* x;
@@ -45,10 +46,35 @@ struct StreamArgs {
     const int* stop;
 };
 
+// 16-byte packets of the factor store: 2 fp64 or (fast mode) 4 fp32 entries; sums in fp64
+template <typename T>
+struct Pkt;
+template <>
+struct Pkt<double> {
+    using V = double2;
+    static constexpr int N = 2;
+    static __device__ __forceinline__ double mac(const V& m, const double* v, double acc) {
+        const double2 w = *reinterpret_cast<const double2*>(v);
+        return fma(m.y, w.y, fma(m.x, w.x, acc));
+    }
+};
+template <>
+struct Pkt<float> {
+    using V = float4;
+    static constexpr int N = 4;
+    static __device__ __forceinline__ double mac(const V& m, const double* v, double acc) {
+        const double2 w0 = *reinterpret_cast<const double2*>(v), w1 = *reinterpret_cast<const double2*>(v + 2);
+        return fma((double)m.w, w1.y, fma((double)m.z, w1.x, fma((double)m.y, w0.y, fma((double)m.x, w0.x, acc))));
+    }
+};
+
 // RPW rows per warp: a unit has up to 8 * RPW rows (64 by default; 32 or 16 on levels with few
 // units, where more CTAs keep more bytes in flight)
-template <int NR, int RPW>
+template <int NR, int RPW, typename T>
 __global__ void __launch_bounds__(kSThreads, 4) k_nd_stream(StreamArgs a, int u0) {
+    using P = Pkt<T>;
+    using V = typename P::V;
+    constexpr int PN = P::N;
     if (a.stop && *a.stop) return;  // speculative GMRES step after the cycle ended
     __shared__ double vs[NR][kSTile];
     __shared__ NdStreamUnit Us;
@@ -65,11 +91,12 @@ __global__ void __launch_bounds__(kSThreads, 4) k_nd_stream(StreamArgs a, int u0
 #pragma unroll
         for (int k = 0; k < NR; ++k) acc[j][k] = 0.0;
     const int rw = warp * RPW;  // this warp's first row within the unit
-    const double* rowp = a.store + U.src + (long long)(U.r0 + rw) * U.ld;
+    const T* store = sizeof(T) == 8 ? reinterpret_cast<const T*>(a.store) : reinterpret_cast<const T*>(a.store32);
+    const T* rowp = store + U.src + (long long)(U.r0 + rw) * U.ld;
     for (int c0 = U.cbeg; c0 < U.ncols; c0 += kSTile) {
         const int nc = min(kSTile, U.ncols - c0);
         // ---- the input vector tile ----
-        for (int c = tid; c < ((nc + 1) & ~1); c += kSThreads) {
+        for (int c = tid; c < ((nc + PN - 1) & ~(PN - 1)); c += kSThreads) {
             const int gc = c0 + c;
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
@@ -88,37 +115,35 @@ __global__ void __launch_bounds__(kSThreads, 4) k_nd_stream(StreamArgs a, int u0
         }
         __syncthreads();
         // ---- RPW rows per warp against the tile ----
-        const int np = (nc + 1) >> 1;
+        const int np = (nc + PN - 1) / PN;
         const int nrw = min(RPW, U.nrows - rw);  // rows of this warp (<= 0: none)
         if (nrw == RPW) {
             constexpr int UN = 8 / RPW;  // 8 16-byte loads in flight per lane
             int p = lane;
             if constexpr (UN > 1)
             for (; p + 32 * (UN - 1) < np; p += 32 * UN) {
-                double2 m[UN][RPW];
+                V m[UN][RPW];
 #pragma unroll
                 for (int q = 0; q < UN; ++q)
 #pragma unroll
                     for (int j = 0; j < RPW; ++j)
-                        m[q][j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p + 32 * q);
+                        m[q][j] = __ldcs(reinterpret_cast<const V*>(rowp + (long long)j * U.ld + c0) + p + 32 * q);
 #pragma unroll
                 for (int q = 0; q < UN; ++q)
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {
-                        const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * (p + 32 * q)]);
 #pragma unroll
-                        for (int j = 0; j < RPW; ++j) acc[j][k] = fma(m[q][j].y, v.y, fma(m[q][j].x, v.x, acc[j][k]));
+                        for (int j = 0; j < RPW; ++j) acc[j][k] = P::mac(m[q][j], &vs[k][PN * (p + 32 * q)], acc[j][k]);
                     }
             }
             for (; p < np; p += 32) {
-                double2 m[RPW];
+                V m[RPW];
 #pragma unroll
-                for (int j = 0; j < RPW; ++j) m[j] = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
+                for (int j = 0; j < RPW; ++j) m[j] = __ldcs(reinterpret_cast<const V*>(rowp + (long long)j * U.ld + c0) + p);
 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
-                    const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * p]);
 #pragma unroll
-                    for (int j = 0; j < RPW; ++j) acc[j][k] = fma(m[j].y, v.y, fma(m[j].x, v.x, acc[j][k]));
+                    for (int j = 0; j < RPW; ++j) acc[j][k] = P::mac(m[j], &vs[k][PN * p], acc[j][k]);
                 }
             }
         } else if (nrw > 0) {
@@ -126,12 +151,9 @@ __global__ void __launch_bounds__(kSThreads, 4) k_nd_stream(StreamArgs a, int u0
 #pragma unroll
                 for (int j = 0; j < RPW; ++j) {
                     if (j < nrw) {
-                        const double2 mv = __ldcs(reinterpret_cast<const double2*>(rowp + (long long)j * U.ld + c0) + p);
+                        const V mv = __ldcs(reinterpret_cast<const V*>(rowp + (long long)j * U.ld + c0) + p);
 #pragma unroll
-                        for (int k = 0; k < NR; ++k) {
-                            const double2 v = *reinterpret_cast<const double2*>(&vs[k][2 * p]);
-                            acc[j][k] = fma(mv.y, v.y, fma(mv.x, v.x, acc[j][k]));
-                        }
+                        for (int k = 0; k < NR; ++k) acc[j][k] = P::mac(mv, &vs[k][PN * p], acc[j][k]);
                     }
                 }
             }
@@ -200,8 +222,8 @@ void NdChol::build_stream(cudaStream_t st) {
                 // L_SS^{-1} is lower triangular: a forward row r < s has entries in columns <= r, a
                 // backward row r (of L_SS^{-T} | G^T) in columns >= r; the exact zeros are not read
                 u.ncols = type == 1 ? (r0 + u.nrows <= F.s ? r0 + u.nrows : F.s) : F.s + F.b;
-                u.cbeg = type == 1 ? 0 : (r0 & ~1);
-                read_bytes += 8.0 * u.nrows * (u.ncols - u.cbeg);
+                u.cbeg = type == 1 ? 0 : (fp32 ? (r0 & ~3) : (r0 & ~1));
+                read_bytes += (fp32 ? 4.0 : 8.0) * u.nrows * (u.ncols - u.cbeg);
                 u.ld = type == 1 ? F.ldm : F.ldt;
                 u.s = F.s;
                 u.b = F.b;
@@ -221,21 +243,27 @@ void NdChol::build_stream(cudaStream_t st) {
 }
 
 void NdChol::solve_stream(const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st) {
-    StreamArgs a{d_sunits.p, sdofs.p, bpos.p, cbdst.p, store.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, cbtot, n, guard};
+    StreamArgs a{d_sunits.p, sdofs.p, bpos.p, cbdst.p, store.p, store32.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, cbtot, n, guard};
     const int nl = static_cast<int>(stream_off.size()) - 1;
+    auto launch = [&](auto tag, int nu, int u0, int rpw) {
+        using T = decltype(tag);
+        if (nrhs == 1) {
+            if (rpw == 8) k_nd_stream<1, 8, T><<<nu, kSThreads, 0, st>>>(a, u0);
+            else if (rpw == 4) k_nd_stream<1, 4, T><<<nu, kSThreads, 0, st>>>(a, u0);
+            else k_nd_stream<1, 2, T><<<nu, kSThreads, 0, st>>>(a, u0);
+        } else {
+            if (rpw == 8) k_nd_stream<2, 8, T><<<nu, kSThreads, 0, st>>>(a, u0);
+            else if (rpw == 4) k_nd_stream<2, 4, T><<<nu, kSThreads, 0, st>>>(a, u0);
+            else k_nd_stream<2, 2, T><<<nu, kSThreads, 0, st>>>(a, u0);
+        }
+    };
     for (int l = 0; l < nl; ++l) {
         const int u0 = stream_off[l], nu = stream_off[l + 1] - u0;
         if (nu == 0) continue;
-        const int rpw = stream_rpw[l];
-        if (nrhs == 1) {
-            if (rpw == 8) k_nd_stream<1, 8><<<nu, kSThreads, 0, st>>>(a, u0);
-            else if (rpw == 4) k_nd_stream<1, 4><<<nu, kSThreads, 0, st>>>(a, u0);
-            else k_nd_stream<1, 2><<<nu, kSThreads, 0, st>>>(a, u0);
-        } else {
-            if (rpw == 8) k_nd_stream<2, 8><<<nu, kSThreads, 0, st>>>(a, u0);
-            else if (rpw == 4) k_nd_stream<2, 4><<<nu, kSThreads, 0, st>>>(a, u0);
-            else k_nd_stream<2, 2><<<nu, kSThreads, 0, st>>>(a, u0);
-        }
+        if (fp32)
+            launch(float{}, nu, u0, stream_rpw[l]);
+        else
+            launch(double{}, nu, u0, stream_rpw[l]);
         count_launch(1);
     }
     PDG_CHECK_LAUNCH();

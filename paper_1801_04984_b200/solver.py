@@ -65,12 +65,16 @@ class SolveOptions:
     fs: FixedStressConfig = field(default_factory=FixedStressConfig)
     # "reference": candidate x + P(V y) (gmres.hpp:116); "flexible": x + Z y (gmres_flexible)
     candidate: str = "reference"
+    # "parity": exact fp64 inner solves (the reference's sparse-direct LU); "fast": the streamed
+    # displacement factor of 3D meshes stored in fp32 (pdg_gmres_opts.mode; no effect in 2D)
+    mode: str = "parity"
 
     def to_struct(self):
         o = _lib.GmresOpts()
         o.tol, o.restart, o.max_iter = self.gmres.tol, self.gmres.restart, self.gmres.max_iter
         o.sweeps, o.stab = self.fs.truncation_sweeps, self.fs.stab
         o.candidate = {"reference": 0, "flexible": 1}[self.candidate]
+        o.mode = {"parity": 0, "fast": 1}[self.mode]
         return o
 
 

@@ -178,7 +178,8 @@ def test_nd_streaming_mode_matches_default(oracle, monkeypatch, dim):
     opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
     blk = S.BlockSolver(ops, T, tau, opt=opt)
     monkeypatch.setenv("PDG_ND_STREAM", "1")
-    blk_s = S.BlockSolver(ops, T, tau, opt=opt)
+    ops_s = S.SpatialOperators.assemble(spec)  # its own operators: the displacement factorization is cached per handle
+    blk_s = S.BlockSolver(ops_s, T, tau, opt=opt)
     monkeypatch.delenv("PDG_ND_STREAM")
     rvec = P.uniform_vector(9, blk.rows)
     z, zs = blk.precondition(rvec), blk_s.precondition(rvec)
@@ -191,6 +192,49 @@ def test_nd_streaming_mode_matches_default(oracle, monkeypatch, dim):
     assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(x)
     xr, _ = rp.block_solve(r, tau, rhs, tol=1e-10, restart=50, backend=1, flexible=True)
     assert np.linalg.norm(xs - xr) <= SOLVE_RTOL * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("r", [0, 1])
+def test_fast_mode_fp32_factor(oracle, monkeypatch, r):
+    """pdg_gmres_opts.mode 1 (SURVEY 8(b) SolveOptions mode = fast): the streamed displacement factor
+    stored in fp32, sums in fp64. The preconditioner differs from the exact one at the fp32 level
+    (so the path really ran), GMRES reaches the same fp64 true-residual tolerance within one extra
+    iteration, the solution is within 1e-8 of the parity mode's and of the oracle's, and repeats
+    are bit-identical. Parity mode on the same operators is untouched (its own factorization)."""
+    spec = P.config2(6)
+    rp = oracle.RefProblem(spec.to_dict())
+    T = oracle.time_constants(r)["T"]
+    tau = 0.05
+    monkeypatch.setenv("PDG_ND_STREAM", "1")
+    ops = S.SpatialOperators.assemble(spec)
+    par = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
+    fast = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible", mode="fast")
+    blk = S.BlockSolver(ops, T, tau, opt=par)
+    blk_f = S.BlockSolver(ops, T, tau, opt=fast)
+    monkeypatch.delenv("PDG_ND_STREAM")
+    rvec = P.uniform_vector(9, blk.rows)
+    z, zf = blk.precondition(rvec), blk_f.precondition(rvec)
+    nu = ops.n_u  # the displacement part of component 0 (the flux and pressure parts do not use the factor)
+    dz = np.linalg.norm(z[:nu] - zf[:nu]) / np.linalg.norm(z[:nu])
+    assert 1e-10 < dz < 1e-5, dz  # fp32-stored factor: different from, and close to, the exact solve
+    assert np.array_equal(zf, blk_f.precondition(rvec))
+    assert np.array_equal(z, blk.precondition(rvec))
+    rhs = P.uniform_vector(10, blk.rows)
+    x, rep = blk.solve(rhs)
+    xf, repf = blk_f.solve(rhs)
+    assert repf.converged and repf.final_relative_residual <= 1e-10
+    assert rep.iterations <= repf.iterations <= rep.iterations + 1, (rep.iterations, repf.iterations)
+    assert np.linalg.norm(x - xf) <= 1e-8 * np.linalg.norm(x)
+    xr, _ = rp.block_solve(r, tau, rhs, tol=1e-10, restart=50, backend=1, flexible=True)
+    assert np.linalg.norm(xf - xr) <= 1e-8 * np.linalg.norm(xr)
+    import ctypes as C
+    from paper_1801_04984_b200 import _lib
+    bad = par.to_struct()
+    bad.mode = 7
+    h = C.c_void_p()
+    th = np.ones(1)
+    with pytest.raises(_lib.InvalidArgument):
+        _lib.check(_lib.lib().pdg_block_create(ops._h, 1, th.ctypes.data_as(_lib.DP), tau, 1.0, C.byref(bad), C.byref(h)))
 
 
 @pytest.mark.parametrize("candidate", ["reference", "flexible"])
