@@ -706,7 +706,17 @@ def main():
         try:
             cfg4 = config2_leg(args.config4_n, 8, 1, peak, local, which="config4")
             cfg4.pop("cpu_baseline_note", None)
-            cfg4.pop("_state", None)
+            s0 = cfg4.pop("_state", None)
+            import gc
+            gc.collect()
+            torch.cuda.empty_cache()
+            fast = config2_leg(args.config4_n, 8, 1, peak, local, which="config4", mode="fast")
+            s1 = fast.pop("_state")
+            cfg4["fast_mode"] = {"what": "pdg_gmres_opts.mode 1 (opt-in, NOT the headline): fp32-stored displacement factor",
+                                 "value": fast["value"], "unit": "ms/slab", "iterations": fast["iterations"],
+                                 "final_rel_res_max": fast["final_rel_res_max"],
+                                 "max_rel_l2_vs_parity": float(np.linalg.norm(s1 - s0) / np.linalg.norm(s0)),
+                                 "a_solve_GBs": fast["roofline"]["achieved"], "a_solve_frac": fast["roofline"]["frac"]}
         except Exception as e:
             cfg4 = {"error": repr(e)[:300]}
     if rank == 0:
