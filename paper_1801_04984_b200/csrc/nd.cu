@@ -4,6 +4,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cmath>
 #include <numeric>
@@ -1214,6 +1215,20 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         for (int d = 0; d <= maxdepth; ++d)
             if (level_first[d] >= 0 && batched[level_first[d]]) level_first[d] = -2 - level_desc0[d];
     }
+    // PDG_ND_FACTOR_TIMING: host-synchronised time and flops per library call type (diagnostic)
+    const bool ftime = std::getenv("PDG_ND_FACTOR_TIMING") != nullptr;
+    double fsec[6] = {0, 0, 0, 0, 0, 0}, fflop[6] = {0, 0, 0, 0, 0, 0};
+    std::chrono::steady_clock::time_point ft0;
+    auto tick = [&](int which, double flops = 0.0) {
+        if (!ftime) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        if (which >= 0) {
+            fsec[which] += std::chrono::duration<double>(now - ft0).count();
+            fflop[which] += flops;
+        }
+        ft0 = now;
+    };
     for (int k : porder) {
         const NdFront& F = fronts[k];
         const int s = F.s, b = F.b, f = s + b;
@@ -1252,19 +1267,25 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 fptr[c] = nullptr;
             }
         }
+        tick(-1);
         PDG_ND_CUSOLVER(cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, s, Fk, f, work.p, lwork, info.p + k));
+        tick(0, (double)s * s * s / 3.0);
         if (b > 0) {
             PDG_ND_CUBLAS(cublasDtrsm(h.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
                                       CUBLAS_DIAG_NON_UNIT, b, s, &one, Fk, f, Fk + s, f));
+            tick(1, (double)b * s * s);
             PDG_ND_CUBLAS(cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, b, s, &mone, Fk + s, f, &one,
                                       Fk + s + (long long)s * f, f));
+            tick(2, (double)b * b * s);
         }
         k_nd_identity<<<grid_for((long long)s * s, 256), 256, 0, st>>>(s, T.p);
         PDG_CHECK_LAUNCH();
         PDG_ND_CUBLAS(cublasDtrsm(h.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
                                   s, s, &one, Fk, f, T.p, s));
+        tick(3, (double)s * s * s);
         if (b > 0)
             PDG_ND_CUBLAS(cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, b, s, s, &one, Fk + s, f, T.p, s, &zero, G.p, b));
+        tick(4, 2.0 * b * s * s);
         if (fp32)
             k_nd_pack<float><<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store32.p + F.moff, F.ldm,
                                                                                  store32.p + F.mtoff, F.ldt);
@@ -1272,6 +1293,13 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             k_nd_pack<double><<<grid_for((long long)f * F.ldm, 256), 256, 0, st>>>(s, b, T.p, G.p, store.p + F.moff, F.ldm,
                                                                                   store.p + F.mtoff, F.ldt);
         PDG_CHECK_LAUNCH();
+        tick(5);
+    }
+    if (ftime) {
+        const char* nm[6] = {"potrf", "trsm L_BS", "syrk", "trsm L^-1", "gemm G", "alloc/scatter/extend-add/pack"};
+        for (int i = 0; i < 6; ++i)
+            std::fprintf(stderr, "nd factor %-30s %8.3f s %9.2f TFLOP %7.2f TFLOP/s\n", nm[i], fsec[i], fflop[i] / 1e12,
+                         fsec[i] > 0 ? fflop[i] / fsec[i] / 1e12 : 0.0);
     }
     if (stream) {  // the roots' front matrices, then the pool's cached blocks back to the driver
         for (int k = 0; k < nf; ++k)
