@@ -1,11 +1,14 @@
 // Host C++ over the C ABI, 3D extension: a BASELINE config-2-type problem (n^3 hexahedra,
 // dG(0), fixed bottom, loaded drained top, 8 permeability layers) assembled on the device
-// and solved for its first slab. Build:
+// and solved for its first slab; a second argument "fast" selects SolveOptions::fast (the
+// fp32-stored streaming factor; it only differs from parity mode where the displacement solve
+// streams, i.e. from about 14^3). Build:
 //   g++ -std=c++17 -O2 -I include examples/slab_solve3d.cpp
 //       -L paper_1801_04984_b200/_lib -lporodg_b200 -Wl,-rpath,$PWD/paper_1801_04984_b200/_lib
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "porodg_b200.hpp"
@@ -13,6 +16,7 @@
 int main(int argc, char** argv) {
     using namespace porodg_b200;
     const int n = argc > 1 ? std::atoi(argv[1]) : 8;
+    const bool fast = argc > 2 && std::string(argv[2]) == "fast";
     pdg_problem3 p{};
     p.nx = p.ny = p.nz = n;
     p.lx = p.ly = p.lz = 1.0;
@@ -42,6 +46,7 @@ int main(int argc, char** argv) {
         const double tau = 0.1;
         SolveOptions opt;
         opt.gmres.restart = 50;
+        opt.fast = fast;
         SlabSolver slab(ops, 0, tau, opt);
         // first slab from rest: R = tau b(t_1) (slab.hpp:76-84 with zero jump data)
         std::vector<double> rhs(nt);
@@ -57,7 +62,7 @@ int main(int argc, char** argv) {
         const int worst_it = rep.iterations;
         double uz_min = 0.0;
         for (long long i = 2; i < sz[0]; i += 3) uz_min = std::fmin(uz_min, x[i]);
-        std::printf("config2-type %d^3: n_total=%lld iterations=%d mass max|res|/scale=%.3e min u_z=%.6e\n", n, nt, worst_it,
+        std::printf("config2-type %d^3 (%s mode): n_total=%lld iterations=%d mass max|res|/scale=%.3e min u_z=%.6e\n", n, fast ? "fast" : "parity", nt, worst_it,
                     worst_mass, uz_min);
         return 0;
     } catch (const std::exception& e) {

@@ -53,6 +53,14 @@ def test_cpp_host_layer_solves_3d_slab(tmp_path):
     assert "iterations=4" in out.stdout
     assert float(out.stdout.split("max|res|/scale=")[1].split()[0]) < 1e-8
     assert float(out.stdout.split("min u_z=")[1].split()[0]) < 0.0
+    # SolveOptions::fast through the C++ layer, at a size whose displacement solve streams (16^3)
+    uz = {}
+    for mode in ("parity", "fast"):
+        o = subprocess.run([_build3d(tmp_path), "16", mode], capture_output=True, text=True, timeout=300)
+        assert o.returncode == 0, o.stdout + o.stderr
+        assert f"({mode} mode)" in o.stdout and "iterations=4" in o.stdout
+        uz[mode] = float(o.stdout.split("min u_z=")[1].split()[0])
+    assert abs(uz["fast"] - uz["parity"]) <= 1e-6 * abs(uz["parity"])
 
 
 def _build_adapter(tmp_path):
