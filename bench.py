@@ -733,6 +733,9 @@ def main():
                        "gmres_candidate": "flexible: x + Z y (gmres_flexible, gmres.hpp:113-114; 20-slab oracle "
                                           "parity tested for both candidates)",
                        "l2": "no flush: per-step working set (nested-dissection factor matrices 0.73 GB) > 126 MB L2",
+                       "step": "pdg_slab_step_device: slab right-hand side from the previous end trace (the load vector of "
+                               "the constant boundary data is time-independent and assembled once per handle), Schur "
+                               "transform, GMRES block solve, back-transform",
                        "parallelism": parallelism},
             "e2e": e2e_line, "replicas": replicas,
             "value_reference_candidate": {"value": ms_ref, "unit": "ms/slab", "iterations": ref_run["iters"],

@@ -61,6 +61,7 @@ struct pdg_slab {
     DBuf<double> dpt;  // D y_j (p rows) of the solved components, n x n_p
     DBuf<double> d_T;  // the Schur form's T on the device (back-substitution couplings)
     DBuf<double> zero_state;  // n_total zeros: the initial data of pdg_slab_step_device(prev = NULL)
+    bool rhs_const = false;   // rhs_u / rhs_q / rhs_p hold b(t) of the problem's constant boundary data (time-independent)
 };
 
 #define API_BEGIN try {
@@ -979,9 +980,15 @@ void slab_rhs_enqueue(pdg_slab* s, double t0, double tau, const double* u_prev_d
         s->djump.alloc(o.n_p);
     }
     ProfScope prof(PROF_SLAB, st, 8.0 * 2 * nn * o.n_total());
-    for (int i = 0; i < nn; ++i)
-        assemble_rhs_device(o, t0 + s->tc.nodes[i] * tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
-                            s->rhs_p.p + (size_t)i * o.n_p, st);
+    // b(t_i) of the problem description: constant boundary data, so the same vector at every node and
+    // slab (assemble_rhs_device ignores t); assembled once per handle, as long as nothing else
+    // (the sampled variant) overwrites the buffers
+    if (!s->rhs_const) {
+        for (int i = 0; i < nn; ++i)
+            assemble_rhs_device(o, t0 + s->tc.nodes[i] * tau, s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
+                                s->rhs_p.p + (size_t)i * o.n_p, st);
+        s->rhs_const = true;
+    }
     k_time_derivative<<<grid_for(8LL * o.n_p, 256), 256, 0, st>>>(o.n_p, -o.biot_b, o.inv_m, o.Et.off.p, o.Et.idx.p, o.Et.val.p,
                                                              o.m_p.p, u_prev_dev, p_prev_dev, s->djump.p);
     k_slab_rhs<<<grid_for((long long)nn * o.n_total(), 256), 256, 0, st>>>(nn, o.n_u, o.n_q, o.n_p, tau, s->d_w.p,
@@ -1054,6 +1061,7 @@ int pdg_slab_rhs_sampled_device(pdg_slab* s, double tau, const pdg_rhs_samples* 
         s->rhs_p.alloc((size_t)nn * o.n_p);
         s->djump.alloc(o.n_p);
     }
+    s->rhs_const = false;  // the buffers no longer hold the constant-data vectors
     for (int i = 0; i < nn; ++i)
         assemble_rhs_sampled_device(o, samples[i], s->rhs_u.p + (size_t)i * o.n_u, s->rhs_q.p + (size_t)i * o.n_q,
                                     s->rhs_p.p + (size_t)i * o.n_p, st);
