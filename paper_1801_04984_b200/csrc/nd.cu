@@ -930,17 +930,22 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     }
     std::vector<int> aoff(nn + 1, 0), adj;
     {
-        std::vector<std::vector<int>> nb(nn);
-        for (int d = 0; d < n; ++d)
-            for (int k = off[d]; k < off[d + 1]; ++k) {
-                const int e = node_of[idx[k]];
-                if (e != node_of[d]) nb[node_of[d]].push_back(e);
-            }
+        // one pass over the nonzeros, a neighbour recorded the first time a node's rows meet it
+        std::vector<int> mark(nn, -1);
         for (int u = 0; u < nn; ++u) {
-            std::sort(nb[u].begin(), nb[u].end());
-            nb[u].erase(std::unique(nb[u].begin(), nb[u].end()), nb[u].end());
-            aoff[u + 1] = aoff[u] + static_cast<int>(nb[u].size());
-            adj.insert(adj.end(), nb[u].begin(), nb[u].end());
+            const size_t start = adj.size();
+            for (int q = noff[u]; q < noff[u + 1]; ++q) {
+                const int d = nlist[q];
+                for (int k = off[d]; k < off[d + 1]; ++k) {
+                    const int e = node_of[idx[k]];
+                    if (e != u && mark[e] != u) {
+                        mark[e] = u;
+                        adj.push_back(e);
+                    }
+                }
+            }
+            std::sort(adj.begin() + start, adj.end());
+            aoff[u + 1] = static_cast<int>(adj.size());
         }
     }
     // ---- dissection ----
@@ -1081,6 +1086,8 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
     {
         std::vector<long long> tpos;
         std::vector<double> tval;
+        tpos.reserve(idx.size() / 2 + n);  // the lower triangle
+        tval.reserve(idx.size() / 2 + n);
         for (int k = 0; k < nf; ++k) {
             const NdFront& F = fronts[k];
             const long long f = F.s + F.b;
@@ -1186,6 +1193,19 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             for (int k = level_first[d]; k >= 0 && k < level_first[d] + level_count[d]; ++k)
                 fmax = std::max(fmax, fronts[k].s + fronts[k].b);
             if (level_count[d] < 32 || fmax > 1536) continue;
+            // one CTA per front pays while its rank-1 updates (~1.45 ns per 1000 s f^2, measured at
+            // config 1: 6 / 26 / 50 ms for the levels of 128 / 64 / 32 fronts) stay below the
+            // library path's ~0.25 ms of launches per front (PDG_ND_FACTOR_BATCH_COST=0: always batch)
+            {
+                double sf2 = 0.0;
+                for (int k = level_first[d]; k < level_first[d] + level_count[d]; ++k) {
+                    const double f = fronts[k].s + fronts[k].b;
+                    sf2 = std::max(sf2, fronts[k].s * f * f);
+                }
+                const bool cost_rule = !(std::getenv("PDG_ND_FACTOR_BATCH_COST") && std::atoi(std::getenv("PDG_ND_FACTOR_BATCH_COST")) == 0);
+                const double waves = std::ceil(level_count[d] / 148.0);
+                if (cost_rule && 1.45e-9 * sf2 * waves > 0.25e-3 * level_count[d]) continue;
+            }
             for (int k = level_first[d]; k < level_first[d] + level_count[d]; ++k) {
                 require(fronts[k].depth == d, "nested dissection: fronts of a level are not contiguous");
                 NdFactorDesc D{};
@@ -1236,8 +1256,14 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             const int d = F.depth;
             if (level_first[d] <= -2) {  // first front of a batched level: the whole level in one launch
                 const int d0 = -2 - level_first[d];
+                tick(-1);
                 k_nd_factor_batch<<<level_count[d], kFactorThreads, 0, st>>>(d_descs.p + d0, dense.p, dmap.p, store.p, info.p);
                 PDG_CHECK_LAUNCH();
+                if (ftime) {
+                    tick(5);
+                    std::fprintf(stderr, "nd factor batched level depth %d: %d fronts (s %d b %d), cumulative %.4f s\n", d, level_count[d],
+                                 F.s, F.b, fsec[5]);
+                }
                 level_first[d] = -1;
             }
             continue;
