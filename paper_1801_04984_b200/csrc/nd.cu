@@ -460,41 +460,6 @@ __device__ __forceinline__ void chunk_wide(const double2* __restrict__ rows2, in
     }
 }
 
-// Columns [cb, cb + w) stored by chunk c (rows [c rpc, (c + 1) rpc) of the task) - NdTask::trap
-__host__ __device__ inline void nd_chunk_shape(int trap, int type, int r0, int nrows, int ld, int rpc, int c, int& cb, int& w) {
-    cb = 0;
-    w = ld;
-    if (!trap) return;
-    if (type == 1) {
-        const int last = r0 + (c + 1) * rpc < r0 + nrows ? r0 + (c + 1) * rpc : r0 + nrows;  // rows before `last`
-        const int we = (last + 1) & ~1;
-        w = we < ld ? we : ld;
-    } else {
-        cb = (r0 + c * rpc) & ~1;
-        w = ld - cb;
-    }
-}
-
-// compact store <- row-major store: one block per (front, pass); chunk by chunk, the stored columns only
-struct NdRepack {
-    long long src, dst;
-    int type, rows, ld, rpc;
-};
-__global__ void k_nd_repack(const NdRepack* __restrict__ jobs, const double* __restrict__ store, double* __restrict__ out) {
-    const NdRepack J = jobs[blockIdx.x];
-    long long o = J.dst;
-    for (int c = 0; c * J.rpc < J.rows; ++c) {
-        int cb, w;
-        nd_chunk_shape(1, J.type, 0, J.rows, J.ld, J.rpc, c, cb, w);
-        const int r0 = c * J.rpc, nr = min(J.rpc, J.rows - r0);
-        for (int e = threadIdx.x; e < nr * w; e += blockDim.x) {
-            const int r = e / w, col = e - r * w;
-            out[o + e] = store[J.src + (long long)(r0 + r) * J.ld + cb + col];
-        }
-        o += (long long)nr * w;
-    }
-}
-
 // Shared-memory layout of the solve kernel: mbarriers + task descriptors, the TMA
 // ring, then the buffer arena: per task (FIFO, offsets placed on the host so small
 // tasks pack densely and up to kNdBufs tasks are in flight) [v: rhs x vmt doubles]
@@ -586,12 +551,10 @@ __global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
         if (lane == 0) {
             // two cursors over this CTA's matrix chunks: the ring fill, and an L2
             // prefetch running pf chunks ahead of it (keeps HBM busy through dependency waits)
-            // (task, row, offset of that row's chunk within the task in doubles)
             int ti = 0, tr = 0, pi = 0, pr = 0, seq = 0, pseq = 0;
-            long long to = 0, po = 0;
             NdTask Ti{}, Tp{};
             int ti_loaded = -1, pi_loaded = -1;
-            auto next = [&](int& i, int& r, long long& o, NdTask& T, int& loaded) -> bool {
+            auto next = [&](int& i, int& r, NdTask& T, int& loaded) -> bool {
                 while (i < nt) {
                     if (loaded != i) {
                         T = tsk[i];
@@ -600,40 +563,31 @@ __global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
                     if (r < T.nrows) return true;
                     ++i;
                     r = 0;
-                    o = 0;
                 }
                 return false;
             };
-            // the chunk at row r of task T: its size in doubles (rows x stored columns)
-            auto chunk_doubles = [&](const NdTask& T, int r, int rpc) -> unsigned {
-                int cb, w;
-                nd_chunk_shape(T.trap, T.type, T.r0, T.nrows, T.ld, rpc, r / rpc, cb, w);
-                return static_cast<unsigned>(min(rpc, T.nrows - r)) * static_cast<unsigned>(w);
-            };
             while (true) {
-                while (pseq < seq + a.pf && next(pi, pr, po, Tp, pi_loaded)) {
+                while (pseq < seq + a.pf && next(pi, pr, Tp, pi_loaded)) {
                     const int rpc = static_cast<int>(a.stage_bytes / (8u * Tp.ld));
-                    const unsigned cd = chunk_doubles(Tp, pr, rpc);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.store + Tp.src + po), "r"(cd * 8u)
+                    const unsigned bytes = static_cast<unsigned>(min(rpc, Tp.nrows - pr)) * Tp.ld * 8u;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.store + Tp.src + (long long)pr * Tp.ld),
+                                 "r"(bytes)
                                  : "memory");
                     pr += rpc;
-                    po += cd;
                     ++pseq;
                 }
-                if (!next(ti, tr, to, Ti, ti_loaded)) break;
+                if (!next(ti, tr, Ti, ti_loaded)) break;
                 const int rpc = static_cast<int>(a.stage_bytes / (8u * Ti.ld));
                 const int k = seq % a.stages;
                 if (seq >= a.stages) mbar_wait(&empty[k], static_cast<unsigned>(((seq / a.stages) - 1) & 1));
-                const unsigned cd = chunk_doubles(Ti, tr, rpc);
-                mbar_arrive_expect_tx(&full[k], cd * 8u);
-                bulk_g2s(ring + (size_t)k * a.stage_bytes, a.store + Ti.src + to, cd * 8u, &full[k]);
+                const unsigned bytes = static_cast<unsigned>(min(rpc, Ti.nrows - tr)) * Ti.ld * 8u;
+                mbar_arrive_expect_tx(&full[k], bytes);
+                bulk_g2s(ring + (size_t)k * a.stage_bytes, a.store + Ti.src + (long long)tr * Ti.ld, bytes, &full[k]);
                 tr += rpc;
-                to += cd;
                 ++seq;
                 if (pseq < seq) {  // prefetch cursor never behind the fill
                     pi = ti;
                     pr = tr;
-                    po = to;
                     pseq = seq;
                 }
             }
@@ -827,7 +781,6 @@ __global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
         const int q = i % kNdBufs;
         const NdTask& Ts = tsk[i];
         const int type = Ts.type, r0t = Ts.r0, nrows = Ts.nrows, ld = Ts.ld, s = Ts.s, sdof = Ts.sdof, leaf = Ts.leaf;
-        const int trap = Ts.trap;
         const int rpc = static_cast<int>(a.stage_bytes / (8u * ld));
         const int nch = (nrows + rpc - 1) / rpc;
         // chunks of this task owned by this warp: seq + c with (seq + c) % 8 == warp
@@ -844,8 +797,9 @@ __global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
             const double* v = vbuf(Ts);
             const int* oix = oixbuf(Ts);
             const int vm = Ts.vmt;
-            const double2* va0 = reinterpret_cast<const double2*>(v);
-            const double2* vb0 = va0 + (vm >> 1);
+            const double2* va = reinterpret_cast<const double2*>(v);
+            const double2* vb = va + (vm >> 1);
+            const int ld2 = ld >> 1;
             auto write_out = [&](int k, int lr, double t) {  // row lr of the task, rhs k
                 const int gr = r0t + lr;
                 if (type == 2) {
@@ -869,11 +823,6 @@ __global__ void __launch_bounds__(kNdBlock, PDG_ND_MINB) k_nd_solve(NdArgs a) {
                 mbar_wait(&full[slot], static_cast<unsigned>((sq / a.stages) & 1));
                 const double2* rows2 = reinterpret_cast<const double2*>(ring + (size_t)slot * a.stage_bytes);
                 const int nrow = min(rpc, nrows - rc);
-                int cbeg, cw;  // the chunk's stored columns
-                nd_chunk_shape(trap, type, r0t, nrows, ld, rpc, c, cbeg, cw);
-                const double2* va = va0 + (cbeg >> 1);
-                const double2* vb = vb0 + (cbeg >> 1);
-                const int ld2 = cw >> 1;
                 if (a.nomath) {
                 } else if (rpc >= 8 && !a.tile8) {
                     // rows per pass 4 R, with at least npart passes per chunk
@@ -1664,52 +1613,6 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
                 head += sz;
             }
         }
-        // ---- compact store (trapezoid chunks, NdTask::trap; opt-in, PDG_ND_TRAP=1): the zero
-        // triangles of L_SS^{-1} / L_SS^{-T} are neither stored nor read. Measured at config 1: the
-        // chunk kernel's bytes drop by a fifth and its time does not move (227.6 vs 229.4 us per
-        // displacement solve): it is bound by its dependency chain, not by bandwidth. ----
-        if (std::getenv("PDG_ND_TRAP") && std::atoi(std::getenv("PDG_ND_TRAP")) == 1) {
-            std::vector<long long> base(2 * (size_t)nf, -1);
-            std::vector<NdRepack> jobs;
-            long long tot = 0;
-            double saved = 0.0;
-            auto rows_of = [&](int k, int type) { return type == 1 ? fronts[k].s + fronts[k].b : fronts[k].s; };
-            auto chunk_off = [&](int type, int rows, int ld, int rpc, int r) {  // doubles before row r (multiple of rpc)
-                long long o = 0;
-                for (int c = 0; c * rpc < r; ++c) {
-                    int cb, w;
-                    nd_chunk_shape(1, type, 0, rows, ld, rpc, c, cb, w);
-                    o += (long long)std::min(rpc, rows - c * rpc) * w;
-                }
-                return o;
-            };
-            for (auto& v : per_cta)
-                for (auto& t : v) {
-                    const size_t key = 2 * (size_t)t.front + (t.type - 1);
-                    const int rows = rows_of(t.front, t.type);
-                    const int rpc = std::max(1, static_cast<int>(stage_bytes / (8u * t.ld)));
-                    require(t.r0 % rpc == 0, "nested dissection: task does not start on a chunk boundary");
-                    if (base[key] < 0) {
-                        base[key] = tot;
-                        const long long sz = chunk_off(t.type, rows, t.ld, rpc, rows + rpc - 1 - (rows + rpc - 1) % rpc);
-                        const NdFront& F = fronts[t.front];
-                        jobs.push_back({t.type == 1 ? F.moff : F.mtoff, tot, t.type, rows, t.ld, rpc});
-                        tot += sz;
-                        saved += 8.0 * ((double)rows * t.ld - (double)sz);
-                    }
-                    t.src = base[key] + chunk_off(t.type, rows, t.ld, rpc, t.r0);
-                    t.trap = 1;
-                }
-            if (!jobs.empty()) {
-                cstore.alloc((size_t)tot);
-                DBuf<NdRepack> djobs;
-                djobs.upload(jobs, st);
-                k_nd_repack<<<static_cast<unsigned>(jobs.size()), 256, 0, st>>>(djobs.p, store.p, cstore.p);
-                PDG_CHECK_LAUNCH();
-                PDG_CUDA(cudaStreamSynchronize(st));
-                factor_bytes -= saved;  // a solve no longer reads them
-            }
-        }
         std::vector<NdTask> all, all_b;
         std::vector<int> hct(grid + 1, 0), hct_b(grid + 1, 0);
         for (int q = 0; q < grid; ++q) {
@@ -1743,11 +1646,9 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
             lvl_max_depth = hybrid_top;
             build_tiles(children, parent, hs, hbp, hcbdst, st);
         }
-        if (cstore.n) store.release();  // every solve kernel now reads the compact store / the tile store
     } catch (const Error& e) {
         if (e.status != PDG_INVALID_ARGUMENT || std::getenv("PDG_ND_STRICT")) throw;
         fallback_reason = e.what();
-        cstore.release();
         hybrid = split = false;
         lvl_max_depth = -1;
         tiles = levels = true;
@@ -1759,7 +1660,7 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
 // one launch of the chunk kernel on a task schedule (the hybrid's local forward / backward)
 void NdChol::launch_chunks(const NdTask* tasks, const int* cto, const double* b, long long ldb, double* x, long long ldx,
                            int nrhs, cudaStream_t st) {
-    NdArgs a{tasks, cto, sdofs.p, bpos.p, cbdst.p, cstore.n ? cstore.p : store.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, counters.p, call, cbtot, n,
+    NdArgs a{tasks, cto, sdofs.p, bpos.p, cbdst.p, store.p, b, ldb, x, ldx, y.p, xpos.p, cbuf.p, counters.p, call, cbtot, n,
              nrhs, stages, vmax, smem_tasks, pf, stage_bytes, nullptr, 0, 0, std::getenv("PDG_ND_FENCE") != nullptr, guard,
              0, 0};
     void* args[] = {&a};
@@ -1805,7 +1706,7 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
         solve_tiles(b, ldb, x, ldx, nrhs, st);
         return;
     }
-    NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, cstore.n ? cstore.p : store.p, b,         ldb,        x,       ldx,
+    NdArgs a{d_tasks.p, ctoff.p, sdofs.p,    bpos.p, cbdst.p, store.p, b,         ldb,        x,       ldx,
              y.p,       xpos.p,  cbuf.p,     counters.p, call, cbtot,   n,         nrhs,       stages,  vmax,
              smem_tasks, pf,     stage_bytes, nullptr, std::getenv("PDG_ND_NODEP") != nullptr,
              std::getenv("PDG_ND_NOMATH") != nullptr, std::getenv("PDG_ND_FENCE") != nullptr, guard,

@@ -59,11 +59,7 @@ struct NdTask {
     // stride between the right-hand sides of v (doubles), and the newest earlier task of this
     // CTA whose buffer must be released first (-1: none)
     int boff, vmt, fdep;
-    // trapezoid chunks (compact store): a chunk keeps only the columns that can be nonzero - a
-    // forward chunk (rows of [L_SS^{-1}; G]) the columns [0, w), w = rows up to the chunk's last
-    // (all s once it reaches the G rows); a backward chunk (rows of [L_SS^{-T} | G^T]) the columns
-    // from its first row on. src then points at the task's first chunk in the compact store.
-    int trap;
+    int pad_;
 };
 
 // One task of the tile-streaming solve (nd_tile.cu): rows [r0, r0 + nrows) of a
@@ -106,7 +102,6 @@ struct NdChol {
     // y, xpos in pivot-position order; cbuf: per front, the two children's update vectors
     // scattered to the front's local positions ([child][s + b], per right-hand side)
     DBuf<double> store, y, xpos, cbuf;
-    DBuf<double> cstore;  // compact (trapezoid-chunk) copy of the fronts the chunk kernel solves; replaces store then
     DBuf<int> sdofs, bpos, cbdst, ctoff;  // bpos: pivot position of each boundary dof; cbdst: its slot in the parent's cbuf
     DBuf<unsigned long long> counters;          // [front][-, forward, backward] completed tasks
     DBuf<NdTask> d_tasks;

@@ -194,32 +194,6 @@ def test_nd_streaming_mode_matches_default(oracle, monkeypatch, dim):
     assert np.linalg.norm(xs - xr) <= SOLVE_RTOL * np.linalg.norm(xr)
 
 
-def test_nd_trapezoid_store_matches_default(oracle, monkeypatch):
-    """PDG_ND_TRAP=1 (opt-in): the chunk kernel reads a compact store whose chunks keep only the
-    columns that can be nonzero (the zero triangles of L_SS^{-1} / L_SS^{-T} dropped). Same exact
-    solve: preconditioner within roundoff of the default layout, repeats bit-identical, solution
-    within 1e-9 of the oracle (config 1 at 64^2: hybrid displacement solve and chunk-only flux solve)."""
-    spec = P.config1(64)
-    rp = oracle.RefProblem(spec.to_dict())
-    T = oracle.time_constants(1)["T"]
-    tau = 0.05
-    opt = S.SolveOptions(gmres=S.GmresOptions(tol=1e-10, restart=50), candidate="flexible")
-    blk = S.BlockSolver(S.SpatialOperators.assemble(spec), T, tau, opt=opt)
-    monkeypatch.setenv("PDG_ND_TRAP", "1")
-    blk_t = S.BlockSolver(S.SpatialOperators.assemble(spec), T, tau, opt=opt)
-    monkeypatch.delenv("PDG_ND_TRAP")
-    rvec = P.uniform_vector(9, blk.rows)
-    z, zt = blk.precondition(rvec), blk_t.precondition(rvec)
-    assert np.linalg.norm(z - zt) <= 1e-11 * np.linalg.norm(z)
-    assert np.array_equal(zt, blk_t.precondition(rvec))
-    rhs = P.uniform_vector(10, blk.rows)
-    x, rep = blk.solve(rhs)
-    xt, rept = blk_t.solve(rhs)
-    assert rep.iterations == rept.iterations
-    xr, _ = rp.block_solve(1, tau, rhs, tol=1e-10, restart=50, backend=1, flexible=True)
-    assert np.linalg.norm(xt - xr) <= SOLVE_RTOL * np.linalg.norm(xr)
-
-
 @pytest.mark.parametrize("r", [0, 1])
 def test_fast_mode_fp32_factor(oracle, monkeypatch, r):
     """pdg_gmres_opts.mode 1 (SURVEY 8(b) SolveOptions mode = fast): the streamed displacement factor
