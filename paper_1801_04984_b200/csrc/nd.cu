@@ -1645,7 +1645,6 @@ void NdChol::factor(int n_, const std::vector<int>& off, const std::vector<int>&
         if (hybrid) {  // the top levels as level kernels (tiles for those fronts only)
             lvl_max_depth = hybrid_top;
             build_tiles(children, parent, hs, hbp, hcbdst, st);
-            build_local(children, st);
         }
     } catch (const Error& e) {
         if (e.status != PDG_INVALID_ARGUMENT || std::getenv("PDG_ND_STRICT")) throw;
@@ -1696,17 +1695,11 @@ void NdChol::solve(const double* b, long long ldb, double* x, long long ldx, int
         return;
     }
     if (split) {  // local forward (chunk kernel), level kernels, dense top, level kernels, local backward
-        if (local_lvl)
-            solve_local(1, b, ldb, x, ldx, nrhs, st);
-        else
-            launch_chunks(d_tasks.p, ctoff.p, b, ldb, x, ldx, nrhs, st);
+        launch_chunks(d_tasks.p, ctoff.p, b, ldb, x, ldx, nrhs, st);
         if (hybrid) solve_levels_range(b, ldb, x, ldx, nrhs, 0, nl / 2, st);
         if (top_depth >= 0) solve_top(b, ldb, x, ldx, nrhs, st);
         if (hybrid) solve_levels_range(b, ldb, x, ldx, nrhs, nl / 2, nl, st);
-        if (local_lvl)
-            solve_local(2, b, ldb, x, ldx, nrhs, st);
-        else
-            launch_chunks(d_tasks_b.p, ctoff_b.p, b, ldb, x, ldx, nrhs, st);
+        launch_chunks(d_tasks_b.p, ctoff_b.p, b, ldb, x, ldx, nrhs, st);
         return;
     }
     if (tiles) {

@@ -83,11 +83,6 @@ struct NdStreamUnit {
     int s, b, sdof, bdof, cboff;
     int cbeg;  // first column read (even); columns [cbeg, ncols)
 };
-// One front of a local subtree for the level-synchronous local kernel (nd_local.cu)
-struct NdLocalFront {
-    long long moff, mtoff;  // M and M^T in the row-major store
-    int ldm, ldt, s, b, sdof, bdof, cboff, pad_;
-};
 bool nd_tile_default();
 bool nd_levels_default();
 bool nd_hybrid_default(int prof_phase);
@@ -150,15 +145,6 @@ struct NdChol {
     DBuf<int> ctoff_b;
     void launch_chunks(const NdTask* tasks, const int* cto, const double* b, long long ldb, double* x, long long ldx,
                        int nrhs, cudaStream_t st);
-    // level-synchronous local kernel (nd_local.cu, PDG_ND_LOCAL_LEVELS=1) instead of the chunk kernel
-    // for the hybrid's local subtrees: one CTA per subtree, all its fronts of one depth at a time
-    bool local_lvl = false;
-    int local_ctas = 0;
-    size_t local_smem = 0;
-    DBuf<NdLocalFront> d_lfronts;
-    DBuf<int> d_lcta, d_llev;
-    void build_local(const std::vector<std::vector<int>>& children, cudaStream_t st);
-    void solve_local(int pass, const double* b, long long ldb, double* x, long long ldx, int nrhs, cudaStream_t st);
     // dense top (PDG_ND_TOP): the fronts of depth <= top_depth (pivot positions [top0, n)) are
     // not solved front by front; their Schur complement inverse G = S_TT^{-1} (= (A^{-1})_TT)
     // is applied as one GEMV between the forward and backward passes of the fronts below
