@@ -269,15 +269,24 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
             else
                 block_column_sums(pass == 0 ? p1 : p2, ncols, hs, h_out + (size_t)pass * ncols);
             double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
-                double v = __ldcg(w + r);
-                double vj[8];
+            // two rows per trip: both rows' loads are issued before either is used (a thread has ~6
+            // rows at config 1, each a round trip to L2); the rows are then processed in order, so
+            // the sums are those of the one-row loop
+            const long long stride = (long long)gridDim.x * blockDim.x;
+            for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += 2 * stride) {
+                const long long r2 = r + stride;
+                const bool two = r2 < n;
+                double v = __ldcg(w + r), v2 = two ? __ldcg(w + r2) : 0.0;
+                double vj[8], vk[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (j < ncols) {
                         vj[j] = V[(long long)j * n + r];
-                        v -= hs[j] * vj[j];
+                        vk[j] = two ? V[(long long)j * n + r2] : 0.0;
                     }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < ncols) v -= hs[j] * vj[j];
                 w[r] = v;
                 if (pass == 0) {
 #pragma unroll
@@ -285,6 +294,19 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
                         if (q < ncols) a[q] += vj[q] * v;
                 } else {
                     a[0] += v * v;
+                }
+                if (two) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < ncols) v2 -= hs[j] * vk[j];
+                    w[r2] = v2;
+                    if (pass == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q < ncols) a[q] += vk[q] * v2;
+                    } else {
+                        a[0] += v2 * v2;
+                    }
                 }
             }
             const int nq = pass == 0 ? ncols : 1;
@@ -336,8 +358,13 @@ __global__ void __launch_bounds__(kRedThreads) k_arnoldi_gs(long long n, int nco
             if (ls) givens_step(ncols - 1, mm, h_out, h_out + ncols, nv, Hcol, cs, sn, g, tolb, ls);
         }
         const double d = nv;
-        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
-            vnext[r] = __ldcg(w + r) / d;
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += 2 * stride) {
+            const long long r2 = r + stride;
+            const double x0 = __ldcg(w + r), x1 = r2 < n ? __ldcg(w + r2) : 0.0;
+            vnext[r] = x0 / d;
+            if (r2 < n) vnext[r2] = x1 / d;
+        }
     }
 }
 
